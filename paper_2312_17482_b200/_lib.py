@@ -1,0 +1,280 @@
+"""ctypes binding of libmosaicbert.so — argument marshalling only.
+
+Every function here has the name of the C entry point it wraps (without the ``mb_`` prefix) and
+does nothing but turn torch tensors into pointers / sizes and the current CUDA stream into a
+``cudaStream_t``; every step of the path runs in the library's kernels.  There is no fallback:
+if the library is missing or a call fails, a RuntimeError is raised.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmosaicbert.so")
+
+P = C.c_void_p
+I32 = C.c_int32
+I64 = C.c_int64
+F32 = C.c_float
+SZ = C.c_size_t
+
+EPI_BF16, EPI_F32_ACC, EPI_F32, EPI_GELU_AUX = 0, 1, 2, 3
+STATUS = {0: "MB_OK", 1: "MB_ERR_INVALID_ARG", 2: "MB_ERR_CONFIG", 3: "MB_ERR_SHAPE", 4: "MB_ERR_MASK_LAYOUT",
+          5: "MB_ERR_LABEL_RANGE", 6: "MB_ERR_WORKSPACE", 7: "MB_ERR_ARCH", 8: "MB_ERR_CUDA"}
+
+
+class Dims(C.Structure):
+    _fields_ = [("hidden", I32), ("heads", I32), ("intermediate", I32), ("vocab", I32), ("ln_eps", F32)]
+
+
+class Packed(C.Structure):
+    _fields_ = [("cu_seqlens", P), ("batch", I32), ("nnz", I32), ("max_seqlen", I32)]
+
+
+LAYER_FIELDS = ("w_qkv", "b_qkv", "w_o", "b_o", "ln1_g", "ln1_b", "w_1v", "b_1v", "w_2", "b_2", "ln2_g", "ln2_b")
+HEAD_FIELDS = ("w_t", "b_t", "ln_g", "ln_b", "emb", "b_dec")
+
+
+class LayerPtrs(C.Structure):
+    _fields_ = [(f, P) for f in LAYER_FIELDS]
+
+
+class HeadPtrs(C.Structure):
+    _fields_ = [(f, P) for f in HEAD_FIELDS]
+
+
+_SIGS = {
+    "mb_status_string": (C.c_char_p, [C.c_int]),
+    "mb_version": (C.c_char_p, []),
+    "mb_alibi_slopes": (C.c_int, [I32, P]),
+    "mb_unpad_index": (C.c_int, [P, I32, I32, P, P, P, P]),
+    "mb_mlm_select": (C.c_int, [P, P, I32, I32, P, P, P, P]),
+    "mb_gather_rows": (C.c_int, [P, P, I32, I32, P, P]),
+    "mb_scatter_rows": (C.c_int, [P, P, I32, I32, I32, P, P]),
+    "mb_layernorm_forward": (C.c_int, [P, P, P, I32, I32, F32, P, P, P]),
+    "mb_layernorm_backward": (C.c_int, [P, P, P, P, I32, I32, P, P, P, P, P, P]),
+    "mb_gemm": (C.c_int, [I32, I32, I32, P, I64, I32, P, I64, I32, P, I64, I32, P, P, I64, P, I64, P]),
+    "mb_geglu_forward": (C.c_int, [P, I32, I32, I32, P, P, P, P, P]),
+    "mb_geglu_backward": (C.c_int, [P, I32, I32, I32, P, P, P, P]),
+    "mb_attention_forward": (C.c_int, [P, P, I32, I32, I32, I32, I32, P, P, P, P]),
+    "mb_attention_workspace_bytes": (SZ, [I32, I32, I32, I32]),
+    "mb_attention_backward": (C.c_int, [P, P, P, P, P, I32, I32, I32, I32, I32, P, P, P, SZ, P]),
+    "mb_colsum": (C.c_int, [P, I32, I32, P, P]),
+    "mb_layer_saved_bytes": (SZ, [C.POINTER(Dims), I32]),
+    "mb_layer_workspace_bytes": (SZ, [C.POINTER(Dims), I32, I32]),
+    "mb_encoder_forward": (C.c_int, [C.POINTER(Dims), C.POINTER(LayerPtrs), C.POINTER(Packed), P, P, P, P, P]),
+    "mb_encoder_backward": (C.c_int, [C.POINTER(Dims), C.POINTER(LayerPtrs), C.POINTER(Packed), P, P, P, P, P,
+                                      C.POINTER(LayerPtrs), P, SZ, P]),
+    "mb_embed_forward": (C.c_int, [C.POINTER(Dims), P, P, I32, P, P, P, P, P, P, P]),
+    "mb_embed_backward": (C.c_int, [C.POINTER(Dims), P, P, I32, P, P, P, P, P, P, P, P, P, P]),
+    "mb_mlm_workspace_bytes": (SZ, [C.POINTER(Dims), I32]),
+    "mb_mlm_loss": (C.c_int, [C.POINTER(Dims), C.POINTER(HeadPtrs), P, I32, P, P, I32, F32, P, P, P,
+                              C.POINTER(HeadPtrs), P, SZ, P]),
+    "mb_adamw_step": (C.c_int, [P, P, P, P, P, I64, F32, F32, F32, F32, F32, F32, I32, P]),
+}
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libmosaicbert.so (fails loudly if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: build it with `python -m paper_2312_17482_b200.build`")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def exported_symbols():
+    return sorted(_SIGS)
+
+
+def _ck(name: str, status: int):
+    if status != 0:
+        raise RuntimeError(f"{name} failed: {STATUS.get(status, status)}")
+
+
+def _p(t):
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    assert t.is_cuda and t.is_contiguous(), "device tensors must be contiguous CUDA tensors"
+    return t.data_ptr()
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def dims(hidden, heads, intermediate, vocab, ln_eps=1e-12) -> Dims:
+    return Dims(hidden, heads, intermediate, vocab, ln_eps)
+
+
+# --------------------------------------------------------------------------------------- wrappers
+def alibi_slopes(heads: int) -> np.ndarray:
+    out = np.zeros(max(heads, 1), dtype=np.float32)
+    _ck("mb_alibi_slopes", lib().mb_alibi_slopes(heads, out.ctypes.data))
+    return out[:heads]
+
+
+def unpad_index(mask: torch.Tensor, meta: torch.Tensor | None = None):
+    """mask: cuda int32 [B, L] -> (cu_seqlens [B+1], indices [B*L] (first nnz valid), meta [4])."""
+    B, L = mask.shape
+    cu = torch.empty(B + 1, dtype=torch.int32, device=mask.device)
+    idx = torch.empty(B * L, dtype=torch.int32, device=mask.device)
+    if meta is None:
+        meta = torch.zeros(4, dtype=torch.int32, device=mask.device)
+    _ck("mb_unpad_index", lib().mb_unpad_index(_p(mask), B, L, _p(cu), _p(idx), _p(meta), _stream()))
+    return cu, idx, meta
+
+
+def mlm_select(labels: torch.Tensor, indices: torch.Tensor, vocab: int, meta: torch.Tensor):
+    cap = indices.numel()
+    rows = torch.empty(cap, dtype=torch.int32, device=labels.device)
+    labs = torch.empty(cap, dtype=torch.int32, device=labels.device)
+    _ck("mb_mlm_select", lib().mb_mlm_select(_p(labels), _p(indices), cap, vocab, _p(rows), _p(labs), _p(meta),
+                                             _stream()))
+    return rows, labs
+
+
+def gather_rows(src, idx, n, dst):
+    _ck("mb_gather_rows", lib().mb_gather_rows(_p(src), _p(idx), n, src.shape[-1], _p(dst), _stream()))
+    return dst
+
+
+def scatter_rows(src, idx, n, rows, dst):
+    _ck("mb_scatter_rows", lib().mb_scatter_rows(_p(src), _p(idx), n, src.shape[-1], rows, _p(dst), _stream()))
+    return dst
+
+
+def layernorm_forward(x, gamma, beta, eps, y, stats):
+    n, H = x.shape
+    _ck("mb_layernorm_forward", lib().mb_layernorm_forward(_p(x), _p(gamma), _p(beta), n, H, eps, _p(y), _p(stats),
+                                                           _stream()))
+    return y, stats
+
+
+def layernorm_backward(dy, x, stats, gamma, dx, dgamma, dbeta, dsum=None, gelu_pre=None):
+    n, H = x.shape
+    _ck("mb_layernorm_backward", lib().mb_layernorm_backward(_p(dy), _p(x), _p(stats), _p(gamma), n, H, _p(gelu_pre),
+                                                             _p(dx), _p(dgamma), _p(dbeta), _p(dsum), _stream()))
+    return dx
+
+
+def gemm(M, N, K, A, lda, a_t, B, ldb, b_t, Cout, ldc, epilogue=EPI_BF16, bias=None, residual=None, ldr=0, aux=None,
+         ldaux=0):
+    _ck("mb_gemm", lib().mb_gemm(M, N, K, _p(A), lda, int(a_t), _p(B), ldb, int(b_t), _p(Cout), ldc, epilogue,
+                                 _p(bias), _p(residual), ldr, _p(aux), ldaux, _stream()))
+    return Cout
+
+
+def geglu_forward(X, w_1v, b_1v, U, Z):
+    n, H = X.shape
+    I = Z.shape[-1]
+    _ck("mb_geglu_forward", lib().mb_geglu_forward(_p(X), n, H, I, _p(w_1v), _p(b_1v), _p(U), _p(Z), _stream()))
+    return U, Z
+
+
+def geglu_backward(dF, w_2, U, dU):
+    n, H = dF.shape
+    I = w_2.shape[1]
+    _ck("mb_geglu_backward", lib().mb_geglu_backward(_p(dF), n, H, I, _p(w_2), _p(U), _p(dU), _stream()))
+    return dU
+
+
+def attention_forward(qkv, cu_seqlens, batch, nnz, max_seqlen, heads, head_dim, slopes, O, lse):
+    _ck("mb_attention_forward", lib().mb_attention_forward(_p(qkv), _p(cu_seqlens), batch, nnz, max_seqlen, heads,
+                                                           head_dim, _p(slopes), _p(O), _p(lse), _stream()))
+    return O, lse
+
+
+def attention_workspace_bytes(nnz, heads, head_dim, max_seqlen):
+    return int(lib().mb_attention_workspace_bytes(nnz, heads, head_dim, max_seqlen))
+
+
+def attention_backward(qkv, O, dO, lse, cu_seqlens, batch, nnz, max_seqlen, heads, head_dim, slopes, dqkv, ws=None):
+    nb = attention_workspace_bytes(nnz, heads, head_dim, max_seqlen)
+    if ws is None and nb:
+        ws = torch.empty(nb, dtype=torch.uint8, device=qkv.device)
+    _ck("mb_attention_backward", lib().mb_attention_backward(_p(qkv), _p(O), _p(dO), _p(lse), _p(cu_seqlens), batch,
+                                                             nnz, max_seqlen, heads, head_dim, _p(slopes), _p(dqkv),
+                                                             _p(ws), nb, _stream()))
+    return dqkv
+
+
+def colsum(x, out):
+    n, Cc = x.shape
+    _ck("mb_colsum", lib().mb_colsum(_p(x), n, Cc, _p(out), _stream()))
+    return out
+
+
+def layer_saved_bytes(d: Dims, nnz: int) -> int:
+    return int(lib().mb_layer_saved_bytes(C.byref(d), nnz))
+
+
+def layer_workspace_bytes(d: Dims, nnz: int, max_seqlen: int) -> int:
+    return int(lib().mb_layer_workspace_bytes(C.byref(d), nnz, max_seqlen))
+
+
+def layer_ptrs(p: dict) -> LayerPtrs:
+    return LayerPtrs(*[_p(p[f]) for f in LAYER_FIELDS])
+
+
+def head_ptrs(p: dict) -> HeadPtrs:
+    return HeadPtrs(*[_p(p[f]) for f in HEAD_FIELDS])
+
+
+def encoder_forward(d: Dims, params, packed: Packed, slopes, x, y, saved):
+    lp = params if isinstance(params, LayerPtrs) else layer_ptrs(params)
+    _ck("mb_encoder_forward", lib().mb_encoder_forward(C.byref(d), C.byref(lp), C.byref(packed), _p(slopes), _p(x),
+                                                       _p(y), _p(saved), _stream()))
+    return y
+
+
+def encoder_backward(d: Dims, params, packed: Packed, slopes, x, saved, dy, dx, grads, ws):
+    lp = params if isinstance(params, LayerPtrs) else layer_ptrs(params)
+    lg = grads if isinstance(grads, LayerPtrs) else layer_ptrs(grads)
+    _ck("mb_encoder_backward", lib().mb_encoder_backward(C.byref(d), C.byref(lp), C.byref(packed), _p(slopes), _p(x),
+                                                         _p(saved), _p(dy), _p(dx), C.byref(lg), _p(ws), ws.numel(),
+                                                         _stream()))
+    return dx
+
+
+def embed_forward(d: Dims, ids, indices, nnz, emb, type_emb, ln_g, ln_b, x0, stats):
+    _ck("mb_embed_forward", lib().mb_embed_forward(C.byref(d), _p(ids), _p(indices), nnz, _p(emb), _p(type_emb),
+                                                   _p(ln_g), _p(ln_b), _p(x0), _p(stats), _stream()))
+    return x0
+
+
+def embed_backward(d: Dims, ids, indices, nnz, emb, type_emb, ln_g, stats, dx0, d_emb, d_type_emb, d_ln_g, d_ln_b):
+    _ck("mb_embed_backward", lib().mb_embed_backward(C.byref(d), _p(ids), _p(indices), nnz, _p(emb), _p(type_emb),
+                                                     _p(ln_g), _p(stats), _p(dx0), _p(d_emb), _p(d_type_emb),
+                                                     _p(d_ln_g), _p(d_ln_b), _stream()))
+
+
+def mlm_workspace_bytes(d: Dims, n_masked: int) -> int:
+    return int(lib().mb_mlm_workspace_bytes(C.byref(d), n_masked))
+
+
+def mlm_loss(d: Dims, head, y, nnz, masked_rows, labels, n_masked, inv_norm, loss_sum, lse, dy_top, grads, ws):
+    hp = head if isinstance(head, HeadPtrs) else head_ptrs(head)
+    hg = grads if isinstance(grads, HeadPtrs) else head_ptrs(grads)
+    _ck("mb_mlm_loss", lib().mb_mlm_loss(C.byref(d), C.byref(hp), _p(y), nnz, _p(masked_rows), _p(labels), n_masked,
+                                         inv_norm, _p(loss_sum), _p(lse), _p(dy_top), C.byref(hg), _p(ws), ws.numel(),
+                                         _stream()))
+
+
+def adamw_step(master, m, v, g, w_bf16, lr, beta1, beta2, eps, weight_decay, grad_scale, step):
+    _ck("mb_adamw_step", lib().mb_adamw_step(_p(master), _p(m), _p(v), _p(g), _p(w_bf16), master.numel(), lr, beta1,
+                                             beta2, eps, weight_decay, grad_scale, step, _stream()))

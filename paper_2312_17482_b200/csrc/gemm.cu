@@ -1,0 +1,412 @@
+// Persistent warp-specialised tcgen05 GEMM with fused epilogues.
+//
+//   warp 0      : TMA producer (one lane) — A/B tiles into a STAGES-deep smem ring (full/empty mbarriers)
+//   warp 1      : MMA issuer (one lane)   — tcgen05.mma kind::f16, 128 x BN x 16 per instruction,
+//                 accumulating in TMEM; double-buffered accumulator (2 x BN fp32 columns)
+//   warp 2      : TMEM allocator
+//   warps 4..7  : epilogue — tcgen05.ld 32 lanes x 32 columns, fused bias / residual / GeLU /
+//                 GeGLU fwd+bwd / fp32 atomic accumulate, stores to global
+//
+// Operands may be K-major (the nn.Linear forward layout) or MN-major (the transposed operands of
+// dX = dY W and dW = dY^T X); both are expressed with 128-byte-swizzled TMA boxes and the matching
+// UMMA shared-memory descriptors, so no operand is ever transposed in memory.
+#include <algorithm>
+#include "common.cuh"
+#include "kernels.h"
+#include "sm100.cuh"
+#include "tma.h"
+
+namespace mb {
+namespace {
+
+constexpr int BM = 128, BK = 64, NTHREADS = 256;
+
+template <int BN, int STAGES>
+struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int DATA = STAGE_BYTES * STAGES;
+  static constexpr int SMEM = DATA + 1024 + 256;
+  static constexpr int TMEM_COLS = 2 * BN;
+};
+
+struct Sched {
+  int num_m, num_n, splits, nkb, kb_per, total;
+  __device__ __forceinline__ void decode(int u, int& m, int& n, int& kb0, int& kb1) const {
+    const int tiles = num_m * num_n;
+    const int s = u / tiles;
+    const int t = u - s * tiles;
+    m = t / num_n;
+    n = t - m * num_n;
+    kb0 = s * kb_per;
+    kb1 = min(nkb, kb0 + kb_per);
+  }
+};
+
+__device__ __forceinline__ void store_bf16x32(bf16* dst, const float* v, int ncols_valid) {
+  // ncols_valid is a multiple of 8 (host guarantees N % 8 == 0)
+#pragma unroll
+  for (int g = 0; g < 4; ++g)
+    if (g * 8 < ncols_valid) *reinterpret_cast<uint4*>(dst + g * 8) = f32_to_bf16x8(v + g * 8);
+}
+
+__device__ __forceinline__ void load_bf16x32(const bf16* src, float* v, int ncols_valid) {
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    if (g * 8 < ncols_valid) {
+      uint4 u = *reinterpret_cast<const uint4*>(src + g * 8);
+      bf16x8_to_f32(u, v + g * 8);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[g * 8 + j] = 0.f;
+    }
+  }
+}
+
+template <int BN, int STAGES, int A_MN, int B_MN, int PAIRED>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                Sched sc, Epi ep) {
+  using C = Cfg<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATA);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch(&tmA);
+    sm100::tma_prefetch(&tmB);
+    for (int i = 0; i < STAGES; ++i) {
+      sm100::mbar_init(&full[i], 1);
+      sm100::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&tfull[i], 1);
+      sm100::mbar_init(&tempty[i], 4);
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 2) sm100::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < sc.total; u += gridDim.x) {
+        int mb, nb, kb0, kb1;
+        sc.decode(u, mb, nb, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          sm100::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C::STAGE_BYTES;
+          uint8_t* sb = sa + C::A_BYTES;
+          sm100::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          const int k0 = kb * BK;
+          if (!A_MN) {
+            sm100::tma_load_2d(sa, &tmA, &full[stage], k0, mb * BM);
+          } else {
+#pragma unroll
+            for (int i = 0; i < BM / 64; ++i) sm100::tma_load_2d(sa + i * 8192, &tmA, &full[stage], mb * BM + i * 64, k0);
+          }
+          if (PAIRED) {
+            sm100::tma_load_2d(sb, &tmB, &full[stage], k0, nb * 128);
+            sm100::tma_load_2d(sb + 128 * 128, &tmB, &full[stage], k0, ep.I + nb * 128);
+          } else if (!B_MN) {
+            sm100::tma_load_2d(sb, &tmB, &full[stage], k0, nb * BN);
+          } else {
+#pragma unroll
+            for (int i = 0; i < BN / 64; ++i) sm100::tma_load_2d(sb + i * 8192, &tmB, &full[stage], nb * BN + i * 64, k0);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = sm100::idesc_bf16(BM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = blockIdx.x; u < sc.total; u += gridDim.x) {
+        int mb, nb, kb0, kb1;
+        sc.decode(u, mb, nb, kb0, kb1);
+        sm100::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        sm100::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          sm100::mbar_wait(&full[stage], phase);
+          sm100::tc_fence_after();
+          const uint32_t sa = sm100::smem_u32(smem + stage * C::STAGE_BYTES);
+          const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_MN ? sm100::desc_mnmajor_sw128(sa + k * 2048, 8192) : sm100::desc_kmajor_sw128(sa + k * 32);
+            const uint64_t bd = B_MN ? sm100::desc_mnmajor_sw128(sb + k * 2048, 8192) : sm100::desc_kmajor_sw128(sb + k * 32);
+            sm100::mma_bf16_ss(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          sm100::mma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        sm100::mma_commit(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = blockIdx.x; u < sc.total; u += gridDim.x) {
+      int mb, nb, kb0, kb1;
+      sc.decode(u, mb, nb, kb0, kb1);
+      sm100::mbar_wait(&tfull[acc], acc_phase);
+      sm100::tc_fence_after();
+      const int row = mb * BM + q * 32 + lane;
+      const bool row_ok = row < M;
+      const uint32_t tb = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
+      float v[32];
+      if (ep.mode == E_GEGLU_FWD) {
+        // paired tile: TMEM cols [0,128) = a (W1 half), [128,256) = g (V half) for columns nb*128..
+        float g[32];
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          sm100::tmem_ld32(tb + c * 32, v);
+          sm100::tmem_ld32(tb + 128 + c * 32, g);
+          sm100::tmem_ld_wait();
+          const int col = nb * 128 + c * 32;
+          if (row_ok) {
+            float ba[32], bg[32];
+            load_bf16x32(ep.bias + col, ba, 32);
+            load_bf16x32(ep.bias + ep.I + col, bg, 32);
+            float z[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              v[j] += ba[j];
+              g[j] += bg[j];
+              z[j] = gelu_f(v[j]) * g[j];
+            }
+            bf16* U = ep.aux + (int64_t)row * ep.ldaux;
+            store_bf16x32(U + col, v, 32);
+            store_bf16x32(U + ep.I + col, g, 32);
+            store_bf16x32(reinterpret_cast<bf16*>(ep.C) + (int64_t)row * ep.ldc + col, z, 32);
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          const int col = nb * BN + c * 32;
+          if (col >= N) break;  // warp-uniform
+          sm100::tmem_ld32(tb + c * 32, v);
+          sm100::tmem_ld_wait();
+          if (!row_ok) continue;
+          const int nv = min(32, N - col);
+          if (ep.mode == E_F32_ACC) {
+            float* dst = reinterpret_cast<float*>(ep.C) + (int64_t)row * ep.ldc + col;
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+              if (j < nv) red_add_v4(dst + j, v[j], v[j + 1], v[j + 2], v[j + 3]);
+          } else if (ep.mode == E_F32) {
+            if (ep.bias) {
+              float b[32];
+              load_bf16x32(ep.bias + col, b, nv);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] += b[j];
+            }
+            float* dst = reinterpret_cast<float*>(ep.C) + (int64_t)row * ep.ldc + col;
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+              if (j < nv) *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+          } else if (ep.mode == E_GEGLU_BWD) {
+            // v = dZ; U row holds a at [col..], g at [I+col..]
+            float a[32], g[32];
+            const bf16* Ur = ep.U + (int64_t)row * ep.ldu;
+            load_bf16x32(Ur + col, a, nv);
+            load_bf16x32(Ur + ep.I + col, g, nv);
+            float da[32], dg[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              da[j] = v[j] * g[j] * gelu_grad_f(a[j]);
+              dg[j] = v[j] * gelu_f(a[j]);
+            }
+            bf16* D = reinterpret_cast<bf16*>(ep.C) + (int64_t)row * ep.ldc;
+            store_bf16x32(D + col, da, nv);
+            store_bf16x32(D + ep.I + col, dg, nv);
+          } else {  // E_BF16 / E_GELU_AUX
+            if (ep.bias) {
+              float b[32];
+              load_bf16x32(ep.bias + col, b, nv);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] += b[j];
+            }
+            if (ep.res) {
+              float r[32];
+              load_bf16x32(ep.res + (int64_t)row * ep.ldr + col, r, nv);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] += r[j];
+            }
+            if (ep.mode == E_GELU_AUX) {
+              store_bf16x32(ep.aux + (int64_t)row * ep.ldaux + col, v, nv);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
+            }
+            store_bf16x32(reinterpret_cast<bf16*>(ep.C) + (int64_t)row * ep.ldc + col, v, nv);
+          }
+        }
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  if (warp == 2) sm100::tmem_dealloc(tmem_base, C::TMEM_COLS);
+}
+
+template <int BN, int STAGES, int A_MN, int B_MN, int PAIRED>
+mb_status launch(const GemmArgs& g, const CUtensorMap& ta, const CUtensorMap& tb, const Sched& sc, cudaStream_t s) {
+  using C = Cfg<BN, STAGES>;
+  auto k = gemm_kernel<BN, STAGES, A_MN, B_MN, PAIRED>;
+  static bool attr_set = false;  // benign race: idempotent
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) != cudaSuccess)
+      return MB_ERR_CUDA;
+    attr_set = true;
+  }
+  const int grid = std::max(1, std::min(sc.total, num_sms()));
+  k<<<grid, NTHREADS, C::SMEM, s>>>(ta, tb, g.M, g.N, sc, g.ep);
+  MB_CHECK_LAUNCH();
+  return MB_OK;
+}
+
+template <int BN, int STAGES>
+mb_status dispatch_majors(const GemmArgs& g, const CUtensorMap& ta, const CUtensorMap& tb, const Sched& sc,
+                          bool paired, cudaStream_t s) {
+  if (paired) return launch<BN, STAGES, 0, 0, 1>(g, ta, tb, sc, s);
+  if (!g.a_t && !g.b_t) return launch<BN, STAGES, 0, 0, 0>(g, ta, tb, sc, s);
+  if (!g.a_t && g.b_t) return launch<BN, STAGES, 0, 1, 0>(g, ta, tb, sc, s);
+  if (g.a_t && g.b_t) return launch<BN, STAGES, 1, 1, 0>(g, ta, tb, sc, s);
+  return launch<BN, STAGES, 1, 0, 0>(g, ta, tb, sc, s);
+}
+
+}  // namespace
+
+mb_status gemm(const GemmArgs& g, cudaStream_t s) {
+  MB_REQUIRE(g.A && g.B && g.ep.C, MB_ERR_INVALID_ARG);
+  MB_REQUIRE(g.M >= 0 && g.N >= 0 && g.K >= 0, MB_ERR_INVALID_ARG);
+  if (g.M == 0 || g.N == 0) return MB_OK;
+  MB_REQUIRE(g.K > 0, MB_ERR_INVALID_ARG);
+  MB_REQUIRE(g.N % 8 == 0 && g.lda % 8 == 0 && g.ldb % 8 == 0, MB_ERR_CONFIG);
+  const bool paired = g.ep.mode == E_GEGLU_FWD;
+  if (paired) MB_REQUIRE(g.ep.I % 128 == 0 && g.N == 2 * g.ep.I && !g.a_t && !g.b_t, MB_ERR_CONFIG);
+  if (g.ep.mode == E_GEGLU_BWD) MB_REQUIRE(g.N == g.ep.I, MB_ERR_CONFIG);
+
+  // BN: 256 for wide outputs, 128 when N is small (tiny configs) — GeGLU fwd is always a 256-wide
+  // paired tile (128 columns of W1 + the matching 128 of V).
+  const int BN = paired ? 256 : (g.N <= 128 ? 128 : 256);
+  CUtensorMap ta, tb;
+  bool ok;
+  if (!g.a_t) ok = make_tmap_bf16_2d(&ta, g.A, g.K, g.M, g.lda, BK, BM);
+  else ok = make_tmap_bf16_2d(&ta, g.A, g.M, g.K, g.lda, 64, BK);
+  MB_REQUIRE(ok, MB_ERR_CUDA);
+  if (paired) ok = make_tmap_bf16_2d(&tb, g.B, g.K, g.N, g.ldb, BK, 128);
+  else if (!g.b_t) ok = make_tmap_bf16_2d(&tb, g.B, g.K, g.N, g.ldb, BK, BN);
+  else ok = make_tmap_bf16_2d(&tb, g.B, g.N, g.K, g.ldb, 64, BK);
+  MB_REQUIRE(ok, MB_ERR_CUDA);
+
+  Sched sc;
+  sc.num_m = (g.M + BM - 1) / BM;
+  sc.num_n = paired ? g.ep.I / 128 : (g.N + BN - 1) / BN;
+  sc.nkb = (g.K + BK - 1) / BK;
+  int splits = 1;
+  if (g.ep.mode == E_F32_ACC) {
+    // split-K for the weight gradients (few output tiles, K = tokens): aim for >= 2 waves while
+    // keeping >= 8 k-blocks per split; partial sums meet in fp32 atomics (the += contract).
+    const int tiles = sc.num_m * sc.num_n;
+    const int want = (2 * num_sms() + tiles - 1) / tiles;
+    splits = std::max(1, std::min(want, sc.nkb / 8));
+  }
+  sc.kb_per = (sc.nkb + splits - 1) / splits;
+  sc.splits = (sc.nkb + sc.kb_per - 1) / sc.kb_per;
+  sc.total = sc.num_m * sc.num_n * sc.splits;
+
+  if (BN == 256) return dispatch_majors<256, 4>(g, ta, tb, sc, paired, s);
+  return dispatch_majors<128, 6>(g, ta, tb, sc, paired, s);
+}
+
+}  // namespace mb
+
+extern "C" mb_status mb_gemm(int32_t M, int32_t N, int32_t K, const mb_bf16* A, int64_t lda, int32_t a_t,
+                             const mb_bf16* B, int64_t ldb, int32_t b_t, void* C, int64_t ldc, int32_t epilogue,
+                             const mb_bf16* bias, const mb_bf16* residual, int64_t ldr, mb_bf16* aux, int64_t ldaux,
+                             mb_stream_t s) {
+  mb::GemmArgs g;
+  g.M = M, g.N = N, g.K = K;
+  g.A = reinterpret_cast<const bf16*>(A), g.lda = lda, g.a_t = a_t != 0;
+  g.B = reinterpret_cast<const bf16*>(B), g.ldb = ldb, g.b_t = b_t != 0;
+  switch (epilogue) {
+    case MB_EPI_BF16: g.ep.mode = mb::E_BF16; break;
+    case MB_EPI_F32_ACC: g.ep.mode = mb::E_F32_ACC; break;
+    case MB_EPI_F32: g.ep.mode = mb::E_F32; break;
+    case MB_EPI_GELU_AUX: g.ep.mode = mb::E_GELU_AUX; MB_REQUIRE(aux, MB_ERR_INVALID_ARG); break;
+    default: return MB_ERR_INVALID_ARG;
+  }
+  g.ep.C = C, g.ep.ldc = ldc;
+  g.ep.bias = reinterpret_cast<const bf16*>(bias);
+  g.ep.res = reinterpret_cast<const bf16*>(residual), g.ep.ldr = ldr;
+  g.ep.aux = reinterpret_cast<bf16*>(aux), g.ep.ldaux = ldaux;
+  return mb::gemm(g, reinterpret_cast<cudaStream_t>(s));
+}
+
+extern "C" mb_status mb_geglu_forward(const mb_bf16* X, int32_t n, int32_t H, int32_t I, const mb_bf16* w_1v,
+                                      const mb_bf16* b_1v, mb_bf16* U, mb_bf16* Z, mb_stream_t s) {
+  MB_REQUIRE(X && w_1v && b_1v && U && Z, MB_ERR_INVALID_ARG);
+  mb::GemmArgs g;
+  g.M = n, g.N = 2 * I, g.K = H;
+  g.A = reinterpret_cast<const bf16*>(X), g.lda = H;
+  g.B = reinterpret_cast<const bf16*>(w_1v), g.ldb = H;
+  g.ep.mode = mb::E_GEGLU_FWD;
+  g.ep.C = Z, g.ep.ldc = I;
+  g.ep.bias = reinterpret_cast<const bf16*>(b_1v);
+  g.ep.aux = reinterpret_cast<bf16*>(U), g.ep.ldaux = 2 * I;
+  g.ep.I = I;
+  return mb::gemm(g, reinterpret_cast<cudaStream_t>(s));
+}
+
+extern "C" mb_status mb_geglu_backward(const mb_bf16* dF, int32_t n, int32_t H, int32_t I, const mb_bf16* w_2,
+                                       const mb_bf16* U, mb_bf16* dU, mb_stream_t s) {
+  MB_REQUIRE(dF && w_2 && U && dU, MB_ERR_INVALID_ARG);
+  mb::GemmArgs g;
+  g.M = n, g.N = I, g.K = H;
+  g.A = reinterpret_cast<const bf16*>(dF), g.lda = H;
+  g.B = reinterpret_cast<const bf16*>(w_2), g.ldb = I, g.b_t = true;  // W2 [H, I] = [K, N]
+  g.ep.mode = mb::E_GEGLU_BWD;
+  g.ep.C = dU, g.ep.ldc = 2 * I;
+  g.ep.U = reinterpret_cast<const bf16*>(U), g.ep.ldu = 2 * I;
+  g.ep.I = I;
+  return mb::gemm(g, reinterpret_cast<cudaStream_t>(s));
+}

@@ -1,0 +1,266 @@
+// A11 — sparse MLM head on the masked tokens only + softmax cross-entropy ("30% masking
+// ratio"; vocab 30528 P:174; tied decoder R15; loss = mean over labelled positions S:534 with the
+// global count R18), A3 embedding composites, and the F1 fused AdamW step.
+#include <algorithm>
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mb {
+namespace {
+
+constexpr int CE_THREADS = 256;
+
+// one CTA per masked row: online (max, sum exp) over V, LSE, row loss, then
+// dz = (softmax(z) - onehot(y)) * inv_norm stored as bf16 (consumed by the dU / dE GEMMs)
+__global__ void __launch_bounds__(CE_THREADS) ce_kernel(const float* __restrict__ logits, const int* __restrict__ labels,
+                                                        int V, float inv_norm, float* __restrict__ lse_out,
+                                                        float* __restrict__ row_loss, bf16* __restrict__ dz) {
+  const int row = blockIdx.x;
+  const float* z = logits + (size_t)row * V;
+  float m = -INFINITY, s = 0.f;
+  for (int c = threadIdx.x * 4; c < V; c += CE_THREADS * 4) {
+    const float4 q = *reinterpret_cast<const float4*>(z + c);
+    const float mx = fmaxf(fmaxf(q.x, q.y), fmaxf(q.z, q.w));
+    const float nm = fmaxf(m, mx);
+    s = s * __expf(m - nm) + __expf(q.x - nm) + __expf(q.y - nm) + __expf(q.z - nm) + __expf(q.w - nm);
+    m = nm;
+  }
+  // block reduce (m, s)
+  __shared__ float sm[CE_THREADS / 32], ss[CE_THREADS / 32];
+  __shared__ float s_lse;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float om = __shfl_xor_sync(0xffffffffu, m, o);
+    const float os = __shfl_xor_sync(0xffffffffu, s, o);
+    const float nm = fmaxf(m, om);
+    s = (m == -INFINITY ? 0.f : s * __expf(m - nm)) + (om == -INFINITY ? 0.f : os * __expf(om - nm));
+    m = nm;
+  }
+  if (lane == 0) {
+    sm[warp] = m;
+    ss[warp] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float M = sm[0], S = ss[0];
+    for (int w = 1; w < CE_THREADS / 32; ++w) {
+      const float nm = fmaxf(M, sm[w]);
+      S = S * __expf(M - nm) + ss[w] * __expf(sm[w] - nm);
+      M = nm;
+    }
+    const float l = M + logf(S);
+    s_lse = l;
+    const int y = labels[row];
+    lse_out[row] = l;
+    row_loss[row] = l - z[y];
+  }
+  __syncthreads();
+  const float l = s_lse;
+  const int y = labels[row];
+  bf16* d = dz + (size_t)row * V;
+  for (int c = threadIdx.x * 4; c < V; c += CE_THREADS * 4) {
+    const float4 q = *reinterpret_cast<const float4*>(z + c);
+    float p0 = __expf(q.x - l), p1 = __expf(q.y - l), p2 = __expf(q.z - l), p3 = __expf(q.w - l);
+    if (y >= c && y < c + 4) {
+      if (y == c) p0 -= 1.f;
+      else if (y == c + 1) p1 -= 1.f;
+      else if (y == c + 2) p2 -= 1.f;
+      else p3 -= 1.f;
+    }
+    uint2 u;
+    u.x = pack_bf16x2(p0 * inv_norm, p1 * inv_norm);
+    u.y = pack_bf16x2(p2 * inv_norm, p3 * inv_norm);
+    *reinterpret_cast<uint2*>(d + c) = u;
+  }
+}
+
+__global__ void sum_kernel(const float* __restrict__ x, int n, float scale, float* __restrict__ out) {
+  __shared__ float sw[32];
+  float t = 0.f;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) t += x[i];
+  t = warp_sum(t);
+  if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = t;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float u = threadIdx.x < (blockDim.x >> 5) ? sw[threadIdx.x] : 0.f;
+    u = warp_sum(u);
+    if (threadIdx.x == 0) *out += u * scale;
+  }
+}
+
+__global__ void adamw_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
+                             const float* __restrict__ g, bf16* __restrict__ w, int64_t n, float lr, float b1, float b2,
+                             float eps, float wd, float gscale, float bc1, float bc2) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float gi = g[i] * gscale;
+    const float mi = b1 * m[i] + (1.f - b1) * gi;
+    const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    const float mh = mi / bc1, vh = vi / bc2;
+    float pi = p[i];
+    pi -= lr * (mh / (sqrtf(vh) + eps) + wd * pi);
+    p[i] = pi;
+    w[i] = __float2bfloat16_rn(pi);
+  }
+}
+
+inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace
+
+struct HeadWs {
+  bf16 *h, *tpre, *t, *u, *du;
+  float *stats, *logits, *row_loss;
+  bf16* dz;
+  size_t bytes;
+  HeadWs(char* base, int n, int H, int V) {
+    size_t o = 0;
+    auto take = [&](size_t b) {
+      char* p = base ? base + o : nullptr;
+      o += al(b);
+      return p;
+    };
+    h = (bf16*)take((size_t)n * H * 2);
+    tpre = (bf16*)take((size_t)n * H * 2);
+    t = (bf16*)take((size_t)n * H * 2);
+    u = (bf16*)take((size_t)n * H * 2);
+    du = (bf16*)take((size_t)n * H * 2);
+    stats = (float*)take((size_t)n * 2 * 4);
+    row_loss = (float*)take((size_t)n * 4);
+    logits = (float*)take((size_t)n * V * 4);
+    dz = (bf16*)take((size_t)n * V * 2);
+    bytes = o;
+  }
+};
+
+}  // namespace mb
+
+extern "C" {
+
+size_t mb_mlm_workspace_bytes(const mb_dims* d, int32_t n_masked) {
+  if (!d) return 0;
+  return mb::HeadWs(nullptr, std::max(n_masked, 1), d->hidden, d->vocab).bytes;
+}
+
+mb_status mb_mlm_loss(const mb_dims* d, const mb_head_params* p, const mb_bf16* y, int32_t nnz,
+                      const int32_t* masked_rows, const int32_t* labels, int32_t n_masked, float inv_norm,
+                      float* loss_sum, float* lse, mb_bf16* dy_top, const mb_head_grads* g, void* ws, size_t ws_bytes,
+                      mb_stream_t s_) {
+  using namespace mb;
+  if (!d || !p || !y || !masked_rows || !labels || !loss_sum || !lse || !dy_top || !g || !ws) return MB_ERR_INVALID_ARG;
+  if (n_masked < 0 || nnz < 0) return MB_ERR_INVALID_ARG;
+  if (n_masked > nnz) return MB_ERR_SHAPE;
+  const int H = d->hidden, V = d->vocab;
+  if (V < 1 || H % 8 || V % 8) return MB_ERR_CONFIG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(s_);
+  HeadWs w(reinterpret_cast<char*>(ws), std::max(n_masked, 1), H, V);
+  if (ws_bytes < w.bytes) return MB_ERR_WORKSPACE;
+  bf16* dyt = reinterpret_cast<bf16*>(dy_top);
+  if (n_masked == 0) {
+    if (cudaMemsetAsync(dyt, 0, (size_t)nnz * H * 2, s) != cudaSuccess) return MB_ERR_CUDA;
+    return MB_OK;
+  }
+  const int n = n_masked;
+  auto B = [](const mb_bf16* q) { return reinterpret_cast<const bf16*>(q); };
+  mb_status st;
+#define TRY(x)                      \
+  do {                              \
+    if ((st = (x)) != MB_OK) return st; \
+  } while (0)
+  // forward: h = Y[rows]; t = GeLU(h W_t^T + b_t); u = LN_h(t); z = u E^T + b_dec
+  TRY(gather_rows(B(y), masked_rows, n, H, w.h, s));
+  {
+    GemmArgs a;
+    a.M = n, a.N = H, a.K = H, a.A = w.h, a.lda = H, a.B = B(p->w_t), a.ldb = H;
+    a.ep.mode = E_GELU_AUX, a.ep.C = w.t, a.ep.ldc = H, a.ep.bias = B(p->b_t), a.ep.aux = w.tpre, a.ep.ldaux = H;
+    TRY(gemm(a, s));
+  }
+  TRY(layernorm_fwd(w.t, B(p->ln_g), B(p->ln_b), n, H, d->ln_eps, w.u, w.stats, s));
+  {
+    GemmArgs a;
+    a.M = n, a.N = V, a.K = H, a.A = w.u, a.lda = H, a.B = B(p->emb), a.ldb = H;
+    a.ep.mode = E_F32, a.ep.C = w.logits, a.ep.ldc = V, a.ep.bias = B(p->b_dec);
+    TRY(gemm(a, s));
+  }
+  ce_kernel<<<n, CE_THREADS, 0, s>>>(w.logits, labels, V, inv_norm, lse, w.row_loss, w.dz);
+  MB_CHECK_LAUNCH();
+  sum_kernel<<<1, 1024, 0, s>>>(w.row_loss, n, inv_norm, loss_sum);
+  MB_CHECK_LAUNCH();
+  // backward
+  TRY(colsum(w.dz, n, V, g->b_dec, s));
+  {
+    GemmArgs a;  // du = dz E   (E [V, H] = [K, N])
+    a.M = n, a.N = H, a.K = V, a.A = w.dz, a.lda = V, a.B = B(p->emb), a.ldb = H, a.b_t = true;
+    a.ep.mode = E_BF16, a.ep.C = w.du, a.ep.ldc = H;
+    TRY(gemm(a, s));
+  }
+  {
+    GemmArgs a;  // dE += dz^T u
+    a.M = V, a.N = H, a.K = n, a.A = w.dz, a.lda = V, a.a_t = true, a.B = w.u, a.ldb = H, a.b_t = true;
+    a.ep.mode = E_F32_ACC, a.ep.C = g->emb, a.ep.ldc = H;
+    TRY(gemm(a, s));
+  }
+  // LN_h backward fused with the GeLU' of the transform: du -> dt_pre (in place); db_t = sum dt_pre
+  TRY(layernorm_bwd(w.du, w.t, w.stats, B(p->ln_g), n, H, w.tpre, w.du, g->ln_g, g->ln_b, g->b_t, s));
+  {
+    GemmArgs a;  // dh = dt_pre W_t  (W_t [H_out, H_in] = [K, N]) -> reuse t
+    a.M = n, a.N = H, a.K = H, a.A = w.du, a.lda = H, a.B = B(p->w_t), a.ldb = H, a.b_t = true;
+    a.ep.mode = E_BF16, a.ep.C = w.t, a.ep.ldc = H;
+    TRY(gemm(a, s));
+  }
+  {
+    GemmArgs a;  // dW_t += dt_pre^T h
+    a.M = H, a.N = H, a.K = n, a.A = w.du, a.lda = H, a.a_t = true, a.B = w.h, a.ldb = H, a.b_t = true;
+    a.ep.mode = E_F32_ACC, a.ep.C = g->w_t, a.ep.ldc = H;
+    TRY(gemm(a, s));
+  }
+  TRY(scatter_rows(w.t, masked_rows, n, H, nnz, dyt, s));
+#undef TRY
+  return MB_OK;
+}
+
+mb_status mb_embed_forward(const mb_dims* d, const int32_t* ids, const int32_t* indices, int32_t nnz,
+                           const mb_bf16* emb, const mb_bf16* type_emb, const mb_bf16* ln_g, const mb_bf16* ln_b,
+                           mb_bf16* x0, float* stats, mb_stream_t s) {
+  if (!d || !ids || !indices || !emb || !type_emb || !ln_g || !ln_b || !x0 || !stats || nnz < 0)
+    return MB_ERR_INVALID_ARG;
+  if (d->hidden % 8 || d->hidden > 1024) return MB_ERR_CONFIG;
+  mb::EmbedSrc e;
+  e.ids = ids, e.indices = indices, e.emb = reinterpret_cast<const bf16*>(emb);
+  e.type_emb = reinterpret_cast<const bf16*>(type_emb);
+  return mb::embed_ln_fwd(e, reinterpret_cast<const bf16*>(ln_g), reinterpret_cast<const bf16*>(ln_b), nnz, d->hidden,
+                          d->ln_eps, reinterpret_cast<bf16*>(x0), stats, reinterpret_cast<cudaStream_t>(s));
+}
+
+mb_status mb_embed_backward(const mb_dims* d, const int32_t* ids, const int32_t* indices, int32_t nnz,
+                            const mb_bf16* emb, const mb_bf16* type_emb, const mb_bf16* ln_g, const float* stats,
+                            mb_bf16* dx0, float* d_emb, float* d_type_emb, float* d_ln_g, float* d_ln_b,
+                            mb_stream_t s) {
+  if (!d || !ids || !indices || !emb || !type_emb || !ln_g || !stats || !dx0 || !d_emb || !d_type_emb || !d_ln_g ||
+      !d_ln_b || nnz < 0)
+    return MB_ERR_INVALID_ARG;
+  if (d->hidden % 8 || d->hidden > 1024) return MB_ERR_CONFIG;
+  mb::EmbedSrc e;
+  e.ids = ids, e.indices = indices, e.emb = reinterpret_cast<const bf16*>(emb);
+  e.type_emb = reinterpret_cast<const bf16*>(type_emb), e.d_emb = d_emb;
+  // d_type_emb[0] = sum over tokens of dv (every token has type 0, R17) == the LN "dsum"
+  return mb::embed_ln_bwd(e, reinterpret_cast<const bf16*>(dx0), stats, reinterpret_cast<const bf16*>(ln_g), nnz,
+                          d->hidden, d_ln_g, d_ln_b, d_type_emb, reinterpret_cast<cudaStream_t>(s));
+}
+
+mb_status mb_adamw_step(float* master, float* m, float* v, const float* g, mb_bf16* w_bf16, int64_t n, float lr,
+                        float beta1, float beta2, float eps, float weight_decay, float grad_scale, int32_t step,
+                        mb_stream_t s) {
+  if (!master || !m || !v || !g || !w_bf16 || n < 0 || step < 1) return MB_ERR_INVALID_ARG;
+  if (n == 0) return MB_OK;
+  const float bc1 = 1.f - powf(beta1, (float)step), bc2 = 1.f - powf(beta2, (float)step);
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 8 * mb::num_sms());
+  mb::adamw_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(
+      master, m, v, g, reinterpret_cast<bf16*>(w_bf16), n, lr, beta1, beta2, eps, weight_decay, grad_scale, bc1, bc2);
+  MB_CHECK_LAUNCH();
+  return MB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,337 @@
+// A7 / A3 — bf16 LayerNorm forward/backward (LN "run in bfloat16 ... only 2-bytes are
+// required per-element"), the fused embedding gather + LN (no position table), and the
+// bias-gradient column sums.
+//
+// One warp per row, 16-byte (8 x bf16) vector loads, VPL vectors per lane held in registers,
+// warp-shuffle reductions; statistics, gamma/beta arithmetic and all reductions in fp32 (R12); the
+// output is rounded once to bf16.  Backward column sums (dgamma, dbeta, and the preceding linear's
+// bias gradient sum dx) accumulate per warp in registers, reduce per CTA through shared memory and
+// reach global fp32 with one atomic per column per CTA.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mb {
+namespace {
+
+constexpr int LN_THREADS = 256;
+constexpr int LN_WARPS = LN_THREADS / 32;
+
+struct RowSrc {
+  const bf16* x;          // plain mode: x[row*H]
+  const int* ids;         // embed mode: x = emb[ids[indices[row]]] + type_emb[0]
+  const int* indices;
+  const bf16* emb;
+  const bf16* type_emb;
+};
+
+template <int VPL, bool EMBED>
+__device__ __forceinline__ void load_row(const RowSrc& src, int row, int H, int lane, float* v, int& id) {
+  const bf16* base;
+  if (EMBED) {
+    id = src.ids[src.indices[row]];
+    base = src.emb + (size_t)id * H;
+  } else {
+    base = src.x + (size_t)row * H;
+  }
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int c = (i * 32 + lane) * 8;
+    if (c < H) {
+      bf16x8_to_f32(*reinterpret_cast<const uint4*>(base + c), v + i * 8);
+      if (EMBED) {
+        float t[8];
+        bf16x8_to_f32(*reinterpret_cast<const uint4*>(src.type_emb + c), t);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[i * 8 + j] += t[j];
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[i * 8 + j] = 0.f;
+    }
+  }
+}
+
+template <int VPL, bool EMBED>
+__global__ void __launch_bounds__(LN_THREADS) ln_fwd_kernel(RowSrc src, const bf16* __restrict__ gamma,
+                                                            const bf16* __restrict__ beta, int n, int H, float eps,
+                                                            bf16* __restrict__ y, float* __restrict__ stats) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * LN_WARPS + (threadIdx.x >> 5);
+  if (row >= n) return;
+  float v[VPL * 8];
+  int id;
+  load_row<VPL, EMBED>(src, row, H, lane, v, id);
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPL * 8; ++i) s += v[i];
+  const float mean = warp_sum(s) / H;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int c = (i * 32 + lane) * 8;
+    if (c < H) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float d = v[i * 8 + j] - mean;
+        q += d * d;
+      }
+    }
+  }
+  const float rstd = rsqrtf(warp_sum(q) / H + eps);
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int c = (i * 32 + lane) * 8;
+    if (c < H) {
+      float g[8], b[8], o[8];
+      bf16x8_to_f32(*reinterpret_cast<const uint4*>(gamma + c), g);
+      bf16x8_to_f32(*reinterpret_cast<const uint4*>(beta + c), b);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = (v[i * 8 + j] - mean) * rstd * g[j] + b[j];
+      *reinterpret_cast<uint4*>(y + (size_t)row * H + c) = f32_to_bf16x8(o);
+    }
+  }
+  if (lane == 0) *reinterpret_cast<float2*>(stats + 2 * (size_t)row) = make_float2(mean, rstd);
+}
+
+// Reduce one per-lane register vector (the same column layout in every warp) across the CTA and
+// atomically add it to out[H].
+template <int VPL>
+__device__ __forceinline__ void cta_column_reduce(const float* acc, float* sbuf, int H, float* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int c = (i * 32 + lane) * 8;
+    if (c < H) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sbuf[warp * H + c + j] = acc[i * 8 + j];
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < H; c += LN_THREADS) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < LN_WARPS; ++w) t += sbuf[w * H + c];
+    atomicAdd(out + c, t);
+  }
+}
+
+template <int VPL, bool EMBED, bool GELU>
+__global__ void __launch_bounds__(LN_THREADS) ln_bwd_kernel(RowSrc src, const bf16* __restrict__ dy,
+                                                            const float* __restrict__ stats,
+                                                            const bf16* __restrict__ gamma,
+                                                            const bf16* __restrict__ gelu_pre, int n, int H,
+                                                            bf16* dx, float* __restrict__ d_emb,
+                                                            float* __restrict__ dgamma, float* __restrict__ dbeta,
+                                                            float* __restrict__ dsum) {
+  extern __shared__ float sbuf[];
+  const int lane = threadIdx.x & 31;
+  float acc_g[VPL * 8], acc_b[VPL * 8], acc_s[VPL * 8];
+#pragma unroll
+  for (int i = 0; i < VPL * 8; ++i) acc_g[i] = acc_b[i] = acc_s[i] = 0.f;
+  float gm[VPL * 8];
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int c = (i * 32 + lane) * 8;
+    if (c < H) bf16x8_to_f32(*reinterpret_cast<const uint4*>(gamma + c), gm + i * 8);
+    else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) gm[i * 8 + j] = 0.f;
+    }
+  }
+  for (int row = blockIdx.x * LN_WARPS + (threadIdx.x >> 5); row < n; row += gridDim.x * LN_WARPS) {
+    float v[VPL * 8], g[VPL * 8];
+    int id = 0;
+    load_row<VPL, EMBED>(src, row, H, lane, v, id);
+    const float2 st = *reinterpret_cast<const float2*>(stats + 2 * (size_t)row);
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const int c = (i * 32 + lane) * 8;
+      if (c < H) {
+        float d[8];
+        bf16x8_to_f32(*reinterpret_cast<const uint4*>(dy + (size_t)row * H + c), d);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int k = i * 8 + j;
+          const float xh = (v[k] - st.x) * st.y;
+          v[k] = xh;
+          g[k] = d[j] * gm[k];
+          acc_g[k] += d[j] * xh;
+          acc_b[k] += d[j];
+          s1 += g[k];
+          s2 += g[k] * xh;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) g[i * 8 + j] = 0.f;
+      }
+    }
+    s1 = warp_sum(s1) / H;
+    s2 = warp_sum(s2) / H;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const int c = (i * 32 + lane) * 8;
+      if (c < H) {
+        float o[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int k = i * 8 + j;
+          o[j] = st.y * (g[k] - s1 - v[k] * s2);
+        }
+        if (GELU) {
+          float p[8];
+          bf16x8_to_f32(*reinterpret_cast<const uint4*>(gelu_pre + (size_t)row * H + c), p);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) o[j] *= gelu_grad_f(p[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc_s[i * 8 + j] += o[j];
+        if (EMBED) {
+          float* dst = d_emb + (size_t)id * H + c;
+          red_add_v4(dst, o[0], o[1], o[2], o[3]);
+          red_add_v4(dst + 4, o[4], o[5], o[6], o[7]);
+        } else {
+          *reinterpret_cast<uint4*>(dx + (size_t)row * H + c) = f32_to_bf16x8(o);
+        }
+      }
+    }
+  }
+  cta_column_reduce<VPL>(acc_g, sbuf, H, dgamma);
+  cta_column_reduce<VPL>(acc_b, sbuf, H, dbeta);
+  if (dsum) cta_column_reduce<VPL>(acc_s, sbuf, H, dsum);
+}
+
+// out[c] += sum_r x[r, c]; thread = one 8-column vector, blockIdx.y = row chunk
+__global__ void colsum_kernel(const bf16* __restrict__ x, int n, int C, int rows_per, float* __restrict__ out) {
+  const int cv = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = cv * 8;
+  if (c >= C) return;
+  const int r0 = blockIdx.y * rows_per, r1 = min(n, r0 + rows_per);
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int r = r0; r < r1; ++r) {
+    float f[8];
+    bf16x8_to_f32(ld_nc_v4(x + (size_t)r * C + c), f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] += f[j];
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) atomicAdd(out + c + j, acc[j]);
+}
+
+template <bool EMBED>
+mb_status ln_fwd_dispatch(const RowSrc& src, const bf16* gamma, const bf16* beta, int n, int H, float eps, bf16* y,
+                          float* stats, cudaStream_t s) {
+  if (n == 0) return MB_OK;
+  const int grid = (n + LN_WARPS - 1) / LN_WARPS;
+  const int vpl = (H / 8 + 31) / 32;
+  switch (vpl) {
+    case 1: ln_fwd_kernel<1, EMBED><<<grid, LN_THREADS, 0, s>>>(src, gamma, beta, n, H, eps, y, stats); break;
+    case 2: ln_fwd_kernel<2, EMBED><<<grid, LN_THREADS, 0, s>>>(src, gamma, beta, n, H, eps, y, stats); break;
+    case 3: ln_fwd_kernel<3, EMBED><<<grid, LN_THREADS, 0, s>>>(src, gamma, beta, n, H, eps, y, stats); break;
+    case 4: ln_fwd_kernel<4, EMBED><<<grid, LN_THREADS, 0, s>>>(src, gamma, beta, n, H, eps, y, stats); break;
+    default: return MB_ERR_CONFIG;
+  }
+  MB_CHECK_LAUNCH();
+  return MB_OK;
+}
+
+template <int VPL, bool EMBED>
+mb_status ln_bwd_launch(const RowSrc& src, const bf16* dy, const float* stats, const bf16* gamma,
+                        const bf16* gelu_pre, int n, int H, bf16* dx, float* d_emb, float* dg, float* db,
+                        float* dsum, cudaStream_t s) {
+  const int smem = LN_WARPS * H * sizeof(float);
+  const int grid = std::max(1, std::min((n + LN_WARPS - 1) / LN_WARPS, 4 * num_sms()));
+  if (gelu_pre)
+    ln_bwd_kernel<VPL, EMBED, true><<<grid, LN_THREADS, smem, s>>>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb,
+                                                                    dg, db, dsum);
+  else
+    ln_bwd_kernel<VPL, EMBED, false><<<grid, LN_THREADS, smem, s>>>(src, dy, stats, gamma, gelu_pre, n, H, dx,
+                                                                     d_emb, dg, db, dsum);
+  MB_CHECK_LAUNCH();
+  return MB_OK;
+}
+
+template <bool EMBED>
+mb_status ln_bwd_dispatch(const RowSrc& src, const bf16* dy, const float* stats, const bf16* gamma,
+                          const bf16* gelu_pre, int n, int H, bf16* dx, float* d_emb, float* dg, float* db,
+                          float* dsum, cudaStream_t s) {
+  if (n == 0) return MB_OK;
+  switch ((H / 8 + 31) / 32) {
+    case 1: return ln_bwd_launch<1, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s);
+    case 2: return ln_bwd_launch<2, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s);
+    case 3: return ln_bwd_launch<3, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s);
+    case 4: return ln_bwd_launch<4, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s);
+  }
+  return MB_ERR_CONFIG;
+}
+
+}  // namespace
+
+mb_status layernorm_fwd(const bf16* x, const bf16* gamma, const bf16* beta, int n, int H, float eps, bf16* y,
+                        float* stats, cudaStream_t s) {
+  RowSrc src{x, nullptr, nullptr, nullptr, nullptr};
+  return ln_fwd_dispatch<false>(src, gamma, beta, n, H, eps, y, stats, s);
+}
+
+mb_status layernorm_bwd(const bf16* dy, const bf16* x, const float* stats, const bf16* gamma, int n, int H,
+                        const bf16* gelu_pre, bf16* dx, float* dgamma, float* dbeta, float* dsum, cudaStream_t s) {
+  RowSrc src{x, nullptr, nullptr, nullptr, nullptr};
+  return ln_bwd_dispatch<false>(src, dy, stats, gamma, gelu_pre, n, H, dx, nullptr, dgamma, dbeta, dsum, s);
+}
+
+mb_status embed_ln_fwd(const EmbedSrc& e, const bf16* gamma, const bf16* beta, int n, int H, float eps, bf16* y,
+                       float* stats, cudaStream_t s) {
+  RowSrc src{nullptr, e.ids, e.indices, e.emb, e.type_emb};
+  return ln_fwd_dispatch<true>(src, gamma, beta, n, H, eps, y, stats, s);
+}
+
+mb_status embed_ln_bwd(const EmbedSrc& e, const bf16* dy, const float* stats, const bf16* gamma, int n, int H,
+                       float* dgamma, float* dbeta, float* dsum, cudaStream_t s) {
+  RowSrc src{nullptr, e.ids, e.indices, e.emb, e.type_emb};
+  return ln_bwd_dispatch<true>(src, dy, stats, gamma, nullptr, n, H, nullptr, e.d_emb, dgamma, dbeta, dsum, s);
+}
+
+mb_status colsum(const bf16* x, int n, int C, float* out, cudaStream_t s) {
+  if (n == 0 || C == 0) return MB_OK;
+  if (C % 8) return MB_ERR_CONFIG;
+  const int cvec = C / 8;
+  const int bx = (cvec + 127) / 128;
+  const int target = 4 * num_sms();
+  int by = std::max(1, std::min((target + bx - 1) / bx, (n + 63) / 64));
+  const int rows_per = (n + by - 1) / by;
+  by = (n + rows_per - 1) / rows_per;
+  colsum_kernel<<<dim3(bx, by), 128, 0, s>>>(x, n, C, rows_per, out);
+  MB_CHECK_LAUNCH();
+  return MB_OK;
+}
+
+}  // namespace mb
+
+extern "C" {
+
+mb_status mb_layernorm_forward(const mb_bf16* x, const mb_bf16* gamma, const mb_bf16* beta, int32_t n, int32_t H,
+                               float eps, mb_bf16* y, float* stats, mb_stream_t s) {
+  if (!x || !gamma || !beta || !y || !stats || n < 0 || H <= 0) return MB_ERR_INVALID_ARG;
+  if (H % 8 || H > 1024) return MB_ERR_CONFIG;
+  return mb::layernorm_fwd(reinterpret_cast<const bf16*>(x), reinterpret_cast<const bf16*>(gamma),
+                           reinterpret_cast<const bf16*>(beta), n, H, eps, reinterpret_cast<bf16*>(y), stats,
+                           reinterpret_cast<cudaStream_t>(s));
+}
+
+mb_status mb_layernorm_backward(const mb_bf16* dy, const mb_bf16* x, const float* stats, const mb_bf16* gamma,
+                                int32_t n, int32_t H, const mb_bf16* gelu_pre, mb_bf16* dx, float* dgamma,
+                                float* dbeta, float* dsum, mb_stream_t s) {
+  if (!dy || !x || !stats || !gamma || !dx || !dgamma || !dbeta || n < 0 || H <= 0) return MB_ERR_INVALID_ARG;
+  if (H % 8 || H > 1024) return MB_ERR_CONFIG;
+  return mb::layernorm_bwd(reinterpret_cast<const bf16*>(dy), reinterpret_cast<const bf16*>(x), stats,
+                           reinterpret_cast<const bf16*>(gamma), n, H, reinterpret_cast<const bf16*>(gelu_pre),
+                           reinterpret_cast<bf16*>(dx), dgamma, dbeta, dsum, reinterpret_cast<cudaStream_t>(s));
+}
+
+mb_status mb_colsum(const mb_bf16* x, int32_t n, int32_t C, float* out, mb_stream_t s) {
+  if (!x || !out || n < 0 || C < 0) return MB_ERR_INVALID_ARG;
+  return mb::colsum(reinterpret_cast<const bf16*>(x), n, C, out, reinterpret_cast<cudaStream_t>(s));
+}
+
+}  // extern "C"

@@ -1,0 +1,89 @@
+// Host runtime pieces of the C ABI: status strings, version, device attribute cache, TMA maps,
+// ALiBi slopes.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <mutex>
+#include "common.cuh"
+#include "tma.h"
+
+namespace mb {
+
+static int g_sms[64];
+static std::once_flag g_sms_once[64];
+
+int num_sms() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 148;
+  std::call_once(g_sms_once[dev], [dev] {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    g_sms[dev] = n > 0 ? n : 148;
+  });
+  return g_sms[dev];
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+bool make_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems,
+                       uint32_t box_inner, uint32_t box_outer, bool swizzle128) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld_elems * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace mb
+
+extern "C" {
+
+const char* mb_status_string(int s) {
+  switch (s) {
+    case MB_OK: return "MB_OK";
+    case MB_ERR_INVALID_ARG: return "MB_ERR_INVALID_ARG";
+    case MB_ERR_CONFIG: return "MB_ERR_CONFIG";
+    case MB_ERR_SHAPE: return "MB_ERR_SHAPE";
+    case MB_ERR_MASK_LAYOUT: return "MB_ERR_MASK_LAYOUT";
+    case MB_ERR_LABEL_RANGE: return "MB_ERR_LABEL_RANGE";
+    case MB_ERR_WORKSPACE: return "MB_ERR_WORKSPACE";
+    case MB_ERR_ARCH: return "MB_ERR_ARCH";
+    case MB_ERR_CUDA: return "MB_ERR_CUDA";
+  }
+  return "MB_ERR_UNKNOWN";
+}
+
+const char* mb_version(void) { return "mosaicbert-b200 0.1 (sm_100a)"; }
+
+// geometric sequence with ratio 2^(-8/n) starting at 2^(-8/n) (R3).  Computed in double
+// and rounded once to float, so it is the correctly rounded fp32 value of the closed form.
+mb_status mb_alibi_slopes(int32_t heads, float* out) {
+  if (!out) return MB_ERR_INVALID_ARG;
+  if (heads <= 0) return MB_ERR_CONFIG;
+  for (int h = 0; h < heads; ++h) out[h] = (float)exp2(-8.0 * (double)(h + 1) / (double)heads);
+  return MB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,284 @@
+"""MosaicBERT data-parallel training step on the unpadded stream (SURVEY §3 call stack 2).
+
+Host-side orchestration only: every numeric step runs in libmosaicbert.so (see _lib.py).  torch
+provides device memory, the CUDA stream and the NCCL process group.
+
+Memory layout (HBM):
+  * one flat bf16 parameter buffer and one flat fp32 gradient buffer per encoder layer (the
+    layer's allreduce bucket), plus a "head" bucket (MLM transform + LN_h + decoder bias) and an
+    "embedding" bucket (E_tok — tied with the decoder, R15 — E_type, LN_e);
+  * fp32 master weights + AdamW moments per bucket (F1);
+  * per-layer forward "saved" buffers and one backward workspace, sized for the largest micro-batch
+    and reused every step (no allocation inside a step).
+
+Data parallelism (P:580 DDP): each rank runs its micro-batches; on the last micro-step
+of an optimizer step, each layer's gradient bucket is all-reduced asynchronously as soon as that
+layer's backward is enqueued (NCCL orders its stream after the compute stream), so the transfers
+overlap the remaining backward.  The loss is the sum over masked tokens divided by the GLOBAL masked
+count of the optimizer step (R18), applied as the optimizer's gradient scale.
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+from typing import Sequence
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib as L
+
+LAYER_SHAPES = lambda H, I: [  # noqa: E731  (nn.Linear W[out, in])
+    ("w_qkv", (3 * H, H)), ("b_qkv", (3 * H,)), ("w_o", (H, H)), ("b_o", (H,)), ("ln1_g", (H,)), ("ln1_b", (H,)),
+    ("w_1v", (2 * I, H)), ("b_1v", (2 * I,)), ("w_2", (H, I)), ("b_2", (H,)), ("ln2_g", (H,)), ("ln2_b", (H,))]
+HEAD_SHAPES = lambda H, V: [("w_t", (H, H)), ("b_t", (H,)), ("lnh_g", (H,)), ("lnh_b", (H,)), ("b_dec", (V,))]  # noqa
+EMB_SHAPES = lambda H, V: [("emb", (V, H)), ("type_emb", (2, H)), ("lne_g", (H,)), ("lne_b", (H,))]  # noqa
+
+
+@dataclasses.dataclass(frozen=True)
+class ModelDims:
+    hidden: int
+    heads: int
+    intermediate: int
+    vocab: int
+    layers: int
+    ln_eps: float = 1e-12
+
+    def c(self) -> L.Dims:
+        return L.dims(self.hidden, self.heads, self.intermediate, self.vocab, self.ln_eps)
+
+
+def param_count(d: ModelDims) -> int:
+    n = sum(int(np.prod(s)) for _, s in LAYER_SHAPES(d.hidden, d.intermediate)) * d.layers
+    n += sum(int(np.prod(s)) for _, s in HEAD_SHAPES(d.hidden, d.vocab))
+    n += sum(int(np.prod(s)) for _, s in EMB_SHAPES(d.hidden, d.vocab))
+    return n
+
+
+class Bucket:
+    """A flat bf16 parameter buffer + fp32 grad buffer (+ optimizer state) with named views."""
+
+    def __init__(self, shapes, device):
+        self.shapes = shapes
+        self.numel = sum(int(np.prod(s)) for _, s in shapes)
+        pad = (self.numel + 63) // 64 * 64
+        self.w = torch.zeros(pad, dtype=torch.bfloat16, device=device)
+        self.g = torch.zeros(pad, dtype=torch.float32, device=device)
+        self.master = None
+        self.m = None
+        self.v = None
+        self.p, self.gv = {}, {}
+        o = 0
+        for name, s in shapes:
+            n = int(np.prod(s))
+            self.p[name] = self.w[o:o + n].view(*s)
+            self.gv[name] = self.g[o:o + n].view(*s)
+            o += n
+        self._off = o
+
+    def load(self, src: dict):
+        for name, _ in self.shapes:
+            v = src[name]
+            t = torch.as_tensor(np.asarray(v, dtype=np.float32)) if not torch.is_tensor(v) else v
+            self.p[name].copy_(t.to(torch.bfloat16))
+
+    def init_optimizer(self):
+        self.master = self.w.float().clone()
+        self.m = torch.zeros_like(self.master)
+        self.v = torch.zeros_like(self.master)
+
+
+class MosaicBert:
+    """MosaicBERT encoder + MLM head whose forward/backward run in libmosaicbert.so."""
+
+    def __init__(self, dims: ModelDims, params: dict | None = None, device: str | torch.device = "cuda",
+                 process_group=None):
+        self.d = dims
+        self.cd = dims.c()
+        self.device = torch.device(device)
+        L.lib()  # fail loudly now if the library is missing
+        H, I, V = dims.hidden, dims.intermediate, dims.vocab
+        for name, s in LAYER_SHAPES(H, I):
+            assert all(x % 8 == 0 for x in s[-1:]), name
+        # bucket offsets must keep every tensor 16-byte aligned: all sizes are multiples of 8
+        self.layer_buckets = [Bucket(LAYER_SHAPES(H, I), self.device) for _ in range(dims.layers)]
+        self.head_bucket = Bucket(HEAD_SHAPES(H, V), self.device)
+        self.emb_bucket = Bucket(EMB_SHAPES(H, V), self.device)
+        self.buckets = [*self.layer_buckets, self.head_bucket, self.emb_bucket]
+        self.slopes = torch.from_numpy(L.alibi_slopes(dims.heads)).to(self.device)
+        self.pg = process_group
+        self._cap = (0, 0)
+        self._nm_cap = 0
+        self.step_count = 0
+        self.loss_sum = torch.zeros(1, dtype=torch.float32, device=self.device)
+        self.masked_count = 0
+        if params is not None:
+            self.load(params)
+
+    # ------------------------------------------------------------------ parameters
+    def load(self, params: dict):
+        for b, lp in zip(self.layer_buckets, params["layers"]):
+            b.load(lp)
+        self.head_bucket.load(params)
+        self.emb_bucket.load(params)
+        torch.cuda.synchronize(self.device)
+
+    def head_params(self):
+        h, e = self.head_bucket.p, self.emb_bucket.p
+        return L.HeadPtrs(*[L._p(x) for x in (h["w_t"], h["b_t"], h["lnh_g"], h["lnh_b"], e["emb"], h["b_dec"])])
+
+    def head_grads(self):
+        h, e = self.head_bucket.gv, self.emb_bucket.gv
+        return L.HeadPtrs(*[L._p(x) for x in (h["w_t"], h["b_t"], h["lnh_g"], h["lnh_b"], e["emb"], h["b_dec"])])
+
+    def zero_grad(self):
+        for b in self.buckets:
+            b.g.zero_()
+        self.loss_sum.zero_()
+        self.masked_count = 0
+
+    # ------------------------------------------------------------------ buffers
+    def _ensure(self, B: int, Lmax: int):
+        if self._cap[0] >= B and self._cap[1] >= Lmax:
+            return
+        B = max(B, self._cap[0])
+        Lmax = max(Lmax, self._cap[1])
+        T = B * Lmax
+        H = self.d.hidden
+        dev = self.device
+        self.cu = torch.empty(B + 1, dtype=torch.int32, device=dev)
+        self.indices = torch.empty(T, dtype=torch.int32, device=dev)
+        self.meta = torch.zeros(4, dtype=torch.int32, device=dev)
+        self.meta_host = torch.zeros(4, dtype=torch.int32).pin_memory()
+        self.rows = torch.empty(T, dtype=torch.int32, device=dev)
+        self.labs = torch.empty(T, dtype=torch.int32, device=dev)
+        self.xs = [torch.empty(T, H, dtype=torch.bfloat16, device=dev) for _ in range(self.d.layers + 1)]
+        self.estats = torch.empty(T, 2, dtype=torch.float32, device=dev)
+        sb = L.layer_saved_bytes(self.cd, T)
+        self.saved = [torch.empty(sb, dtype=torch.uint8, device=dev) for _ in range(self.d.layers)]
+        self.ws = torch.empty(L.layer_workspace_bytes(self.cd, T, Lmax), dtype=torch.uint8, device=dev)
+        self.dy = [torch.empty(T, H, dtype=torch.bfloat16, device=dev) for _ in range(2)]
+        self.lse = torch.empty(T, dtype=torch.float32, device=dev)
+        self._cap = (B, Lmax)
+
+    def _ensure_head(self, n_m: int):
+        if n_m <= self._nm_cap:
+            return
+        cap = max(n_m, int(self._nm_cap * 1.25) + 64)
+        self.head_ws = torch.empty(L.mlm_workspace_bytes(self.cd, cap), dtype=torch.uint8, device=self.device)
+        self._nm_cap = cap
+
+    # ------------------------------------------------------------------ one micro-step
+    def micro_step(self, ids: torch.Tensor, mask: torch.Tensor, labels: torch.Tensor, inv_norm: float = 1.0,
+                   allreduce: bool = False, timers: dict | None = None):
+        """Forward + backward of one micro-batch (device int32 [B, L] tensors, right-padded).
+        Gradients accumulate (+=) into the buckets.  Returns (nnz, n_masked)."""
+        B, Lq = mask.shape
+        self._ensure(B, Lq)
+        cd = self.cd
+        # A1: unpad index + MLM selection; one 16-byte D2H read of {nnz, max_seqlen, status, n_masked}
+        L._ck("mb_unpad_index", L.lib().mb_unpad_index(L._p(mask), B, Lq, L._p(self.cu), L._p(self.indices),
+                                                        L._p(self.meta), L._stream()))
+        L._ck("mb_mlm_select", L.lib().mb_mlm_select(L._p(labels), L._p(self.indices), B * Lq, self.d.vocab,
+                                                      L._p(self.rows), L._p(self.labs), L._p(self.meta), L._stream()))
+        self.meta_host.copy_(self.meta, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        nnz, max_seqlen, status, n_m = (int(x) for x in self.meta_host.tolist())
+        if status != 0:
+            raise RuntimeError(f"batch rejected: {L.STATUS.get(status, status)}")
+        self.masked_count += n_m
+        if nnz == 0:
+            return 0, 0
+        packed = L.Packed(L._p(self.cu), B, nnz, max_seqlen)
+        e = self.emb_bucket.p
+        # A3: embedding gather + LN
+        L.embed_forward(cd, ids, self.indices, nnz, e["emb"], e["type_emb"], e["lne_g"], e["lne_b"], self.xs[0],
+                        self.estats)
+        # A4-A9: encoder layers
+        lps = [L.layer_ptrs(b.p) for b in self.layer_buckets]
+        for l in range(self.d.layers):
+            L.encoder_forward(cd, lps[l], packed, self.slopes, self.xs[l], self.xs[l + 1], self.saved[l])
+        # A11: MLM head + CE (fwd + bwd)
+        self._ensure_head(max(n_m, 1))
+        dy, dx = self.dy
+        t = timers.get("head") if timers else None
+        if t is not None:
+            t[0].record()
+        L.mlm_loss(cd, self.head_params(), self.xs[self.d.layers], nnz, self.rows, self.labs, n_m, inv_norm,
+                   self.loss_sum, self.lse, dy, self.head_grads(), self.head_ws)
+        if t is not None:
+            t[1].record()
+        handles = []
+        if allreduce:
+            handles.append(self._allreduce(self.head_bucket))
+        # backward through the layers; each bucket's allreduce is issued as soon as it is final
+        for l in range(self.d.layers - 1, -1, -1):
+            L.encoder_backward(cd, lps[l], packed, self.slopes, self.xs[l], self.saved[l], dy, dx,
+                               L.layer_ptrs(self.layer_buckets[l].gv), self.ws)
+            dy, dx = dx, dy
+            if allreduce:
+                handles.append(self._allreduce(self.layer_buckets[l]))
+        g = self.emb_bucket.gv
+        L.embed_backward(cd, ids, self.indices, nnz, e["emb"], e["type_emb"], e["lne_g"], self.estats, dy, g["emb"],
+                         g["type_emb"][0], g["lne_g"], g["lne_b"])
+        if allreduce:
+            handles.append(self._allreduce(self.emb_bucket))
+        self._handles = [h for h in handles if h is not None]
+        return nnz, n_m
+
+    def _allreduce(self, b: Bucket):
+        if self.pg is None and not (dist.is_available() and dist.is_initialized()):
+            return None
+        if dist.get_world_size(self.pg) == 1:
+            return None
+        return dist.all_reduce(b.g, op=dist.ReduceOp.SUM, group=self.pg, async_op=True)
+
+    def wait_grads(self):
+        for h in getattr(self, "_handles", []):
+            h.wait()
+        self._handles = []
+
+    # ------------------------------------------------------------------ optimizer (F1)
+    def optimizer_step(self, grad_scale: float, lr: float = 5e-4, betas=(0.9, 0.98), eps=1e-6,
+                       weight_decay: float = 1e-5):
+        """Decoupled AdamW (Table A1) over every bucket; rewrites the bf16 weights."""
+        self.step_count += 1
+        for b in self.buckets:
+            if b.master is None:
+                b.init_optimizer()
+            L.adamw_step(b.master, b.m, b.v, b.g, b.w, lr, betas[0], betas[1], eps, weight_decay, grad_scale,
+                         self.step_count)
+
+    # ------------------------------------------------------------------ whole optimizer step
+    def train_step(self, micro_batches: Sequence[tuple], global_masked: int | None = None, lr: float = 5e-4,
+                   optimizer: bool = True):
+        """micro_batches: [(ids, mask, labels), ...] device int32 tensors.  Gradients are summed over
+        micro-steps (+= contract) and ranks (allreduce on the last micro-step), then scaled by
+        1/N_masked_global in the optimizer.  Returns the device loss tensor (mean CE)."""
+        self.zero_grad()
+        n = len(micro_batches)
+        for i, (ids, mask, labels) in enumerate(micro_batches):
+            self.micro_step(ids, mask, labels, inv_norm=1.0, allreduce=(i == n - 1))
+        if global_masked is None:
+            global_masked = self.masked_count
+            if self.pg is not None or (dist.is_available() and dist.is_initialized()):
+                if dist.get_world_size(self.pg) > 1:
+                    t = torch.tensor([global_masked], dtype=torch.int64, device=self.device)
+                    dist.all_reduce(t, group=self.pg)
+                    global_masked = int(t.item())
+        self.wait_grads()
+        scale = 1.0 / max(global_masked, 1)
+        if optimizer:
+            self.optimizer_step(scale, lr=lr)
+        return self.loss_sum * scale
+
+    def grads_numpy(self, scale: float = 1.0) -> dict:
+        """All gradients as float64 numpy arrays in the synth/oracle naming (tests)."""
+        out = {"layers": []}
+        for b in self.layer_buckets:
+            out["layers"].append({k: v.double().cpu().numpy() * scale for k, v in b.gv.items()})
+        for b in (self.head_bucket, self.emb_bucket):
+            for k, v in b.gv.items():
+                out[k] = v.double().cpu().numpy() * scale
+        return out

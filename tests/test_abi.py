@@ -1,0 +1,88 @@
+"""CPU-side checks of the C ABI: the library loads, exports every symbol include/mosaicbert.h
+declares, and the host-only entry points behave (no GPU needed: nothing here launches a kernel)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "mosaicbert.h")
+LIB = os.path.join(ROOT, "paper_2312_17482_b200", "libmosaicbert.so")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(LIB):
+        from paper_2312_17482_b200 import build
+        build.build(verbose=False)
+    from paper_2312_17482_b200 import _lib
+    return _lib.lib()
+
+
+def declared_symbols():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"MB_API\s+[\w\s\*]*?\b(mb_\w+)\s*\(", txt)))
+
+
+def test_header_declares_abi():
+    syms = declared_symbols()
+    for s in ("mb_unpad_index", "mb_encoder_forward", "mb_encoder_backward", "mb_mlm_loss", "mb_alibi_slopes",
+              "mb_gather_rows", "mb_scatter_rows", "mb_embed_forward", "mb_embed_backward"):
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol(lib):
+    out = subprocess.run(["nm", "-D", "--defined-only", LIB], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\sT\s(mb_\w+)", out))
+    missing = [s for s in declared_symbols() if s not in exported]
+    assert not missing, missing
+    from paper_2312_17482_b200 import _lib
+    assert set(_lib.exported_symbols()) <= exported
+
+
+def test_sass_is_sm100a_tcgen05(lib):
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    for mnemonic in ("UTCHMMA", "UTMALDG", "LDTM"):  # tcgen05.mma, TMA loads, tcgen05.ld
+        assert mnemonic in out, mnemonic
+
+
+@pytest.mark.parametrize("n", [1, 2, 8, 12, 16, 24])
+def test_alibi_slopes_bitexact_vs_oracle(lib, n):
+    from paper_2312_17482_b200 import _lib
+    got = _lib.alibi_slopes(n)
+    want = O.alibi_slopes(n).astype(np.float32)  # correctly rounded fp32 of the closed form
+    assert got.dtype == np.float32 and np.array_equal(got, want)
+
+
+def test_host_argument_errors(lib):
+    out = np.zeros(4, np.float32)
+    assert lib.mb_alibi_slopes(0, out.ctypes.data) == 2  # MB_ERR_CONFIG
+    assert lib.mb_alibi_slopes(4, None) == 1
+    assert lib.mb_unpad_index(None, 1, 1, None, None, None, None) == 1
+    assert lib.mb_gemm(4, 4, 4, None, 8, 0, None, 8, 0, None, 8, 0, None, None, 0, None, 0, None) == 1
+    from paper_2312_17482_b200 import _lib
+    d = _lib.dims(96, 5, 256, 128)  # hidden % heads != 0
+    lp = _lib.LayerPtrs()
+    pk = _lib.Packed(1, 1, 1, 1)
+    assert lib.mb_encoder_forward(ctypes.byref(d), ctypes.byref(lp), ctypes.byref(pk), 1, 1, 1, 1, None) == 2
+    d = _lib.dims(64, 1, 256, 128)  # head_dim 64 ok, but I=256 ok -> null ptrs -> invalid arg
+    assert lib.mb_encoder_forward(ctypes.byref(d), ctypes.byref(lp), ctypes.byref(pk), None, None, None, None,
+                                  None) == 1
+    assert lib.mb_status_string(4) == b"MB_ERR_MASK_LAYOUT"
+
+
+def test_workspace_queries(lib):
+    from paper_2312_17482_b200 import _lib
+    d = _lib.dims(768, 12, 3072, 30528)
+    sb = _lib.layer_saved_bytes(d, 65536)
+    # QKV 3H + O H + S1 H + Y1 H + U 2I + Z I + S2 H (bf16) + LSE heads + 2x stats (fp32) per token
+    per_tok = 2 * (3 * 768 + 768 + 768 + 768 + 2 * 3072 + 3072 + 768) + 4 * 12 + 16
+    assert per_tok * 65536 <= sb <= per_tok * 65536 + 16 * 256
+    assert _lib.layer_workspace_bytes(d, 65536, 128) > 0
+    assert _lib.mlm_workspace_bytes(d, 100) >= 100 * 30528 * 6

@@ -1,0 +1,296 @@
+"""GPU parity of every kernel behind the C ABI against the fp64 oracle (or, for the plain GEMM, the
+fp64 product of the same bf16 operands).  Integer work is compared bit-exactly."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import synth
+from parity import check, np64, to_dev
+
+pytestmark = pytest.mark.gpu
+
+mb = pytest.importorskip("paper_2312_17482_b200")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    mb.lib()
+
+
+BF = torch.bfloat16
+I32 = torch.int32
+
+
+def _bf(a):
+    return to_dev(a, torch.float32).to(BF)
+
+
+# ------------------------------------------------------------------------------------ A1 / A2
+MASK_CASES = {
+    "C1": lambda: synth.make_batch("C1", 0)["attention_mask"],
+    "C2": lambda: synth.make_batch("C2", 2000)["attention_mask"],
+    "C5": lambda: synth.make_batch("C5", 5000)["attention_mask"],
+    "C4": lambda: synth.make_batch("C4", 4000)["attention_mask"],
+    "zero_rows": lambda: synth.mask_from_lengths(np.array([0, 5, 0, 3, 0]), 7),
+    "L1": lambda: synth.mask_from_lengths(np.array([1, 0, 1, 1]), 1),
+    "big_ragged": lambda: synth.mask_from_lengths(np.random.default_rng(0).integers(0, 301, 3000), 300),
+}
+
+
+@pytest.mark.parametrize("case", sorted(MASK_CASES))
+def test_unpad_index_bitexact(case):
+    mask = MASK_CASES[case]().astype(np.int32)
+    cu, idx, meta = mb.unpad_index(to_dev(mask, I32))
+    torch.cuda.synchronize()
+    ocu, oidx, omax, ost = O.unpad_index(mask)
+    m = meta.cpu().numpy()
+    assert m[0] == len(oidx) and m[1] == omax and m[2] == ost
+    assert np.array_equal(cu.cpu().numpy(), ocu)
+    assert np.array_equal(idx.cpu().numpy()[: m[0]], oidx)
+
+
+def test_unpad_index_nonprefix_status():
+    mask = np.array([[1, 0, 1, 0], [1, 1, 0, 0]], dtype=np.int32)
+    _, idx, meta = mb.unpad_index(to_dev(mask, I32))
+    m = meta.cpu().numpy()
+    assert m[2] == O.MB_ERR_MASK_LAYOUT
+    assert idx.cpu().numpy()[: m[0]].tolist() == O.unpad_index(mask)[1].tolist()
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C5"])
+def test_mlm_select_bitexact(cfg):
+    bt = synth.make_batch(cfg, 7)
+    mask, labels = bt["attention_mask"], bt["labels"]
+    V = synth.CONFIGS[cfg].dims.vocab
+    cu, idx, meta = mb.unpad_index(to_dev(mask, I32))
+    rows, labs = mb.mlm_select(to_dev(labels, I32).reshape(-1), idx, V, meta)
+    m = meta.cpu().numpy()
+    _, oidx, _, _ = O.unpad_index(mask)
+    lab_packed = labels.reshape(-1)[oidx]
+    want = np.flatnonzero(lab_packed != -100)
+    assert m[3] == len(want) and m[2] == 0
+    assert np.array_equal(rows.cpu().numpy()[: m[3]], want)
+    assert np.array_equal(labs.cpu().numpy()[: m[3]], lab_packed[want])
+
+
+def test_mlm_select_label_range():
+    mask = np.ones((1, 4), dtype=np.int32)
+    labels = np.array([[-100, 5, 200, -100]], dtype=np.int32)
+    cu, idx, meta = mb.unpad_index(to_dev(mask, I32))
+    mb.mlm_select(to_dev(labels, I32).reshape(-1), idx, 128, meta)
+    assert meta.cpu().numpy()[2] == O.MB_ERR_LABEL_RANGE
+
+
+@pytest.mark.parametrize("H", [64, 768])
+def test_gather_scatter_roundtrip_bitwise(H):
+    mask = synth.make_batch("C5", 3, B=64)["attention_mask"]
+    B, L = mask.shape
+    x = synth.make_hidden(mask, H, 1)
+    xd = _bf(x.reshape(B * L, H))
+    cu, idx, meta = mb.unpad_index(to_dev(mask, I32))
+    nnz = int(meta[0].item())
+    packed = torch.empty(nnz, H, dtype=BF, device="cuda")
+    mb.gather_rows(xd, idx, nnz, packed)
+    _, oidx, _, _ = O.unpad_index(mask)
+    assert torch.equal(packed.cpu(), xd.cpu()[torch.from_numpy(oidx).long()])
+    back = torch.full((B * L, H), 7.0, dtype=BF, device="cuda")
+    mb.scatter_rows(packed, idx, nnz, B * L, back)
+    want = torch.from_numpy(O.pad(O.unpad(x, oidx), oidx, B, L).reshape(B * L, H)).to(BF)
+    assert torch.equal(back.cpu(), want)
+
+
+# ------------------------------------------------------------------------------------ A7 LayerNorm
+@pytest.mark.parametrize("H", [64, 768, 1024])
+@pytest.mark.parametrize("gelu", [False, True])
+def test_layernorm_fwd_bwd(H, gelu):
+    rng = np.random.default_rng(H)
+    n = 333
+    x = synth.bf16_round(rng.standard_normal((n, H)) * 3 + 1)
+    g = synth.bf16_round(1 + 0.1 * rng.standard_normal(H))
+    b = synth.bf16_round(0.1 * rng.standard_normal(H))
+    dy = synth.bf16_round(rng.standard_normal((n, H)))
+    pre = synth.bf16_round(rng.standard_normal((n, H)))
+    y = torch.empty(n, H, dtype=BF, device="cuda")
+    st = torch.empty(n, 2, dtype=torch.float32, device="cuda")
+    mb.layernorm_forward(_bf(x), _bf(g), _bf(b), 1e-12, y, st)
+    yo, cache = O.layer_norm(x, g, b, 1e-12)
+    check("ln.y", np64(y), yo, max_rel=1e-2)
+    xhat, r = cache
+    check("ln.rstd", np64(st)[:, 1], r[:, 0], max_rel=1e-5)
+    dx = torch.empty(n, H, dtype=BF, device="cuda")
+    dg = torch.zeros(H, device="cuda")
+    dbb = torch.zeros(H, device="cuda")
+    ds = torch.zeros(H, device="cuda")
+    mb.layernorm_backward(_bf(dy), _bf(x), st, _bf(g), dx, dg, dbb, ds, gelu_pre=_bf(pre) if gelu else None)
+    dxo, dgo, dbo = O.layer_norm_backward(dy, cache, g)
+    if gelu:
+        dxo = dxo * O.gelu_grad(pre)
+    check("ln.dx", np64(dx), dxo)
+    check("ln.dgamma", np64(dg), dgo)
+    check("ln.dbeta", np64(dbb), dbo, max_rel=1e-4)
+    check("ln.dsum", np64(ds), dxo.sum(0))
+
+
+# ------------------------------------------------------------------------------------ GEMM
+GEMM_SHAPES = [(300, 200, 136), (1000, 768, 768), (130, 64, 64), (257, 512, 1000)]
+
+
+@pytest.mark.parametrize("shape", GEMM_SHAPES)
+@pytest.mark.parametrize("a_t,b_t", [(0, 0), (0, 1), (1, 0), (1, 1)])
+def test_gemm_transposes_bf16(shape, a_t, b_t):
+    M, N, K = shape
+    rng = np.random.default_rng(M + N + K + 10 * a_t + b_t)
+    A = synth.bf16_round(rng.standard_normal((K, M) if a_t else (M, K)))
+    Bm = synth.bf16_round(rng.standard_normal((K, N) if b_t else (N, K)))
+    bias = synth.bf16_round(rng.standard_normal(N))
+    res = synth.bf16_round(rng.standard_normal((M, N)))
+    ref = (A.T if a_t else A).astype(np.float64) @ (Bm if b_t else Bm.T).astype(np.float64) + bias + res
+    C = torch.empty(M, N, dtype=BF, device="cuda")
+    mb.gemm(M, N, K, _bf(A), M if a_t else K, a_t, _bf(Bm), N if b_t else K, b_t, C, N, 0, bias=_bf(bias),
+            residual=_bf(res), ldr=N)
+    check(f"gemm{shape}{a_t}{b_t}", np64(C), ref, max_rel=1e-2, min_cos=0.9999)
+
+
+@pytest.mark.parametrize("shape", [(768, 768, 4096), (2304, 768, 333), (64, 64, 40)])
+def test_gemm_f32_acc_weight_grad(shape):
+    """dW += dY^T X (both operands MN-major, split-K, fp32 atomics into an existing buffer)."""
+    M, N, K = shape
+    rng = np.random.default_rng(K)
+    dY = synth.bf16_round(rng.standard_normal((K, M)))
+    X = synth.bf16_round(rng.standard_normal((K, N)))
+    C0 = rng.standard_normal((M, N)).astype(np.float32)
+    Cd = to_dev(C0, torch.float32)
+    mb.gemm(M, N, K, _bf(dY), M, 1, _bf(X), N, 1, Cd, N, 1)
+    ref = C0 + dY.T.astype(np.float64) @ X.astype(np.float64)
+    check("gemm.f32acc", np64(Cd), ref, max_rel=1e-4, min_cos=0.999999)
+
+
+def test_gemm_f32_and_gelu_aux():
+    M, N, K = 200, 256, 192
+    rng = np.random.default_rng(1)
+    A = synth.bf16_round(rng.standard_normal((M, K)))
+    W = synth.bf16_round(rng.standard_normal((N, K)) / np.sqrt(K))
+    b = synth.bf16_round(rng.standard_normal(N))
+    ref = A.astype(np.float64) @ W.T.astype(np.float64) + b
+    C = torch.empty(M, N, dtype=torch.float32, device="cuda")
+    mb.gemm(M, N, K, _bf(A), K, 0, _bf(W), K, 0, C, N, 2, bias=_bf(b))
+    check("gemm.f32", np64(C), ref, max_rel=1e-4, min_cos=0.999999)
+    G = torch.empty(M, N, dtype=BF, device="cuda")
+    pre = torch.empty(M, N, dtype=BF, device="cuda")
+    mb.gemm(M, N, K, _bf(A), K, 0, _bf(W), K, 0, G, N, 3, bias=_bf(b), aux=pre, ldaux=N)
+    check("gemm.pre", np64(pre), ref, max_rel=1e-2)
+    check("gemm.gelu", np64(G), O.gelu(ref), max_rel=1e-2)
+
+
+# ------------------------------------------------------------------------------------ GeGLU
+@pytest.mark.parametrize("H,I", [(64, 256), (768, 3072)])
+def test_geglu_fwd_bwd(H, I):
+    n = 300
+    rng = np.random.default_rng(H)
+    X = synth.bf16_round(rng.standard_normal((n, H)))
+    W = synth.bf16_round(rng.standard_normal((2 * I, H)) / np.sqrt(H))
+    b = synth.bf16_round(0.1 * rng.standard_normal(2 * I))
+    W2 = synth.bf16_round(rng.standard_normal((H, I)) / np.sqrt(I))
+    dF = synth.bf16_round(rng.standard_normal((n, H)))
+    U = torch.empty(n, 2 * I, dtype=BF, device="cuda")
+    Z = torch.empty(n, I, dtype=BF, device="cuda")
+    mb.geglu_forward(_bf(X), _bf(W), _bf(b), U, Z)
+    Uo = X.astype(np.float64) @ W.T.astype(np.float64) + b
+    a, g = Uo[:, :I], Uo[:, I:]
+    check("geglu.U", np64(U), Uo, max_rel=1e-2)
+    check("geglu.Z", np64(Z), O.gelu(a) * g, max_rel=1e-2)
+    dU = torch.empty(n, 2 * I, dtype=BF, device="cuda")
+    mb.geglu_backward(_bf(dF), _bf(W2), U, dU)
+    Ug = np64(U)  # the backward consumes the saved (bf16) U
+    a, g = Ug[:, :I], Ug[:, I:]
+    dZ = dF.astype(np.float64) @ W2.astype(np.float64)
+    check("geglu.da", np64(dU)[:, :I], dZ * g * O.gelu_grad(a))
+    check("geglu.dg", np64(dU)[:, I:], dZ * O.gelu(a))
+
+
+# ------------------------------------------------------------------------------------ attention
+ATTN_CASES = {
+    "tiny_d32": (2, 32, [16, 9, 3, 1]),
+    "base_d64_ragged": (12, 64, [128, 77, 1, 64, 100, 2]),
+    "full128": (12, 64, [128] * 6),
+    "multi_tile_512": (4, 64, [512, 300, 129, 128, 1]),
+    "d32_multi": (2, 32, [200, 17]),
+}
+
+
+def _attn_inputs(heads, d, lens, seed):
+    rng = np.random.default_rng(seed)
+    H = heads * d
+    lens = np.array(lens)
+    Lmax = int(lens.max())
+    mask = synth.mask_from_lengths(lens, Lmax)
+    qkv_p = synth.bf16_round(rng.standard_normal((len(lens), Lmax, 3 * H)) * 1.5)
+    do_p = synth.bf16_round(rng.standard_normal((len(lens), Lmax, H))) * mask[..., None]
+    return mask, qkv_p, do_p
+
+
+@pytest.mark.parametrize("case", sorted(ATTN_CASES))
+def test_attention_fwd_bwd(case):
+    heads, d, lens = ATTN_CASES[case]
+    H = heads * d
+    mask, qkv_p, do_p = _attn_inputs(heads, d, lens, len(case))
+    B, Lmax = mask.shape
+    cu, oidx, maxlen, _ = O.unpad_index(mask)
+    nnz = len(oidx)
+    slopes_np = mb.alibi_slopes(heads)
+    qkv = _bf(O.unpad(qkv_p, oidx))
+    dO = _bf(O.unpad(do_p, oidx))
+    cud = to_dev(cu, I32)
+    sl = to_dev(slopes_np, torch.float32)
+    Od = torch.empty(nnz, H, dtype=BF, device="cuda")
+    lse = torch.empty(heads, nnz, dtype=torch.float32, device="cuda")
+    mb.attention_forward(qkv, cud, B, nnz, maxlen, heads, d, sl, Od, lse)
+    sp = lambda t: t.reshape(B, Lmax, heads, d)  # noqa: E731
+    C, cache = O.attention_forward(sp(qkv_p[..., :H]), sp(qkv_p[..., H:2 * H]), sp(qkv_p[..., 2 * H:]), mask,
+                                   slopes_np.astype(np.float64))
+    check(f"{case}.O", np64(Od), O.unpad(C.reshape(B, Lmax, H), oidx), max_rel=2e-2)
+    q, k, v, P, _ = cache
+    s = np.einsum("blhd,bmhd->bhlm", q, k) / np.sqrt(d)
+    i = np.arange(Lmax)
+    s = s - slopes_np[None, :, None, None] * np.abs(i[:, None] - i[None, :])
+    s = np.where(mask[:, None, None, :].astype(bool), s, -np.inf)
+    lse_o = np.log(np.exp(s - s.max(-1, keepdims=True)).sum(-1)) + s.max(-1)
+    lse_o = np.stack([O.unpad(lse_o[:, h, :], oidx) for h in range(heads)])
+    assert np.max(np.abs(np64(lse) - lse_o)) < 2e-2
+    dqkv = torch.zeros(nnz, 3 * H, dtype=BF, device="cuda")
+    mb.attention_backward(qkv, Od, dO, lse, cud, B, nnz, maxlen, heads, d, sl, dqkv)
+    dq, dk, dv = O.attention_backward(sp(do_p), cache)
+    ref = np.concatenate([x.reshape(B, Lmax, H) for x in (dq, dk, dv)], -1)
+    ref = O.unpad(ref, oidx)
+    got = np64(dqkv)
+    for nm, sl_ in (("dq", slice(0, H)), ("dk", slice(H, 2 * H)), ("dv", slice(2 * H, 3 * H))):
+        check(f"{case}.{nm}", got[:, sl_], ref[:, sl_])
+
+
+def test_attention_alibi_closed_form():
+    """Pin P4b on the kernel: Q = K = 0 -> weights e^{-m|i-j|}/sum (in-kernel bias, masking and the
+    per-sequence position restart); l=2, m=ln 3 -> [3/4, 1/4]."""
+    heads, d = 2, 32
+    H = heads * d
+    lens = [2, 5, 7]
+    nnz = sum(lens)
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    qkv = np.zeros((nnz, 3 * H), np.float32)
+    pos = np.concatenate([np.arange(l) for l in lens])
+    qkv[:, 2 * H: 2 * H + 1] = pos[:, None]  # v[:, head0, 0] = position
+    qkv[:, 2 * H + d: 2 * H + d + 1] = 1.0   # v[:, head1, 0] = 1
+    m = np.array([np.log(3.0), 0.5], dtype=np.float32)
+    Od = torch.empty(nnz, H, dtype=BF, device="cuda")
+    lse = torch.empty(heads, nnz, dtype=torch.float32, device="cuda")
+    mb.attention_forward(_bf(qkv), to_dev(cu, I32), 3, nnz, 7, heads, d, to_dev(m, torch.float32), Od, lse)
+    out = np64(Od)
+    for b, l in enumerate(lens):
+        for i in range(l):
+            w = np.exp(-float(m[0]) * np.abs(i - np.arange(l)))
+            w /= w.sum()
+            assert abs(out[cu[b] + i, 0] - np.dot(w, np.arange(l))) < 1e-2 * max(1, l)
+            assert abs(out[cu[b] + i, d] - 1.0) < 1e-2
+    assert abs(out[0, 0] - 0.25) < 4e-3 and abs(out[1, 0] - 0.75) < 4e-3
