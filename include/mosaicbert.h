@@ -54,6 +54,16 @@ MB_API const char* mb_status_string(int status);
 /* Library version string and the SASS target it was built for ("sm_100a"). */
 MB_API const char* mb_version(void);
 
+/* Instrumentation (host only; not used by the compute path):
+ *  mb_launch_count: total kernels this process has launched through the library (monotonic).
+ *  mb_probe_set: record caller-created cudaEvent_t pairs around every launch of one kernel site so
+ *    that a benchmark can time that kernel inside a real step on the stream it runs on.
+ *    site: 0 = off, 1 = GeGLU up-projection GEMM (A8), 2 = attention fwd (A5), 3 = attention bwd
+ *    (A10), 4 = LayerNorm fwd (A7).  events: host array of `capacity` cudaEvent_t (pairs
+ *    start/end); *count (host int) is incremented per recorded pair.  Not thread-safe. */
+MB_API unsigned long long mb_launch_count(void);
+MB_API mb_status mb_probe_set(int32_t site, void* events, int32_t capacity, int32_t* count);
+
 /* Model dimensions.  d = hidden/heads (head_dim, 32 or 64).  ln_eps: LayerNorm epsilon (R11). */
 typedef struct {
   int32_t hidden, heads, intermediate, vocab;

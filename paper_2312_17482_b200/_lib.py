@@ -50,6 +50,8 @@ class HeadPtrs(C.Structure):
 _SIGS = {
     "mb_status_string": (C.c_char_p, [C.c_int]),
     "mb_version": (C.c_char_p, []),
+    "mb_launch_count": (C.c_ulonglong, []),
+    "mb_probe_set": (C.c_int, [I32, P, I32, P]),
     "mb_alibi_slopes": (C.c_int, [I32, P]),
     "mb_unpad_index": (C.c_int, [P, I32, I32, P, P, P, P]),
     "mb_mlm_select": (C.c_int, [P, P, I32, I32, P, P, P, P]),
@@ -115,6 +117,35 @@ def _p(t):
 
 def _stream():
     return torch.cuda.current_stream().cuda_stream
+
+
+def launch_count() -> int:
+    """Kernels launched by the library in this process so far (host counter)."""
+    return int(lib().mb_launch_count())
+
+
+class Probe:
+    """Times every launch of one kernel site inside real steps with CUDA events recorded on the
+    launching stream (mb_probe_set).  site: 1 GeGLU GEMM, 2 attention fwd, 3 attention bwd, 4 LN fwd."""
+
+    def __init__(self, site: int, capacity: int = 4096):
+        self.site = site
+        self.events = [torch.cuda.Event(enable_timing=True) for _ in range(capacity)]
+        self.handles = (C.c_void_p * capacity)(*[e.cuda_event for e in self.events])
+        self.count = C.c_int32(0)
+        self.capacity = capacity
+
+    def __enter__(self):
+        self.count.value = 0
+        _ck("mb_probe_set", lib().mb_probe_set(self.site, self.handles, self.capacity, C.byref(self.count)))
+        return self
+
+    def __exit__(self, *a):
+        lib().mb_probe_set(0, None, 0, None)
+
+    def times_ms(self):
+        n = self.count.value
+        return [self.events[2 * i].elapsed_time(self.events[2 * i + 1]) for i in range(n)]
 
 
 def dims(hidden, heads, intermediate, vocab, ln_eps=1e-12) -> Dims:

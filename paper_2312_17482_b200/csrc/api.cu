@@ -108,7 +108,9 @@ mb_status mb_encoder_forward(const mb_dims* d, const mb_layer_params* p, const m
     TRY(gemm(a, s));
   }
   // A5: varlen ALiBi attention
+  probe_begin(PROBE_ATTN_FWD, s);
   TRY(attention_fwd(sv.qkv, pk->cu_seqlens, pk->batch, T, pk->max_seqlen, nh, H / nh, slopes, sv.o, sv.lse, s));
+  probe_end(PROBE_ATTN_FWD, s);
   {  // A6: S1 = O Wo^T + bo + X
     GemmArgs a;
     a.M = T, a.N = H, a.K = H, a.A = sv.o, a.lda = H, a.B = B(p->w_o), a.ldb = H;
@@ -116,13 +118,17 @@ mb_status mb_encoder_forward(const mb_dims* d, const mb_layer_params* p, const m
     TRY(gemm(a, s));
   }
   // A7: Y1 = LN1(S1)
+  probe_begin(PROBE_LN_FWD, s);
   TRY(layernorm_fwd(sv.s1, B(p->ln1_g), B(p->ln1_b), T, H, d->ln_eps, sv.y1, sv.st1, s));
+  probe_end(PROBE_LN_FWD, s);
   {  // A8: U = Y1 W1v^T + b1v, Z = GeLU(U_a) * U_g
     GemmArgs a;
     a.M = T, a.N = 2 * I, a.K = H, a.A = sv.y1, a.lda = H, a.B = B(p->w_1v), a.ldb = H;
     a.ep.mode = E_GEGLU_FWD, a.ep.C = sv.z, a.ep.ldc = I, a.ep.bias = B(p->b_1v), a.ep.aux = sv.u,
     a.ep.ldaux = 2 * I, a.ep.I = I;
+    probe_begin(PROBE_GEGLU_FWD, s);
     TRY(gemm(a, s));
+    probe_end(PROBE_GEGLU_FWD, s);
   }
   {  // A9: S2 = Z W2^T + b2 + Y1
     GemmArgs a;
@@ -193,8 +199,10 @@ mb_status mb_encoder_backward(const mb_dims* d, const mb_layer_params* p, const 
     TRY(gemm(a, s));
   }
   // A10: attention backward -> dQKV
+  probe_begin(PROBE_ATTN_BWD, s);
   TRY(attention_bwd(sv.qkv, sv.o, w.dO, sv.lse, pk->cu_seqlens, pk->batch, T, pk->max_seqlen, nh, H / nh, slopes,
                     w.dqkv, w.attn, w.attn_bytes, s));
+  probe_end(PROBE_ATTN_BWD, s);
   TRY(colsum(w.dqkv, T, 3 * H, g->b_qkv, s));  // dbqkv
   {  // dX = dQKV Wqkv + dS1
     GemmArgs a;

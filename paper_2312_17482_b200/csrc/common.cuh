@@ -10,6 +10,7 @@ typedef __nv_bfloat162 bf162;
 
 #define MB_CHECK_LAUNCH()                                   \
   do {                                                      \
+    mb::count_launch();                                     \
     cudaError_t e__ = cudaGetLastError();                   \
     if (e__ != cudaSuccess) return MB_ERR_CUDA;             \
   } while (0)
@@ -81,5 +82,10 @@ __device__ __forceinline__ float gelu_grad_f(float x) {
 }
 
 int num_sms();  // cached per device (host)
+void count_launch();  // host-side counter of kernel launches (mb_launch_count)
+// optional timing probe around one kernel site (mb_probe_set): records caller-provided CUDA events
+enum ProbeSite { PROBE_NONE = 0, PROBE_GEGLU_FWD = 1, PROBE_ATTN_FWD = 2, PROBE_ATTN_BWD = 3, PROBE_LN_FWD = 4 };
+void probe_begin(int site, cudaStream_t s);
+void probe_end(int site, cudaStream_t s);
 
 }  // namespace mb

@@ -3,6 +3,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <math.h>
+#include <atomic>
 #include <mutex>
 #include "common.cuh"
 #include "tma.h"
@@ -22,6 +23,30 @@ int num_sms() {
     g_sms[dev] = n > 0 ? n : 148;
   });
   return g_sms[dev];
+}
+
+static std::atomic<unsigned long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+struct Probe {
+  int site = PROBE_NONE;
+  cudaEvent_t* events = nullptr;
+  int capacity = 0;
+  int* count = nullptr;
+};
+static Probe g_probe;
+void probe_begin(int site, cudaStream_t s) {
+  if (site != g_probe.site || !g_probe.events) return;
+  const int i = *g_probe.count;
+  if (2 * i + 1 < g_probe.capacity) cudaEventRecord(g_probe.events[2 * i], s);
+}
+void probe_end(int site, cudaStream_t s) {
+  if (site != g_probe.site || !g_probe.events) return;
+  const int i = *g_probe.count;
+  if (2 * i + 1 < g_probe.capacity) {
+    cudaEventRecord(g_probe.events[2 * i + 1], s);
+    *g_probe.count = i + 1;
+  }
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -76,6 +101,17 @@ const char* mb_status_string(int s) {
 }
 
 const char* mb_version(void) { return "mosaicbert-b200 0.1 (sm_100a)"; }
+
+unsigned long long mb_launch_count(void) { return mb::g_launches.load(); }
+
+mb_status mb_probe_set(int32_t site, void* events, int32_t capacity, int32_t* count) {
+  if (site != 0 && (!events || !count || capacity < 2)) return MB_ERR_INVALID_ARG;
+  mb::g_probe.site = site;
+  mb::g_probe.events = reinterpret_cast<cudaEvent_t*>(events);
+  mb::g_probe.capacity = capacity;
+  mb::g_probe.count = count;
+  return MB_OK;
+}
 
 // geometric sequence with ratio 2^(-8/n) starting at 2^(-8/n) (R3).  Computed in double
 // and rounded once to float, so it is the correctly rounded fp32 value of the closed form.
