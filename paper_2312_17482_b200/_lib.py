@@ -131,6 +131,9 @@ class Probe:
     def __init__(self, site: int, capacity: int = 4096):
         self.site = site
         self.events = [torch.cuda.Event(enable_timing=True) for _ in range(capacity)]
+        for e in self.events:  # torch creates the underlying cudaEvent_t lazily, on first record
+            e.record()
+        torch.cuda.current_stream().synchronize()
         self.handles = (C.c_void_p * capacity)(*[e.cuda_event for e in self.events])
         self.count = C.c_int32(0)
         self.capacity = capacity

@@ -38,14 +38,15 @@ static Probe g_probe;
 void probe_begin(int site, cudaStream_t s) {
   if (site != g_probe.site || !g_probe.events) return;
   const int i = *g_probe.count;
-  if (2 * i + 1 < g_probe.capacity) cudaEventRecord(g_probe.events[2 * i], s);
+  if (2 * i + 1 < g_probe.capacity && cudaEventRecord(g_probe.events[2 * i], s) != cudaSuccess)
+    cudaGetLastError();  // a bad probe must never poison the compute path's launch checks
 }
 void probe_end(int site, cudaStream_t s) {
   if (site != g_probe.site || !g_probe.events) return;
   const int i = *g_probe.count;
   if (2 * i + 1 < g_probe.capacity) {
-    cudaEventRecord(g_probe.events[2 * i + 1], s);
-    *g_probe.count = i + 1;
+    if (cudaEventRecord(g_probe.events[2 * i + 1], s) == cudaSuccess) *g_probe.count = i + 1;
+    else cudaGetLastError();
   }
 }
 
