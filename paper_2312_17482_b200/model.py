@@ -122,7 +122,8 @@ class MosaicBert:
             b.load(lp)
         self.head_bucket.load(params)
         self.emb_bucket.load(params)
-        torch.cuda.synchronize(self.device)
+        if self.device.type == "cuda":
+            torch.cuda.synchronize(self.device)
 
     def head_params(self):
         h, e = self.head_bucket.p, self.emb_bucket.p
@@ -227,12 +228,26 @@ class MosaicBert:
         self._handles = [h for h in handles if h is not None]
         return nnz, n_m
 
+    def _dp(self) -> bool:
+        return dist.is_available() and dist.is_initialized() and dist.get_world_size(self.pg) > 1
+
     def _allreduce(self, b: Bucket):
-        if self.pg is None and not (dist.is_available() and dist.is_initialized()):
-            return None
-        if dist.get_world_size(self.pg) == 1:
+        """Sum one fp32 gradient bucket over the data-parallel ranks (async; A12)."""
+        if not self._dp():
             return None
         return dist.all_reduce(b.g, op=dist.ReduceOp.SUM, group=self.pg, async_op=True)
+
+    def allreduce_grads(self):
+        """Issue the allreduce of every bucket (used when gradients were produced elsewhere)."""
+        self._handles = [h for h in (self._allreduce(b) for b in self.buckets) if h is not None]
+
+    def global_masked(self, n_local: int) -> int:
+        """N_masked of the whole optimizer step over all ranks (R18: the loss normaliser)."""
+        if not self._dp():
+            return int(n_local)
+        t = torch.tensor([int(n_local)], dtype=torch.int64, device=self.device if self.device.type == "cuda" else "cpu")
+        dist.all_reduce(t, group=self.pg)
+        return int(t.item())
 
     def wait_grads(self):
         for h in getattr(self, "_handles", []):
@@ -261,12 +276,7 @@ class MosaicBert:
         for i, (ids, mask, labels) in enumerate(micro_batches):
             self.micro_step(ids, mask, labels, inv_norm=1.0, allreduce=(i == n - 1))
         if global_masked is None:
-            global_masked = self.masked_count
-            if self.pg is not None or (dist.is_available() and dist.is_initialized()):
-                if dist.get_world_size(self.pg) > 1:
-                    t = torch.tensor([global_masked], dtype=torch.int64, device=self.device)
-                    dist.all_reduce(t, group=self.pg)
-                    global_masked = int(t.item())
+            global_masked = self.global_masked(self.masked_count)
         self.wait_grads()
         scale = 1.0 / max(global_masked, 1)
         if optimizer:
