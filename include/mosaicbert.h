@@ -143,14 +143,16 @@ MB_API mb_status mb_gemm(int32_t M, int32_t N, int32_t K, const mb_bf16* A, int6
 
 /* A8 — fused GLU up-projection with the GeGLU epilogue (Eq. 2; fused W1||V):
  *   U = X W_1v^T + b_1v  ([n, 2I]; first I outputs = W1 half "a", last I = V half "g", reading R8)
- *   Z = GeLU(a) * g      ([n, I])
- * Both U (saved for backward) and Z are written.  I must be a multiple of 128. */
+ *   Z = GeLU(a) * g      ([n, I], written)
+ *   Gd = [g * GeLU'(a) | GeLU(a)]   ([n, 2I], written; the two factors the backward needs, so U
+ *        itself never reaches memory and the backward epilogue evaluates no transcendental)
+ * I must be a multiple of 128. */
 MB_API mb_status mb_geglu_forward(const mb_bf16* X, int32_t n, int32_t H, int32_t I, const mb_bf16* w_1v,
-                           const mb_bf16* b_1v, mb_bf16* U, mb_bf16* Z, mb_stream_t s);
+                                  const mb_bf16* b_1v, mb_bf16* Gd, mb_bf16* Z, mb_stream_t s);
 /* GeGLU backward fused into the dZ = dF W_2 GEMM: dZ never reaches memory;
- *   dU[:, :I] = dZ * g * GeLU'(a),  dU[:, I:] = dZ * GeLU(a)   (dU bf16 [n, 2I]). */
+ *   dU = dZ * Gd  i.e.  dU[:, :I] = dZ * g * GeLU'(a),  dU[:, I:] = dZ * GeLU(a)   (bf16 [n, 2I]). */
 MB_API mb_status mb_geglu_backward(const mb_bf16* dF, int32_t n, int32_t H, int32_t I, const mb_bf16* w_2,
-                            const mb_bf16* U, mb_bf16* dU, mb_stream_t s);
+                                   const mb_bf16* Gd, mb_bf16* dU, mb_stream_t s);
 
 /* A5 — varlen ALiBi attention forward (Eq. 1; FlashAttention P:120), on the packed
  * stream, with the bias -m_h |i-j| generated in-kernel (never materialised):
@@ -164,12 +166,14 @@ MB_API mb_status mb_attention_forward(const mb_bf16* qkv, const int32_t* cu_seql
                                mb_bf16* O, float* lse, mb_stream_t s);
 /* A10 — varlen ALiBi attention backward (recomputes P from LSE; no dropout P:152):
  *   dV = P^T dO, dP = dO V^T, dS = P (dP - D), D_i = dO_i . O_i, dQ = dS K/sqrt d, dK = dS^T Q/sqrt d
- * written into dqkv bf16 [nnz, 3H] in the qkv column layout.  ws: mb_attention_workspace_bytes. */
+ * written into dqkv bf16 [nnz, 3H] in the qkv column layout.  If db_qkv != NULL, the column sums of
+ * dqkv (the QKV-projection bias gradient) are accumulated into it (fp32 [3H], +=).
+ * ws: mb_attention_workspace_bytes. */
 MB_API size_t mb_attention_workspace_bytes(int32_t nnz, int32_t heads, int32_t head_dim, int32_t max_seqlen);
 MB_API mb_status mb_attention_backward(const mb_bf16* qkv, const mb_bf16* O, const mb_bf16* dO, const float* lse,
                                 const int32_t* cu_seqlens, int32_t batch, int32_t nnz, int32_t max_seqlen,
-                                int32_t heads, int32_t head_dim, const float* slopes, mb_bf16* dqkv, void* ws,
-                                size_t ws_bytes, mb_stream_t s);
+                                int32_t heads, int32_t head_dim, const float* slopes, mb_bf16* dqkv,
+                                float* db_qkv, void* ws, size_t ws_bytes, mb_stream_t s);
 
 /* Column sums: out[c] += sum_r x[r, c] (fp32 accumulate) — bias gradients.  x bf16 [n, C]. */
 MB_API mb_status mb_colsum(const mb_bf16* x, int32_t n, int32_t C, float* out, mb_stream_t s);
@@ -180,7 +184,7 @@ MB_API mb_status mb_colsum(const mb_bf16* x, int32_t n, int32_t C, float* out, m
  *   U = Y1 W1v^T + b1v; Z = GeLU(U_a) * U_g; Y = LN2(Z W2^T + b2 + Y1)
  * x, y: bf16 [nnz, H] packed; slopes device fp32[heads].
  * saved: device buffer of mb_layer_saved_bytes(d, nnz) bytes, written by forward and read by the
- *        matching backward (QKV, attention output, LSE, LN inputs/stats, Y1, U, Z).
+ *        matching backward (QKV, attention output, LSE, LN inputs/stats, Y1, GeGLU factors Gd, Z).
  * ws:    device workspace of mb_layer_workspace_bytes(d, nnz, max_seqlen) bytes (backward only). */
 typedef struct {
   const int32_t* cu_seqlens; /* device int32[batch+1] */

@@ -64,7 +64,7 @@ _SIGS = {
     "mb_geglu_backward": (C.c_int, [P, I32, I32, I32, P, P, P, P]),
     "mb_attention_forward": (C.c_int, [P, P, I32, I32, I32, I32, I32, P, P, P, P]),
     "mb_attention_workspace_bytes": (SZ, [I32, I32, I32, I32]),
-    "mb_attention_backward": (C.c_int, [P, P, P, P, P, I32, I32, I32, I32, I32, P, P, P, SZ, P]),
+    "mb_attention_backward": (C.c_int, [P, P, P, P, P, I32, I32, I32, I32, I32, P, P, P, P, SZ, P]),
     "mb_colsum": (C.c_int, [P, I32, I32, P, P]),
     "mb_layer_saved_bytes": (SZ, [C.POINTER(Dims), I32]),
     "mb_layer_workspace_bytes": (SZ, [C.POINTER(Dims), I32, I32]),
@@ -213,17 +213,17 @@ def gemm(M, N, K, A, lda, a_t, B, ldb, b_t, Cout, ldc, epilogue=EPI_BF16, bias=N
     return Cout
 
 
-def geglu_forward(X, w_1v, b_1v, U, Z):
+def geglu_forward(X, w_1v, b_1v, Gd, Z):
     n, H = X.shape
     I = Z.shape[-1]
-    _ck("mb_geglu_forward", lib().mb_geglu_forward(_p(X), n, H, I, _p(w_1v), _p(b_1v), _p(U), _p(Z), _stream()))
-    return U, Z
+    _ck("mb_geglu_forward", lib().mb_geglu_forward(_p(X), n, H, I, _p(w_1v), _p(b_1v), _p(Gd), _p(Z), _stream()))
+    return Gd, Z
 
 
-def geglu_backward(dF, w_2, U, dU):
+def geglu_backward(dF, w_2, Gd, dU):
     n, H = dF.shape
     I = w_2.shape[1]
-    _ck("mb_geglu_backward", lib().mb_geglu_backward(_p(dF), n, H, I, _p(w_2), _p(U), _p(dU), _stream()))
+    _ck("mb_geglu_backward", lib().mb_geglu_backward(_p(dF), n, H, I, _p(w_2), _p(Gd), _p(dU), _stream()))
     return dU
 
 
@@ -237,13 +237,14 @@ def attention_workspace_bytes(nnz, heads, head_dim, max_seqlen):
     return int(lib().mb_attention_workspace_bytes(nnz, heads, head_dim, max_seqlen))
 
 
-def attention_backward(qkv, O, dO, lse, cu_seqlens, batch, nnz, max_seqlen, heads, head_dim, slopes, dqkv, ws=None):
+def attention_backward(qkv, O, dO, lse, cu_seqlens, batch, nnz, max_seqlen, heads, head_dim, slopes, dqkv, ws=None,
+                       db_qkv=None):
     nb = attention_workspace_bytes(nnz, heads, head_dim, max_seqlen)
     if ws is None and nb:
         ws = torch.empty(nb, dtype=torch.uint8, device=qkv.device)
     _ck("mb_attention_backward", lib().mb_attention_backward(_p(qkv), _p(O), _p(dO), _p(lse), _p(cu_seqlens), batch,
                                                              nnz, max_seqlen, heads, head_dim, _p(slopes), _p(dqkv),
-                                                             _p(ws), nb, _stream()))
+                                                             _p(db_qkv), _p(ws), nb, _stream()))
     return dqkv
 
 

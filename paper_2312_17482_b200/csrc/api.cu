@@ -121,7 +121,7 @@ mb_status mb_encoder_forward(const mb_dims* d, const mb_layer_params* p, const m
   probe_begin(PROBE_LN_FWD, s);
   TRY(layernorm_fwd(sv.s1, B(p->ln1_g), B(p->ln1_b), T, H, d->ln_eps, sv.y1, sv.st1, s));
   probe_end(PROBE_LN_FWD, s);
-  {  // A8: U = Y1 W1v^T + b1v, Z = GeLU(U_a) * U_g
+  {  // A8: U = Y1 W1v^T + b1v, Z = GeLU(U_a) * U_g; saves Gd = [U_g GeLU'(U_a) | GeLU(U_a)] in sv.u
     GemmArgs a;
     a.M = T, a.N = 2 * I, a.K = H, a.A = sv.y1, a.lda = H, a.B = B(p->w_1v), a.ldb = H;
     a.ep.mode = E_GEGLU_FWD, a.ep.C = sv.z, a.ep.ldc = I, a.ep.bias = B(p->b_1v), a.ep.aux = sv.u,
@@ -159,7 +159,7 @@ mb_status mb_encoder_backward(const mb_dims* d, const mb_layer_params* p, const 
   // LN2 backward: dS2; dgamma2, dbeta2; db2 = sum dS2
   TRY(layernorm_bwd(reinterpret_cast<bf16*>(dy), sv.s2, sv.st2, B(p->ln2_g), T, H, nullptr, w.ds2, g->ln2_g,
                     g->ln2_b, g->b_2, s));
-  {  // dZ = dS2 W2 fused with the GeGLU backward -> dU = [dZ g GeLU'(a) | dZ GeLU(a)]
+  {  // dZ = dS2 W2 fused with the GeGLU backward -> dU = dZ * Gd = [dZ g GeLU'(a) | dZ GeLU(a)]
     GemmArgs a;
     a.M = T, a.N = I, a.K = H, a.A = w.ds2, a.lda = H, a.B = B(p->w_2), a.ldb = I, a.b_t = true;
     a.ep.mode = E_GEGLU_BWD, a.ep.C = w.du, a.ep.ldc = 2 * I, a.ep.U = sv.u, a.ep.ldu = 2 * I, a.ep.I = I;
@@ -201,9 +201,8 @@ mb_status mb_encoder_backward(const mb_dims* d, const mb_layer_params* p, const 
   // A10: attention backward -> dQKV
   probe_begin(PROBE_ATTN_BWD, s);
   TRY(attention_bwd(sv.qkv, sv.o, w.dO, sv.lse, pk->cu_seqlens, pk->batch, T, pk->max_seqlen, nh, H / nh, slopes,
-                    w.dqkv, w.attn, w.attn_bytes, s));
+                    w.dqkv, g->b_qkv, w.attn, w.attn_bytes, s));  // also dbqkv = column sums of dQKV
   probe_end(PROBE_ATTN_BWD, s);
-  TRY(colsum(w.dqkv, T, 3 * H, g->b_qkv, s));  // dbqkv
   {  // dX = dQKV Wqkv + dS1
     GemmArgs a;
     a.M = T, a.N = H, a.K = 3 * H, a.A = w.dqkv, a.lda = 3 * H, a.B = B(p->w_qkv), a.ldb = H, a.b_t = true;

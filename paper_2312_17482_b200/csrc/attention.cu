@@ -408,6 +408,369 @@ __global__ void dq_convert_kernel(const float* __restrict__ dq_acc, const int* _
   }
 }
 
+
+// ------------------------------------------------------------------------------------------
+// Short-sequence path (l <= 128: every workload of BASELINE configs 1, 2, 3, 5): one (sequence,
+// head) unit = one Q tile and one K/V tile, single-pass softmax (no rescaling).  Persistent CTAs of
+// 8 warps: warp w reads TMEM lane quarter (w & 3) and column half (w >> 2), so two threads share a
+// query row and exchange its max / sum through shared memory.  The next unit's TMA loads are issued
+// as soon as the MMAs that read the current tiles have completed, overlapping the output epilogue.
+// ------------------------------------------------------------------------------------------
+constexpr int SH_THREADS = 256;
+constexpr int SH_FWD_SMEM = 3 * TILE_BYTES + P_BYTES + 1024 + 256 + 4 * 128 * 4;
+
+__device__ __forceinline__ int unit_len(const int* cu, int heads, int u) {
+  const int b = u / heads;
+  return cu[b + 1] - cu[b];
+}
+__device__ __forceinline__ int next_unit(const int* cu, int heads, int total, int u) {
+  for (u += gridDim.x; u < total; u += gridDim.x)
+    if (unit_len(cu, heads, u) > 0) return u;
+  return total;
+}
+
+__global__ void __launch_bounds__(SH_THREADS, 1) attn_fwd_short_kernel(const __grid_constant__ CUtensorMap tm_qkv,
+                                                                      const int* __restrict__ cu, int batch,
+                                                                      int heads, int d,
+                                                                      const float* __restrict__ slopes,
+                                                                      bf16* __restrict__ O, float* __restrict__ lse,
+                                                                      int nnz) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + TILE_BYTES;
+  uint8_t* sV = sK + TILE_BYTES;
+  uint8_t* sP = sV + TILE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + P_BYTES);  // load, s, o
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
+  float* rmax = reinterpret_cast<float*>(sP + P_BYTES + 256);  // [2][128]
+  float* rsum = rmax + 256;                                    // [2][128]
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ch = warp >> 2;
+  const int r = (warp & 3) * 32 + lane;
+  const int H = heads * d;
+  const int total = batch * heads;
+  if (tid == 0) {
+    sm100::tma_prefetch(&tm_qkv);
+    for (int i = 0; i < 4; ++i) sm100::mbar_init(&bars[i], 1);
+    sm100::fence_barrier_init();
+  }
+  if (warp == 0) sm100::tmem_alloc(tslot, 256);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tbase = *tslot;
+  const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+  const uint32_t tS = tbase + lane_off + 64 * ch, tO = tbase + 128 + lane_off + 32 * ch;
+  const uint32_t sQa = sm100::smem_u32(sQ), sKa = sm100::smem_u32(sK), sVa = sm100::smem_u32(sV),
+                 sPa = sm100::smem_u32(sP);
+  const float sc2 = rsqrtf((float)d) * LOG2E;
+
+  auto issue_loads = [&](int u) {
+    const int b = u / heads, h = u - b * heads;
+    const int st = cu[b];
+    sm100::mbar_arrive_expect_tx(&bars[0], 3 * TILE_BYTES);
+    sm100::tma_load_2d(sQ, &tm_qkv, &bars[0], h * d, st);
+    sm100::tma_load_2d(sK, &tm_qkv, &bars[0], H + h * d, st);
+    sm100::tma_load_2d(sV, &tm_qkv, &bars[0], 2 * H + h * d, st);
+  };
+
+  int u = blockIdx.x;
+  if (u < total && unit_len(cu, heads, u) == 0) u = next_unit(cu, heads, total, u);
+  if (tid == 0 && u < total) issue_loads(u);
+  for (int it = 0; u < total; ++it) {
+    const uint32_t ph = it & 1;
+    const int b = u / heads, h = u - b * heads;
+    const int start = cu[b];
+    const int len = cu[b + 1] - start;
+    const float sl2 = slopes[h] * LOG2E;
+    if (tid == 0) {
+      sm100::mbar_wait(&bars[0], ph);
+      sm100::tc_fence_after();
+      constexpr uint32_t id_s = sm100::idesc_bf16(128, 128, 0, 0);
+      for (int k = 0; k < d / 16; ++k)
+        sm100::mma_bf16_ss(tbase, sm100::desc_kmajor_sw128(sQa + k * 32), sm100::desc_kmajor_sw128(sKa + k * 32),
+                           id_s, k > 0);
+      sm100::mma_commit(&bars[1]);
+    }
+    __syncwarp();
+    sm100::mbar_wait(&bars[1], ph);
+    sm100::tc_fence_after();
+    float x[64];
+    sm100::tmem_ld32(tS, x);
+    sm100::tmem_ld32(tS + 32, x + 32);
+    sm100::tmem_ld_wait();
+    float mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 64; ++j) {
+      const int key = 64 * ch + j;
+      const float t = x[j] * sc2 - sl2 * fabsf((float)(r - key));
+      x[j] = key < len ? t : -INFINITY;
+      mx = fmaxf(mx, x[j]);
+    }
+    rmax[ch * 128 + r] = mx;
+    __syncthreads();
+    mx = fmaxf(rmax[r], rmax[128 + r]);
+    float sum = 0.f;
+#pragma unroll
+    for (int j8 = 0; j8 < 8; ++j8) {
+      uint32_t pk[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const bf162 hp = __floats2bfloat162_rn(exp2f(x[j8 * 8 + 2 * e] - mx), exp2f(x[j8 * 8 + 2 * e + 1] - mx));
+        const float2 pr = __bfloat1622float2(hp);
+        sum += pr.x + pr.y;
+        pk[e] = *reinterpret_cast<const uint32_t*>(&hp);
+      }
+      st_shared_v4(sPa + p_off(r, 64 * ch + 8 * j8), pk[0], pk[1], pk[2], pk[3]);
+    }
+    rsum[ch * 128 + r] = sum;
+    sm100::fence_proxy_async_smem();
+    sm100::tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      sm100::tc_fence_after();
+      constexpr uint32_t id_o = sm100::idesc_bf16(128, 64, 0, 1);
+#pragma unroll
+      for (int k = 0; k < TILE / 16; ++k)
+        sm100::mma_bf16_ss(tbase + 128, sm100::desc_kmajor_sw128(sPa + (k >> 2) * (TILE * 128) + (k & 3) * 32),
+                           sm100::desc_mnmajor_sw128(sVa + k * 2048, 8192), id_o, k > 0);
+      sm100::mma_commit(&bars[2]);
+    }
+    __syncwarp();
+    sm100::mbar_wait(&bars[2], ph);
+    sm100::tc_fence_after();
+    const int un = next_unit(cu, heads, total, u);
+    if (tid == 0 && un < total) issue_loads(un);  // tiles are free: both MMAs have completed
+    float v[32];
+    sm100::tmem_ld32(tO, v);
+    sm100::tmem_ld_wait();
+    const float l = rsum[r] + rsum[128 + r];
+    if (r < len) {
+      const float inv = 1.f / l;
+      bf16* dst = O + (size_t)(start + r) * H + h * d + 32 * ch;
+#pragma unroll
+      for (int c = 0; c < 32; c += 8) {
+        if (32 * ch + c < d) {
+          float t[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) t[e] = v[c + e] * inv;
+          *reinterpret_cast<uint4*>(dst + c) = f32_to_bf16x8(t);
+        }
+      }
+      if (ch == 0) lse[(size_t)h * nnz + start + r] = (mx + log2f(l)) * LN2;
+    }
+    sm100::tc_fence_before();
+    __syncthreads();
+    u = un;
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) sm100::tmem_dealloc(tbase, 256);
+}
+
+constexpr int SH_BWD_SMEM = 4 * TILE_BYTES + 2 * P_BYTES + 1024 + 256 + 2 * 128 * 4 + 3 * 64 * 4;
+
+// per-warp transpose-reduce: lane l ends with sum over the warp's 32 rows of column l of v[32]
+__device__ __forceinline__ float warp_colsum32(float* v, int lane) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+#pragma unroll
+    for (int j = 0; j < s; ++j) {
+      const bool up = lane & s;
+      const float send = up ? v[j] : v[j + s];
+      const float keep = up ? v[j + s] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+  }
+  return v[0];
+}
+
+__global__ void __launch_bounds__(SH_THREADS, 1) attn_bwd_short_kernel(
+    const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do, const int* __restrict__ cu,
+    int batch, int heads, int d, const float* __restrict__ slopes, const bf16* __restrict__ O,
+    const bf16* __restrict__ dO, const float* __restrict__ lse, bf16* __restrict__ dqkv, float* __restrict__ dbias,
+    int nnz) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + TILE_BYTES;
+  uint8_t* sV = sK + TILE_BYTES;
+  uint8_t* sdO = sV + TILE_BYTES;
+  uint8_t* sP = sdO + TILE_BYTES;
+  uint8_t* sdS = sP + P_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sdS + P_BYTES);  // load, sp, acc
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
+  float* dred = reinterpret_cast<float*>(sdS + P_BYTES + 256);  // [2][128] partial D
+  float* bsm = dred + 256;                                      // [3][64] bias-grad partials
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ch = warp >> 2;
+  const int r = (warp & 3) * 32 + lane;
+  const int H = heads * d;
+  const int total = batch * heads;
+  if (tid == 0) {
+    sm100::tma_prefetch(&tm_qkv);
+    sm100::tma_prefetch(&tm_do);
+    for (int i = 0; i < 4; ++i) sm100::mbar_init(&bars[i], 1);
+    sm100::fence_barrier_init();
+  }
+  if (warp == 0) sm100::tmem_alloc(tslot, 512);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tbase = *tslot;
+  const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+  const uint32_t tS = tbase, tdP = tbase + 128, tdV = tbase + 256, tdK = tbase + 320, tdQ = tbase + 384;
+  const uint32_t sQa = sm100::smem_u32(sQ), sKa = sm100::smem_u32(sK), sVa = sm100::smem_u32(sV),
+                 sdOa = sm100::smem_u32(sdO), sPa = sm100::smem_u32(sP), sdSa = sm100::smem_u32(sdS);
+  const float rsd = rsqrtf((float)d);
+  const float sc2 = rsd * LOG2E;
+
+  auto issue_loads = [&](int u) {
+    const int b = u / heads, h = u - b * heads;
+    const int st = cu[b];
+    sm100::mbar_arrive_expect_tx(&bars[0], 4 * TILE_BYTES);
+    sm100::tma_load_2d(sQ, &tm_qkv, &bars[0], h * d, st);
+    sm100::tma_load_2d(sK, &tm_qkv, &bars[0], H + h * d, st);
+    sm100::tma_load_2d(sV, &tm_qkv, &bars[0], 2 * H + h * d, st);
+    sm100::tma_load_2d(sdO, &tm_do, &bars[0], h * d, st);
+  };
+
+  int u = blockIdx.x;
+  if (u < total && unit_len(cu, heads, u) == 0) u = next_unit(cu, heads, total, u);
+  if (tid == 0 && u < total) issue_loads(u);
+  for (int it = 0; u < total; ++it) {
+    const uint32_t ph = it & 1;
+    const int b = u / heads, h = u - b * heads;
+    const int start = cu[b];
+    const int len = cu[b + 1] - start;
+    const float sl2 = slopes[h] * LOG2E;
+    // D_i = dO_i . O_i (this thread's half of the head dimension), LSE
+    float Dp = 0.f, lse2 = 0.f;
+    if (r < len) {
+      lse2 = lse[(size_t)h * nnz + start + r] * LOG2E;
+      if (32 * ch < d) {
+        const bf16* o_row = O + (size_t)(start + r) * H + h * d + 32 * ch;
+        const bf16* do_row = dO + (size_t)(start + r) * H + h * d + 32 * ch;
+#pragma unroll
+        for (int c = 0; c < 32; c += 8) {
+          float a[8], g[8];
+          bf16x8_to_f32(*reinterpret_cast<const uint4*>(o_row + c), a);
+          bf16x8_to_f32(*reinterpret_cast<const uint4*>(do_row + c), g);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) Dp += a[e] * g[e];
+        }
+      }
+    }
+    dred[ch * 128 + r] = Dp;
+    if (tid < 192) bsm[tid] = 0.f;
+    if (tid == 0) {
+      sm100::mbar_wait(&bars[0], ph);
+      sm100::tc_fence_after();
+      constexpr uint32_t id_s = sm100::idesc_bf16(128, 128, 0, 0);
+      for (int k = 0; k < d / 16; ++k) {
+        sm100::mma_bf16_ss(tS, sm100::desc_kmajor_sw128(sQa + k * 32), sm100::desc_kmajor_sw128(sKa + k * 32), id_s,
+                           k > 0);
+        sm100::mma_bf16_ss(tdP, sm100::desc_kmajor_sw128(sdOa + k * 32), sm100::desc_kmajor_sw128(sVa + k * 32),
+                           id_s, k > 0);
+      }
+      sm100::mma_commit(&bars[1]);
+    }
+    __syncthreads();
+    const float Dr = dred[r] + dred[128 + r];
+    sm100::mbar_wait(&bars[1], ph);
+    sm100::tc_fence_after();
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      const int c0 = 64 * ch + 32 * c;
+      float v[32], w[32];
+      sm100::tmem_ld32(tS + lane_off + c0, v);
+      sm100::tmem_ld32(tdP + lane_off + c0, w);
+      sm100::tmem_ld_wait();
+      uint32_t pp[16], pd[16];
+#pragma unroll
+      for (int jj = 0; jj < 32; jj += 2) {
+        float p2[2], ds2[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int key = c0 + jj + e;
+          const bool ok = (r < len) && (key < len);
+          const float p = ok ? exp2f(v[jj + e] * sc2 - sl2 * fabsf((float)(r - key)) - lse2) : 0.f;
+          p2[e] = p;
+          ds2[e] = p * (w[jj + e] - Dr);
+        }
+        pp[jj >> 1] = pack_bf16x2(p2[0], p2[1]);
+        pd[jj >> 1] = pack_bf16x2(ds2[0], ds2[1]);
+      }
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const uint32_t off = p_off(r, c0 + q4 * 8);
+        st_shared_v4(sPa + off, pp[4 * q4], pp[4 * q4 + 1], pp[4 * q4 + 2], pp[4 * q4 + 3]);
+        st_shared_v4(sdSa + off, pd[4 * q4], pd[4 * q4 + 1], pd[4 * q4 + 2], pd[4 * q4 + 3]);
+      }
+    }
+    sm100::fence_proxy_async_smem();
+    sm100::tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      sm100::tc_fence_after();
+      constexpr uint32_t id_t = sm100::idesc_bf16(128, 64, 1, 1);  // P^T dO, dS^T Q
+      constexpr uint32_t id_q = sm100::idesc_bf16(128, 64, 0, 1);  // dS K
+#pragma unroll
+      for (int k = 0; k < TILE / 16; ++k) {
+        sm100::mma_bf16_ss(tdV, sm100::desc_mnmajor_sw128(sPa + k * 2048, TILE * 128),
+                           sm100::desc_mnmajor_sw128(sdOa + k * 2048, 8192), id_t, k > 0);
+        sm100::mma_bf16_ss(tdK, sm100::desc_mnmajor_sw128(sdSa + k * 2048, TILE * 128),
+                           sm100::desc_mnmajor_sw128(sQa + k * 2048, 8192), id_t, k > 0);
+        sm100::mma_bf16_ss(tdQ, sm100::desc_kmajor_sw128(sdSa + (k >> 2) * (TILE * 128) + (k & 3) * 32),
+                           sm100::desc_mnmajor_sw128(sKa + k * 2048, 8192), id_q, k > 0);
+      }
+      sm100::mma_commit(&bars[2]);
+    }
+    __syncwarp();
+    sm100::mbar_wait(&bars[2], ph);
+    sm100::tc_fence_after();
+    const int un = next_unit(cu, heads, total, u);
+    if (tid == 0 && un < total) issue_loads(un);  // all tiles are free: every MMA reading them completed
+    // dQ (row = query r), dK (row = key r), dV (row = key r): this thread's 32 of the 64 columns
+    const bool ok = r < len;
+    const bool col_ok = 32 * ch < d;
+#pragma unroll 1
+    for (int which = 0; which < 3; ++which) {
+      float v[32];
+      const uint32_t src = which == 0 ? tdQ : (which == 1 ? tdK : tdV);
+      sm100::tmem_ld32(src + lane_off + 32 * ch, v);
+      sm100::tmem_ld_wait();
+      const float sc = which == 2 ? 1.f : rsd;
+#pragma unroll
+      for (int e = 0; e < 32; ++e) v[e] = ok ? v[e] * sc : 0.f;
+      if (ok && col_ok) {
+        bf16* dst = dqkv + (size_t)(start + r) * 3 * H + which * H + h * d + 32 * ch;
+#pragma unroll
+        for (int c = 0; c < 32; c += 8) *reinterpret_cast<uint4*>(dst + c) = f32_to_bf16x8(v + c);
+      }
+      if (dbias) {
+        // bias gradient of the QKV projection = column sums of dQKV, reduced per warp by a
+        // transpose-reduce, then across the 4 row-quarter warps in shared memory
+        const float cs = warp_colsum32(v, lane);
+        atomicAdd(&bsm[which * 64 + 32 * ch + lane], cs);
+      }
+    }
+    sm100::tc_fence_before();
+    __syncthreads();
+    if (dbias && tid < 3 * 64) {
+      const int which = tid >> 6, c = tid & 63;
+      if (c < d) atomicAdd(dbias + which * H + h * d + c, bsm[tid]);
+    }
+    u = un;
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) sm100::tmem_dealloc(tbase, 512);
+}
+
 }  // namespace
 
 mb_status attention_fwd(const bf16* qkv, const int* cu, int batch, int nnz, int max_seqlen, int heads, int d,
@@ -418,6 +781,20 @@ mb_status attention_fwd(const bf16* qkv, const int* cu, int batch, int nnz, int 
   const int H = heads * d;
   CUtensorMap tm;
   MB_REQUIRE(make_tmap_bf16_2d(&tm, qkv, 3 * H, nnz, 3 * H, DT, TILE), MB_ERR_CUDA);
+  if (max_seqlen <= TILE) {
+    static bool attr_s = false;
+    if (!attr_s) {
+      if (cudaFuncSetAttribute(attn_fwd_short_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SH_FWD_SMEM) !=
+          cudaSuccess)
+        return MB_ERR_CUDA;
+      attr_s = true;
+    }
+    const int units = batch * heads;
+    const int grid = std::max(1, std::min(units, num_sms()));
+    attn_fwd_short_kernel<<<grid, SH_THREADS, SH_FWD_SMEM, s>>>(tm, cu, batch, heads, d, slopes, O, lse, nnz);
+    MB_CHECK_LAUNCH();
+    return MB_OK;
+  }
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FWD_SMEM) != cudaSuccess)
@@ -435,8 +812,8 @@ size_t attention_ws_bytes(int nnz, int heads, int d, int max_seqlen) {
 }
 
 mb_status attention_bwd(const bf16* qkv, const bf16* O, const bf16* dO, const float* lse, const int* cu, int batch,
-                        int nnz, int max_seqlen, int heads, int d, const float* slopes, bf16* dqkv, void* ws,
-                        size_t ws_bytes, cudaStream_t s) {
+                        int nnz, int max_seqlen, int heads, int d, const float* slopes, bf16* dqkv, float* dbias,
+                        void* ws, size_t ws_bytes, cudaStream_t s) {
   if (nnz == 0 || batch == 0) return MB_OK;
   MB_REQUIRE(d == 32 || d == 64, MB_ERR_CONFIG);
   MB_REQUIRE(max_seqlen >= 1 && max_seqlen <= 512, MB_ERR_SHAPE);
@@ -446,6 +823,21 @@ mb_status attention_bwd(const bf16* qkv, const bf16* O, const bf16* dO, const fl
   CUtensorMap tq, tdo;
   MB_REQUIRE(make_tmap_bf16_2d(&tq, qkv, 3 * H, nnz, 3 * H, DT, TILE), MB_ERR_CUDA);
   MB_REQUIRE(make_tmap_bf16_2d(&tdo, dO, H, nnz, H, DT, TILE), MB_ERR_CUDA);
+  if (max_seqlen <= TILE) {
+    static bool attr_s = false;
+    if (!attr_s) {
+      if (cudaFuncSetAttribute(attn_bwd_short_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SH_BWD_SMEM) !=
+          cudaSuccess)
+        return MB_ERR_CUDA;
+      attr_s = true;
+    }
+    const int units = batch * heads;
+    const int grid = std::max(1, std::min(units, num_sms()));
+    attn_bwd_short_kernel<<<grid, SH_THREADS, SH_BWD_SMEM, s>>>(tq, tdo, cu, batch, heads, d, slopes, O, dO, lse,
+                                                                 dqkv, dbias, nnz);
+    MB_CHECK_LAUNCH();
+    return MB_OK;
+  }
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_SMEM) != cudaSuccess)
@@ -463,6 +855,7 @@ mb_status attention_bwd(const bf16* qkv, const bf16* O, const bf16* dO, const fl
     dq_convert_kernel<<<nnz, 64, 0, s>>>(dq_acc, cu, batch, nnz, H, dqkv);
     MB_CHECK_LAUNCH();
   }
+  if (dbias) return colsum(dqkv, nnz, 3 * H, dbias, s);
   return MB_OK;
 }
 
@@ -485,14 +878,14 @@ size_t mb_attention_workspace_bytes(int32_t nnz, int32_t heads, int32_t head_dim
 
 mb_status mb_attention_backward(const mb_bf16* qkv, const mb_bf16* O, const mb_bf16* dO, const float* lse,
                                 const int32_t* cu_seqlens, int32_t batch, int32_t nnz, int32_t max_seqlen,
-                                int32_t heads, int32_t head_dim, const float* slopes, mb_bf16* dqkv, void* ws,
-                                size_t ws_bytes, mb_stream_t s) {
+                                int32_t heads, int32_t head_dim, const float* slopes, mb_bf16* dqkv, float* db_qkv,
+                                void* ws, size_t ws_bytes, mb_stream_t s) {
   if (!qkv || !O || !dO || !lse || !cu_seqlens || !slopes || !dqkv || batch < 0 || nnz < 0)
     return MB_ERR_INVALID_ARG;
   if (heads <= 0) return MB_ERR_CONFIG;
   return mb::attention_bwd(reinterpret_cast<const bf16*>(qkv), reinterpret_cast<const bf16*>(O),
                            reinterpret_cast<const bf16*>(dO), lse, cu_seqlens, batch, nnz, max_seqlen, heads,
-                           head_dim, slopes, reinterpret_cast<bf16*>(dqkv), ws, ws_bytes,
+                           head_dim, slopes, reinterpret_cast<bf16*>(dqkv), db_qkv, ws, ws_bytes,
                            reinterpret_cast<cudaStream_t>(s));
 }
 

@@ -4,8 +4,10 @@
 //   warp 1      : MMA issuer (one lane)   — tcgen05.mma kind::f16, 128 x BN x 16 per instruction,
 //                 accumulating in TMEM; double-buffered accumulator (2 x BN fp32 columns)
 //   warp 2      : TMEM allocator
-//   warps 4..7  : epilogue — tcgen05.ld 32 lanes x 32 columns, fused bias / residual / GeLU /
-//                 GeGLU fwd+bwd / fp32 atomic accumulate, stores to global
+//   warps 4..11 : epilogue (two warps per TMEM lane quarter, one per half of the tile's columns) —
+//                 tcgen05.ld 32 lanes x 32 columns, fused bias / residual / GeLU / GeGLU fwd+bwd /
+//                 fp32 atomic accumulate; bf16 inputs and outputs move through a per-warp smem
+//                 scratch so that every global access is coalesced (8 rows x 64 B per instruction)
 //
 // Operands may be K-major (the nn.Linear forward layout) or MN-major (the transposed operands of
 // dX = dY W and dW = dY^T X); both are expressed with 128-byte-swizzled TMA boxes and the matching
@@ -19,15 +21,20 @@
 namespace mb {
 namespace {
 
-constexpr int BM = 128, BK = 64, NTHREADS = 256;
+constexpr int BM = 128, BK = 64;
+constexpr int NUM_EPI_WARPS = 8;                     // two warps per TMEM lane quarter
+constexpr int NTHREADS = 128 + 32 * NUM_EPI_WARPS;  // warps 0-3: TMA, MMA, TMEM alloc, spare
+constexpr int SCR_ROW = 80;                          // scratch row: 32 bf16 (64 B) + 16 B pad (conflict-free)
+constexpr int SCR_BYTES = 32 * SCR_ROW;
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int NSCR>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int DATA = STAGE_BYTES * STAGES;
-  static constexpr int SMEM = DATA + 1024 + 256;
+  static constexpr int SCR = NUM_EPI_WARPS * NSCR * SCR_BYTES;
+  static constexpr int SMEM = DATA + SCR + 1024 + 256;
   static constexpr int TMEM_COLS = 2 * BN;
 };
 
@@ -44,13 +51,6 @@ struct Sched {
   }
 };
 
-__device__ __forceinline__ void store_bf16x32(bf16* dst, const float* v, int ncols_valid) {
-  // ncols_valid is a multiple of 8 (host guarantees N % 8 == 0)
-#pragma unroll
-  for (int g = 0; g < 4; ++g)
-    if (g * 8 < ncols_valid) *reinterpret_cast<uint4*>(dst + g * 8) = f32_to_bf16x8(v + g * 8);
-}
-
 __device__ __forceinline__ void load_bf16x32(const bf16* src, float* v, int ncols_valid) {
 #pragma unroll
   for (int g = 0; g < 4; ++g) {
@@ -64,14 +64,62 @@ __device__ __forceinline__ void load_bf16x32(const bf16* src, float* v, int ncol
   }
 }
 
-template <int BN, int STAGES, int A_MN, int B_MN, int PAIRED>
+// ---- warp-cooperative coalesced movement of a 32-row x 32-column bf16 chunk through a per-warp
+// smem scratch: lane l covers rows (l>>2)+8i, 16-byte segment (l&3), so every global access
+// instruction touches 8 full 64-byte row segments instead of 32 scattered half-sectors.
+__device__ __forceinline__ void chunk_load(uint4 (&r)[4], const bf16* base, int64_t ld, int row0, int M, int col,
+                                           int N, int lane) {
+  const int c = col + (lane & 3) * 8;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = row0 + (lane >> 2) + 8 * i;
+    if (row < M && c < N) r[i] = *reinterpret_cast<const uint4*>(base + (int64_t)row * ld + c);
+    else r[i] = make_uint4(0, 0, 0, 0);
+  }
+}
+__device__ __forceinline__ void chunk_to_scr(uint8_t* scr, const uint4 (&r)[4], int lane) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    *reinterpret_cast<uint4*>(scr + ((lane >> 2) + 8 * i) * SCR_ROW + (lane & 3) * 16) = r[i];
+}
+__device__ __forceinline__ void scr_row_read(const uint8_t* scr, int lane, float* v) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) bf16x8_to_f32(*reinterpret_cast<const uint4*>(scr + lane * SCR_ROW + j * 16), v + 8 * j);
+}
+__device__ __forceinline__ void scr_row_write(uint8_t* scr, int lane, const float* v) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) *reinterpret_cast<uint4*>(scr + lane * SCR_ROW + j * 16) = f32_to_bf16x8(v + 8 * j);
+}
+__device__ __forceinline__ void scr_to_global(const uint8_t* scr, bf16* base, int64_t ld, int row0, int M, int col,
+                                              int N, int lane) {
+  const int c = col + (lane & 3) * 8;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int rr = (lane >> 2) + 8 * i;
+    const int row = row0 + rr;
+    if (row < M && c < N)
+      *reinterpret_cast<uint4*>(base + (int64_t)row * ld + c) =
+          *reinterpret_cast<const uint4*>(scr + rr * SCR_ROW + (lane & 3) * 16);
+  }
+}
+// row-wise values of this lane -> scratch -> coalesced global store
+__device__ __forceinline__ void emit_chunk(uint8_t* scr, const float* v, bf16* base, int64_t ld, int row0, int M,
+                                           int col, int N, int lane) {
+  scr_row_write(scr, lane, v);
+  __syncwarp();
+  scr_to_global(scr, base, ld, row0, M, col, N, lane);
+  __syncwarp();
+}
+
+template <int BN, int STAGES, int A_MN, int B_MN, int PAIRED, int NSCR>
 __global__ void __launch_bounds__(NTHREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                 Sched sc, Epi ep) {
-  using C = Cfg<BN, STAGES>;
+  using C = Cfg<BN, STAGES, NSCR>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATA);
+  uint8_t* scr_base = smem + C::DATA;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATA + C::SCR);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -89,7 +137,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&tfull[i], 1);
-      sm100::mbar_init(&tempty[i], 4);
+      sm100::mbar_init(&tempty[i], NUM_EPI_WARPS);
     }
     sm100::fence_barrier_init();
   }
@@ -172,103 +220,160 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   } else if (warp >= 4) {
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int ew = warp - 4;
+    const int q = warp & 3;     // TMEM lane quarter this warp may access
+    const int grp = ew >> 2;    // which half of the tile's columns
+    uint8_t* scrA = scr_base + ew * NSCR * SCR_BYTES;
+    uint8_t* scrB = scrA + (NSCR > 1 ? SCR_BYTES : 0);
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < sc.total; u += gridDim.x) {
       int mb, nb, kb0, kb1;
       sc.decode(u, mb, nb, kb0, kb1);
+      const int row0 = mb * BM + q * 32;
+      const int row = row0 + lane;
+      const bool row_ok = row < M;
       sm100::mbar_wait(&tfull[acc], acc_phase);
       sm100::tc_fence_after();
-      const int row = mb * BM + q * 32 + lane;
-      const bool row_ok = row < M;
       const uint32_t tb = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
       float v[32];
-      if (ep.mode == E_GEGLU_FWD) {
-        // paired tile: TMEM cols [0,128) = a (W1 half), [128,256) = g (V half) for columns nb*128..
+      if (PAIRED) {
+        // paired tile: TMEM cols [0,128) = a (W1 half), [128,256) = g (V half); this warp group
+        // owns a-columns [grp*64, grp*64+64) of the 128 output columns nb*128..
         float g[32];
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          sm100::tmem_ld32(tb + c * 32, v);
-          sm100::tmem_ld32(tb + 128 + c * 32, g);
+        for (int c = 0; c < 2; ++c) {
+          const int crel = grp * 64 + c * 32;
+          const int col = nb * 128 + crel;
+          sm100::tmem_ld32(tb + crel, v);
+          sm100::tmem_ld32(tb + 128 + crel, g);
+          float ba[32], bg[32];
+          load_bf16x32(ep.bias + col, ba, 32);
+          load_bf16x32(ep.bias + ep.I + col, bg, 32);
           sm100::tmem_ld_wait();
-          const int col = nb * 128 + c * 32;
-          if (row_ok) {
-            float ba[32], bg[32];
-            load_bf16x32(ep.bias + col, ba, 32);
-            load_bf16x32(ep.bias + ep.I + col, bg, 32);
-            float z[32];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              v[j] += ba[j];
-              g[j] += bg[j];
-              z[j] = gelu_f(v[j]) * g[j];
-            }
-            bf16* U = ep.aux + (int64_t)row * ep.ldaux;
-            store_bf16x32(U + col, v, 32);
-            store_bf16x32(U + ep.I + col, g, 32);
-            store_bf16x32(reinterpret_cast<bf16*>(ep.C) + (int64_t)row * ep.ldc + col, z, 32);
+          for (int j = 0; j < 32; ++j) {
+            v[j] += ba[j];
+            g[j] += bg[j];
           }
+          // output Z = GeLU(a) * g; saved for backward Gd = [g * GeLU'(a) | GeLU(a)] (the two factors
+          // of dU = [dZ g GeLU'(a) | dZ GeLU(a)], so the backward epilogue needs no transcendental)
+          float z[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float x = v[j];
+            const float cdf = 0.5f + 0.5f * erff(x * 0.70710678118654752f);
+            const float pdf = 0.3989422804014327f * __expf(-0.5f * x * x);
+            const float ge = x * cdf;
+            z[j] = ge * g[j];
+            v[j] = g[j] * (cdf + x * pdf);
+            g[j] = ge;
+          }
+          emit_chunk(scrA, v, ep.aux, ep.ldaux, row0, M, col, ep.I, lane);
+          emit_chunk(scrA, g, ep.aux + ep.I, ep.ldaux, row0, M, col, ep.I, lane);
+          emit_chunk(scrA, z, reinterpret_cast<bf16*>(ep.C), ep.ldc, row0, M, col, ep.I, lane);
         }
       } else {
+        constexpr int HALF = BN / 2;
+        const int cbase = nb * BN + grp * HALF;
+        uint4 pa[4], pg[4];
+        if (ep.mode == E_GEGLU_BWD) {
+          chunk_load(pa, ep.U, ep.ldu, row0, M, cbase, N, lane);
+          chunk_load(pg, ep.U + ep.I, ep.ldu, row0, M, cbase, N, lane);
+        } else if (ep.mode == E_BF16 && ep.res) {
+          chunk_load(pa, ep.res, ep.ldr, row0, M, cbase, N, lane);
+        }
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          const int col = nb * BN + c * 32;
+        for (int c = 0; c < HALF / 32; ++c) {
+          const int crel = grp * HALF + c * 32;
+          const int col = cbase + c * 32;
           if (col >= N) break;  // warp-uniform
-          sm100::tmem_ld32(tb + c * 32, v);
-          sm100::tmem_ld_wait();
-          if (!row_ok) continue;
+          sm100::tmem_ld32(tb + crel, v);
           const int nv = min(32, N - col);
           if (ep.mode == E_F32_ACC) {
-            float* dst = reinterpret_cast<float*>(ep.C) + (int64_t)row * ep.ldc + col;
+            sm100::tmem_ld_wait();
+            if (row_ok) {
+              float* dst = reinterpret_cast<float*>(ep.C) + (int64_t)row * ep.ldc + col;
 #pragma unroll
-            for (int j = 0; j < 32; j += 4)
-              if (j < nv) red_add_v4(dst + j, v[j], v[j + 1], v[j + 2], v[j + 3]);
+              for (int j = 0; j < 32; j += 4)
+                if (j < nv) red_add_v4(dst + j, v[j], v[j + 1], v[j + 2], v[j + 3]);
+            }
           } else if (ep.mode == E_F32) {
+            float b[32];
+            if (ep.bias) load_bf16x32(ep.bias + col, b, nv);
+            sm100::tmem_ld_wait();
             if (ep.bias) {
-              float b[32];
-              load_bf16x32(ep.bias + col, b, nv);
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] += b[j];
             }
-            float* dst = reinterpret_cast<float*>(ep.C) + (int64_t)row * ep.ldc + col;
+            if (row_ok) {
+              float* dst = reinterpret_cast<float*>(ep.C) + (int64_t)row * ep.ldc + col;
 #pragma unroll
-            for (int j = 0; j < 32; j += 4)
-              if (j < nv) *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-          } else if (ep.mode == E_GEGLU_BWD) {
-            // v = dZ; U row holds a at [col..], g at [I+col..]
-            float a[32], g[32];
-            const bf16* Ur = ep.U + (int64_t)row * ep.ldu;
-            load_bf16x32(Ur + col, a, nv);
-            load_bf16x32(Ur + ep.I + col, g, nv);
-            float da[32], dg[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              da[j] = v[j] * g[j] * gelu_grad_f(a[j]);
-              dg[j] = v[j] * gelu_f(a[j]);
+              for (int j = 0; j < 32; j += 4)
+                if (j < nv) *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
             }
-            bf16* D = reinterpret_cast<bf16*>(ep.C) + (int64_t)row * ep.ldc;
-            store_bf16x32(D + col, da, nv);
-            store_bf16x32(D + ep.I + col, dg, nv);
+          } else if (ep.mode == E_GEGLU_BWD) {
+            // v = dZ; saved Gd row holds g GeLU'(a) at [col..], GeLU(a) at [I+col..]  ->  dU = dZ * Gd
+            chunk_to_scr(scrA, pa, lane);
+            chunk_to_scr(scrB, pg, lane);
+            __syncwarp();
+            if (c + 1 < HALF / 32) {
+              chunk_load(pa, ep.U, ep.ldu, row0, M, col + 32, N, lane);
+              chunk_load(pg, ep.U + ep.I, ep.ldu, row0, M, col + 32, N, lane);
+            }
+            sm100::tmem_ld_wait();
+            // 16 columns at a time keeps the live register set small (a, g, dZ)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              float a[16], g[16];
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                bf16x8_to_f32(*reinterpret_cast<const uint4*>(scrA + lane * SCR_ROW + (2 * h + j) * 16), a + 8 * j);
+                bf16x8_to_f32(*reinterpret_cast<const uint4*>(scrB + lane * SCR_ROW + (2 * h + j) * 16), g + 8 * j);
+              }
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const float dz = v[16 * h + j];
+                a[j] = dz * a[j];  // dZ * g * GeLU'(a)
+                g[j] = dz * g[j];  // dZ * GeLU(a)
+              }
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                *reinterpret_cast<uint4*>(scrA + lane * SCR_ROW + (2 * h + j) * 16) = f32_to_bf16x8(a + 8 * j);
+                *reinterpret_cast<uint4*>(scrB + lane * SCR_ROW + (2 * h + j) * 16) = f32_to_bf16x8(g + 8 * j);
+              }
+            }
+            __syncwarp();
+            bf16* D = reinterpret_cast<bf16*>(ep.C);
+            scr_to_global(scrA, D, ep.ldc, row0, M, col, N, lane);
+            scr_to_global(scrB, D + ep.I, ep.ldc, row0, M, col, N, lane);
+            __syncwarp();
           } else {  // E_BF16 / E_GELU_AUX
+            float b[32];
+            if (ep.bias) load_bf16x32(ep.bias + col, b, nv);
+            if (ep.res) {
+              chunk_to_scr(scrA, pa, lane);
+              __syncwarp();
+              if (c + 1 < HALF / 32) chunk_load(pa, ep.res, ep.ldr, row0, M, col + 32, N, lane);
+            }
+            sm100::tmem_ld_wait();
             if (ep.bias) {
-              float b[32];
-              load_bf16x32(ep.bias + col, b, nv);
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] += b[j];
             }
             if (ep.res) {
               float r[32];
-              load_bf16x32(ep.res + (int64_t)row * ep.ldr + col, r, nv);
+              scr_row_read(scrA, lane, r);
+              __syncwarp();
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] += r[j];
             }
             if (ep.mode == E_GELU_AUX) {
-              store_bf16x32(ep.aux + (int64_t)row * ep.ldaux + col, v, nv);
+              emit_chunk(scrA, v, ep.aux, ep.ldaux, row0, M, col, N, lane);
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
             }
-            store_bf16x32(reinterpret_cast<bf16*>(ep.C) + (int64_t)row * ep.ldc + col, v, nv);
+            emit_chunk(scrA, v, reinterpret_cast<bf16*>(ep.C), ep.ldc, row0, M, col, N, lane);
           }
         }
       }
@@ -287,10 +392,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp == 2) sm100::tmem_dealloc(tmem_base, C::TMEM_COLS);
 }
 
-template <int BN, int STAGES, int A_MN, int B_MN, int PAIRED>
+template <int BN, int STAGES, int A_MN, int B_MN, int PAIRED, int NSCR>
 mb_status launch(const GemmArgs& g, const CUtensorMap& ta, const CUtensorMap& tb, const Sched& sc, cudaStream_t s) {
-  using C = Cfg<BN, STAGES>;
-  auto k = gemm_kernel<BN, STAGES, A_MN, B_MN, PAIRED>;
+  using C = Cfg<BN, STAGES, NSCR>;
+  auto k = gemm_kernel<BN, STAGES, A_MN, B_MN, PAIRED, NSCR>;
   static bool attr_set = false;  // benign race: idempotent
   if (!attr_set) {
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) != cudaSuccess)
@@ -303,14 +408,13 @@ mb_status launch(const GemmArgs& g, const CUtensorMap& ta, const CUtensorMap& tb
   return MB_OK;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int NSCR>
 mb_status dispatch_majors(const GemmArgs& g, const CUtensorMap& ta, const CUtensorMap& tb, const Sched& sc,
-                          bool paired, cudaStream_t s) {
-  if (paired) return launch<BN, STAGES, 0, 0, 1>(g, ta, tb, sc, s);
-  if (!g.a_t && !g.b_t) return launch<BN, STAGES, 0, 0, 0>(g, ta, tb, sc, s);
-  if (!g.a_t && g.b_t) return launch<BN, STAGES, 0, 1, 0>(g, ta, tb, sc, s);
-  if (g.a_t && g.b_t) return launch<BN, STAGES, 1, 1, 0>(g, ta, tb, sc, s);
-  return launch<BN, STAGES, 1, 0, 0>(g, ta, tb, sc, s);
+                          cudaStream_t s) {
+  if (!g.a_t && !g.b_t) return launch<BN, STAGES, 0, 0, 0, NSCR>(g, ta, tb, sc, s);
+  if (!g.a_t && g.b_t) return launch<BN, STAGES, 0, 1, 0, NSCR>(g, ta, tb, sc, s);
+  if (g.a_t && g.b_t) return launch<BN, STAGES, 1, 1, 0, NSCR>(g, ta, tb, sc, s);
+  return launch<BN, STAGES, 1, 0, 0, NSCR>(g, ta, tb, sc, s);
 }
 
 }  // namespace
@@ -325,9 +429,11 @@ mb_status gemm(const GemmArgs& g, cudaStream_t s) {
   if (paired) MB_REQUIRE(g.ep.I % 128 == 0 && g.N == 2 * g.ep.I && !g.a_t && !g.b_t, MB_ERR_CONFIG);
   if (g.ep.mode == E_GEGLU_BWD) MB_REQUIRE(g.N == g.ep.I, MB_ERR_CONFIG);
 
-  // BN: 256 for wide outputs, 128 when N is small (tiny configs) — GeGLU fwd is always a 256-wide
-  // paired tile (128 columns of W1 + the matching 128 of V).
-  const int BN = paired ? 256 : (g.N <= 128 ? 128 : 256);
+  // BN: 256 for wide outputs, 128 when N is small (tiny configs) or for the GeGLU backward (whose
+  // epilogue streams two input tiles); GeGLU fwd is always a 256-wide paired tile (128 columns of
+  // W1 + the matching 128 of V).
+  const bool geglu_bwd = g.ep.mode == E_GEGLU_BWD;
+  const int BN = paired ? 256 : ((g.N <= 128 || geglu_bwd) ? 128 : 256);
   CUtensorMap ta, tb;
   bool ok;
   if (!g.a_t) ok = make_tmap_bf16_2d(&ta, g.A, g.K, g.M, g.lda, BK, BM);
@@ -354,8 +460,13 @@ mb_status gemm(const GemmArgs& g, cudaStream_t s) {
   sc.splits = (sc.nkb + sc.kb_per - 1) / sc.kb_per;
   sc.total = sc.num_m * sc.num_n * sc.splits;
 
-  if (BN == 256) return dispatch_majors<256, 4>(g, ta, tb, sc, paired, s);
-  return dispatch_majors<128, 6>(g, ta, tb, sc, paired, s);
+  if (paired) return launch<256, 4, 0, 0, 1, 1>(g, ta, tb, sc, s);
+  if (geglu_bwd) {
+    if (g.a_t || !g.b_t) return MB_ERR_CONFIG;
+    return launch<128, 5, 0, 1, 0, 2>(g, ta, tb, sc, s);
+  }
+  if (BN == 256) return dispatch_majors<256, 4, 1>(g, ta, tb, sc, s);
+  return dispatch_majors<128, 6, 1>(g, ta, tb, sc, s);
 }
 
 }  // namespace mb
@@ -383,8 +494,8 @@ extern "C" mb_status mb_gemm(int32_t M, int32_t N, int32_t K, const mb_bf16* A, 
 }
 
 extern "C" mb_status mb_geglu_forward(const mb_bf16* X, int32_t n, int32_t H, int32_t I, const mb_bf16* w_1v,
-                                      const mb_bf16* b_1v, mb_bf16* U, mb_bf16* Z, mb_stream_t s) {
-  MB_REQUIRE(X && w_1v && b_1v && U && Z, MB_ERR_INVALID_ARG);
+                                      const mb_bf16* b_1v, mb_bf16* Gd, mb_bf16* Z, mb_stream_t s) {
+  MB_REQUIRE(X && w_1v && b_1v && Gd && Z, MB_ERR_INVALID_ARG);
   mb::GemmArgs g;
   g.M = n, g.N = 2 * I, g.K = H;
   g.A = reinterpret_cast<const bf16*>(X), g.lda = H;
@@ -392,21 +503,21 @@ extern "C" mb_status mb_geglu_forward(const mb_bf16* X, int32_t n, int32_t H, in
   g.ep.mode = mb::E_GEGLU_FWD;
   g.ep.C = Z, g.ep.ldc = I;
   g.ep.bias = reinterpret_cast<const bf16*>(b_1v);
-  g.ep.aux = reinterpret_cast<bf16*>(U), g.ep.ldaux = 2 * I;
+  g.ep.aux = reinterpret_cast<bf16*>(Gd), g.ep.ldaux = 2 * I;
   g.ep.I = I;
   return mb::gemm(g, reinterpret_cast<cudaStream_t>(s));
 }
 
 extern "C" mb_status mb_geglu_backward(const mb_bf16* dF, int32_t n, int32_t H, int32_t I, const mb_bf16* w_2,
-                                       const mb_bf16* U, mb_bf16* dU, mb_stream_t s) {
-  MB_REQUIRE(dF && w_2 && U && dU, MB_ERR_INVALID_ARG);
+                                       const mb_bf16* Gd, mb_bf16* dU, mb_stream_t s) {
+  MB_REQUIRE(dF && w_2 && Gd && dU, MB_ERR_INVALID_ARG);
   mb::GemmArgs g;
   g.M = n, g.N = I, g.K = H;
   g.A = reinterpret_cast<const bf16*>(dF), g.lda = H;
   g.B = reinterpret_cast<const bf16*>(w_2), g.ldb = I, g.b_t = true;  // W2 [H, I] = [K, N]
   g.ep.mode = mb::E_GEGLU_BWD;
   g.ep.C = dU, g.ep.ldc = 2 * I;
-  g.ep.U = reinterpret_cast<const bf16*>(U), g.ep.ldu = 2 * I;
+  g.ep.U = reinterpret_cast<const bf16*>(Gd), g.ep.ldu = 2 * I;
   g.ep.I = I;
   return mb::gemm(g, reinterpret_cast<cudaStream_t>(s));
 }

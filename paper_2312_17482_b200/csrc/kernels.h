@@ -14,9 +14,9 @@ struct Epi {
   const bf16* bias = nullptr;   // [N] (GEGLU_FWD: [2I])
   const bf16* res = nullptr;    // residual [M, N] (E_BF16)
   int64_t ldr = 0;
-  bf16* aux = nullptr;          // GELU_AUX: pre-activation out; GEGLU_FWD: U out [M, 2I]
+  bf16* aux = nullptr;          // GELU_AUX: pre-activation out; GEGLU_FWD: Gd out [M, 2I]
   int64_t ldaux = 0;
-  const bf16* U = nullptr;      // GEGLU_BWD: saved U [M, 2I]
+  const bf16* U = nullptr;      // GEGLU_BWD: saved Gd = [g GeLU'(a) | GeLU(a)] [M, 2I]
   int64_t ldu = 0;
   int I = 0;                    // GeGLU half width
 };
@@ -59,7 +59,7 @@ mb_status attention_fwd(const bf16* qkv, const int* cu, int batch, int nnz, int 
                         const float* slopes, bf16* O, float* lse, cudaStream_t s);
 size_t attention_ws_bytes(int nnz, int heads, int d, int max_seqlen);
 mb_status attention_bwd(const bf16* qkv, const bf16* O, const bf16* dO, const float* lse, const int* cu, int batch,
-                        int nnz, int max_seqlen, int heads, int d, const float* slopes, bf16* dqkv, void* ws,
-                        size_t ws_bytes, cudaStream_t s);
+                        int nnz, int max_seqlen, int heads, int d, const float* slopes, bf16* dqkv, float* dbias,
+                        void* ws, size_t ws_bytes, cudaStream_t s);
 
 }  // namespace mb

@@ -195,17 +195,16 @@ def test_geglu_fwd_bwd(H, I):
     b = synth.bf16_round(0.1 * rng.standard_normal(2 * I))
     W2 = synth.bf16_round(rng.standard_normal((H, I)) / np.sqrt(I))
     dF = synth.bf16_round(rng.standard_normal((n, H)))
-    U = torch.empty(n, 2 * I, dtype=BF, device="cuda")
+    Gd = torch.empty(n, 2 * I, dtype=BF, device="cuda")
     Z = torch.empty(n, I, dtype=BF, device="cuda")
-    mb.geglu_forward(_bf(X), _bf(W), _bf(b), U, Z)
+    mb.geglu_forward(_bf(X), _bf(W), _bf(b), Gd, Z)
     Uo = X.astype(np.float64) @ W.T.astype(np.float64) + b
     a, g = Uo[:, :I], Uo[:, I:]
-    check("geglu.U", np64(U), Uo, max_rel=1e-2)
     check("geglu.Z", np64(Z), O.gelu(a) * g, max_rel=1e-2)
+    check("geglu.Gd_a", np64(Gd)[:, :I], g * O.gelu_grad(a), max_rel=1e-2)
+    check("geglu.Gd_g", np64(Gd)[:, I:], O.gelu(a), max_rel=1e-2)
     dU = torch.empty(n, 2 * I, dtype=BF, device="cuda")
-    mb.geglu_backward(_bf(dF), _bf(W2), U, dU)
-    Ug = np64(U)  # the backward consumes the saved (bf16) U
-    a, g = Ug[:, :I], Ug[:, I:]
+    mb.geglu_backward(_bf(dF), _bf(W2), Gd, dU)
     dZ = dF.astype(np.float64) @ W2.astype(np.float64)
     check("geglu.da", np64(dU)[:, :I], dZ * g * O.gelu_grad(a))
     check("geglu.dg", np64(dU)[:, I:], dZ * O.gelu(a))
@@ -261,13 +260,19 @@ def test_attention_fwd_bwd(case):
     lse_o = np.stack([O.unpad(lse_o[:, h, :], oidx) for h in range(heads)])
     assert np.max(np.abs(np64(lse) - lse_o)) < 2e-2
     dqkv = torch.zeros(nnz, 3 * H, dtype=BF, device="cuda")
-    mb.attention_backward(qkv, Od, dO, lse, cud, B, nnz, maxlen, heads, d, sl, dqkv)
+    db = torch.zeros(3 * H, dtype=torch.float32, device="cuda")
+    mb.attention_backward(qkv, Od, dO, lse, cud, B, nnz, maxlen, heads, d, sl, dqkv, db_qkv=db)
     dq, dk, dv = O.attention_backward(sp(do_p), cache)
     ref = np.concatenate([x.reshape(B, Lmax, H) for x in (dq, dk, dv)], -1)
     ref = O.unpad(ref, oidx)
     got = np64(dqkv)
     for nm, sl_ in (("dq", slice(0, H)), ("dk", slice(H, 2 * H)), ("dv", slice(2 * H, 3 * H))):
         check(f"{case}.{nm}", got[:, sl_], ref[:, sl_])
+    # fused bias gradient: column sums of dQKV (db_k is ~0 analytically: rows of dS sum to zero)
+    dbref = ref.sum(0)
+    check(f"{case}.db_qv", np.concatenate([np64(db)[:H], np64(db)[2 * H:]]),
+          np.concatenate([dbref[:H], dbref[2 * H:]]))
+    assert np.max(np.abs(np64(db)[H:2 * H])) <= 2e-2 * np.max(np.abs(dbref))
 
 
 def test_attention_alibi_closed_form():
