@@ -163,6 +163,7 @@ mb_status mb_encoder_backward(const mb_dims* d, const mb_layer_params* p, const 
     GemmArgs a;
     a.M = T, a.N = I, a.K = H, a.A = w.ds2, a.lda = H, a.B = B(p->w_2), a.ldb = I, a.b_t = true;
     a.ep.mode = E_GEGLU_BWD, a.ep.C = w.du, a.ep.ldc = 2 * I, a.ep.U = sv.u, a.ep.ldu = 2 * I, a.ep.I = I;
+    a.ep.dbias = g->b_1v;  // db1v = column sums of dU, fused into the epilogue
     TRY(gemm(a, s));
   }
   {  // dW2 += dS2^T Z
@@ -171,7 +172,6 @@ mb_status mb_encoder_backward(const mb_dims* d, const mb_layer_params* p, const 
     a.ep.mode = E_F32_ACC, a.ep.C = g->w_2, a.ep.ldc = I;
     TRY(gemm(a, s));
   }
-  TRY(colsum(w.du, T, 2 * I, g->b_1v, s));  // db1v
   {  // dY1 = dU W1v + dS2
     GemmArgs a;
     a.M = T, a.N = H, a.K = 2 * I, a.A = w.du, a.lda = 2 * I, a.B = B(p->w_1v), a.ldb = H, a.b_t = true;

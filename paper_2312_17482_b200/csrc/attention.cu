@@ -570,7 +570,15 @@ __global__ void __launch_bounds__(SH_THREADS, 1) attn_fwd_short_kernel(const __g
   if (warp == 0) sm100::tmem_dealloc(tbase, 256);
 }
 
-constexpr int SH_BWD_SMEM = 4 * TILE_BYTES + 2 * P_BYTES + 1024 + 256 + 2 * 128 * 4 + 3 * 64 * 4;
+// Backward: a software-pipelined persistent kernel.  Warp 8 (one lane) is the producer/issuer:
+// TMA loads of (Q, K, V, dO) for the next two units into two smem buffers, S = QK^T and dP = dO V^T
+// of unit i+1 issued as soon as the compute warps have consumed unit i's S/dP, and the second MMA
+// batch (dV, dK, dQ) of unit i; warps 0-7 do the elementwise softmax-gradient of unit i and the
+// readout of unit i-1, so loads, both MMA batches and the CUDA-core work of neighbouring units
+// overlap.  TMEM: S [0,128), dP [128,256), dV [256,320), dK [320,384), dQ [384,448).
+constexpr int BWD_BUF_BYTES = 4 * TILE_BYTES;  // Q, K, V, dO
+constexpr int SH_BWD_THREADS = SH_THREADS + 32;
+constexpr int SH_BWD_SMEM = 2 * BWD_BUF_BYTES + 2 * P_BYTES + 1024 + 256 + 2 * 128 * 4;
 
 // per-warp transpose-reduce: lane l ends with sum over the warp's 32 rows of column l of v[32]
 __device__ __forceinline__ float warp_colsum32(float* v, int lane) {
@@ -587,33 +595,37 @@ __device__ __forceinline__ float warp_colsum32(float* v, int lane) {
   return v[0];
 }
 
-__global__ void __launch_bounds__(SH_THREADS, 1) attn_bwd_short_kernel(
+__device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+
+__global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
     const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do, const int* __restrict__ cu,
     int batch, int heads, int d, const float* __restrict__ slopes, const bf16* __restrict__ O,
     const bf16* __restrict__ dO, const float* __restrict__ lse, bf16* __restrict__ dqkv, float* __restrict__ dbias,
     int nnz) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sK = sQ + TILE_BYTES;
-  uint8_t* sV = sK + TILE_BYTES;
-  uint8_t* sdO = sV + TILE_BYTES;
-  uint8_t* sP = sdO + TILE_BYTES;
+  uint8_t* bufs = smem;                        // 2 x (Q, K, V, dO)
+  uint8_t* sP = smem + 2 * BWD_BUF_BYTES;
   uint8_t* sdS = sP + P_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sdS + P_BYTES);  // load, sp, acc
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sdS + P_BYTES);  // load[2], sp, elem, acc
+  uint64_t* load_full = bars;
+  uint64_t* sp_full = bars + 2;
+  uint64_t* elem_done = bars + 3;
+  uint64_t* acc_full = bars + 4;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 8);
   float* dred = reinterpret_cast<float*>(sdS + P_BYTES + 256);  // [2][128] partial D
-  float* bsm = dred + 256;                                      // [3][64] bias-grad partials
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int ch = warp >> 2;
-  const int r = (warp & 3) * 32 + lane;
   const int H = heads * d;
   const int total = batch * heads;
   if (tid == 0) {
     sm100::tma_prefetch(&tm_qkv);
     sm100::tma_prefetch(&tm_do);
-    for (int i = 0; i < 4; ++i) sm100::mbar_init(&bars[i], 1);
+    sm100::mbar_init(&load_full[0], 1);
+    sm100::mbar_init(&load_full[1], 1);
+    sm100::mbar_init(sp_full, 1);
+    sm100::mbar_init(elem_done, 8);
+    sm100::mbar_init(acc_full, 1);
     sm100::fence_barrier_init();
   }
   if (warp == 0) sm100::tmem_alloc(tslot, 512);
@@ -621,153 +633,181 @@ __global__ void __launch_bounds__(SH_THREADS, 1) attn_bwd_short_kernel(
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tbase = *tslot;
-  const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
   const uint32_t tS = tbase, tdP = tbase + 128, tdV = tbase + 256, tdK = tbase + 320, tdQ = tbase + 384;
-  const uint32_t sQa = sm100::smem_u32(sQ), sKa = sm100::smem_u32(sK), sVa = sm100::smem_u32(sV),
-                 sdOa = sm100::smem_u32(sdO), sPa = sm100::smem_u32(sP), sdSa = sm100::smem_u32(sdS);
-  const float rsd = rsqrtf((float)d);
-  const float sc2 = rsd * LOG2E;
+  const uint32_t sPa = sm100::smem_u32(sP), sdSa = sm100::smem_u32(sdS);
 
-  auto issue_loads = [&](int u) {
-    const int b = u / heads, h = u - b * heads;
-    const int st = cu[b];
-    sm100::mbar_arrive_expect_tx(&bars[0], 4 * TILE_BYTES);
-    sm100::tma_load_2d(sQ, &tm_qkv, &bars[0], h * d, st);
-    sm100::tma_load_2d(sK, &tm_qkv, &bars[0], H + h * d, st);
-    sm100::tma_load_2d(sV, &tm_qkv, &bars[0], 2 * H + h * d, st);
-    sm100::tma_load_2d(sdO, &tm_do, &bars[0], h * d, st);
-  };
+  int u0 = blockIdx.x;
+  if (u0 < total && unit_len(cu, heads, u0) == 0) u0 = next_unit(cu, heads, total, u0);
 
-  int u = blockIdx.x;
-  if (u < total && unit_len(cu, heads, u) == 0) u = next_unit(cu, heads, total, u);
-  if (tid == 0 && u < total) issue_loads(u);
-  for (int it = 0; u < total; ++it) {
-    const uint32_t ph = it & 1;
-    const int b = u / heads, h = u - b * heads;
-    const int start = cu[b];
-    const int len = cu[b + 1] - start;
-    const float sl2 = slopes[h] * LOG2E;
-    // D_i = dO_i . O_i (this thread's half of the head dimension), LSE
-    float Dp = 0.f, lse2 = 0.f;
-    if (r < len) {
-      lse2 = lse[(size_t)h * nnz + start + r] * LOG2E;
-      if (32 * ch < d) {
-        const bf16* o_row = O + (size_t)(start + r) * H + h * d + 32 * ch;
-        const bf16* do_row = dO + (size_t)(start + r) * H + h * d + 32 * ch;
-#pragma unroll
-        for (int c = 0; c < 32; c += 8) {
-          float a[8], g[8];
-          bf16x8_to_f32(*reinterpret_cast<const uint4*>(o_row + c), a);
-          bf16x8_to_f32(*reinterpret_cast<const uint4*>(do_row + c), g);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) Dp += a[e] * g[e];
+  if (warp == 8) {
+    // ------------------------------------------------------------------ producer / MMA issuer
+    if (lane == 0) {
+      auto buf_addr = [&](int b) { return bufs + b * BWD_BUF_BYTES; };
+      auto issue_loads = [&](int u, int b) {
+        const int bb = u / heads, h = u - bb * heads;
+        const int st = cu[bb];
+        uint8_t* base = buf_addr(b);
+        sm100::mbar_arrive_expect_tx(&load_full[b], BWD_BUF_BYTES);
+        sm100::tma_load_2d(base, &tm_qkv, &load_full[b], h * d, st);
+        sm100::tma_load_2d(base + TILE_BYTES, &tm_qkv, &load_full[b], H + h * d, st);
+        sm100::tma_load_2d(base + 2 * TILE_BYTES, &tm_qkv, &load_full[b], 2 * H + h * d, st);
+        sm100::tma_load_2d(base + 3 * TILE_BYTES, &tm_do, &load_full[b], h * d, st);
+      };
+      auto mma1 = [&](int b) {  // S = Q K^T, dP = dO V^T
+        const uint32_t q = sm100::smem_u32(buf_addr(b));
+        const uint32_t k = q + TILE_BYTES, v = q + 2 * TILE_BYTES, o = q + 3 * TILE_BYTES;
+        constexpr uint32_t id_s = sm100::idesc_bf16(128, 128, 0, 0);
+        for (int kk = 0; kk < d / 16; ++kk) {
+          sm100::mma_bf16_ss(tS, sm100::desc_kmajor_sw128(q + kk * 32), sm100::desc_kmajor_sw128(k + kk * 32), id_s,
+                             kk > 0);
+          sm100::mma_bf16_ss(tdP, sm100::desc_kmajor_sw128(o + kk * 32), sm100::desc_kmajor_sw128(v + kk * 32), id_s,
+                             kk > 0);
         }
-      }
-    }
-    dred[ch * 128 + r] = Dp;
-    if (tid < 192) bsm[tid] = 0.f;
-    if (tid == 0) {
-      sm100::mbar_wait(&bars[0], ph);
-      sm100::tc_fence_after();
-      constexpr uint32_t id_s = sm100::idesc_bf16(128, 128, 0, 0);
-      for (int k = 0; k < d / 16; ++k) {
-        sm100::mma_bf16_ss(tS, sm100::desc_kmajor_sw128(sQa + k * 32), sm100::desc_kmajor_sw128(sKa + k * 32), id_s,
-                           k > 0);
-        sm100::mma_bf16_ss(tdP, sm100::desc_kmajor_sw128(sdOa + k * 32), sm100::desc_kmajor_sw128(sVa + k * 32),
-                           id_s, k > 0);
-      }
-      sm100::mma_commit(&bars[1]);
-    }
-    __syncthreads();
-    const float Dr = dred[r] + dred[128 + r];
-    sm100::mbar_wait(&bars[1], ph);
-    sm100::tc_fence_after();
-#pragma unroll 1
-    for (int c = 0; c < 2; ++c) {
-      const int c0 = 64 * ch + 32 * c;
-      float v[32], w[32];
-      sm100::tmem_ld32(tS + lane_off + c0, v);
-      sm100::tmem_ld32(tdP + lane_off + c0, w);
-      sm100::tmem_ld_wait();
-      uint32_t pp[16], pd[16];
+        sm100::mma_commit(sp_full);
+      };
+      auto mma2 = [&](int b) {  // dV = P^T dO, dK = dS^T Q, dQ = dS K
+        const uint32_t q = sm100::smem_u32(buf_addr(b));
+        const uint32_t k = q + TILE_BYTES, o = q + 3 * TILE_BYTES;
+        constexpr uint32_t id_t = sm100::idesc_bf16(128, 64, 1, 1);
+        constexpr uint32_t id_q = sm100::idesc_bf16(128, 64, 0, 1);
 #pragma unroll
-      for (int jj = 0; jj < 32; jj += 2) {
-        float p2[2], ds2[2];
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int key = c0 + jj + e;
-          const bool ok = (r < len) && (key < len);
-          const float p = ok ? exp2f(v[jj + e] * sc2 - sl2 * fabsf((float)(r - key)) - lse2) : 0.f;
-          p2[e] = p;
-          ds2[e] = p * (w[jj + e] - Dr);
+        for (int kk = 0; kk < TILE / 16; ++kk) {
+          sm100::mma_bf16_ss(tdV, sm100::desc_mnmajor_sw128(sPa + kk * 2048, TILE * 128),
+                             sm100::desc_mnmajor_sw128(o + kk * 2048, 8192), id_t, kk > 0);
+          sm100::mma_bf16_ss(tdK, sm100::desc_mnmajor_sw128(sdSa + kk * 2048, TILE * 128),
+                             sm100::desc_mnmajor_sw128(q + kk * 2048, 8192), id_t, kk > 0);
+          sm100::mma_bf16_ss(tdQ, sm100::desc_kmajor_sw128(sdSa + (kk >> 2) * (TILE * 128) + (kk & 3) * 32),
+                             sm100::desc_mnmajor_sw128(k + kk * 2048, 8192), id_q, kk > 0);
         }
-        pp[jj >> 1] = pack_bf16x2(p2[0], p2[1]);
-        pd[jj >> 1] = pack_bf16x2(ds2[0], ds2[1]);
+        sm100::mma_commit(acc_full);
+      };
+      int u_cur = u0;
+      int u_nxt = u_cur < total ? next_unit(cu, heads, total, u_cur) : total;
+      if (u_cur < total) issue_loads(u_cur, 0);
+      if (u_nxt < total) issue_loads(u_nxt, 1);
+      if (u_cur < total) {
+        sm100::mbar_wait(&load_full[0], 0);
+        sm100::tc_fence_after();
+        mma1(0);
       }
-#pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) {
-        const uint32_t off = p_off(r, c0 + q4 * 8);
-        st_shared_v4(sPa + off, pp[4 * q4], pp[4 * q4 + 1], pp[4 * q4 + 2], pp[4 * q4 + 3]);
-        st_shared_v4(sdSa + off, pd[4 * q4], pd[4 * q4 + 1], pd[4 * q4 + 2], pd[4 * q4 + 3]);
+      for (int i = 0; u_cur < total; ++i) {
+        const int b = i & 1;
+        sm100::mbar_wait(elem_done, i & 1);  // compute warps consumed S/dP(i), wrote P/dS(i)
+        sm100::tc_fence_after();
+        mma2(b);
+        if (u_nxt < total) {
+          sm100::mbar_wait(&load_full[b ^ 1], ((i + 1) >> 1) & 1);
+          sm100::tc_fence_after();
+          mma1(b ^ 1);
+        }
+        sm100::mbar_wait(acc_full, i & 1);  // MMA2(i) done: buffer b and P/dS are free
+        const int u_n2 = u_nxt < total ? next_unit(cu, heads, total, u_nxt) : total;
+        if (u_n2 < total) issue_loads(u_n2, b);
+        u_cur = u_nxt;
+        u_nxt = u_n2;
       }
-    }
-    sm100::fence_proxy_async_smem();
-    sm100::tc_fence_before();
-    __syncthreads();
-    if (tid == 0) {
-      sm100::tc_fence_after();
-      constexpr uint32_t id_t = sm100::idesc_bf16(128, 64, 1, 1);  // P^T dO, dS^T Q
-      constexpr uint32_t id_q = sm100::idesc_bf16(128, 64, 0, 1);  // dS K
-#pragma unroll
-      for (int k = 0; k < TILE / 16; ++k) {
-        sm100::mma_bf16_ss(tdV, sm100::desc_mnmajor_sw128(sPa + k * 2048, TILE * 128),
-                           sm100::desc_mnmajor_sw128(sdOa + k * 2048, 8192), id_t, k > 0);
-        sm100::mma_bf16_ss(tdK, sm100::desc_mnmajor_sw128(sdSa + k * 2048, TILE * 128),
-                           sm100::desc_mnmajor_sw128(sQa + k * 2048, 8192), id_t, k > 0);
-        sm100::mma_bf16_ss(tdQ, sm100::desc_kmajor_sw128(sdSa + (k >> 2) * (TILE * 128) + (k & 3) * 32),
-                           sm100::desc_mnmajor_sw128(sKa + k * 2048, 8192), id_q, k > 0);
-      }
-      sm100::mma_commit(&bars[2]);
     }
     __syncwarp();
-    sm100::mbar_wait(&bars[2], ph);
-    sm100::tc_fence_after();
-    const int un = next_unit(cu, heads, total, u);
-    if (tid == 0 && un < total) issue_loads(un);  // all tiles are free: every MMA reading them completed
-    // dQ (row = query r), dK (row = key r), dV (row = key r): this thread's 32 of the 64 columns
-    const bool ok = r < len;
-    const bool col_ok = 32 * ch < d;
+  } else {
+    // ------------------------------------------------------------------ compute warps 0-7
+    const int ch = warp >> 2;
+    const int r = (warp & 3) * 32 + lane;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const float rsd = rsqrtf((float)d);
+    const float sc2 = rsd * LOG2E;
+    for (int i = 0, u = u0; u < total; ++i) {
+      const int b = u / heads, h = u - b * heads;
+      const int start = cu[b];
+      const int len = cu[b + 1] - start;
+      const float sl2 = slopes[h] * LOG2E;
+      // D_i = dO_i . O_i (this thread's half of the head dimension) and LSE, from global
+      float Dp = 0.f, lse2 = 0.f;
+      if (r < len) {
+        lse2 = lse[(size_t)h * nnz + start + r] * LOG2E;
+        if (32 * ch < d) {
+          const bf16* o_row = O + (size_t)(start + r) * H + h * d + 32 * ch;
+          const bf16* do_row = dO + (size_t)(start + r) * H + h * d + 32 * ch;
+#pragma unroll
+          for (int c = 0; c < 32; c += 8) {
+            float a[8], g[8];
+            bf16x8_to_f32(*reinterpret_cast<const uint4*>(o_row + c), a);
+            bf16x8_to_f32(*reinterpret_cast<const uint4*>(do_row + c), g);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) Dp += a[e] * g[e];
+          }
+        }
+      }
+      dred[ch * 128 + r] = Dp;
+      named_bar_sync(1, SH_THREADS);
+      const float Dr = dred[r] + dred[128 + r];
+      sm100::mbar_wait(sp_full, i & 1);
+      sm100::tc_fence_after();
 #pragma unroll 1
-    for (int which = 0; which < 3; ++which) {
-      float v[32];
-      const uint32_t src = which == 0 ? tdQ : (which == 1 ? tdK : tdV);
-      sm100::tmem_ld32(src + lane_off + 32 * ch, v);
-      sm100::tmem_ld_wait();
-      const float sc = which == 2 ? 1.f : rsd;
+      for (int c = 0; c < 2; ++c) {
+        const int c0 = 64 * ch + 32 * c;
+        float v[32], w[32];
+        sm100::tmem_ld32(tS + lane_off + c0, v);
+        sm100::tmem_ld32(tdP + lane_off + c0, w);
+        sm100::tmem_ld_wait();
+        uint32_t pp[16], pd[16];
 #pragma unroll
-      for (int e = 0; e < 32; ++e) v[e] = ok ? v[e] * sc : 0.f;
-      if (ok && col_ok) {
-        bf16* dst = dqkv + (size_t)(start + r) * 3 * H + which * H + h * d + 32 * ch;
+        for (int jj = 0; jj < 32; jj += 2) {
+          float p2[2], ds2[2];
 #pragma unroll
-        for (int c = 0; c < 32; c += 8) *reinterpret_cast<uint4*>(dst + c) = f32_to_bf16x8(v + c);
+          for (int e = 0; e < 2; ++e) {
+            const int key = c0 + jj + e;
+            const bool ok = (r < len) && (key < len);
+            const float p = ok ? exp2f(v[jj + e] * sc2 - sl2 * fabsf((float)(r - key)) - lse2) : 0.f;
+            p2[e] = p;
+            ds2[e] = p * (w[jj + e] - Dr);
+          }
+          pp[jj >> 1] = pack_bf16x2(p2[0], p2[1]);
+          pd[jj >> 1] = pack_bf16x2(ds2[0], ds2[1]);
+        }
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const uint32_t off = p_off(r, c0 + q4 * 8);
+          st_shared_v4(sPa + off, pp[4 * q4], pp[4 * q4 + 1], pp[4 * q4 + 2], pp[4 * q4 + 3]);
+          st_shared_v4(sdSa + off, pd[4 * q4], pd[4 * q4 + 1], pd[4 * q4 + 2], pd[4 * q4 + 3]);
+        }
       }
-      if (dbias) {
-        // bias gradient of the QKV projection = column sums of dQKV, reduced per warp by a
-        // transpose-reduce, then across the 4 row-quarter warps in shared memory
-        const float cs = warp_colsum32(v, lane);
-        atomicAdd(&bsm[which * 64 + 32 * ch + lane], cs);
+      sm100::fence_proxy_async_smem();
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(elem_done);
+      sm100::mbar_wait(acc_full, i & 1);
+      sm100::tc_fence_after();
+      // dQ (row = query r), dK (row = key r), dV (row = key r): this thread's 32 of the 64 columns
+      const bool ok = r < len;
+      const bool col_ok = 32 * ch < d;
+#pragma unroll 1
+      for (int which = 0; which < 3; ++which) {
+        float v[32];
+        const uint32_t src = which == 0 ? tdQ : (which == 1 ? tdK : tdV);
+        sm100::tmem_ld32(src + lane_off + 32 * ch, v);
+        sm100::tmem_ld_wait();
+        const float sc = which == 2 ? 1.f : rsd;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[e] = ok ? v[e] * sc : 0.f;
+        if (ok && col_ok) {
+          bf16* dst = dqkv + (size_t)(start + r) * 3 * H + which * H + h * d + 32 * ch;
+#pragma unroll
+          for (int c = 0; c < 32; c += 8) *reinterpret_cast<uint4*>(dst + c) = f32_to_bf16x8(v + c);
+        }
+        if (dbias) {
+          // QKV-projection bias gradient = column sums of dQKV: transpose-reduce over the warp's
+          // 32 rows, one atomic per column per warp
+          const float cs = warp_colsum32(v, lane);
+          if (col_ok && 32 * ch + lane < d) atomicAdd(dbias + which * H + h * d + 32 * ch + lane, cs);
+        }
       }
+      sm100::tc_fence_before();
+      u = next_unit(cu, heads, total, u);
     }
-    sm100::tc_fence_before();
-    __syncthreads();
-    if (dbias && tid < 3 * 64) {
-      const int which = tid >> 6, c = tid & 63;
-      if (c < d) atomicAdd(dbias + which * H + h * d + c, bsm[tid]);
-    }
-    u = un;
   }
   sm100::tc_fence_before();
   __syncthreads();
+  sm100::tc_fence_after();
   if (warp == 0) sm100::tmem_dealloc(tbase, 512);
 }
 
@@ -833,8 +873,8 @@ mb_status attention_bwd(const bf16* qkv, const bf16* O, const bf16* dO, const fl
     }
     const int units = batch * heads;
     const int grid = std::max(1, std::min(units, num_sms()));
-    attn_bwd_short_kernel<<<grid, SH_THREADS, SH_BWD_SMEM, s>>>(tq, tdo, cu, batch, heads, d, slopes, O, dO, lse,
-                                                                 dqkv, dbias, nnz);
+    attn_bwd_short_kernel<<<grid, SH_BWD_THREADS, SH_BWD_SMEM, s>>>(tq, tdo, cu, batch, heads, d, slopes, O, dO,
+                                                                     lse, dqkv, dbias, nnz);
     MB_CHECK_LAUNCH();
     return MB_OK;
   }

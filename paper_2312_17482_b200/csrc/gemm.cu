@@ -111,6 +111,21 @@ __device__ __forceinline__ void emit_chunk(uint8_t* scr, const float* v, bf16* b
   __syncwarp();
 }
 
+// per-warp transpose-reduce: lane l ends with the sum over the warp's 32 rows of column l of v[32]
+__device__ __forceinline__ float warp_colsum32(float* v, int lane) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+#pragma unroll
+    for (int j = 0; j < s; ++j) {
+      const bool up = lane & s;
+      const float send = up ? v[j] : v[j + s];
+      const float keep = up ? v[j + s] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+  }
+  return v[0];
+}
+
 template <int BN, int STAGES, int A_MN, int B_MN, int PAIRED, int NSCR>
 __global__ void __launch_bounds__(NTHREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
@@ -347,6 +362,23 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             bf16* D = reinterpret_cast<bf16*>(ep.C);
             scr_to_global(scrA, D, ep.ldc, row0, M, col, N, lane);
             scr_to_global(scrB, D + ep.I, ep.ldc, row0, M, col, N, lane);
+            if (ep.dbias) {
+              // db_1v = column sums of dU (the rounded values that were stored), fused here:
+              // transpose-reduce over the warp's 32 rows, one atomic per column per warp
+              float t[32];
+              scr_row_read(scrA, lane, t);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) t[j] = row_ok ? t[j] : 0.f;
+              const float ca = warp_colsum32(t, lane);
+              scr_row_read(scrB, lane, t);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) t[j] = row_ok ? t[j] : 0.f;
+              const float cg = warp_colsum32(t, lane);
+              if (col + lane < N) {
+                atomicAdd(ep.dbias + col + lane, ca);
+                atomicAdd(ep.dbias + ep.I + col + lane, cg);
+              }
+            }
             __syncwarp();
           } else {  // E_BF16 / E_GELU_AUX
             float b[32];

@@ -19,6 +19,7 @@ struct Epi {
   const bf16* U = nullptr;      // GEGLU_BWD: saved Gd = [g GeLU'(a) | GeLU(a)] [M, 2I]
   int64_t ldu = 0;
   int I = 0;                    // GeGLU half width
+  float* dbias = nullptr;       // GEGLU_BWD: column sums of dU accumulated here (fp32 [2I], +=)
 };
 
 struct GemmArgs {

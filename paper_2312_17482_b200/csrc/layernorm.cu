@@ -117,54 +117,43 @@ __device__ __forceinline__ void cta_column_reduce(const float* acc, float* sbuf,
 }
 
 template <int VPL, bool EMBED, bool GELU>
-__global__ void __launch_bounds__(LN_THREADS) ln_bwd_kernel(RowSrc src, const bf16* __restrict__ dy,
-                                                            const float* __restrict__ stats,
-                                                            const bf16* __restrict__ gamma,
-                                                            const bf16* __restrict__ gelu_pre, int n, int H,
-                                                            bf16* dx, float* __restrict__ d_emb,
-                                                            float* __restrict__ dgamma, float* __restrict__ dbeta,
-                                                            float* __restrict__ dsum) {
+__global__ void __launch_bounds__(LN_THREADS, VPL <= 3 ? 2 : 1)
+    ln_bwd_kernel(RowSrc src, const bf16* __restrict__ dy, const float* __restrict__ stats,
+                  const bf16* __restrict__ gamma, const bf16* __restrict__ gelu_pre, int n, int H, bf16* dx,
+                  float* __restrict__ d_emb, float* __restrict__ dgamma, float* __restrict__ dbeta,
+                  float* __restrict__ dsum) {
+  // Register budget (2 CTAs x 8 warps per SM): per lane only x-hat and the three column
+  // accumulators stay live; dy and gamma are re-read (L1 hits) in the second pass.
   extern __shared__ float sbuf[];
   const int lane = threadIdx.x & 31;
   float acc_g[VPL * 8], acc_b[VPL * 8], acc_s[VPL * 8];
 #pragma unroll
   for (int i = 0; i < VPL * 8; ++i) acc_g[i] = acc_b[i] = acc_s[i] = 0.f;
-  float gm[VPL * 8];
-#pragma unroll
-  for (int i = 0; i < VPL; ++i) {
-    const int c = (i * 32 + lane) * 8;
-    if (c < H) bf16x8_to_f32(*reinterpret_cast<const uint4*>(gamma + c), gm + i * 8);
-    else {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) gm[i * 8 + j] = 0.f;
-    }
-  }
   for (int row = blockIdx.x * LN_WARPS + (threadIdx.x >> 5); row < n; row += gridDim.x * LN_WARPS) {
-    float v[VPL * 8], g[VPL * 8];
+    float v[VPL * 8];
     int id = 0;
     load_row<VPL, EMBED>(src, row, H, lane, v, id);
     const float2 st = *reinterpret_cast<const float2*>(stats + 2 * (size_t)row);
+    const bf16* dyr = dy + (size_t)row * H;
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
       const int c = (i * 32 + lane) * 8;
       if (c < H) {
-        float d[8];
-        bf16x8_to_f32(*reinterpret_cast<const uint4*>(dy + (size_t)row * H + c), d);
+        float d[8], gm[8];
+        bf16x8_to_f32(*reinterpret_cast<const uint4*>(dyr + c), d);
+        bf16x8_to_f32(*reinterpret_cast<const uint4*>(gamma + c), gm);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int k = i * 8 + j;
           const float xh = (v[k] - st.x) * st.y;
           v[k] = xh;
-          g[k] = d[j] * gm[k];
+          const float gg = d[j] * gm[j];
           acc_g[k] += d[j] * xh;
           acc_b[k] += d[j];
-          s1 += g[k];
-          s2 += g[k] * xh;
+          s1 += gg;
+          s2 += gg * xh;
         }
-      } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) g[i * 8 + j] = 0.f;
       }
     }
     s1 = warp_sum(s1) / H;
@@ -173,12 +162,11 @@ __global__ void __launch_bounds__(LN_THREADS) ln_bwd_kernel(RowSrc src, const bf
     for (int i = 0; i < VPL; ++i) {
       const int c = (i * 32 + lane) * 8;
       if (c < H) {
-        float o[8];
+        float d[8], gm[8], o[8];
+        bf16x8_to_f32(*reinterpret_cast<const uint4*>(dyr + c), d);
+        bf16x8_to_f32(*reinterpret_cast<const uint4*>(gamma + c), gm);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int k = i * 8 + j;
-          o[j] = st.y * (g[k] - s1 - v[k] * s2);
-        }
+        for (int j = 0; j < 8; ++j) o[j] = st.y * (d[j] * gm[j] - s1 - v[i * 8 + j] * s2);
         if (GELU) {
           float p[8];
           bf16x8_to_f32(*reinterpret_cast<const uint4*>(gelu_pre + (size_t)row * H + c), p);
@@ -241,7 +229,7 @@ mb_status ln_bwd_launch(const RowSrc& src, const bf16* dy, const float* stats, c
                         const bf16* gelu_pre, int n, int H, bf16* dx, float* d_emb, float* dg, float* db,
                         float* dsum, cudaStream_t s) {
   const int smem = LN_WARPS * H * sizeof(float);
-  const int grid = std::max(1, std::min((n + LN_WARPS - 1) / LN_WARPS, 4 * num_sms()));
+  const int grid = std::max(1, std::min((n + LN_WARPS - 1) / LN_WARPS, (VPL <= 3 ? 2 : 1) * num_sms()));
   if (gelu_pre)
     ln_bwd_kernel<VPL, EMBED, true><<<grid, LN_THREADS, smem, s>>>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb,
                                                                     dg, db, dsum);
