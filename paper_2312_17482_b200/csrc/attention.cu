@@ -417,7 +417,7 @@ __global__ void dq_convert_kernel(const float* __restrict__ dq_acc, const int* _
 // as soon as the MMAs that read the current tiles have completed, overlapping the output epilogue.
 // ------------------------------------------------------------------------------------------
 constexpr int SH_THREADS = 256;
-constexpr int SH_FWD_SMEM = 3 * TILE_BYTES + P_BYTES + 1024 + 256 + 4 * 128 * 4;
+__device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
 __device__ __forceinline__ int unit_len(const int* cu, int heads, int u) {
   const int b = u / heads;
@@ -429,145 +429,185 @@ __device__ __forceinline__ int next_unit(const int* cu, int heads, int total, in
   return total;
 }
 
-__global__ void __launch_bounds__(SH_THREADS, 1) attn_fwd_short_kernel(const __grid_constant__ CUtensorMap tm_qkv,
-                                                                      const int* __restrict__ cu, int batch,
-                                                                      int heads, int d,
-                                                                      const float* __restrict__ slopes,
-                                                                      bf16* __restrict__ O, float* __restrict__ lse,
-                                                                      int nnz) {
+// Forward, software-pipelined: warp 8 (one lane) issues the TMA loads of units i+1, i+2 into two
+// smem buffers and S(i+1) = Q K^T into the second TMEM S buffer while warps 0-7 run the softmax of
+// unit i; then O(i) = P V.  TMEM: S[0] [0,128), S[1] [128,256), O [256,320).
+constexpr int SH_FWD_THREADS = SH_THREADS + 32;
+constexpr int FWD_BUF_BYTES = 3 * TILE_BYTES;  // Q, K, V
+constexpr int SH_FWD_SMEM2 = 2 * FWD_BUF_BYTES + P_BYTES + 1024 + 256;
+
+__global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const __grid_constant__ CUtensorMap tm_qkv,
+                                                                          const int* __restrict__ cu, int batch,
+                                                                          int heads, int d,
+                                                                          const float* __restrict__ slopes,
+                                                                          bf16* __restrict__ O,
+                                                                          float* __restrict__ lse, int nnz) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sK = sQ + TILE_BYTES;
-  uint8_t* sV = sK + TILE_BYTES;
-  uint8_t* sP = sV + TILE_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + P_BYTES);  // load, s, o
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
-  float* rmax = reinterpret_cast<float*>(sP + P_BYTES + 256);  // [2][128]
-  float* rsum = rmax + 256;                                    // [2][128]
+  uint8_t* bufs = smem;  // 2 x (Q, K, V)
+  uint8_t* sP = smem + 2 * FWD_BUF_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + P_BYTES);
+  uint64_t* load_full = bars;     // [2]
+  // one S barrier per TMEM S buffer: S(i+1) is committed before the softmax of unit i ends, so a
+  // single barrier could run two phases ahead of a slow waiter (parity aliasing)
+  uint64_t* s_full = bars + 2;    // [2]
+  uint64_t* p_ready = bars + 4;   // 8 compute warps arrive per unit
+  uint64_t* o_full = bars + 5;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 8);
+  __shared__ float rmax[2 * 128], rsum[2 * 128];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int ch = warp >> 2;
-  const int r = (warp & 3) * 32 + lane;
   const int H = heads * d;
   const int total = batch * heads;
   if (tid == 0) {
     sm100::tma_prefetch(&tm_qkv);
-    for (int i = 0; i < 4; ++i) sm100::mbar_init(&bars[i], 1);
+    sm100::mbar_init(&load_full[0], 1);
+    sm100::mbar_init(&load_full[1], 1);
+    sm100::mbar_init(&s_full[0], 1);
+    sm100::mbar_init(&s_full[1], 1);
+    sm100::mbar_init(p_ready, 8);
+    sm100::mbar_init(o_full, 1);
     sm100::fence_barrier_init();
   }
-  if (warp == 0) sm100::tmem_alloc(tslot, 256);
+  if (warp == 0) sm100::tmem_alloc(tslot, 512);
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tbase = *tslot;
-  const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-  const uint32_t tS = tbase + lane_off + 64 * ch, tO = tbase + 128 + lane_off + 32 * ch;
-  const uint32_t sQa = sm100::smem_u32(sQ), sKa = sm100::smem_u32(sK), sVa = sm100::smem_u32(sV),
-                 sPa = sm100::smem_u32(sP);
-  const float sc2 = rsqrtf((float)d) * LOG2E;
+  const uint32_t sPa = sm100::smem_u32(sP);
 
-  auto issue_loads = [&](int u) {
-    const int b = u / heads, h = u - b * heads;
-    const int st = cu[b];
-    sm100::mbar_arrive_expect_tx(&bars[0], 3 * TILE_BYTES);
-    sm100::tma_load_2d(sQ, &tm_qkv, &bars[0], h * d, st);
-    sm100::tma_load_2d(sK, &tm_qkv, &bars[0], H + h * d, st);
-    sm100::tma_load_2d(sV, &tm_qkv, &bars[0], 2 * H + h * d, st);
-  };
+  int u0 = blockIdx.x;
+  if (u0 < total && unit_len(cu, heads, u0) == 0) u0 = next_unit(cu, heads, total, u0);
 
-  int u = blockIdx.x;
-  if (u < total && unit_len(cu, heads, u) == 0) u = next_unit(cu, heads, total, u);
-  if (tid == 0 && u < total) issue_loads(u);
-  for (int it = 0; u < total; ++it) {
-    const uint32_t ph = it & 1;
-    const int b = u / heads, h = u - b * heads;
-    const int start = cu[b];
-    const int len = cu[b + 1] - start;
-    const float sl2 = slopes[h] * LOG2E;
-    if (tid == 0) {
-      sm100::mbar_wait(&bars[0], ph);
-      sm100::tc_fence_after();
-      constexpr uint32_t id_s = sm100::idesc_bf16(128, 128, 0, 0);
-      for (int k = 0; k < d / 16; ++k)
-        sm100::mma_bf16_ss(tbase, sm100::desc_kmajor_sw128(sQa + k * 32), sm100::desc_kmajor_sw128(sKa + k * 32),
-                           id_s, k > 0);
-      sm100::mma_commit(&bars[1]);
-    }
-    __syncwarp();
-    sm100::mbar_wait(&bars[1], ph);
-    sm100::tc_fence_after();
-    float x[64];
-    sm100::tmem_ld32(tS, x);
-    sm100::tmem_ld32(tS + 32, x + 32);
-    sm100::tmem_ld_wait();
-    float mx = -INFINITY;
+  if (warp == 8) {
+    if (lane == 0) {
+      auto issue_loads = [&](int u, int b) {
+        const int bb = u / heads, h = u - bb * heads;
+        const int st = cu[bb];
+        uint8_t* base = bufs + b * FWD_BUF_BYTES;
+        sm100::mbar_arrive_expect_tx(&load_full[b], FWD_BUF_BYTES);
+        sm100::tma_load_2d(base, &tm_qkv, &load_full[b], h * d, st);
+        sm100::tma_load_2d(base + TILE_BYTES, &tm_qkv, &load_full[b], H + h * d, st);
+        sm100::tma_load_2d(base + 2 * TILE_BYTES, &tm_qkv, &load_full[b], 2 * H + h * d, st);
+      };
+      auto mma_s = [&](int b) {
+        const uint32_t q = sm100::smem_u32(bufs + b * FWD_BUF_BYTES), k = q + TILE_BYTES;
+        constexpr uint32_t id_s = sm100::idesc_bf16(128, 128, 0, 0);
+        for (int kk = 0; kk < d / 16; ++kk)
+          sm100::mma_bf16_ss(tbase + 128 * b, sm100::desc_kmajor_sw128(q + kk * 32),
+                             sm100::desc_kmajor_sw128(k + kk * 32), id_s, kk > 0);
+        sm100::mma_commit(&s_full[b]);
+      };
+      auto mma_o = [&](int b) {
+        const uint32_t v = sm100::smem_u32(bufs + b * FWD_BUF_BYTES) + 2 * TILE_BYTES;
+        constexpr uint32_t id_o = sm100::idesc_bf16(128, 64, 0, 1);
 #pragma unroll
-    for (int j = 0; j < 64; ++j) {
-      const int key = 64 * ch + j;
-      const float t = x[j] * sc2 - sl2 * fabsf((float)(r - key));
-      x[j] = key < len ? t : -INFINITY;
-      mx = fmaxf(mx, x[j]);
-    }
-    rmax[ch * 128 + r] = mx;
-    __syncthreads();
-    mx = fmaxf(rmax[r], rmax[128 + r]);
-    float sum = 0.f;
-#pragma unroll
-    for (int j8 = 0; j8 < 8; ++j8) {
-      uint32_t pk[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const bf162 hp = __floats2bfloat162_rn(exp2f(x[j8 * 8 + 2 * e] - mx), exp2f(x[j8 * 8 + 2 * e + 1] - mx));
-        const float2 pr = __bfloat1622float2(hp);
-        sum += pr.x + pr.y;
-        pk[e] = *reinterpret_cast<const uint32_t*>(&hp);
+        for (int kk = 0; kk < TILE / 16; ++kk)
+          sm100::mma_bf16_ss(tbase + 256, sm100::desc_kmajor_sw128(sPa + (kk >> 2) * (TILE * 128) + (kk & 3) * 32),
+                             sm100::desc_mnmajor_sw128(v + kk * 2048, 8192), id_o, kk > 0);
+        sm100::mma_commit(o_full);
+      };
+      int u_cur = u0;
+      int u_nxt = u_cur < total ? next_unit(cu, heads, total, u_cur) : total;
+      if (u_cur < total) issue_loads(u_cur, 0);
+      if (u_nxt < total) issue_loads(u_nxt, 1);
+      if (u_cur < total) {
+        sm100::mbar_wait(&load_full[0], 0);
+        sm100::tc_fence_after();
+        mma_s(0);
       }
-      st_shared_v4(sPa + p_off(r, 64 * ch + 8 * j8), pk[0], pk[1], pk[2], pk[3]);
-    }
-    rsum[ch * 128 + r] = sum;
-    sm100::fence_proxy_async_smem();
-    sm100::tc_fence_before();
-    __syncthreads();
-    if (tid == 0) {
-      sm100::tc_fence_after();
-      constexpr uint32_t id_o = sm100::idesc_bf16(128, 64, 0, 1);
-#pragma unroll
-      for (int k = 0; k < TILE / 16; ++k)
-        sm100::mma_bf16_ss(tbase + 128, sm100::desc_kmajor_sw128(sPa + (k >> 2) * (TILE * 128) + (k & 3) * 32),
-                           sm100::desc_mnmajor_sw128(sVa + k * 2048, 8192), id_o, k > 0);
-      sm100::mma_commit(&bars[2]);
-    }
-    __syncwarp();
-    sm100::mbar_wait(&bars[2], ph);
-    sm100::tc_fence_after();
-    const int un = next_unit(cu, heads, total, u);
-    if (tid == 0 && un < total) issue_loads(un);  // tiles are free: both MMAs have completed
-    float v[32];
-    sm100::tmem_ld32(tO, v);
-    sm100::tmem_ld_wait();
-    const float l = rsum[r] + rsum[128 + r];
-    if (r < len) {
-      const float inv = 1.f / l;
-      bf16* dst = O + (size_t)(start + r) * H + h * d + 32 * ch;
-#pragma unroll
-      for (int c = 0; c < 32; c += 8) {
-        if (32 * ch + c < d) {
-          float t[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) t[e] = v[c + e] * inv;
-          *reinterpret_cast<uint4*>(dst + c) = f32_to_bf16x8(t);
+      for (int i = 0; u_cur < total; ++i) {
+        const int b = i & 1;
+        if (u_nxt < total) {  // S(i+1) into the other TMEM buffer while the softmax of unit i runs
+          sm100::mbar_wait(&load_full[b ^ 1], ((i + 1) >> 1) & 1);
+          sm100::tc_fence_after();
+          mma_s(b ^ 1);
         }
+        sm100::mbar_wait(p_ready, i & 1);
+        sm100::tc_fence_after();
+        mma_o(b);
+        sm100::mbar_wait(o_full, i & 1);  // P V(i) done: buffer b and sP are free
+        const int u_n2 = u_nxt < total ? next_unit(cu, heads, total, u_nxt) : total;
+        if (u_n2 < total) issue_loads(u_n2, b);
+        u_cur = u_nxt;
+        u_nxt = u_n2;
       }
-      if (ch == 0) lse[(size_t)h * nnz + start + r] = (mx + log2f(l)) * LN2;
     }
-    sm100::tc_fence_before();
-    __syncthreads();
-    u = un;
+    __syncwarp();
+  } else {
+    const int ch = warp >> 2;
+    const int r = (warp & 3) * 32 + lane;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const float sc2 = rsqrtf((float)d) * LOG2E;
+    for (int i = 0, u = u0; u < total; ++i) {
+      const int b = u / heads, h = u - b * heads;
+      const int start = cu[b];
+      const int len = cu[b + 1] - start;
+      const float sl2 = slopes[h] * LOG2E;
+      sm100::mbar_wait(&s_full[i & 1], (i >> 1) & 1);
+      sm100::tc_fence_after();
+      const uint32_t tS = tbase + 128 * (i & 1) + lane_off + 64 * ch;
+      float x[64];
+      sm100::tmem_ld32(tS, x);
+      sm100::tmem_ld32(tS + 32, x + 32);
+      sm100::tmem_ld_wait();
+      float mx = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 64; ++j) {
+        const int key = 64 * ch + j;
+        const float t = x[j] * sc2 - sl2 * fabsf((float)(r - key));
+        x[j] = key < len ? t : -INFINITY;
+        mx = fmaxf(mx, x[j]);
+      }
+      rmax[ch * 128 + r] = mx;
+      named_bar_sync(1, SH_THREADS);
+      mx = fmaxf(rmax[r], rmax[128 + r]);
+      float sum = 0.f;
+#pragma unroll
+      for (int j8 = 0; j8 < 8; ++j8) {
+        uint32_t pk[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const bf162 hp = __floats2bfloat162_rn(exp2f(x[j8 * 8 + 2 * e] - mx), exp2f(x[j8 * 8 + 2 * e + 1] - mx));
+          const float2 pr = __bfloat1622float2(hp);
+          sum += pr.x + pr.y;
+          pk[e] = *reinterpret_cast<const uint32_t*>(&hp);
+        }
+        st_shared_v4(sPa + p_off(r, 64 * ch + 8 * j8), pk[0], pk[1], pk[2], pk[3]);
+      }
+      rsum[ch * 128 + r] = sum;
+      sm100::fence_proxy_async_smem();
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(p_ready);
+      sm100::mbar_wait(o_full, i & 1);
+      sm100::tc_fence_after();
+      float v[32];
+      sm100::tmem_ld32(tbase + 256 + lane_off + 32 * ch, v);
+      sm100::tmem_ld_wait();
+      const float l = rsum[r] + rsum[128 + r];
+      if (r < len) {
+        const float inv = 1.f / l;
+        bf16* dst = O + (size_t)(start + r) * H + h * d + 32 * ch;
+#pragma unroll
+        for (int c = 0; c < 32; c += 8) {
+          if (32 * ch + c < d) {
+            float t[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) t[e] = v[c + e] * inv;
+            *reinterpret_cast<uint4*>(dst + c) = f32_to_bf16x8(t);
+          }
+        }
+        if (ch == 0) lse[(size_t)h * nnz + start + r] = (mx + log2f(l)) * LN2;
+      }
+      sm100::tc_fence_before();
+      u = next_unit(cu, heads, total, u);
+    }
   }
   sm100::tc_fence_before();
   __syncthreads();
-  if (warp == 0) sm100::tmem_dealloc(tbase, 256);
+  sm100::tc_fence_after();
+  if (warp == 0) sm100::tmem_dealloc(tbase, 512);
 }
 
 // Backward: a software-pipelined persistent kernel.  Warp 8 (one lane) is the producer/issuer:
@@ -578,7 +618,7 @@ __global__ void __launch_bounds__(SH_THREADS, 1) attn_fwd_short_kernel(const __g
 // overlap.  TMEM: S [0,128), dP [128,256), dV [256,320), dK [320,384), dQ [384,448).
 constexpr int BWD_BUF_BYTES = 4 * TILE_BYTES;  // Q, K, V, dO
 constexpr int SH_BWD_THREADS = SH_THREADS + 32;
-constexpr int SH_BWD_SMEM = 2 * BWD_BUF_BYTES + 2 * P_BYTES + 1024 + 256 + 2 * 128 * 4;
+constexpr int SH_BWD_SMEM = 2 * BWD_BUF_BYTES + 2 * P_BYTES + 1024 + 256;
 
 // per-warp transpose-reduce: lane l ends with sum over the warp's 32 rows of column l of v[32]
 __device__ __forceinline__ float warp_colsum32(float* v, int lane) {
@@ -595,7 +635,6 @@ __device__ __forceinline__ float warp_colsum32(float* v, int lane) {
   return v[0];
 }
 
-__device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
 __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
     const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do, const int* __restrict__ cu,
@@ -613,7 +652,7 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
   uint64_t* elem_done = bars + 3;
   uint64_t* acc_full = bars + 4;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 8);
-  float* dred = reinterpret_cast<float*>(sdS + P_BYTES + 256);  // [2][128] partial D
+  __shared__ float dred[2 * 128];  // partial D of the two half-row threads
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int H = heads * d;
@@ -720,56 +759,55 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
       const int start = cu[b];
       const int len = cu[b + 1] - start;
       const float sl2 = slopes[h] * LOG2E;
-      // D_i = dO_i . O_i (this thread's half of the head dimension) and LSE, from global
-      float Dp = 0.f, lse2 = 0.f;
-      if (r < len) {
-        lse2 = lse[(size_t)h * nnz + start + r] * LOG2E;
-        if (32 * ch < d) {
-          const bf16* o_row = O + (size_t)(start + r) * H + h * d + 32 * ch;
-          const bf16* do_row = dO + (size_t)(start + r) * H + h * d + 32 * ch;
-#pragma unroll
-          for (int c = 0; c < 32; c += 8) {
-            float a[8], g[8];
-            bf16x8_to_f32(*reinterpret_cast<const uint4*>(o_row + c), a);
-            bf16x8_to_f32(*reinterpret_cast<const uint4*>(do_row + c), g);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) Dp += a[e] * g[e];
-          }
-        }
-      }
-      dred[ch * 128 + r] = Dp;
-      named_bar_sync(1, SH_THREADS);
-      const float Dr = dred[r] + dred[128 + r];
+      const float lse2 = (r < len) ? lse[(size_t)h * nnz + start + r] * LOG2E : 0.f;
       sm100::mbar_wait(sp_full, i & 1);
       sm100::tc_fence_after();
-#pragma unroll 1
+      // pass 1: P = exp2(S*log2e/sqrt(d) - m log2e |i-j| - LSE log2e) in fp32 (kept in registers,
+      // stored as bf16 for the MMAs) and the partial row sum of P * dP.  Since O = P V,
+      // D_i = dO_i . O_i = sum_j P_ij dP_ij, so D needs neither O nor dO from memory.
+      float p[64];
+      float Dp = 0.f;
+#pragma unroll
       for (int c = 0; c < 2; ++c) {
         const int c0 = 64 * ch + 32 * c;
         float v[32], w[32];
         sm100::tmem_ld32(tS + lane_off + c0, v);
         sm100::tmem_ld32(tdP + lane_off + c0, w);
         sm100::tmem_ld_wait();
-        uint32_t pp[16], pd[16];
+        uint32_t pp[16];
 #pragma unroll
         for (int jj = 0; jj < 32; jj += 2) {
-          float p2[2], ds2[2];
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int key = c0 + jj + e;
             const bool ok = (r < len) && (key < len);
-            const float p = ok ? exp2f(v[jj + e] * sc2 - sl2 * fabsf((float)(r - key)) - lse2) : 0.f;
-            p2[e] = p;
-            ds2[e] = p * (w[jj + e] - Dr);
+            const float pv = ok ? exp2f(v[jj + e] * sc2 - sl2 * fabsf((float)(r - key)) - lse2) : 0.f;
+            p[32 * c + jj + e] = pv;
+            Dp += pv * w[jj + e];
           }
-          pp[jj >> 1] = pack_bf16x2(p2[0], p2[1]);
-          pd[jj >> 1] = pack_bf16x2(ds2[0], ds2[1]);
+          pp[jj >> 1] = pack_bf16x2(p[32 * c + jj], p[32 * c + jj + 1]);
         }
 #pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          const uint32_t off = p_off(r, c0 + q4 * 8);
-          st_shared_v4(sPa + off, pp[4 * q4], pp[4 * q4 + 1], pp[4 * q4 + 2], pp[4 * q4 + 3]);
-          st_shared_v4(sdSa + off, pd[4 * q4], pd[4 * q4 + 1], pd[4 * q4 + 2], pd[4 * q4 + 3]);
-        }
+        for (int q4 = 0; q4 < 4; ++q4)
+          st_shared_v4(sPa + p_off(r, c0 + q4 * 8), pp[4 * q4], pp[4 * q4 + 1], pp[4 * q4 + 2], pp[4 * q4 + 3]);
+      }
+      dred[ch * 128 + r] = Dp;
+      named_bar_sync(1, SH_THREADS);
+      const float Dr = dred[r] + dred[128 + r];
+      // pass 2: dS = P (dP - D)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int c0 = 64 * ch + 32 * c;
+        float w[32];
+        sm100::tmem_ld32(tdP + lane_off + c0, w);
+        sm100::tmem_ld_wait();
+        uint32_t pd[16];
+#pragma unroll
+        for (int jj = 0; jj < 32; jj += 2)
+          pd[jj >> 1] = pack_bf16x2(p[32 * c + jj] * (w[jj] - Dr), p[32 * c + jj + 1] * (w[jj + 1] - Dr));
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4)
+          st_shared_v4(sdSa + p_off(r, c0 + q4 * 8), pd[4 * q4], pd[4 * q4 + 1], pd[4 * q4 + 2], pd[4 * q4 + 3]);
       }
       sm100::fence_proxy_async_smem();
       sm100::tc_fence_before();
@@ -824,14 +862,14 @@ mb_status attention_fwd(const bf16* qkv, const int* cu, int batch, int nnz, int 
   if (max_seqlen <= TILE) {
     static bool attr_s = false;
     if (!attr_s) {
-      if (cudaFuncSetAttribute(attn_fwd_short_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SH_FWD_SMEM) !=
+      if (cudaFuncSetAttribute(attn_fwd_short_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SH_FWD_SMEM2) !=
           cudaSuccess)
         return MB_ERR_CUDA;
       attr_s = true;
     }
     const int units = batch * heads;
     const int grid = std::max(1, std::min(units, num_sms()));
-    attn_fwd_short_kernel<<<grid, SH_THREADS, SH_FWD_SMEM, s>>>(tm, cu, batch, heads, d, slopes, O, lse, nnz);
+    attn_fwd_short_kernel<<<grid, SH_FWD_THREADS, SH_FWD_SMEM2, s>>>(tm, cu, batch, heads, d, slopes, O, lse, nnz);
     MB_CHECK_LAUNCH();
     return MB_OK;
   }

@@ -34,11 +34,11 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t a, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
       "selp.b32 %0, 1, 0, P1;\n"
       "}\n"
       : "=r"(ok)
-      : "r"(a), "r"(parity), "r"(0x989680)
+      : "r"(a), "r"(parity)
       : "memory");
   return ok != 0;
 }
