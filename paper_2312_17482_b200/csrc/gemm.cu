@@ -34,7 +34,8 @@ struct Cfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int DATA = STAGE_BYTES * STAGES;
   static constexpr int SCR = NUM_EPI_WARPS * NSCR * SCR_BYTES;
-  static constexpr int SMEM = DATA + SCR + 1024 + 256;
+  static constexpr int BIAS = NUM_EPI_WARPS * 256;  // per-warp staged bias slice of the current tile
+  static constexpr int SMEM = DATA + SCR + BIAS + 1024 + 256;
   static constexpr int TMEM_COLS = 2 * BN;
 };
 
@@ -111,6 +112,15 @@ __device__ __forceinline__ void emit_chunk(uint8_t* scr, const float* v, bf16* b
   __syncwarp();
 }
 
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sm100::smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void load_bias32_smem(const uint8_t* sb, float* v) {
+#pragma unroll
+  for (int g = 0; g < 4; ++g) bf16x8_to_f32(*reinterpret_cast<const uint4*>(sb + g * 16), v + g * 8);
+}
+
 // per-warp transpose-reduce: lane l ends with the sum over the warp's 32 rows of column l of v[32]
 __device__ __forceinline__ float warp_colsum32(float* v, int lane) {
 #pragma unroll
@@ -134,7 +144,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* scr_base = smem + C::DATA;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATA + C::SCR);
+  uint8_t* bias_base = smem + C::DATA + C::SCR;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATA + C::SCR + C::BIAS);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -248,8 +259,33 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int row0 = mb * BM + q * 32;
       const int row = row0 + lane;
       const bool row_ok = row < M;
+      // stage this tile's bias slice in smem (async, overlapped with the MMA of the tile): L1 is
+      // nearly all carved out for the operand ring, so per-chunk bias reads would go to L2
+      uint8_t* sbias = bias_base + ew * 256;
+      if (ep.bias && lane < 16) {
+        if (PAIRED) {
+          const int c = lane >> 3, t = (lane >> 2) & 1, seg = lane & 3;
+          cp_async16(sbias + (c * 2 + t) * 64 + seg * 16, ep.bias + t * ep.I + nb * 128 + grp * 64 + c * 32 + seg * 8);
+        } else {
+          const int c = lane >> 2, seg = lane & 3;
+          const int col = nb * BN + grp * (BN / 2) + c * 32 + seg * 8;
+          if (c < BN / 64 && col < N) cp_async16(sbias + c * 64 + seg * 16, ep.bias + col);
+        }
+      }
+      uint4 pa[4], pg[4];  // first input chunk (residual / Gd), prefetched before the accumulator is ready
+      if (!PAIRED) {
+        const int cbase0 = nb * BN + grp * (BN / 2);
+        if (ep.mode == E_GEGLU_BWD) {
+          chunk_load(pa, ep.U, ep.ldu, row0, M, cbase0, N, lane);
+          chunk_load(pg, ep.U + ep.I, ep.ldu, row0, M, cbase0, N, lane);
+        } else if (ep.mode == E_BF16 && ep.res) {
+          chunk_load(pa, ep.res, ep.ldr, row0, M, cbase0, N, lane);
+        }
+      }
       sm100::mbar_wait(&tfull[acc], acc_phase);
       sm100::tc_fence_after();
+      if (ep.bias) cp_async_wait_all();
+      __syncwarp();
       const uint32_t tb = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
       float v[32];
       if (PAIRED) {
@@ -263,8 +299,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           sm100::tmem_ld32(tb + crel, v);
           sm100::tmem_ld32(tb + 128 + crel, g);
           float ba[32], bg[32];
-          load_bf16x32(ep.bias + col, ba, 32);
-          load_bf16x32(ep.bias + ep.I + col, bg, 32);
+          load_bias32_smem(sbias + (c * 2 + 0) * 64, ba);
+          load_bias32_smem(sbias + (c * 2 + 1) * 64, bg);
           sm100::tmem_ld_wait();
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
@@ -291,13 +327,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       } else {
         constexpr int HALF = BN / 2;
         const int cbase = nb * BN + grp * HALF;
-        uint4 pa[4], pg[4];
-        if (ep.mode == E_GEGLU_BWD) {
-          chunk_load(pa, ep.U, ep.ldu, row0, M, cbase, N, lane);
-          chunk_load(pg, ep.U + ep.I, ep.ldu, row0, M, cbase, N, lane);
-        } else if (ep.mode == E_BF16 && ep.res) {
-          chunk_load(pa, ep.res, ep.ldr, row0, M, cbase, N, lane);
-        }
 #pragma unroll 1
         for (int c = 0; c < HALF / 32; ++c) {
           const int crel = grp * HALF + c * 32;
@@ -315,7 +344,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
           } else if (ep.mode == E_F32) {
             float b[32];
-            if (ep.bias) load_bf16x32(ep.bias + col, b, nv);
+            if (ep.bias) load_bias32_smem(sbias + c * 64, b);
             sm100::tmem_ld_wait();
             if (ep.bias) {
 #pragma unroll
@@ -382,7 +411,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             __syncwarp();
           } else {  // E_BF16 / E_GELU_AUX
             float b[32];
-            if (ep.bias) load_bf16x32(ep.bias + col, b, nv);
+            if (ep.bias) load_bias32_smem(sbias + c * 64, b);
             if (ep.res) {
               chunk_to_scr(scrA, pa, lane);
               __syncwarp();
