@@ -274,7 +274,7 @@ def main():
             traffic = json.load(open(tp)).get("geglu_fwd_gemm_dram_bytes_per_launch")
         except Exception:
             traffic = None
-    roofline = {"kernel": "gemm_kernel<256,4,0,0,1> (A8 GeGLU up-projection, fused bias+GeLU-gate epilogue)",
+    roofline = {"kernel": "gemm_kernel<256,4,0,0,1,1> (A8 GeGLU up-projection GEMM, paired W1|V tile, fused bias+GeLU-gate epilogue)",
                 "bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": (achieved / peak_tf) if achieved else None, "traffic": traffic,
                 "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside a long step)",

@@ -78,33 +78,41 @@ __device__ __forceinline__ void chunk_load(uint4 (&r)[4], const bf16* base, int6
     else r[i] = make_uint4(0, 0, 0, 0);
   }
 }
-__device__ __forceinline__ void chunk_to_scr(uint8_t* scr, const uint4 (&r)[4], int lane) {
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-    *reinterpret_cast<uint4*>(scr + ((lane >> 2) + 8 * i) * SCR_ROW + (lane & 3) * 16) = r[i];
+// explicit shared-window accesses (the scratch lives behind a 1024-aligned dynamic-smem pointer, so
+// plain C++ dereferences would compile to generic LD.E/ST.E)
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 r;
+  asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a));
+  return r;
 }
-__device__ __forceinline__ void scr_row_read(const uint8_t* scr, int lane, float* v) {
-#pragma unroll
-  for (int j = 0; j < 4; ++j) bf16x8_to_f32(*reinterpret_cast<const uint4*>(scr + lane * SCR_ROW + j * 16), v + 8 * j);
+__device__ __forceinline__ void sts128(uint32_t a, const uint4& v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
-__device__ __forceinline__ void scr_row_write(uint8_t* scr, int lane, const float* v) {
+__device__ __forceinline__ void chunk_to_scr(uint32_t scr, const uint4 (&r)[4], int lane) {
 #pragma unroll
-  for (int j = 0; j < 4; ++j) *reinterpret_cast<uint4*>(scr + lane * SCR_ROW + j * 16) = f32_to_bf16x8(v + 8 * j);
+  for (int i = 0; i < 4; ++i) sts128(scr + ((lane >> 2) + 8 * i) * SCR_ROW + (lane & 3) * 16, r[i]);
 }
-__device__ __forceinline__ void scr_to_global(const uint8_t* scr, bf16* base, int64_t ld, int row0, int M, int col,
-                                              int N, int lane) {
+__device__ __forceinline__ void scr_row_read(uint32_t scr, int lane, float* v) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) bf16x8_to_f32(lds128(scr + lane * SCR_ROW + j * 16), v + 8 * j);
+}
+__device__ __forceinline__ void scr_row_write(uint32_t scr, int lane, const float* v) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) sts128(scr + lane * SCR_ROW + j * 16, f32_to_bf16x8(v + 8 * j));
+}
+__device__ __forceinline__ void scr_to_global(uint32_t scr, bf16* base, int64_t ld, int row0, int M, int col, int N,
+                                              int lane) {
   const int c = col + (lane & 3) * 8;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int rr = (lane >> 2) + 8 * i;
     const int row = row0 + rr;
-    if (row < M && c < N)
-      *reinterpret_cast<uint4*>(base + (int64_t)row * ld + c) =
-          *reinterpret_cast<const uint4*>(scr + rr * SCR_ROW + (lane & 3) * 16);
+    const uint4 v = lds128(scr + rr * SCR_ROW + (lane & 3) * 16);
+    if (row < M && c < N) *reinterpret_cast<uint4*>(base + (int64_t)row * ld + c) = v;
   }
 }
 // row-wise values of this lane -> scratch -> coalesced global store
-__device__ __forceinline__ void emit_chunk(uint8_t* scr, const float* v, bf16* base, int64_t ld, int row0, int M,
+__device__ __forceinline__ void emit_chunk(uint32_t scr, const float* v, bf16* base, int64_t ld, int row0, int M,
                                            int col, int N, int lane) {
   scr_row_write(scr, lane, v);
   __syncwarp();
@@ -112,13 +120,13 @@ __device__ __forceinline__ void emit_chunk(uint8_t* scr, const float* v, bf16* b
   __syncwarp();
 }
 
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sm100::smem_u32(smem_dst)), "l"(gsrc) : "memory");
+__device__ __forceinline__ void cp_async16(uint32_t smem_dst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_dst), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-__device__ __forceinline__ void load_bias32_smem(const uint8_t* sb, float* v) {
+__device__ __forceinline__ void load_bias32_smem(uint32_t sb, float* v) {
 #pragma unroll
-  for (int g = 0; g < 4; ++g) bf16x8_to_f32(*reinterpret_cast<const uint4*>(sb + g * 16), v + g * 8);
+  for (int g = 0; g < 4; ++g) bf16x8_to_f32(lds128(sb + g * 16), v + g * 8);
 }
 
 // per-warp transpose-reduce: lane l ends with the sum over the warp's 32 rows of column l of v[32]
@@ -249,8 +257,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int ew = warp - 4;
     const int q = warp & 3;     // TMEM lane quarter this warp may access
     const int grp = ew >> 2;    // which half of the tile's columns
-    uint8_t* scrA = scr_base + ew * NSCR * SCR_BYTES;
-    uint8_t* scrB = scrA + (NSCR > 1 ? SCR_BYTES : 0);
+    const uint32_t scrA = sm100::smem_u32(scr_base) + ew * NSCR * SCR_BYTES;
+    const uint32_t scrB = scrA + (NSCR > 1 ? SCR_BYTES : 0);
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < sc.total; u += gridDim.x) {
@@ -261,7 +269,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const bool row_ok = row < M;
       // stage this tile's bias slice in smem (async, overlapped with the MMA of the tile): L1 is
       // nearly all carved out for the operand ring, so per-chunk bias reads would go to L2
-      uint8_t* sbias = bias_base + ew * 256;
+      const uint32_t sbias = sm100::smem_u32(bias_base) + ew * 256;
       if (ep.bias && lane < 16) {
         if (PAIRED) {
           const int c = lane >> 3, t = (lane >> 2) & 1, seg = lane & 3;
@@ -372,8 +380,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               float a[16], g[16];
 #pragma unroll
               for (int j = 0; j < 2; ++j) {
-                bf16x8_to_f32(*reinterpret_cast<const uint4*>(scrA + lane * SCR_ROW + (2 * h + j) * 16), a + 8 * j);
-                bf16x8_to_f32(*reinterpret_cast<const uint4*>(scrB + lane * SCR_ROW + (2 * h + j) * 16), g + 8 * j);
+                bf16x8_to_f32(lds128(scrA + lane * SCR_ROW + (2 * h + j) * 16), a + 8 * j);
+                bf16x8_to_f32(lds128(scrB + lane * SCR_ROW + (2 * h + j) * 16), g + 8 * j);
               }
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
@@ -383,8 +391,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               }
 #pragma unroll
               for (int j = 0; j < 2; ++j) {
-                *reinterpret_cast<uint4*>(scrA + lane * SCR_ROW + (2 * h + j) * 16) = f32_to_bf16x8(a + 8 * j);
-                *reinterpret_cast<uint4*>(scrB + lane * SCR_ROW + (2 * h + j) * 16) = f32_to_bf16x8(g + 8 * j);
+                sts128(scrA + lane * SCR_ROW + (2 * h + j) * 16, f32_to_bf16x8(a + 8 * j));
+                sts128(scrB + lane * SCR_ROW + (2 * h + j) * 16, f32_to_bf16x8(g + 8 * j));
               }
             }
             __syncwarp();
@@ -452,6 +460,235 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   sm100::tc_fence_after();
   if (warp == 2) sm100::tmem_dealloc(tmem_base, C::TMEM_COLS);
 }
+
+
+// ------------------------------------------------------------------------------------------------
+// GeGLU backward (A8 bwd, epilogue E4) as a dedicated kernel with asynchronous epilogue I/O:
+//   dZ = dF W2 (tcgen05, never stored);  dU = dZ * Gd,  Gd = [g GeLU'(a) | GeLU(a)] saved by the
+//   forward;  db_1v += column sums of dU.
+// The tile is 128 rows x 128 columns of dZ.  The producer warp TMA-loads the tile's Gd slice
+// ([128 x 128] of each half, 64 KB) into one of two smem slots while the tile's MMAs run; the 8
+// epilogue warps multiply in place (swizzled layout) and the tile leaves by TMA stores, so the
+// kernel streams Gd in / dU out at HBM rate with no per-thread global accesses.
+// ------------------------------------------------------------------------------------------------
+constexpr int GB_BN = 128, GB_STAGES = 3;
+constexpr int GB_STAGE_BYTES = BM * BK * 2 + GB_BN * BK * 2;  // 32 KB
+constexpr int GB_SLOT_BYTES = 4 * 128 * 128;                  // 4 boxes of 128 rows x 64 cols bf16 (64 KB)
+constexpr int GB_SMEM = GB_STAGES * GB_STAGE_BYTES + 2 * GB_SLOT_BYTES + 1024 + 256;
+
+__global__ void __launch_bounds__(NTHREADS, 1)
+    geglu_bwd_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmGd, const __grid_constant__ CUtensorMap tmDU, int M, int I,
+                     Sched sc, float* __restrict__ dbias) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* slots = smem + GB_STAGES * GB_STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(slots + 2 * GB_SLOT_BYTES);
+  uint64_t* empty = full + GB_STAGES;
+  uint64_t* tfull = empty + GB_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* gfull = tempty + 2;   // [2] Gd slice landed
+  uint64_t* gempty = gfull + 2;   // [2] slot free (2 arrivals: one per epilogue group)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch(&tmA);
+    sm100::tma_prefetch(&tmB);
+    sm100::tma_prefetch(&tmGd);
+    sm100::tma_prefetch(&tmDU);
+    for (int i = 0; i < GB_STAGES; ++i) {
+      sm100::mbar_init(&full[i], 1);
+      sm100::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&tfull[i], 1);
+      sm100::mbar_init(&tempty[i], NUM_EPI_WARPS);
+      sm100::mbar_init(&gfull[i], 1);
+      sm100::mbar_init(&gempty[i], 2);
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 2) sm100::tmem_alloc(tmem_slot, 2 * GB_BN);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int u = blockIdx.x; u < sc.total; u += gridDim.x, ++it) {
+        int mb, nb, kb0, kb1;
+        sc.decode(u, mb, nb, kb0, kb1);
+        // the tile's Gd slice first, so it lands while the MMAs run
+        const int sl = it & 1;
+        sm100::mbar_wait(&gempty[sl], ((it >> 1) & 1) ^ 1);
+        uint8_t* slot = slots + sl * GB_SLOT_BYTES;
+        sm100::mbar_arrive_expect_tx(&gfull[sl], GB_SLOT_BYTES);
+#pragma unroll
+        for (int bx = 0; bx < 4; ++bx)
+          sm100::tma_load_2d(slot + bx * 16384, &tmGd, &gfull[sl], (bx >> 1) * I + nb * GB_BN + (bx & 1) * 64, mb * BM);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          sm100::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * GB_STAGE_BYTES;
+          uint8_t* sb = sa + BM * BK * 2;
+          sm100::mbar_arrive_expect_tx(&full[stage], GB_STAGE_BYTES);
+          const int k0 = kb * BK;
+          sm100::tma_load_2d(sa, &tmA, &full[stage], k0, mb * BM);
+#pragma unroll
+          for (int i = 0; i < GB_BN / 64; ++i)
+            sm100::tma_load_2d(sb + i * 8192, &tmB, &full[stage], nb * GB_BN + i * 64, k0);
+          if (++stage == GB_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = sm100::idesc_bf16(BM, GB_BN, 0, 1);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = blockIdx.x; u < sc.total; u += gridDim.x) {
+        int mb, nb, kb0, kb1;
+        sc.decode(u, mb, nb, kb0, kb1);
+        sm100::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        sm100::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * GB_BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          sm100::mbar_wait(&full[stage], phase);
+          sm100::tc_fence_after();
+          const uint32_t sa = sm100::smem_u32(smem + stage * GB_STAGE_BYTES);
+          const uint32_t sb = sa + BM * BK * 2;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            sm100::mma_bf16_ss(d_tmem, sm100::desc_kmajor_sw128(sa + k * 32),
+                               sm100::desc_mnmajor_sw128(sb + k * 2048, 8192), idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          sm100::mma_commit(&empty[stage]);
+          if (++stage == GB_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        sm100::mma_commit(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    const int q = warp & 3;   // TMEM lane quarter = rows [32q, 32q+32) of the tile
+    const int grp = ew >> 2;  // column half: dZ columns [64 grp, 64 grp + 64) of the tile
+    const int gtid = threadIdx.x - 128 - grp * 128;  // 0..127 within the group
+    const int r = q * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int it = 0;
+    for (int u = blockIdx.x; u < sc.total; u += gridDim.x, ++it) {
+      int mb, nb, kb0, kb1;
+      sc.decode(u, mb, nb, kb0, kb1);
+      const int sl = it & 1;
+      const uint32_t slot = sm100::smem_u32(slots + sl * GB_SLOT_BYTES);
+      const uint32_t box_a = slot + grp * 16384, box_g = slot + (2 + grp) * 16384;
+      sm100::mbar_wait(&gfull[sl], (it >> 1) & 1);
+      sm100::mbar_wait(&tfull[acc], acc_phase);
+      sm100::tc_fence_after();
+      const uint32_t tb = tmem_base + acc * GB_BN + ((uint32_t)(q * 32) << 16) + grp * 64;
+      float v[32], w[32];
+      sm100::tmem_ld32(tb, v);
+      sm100::tmem_ld32(tb + 32, w);
+      sm100::tmem_ld_wait();
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&tempty[acc]);  // accumulator drained: next tile's MMA may start
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+      // dU = dZ * Gd in place; row r, 16-byte chunks j = 0..7 of the 64-column box (swizzled).
+      // All 16 loads are issued before any store (the volatile shared accesses keep program order).
+      uint4 A[8], G[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t off = r * 128 + ((j ^ (r & 7)) << 4);
+        A[j] = lds128(box_a + off);
+        G[j] = lds128(box_g + off);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t off = r * 128 + ((j ^ (r & 7)) << 4);
+        const float* dz = j < 4 ? v + 8 * j : w + 8 * (j - 4);
+        float ga[8], gg[8];
+        bf16x8_to_f32(A[j], ga);
+        bf16x8_to_f32(G[j], gg);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          ga[e] *= dz[e];
+          gg[e] *= dz[e];
+        }
+        sts128(box_a + off, f32_to_bf16x8(ga));
+        sts128(box_g + off, f32_to_bf16x8(gg));
+      }
+      sm100::fence_proxy_async_smem();
+      sm100::named_bar(1 + grp, 128);
+      const int row0 = mb * BM;
+      if (gtid == 0) {
+        sm100::tma_store_2d(&tmDU, slots + sl * GB_SLOT_BYTES + grp * 16384, nb * GB_BN + grp * 64, row0);
+        sm100::tma_store_2d(&tmDU, slots + sl * GB_SLOT_BYTES + (2 + grp) * 16384, I + nb * GB_BN + grp * 64, row0);
+        sm100::bulk_commit();
+      }
+      // db_1v: column sums of the tile's dU.  Thread gtid covers box (gtid >> 6), 8-column chunk
+      // ((gtid >> 3) & 7) and rows [16 (gtid & 7), +16): 16 independent 16-byte loads, then a
+      // 3-step shuffle reduction over the 8 row blocks (consecutive lanes).
+      if (dbias) {
+        const uint32_t box = (gtid >> 6) ? box_g : box_a;
+        const int cj = (gtid >> 3) & 7, rb = gtid & 7;
+        const int rows = min(BM, M - row0);
+        float cs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int rr = rb * 16 + k;
+          float t[8];
+          bf16x8_to_f32(lds128(box + rr * 128 + ((cj ^ (rr & 7)) << 4)), t);
+          if (rr < rows) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) cs[e] += t[e];
+          }
+        }
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) cs[e] += __shfl_xor_sync(0xffffffffu, cs[e], o);
+        }
+        if (rb == 0) {
+          float* dst = dbias + ((gtid >> 6) ? I : 0) + nb * GB_BN + grp * 64 + cj * 8;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) atomicAdd(dst + e, cs[e]);
+        }
+      }
+      sm100::named_bar(1 + grp, 128);
+      if (gtid == 0) {
+        sm100::bulk_wait_read0();  // the stores have read the slot
+        sm100::mbar_arrive(&gempty[sl]);
+      }
+    }
+    if (gtid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  if (warp == 2) sm100::tmem_dealloc(tmem_base, 2 * GB_BN);
+}
+
 
 template <int BN, int STAGES, int A_MN, int B_MN, int PAIRED, int NSCR>
 mb_status launch(const GemmArgs& g, const CUtensorMap& ta, const CUtensorMap& tb, const Sched& sc, cudaStream_t s) {
@@ -523,8 +760,20 @@ mb_status gemm(const GemmArgs& g, cudaStream_t s) {
 
   if (paired) return launch<256, 4, 0, 0, 1, 1>(g, ta, tb, sc, s);
   if (geglu_bwd) {
-    if (g.a_t || !g.b_t) return MB_ERR_CONFIG;
-    return launch<128, 5, 0, 1, 0, 2>(g, ta, tb, sc, s);
+    if (g.a_t || !g.b_t || g.ep.I % GB_BN || g.ep.ldu != 2 * g.ep.I || g.ep.ldc != 2 * g.ep.I) return MB_ERR_CONFIG;
+    CUtensorMap tg, tdu;
+    MB_REQUIRE(make_tmap_bf16_2d(&tg, g.ep.U, 2 * g.ep.I, g.M, g.ep.ldu, 64, BM), MB_ERR_CUDA);
+    MB_REQUIRE(make_tmap_bf16_2d(&tdu, g.ep.C, 2 * g.ep.I, g.M, g.ep.ldc, 64, BM), MB_ERR_CUDA);
+    static bool attr_gb = false;
+    if (!attr_gb) {
+      if (cudaFuncSetAttribute(geglu_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GB_SMEM) != cudaSuccess)
+        return MB_ERR_CUDA;
+      attr_gb = true;
+    }
+    const int grid = std::max(1, std::min(sc.total, num_sms()));
+    geglu_bwd_kernel<<<grid, NTHREADS, GB_SMEM, s>>>(ta, tb, tg, tdu, g.M, g.ep.I, sc, g.ep.dbias);
+    MB_CHECK_LAUNCH();
+    return MB_OK;
   }
   if (BN == 256) return dispatch_majors<256, 4, 1>(g, ta, tb, sc, s);
   return dispatch_majors<128, 6, 1>(g, ta, tb, sc, s);
