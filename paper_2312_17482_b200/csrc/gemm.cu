@@ -27,10 +27,10 @@ constexpr int NTHREADS = 128 + 32 * NUM_EPI_WARPS;  // warps 0-3: TMA, MMA, TMEM
 constexpr int SCR_ROW = 80;                          // scratch row: 32 bf16 (64 B) + 16 B pad (conflict-free)
 constexpr int SCR_BYTES = 32 * SCR_ROW;
 
-template <int BN, int STAGES, int NSCR>
+template <int BN, int STAGES, int NSCR, int CG = 1>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = (BN / CG) * BK * 2;  // a CTA pair splits B's N between its two CTAs
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int DATA = STAGE_BYTES * STAGES;
   static constexpr int SCR = NUM_EPI_WARPS * NSCR * SCR_BYTES;
@@ -144,11 +144,15 @@ __device__ __forceinline__ float warp_colsum32(float* v, int lane) {
   return v[0];
 }
 
-template <int BN, int STAGES, int A_MN, int B_MN, int PAIRED, int NSCR>
+// CG = 2: the CTA pair of a 2-CTA cluster computes a 256 x BN tile with tcgen05.mma.cta_group::2
+// (M = 256): each CTA loads its 128 rows of A and its half of B's N (halving per-SM operand
+// ingest per FLOP), the pair leader (cluster rank 0) issues the MMAs, and each CTA's TMEM holds the
+// accumulator rows of its own half.
+template <int BN, int STAGES, int A_MN, int B_MN, int PAIRED, int NSCR, int CG>
 __global__ void __launch_bounds__(NTHREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                 Sched sc, Epi ep) {
-  using C = Cfg<BN, STAGES, NSCR>;
+  using C = Cfg<BN, STAGES, NSCR, CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* scr_base = smem + C::DATA;
@@ -161,6 +165,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const int rank = CG == 2 ? (int)sm100::cluster_ctarank() : 0;
+  const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;  // this CTA's cluster and the cluster count
 
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch(&tmA);
@@ -171,13 +177,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&tfull[i], 1);
-      sm100::mbar_init(&tempty[i], NUM_EPI_WARPS);
+      sm100::mbar_init(&tempty[i], NUM_EPI_WARPS * CG);
     }
     sm100::fence_barrier_init();
   }
-  if (warp == 2) sm100::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  if (warp == 2) {
+    if (CG == 2) sm100::tmem_alloc_pair(tmem_slot, C::TMEM_COLS);
+    else sm100::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  }
   sm100::tc_fence_before();
-  __syncthreads();
+  if (CG == 2) sm100::cluster_sync();
+  else __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -185,29 +195,38 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < sc.total; u += gridDim.x) {
+      for (int u = cid; u < sc.total; u += ncl) {
         int mb, nb, kb0, kb1;
         sc.decode(u, mb, nb, kb0, kb1);
+        const int m_cta = (mb * CG + rank) * BM;
         for (int kb = kb0; kb < kb1; ++kb) {
           sm100::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
           uint8_t* sb = sa + C::A_BYTES;
-          sm100::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          if (rank == 0) sm100::mbar_arrive_expect_tx(&full[stage], CG * C::STAGE_BYTES);
           const int k0 = kb * BK;
+          auto load = [&](void* dst, const CUtensorMap* m, int c0, int c1) {
+            if (CG == 2) sm100::tma_load_2d_pair(dst, m, &full[stage], c0, c1);
+            else sm100::tma_load_2d(dst, m, &full[stage], c0, c1);
+          };
           if (!A_MN) {
-            sm100::tma_load_2d(sa, &tmA, &full[stage], k0, mb * BM);
+            load(sa, &tmA, k0, m_cta);
           } else {
 #pragma unroll
-            for (int i = 0; i < BM / 64; ++i) sm100::tma_load_2d(sa + i * 8192, &tmA, &full[stage], mb * BM + i * 64, k0);
+            for (int i = 0; i < BM / 64; ++i) load(sa + i * 8192, &tmA, m_cta + i * 64, k0);
           }
           if (PAIRED) {
-            sm100::tma_load_2d(sb, &tmB, &full[stage], k0, nb * 128);
-            sm100::tma_load_2d(sb + 128 * 128, &tmB, &full[stage], k0, ep.I + nb * 128);
+            if (CG == 2) {
+              load(sb, &tmB, k0, rank * ep.I + nb * 128);  // leader: W1 rows (a), peer: V rows (g)
+            } else {
+              load(sb, &tmB, k0, nb * 128);
+              load(sb + 128 * 128, &tmB, k0, ep.I + nb * 128);
+            }
           } else if (!B_MN) {
-            sm100::tma_load_2d(sb, &tmB, &full[stage], k0, nb * BN);
+            load(sb, &tmB, k0, nb * BN + rank * (BN / CG));
           } else {
 #pragma unroll
-            for (int i = 0; i < BN / 64; ++i) sm100::tma_load_2d(sb + i * 8192, &tmB, &full[stage], nb * BN + i * 64, k0);
+            for (int i = 0; i < BN / CG / 64; ++i) load(sb + i * 8192, &tmB, nb * BN + rank * (BN / CG) + i * 64, k0);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -217,13 +236,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = sm100::idesc_bf16(BM, BN, A_MN, B_MN);
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = sm100::idesc_bf16(BM * CG, BN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int u = blockIdx.x; u < sc.total; u += gridDim.x) {
+      for (int u = cid; u < sc.total; u += ncl) {
         int mb, nb, kb0, kb1;
         sc.decode(u, mb, nb, kb0, kb1);
         sm100::mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -238,15 +257,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t ad = A_MN ? sm100::desc_mnmajor_sw128(sa + k * 2048, 8192) : sm100::desc_kmajor_sw128(sa + k * 32);
             const uint64_t bd = B_MN ? sm100::desc_mnmajor_sw128(sb + k * 2048, 8192) : sm100::desc_kmajor_sw128(sb + k * 32);
-            sm100::mma_bf16_ss(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            if (CG == 2) sm100::mma_bf16_ss_pair(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            else sm100::mma_bf16_ss(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
-          sm100::mma_commit(&empty[stage]);
+          if (CG == 2) sm100::mma_commit_pair(&empty[stage]);
+          else sm100::mma_commit(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        sm100::mma_commit(&tfull[acc]);
+        if (CG == 2) sm100::mma_commit_pair(&tfull[acc]);
+        else sm100::mma_commit(&tfull[acc]);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -261,10 +283,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const uint32_t scrB = scrA + (NSCR > 1 ? SCR_BYTES : 0);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = blockIdx.x; u < sc.total; u += gridDim.x) {
+    for (int u = cid; u < sc.total; u += ncl) {
       int mb, nb, kb0, kb1;
       sc.decode(u, mb, nb, kb0, kb1);
-      const int row0 = mb * BM + q * 32;
+      const int row0 = (mb * CG + rank) * BM + q * 32;
       const int row = row0 + lane;
       const bool row_ok = row < M;
       // stage this tile's bias slice in smem (async, overlapped with the MMA of the tile): L1 is
@@ -448,7 +470,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       sm100::tc_fence_before();
       __syncwarp();
-      if (lane == 0) sm100::mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if (CG == 2) sm100::mbar_arrive_leader(&tempty[acc]);
+        else sm100::mbar_arrive(&tempty[acc]);
+      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -456,9 +481,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
   }
   sm100::tc_fence_before();
-  __syncthreads();
+  if (CG == 2) sm100::cluster_sync();
+  else __syncthreads();
   sm100::tc_fence_after();
-  if (warp == 2) sm100::tmem_dealloc(tmem_base, C::TMEM_COLS);
+  if (warp == 2) {
+    if (CG == 2) sm100::tmem_dealloc_pair(tmem_base, C::TMEM_COLS);
+    else sm100::tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
 }
 
 
@@ -690,18 +719,30 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 }
 
 
-template <int BN, int STAGES, int A_MN, int B_MN, int PAIRED, int NSCR>
+template <int BN, int STAGES, int A_MN, int B_MN, int PAIRED, int NSCR, int CG = 2>
 mb_status launch(const GemmArgs& g, const CUtensorMap& ta, const CUtensorMap& tb, const Sched& sc, cudaStream_t s) {
-  using C = Cfg<BN, STAGES, NSCR>;
-  auto k = gemm_kernel<BN, STAGES, A_MN, B_MN, PAIRED, NSCR>;
+  using C = Cfg<BN, STAGES, NSCR, CG>;
+  auto k = gemm_kernel<BN, STAGES, A_MN, B_MN, PAIRED, NSCR, CG>;
   static bool attr_set = false;  // benign race: idempotent
   if (!attr_set) {
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) != cudaSuccess)
       return MB_ERR_CUDA;
     attr_set = true;
   }
-  const int grid = std::max(1, std::min(sc.total, num_sms()));
-  k<<<grid, NTHREADS, C::SMEM, s>>>(ta, tb, g.M, g.N, sc, g.ep);
+  const int clusters = std::max(1, std::min(sc.total, num_sms() / CG));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(clusters * CG);
+  cfg.blockDim = dim3(NTHREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, k, ta, tb, g.M, g.N, sc, g.ep) != cudaSuccess) return MB_ERR_CUDA;
   MB_CHECK_LAUNCH();
   return MB_OK;
 }
@@ -732,18 +773,20 @@ mb_status gemm(const GemmArgs& g, cudaStream_t s) {
   // W1 + the matching 128 of V).
   const bool geglu_bwd = g.ep.mode == E_GEGLU_BWD;
   const int BN = paired ? 256 : ((g.N <= 128 || geglu_bwd) ? 128 : 256);
+  // CG = 2 (generic kernel): pair tiles of 256 rows; each CTA loads 128 rows of A and BN/2 of B's N.
+  constexpr int CGV = 2;
   CUtensorMap ta, tb;
   bool ok;
   if (!g.a_t) ok = make_tmap_bf16_2d(&ta, g.A, g.K, g.M, g.lda, BK, BM);
   else ok = make_tmap_bf16_2d(&ta, g.A, g.M, g.K, g.lda, 64, BK);
   MB_REQUIRE(ok, MB_ERR_CUDA);
   if (paired) ok = make_tmap_bf16_2d(&tb, g.B, g.K, g.N, g.ldb, BK, 128);
-  else if (!g.b_t) ok = make_tmap_bf16_2d(&tb, g.B, g.K, g.N, g.ldb, BK, BN);
+  else if (!g.b_t) ok = make_tmap_bf16_2d(&tb, g.B, g.K, g.N, g.ldb, BK, geglu_bwd ? BN : BN / CGV);
   else ok = make_tmap_bf16_2d(&tb, g.B, g.N, g.K, g.ldb, 64, BK);
   MB_REQUIRE(ok, MB_ERR_CUDA);
 
   Sched sc;
-  sc.num_m = (g.M + BM - 1) / BM;
+  sc.num_m = (g.M + (geglu_bwd ? BM : BM * CGV) - 1) / (geglu_bwd ? BM : BM * CGV);
   sc.num_n = paired ? g.ep.I / 128 : (g.N + BN - 1) / BN;
   sc.nkb = (g.K + BK - 1) / BK;
   int splits = 1;
@@ -751,14 +794,14 @@ mb_status gemm(const GemmArgs& g, cudaStream_t s) {
     // split-K for the weight gradients (few output tiles, K = tokens): aim for >= 2 waves while
     // keeping >= 8 k-blocks per split; partial sums meet in fp32 atomics (the += contract).
     const int tiles = sc.num_m * sc.num_n;
-    const int want = (2 * num_sms() + tiles - 1) / tiles;
+    const int want = (2 * (num_sms() / CGV) + tiles - 1) / tiles;
     splits = std::max(1, std::min(want, sc.nkb / 8));
   }
   sc.kb_per = (sc.nkb + splits - 1) / splits;
   sc.splits = (sc.nkb + sc.kb_per - 1) / sc.kb_per;
   sc.total = sc.num_m * sc.num_n * sc.splits;
 
-  if (paired) return launch<256, 4, 0, 0, 1, 1>(g, ta, tb, sc, s);
+  if (paired) return launch<256, 6, 0, 0, 1, 1>(g, ta, tb, sc, s);
   if (geglu_bwd) {
     if (g.a_t || !g.b_t || g.ep.I % GB_BN || g.ep.ldu != 2 * g.ep.I || g.ep.ldc != 2 * g.ep.I) return MB_ERR_CONFIG;
     CUtensorMap tg, tdu;
@@ -775,8 +818,8 @@ mb_status gemm(const GemmArgs& g, cudaStream_t s) {
     MB_CHECK_LAUNCH();
     return MB_OK;
   }
-  if (BN == 256) return dispatch_majors<256, 4, 1>(g, ta, tb, sc, s);
-  return dispatch_majors<128, 6, 1>(g, ta, tb, sc, s);
+  if (BN == 256) return dispatch_majors<256, 6, 1>(g, ta, tb, sc, s);
+  return dispatch_majors<128, 8, 1>(g, ta, tb, sc, s);
 }
 
 }  // namespace mb
