@@ -73,12 +73,31 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
                : "memory");
 }
 
-// exact-erf GeLU (reading R7) and its derivative Phi(x) + x phi(x)
-__device__ __forceinline__ float gelu_f(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
+// Standard-normal cdf Phi(x) and pdf phi(x) sharing one exponential: Phi(x) = 0.5 (1 + erf(x/sqrt2))
+// with erf from Abramowitz & Stegun 7.1.26 (|error| <= 1.5e-7, far below bf16 resolution):
+//   erf(z) = 1 - t (a1 + t (a2 + t (a3 + t (a4 + t a5)))) e^{-z^2},  t = 1 / (1 + p z),  z >= 0,
+// and e^{-z^2} = e^{-x^2/2} is exactly the exponential of phi.  GeLU(x) = x Phi(x) is the exact-erf
+// GeLU (reading R7) to fp32 accuracy; GeLU'(x) = Phi(x) + x phi(x).
+__device__ __forceinline__ void norm_cdf_pdf(float x, float& cdf, float& pdf) {
+  const float e = exp2f(-0.72134752044448170f * x * x);  // e^{-x^2/2}
+  const float t = __fdividef(1.0f, fmaf(0.2316418882663604f, fabsf(x), 1.0f));  // p / sqrt2
+  float q = fmaf(t, 0.5307027145f, -0.7265760135f);  // halved a5, a4 (0.5 folded in)
+  q = fmaf(t, q, 0.7107068705f);
+  q = fmaf(t, q, -0.1422483680f);
+  q = fmaf(t, q, 0.1274147960f);
+  q = q * t * e;  // = 0.5 (1 - erf(|x|/sqrt2))
+  cdf = x >= 0.f ? 1.0f - q : q;
+  pdf = 0.3989422804014327f * e;
+}
+__device__ __forceinline__ float gelu_f(float x) {
+  float c, p;
+  norm_cdf_pdf(x, c, p);
+  return x * c;
+}
 __device__ __forceinline__ float gelu_grad_f(float x) {
-  const float cdf = 0.5f * (1.0f + erff(x * 0.70710678118654752f));
-  const float pdf = 0.3989422804014327f * __expf(-0.5f * x * x);
-  return cdf + x * pdf;
+  float c, p;
+  norm_cdf_pdf(x, c, p);
+  return c + x * p;
 }
 
 int num_sms();  // cached per device (host)

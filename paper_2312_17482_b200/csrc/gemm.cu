@@ -343,8 +343,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const float x = v[j];
-            const float cdf = 0.5f + 0.5f * erff(x * 0.70710678118654752f);
-            const float pdf = 0.3989422804014327f * __expf(-0.5f * x * x);
+            float cdf, pdf;
+            norm_cdf_pdf(x, cdf, pdf);
             const float ge = x * cdf;
             z[j] = ge * g[j];
             v[j] = g[j] * (cdf + x * pdf);
