@@ -141,6 +141,14 @@ MB_API mb_status mb_gemm(int32_t M, int32_t N, int32_t K, const mb_bf16* A, int6
                   int64_t ldb, int32_t b_t, void* C, int64_t ldc, int32_t epilogue, const mb_bf16* bias,
                   const mb_bf16* residual, int64_t ldr, mb_bf16* aux, int64_t ldaux, mb_stream_t s);
 
+/* Weight gradient with fused bias gradient (the bias of y = x W^T + b has db = sum over rows of dY):
+ *   dW[M,N] += dY^T X   with dY [K, M] (lda), X [K, N] (ldb) row-major bf16, dW fp32 (ldc), and
+ *   db[M] += sum_k dY[k, m]  (if db != NULL), computed on the tensor cores from the dY tiles the GEMM
+ *   already stages (an extra N = 16 MMA against an all-ones tile).  Split-K partials meet in fp32
+ *   atomics (+= contract). */
+MB_API mb_status mb_gemm_wgrad(int32_t M, int32_t N, int32_t K, const mb_bf16* dY, int64_t lda, const mb_bf16* X,
+                               int64_t ldb, float* dW, int64_t ldc, float* db, mb_stream_t s);
+
 /* A8 — fused GLU up-projection with the GeGLU epilogue (Eq. 2; fused W1||V):
  *   U = X W_1v^T + b_1v  ([n, 2I]; first I outputs = W1 half "a", last I = V half "g", reading R8)
  *   Z = GeLU(a) * g      ([n, I], written)

@@ -60,6 +60,7 @@ _SIGS = {
     "mb_layernorm_forward": (C.c_int, [P, P, P, I32, I32, F32, P, P, P]),
     "mb_layernorm_backward": (C.c_int, [P, P, P, P, I32, I32, P, P, P, P, P, P]),
     "mb_gemm": (C.c_int, [I32, I32, I32, P, I64, I32, P, I64, I32, P, I64, I32, P, P, I64, P, I64, P]),
+    "mb_gemm_wgrad": (C.c_int, [I32, I32, I32, P, I64, P, I64, P, I64, P, P]),
     "mb_geglu_forward": (C.c_int, [P, I32, I32, I32, P, P, P, P, P]),
     "mb_geglu_backward": (C.c_int, [P, I32, I32, I32, P, P, P, P]),
     "mb_attention_forward": (C.c_int, [P, P, I32, I32, I32, I32, I32, P, P, P, P]),
@@ -211,6 +212,11 @@ def gemm(M, N, K, A, lda, a_t, B, ldb, b_t, Cout, ldc, epilogue=EPI_BF16, bias=N
     _ck("mb_gemm", lib().mb_gemm(M, N, K, _p(A), lda, int(a_t), _p(B), ldb, int(b_t), _p(Cout), ldc, epilogue,
                                  _p(bias), _p(residual), ldr, _p(aux), ldaux, _stream()))
     return Cout
+
+
+def gemm_wgrad(M, N, K, dY, lda, X, ldb, dW, ldc, db=None):
+    _ck("mb_gemm_wgrad", lib().mb_gemm_wgrad(M, N, K, _p(dY), lda, _p(X), ldb, _p(dW), ldc, _p(db), _stream()))
+    return dW
 
 
 def geglu_forward(X, w_1v, b_1v, Gd, Z):

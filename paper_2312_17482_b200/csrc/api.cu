@@ -156,14 +156,14 @@ mb_status mb_encoder_backward(const mb_dims* d, const mb_layer_params* p, const 
   Saved sv(reinterpret_cast<char*>(const_cast<void*>(saved)), T, H, I, nh);
   Ws w(reinterpret_cast<char*>(ws), T, H, I, nh, pk->max_seqlen);
   if (ws_bytes < w.bytes) return MB_ERR_WORKSPACE;
-  // LN2 backward: dS2; dgamma2, dbeta2; db2 = sum dS2
+  // LN2 backward: dS2; dgamma2, dbeta2; db2 = column sums of dS2 (same pass)
   TRY(layernorm_bwd(reinterpret_cast<bf16*>(dy), sv.s2, sv.st2, B(p->ln2_g), T, H, nullptr, w.ds2, g->ln2_g,
                     g->ln2_b, g->b_2, s));
   {  // dZ = dS2 W2 fused with the GeGLU backward -> dU = dZ * Gd = [dZ g GeLU'(a) | dZ GeLU(a)]
     GemmArgs a;
     a.M = T, a.N = I, a.K = H, a.A = w.ds2, a.lda = H, a.B = B(p->w_2), a.ldb = I, a.b_t = true;
     a.ep.mode = E_GEGLU_BWD, a.ep.C = w.du, a.ep.ldc = 2 * I, a.ep.U = sv.u, a.ep.ldu = 2 * I, a.ep.I = I;
-    a.ep.dbias = g->b_1v;  // db1v = column sums of dU, fused into the epilogue
+    a.ep.dbias = g->b_1v;  // db1v = column sums of dU, from the smem tile before its TMA store
     TRY(gemm(a, s));
   }
   {  // dW2 += dS2^T Z
@@ -184,7 +184,7 @@ mb_status mb_encoder_backward(const mb_dims* d, const mb_layer_params* p, const 
     a.ep.mode = E_F32_ACC, a.ep.C = g->w_1v, a.ep.ldc = H;
     TRY(gemm(a, s));
   }
-  // LN1 backward: dS1; dgamma1, dbeta1; dbo = sum dS1
+  // LN1 backward: dS1; dgamma1, dbeta1; dbo = column sums of dS1 (same pass)
   TRY(layernorm_bwd(w.dy1, sv.s1, sv.st1, B(p->ln1_g), T, H, nullptr, w.ds1, g->ln1_g, g->ln1_b, g->b_o, s));
   {  // dO = dS1 Wo
     GemmArgs a;

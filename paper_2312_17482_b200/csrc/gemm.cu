@@ -27,7 +27,7 @@ constexpr int NTHREADS = 128 + 32 * NUM_EPI_WARPS;  // warps 0-3: TMA, MMA, TMEM
 constexpr int SCR_ROW = 80;                          // scratch row: 32 bf16 (64 B) + 16 B pad (conflict-free)
 constexpr int SCR_BYTES = 32 * SCR_ROW;
 
-template <int BN, int STAGES, int NSCR, int CG = 1>
+template <int BN, int STAGES, int NSCR, int CG = 1, int ACC = 2>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = (BN / CG) * BK * 2;  // a CTA pair splits B's N between its two CTAs
@@ -35,8 +35,12 @@ struct Cfg {
   static constexpr int DATA = STAGE_BYTES * STAGES;
   static constexpr int SCR = NUM_EPI_WARPS * NSCR * SCR_BYTES;
   static constexpr int BIAS = NUM_EPI_WARPS * 256;  // per-warp staged bias slice of the current tile
-  static constexpr int SMEM = DATA + SCR + BIAS + 1024 + 256;
-  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int ONES = 2048;                  // all-ones K-major B tile (16 rows x 64) for db MMAs
+  static constexpr int SMEM = DATA + SCR + BIAS + ONES + 1024 + 256;
+  // ACC accumulator stages of BN columns (+ ACC x 16 columns of bias-gradient accumulators)
+  static constexpr int TMEM_NEED = ACC * BN + ACC * 16;
+  static constexpr int TMEM_COLS = TMEM_NEED <= 256 ? 256 : 512;
+  static constexpr int TMEM_DB = ACC * BN;  // first column of the db accumulators
 };
 
 struct Sched {
@@ -148,16 +152,20 @@ __device__ __forceinline__ float warp_colsum32(float* v, int lane) {
 // (M = 256): each CTA loads its 128 rows of A and its half of B's N (halving per-SM operand
 // ingest per FLOP), the pair leader (cluster rank 0) issues the MMAs, and each CTA's TMEM holds the
 // accumulator rows of its own half.
-template <int BN, int STAGES, int A_MN, int B_MN, int PAIRED, int NSCR, int CG>
+// ACC = 2 double-buffers the TMEM accumulator (epilogue of tile i overlaps the MMAs of tile i+1);
+// ACC = 1 is used by the weight-gradient GEMMs, whose tiles run hundreds of k-blocks per (cheap)
+// epilogue, to make room in TMEM for the bias-gradient accumulator.
+template <int BN, int STAGES, int A_MN, int B_MN, int PAIRED, int NSCR, int CG, int ACC>
 __global__ void __launch_bounds__(NTHREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                 Sched sc, Epi ep) {
-  using C = Cfg<BN, STAGES, NSCR, CG>;
+  using C = Cfg<BN, STAGES, NSCR, CG, ACC>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* scr_base = smem + C::DATA;
   uint8_t* bias_base = smem + C::DATA + C::SCR;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATA + C::SCR + C::BIAS);
+  uint8_t* ones = smem + C::DATA + C::SCR + C::BIAS;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATA + C::SCR + C::BIAS + C::ONES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -184,6 +192,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp == 2) {
     if (CG == 2) sm100::tmem_alloc_pair(tmem_slot, C::TMEM_COLS);
     else sm100::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  }
+  if (ACC == 1 && warp == 3) {  // bf16 1.0 everywhere (the swizzle of an all-ones tile is irrelevant)
+    for (int i = lane; i < C::ONES / 16; i += 32)
+      sts128(sm100::smem_u32(ones) + i * 16, make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u));
+    sm100::fence_proxy_async_smem();
   }
   sm100::tc_fence_before();
   if (CG == 2) sm100::cluster_sync();
@@ -248,6 +261,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         sm100::mbar_wait(&tempty[acc], acc_phase ^ 1);
         sm100::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
+        // bias gradient of a weight-gradient GEMM: db[m] = sum_k A[m, k] comes from the A tiles
+        // already in smem, as an extra N = 16 MMA against an all-ones B tile (only once per m-block)
+        const bool do_db = ACC == 1 && ep.dbias != nullptr && nb == 0;
+        constexpr uint32_t idesc_db = sm100::idesc_bf16(BM * CG, 16, A_MN, 0);
+        const uint32_t d_db = tmem_base + C::TMEM_DB + acc * 16;
+        const uint32_t s_ones = sm100::smem_u32(ones);
         for (int kb = kb0; kb < kb1; ++kb) {
           sm100::mbar_wait(&full[stage], phase);
           sm100::tc_fence_after();
@@ -259,6 +278,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const uint64_t bd = B_MN ? sm100::desc_mnmajor_sw128(sb + k * 2048, 8192) : sm100::desc_kmajor_sw128(sb + k * 32);
             if (CG == 2) sm100::mma_bf16_ss_pair(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
             else sm100::mma_bf16_ss(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            if (ACC == 1 && do_db) {
+              const uint64_t od = sm100::desc_kmajor_sw128(s_ones + k * 32);
+              if (CG == 2) sm100::mma_bf16_ss_pair(d_db, ad, od, idesc_db, (kb > kb0 || k > 0) ? 1u : 0u);
+              else sm100::mma_bf16_ss(d_db, ad, od, idesc_db, (kb > kb0 || k > 0) ? 1u : 0u);
+            }
           }
           if (CG == 2) sm100::mma_commit_pair(&empty[stage]);
           else sm100::mma_commit(&empty[stage]);
@@ -269,7 +293,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         if (CG == 2) sm100::mma_commit_pair(&tfull[acc]);
         else sm100::mma_commit(&tfull[acc]);
-        if (++acc == 2) {
+        if (++acc == ACC) {
           acc = 0;
           acc_phase ^= 1;
         }
@@ -365,6 +389,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           sm100::tmem_ld32(tb + crel, v);
           const int nv = min(32, N - col);
           if (ep.mode == E_F32_ACC) {
+            if (ACC == 1 && c == 0 && grp == 0 && ep.dbias && nb == 0) {
+              float dbv[16];
+              sm100::tmem_ld16(tmem_base + C::TMEM_DB + acc * 16 + ((uint32_t)(q * 32) << 16), dbv);
+              sm100::tmem_ld_wait();
+              if (row_ok) atomicAdd(ep.dbias + row, dbv[0]);
+            }
             sm100::tmem_ld_wait();
             if (row_ok) {
               float* dst = reinterpret_cast<float*>(ep.C) + (int64_t)row * ep.ldc + col;
@@ -474,7 +504,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (CG == 2) sm100::mbar_arrive_leader(&tempty[acc]);
         else sm100::mbar_arrive(&tempty[acc]);
       }
-      if (++acc == 2) {
+      if (++acc == ACC) {
         acc = 0;
         acc_phase ^= 1;
       }
@@ -719,10 +749,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 }
 
 
-template <int BN, int STAGES, int A_MN, int B_MN, int PAIRED, int NSCR, int CG = 2>
+template <int BN, int STAGES, int A_MN, int B_MN, int PAIRED, int NSCR, int CG = 2, int ACC = 2>
 mb_status launch(const GemmArgs& g, const CUtensorMap& ta, const CUtensorMap& tb, const Sched& sc, cudaStream_t s) {
-  using C = Cfg<BN, STAGES, NSCR, CG>;
-  auto k = gemm_kernel<BN, STAGES, A_MN, B_MN, PAIRED, NSCR, CG>;
+  using C = Cfg<BN, STAGES, NSCR, CG, ACC>;
+  auto k = gemm_kernel<BN, STAGES, A_MN, B_MN, PAIRED, NSCR, CG, ACC>;
   static bool attr_set = false;  // benign race: idempotent
   if (!attr_set) {
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) != cudaSuccess)
@@ -818,6 +848,11 @@ mb_status gemm(const GemmArgs& g, cudaStream_t s) {
     MB_CHECK_LAUNCH();
     return MB_OK;
   }
+  if (g.ep.mode == E_F32_ACC && g.a_t && g.b_t && g.ep.dbias) {  // wgrad + fused db: 1 accumulator
+    if (BN == 256) return launch<256, 6, 1, 1, 0, 1, 2, 1>(g, ta, tb, sc, s);
+    return launch<128, 8, 1, 1, 0, 1, 2, 1>(g, ta, tb, sc, s);
+  }
+  MB_REQUIRE(g.ep.dbias == nullptr, MB_ERR_INVALID_ARG);
   if (BN == 256) return dispatch_majors<256, 6, 1>(g, ta, tb, sc, s);
   return dispatch_majors<128, 8, 1>(g, ta, tb, sc, s);
 }
@@ -843,6 +878,17 @@ extern "C" mb_status mb_gemm(int32_t M, int32_t N, int32_t K, const mb_bf16* A, 
   g.ep.bias = reinterpret_cast<const bf16*>(bias);
   g.ep.res = reinterpret_cast<const bf16*>(residual), g.ep.ldr = ldr;
   g.ep.aux = reinterpret_cast<bf16*>(aux), g.ep.ldaux = ldaux;
+  return mb::gemm(g, reinterpret_cast<cudaStream_t>(s));
+}
+
+extern "C" mb_status mb_gemm_wgrad(int32_t M, int32_t N, int32_t K, const mb_bf16* dY, int64_t lda, const mb_bf16* X,
+                                   int64_t ldb, float* dW, int64_t ldc, float* db, mb_stream_t s) {
+  MB_REQUIRE(dY && X && dW, MB_ERR_INVALID_ARG);
+  mb::GemmArgs g;
+  g.M = M, g.N = N, g.K = K;
+  g.A = reinterpret_cast<const bf16*>(dY), g.lda = lda, g.a_t = true;
+  g.B = reinterpret_cast<const bf16*>(X), g.ldb = ldb, g.b_t = true;
+  g.ep.mode = mb::E_F32_ACC, g.ep.C = dW, g.ep.ldc = ldc, g.ep.dbias = db;
   return mb::gemm(g, reinterpret_cast<cudaStream_t>(s));
 }
 

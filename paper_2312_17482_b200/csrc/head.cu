@@ -189,7 +189,6 @@ mb_status mb_mlm_loss(const mb_dims* d, const mb_head_params* p, const mb_bf16* 
   sum_kernel<<<1, 1024, 0, s>>>(w.row_loss, n, inv_norm, loss_sum);
   MB_CHECK_LAUNCH();
   // backward
-  TRY(colsum(w.dz, n, V, g->b_dec, s));
   {
     GemmArgs a;  // du = dz E   (E [V, H] = [K, N])
     a.M = n, a.N = H, a.K = V, a.A = w.dz, a.lda = V, a.B = B(p->emb), a.ldb = H, a.b_t = true;
@@ -200,6 +199,7 @@ mb_status mb_mlm_loss(const mb_dims* d, const mb_head_params* p, const mb_bf16* 
     GemmArgs a;  // dE += dz^T u
     a.M = V, a.N = H, a.K = n, a.A = w.dz, a.lda = V, a.a_t = true, a.B = w.u, a.ldb = H, a.b_t = true;
     a.ep.mode = E_F32_ACC, a.ep.C = g->emb, a.ep.ldc = H;
+    a.ep.dbias = g->b_dec;  // db_dec = column sums of dz, from the A tiles of this GEMM
     TRY(gemm(a, s));
   }
   // LN_h backward fused with the GeLU' of the transform: du -> dt_pre (in place); db_t = sum dt_pre

@@ -116,7 +116,7 @@ __device__ __forceinline__ void cta_column_reduce(const float* acc, float* sbuf,
   }
 }
 
-template <int VPL, bool EMBED, bool GELU>
+template <int VPL, bool EMBED, bool GELU, bool DSUM>
 __global__ void __launch_bounds__(LN_THREADS, VPL <= 3 ? 2 : 1)
     ln_bwd_kernel(RowSrc src, const bf16* __restrict__ dy, const float* __restrict__ stats,
                   const bf16* __restrict__ gamma, const bf16* __restrict__ gelu_pre, int n, int H, bf16* dx,
@@ -126,9 +126,12 @@ __global__ void __launch_bounds__(LN_THREADS, VPL <= 3 ? 2 : 1)
   // accumulators stay live; dy and gamma are re-read (L1 hits) in the second pass.
   extern __shared__ float sbuf[];
   const int lane = threadIdx.x & 31;
-  float acc_g[VPL * 8], acc_b[VPL * 8], acc_s[VPL * 8];
+  float acc_g[VPL * 8], acc_b[VPL * 8], acc_s[DSUM ? VPL * 8 : 1];
 #pragma unroll
-  for (int i = 0; i < VPL * 8; ++i) acc_g[i] = acc_b[i] = acc_s[i] = 0.f;
+  for (int i = 0; i < VPL * 8; ++i) {
+    acc_g[i] = acc_b[i] = 0.f;
+    if (DSUM) acc_s[i] = 0.f;
+  }
   for (int row = blockIdx.x * LN_WARPS + (threadIdx.x >> 5); row < n; row += gridDim.x * LN_WARPS) {
     float v[VPL * 8];
     int id = 0;
@@ -173,8 +176,10 @@ __global__ void __launch_bounds__(LN_THREADS, VPL <= 3 ? 2 : 1)
 #pragma unroll
           for (int j = 0; j < 8; ++j) o[j] *= gelu_grad_f(p[j]);
         }
+        if (DSUM) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc_s[i * 8 + j] += o[j];
+          for (int j = 0; j < 8; ++j) acc_s[i * 8 + j] += o[j];
+        }
         if (EMBED) {
           float* dst = d_emb + (size_t)id * H + c;
           red_add_v4(dst, o[0], o[1], o[2], o[3]);
@@ -187,7 +192,7 @@ __global__ void __launch_bounds__(LN_THREADS, VPL <= 3 ? 2 : 1)
   }
   cta_column_reduce<VPL>(acc_g, sbuf, H, dgamma);
   cta_column_reduce<VPL>(acc_b, sbuf, H, dbeta);
-  if (dsum) cta_column_reduce<VPL>(acc_s, sbuf, H, dsum);
+  if (DSUM) cta_column_reduce<VPL>(acc_s, sbuf, H, dsum);
 }
 
 // out[c] += sum_r x[r, c]; thread = one 8-column vector, blockIdx.y = row chunk
@@ -230,12 +235,18 @@ mb_status ln_bwd_launch(const RowSrc& src, const bf16* dy, const float* stats, c
                         float* dsum, cudaStream_t s) {
   const int smem = LN_WARPS * H * sizeof(float);
   const int grid = std::max(1, std::min((n + LN_WARPS - 1) / LN_WARPS, (VPL <= 3 ? 2 : 1) * num_sms()));
-  if (gelu_pre)
-    ln_bwd_kernel<VPL, EMBED, true><<<grid, LN_THREADS, smem, s>>>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb,
-                                                                    dg, db, dsum);
+  if (gelu_pre && dsum)
+    ln_bwd_kernel<VPL, EMBED, true, true><<<grid, LN_THREADS, smem, s>>>(src, dy, stats, gamma, gelu_pre, n, H, dx,
+                                                                          d_emb, dg, db, dsum);
+  else if (gelu_pre)
+    ln_bwd_kernel<VPL, EMBED, true, false><<<grid, LN_THREADS, smem, s>>>(src, dy, stats, gamma, gelu_pre, n, H, dx,
+                                                                           d_emb, dg, db, dsum);
+  else if (dsum)
+    ln_bwd_kernel<VPL, EMBED, false, true><<<grid, LN_THREADS, smem, s>>>(src, dy, stats, gamma, gelu_pre, n, H,
+                                                                           dx, d_emb, dg, db, dsum);
   else
-    ln_bwd_kernel<VPL, EMBED, false><<<grid, LN_THREADS, smem, s>>>(src, dy, stats, gamma, gelu_pre, n, H, dx,
-                                                                     d_emb, dg, db, dsum);
+    ln_bwd_kernel<VPL, EMBED, false, false><<<grid, LN_THREADS, smem, s>>>(src, dy, stats, gamma, gelu_pre, n, H,
+                                                                            dx, d_emb, dg, db, dsum);
   MB_CHECK_LAUNCH();
   return MB_OK;
 }

@@ -168,6 +168,21 @@ def test_gemm_f32_acc_weight_grad(shape):
     check("gemm.f32acc", np64(Cd), ref, max_rel=1e-4, min_cos=0.999999)
 
 
+@pytest.mark.parametrize("shape", [(768, 768, 4096), (6144, 768, 1000), (128, 64, 40), (30528, 768, 300)])
+def test_gemm_wgrad_fused_bias_grad(shape):
+    """dW += dY^T X and db += column sums of dY (tensor-core all-ones MMA), split-K into fp32."""
+    M, N, K = shape
+    rng = np.random.default_rng(M + K)
+    dY = synth.bf16_round(rng.standard_normal((K, M)))
+    X = synth.bf16_round(rng.standard_normal((K, N)))
+    W0 = rng.standard_normal((M, N)).astype(np.float32)
+    b0 = rng.standard_normal(M).astype(np.float32)
+    Wd, bd = to_dev(W0, torch.float32), to_dev(b0, torch.float32)
+    mb._lib.gemm_wgrad(M, N, K, _bf(dY), M, _bf(X), N, Wd, N, bd)
+    check("wgrad.dW", np64(Wd), W0 + dY.T.astype(np.float64) @ X.astype(np.float64), max_rel=1e-4, min_cos=0.999999)
+    check("wgrad.db", np64(bd), b0 + dY.astype(np.float64).sum(0), max_rel=1e-4, min_cos=0.999999)
+
+
 def test_gemm_f32_and_gelu_aux():
     M, N, K = 200, 256, 192
     rng = np.random.default_rng(1)
