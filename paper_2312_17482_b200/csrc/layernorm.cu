@@ -212,6 +212,150 @@ __global__ void colsum_kernel(const bf16* __restrict__ x, int n, int C, int rows
   for (int j = 0; j < 8; ++j) atomicAdd(out + c + j, acc[j]);
 }
 
+
+// LN backward with W warps per row (H = 256 W): every lane owns exactly one 16-byte vector of the
+// row, so the three column accumulators cost 24 registers and the SM runs at full occupancy (the
+// one-warp-per-row variant needed ~128 registers).  Row sums combine across the W warps through
+// shared memory (double-buffered by row parity, one named barrier per row).
+constexpr int LNW_GROUPS = 4;  // row groups (rows in flight) per CTA
+
+template <int W, bool EMBED, bool GELU, bool DSUM>
+__global__ void __launch_bounds__(LNW_GROUPS * W * 32)
+    ln_bwd_w_kernel(RowSrc src, const bf16* __restrict__ dy, const float* __restrict__ stats,
+                    const bf16* __restrict__ gamma, const bf16* __restrict__ gelu_pre, int n, int H, bf16* dx,
+                    float* __restrict__ d_emb, float* __restrict__ dgamma, float* __restrict__ dbeta,
+                    float* __restrict__ dsum) {
+  __shared__ float red[LNW_GROUPS][2][W][2];
+  extern __shared__ float sbuf[];  // [LNW_GROUPS][H] for the final column reduction
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rg = warp / W, w = warp - rg * W;
+  const int c = (w * 32 + lane) * 8;  // this lane's 8 columns
+  float gm[8];
+  bf16x8_to_f32(*reinterpret_cast<const uint4*>(gamma + c), gm);
+  float ag[8], ab[8], as[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) ag[j] = ab[j] = as[j] = 0.f;
+  int par = 0;
+  // one-row-ahead prefetch of x, dy, stats (doubles the bytes in flight per SM)
+  const int step = gridDim.x * LNW_GROUPS;
+  auto fetch = [&](int r, uint4& xv, uint4& dv, float2& sv, int& idv) {
+    const bf16* base;
+    if (EMBED) {
+      idv = src.ids[src.indices[r]];
+      base = src.emb + (size_t)idv * H;
+    } else {
+      base = src.x + (size_t)r * H;
+    }
+    xv = *reinterpret_cast<const uint4*>(base + c);
+    dv = *reinterpret_cast<const uint4*>(dy + (size_t)r * H + c);
+    sv = *reinterpret_cast<const float2*>(stats + 2 * (size_t)r);
+  };
+  uint4 nx = make_uint4(0, 0, 0, 0), nd = make_uint4(0, 0, 0, 0);
+  float2 nst = make_float2(0.f, 0.f);
+  int nid = 0;
+  int row = blockIdx.x * LNW_GROUPS + rg;
+  if (row < n) fetch(row, nx, nd, nst, nid);
+  for (; row < n; row += step, par ^= 1) {
+    const uint4 cx = nx, cd = nd;
+    const float2 st = nst;
+    const int id = nid;
+    if (row + step < n) fetch(row + step, nx, nd, nst, nid);
+    float xh[8], d[8];
+    bf16x8_to_f32(cx, xh);
+    if (EMBED) {
+      float t[8];
+      bf16x8_to_f32(*reinterpret_cast<const uint4*>(src.type_emb + c), t);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) xh[j] += t[j];
+    }
+    bf16x8_to_f32(cd, d);
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      xh[j] = (xh[j] - st.x) * st.y;
+      const float g = d[j] * gm[j];
+      ag[j] += d[j] * xh[j];
+      ab[j] += d[j];
+      s1 += g;
+      s2 += g * xh[j];
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if (W > 1) {
+      if (lane == 0) {
+        red[rg][par][w][0] = s1;
+        red[rg][par][w][1] = s2;
+      }
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + rg), "r"(W * 32) : "memory");
+      s1 = 0.f;
+      s2 = 0.f;
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        s1 += red[rg][par][k][0];
+        s2 += red[rg][par][k][1];
+      }
+    }
+    s1 /= H;
+    s2 /= H;
+    float o[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = st.y * (d[j] * gm[j] - s1 - xh[j] * s2);
+    if (GELU) {
+      float p[8];
+      bf16x8_to_f32(*reinterpret_cast<const uint4*>(gelu_pre + (size_t)row * H + c), p);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] *= gelu_grad_f(p[j]);
+    }
+    if (DSUM) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) as[j] += o[j];
+    }
+    if (EMBED) {
+      float* dst = d_emb + (size_t)id * H + c;
+      red_add_v4(dst, o[0], o[1], o[2], o[3]);
+      red_add_v4(dst + 4, o[4], o[5], o[6], o[7]);
+    } else {
+      *reinterpret_cast<uint4*>(dx + (size_t)row * H + c) = f32_to_bf16x8(o);
+    }
+  }
+  // column sums: reduce the 4 row groups through smem, one atomic per column per CTA
+  auto reduce = [&](const float* acc, float* out) {
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 8; ++j) sbuf[rg * H + c + j] = acc[j];
+    __syncthreads();
+    for (int cc = threadIdx.x; cc < H; cc += blockDim.x) {
+      float t = 0.f;
+#pragma unroll
+      for (int g = 0; g < LNW_GROUPS; ++g) t += sbuf[g * H + cc];
+      atomicAdd(out + cc, t);
+    }
+  };
+  reduce(ag, dgamma);
+  reduce(ab, dbeta);
+  if (DSUM) reduce(as, dsum);
+}
+
+template <int W, bool EMBED>
+mb_status ln_bwd_w_launch(const RowSrc& src, const bf16* dy, const float* stats, const bf16* gamma,
+                          const bf16* gelu_pre, int n, int H, bf16* dx, float* d_emb, float* dg, float* db,
+                          float* dsum, cudaStream_t s) {
+  const int threads = LNW_GROUPS * W * 32;
+  const int smem = LNW_GROUPS * H * sizeof(float);
+  const int blocks_per_sm = std::max(1, 2048 / threads);
+  const int grid = std::max(1, std::min((n + LNW_GROUPS - 1) / LNW_GROUPS, blocks_per_sm * num_sms()));
+#define LNW_GO(G, D)                                                                                          \
+  ln_bwd_w_kernel<W, EMBED, G, D><<<grid, threads, smem, s>>>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, \
+                                                               dg, db, dsum)
+  if (gelu_pre && dsum) LNW_GO(true, true);
+  else if (gelu_pre) LNW_GO(true, false);
+  else if (dsum) LNW_GO(false, true);
+  else LNW_GO(false, false);
+#undef LNW_GO
+  MB_CHECK_LAUNCH();
+  return MB_OK;
+}
+
 template <bool EMBED>
 mb_status ln_fwd_dispatch(const RowSrc& src, const bf16* gamma, const bf16* beta, int n, int H, float eps, bf16* y,
                           float* stats, cudaStream_t s) {
@@ -256,6 +400,10 @@ mb_status ln_bwd_dispatch(const RowSrc& src, const bf16* dy, const float* stats,
                           const bf16* gelu_pre, int n, int H, bf16* dx, float* d_emb, float* dg, float* db,
                           float* dsum, cudaStream_t s) {
   if (n == 0) return MB_OK;
+  if (H == 768) return ln_bwd_w_launch<3, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s);
+  if (H == 1024) return ln_bwd_w_launch<4, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s);
+  if (H == 512) return ln_bwd_w_launch<2, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s);
+  if (H == 256) return ln_bwd_w_launch<1, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s);
   switch ((H / 8 + 31) / 32) {
     case 1: return ln_bwd_launch<1, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s);
     case 2: return ln_bwd_launch<2, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s);
