@@ -64,7 +64,8 @@ __global__ void __launch_bounds__(LN_THREADS) ln_fwd_kernel(RowSrc src, const bf
   float s = 0.f;
 #pragma unroll
   for (int i = 0; i < VPL * 8; ++i) s += v[i];
-  const float mean = warp_sum(s) / H;
+  const float inv_h = __frcp_rn((float)H);
+  const float mean = warp_sum(s) * inv_h;
   float q = 0.f;
 #pragma unroll
   for (int i = 0; i < VPL; ++i) {
@@ -77,7 +78,7 @@ __global__ void __launch_bounds__(LN_THREADS) ln_fwd_kernel(RowSrc src, const bf
       }
     }
   }
-  const float rstd = rsqrtf(warp_sum(q) / H + eps);
+  const float rstd = rsqrtf(warp_sum(q) * inv_h + eps);
 #pragma unroll
   for (int i = 0; i < VPL; ++i) {
     const int c = (i * 32 + lane) * 8;
@@ -126,6 +127,7 @@ __global__ void __launch_bounds__(LN_THREADS, VPL <= 3 ? 2 : 1)
   // accumulators stay live; dy and gamma are re-read (L1 hits) in the second pass.
   extern __shared__ float sbuf[];
   const int lane = threadIdx.x & 31;
+  const float inv_h = __frcp_rn((float)H);
   float acc_g[VPL * 8], acc_b[VPL * 8], acc_s[DSUM ? VPL * 8 : 1];
 #pragma unroll
   for (int i = 0; i < VPL * 8; ++i) {
@@ -159,8 +161,8 @@ __global__ void __launch_bounds__(LN_THREADS, VPL <= 3 ? 2 : 1)
         }
       }
     }
-    s1 = warp_sum(s1) / H;
-    s2 = warp_sum(s2) / H;
+    s1 = warp_sum(s1) * inv_h;
+    s2 = warp_sum(s2) * inv_h;
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
       const int c = (i * 32 + lane) * 8;
@@ -230,6 +232,7 @@ __global__ void __launch_bounds__(LNW_GROUPS * W * 32)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int rg = warp / W, w = warp - rg * W;
   const int c = (w * 32 + lane) * 8;  // this lane's 8 columns
+  const float inv_h = __frcp_rn((float)H);
   float gm[8];
   bf16x8_to_f32(*reinterpret_cast<const uint4*>(gamma + c), gm);
   float ag[8], ab[8], as[8];
@@ -295,8 +298,8 @@ __global__ void __launch_bounds__(LNW_GROUPS * W * 32)
         s2 += red[rg][par][k][1];
       }
     }
-    s1 /= H;
-    s2 /= H;
+    s1 *= inv_h;
+    s2 *= inv_h;
     float o[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) o[j] = st.y * (d[j] * gm[j] - s1 - xh[j] * s2);
