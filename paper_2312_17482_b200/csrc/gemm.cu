@@ -155,7 +155,7 @@ __device__ __forceinline__ float warp_colsum32(float* v, int lane) {
 // ACC = 2 double-buffers the TMEM accumulator (epilogue of tile i overlaps the MMAs of tile i+1);
 // ACC = 1 is used by the weight-gradient GEMMs, whose tiles run hundreds of k-blocks per (cheap)
 // epilogue, to make room in TMEM for the bias-gradient accumulator.
-template <int BN, int STAGES, int A_MN, int B_MN, int PAIRED, int NSCR, int CG, int ACC>
+template <int BN, int STAGES, int A_MN, int B_MN, int PAIRED, int NSCR, int CG, int ACC, int CE>
 __global__ void __launch_bounds__(NTHREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                 Sched sc, Epi ep) {
@@ -381,6 +381,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       } else {
         constexpr int HALF = BN / 2;
         const int cbase = nb * BN + grp * HALF;
+        // fused cross-entropy state (E_LSE / E_DZ)
+        const bool ce = CE && (ep.mode == E_LSE || ep.mode == E_DZ);  // compiled only into CE kernels
+        int lab = -1;
+        float lse_r = 0.f, run_m = -INFINITY, run_s = 0.f, zl = 0.f;
+        bool has_lab = false;
+        if (ce && row_ok) {
+          lab = ep.labels[row];
+          if (ep.mode == E_DZ) lse_r = ep.lse[row];
+        }
+        constexpr float L2E = 1.4426950408889634f;
 #pragma unroll 1
         for (int c = 0; c < HALF / 32; ++c) {
           const int crel = grp * HALF + c * 32;
@@ -388,7 +398,37 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           if (col >= N) break;  // warp-uniform
           sm100::tmem_ld32(tb + crel, v);
           const int nv = min(32, N - col);
-          if (ep.mode == E_F32_ACC) {
+          if (CE && ce) {
+            float b[32];
+            load_bias32_smem(sbias + c * 64, b);
+            sm100::tmem_ld_wait();
+            if (ep.mode == E_LSE) {
+              float mx = -INFINITY;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                v[j] += b[j];
+                if (col + j < N) mx = fmaxf(mx, v[j]);
+                if (col + j == lab) {
+                  zl = v[j];
+                  has_lab = true;
+                }
+              }
+              const float nm = fmaxf(run_m, mx);
+              float acc_s = 0.f;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) acc_s += (col + j < N) ? exp2f((v[j] - nm) * L2E) : 0.f;
+              run_s = run_s * exp2f((run_m - nm) * L2E) + acc_s;
+              run_m = nm;
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                float pz = exp2f((v[j] + b[j] - lse_r) * L2E);
+                if (col + j == lab) pz -= 1.f;
+                v[j] = pz * ep.inv_norm;
+              }
+              emit_chunk(scrA, v, reinterpret_cast<bf16*>(ep.C), ep.ldc, row0, M, col, N, lane);
+            }
+          } else if (ep.mode == E_F32_ACC) {
             if (ACC == 1 && c == 0 && grp == 0 && ep.dbias && nb == 0) {
               float dbv[16];
               sm100::tmem_ld16(tmem_base + C::TMEM_DB + acc * 16 + ((uint32_t)(q * 32) << 16), dbv);
@@ -496,6 +536,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             emit_chunk(scrA, v, reinterpret_cast<bf16*>(ep.C), ep.ldc, row0, M, col, N, lane);
           }
+        }
+        if (CE && ep.mode == E_LSE && row_ok) {
+          ep.part[(int64_t)row * ep.npart + nb * 2 + grp] = make_float2(run_m, run_s);
+          if (has_lab) ep.zlab[row] = zl;
         }
       }
       sm100::tc_fence_before();
@@ -749,10 +793,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 }
 
 
-template <int BN, int STAGES, int A_MN, int B_MN, int PAIRED, int NSCR, int CG = 2, int ACC = 2>
+template <int BN, int STAGES, int A_MN, int B_MN, int PAIRED, int NSCR, int CG = 2, int ACC = 2, int CE = 0>
 mb_status launch(const GemmArgs& g, const CUtensorMap& ta, const CUtensorMap& tb, const Sched& sc, cudaStream_t s) {
   using C = Cfg<BN, STAGES, NSCR, CG, ACC>;
-  auto k = gemm_kernel<BN, STAGES, A_MN, B_MN, PAIRED, NSCR, CG, ACC>;
+  auto k = gemm_kernel<BN, STAGES, A_MN, B_MN, PAIRED, NSCR, CG, ACC, CE>;
   static bool attr_set = false;  // benign race: idempotent
   if (!attr_set) {
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) != cudaSuccess)
@@ -802,7 +846,8 @@ mb_status gemm(const GemmArgs& g, cudaStream_t s) {
   // epilogue streams two input tiles); GeGLU fwd is always a 256-wide paired tile (128 columns of
   // W1 + the matching 128 of V).
   const bool geglu_bwd = g.ep.mode == E_GEGLU_BWD;
-  const int BN = paired ? 256 : ((g.N <= 128 || geglu_bwd) ? 128 : 256);
+  const bool ce_mode = g.ep.mode == E_LSE || g.ep.mode == E_DZ;  // partial-statistics layout assumes 256
+  const int BN = (paired || ce_mode) ? 256 : ((g.N <= 128 || geglu_bwd) ? 128 : 256);
   // CG = 2 (generic kernel): pair tiles of 256 rows; each CTA loads 128 rows of A and BN/2 of B's N.
   constexpr int CGV = 2;
   CUtensorMap ta, tb;
@@ -853,6 +898,11 @@ mb_status gemm(const GemmArgs& g, cudaStream_t s) {
     return launch<128, 8, 1, 1, 0, 1, 2, 1>(g, ta, tb, sc, s);
   }
   MB_REQUIRE(g.ep.dbias == nullptr, MB_ERR_INVALID_ARG);
+  if (g.ep.mode == E_LSE || g.ep.mode == E_DZ) {  // decoder GEMM with fused softmax-cross-entropy
+    MB_REQUIRE(!g.a_t && !g.b_t && g.ep.labels && g.ep.bias && BN == 256, MB_ERR_CONFIG);
+    MB_REQUIRE(g.ep.mode == E_DZ ? g.ep.lse != nullptr : (g.ep.part && g.ep.zlab), MB_ERR_INVALID_ARG);
+    return launch<256, 6, 0, 0, 0, 1, 2, 2, 1>(g, ta, tb, sc, s);
+  }
   if (BN == 256) return dispatch_majors<256, 6, 1>(g, ta, tb, sc, s);
   return dispatch_majors<128, 8, 1>(g, ta, tb, sc, s);
 }

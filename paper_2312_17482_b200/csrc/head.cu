@@ -8,70 +8,34 @@
 namespace mb {
 namespace {
 
-constexpr int CE_THREADS = 256;
-
-// one CTA per masked row: online (max, sum exp) over V, LSE, row loss, then
-// dz = (softmax(z) - onehot(y)) * inv_norm stored as bf16 (consumed by the dU / dE GEMMs)
-__global__ void __launch_bounds__(CE_THREADS) ce_kernel(const float* __restrict__ logits, const int* __restrict__ labels,
-                                                        int V, float inv_norm, float* __restrict__ lse_out,
-                                                        float* __restrict__ row_loss, bf16* __restrict__ dz) {
-  const int row = blockIdx.x;
-  const float* z = logits + (size_t)row * V;
+// combine the per-(tile, half) online softmax partials of a row: LSE and the row loss
+__global__ void ce_combine_kernel(const float2* __restrict__ part, int npart, const float* __restrict__ zlab, int n,
+                                  float* __restrict__ lse_out, float* __restrict__ row_loss) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  constexpr float L2E = 1.4426950408889634f;
   float m = -INFINITY, s = 0.f;
-  for (int c = threadIdx.x * 4; c < V; c += CE_THREADS * 4) {
-    const float4 q = *reinterpret_cast<const float4*>(z + c);
-    const float mx = fmaxf(fmaxf(q.x, q.y), fmaxf(q.z, q.w));
-    const float nm = fmaxf(m, mx);
-    s = s * __expf(m - nm) + __expf(q.x - nm) + __expf(q.y - nm) + __expf(q.z - nm) + __expf(q.w - nm);
-    m = nm;
+  for (int i = lane; i < npart; i += 32) {
+    const float2 p = part[(int64_t)row * npart + i];
+    if (p.y > 0.f) {
+      const float nm = fmaxf(m, p.x);
+      s = s * exp2f((m - nm) * L2E) + p.y * exp2f((p.x - nm) * L2E);
+      m = nm;
+    }
   }
-  // block reduce (m, s)
-  __shared__ float sm[CE_THREADS / 32], ss[CE_THREADS / 32];
-  __shared__ float s_lse;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const float om = __shfl_xor_sync(0xffffffffu, m, o);
     const float os = __shfl_xor_sync(0xffffffffu, s, o);
     const float nm = fmaxf(m, om);
-    s = (m == -INFINITY ? 0.f : s * __expf(m - nm)) + (om == -INFINITY ? 0.f : os * __expf(om - nm));
+    s = (s > 0.f ? s * exp2f((m - nm) * L2E) : 0.f) + (os > 0.f ? os * exp2f((om - nm) * L2E) : 0.f);
     m = nm;
   }
   if (lane == 0) {
-    sm[warp] = m;
-    ss[warp] = s;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float M = sm[0], S = ss[0];
-    for (int w = 1; w < CE_THREADS / 32; ++w) {
-      const float nm = fmaxf(M, sm[w]);
-      S = S * __expf(M - nm) + ss[w] * __expf(sm[w] - nm);
-      M = nm;
-    }
-    const float l = M + logf(S);
-    s_lse = l;
-    const int y = labels[row];
+    const float l = m + logf(s);
     lse_out[row] = l;
-    row_loss[row] = l - z[y];
-  }
-  __syncthreads();
-  const float l = s_lse;
-  const int y = labels[row];
-  bf16* d = dz + (size_t)row * V;
-  for (int c = threadIdx.x * 4; c < V; c += CE_THREADS * 4) {
-    const float4 q = *reinterpret_cast<const float4*>(z + c);
-    float p0 = __expf(q.x - l), p1 = __expf(q.y - l), p2 = __expf(q.z - l), p3 = __expf(q.w - l);
-    if (y >= c && y < c + 4) {
-      if (y == c) p0 -= 1.f;
-      else if (y == c + 1) p1 -= 1.f;
-      else if (y == c + 2) p2 -= 1.f;
-      else p3 -= 1.f;
-    }
-    uint2 u;
-    u.x = pack_bf16x2(p0 * inv_norm, p1 * inv_norm);
-    u.y = pack_bf16x2(p2 * inv_norm, p3 * inv_norm);
-    *reinterpret_cast<uint2*>(d + c) = u;
+    row_loss[row] = l - zlab[row];
   }
 }
 
@@ -110,9 +74,13 @@ inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
 }  // namespace
 
+// partial softmax statistics per row: one per (256-column tile, column half) of the decoder GEMM
+inline int npart_of(int V) { return 2 * ((V + 255) / 256); }
+
 struct HeadWs {
   bf16 *h, *tpre, *t, *u, *du;
-  float *stats, *logits, *row_loss;
+  float *stats, *row_loss, *zlab;
+  float2* part;
   bf16* dz;
   size_t bytes;
   HeadWs(char* base, int n, int H, int V) {
@@ -129,7 +97,8 @@ struct HeadWs {
     du = (bf16*)take((size_t)n * H * 2);
     stats = (float*)take((size_t)n * 2 * 4);
     row_loss = (float*)take((size_t)n * 4);
-    logits = (float*)take((size_t)n * V * 4);
+    zlab = (float*)take((size_t)n * 4);
+    part = (float2*)take((size_t)n * npart_of(V) * 8);
     dz = (bf16*)take((size_t)n * V * 2);
     bytes = o;
   }
@@ -178,17 +147,28 @@ mb_status mb_mlm_loss(const mb_dims* d, const mb_head_params* p, const mb_bf16* 
     TRY(gemm(a, s));
   }
   TRY(layernorm_fwd(w.t, B(p->ln_g), B(p->ln_b), n, H, d->ln_eps, w.u, w.stats, s));
+  // z = u E^T + b_dec is never stored: the decoder GEMM's epilogue keeps an online (max, sum exp)
+  // per row and tile and picks the label logit (E_LSE); a combine pass gives LSE and the row loss
+  const int npart = npart_of(V);
   {
     GemmArgs a;
     a.M = n, a.N = V, a.K = H, a.A = w.u, a.lda = H, a.B = B(p->emb), a.ldb = H;
-    a.ep.mode = E_F32, a.ep.C = w.logits, a.ep.ldc = V, a.ep.bias = B(p->b_dec);
+    a.ep.mode = E_LSE, a.ep.C = w.dz /* unused */, a.ep.ldc = V, a.ep.bias = B(p->b_dec);
+    a.ep.labels = labels, a.ep.part = w.part, a.ep.zlab = w.zlab, a.ep.npart = npart;
     TRY(gemm(a, s));
   }
-  ce_kernel<<<n, CE_THREADS, 0, s>>>(w.logits, labels, V, inv_norm, lse, w.row_loss, w.dz);
+  ce_combine_kernel<<<(n + 7) / 8, 256, 0, s>>>(w.part, npart, w.zlab, n, lse, w.row_loss);
   MB_CHECK_LAUNCH();
   sum_kernel<<<1, 1024, 0, s>>>(w.row_loss, n, inv_norm, loss_sum);
   MB_CHECK_LAUNCH();
-  // backward
+  // backward: recompute z tile by tile and emit dz = (softmax(z) - onehot(y)) * inv_norm (E_DZ)
+  {
+    GemmArgs a;
+    a.M = n, a.N = V, a.K = H, a.A = w.u, a.lda = H, a.B = B(p->emb), a.ldb = H;
+    a.ep.mode = E_DZ, a.ep.C = w.dz, a.ep.ldc = V, a.ep.bias = B(p->b_dec);
+    a.ep.labels = labels, a.ep.lse = lse, a.ep.inv_norm = inv_norm;
+    TRY(gemm(a, s));
+  }
   {
     GemmArgs a;  // du = dz E   (E [V, H] = [K, N])
     a.M = n, a.N = H, a.K = V, a.A = w.dz, a.lda = V, a.B = B(p->emb), a.ldb = H, a.b_t = true;

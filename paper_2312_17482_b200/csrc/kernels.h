@@ -5,7 +5,7 @@
 
 namespace mb {
 
-enum EpiMode { E_BF16 = 0, E_F32_ACC = 1, E_F32 = 2, E_GELU_AUX = 3, E_GEGLU_FWD = 4, E_GEGLU_BWD = 5 };
+enum EpiMode { E_BF16 = 0, E_F32_ACC = 1, E_F32 = 2, E_GELU_AUX = 3, E_GEGLU_FWD = 4, E_GEGLU_BWD = 5, E_LSE = 6, E_DZ = 7 };
 
 struct Epi {
   int mode = E_BF16;
@@ -20,6 +20,15 @@ struct Epi {
   int64_t ldu = 0;
   int I = 0;                    // GeGLU half width
   float* dbias = nullptr;       // GEGLU_BWD: column sums of dU accumulated here (fp32 [2I], +=)
+  // fused softmax-cross-entropy over the columns (decoder GEMM, A11):
+  //   E_LSE: per row and (tile, column half) the online (max, sum exp) of z = acc + bias -> part,
+  //          and the label logit -> zlab;   E_DZ: C = bf16((exp(z - lse[row]) - [col == label]) * inv_norm)
+  const int* labels = nullptr;
+  const float* lse = nullptr;
+  float2* part = nullptr;
+  float* zlab = nullptr;
+  int npart = 0;
+  float inv_norm = 1.f;
 };
 
 struct GemmArgs {
