@@ -574,11 +574,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 // epilogue warps multiply in place (swizzled layout) and the tile leaves by TMA stores, so the
 // kernel streams Gd in / dU out at HBM rate with no per-thread global accesses.
 // ------------------------------------------------------------------------------------------------
-constexpr int GB_BN = 128, GB_STAGES = 3;
-constexpr int GB_STAGE_BYTES = BM * BK * 2 + GB_BN * BK * 2;  // 32 KB
-constexpr int GB_SLOT_BYTES = 4 * 128 * 128;                  // 4 boxes of 128 rows x 64 cols bf16 (64 KB)
+constexpr int GB_BN = 128, GB_STAGES = 4;
+constexpr int GB_STAGE_BYTES = BM * BK * 2 + (GB_BN / 2) * BK * 2;  // own 128 A rows + half of B (24 KB)
+constexpr int GB_SLOT_BYTES = 4 * 128 * 128;                        // 4 boxes of 128 rows x 64 cols bf16 (64 KB)
 constexpr int GB_SMEM = GB_STAGES * GB_STAGE_BYTES + 2 * GB_SLOT_BYTES + 1024 + 256;
 
+// CTA pair (cta_group::2): the pair computes 256 rows x 128 columns of dZ; each CTA stages its 128
+// rows of dF and half (64 columns) of W2's tile, and owns the epilogue (Gd in, dU out) of its rows.
 __global__ void __launch_bounds__(NTHREADS, 1)
     geglu_bwd_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmGd, const __grid_constant__ CUtensorMap tmDU, int M, int I,
@@ -590,12 +592,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* empty = full + GB_STAGES;
   uint64_t* tfull = empty + GB_STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* gfull = tempty + 2;   // [2] Gd slice landed
+  uint64_t* gfull = tempty + 2;   // [2] Gd slice landed (own CTA)
   uint64_t* gempty = gfull + 2;   // [2] slot free (2 arrivals: one per epilogue group)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gempty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const int rank = (int)sm100::cluster_ctarank();
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch(&tmA);
     sm100::tma_prefetch(&tmB);
@@ -607,15 +611,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&tfull[i], 1);
-      sm100::mbar_init(&tempty[i], NUM_EPI_WARPS);
+      sm100::mbar_init(&tempty[i], 2 * NUM_EPI_WARPS);
       sm100::mbar_init(&gfull[i], 1);
       sm100::mbar_init(&gempty[i], 2);
     }
     sm100::fence_barrier_init();
   }
-  if (warp == 2) sm100::tmem_alloc(tmem_slot, 2 * GB_BN);
+  if (warp == 2) sm100::tmem_alloc_pair(tmem_slot, 2 * GB_BN);
   sm100::tc_fence_before();
-  __syncthreads();
+  sm100::cluster_sync();
   sm100::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -624,27 +628,26 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int u = blockIdx.x; u < sc.total; u += gridDim.x, ++it) {
+      for (int u = cid; u < sc.total; u += ncl, ++it) {
         int mb, nb, kb0, kb1;
         sc.decode(u, mb, nb, kb0, kb1);
-        // the tile's Gd slice first, so it lands while the MMAs run
+        const int m_cta = (mb * 2 + rank) * BM;
+        // this CTA's Gd slice first, so it lands while the MMAs run
         const int sl = it & 1;
         sm100::mbar_wait(&gempty[sl], ((it >> 1) & 1) ^ 1);
         uint8_t* slot = slots + sl * GB_SLOT_BYTES;
         sm100::mbar_arrive_expect_tx(&gfull[sl], GB_SLOT_BYTES);
 #pragma unroll
         for (int bx = 0; bx < 4; ++bx)
-          sm100::tma_load_2d(slot + bx * 16384, &tmGd, &gfull[sl], (bx >> 1) * I + nb * GB_BN + (bx & 1) * 64, mb * BM);
+          sm100::tma_load_2d(slot + bx * 16384, &tmGd, &gfull[sl], (bx >> 1) * I + nb * GB_BN + (bx & 1) * 64, m_cta);
         for (int kb = kb0; kb < kb1; ++kb) {
           sm100::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * GB_STAGE_BYTES;
           uint8_t* sb = sa + BM * BK * 2;
-          sm100::mbar_arrive_expect_tx(&full[stage], GB_STAGE_BYTES);
+          if (rank == 0) sm100::mbar_arrive_expect_tx(&full[stage], 2 * GB_STAGE_BYTES);
           const int k0 = kb * BK;
-          sm100::tma_load_2d(sa, &tmA, &full[stage], k0, mb * BM);
-#pragma unroll
-          for (int i = 0; i < GB_BN / 64; ++i)
-            sm100::tma_load_2d(sb + i * 8192, &tmB, &full[stage], nb * GB_BN + i * 64, k0);
+          sm100::tma_load_2d_pair(sa, &tmA, &full[stage], k0, m_cta);
+          sm100::tma_load_2d_pair(sb, &tmB, &full[stage], nb * GB_BN + rank * 64, k0);
           if (++stage == GB_STAGES) {
             stage = 0;
             phase ^= 1;
@@ -653,13 +656,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = sm100::idesc_bf16(BM, GB_BN, 0, 1);
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = sm100::idesc_bf16(2 * BM, GB_BN, 0, 1);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int u = blockIdx.x; u < sc.total; u += gridDim.x) {
+      for (int u = cid; u < sc.total; u += ncl) {
         int mb, nb, kb0, kb1;
         sc.decode(u, mb, nb, kb0, kb1);
         sm100::mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -672,15 +675,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const uint32_t sb = sa + BM * BK * 2;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            sm100::mma_bf16_ss(d_tmem, sm100::desc_kmajor_sw128(sa + k * 32),
-                               sm100::desc_mnmajor_sw128(sb + k * 2048, 8192), idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-          sm100::mma_commit(&empty[stage]);
+            sm100::mma_bf16_ss_pair(d_tmem, sm100::desc_kmajor_sw128(sa + k * 32),
+                                    sm100::desc_mnmajor_sw128(sb + k * 2048, 8192), idesc,
+                                    (kb > kb0 || k > 0) ? 1u : 0u);
+          sm100::mma_commit_pair(&empty[stage]);
           if (++stage == GB_STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        sm100::mma_commit(&tfull[acc]);
+        sm100::mma_commit_pair(&tfull[acc]);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -689,14 +693,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
   } else if (warp >= 4) {
     const int ew = warp - 4;
-    const int q = warp & 3;   // TMEM lane quarter = rows [32q, 32q+32) of the tile
+    const int q = warp & 3;   // TMEM lane quarter = rows [32q, 32q+32) of this CTA's half
     const int grp = ew >> 2;  // column half: dZ columns [64 grp, 64 grp + 64) of the tile
     const int gtid = threadIdx.x - 128 - grp * 128;  // 0..127 within the group
     const int r = q * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
     int it = 0;
-    for (int u = blockIdx.x; u < sc.total; u += gridDim.x, ++it) {
+    for (int u = cid; u < sc.total; u += ncl, ++it) {
       int mb, nb, kb0, kb1;
       sc.decode(u, mb, nb, kb0, kb1);
       const int sl = it & 1;
@@ -712,7 +716,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       sm100::tmem_ld_wait();
       sm100::tc_fence_before();
       __syncwarp();
-      if (lane == 0) sm100::mbar_arrive(&tempty[acc]);  // accumulator drained: next tile's MMA may start
+      if (lane == 0) sm100::mbar_arrive_leader(&tempty[acc]);  // accumulator drained
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -743,7 +747,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       sm100::fence_proxy_async_smem();
       sm100::named_bar(1 + grp, 128);
-      const int row0 = mb * BM;
+      const int row0 = (mb * 2 + rank) * BM;
       if (gtid == 0) {
         sm100::tma_store_2d(&tmDU, slots + sl * GB_SLOT_BYTES + grp * 16384, nb * GB_BN + grp * 64, row0);
         sm100::tma_store_2d(&tmDU, slots + sl * GB_SLOT_BYTES + (2 + grp) * 16384, I + nb * GB_BN + grp * 64, row0);
@@ -772,7 +776,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
           for (int e = 0; e < 8; ++e) cs[e] += __shfl_xor_sync(0xffffffffu, cs[e], o);
         }
-        if (rb == 0) {
+        if (rb == 0 && rows > 0) {
           float* dst = dbias + ((gtid >> 6) ? I : 0) + nb * GB_BN + grp * 64 + cj * 8;
 #pragma unroll
           for (int e = 0; e < 8; ++e) atomicAdd(dst + e, cs[e]);
@@ -787,11 +791,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (gtid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   sm100::tc_fence_before();
-  __syncthreads();
+  sm100::cluster_sync();
   sm100::tc_fence_after();
-  if (warp == 2) sm100::tmem_dealloc(tmem_base, 2 * GB_BN);
+  if (warp == 2) sm100::tmem_dealloc_pair(tmem_base, 2 * GB_BN);
 }
-
 
 template <int BN, int STAGES, int A_MN, int B_MN, int PAIRED, int NSCR, int CG = 2, int ACC = 2, int CE = 0>
 mb_status launch(const GemmArgs& g, const CUtensorMap& ta, const CUtensorMap& tb, const Sched& sc, cudaStream_t s) {
@@ -888,8 +891,24 @@ mb_status gemm(const GemmArgs& g, cudaStream_t s) {
         return MB_ERR_CUDA;
       attr_gb = true;
     }
-    const int grid = std::max(1, std::min(sc.total, num_sms()));
-    geglu_bwd_kernel<<<grid, NTHREADS, GB_SMEM, s>>>(ta, tb, tg, tdu, g.M, g.ep.I, sc, g.ep.dbias);
+    Sched sg = sc;  // pair tiles of 256 rows
+    sg.num_m = (g.M + 2 * BM - 1) / (2 * BM);
+    sg.total = sg.num_m * sg.num_n * sg.splits;
+    const int clusters = std::max(1, std::min(sg.total, num_sms() / 2));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * clusters);
+    cfg.blockDim = dim3(NTHREADS);
+    cfg.dynamicSmemBytes = GB_SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, geglu_bwd_kernel, ta, tb, tg, tdu, g.M, g.ep.I, sg, g.ep.dbias) != cudaSuccess)
+      return MB_ERR_CUDA;
     MB_CHECK_LAUNCH();
     return MB_OK;
   }
