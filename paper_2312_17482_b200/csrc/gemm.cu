@@ -796,6 +796,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp == 2) sm100::tmem_dealloc_pair(tmem_base, 2 * GB_BN);
 }
 
+
 template <int BN, int STAGES, int A_MN, int B_MN, int PAIRED, int NSCR, int CG = 2, int ACC = 2, int CE = 0>
 mb_status launch(const GemmArgs& g, const CUtensorMap& ta, const CUtensorMap& tb, const Sched& sc, cudaStream_t s) {
   using C = Cfg<BN, STAGES, NSCR, CG, ACC>;
