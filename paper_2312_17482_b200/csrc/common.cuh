@@ -89,6 +89,35 @@ __device__ __forceinline__ void norm_cdf_pdf(float x, float& cdf, float& pdf) {
   cdf = x >= 0.f ? 1.0f - q : q;
   pdf = 0.3989422804014327f * e;
 }
+// norm_cdf_pdf for two values on the paired fp32 pipe (sm_100 FFMA2/FMUL2), same A&S 7.1.26 form:
+// e = 2^{-x^2 log2(e)/2}, t = 1/(1 + p|x|/sqrt2), q = 0.5 t poly(t) e, cdf = 0.5 + sgn(x)(0.5 - q).
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void norm_cdf_pdf2(float2 x, float2& cdf, float2& pdf) {
+  const float2 xx = __fmul2_rn(x, x);
+  const float2 ea = __fmul2_rn(xx, make_float2(-0.72134752044448170f, -0.72134752044448170f));
+  const float2 e = make_float2(ex2_approx(ea.x), ex2_approx(ea.y));
+  const float2 ax = make_float2(fabsf(x.x), fabsf(x.y));
+  const float2 den = __ffma2_rn(ax, make_float2(0.2316418882663604f, 0.2316418882663604f), make_float2(1.f, 1.f));
+  const float2 t = make_float2(rcp_approx(den.x), rcp_approx(den.y));
+  float2 q = __ffma2_rn(t, make_float2(0.5307027145f, 0.5307027145f), make_float2(-0.7265760135f, -0.7265760135f));
+  q = __ffma2_rn(t, q, make_float2(0.7107068705f, 0.7107068705f));
+  q = __ffma2_rn(t, q, make_float2(-0.1422483680f, -0.1422483680f));
+  q = __ffma2_rn(t, q, make_float2(0.1274147960f, 0.1274147960f));
+  q = __fmul2_rn(__fmul2_rn(q, t), e);  // = 0.5 (1 - erf(|x|/sqrt2))
+  const float2 h = __ffma2_rn(q, make_float2(-1.f, -1.f), make_float2(0.5f, 0.5f));
+  const float2 sg = make_float2(copysignf(1.f, x.x), copysignf(1.f, x.y));
+  cdf = __ffma2_rn(sg, h, make_float2(0.5f, 0.5f));
+  pdf = __fmul2_rn(e, make_float2(0.3989422804014327f, 0.3989422804014327f));
+}
 __device__ __forceinline__ float gelu_f(float x) {
   float c, p;
   norm_cdf_pdf(x, c, p);

@@ -13,6 +13,7 @@
 // dX = dY W and dW = dY^T X); both are expressed with 128-byte-swizzled TMA boxes and the matching
 // UMMA shared-memory descriptors, so no operand is ever transposed in memory.
 #include <algorithm>
+#include <cstdlib>
 #include "common.cuh"
 #include "kernels.h"
 #include "sm100.cuh"
@@ -22,6 +23,7 @@ namespace mb {
 namespace {
 
 constexpr int BM = 128, BK = 64;
+constexpr int kSplitOverheadKb = 4;  // split-K cost model: one unit's fp32 flush ~ this many k-blocks
 constexpr int NUM_EPI_WARPS = 8;                     // two warps per TMEM lane quarter
 constexpr int NTHREADS = 128 + 32 * NUM_EPI_WARPS;  // warps 0-3: TMA, MMA, TMEM alloc, spare
 constexpr int SCR_ROW = 80;                          // scratch row: 32 bf16 (64 B) + 16 B pad (conflict-free)
@@ -357,22 +359,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           load_bias32_smem(sbias + (c * 2 + 1) * 64, bg);
           sm100::tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            v[j] += ba[j];
-            g[j] += bg[j];
-          }
           // output Z = GeLU(a) * g; saved for backward Gd = [g * GeLU'(a) | GeLU(a)] (the two factors
-          // of dU = [dZ g GeLU'(a) | dZ GeLU(a)], so the backward epilogue needs no transcendental)
+          // of dU = [dZ g GeLU'(a) | dZ GeLU(a)], so the backward epilogue needs no transcendental).
+          // Two columns at a time on the paired fp32 pipe (FFMA2/FMUL2): this epilogue is ALU-bound.
           float z[32];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float x = v[j];
-            float cdf, pdf;
-            norm_cdf_pdf(x, cdf, pdf);
-            const float ge = x * cdf;
-            z[j] = ge * g[j];
-            v[j] = g[j] * (cdf + x * pdf);
-            g[j] = ge;
+          for (int j = 0; j < 32; j += 2) {
+            const float2 x = __fadd2_rn(make_float2(v[j], v[j + 1]), make_float2(ba[j], ba[j + 1]));
+            const float2 gg = __fadd2_rn(make_float2(g[j], g[j + 1]), make_float2(bg[j], bg[j + 1]));
+            float2 cdf, pdf;
+            norm_cdf_pdf2(x, cdf, pdf);
+            const float2 ge = __fmul2_rn(x, cdf);
+            const float2 zz = __fmul2_rn(ge, gg);
+            const float2 gd = __fmul2_rn(gg, __ffma2_rn(x, pdf, cdf));
+            z[j] = zz.x; z[j + 1] = zz.y;
+            v[j] = gd.x; v[j + 1] = gd.y;
+            g[j] = ge.x; g[j + 1] = ge.y;
           }
           emit_chunk(scrA, v, ep.aux, ep.ldaux, row0, M, col, ep.I, lane);
           emit_chunk(scrA, g, ep.aux + ep.I, ep.ldaux, row0, M, col, ep.I, lane);
@@ -870,11 +872,20 @@ mb_status gemm(const GemmArgs& g, cudaStream_t s) {
   sc.nkb = (g.K + BK - 1) / BK;
   int splits = 1;
   if (g.ep.mode == E_F32_ACC) {
-    // split-K for the weight gradients (few output tiles, K = tokens): aim for >= 2 waves while
-    // keeping >= 8 k-blocks per split; partial sums meet in fp32 atomics (the += contract).
+    // split-K for the weight gradients (few output tiles, K = tokens): pick the split count S that
+    // minimises waves(S) x (k-blocks per unit + a per-unit epilogue overhead): a 2.07-wave launch
+    // idles 1/3 of the machine in its last wave, while every extra split adds an fp32-atomic tile
+    // flush; >= 8 k-blocks per split. Partial sums meet in fp32 atomics (the += contract).
     const int tiles = sc.num_m * sc.num_n;
-    const int want = (2 * (num_sms() / CGV) + tiles - 1) / tiles;
-    splits = std::max(1, std::min(want, sc.nkb / 8));
+    const int C = std::max(1, num_sms() / CGV);
+    double best = 1e30;
+    for (int S = 1; S <= std::max(1, std::min(64, sc.nkb / 8)); ++S) {
+      const int kbp = (sc.nkb + S - 1) / S;
+      const int units = tiles * ((sc.nkb + kbp - 1) / kbp);
+      const double cost = (double)((units + C - 1) / C) * (kbp + kSplitOverheadKb);
+      if (cost < best * 0.98) { best = cost; splits = S; }
+    }
+    if (const char* e = getenv("MB_SPLITK")) splits = std::max(1, std::min(atoi(e), sc.nkb));  // tuning only
   }
   sc.kb_per = (sc.nkb + splits - 1) / splits;
   sc.splits = (sc.nkb + sc.kb_per - 1) / sc.kb_per;

@@ -29,3 +29,6 @@ for k, t in step:
 print(f"launches in last step: {len(step)}, serialized device time {tot/1e3:.2f} ms")
 for name, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
     print(f"{t/1e3:9.3f} ms {100*t/tot:6.2f}%  x{n:4d}  {name}")
+if len(sys.argv) > 2:  # optional: per-launch times (us) of kernels matching a regex, in launch order
+    rx = re.compile(sys.argv[2])
+    print(" ".join(f"{t:.0f}" for k, t in step if rx.search(k)))
