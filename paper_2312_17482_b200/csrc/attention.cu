@@ -637,7 +637,8 @@ __device__ __forceinline__ float warp_colsum32(float* v, int lane) {
 
 
 __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
-    const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do, const int* __restrict__ cu,
+    const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+    const __grid_constant__ CUtensorMap tm_dqkv, const int* __restrict__ cu,
     int batch, int heads, int d, const float* __restrict__ slopes, const bf16* __restrict__ O,
     const bf16* __restrict__ dO, const float* __restrict__ lse, bf16* __restrict__ dqkv, float* __restrict__ dbias,
     int nnz) {
@@ -760,6 +761,10 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
       const int len = cu[b + 1] - start;
       const float sl2 = slopes[h] * LOG2E;
       const float lse2 = (r < len) ? lse[(size_t)h * nnz + start + r] * LOG2E : 0.f;
+      // this warp's P / dS slabs double as its output staging: the previous unit's TMA stores must
+      // have read them before pass 1 overwrites them
+      if (lane == 0) sm100::bulk_wait_read0();
+      __syncwarp();
       sm100::mbar_wait(sp_full, i & 1);
       sm100::tc_fence_after();
       // pass 1: P = exp2(S*log2e/sqrt(d) - m log2e |i-j| - LSE log2e) in fp32 (kept in registers,
@@ -815,9 +820,15 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
       if (lane == 0) sm100::mbar_arrive(elem_done);
       sm100::mbar_wait(acc_full, i & 1);
       sm100::tc_fence_after();
-      // dQ (row = query r), dK (row = key r), dV (row = key r): this thread's 32 of the 64 columns
+      // dQ (row = query r), dK (row = key r), dV (row = key r): this thread's 32 of the 64 columns.
+      // A warp whose 32 rows all lie inside the sequence stages its [32 x 32] bf16 block in its own
+      // P / dS slab (64-byte swizzle, conflict-free) and one lane TMA-stores it; the ragged last
+      // quarter of a short sequence stores its valid rows directly.
       const bool ok = r < len;
       const bool col_ok = 32 * ch < d;
+      const int q4 = warp & 3;
+      const bool full = q4 * 32 + 32 <= len;  // warp-uniform
+      const uint32_t slabP = sPa + ch * (TILE * 128) + q4 * 4096, slabS = sdSa + ch * (TILE * 128) + q4 * 4096;
 #pragma unroll 1
       for (int which = 0; which < 3; ++which) {
         float v[32];
@@ -827,14 +838,31 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
         const float sc = which == 2 ? 1.f : rsd;
 #pragma unroll
         for (int e = 0; e < 32; ++e) v[e] = ok ? v[e] * sc : 0.f;
-        if (ok && col_ok) {
-          bf16* dst = dqkv + (size_t)(start + r) * 3 * H + which * H + h * d + 32 * ch;
+        if (col_ok) {
+          if (full) {
+            const uint32_t stg = which == 2 ? slabS : slabP + which * 2048;
 #pragma unroll
-          for (int c = 0; c < 32; c += 8) *reinterpret_cast<uint4*>(dst + c) = f32_to_bf16x8(v + c);
+            for (int c = 0; c < 4; ++c) {
+              const uint4 pk = f32_to_bf16x8(v + 8 * c);
+              st_shared_v4(stg + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4), pk.x, pk.y, pk.z, pk.w);
+            }
+            sm100::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              sm100::tma_store_2d(&tm_dqkv, stg, which * H + h * d + 32 * ch, start + q4 * 32);
+              sm100::bulk_commit();
+            }
+          } else if (ok) {
+            bf16* dst = dqkv + (size_t)(start + r) * 3 * H + which * H + h * d + 32 * ch;
+#pragma unroll
+            for (int c = 0; c < 32; c += 8) *reinterpret_cast<uint4*>(dst + c) = f32_to_bf16x8(v + c);
+          }
         }
-        if (dbias) {
-          // QKV-projection bias gradient = column sums of dQKV: transpose-reduce over the warp's
-          // 32 rows, one atomic per column per warp
+        // QKV-projection bias gradient = column sums of dQKV: transpose-reduce over the warp's 32
+        // rows, one atomic per column per warp.  The K part is identically zero (R31: a key bias
+        // adds q_i.b_k/sqrt(d) to every score of row i, which the row softmax cancels), so it is
+        // neither summed nor added.
+        if (dbias && which != 1) {
           const float cs = warp_colsum32(v, lane);
           if (col_ok && 32 * ch + lane < d) atomicAdd(dbias + which * H + h * d + 32 * ch + lane, cs);
         }
@@ -842,6 +870,7 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
       sm100::tc_fence_before();
       u = next_unit(cu, heads, total, u);
     }
+    if (lane == 0) sm100::bulk_wait0();
   }
   sm100::tc_fence_before();
   __syncthreads();
@@ -902,6 +931,8 @@ mb_status attention_bwd(const bf16* qkv, const bf16* O, const bf16* dO, const fl
   MB_REQUIRE(make_tmap_bf16_2d(&tq, qkv, 3 * H, nnz, 3 * H, DT, TILE), MB_ERR_CUDA);
   MB_REQUIRE(make_tmap_bf16_2d(&tdo, dO, H, nnz, H, DT, TILE), MB_ERR_CUDA);
   if (max_seqlen <= TILE) {
+    CUtensorMap tdq;  // [32 rows x 32 columns] output blocks, 64-byte swizzle
+    MB_REQUIRE(make_tmap_bf16_2d(&tdq, dqkv, 3 * H, nnz, 3 * H, 32, 32, 64), MB_ERR_CUDA);
     static bool attr_s = false;
     if (!attr_s) {
       if (cudaFuncSetAttribute(attn_bwd_short_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SH_BWD_SMEM) !=
@@ -911,7 +942,7 @@ mb_status attention_bwd(const bf16* qkv, const bf16* O, const bf16* dO, const fl
     }
     const int units = batch * heads;
     const int grid = std::max(1, std::min(units, num_sms()));
-    attn_bwd_short_kernel<<<grid, SH_BWD_THREADS, SH_BWD_SMEM, s>>>(tq, tdo, cu, batch, heads, d, slopes, O, dO,
+    attn_bwd_short_kernel<<<grid, SH_BWD_THREADS, SH_BWD_SMEM, s>>>(tq, tdo, tdq, cu, batch, heads, d, slopes, O, dO,
                                                                      lse, dqkv, dbias, nnz);
     MB_CHECK_LAUNCH();
     return MB_OK;

@@ -6,7 +6,8 @@
 
 namespace mb {
 // tensor [outer, inner] row-major bf16 with row stride ld_elems; box [box_outer, box_inner];
-// 128-byte swizzle; out-of-bounds elements read as zero.  Returns false on failure.
+// swizzle_bytes 128 (default), 64 or 0; out-of-bounds elements read as zero and are dropped on
+// stores.  Returns false on failure.
 bool make_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems,
-                       uint32_t box_inner, uint32_t box_outer, bool swizzle128 = true);
+                       uint32_t box_inner, uint32_t box_outer, int swizzle_bytes = 128);
 }  // namespace mb

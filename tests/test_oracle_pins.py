@@ -224,6 +224,30 @@ def test_p9_no_pad_leak():
         assert np.allclose(g[k], g2[k], rtol=0, atol=1e-12 * max(1, np.abs(g[k]).max())), k
 
 
+def test_p9b_key_bias_gradient_vanishes():
+    """Invariant (R31): a key-projection bias adds q_i.b_k/sqrt(d) to every score of query row i —
+    a per-row constant the row softmax of Eq. 1 cancels — so dL/db_k = 0 while db_q, db_v do not
+    vanish.  Pins the oracle's attention backward (a wrong dS sign/D term breaks the zero rowsum)."""
+    dims = synth.TINY
+    p, mask, X, dY = _layer_case(2)
+    H = dims.hidden
+    _, c = O.encoder_layer_forward(X, mask, O.alibi_slopes(dims.heads), p)
+    _, g = O.encoder_layer_backward(dY, c)
+    db = g["b_qkv"]
+    scale = np.max(np.abs(db))
+    assert scale > 1e-3
+    assert np.max(np.abs(db[H:2 * H])) < 1e-12 * scale
+    assert np.max(np.abs(db[:H])) > 1e-3 * scale and np.max(np.abs(db[2 * H:])) > 1e-3 * scale
+    # and the key bias leaves the forward unchanged (the reason the gradient vanishes)
+    p2 = dict(p)
+    p2["b_qkv"] = p["b_qkv"].copy()
+    p2["b_qkv"][H:2 * H] += np.random.default_rng(4).standard_normal(H)
+    Y1, _ = O.encoder_layer_forward(X, mask, O.alibi_slopes(dims.heads), p)
+    Y2, _ = O.encoder_layer_forward(X, mask, O.alibi_slopes(dims.heads), p2)
+    real = mask.astype(bool)
+    assert np.max(np.abs(Y1[real] - Y2[real])) < 1e-10
+
+
 # ----------------------------------------------------------------------------- P10 GeGLU
 def test_p10_gelu_value():
     assert abs(O.gelu(1.0) - GOLD["gelu_1"]["value"]) < 1e-15
