@@ -429,6 +429,28 @@ __device__ __forceinline__ int next_unit(const int* cu, int heads, int total, in
   return total;
 }
 
+// Forward scores of this thread's 64 keys [64 ch, 64 ch + 64) of query row r, in the exp2 domain:
+// x_j = S_rj log2e / sqrt(d) - m_h log2e |r - j| (-inf past the sequence when MASK); returns max_j.
+template <bool MASK>
+__device__ __forceinline__ float fwd_scores(float (&x)[64], int r, int ch, int len, float sc2, float sl2) {
+  const float rc = (float)(r - 64 * ch);
+  float mx = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < 64; j += 2) {
+    const float2 dd = __fadd2_rn(make_float2(rc, rc), make_float2(-(float)j, -(float)j - 1.f));
+    const float2 t = __ffma2_rn(make_float2(fabsf(dd.x), fabsf(dd.y)), make_float2(-sl2, -sl2),
+                                __fmul2_rn(make_float2(x[j], x[j + 1]), make_float2(sc2, sc2)));
+    x[j] = t.x;
+    x[j + 1] = t.y;
+    if (MASK) {
+      x[j] = 64 * ch + j < len ? x[j] : -INFINITY;
+      x[j + 1] = 64 * ch + j + 1 < len ? x[j + 1] : -INFINITY;
+    }
+    mx = fmaxf(mx, fmaxf(x[j], x[j + 1]));
+  }
+  return mx;
+}
+
 // Forward, software-pipelined: warp 8 (one lane) issues the TMA loads of units i+1, i+2 into two
 // smem buffers and S(i+1) = Q K^T into the second TMEM S buffer while warps 0-7 run the softmax of
 // unit i; then O(i) = P V.  TMEM: S[0] [0,128), S[1] [128,256), O [256,320).
@@ -437,6 +459,7 @@ constexpr int FWD_BUF_BYTES = 3 * TILE_BYTES;  // Q, K, V
 constexpr int SH_FWD_SMEM2 = 2 * FWD_BUF_BYTES + P_BYTES + 1024 + 256;
 
 __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const __grid_constant__ CUtensorMap tm_qkv,
+                                                                          const __grid_constant__ CUtensorMap tm_o,
                                                                           const int* __restrict__ cu, int batch,
                                                                           int heads, int d,
                                                                           const float* __restrict__ slopes,
@@ -544,6 +567,9 @@ __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const
       const int start = cu[b];
       const int len = cu[b + 1] - start;
       const float sl2 = slopes[h] * LOG2E;
+      // this warp's P slab doubles as its O staging: the previous unit's TMA store must have read it
+      if (lane == 0) sm100::bulk_wait_read0();
+      __syncwarp();
       sm100::mbar_wait(&s_full[i & 1], (i >> 1) & 1);
       sm100::tc_fence_after();
       const uint32_t tS = tbase + 128 * (i & 1) + lane_off + 64 * ch;
@@ -551,30 +577,25 @@ __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const
       sm100::tmem_ld32(tS, x);
       sm100::tmem_ld32(tS + 32, x + 32);
       sm100::tmem_ld_wait();
-      float mx = -INFINITY;
-#pragma unroll
-      for (int j = 0; j < 64; ++j) {
-        const int key = 64 * ch + j;
-        const float t = x[j] * sc2 - sl2 * fabsf((float)(r - key));
-        x[j] = key < len ? t : -INFINITY;
-        mx = fmaxf(mx, x[j]);
-      }
+      float mx = len == TILE ? fwd_scores<false>(x, r, ch, len, sc2, sl2) : fwd_scores<true>(x, r, ch, len, sc2, sl2);
       rmax[ch * 128 + r] = mx;
       named_bar_sync(1, SH_THREADS);
       mx = fmaxf(rmax[r], rmax[128 + r]);
-      float sum = 0.f;
+      // P = 2^(x - max) rounded to bf16 (the operand of O = P V); the row sum is taken over the
+      // rounded values so that the normalisation matches the product exactly
+      float2 sum2 = make_float2(0.f, 0.f);
 #pragma unroll
       for (int j8 = 0; j8 < 8; ++j8) {
         uint32_t pk[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const bf162 hp = __floats2bfloat162_rn(exp2f(x[j8 * 8 + 2 * e] - mx), exp2f(x[j8 * 8 + 2 * e + 1] - mx));
-          const float2 pr = __bfloat1622float2(hp);
-          sum += pr.x + pr.y;
-          pk[e] = *reinterpret_cast<const uint32_t*>(&hp);
+          const float2 t = __fadd2_rn(make_float2(x[j8 * 8 + 2 * e], x[j8 * 8 + 2 * e + 1]), make_float2(-mx, -mx));
+          pk[e] = pack_bf16x2(ex2_approx(t.x), ex2_approx(t.y));
+          sum2 = __fadd2_rn(sum2, make_float2(__uint_as_float(pk[e] << 16), __uint_as_float(pk[e] & 0xffff0000u)));
         }
         st_shared_v4(sPa + p_off(r, 64 * ch + 8 * j8), pk[0], pk[1], pk[2], pk[3]);
       }
+      const float sum = sum2.x + sum2.y;
       rsum[ch * 128 + r] = sum;
       sm100::fence_proxy_async_smem();
       sm100::tc_fence_before();
@@ -586,23 +607,35 @@ __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const
       sm100::tmem_ld32(tbase + 256 + lane_off + 32 * ch, v);
       sm100::tmem_ld_wait();
       const float l = rsum[r] + rsum[128 + r];
-      if (r < len) {
-        const float inv = 1.f / l;
-        bf16* dst = O + (size_t)(start + r) * H + h * d + 32 * ch;
+      const float inv = 1.f / l;
 #pragma unroll
-        for (int c = 0; c < 32; c += 8) {
-          if (32 * ch + c < d) {
-            float t[8];
+      for (int e = 0; e < 32; ++e) v[e] *= inv;
+      const int q4 = warp & 3;
+      if (32 * ch < d) {
+        if (q4 * 32 + 32 <= len) {  // warp-uniform: all 32 rows valid -> swizzled staging + TMA store
+          const uint32_t stg = sPa + ch * (TILE * 128) + q4 * 4096;
 #pragma unroll
-            for (int e = 0; e < 8; ++e) t[e] = v[c + e] * inv;
-            *reinterpret_cast<uint4*>(dst + c) = f32_to_bf16x8(t);
+          for (int c = 0; c < 4; ++c) {
+            const uint4 pk = f32_to_bf16x8(v + 8 * c);
+            st_shared_v4(stg + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4), pk.x, pk.y, pk.z, pk.w);
           }
+          sm100::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            sm100::tma_store_2d(&tm_o, stg, h * d + 32 * ch, start + q4 * 32);
+            sm100::bulk_commit();
+          }
+        } else if (r < len) {
+          bf16* dst = O + (size_t)(start + r) * H + h * d + 32 * ch;
+#pragma unroll
+          for (int c = 0; c < 32; c += 8) *reinterpret_cast<uint4*>(dst + c) = f32_to_bf16x8(v + c);
         }
-        if (ch == 0) lse[(size_t)h * nnz + start + r] = (mx + log2f(l)) * LN2;
       }
+      if (ch == 0 && r < len) lse[(size_t)h * nnz + start + r] = (mx + log2f(l)) * LN2;
       sm100::tc_fence_before();
       u = next_unit(cu, heads, total, u);
     }
+    if (lane == 0) sm100::bulk_wait0();
   }
   sm100::tc_fence_before();
   __syncthreads();
@@ -611,11 +644,12 @@ __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const
 }
 
 // Backward: a software-pipelined persistent kernel.  Warp 8 (one lane) is the producer/issuer:
-// TMA loads of (Q, K, V, dO) for the next two units into two smem buffers, S = QK^T and dP = dO V^T
-// of unit i+1 issued as soon as the compute warps have consumed unit i's S/dP, and the second MMA
-// batch (dV, dK, dQ) of unit i; warps 0-7 do the elementwise softmax-gradient of unit i and the
-// readout of unit i-1, so loads, both MMA batches and the CUDA-core work of neighbouring units
-// overlap.  TMEM: S [0,128), dP [128,256), dV [256,320), dK [320,384), dQ [384,448).
+// TMA loads of (Q, K, V, dO) for the next two units into two smem buffers; S = QK^T and dP = dO V^T
+// of unit i+1 as soon as the compute warps have consumed unit i's S/dP; dV = P^T dO of unit i as
+// soon as P is in shared memory (while the compute warps form dS), then dK = dS^T Q, dQ = dS K.
+// Warps 0-7 do the elementwise softmax-gradient of unit i, then read dV (already done) and dK/dQ
+// out of TMEM, so loads, the three MMA batches and the CUDA-core work of neighbouring units overlap.
+// TMEM: S [0,128), dP [128,256), dV [256,320), dK [320,384), dQ [384,448).
 constexpr int BWD_BUF_BYTES = 4 * TILE_BYTES;  // Q, K, V, dO
 constexpr int SH_BWD_THREADS = SH_THREADS + 32;
 constexpr int SH_BWD_SMEM = 2 * BWD_BUF_BYTES + 2 * P_BYTES + 1024 + 256;
@@ -635,6 +669,47 @@ __device__ __forceinline__ float warp_colsum32(float* v, int lane) {
   return v[0];
 }
 
+// Backward pass 1 for this thread's 64 keys [64 ch, 64 ch + 64) of query row r:
+//   P_rj = 2^(S_rj log2e / sqrt(d) - m_h log2e |r - j| - LSE_r log2e)
+// (fp32, kept in p[]; bf16 copy into the swizzled P tile) and the partial row sum of P * dP (D_r =
+// dO_r . O_r = sum_j P_rj dP_rj, so D needs neither O nor dO from memory).  Two keys per
+// instruction on the paired fp32 pipe; MASK = false for units of exactly 128 rows (no masking).
+template <bool MASK>
+__device__ __forceinline__ float bwd_pass1(uint32_t tS, uint32_t tdP, uint32_t sPa, int r, int ch, int len, float sc2,
+                                          float sl2, float lse2, float (&p)[64]) {
+  float2 Dp = make_float2(0.f, 0.f);
+  const float rc = (float)(r - 64 * ch);
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const int c0 = 64 * ch + 32 * c;
+    float v[32], w[32];
+    sm100::tmem_ld32(tS + c0, v);
+    sm100::tmem_ld32(tdP + c0, w);
+    sm100::tmem_ld_wait();
+    uint32_t pp[16];
+#pragma unroll
+    for (int jj = 0; jj < 32; jj += 2) {
+      const float j0 = (float)(32 * c + jj);
+      const float2 dd = __fadd2_rn(make_float2(rc, rc), make_float2(-j0, -j0 - 1.f));
+      const float2 t = __ffma2_rn(make_float2(fabsf(dd.x), fabsf(dd.y)), make_float2(-sl2, -sl2),
+                                  make_float2(-lse2, -lse2));
+      const float2 x = __ffma2_rn(make_float2(v[jj], v[jj + 1]), make_float2(sc2, sc2), t);
+      float2 pv = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+      if (MASK) {
+        pv.x = (r < len && c0 + jj < len) ? pv.x : 0.f;
+        pv.y = (r < len && c0 + jj + 1 < len) ? pv.y : 0.f;
+      }
+      p[32 * c + jj] = pv.x;
+      p[32 * c + jj + 1] = pv.y;
+      Dp = __ffma2_rn(pv, make_float2(w[jj], w[jj + 1]), Dp);
+      pp[jj >> 1] = pack_bf16x2(pv.x, pv.y);
+    }
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4)
+      st_shared_v4(sPa + p_off(r, c0 + q4 * 8), pp[4 * q4], pp[4 * q4 + 1], pp[4 * q4 + 2], pp[4 * q4 + 3]);
+  }
+  return Dp.x + Dp.y;
+}
 
 __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
     const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
@@ -647,11 +722,13 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
   uint8_t* bufs = smem;                        // 2 x (Q, K, V, dO)
   uint8_t* sP = smem + 2 * BWD_BUF_BYTES;
   uint8_t* sdS = sP + P_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sdS + P_BYTES);  // load[2], sp, elem, acc
-  uint64_t* load_full = bars;
-  uint64_t* sp_full = bars + 2;
-  uint64_t* elem_done = bars + 3;
-  uint64_t* acc_full = bars + 4;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sdS + P_BYTES);
+  uint64_t* load_full = bars;      // [2]
+  uint64_t* sp_full = bars + 2;    // S, dP of the unit in TMEM
+  uint64_t* elem_done = bars + 3;  // 8 compute warps: S/dP consumed, dS in smem
+  uint64_t* acc_full = bars + 4;   // dK, dQ (and dV) of the unit in TMEM
+  uint64_t* p_ready = bars + 5;    // 8 compute warps: P in smem
+  uint64_t* dv_full = bars + 6;    // dV of the unit in TMEM
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 8);
   __shared__ float dred[2 * 128];  // partial D of the two half-row threads
 
@@ -661,11 +738,14 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
   if (tid == 0) {
     sm100::tma_prefetch(&tm_qkv);
     sm100::tma_prefetch(&tm_do);
+    sm100::tma_prefetch(&tm_dqkv);
     sm100::mbar_init(&load_full[0], 1);
     sm100::mbar_init(&load_full[1], 1);
     sm100::mbar_init(sp_full, 1);
     sm100::mbar_init(elem_done, 8);
     sm100::mbar_init(acc_full, 1);
+    sm100::mbar_init(p_ready, 8);
+    sm100::mbar_init(dv_full, 1);
     sm100::fence_barrier_init();
   }
   if (warp == 0) sm100::tmem_alloc(tslot, 512);
@@ -705,15 +785,21 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
         }
         sm100::mma_commit(sp_full);
       };
-      auto mma2 = [&](int b) {  // dV = P^T dO, dK = dS^T Q, dQ = dS K
-        const uint32_t q = sm100::smem_u32(buf_addr(b));
-        const uint32_t k = q + TILE_BYTES, o = q + 3 * TILE_BYTES;
-        constexpr uint32_t id_t = sm100::idesc_bf16(128, 64, 1, 1);
-        constexpr uint32_t id_q = sm100::idesc_bf16(128, 64, 0, 1);
+      constexpr uint32_t id_t = sm100::idesc_bf16(128, 64, 1, 1);
+      constexpr uint32_t id_q = sm100::idesc_bf16(128, 64, 0, 1);
+      auto mma_dv = [&](int b) {  // dV = P^T dO
+        const uint32_t o = sm100::smem_u32(buf_addr(b)) + 3 * TILE_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < TILE / 16; ++kk) {
+        for (int kk = 0; kk < TILE / 16; ++kk)
           sm100::mma_bf16_ss(tdV, sm100::desc_mnmajor_sw128(sPa + kk * 2048, TILE * 128),
                              sm100::desc_mnmajor_sw128(o + kk * 2048, 8192), id_t, kk > 0);
+        sm100::mma_commit(dv_full);
+      };
+      auto mma_dkq = [&](int b) {  // dK = dS^T Q, dQ = dS K
+        const uint32_t q = sm100::smem_u32(buf_addr(b));
+        const uint32_t k = q + TILE_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < TILE / 16; ++kk) {
           sm100::mma_bf16_ss(tdK, sm100::desc_mnmajor_sw128(sdSa + kk * 2048, TILE * 128),
                              sm100::desc_mnmajor_sw128(q + kk * 2048, 8192), id_t, kk > 0);
           sm100::mma_bf16_ss(tdQ, sm100::desc_kmajor_sw128(sdSa + (kk >> 2) * (TILE * 128) + (kk & 3) * 32),
@@ -732,15 +818,18 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
       }
       for (int i = 0; u_cur < total; ++i) {
         const int b = i & 1;
-        sm100::mbar_wait(elem_done, i & 1);  // compute warps consumed S/dP(i), wrote P/dS(i)
+        sm100::mbar_wait(p_ready, i & 1);  // P(i) in smem (and dV(i-1) read out)
         sm100::tc_fence_after();
-        mma2(b);
+        mma_dv(b);
+        sm100::mbar_wait(elem_done, i & 1);  // S/dP(i) consumed, dS(i) in smem
+        sm100::tc_fence_after();
+        mma_dkq(b);
         if (u_nxt < total) {
           sm100::mbar_wait(&load_full[b ^ 1], ((i + 1) >> 1) & 1);
           sm100::tc_fence_after();
           mma1(b ^ 1);
         }
-        sm100::mbar_wait(acc_full, i & 1);  // MMA2(i) done: buffer b and P/dS are free
+        sm100::mbar_wait(acc_full, i & 1);  // all MMAs of unit i done: buffer b is free
         const int u_n2 = u_nxt < total ? next_unit(cu, heads, total, u_nxt) : total;
         if (u_n2 < total) issue_loads(u_n2, b);
         u_cur = u_nxt;
@@ -751,51 +840,40 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
   } else {
     // ------------------------------------------------------------------ compute warps 0-7
     const int ch = warp >> 2;
-    const int r = (warp & 3) * 32 + lane;
-    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     const float rsd = rsqrtf((float)d);
     const float sc2 = rsd * LOG2E;
+    const bool col_ok = 32 * ch < d;
+    // this warp's P / dS slabs (rows [32 q4, +32), columns [64 ch, +64)) double as output staging
+    const uint32_t slabP = sPa + ch * (TILE * 128) + q4 * 4096, slabS = sdSa + ch * (TILE * 128) + q4 * 4096;
+    auto lse_of = [&](int uu) {  // LSE of row r of unit uu, prefetched one unit ahead (scaled at use)
+      if (uu >= total) return 0.f;
+      const int bb = uu / heads, hh = uu - bb * heads;
+      const int st = cu[bb];
+      return (r < cu[bb + 1] - st) ? lse[(size_t)hh * nnz + st + r] : 0.f;
+    };
+    float lse_next = lse_of(u0);
     for (int i = 0, u = u0; u < total; ++i) {
       const int b = u / heads, h = u - b * heads;
       const int start = cu[b];
       const int len = cu[b + 1] - start;
       const float sl2 = slopes[h] * LOG2E;
-      const float lse2 = (r < len) ? lse[(size_t)h * nnz + start + r] * LOG2E : 0.f;
-      // this warp's P / dS slabs double as its output staging: the previous unit's TMA stores must
-      // have read them before pass 1 overwrites them
+      const float lse2 = lse_next * LOG2E;
+      const int un = next_unit(cu, heads, total, u);
+      // the previous unit's TMA stores must have read this warp's slabs before they are rewritten
       if (lane == 0) sm100::bulk_wait_read0();
       __syncwarp();
       sm100::mbar_wait(sp_full, i & 1);
       sm100::tc_fence_after();
-      // pass 1: P = exp2(S*log2e/sqrt(d) - m log2e |i-j| - LSE log2e) in fp32 (kept in registers,
-      // stored as bf16 for the MMAs) and the partial row sum of P * dP.  Since O = P V,
-      // D_i = dO_i . O_i = sum_j P_ij dP_ij, so D needs neither O nor dO from memory.
       float p[64];
-      float Dp = 0.f;
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int c0 = 64 * ch + 32 * c;
-        float v[32], w[32];
-        sm100::tmem_ld32(tS + lane_off + c0, v);
-        sm100::tmem_ld32(tdP + lane_off + c0, w);
-        sm100::tmem_ld_wait();
-        uint32_t pp[16];
-#pragma unroll
-        for (int jj = 0; jj < 32; jj += 2) {
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int key = c0 + jj + e;
-            const bool ok = (r < len) && (key < len);
-            const float pv = ok ? exp2f(v[jj + e] * sc2 - sl2 * fabsf((float)(r - key)) - lse2) : 0.f;
-            p[32 * c + jj + e] = pv;
-            Dp += pv * w[jj + e];
-          }
-          pp[jj >> 1] = pack_bf16x2(p[32 * c + jj], p[32 * c + jj + 1]);
-        }
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4)
-          st_shared_v4(sPa + p_off(r, c0 + q4 * 8), pp[4 * q4], pp[4 * q4 + 1], pp[4 * q4 + 2], pp[4 * q4 + 3]);
-      }
+      const float Dp = len == TILE ? bwd_pass1<false>(tS + lane_off, tdP + lane_off, sPa, r, ch, len, sc2, sl2, lse2, p)
+                                   : bwd_pass1<true>(tS + lane_off, tdP + lane_off, sPa, r, ch, len, sc2, sl2, lse2, p);
+      sm100::fence_proxy_async_smem();
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(p_ready);
       dred[ch * 128 + r] = Dp;
       named_bar_sync(1, SH_THREADS);
       const float Dr = dred[r] + dred[128 + r];
@@ -808,29 +886,32 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
         sm100::tmem_ld_wait();
         uint32_t pd[16];
 #pragma unroll
-        for (int jj = 0; jj < 32; jj += 2)
-          pd[jj >> 1] = pack_bf16x2(p[32 * c + jj] * (w[jj] - Dr), p[32 * c + jj + 1] * (w[jj + 1] - Dr));
+        for (int jj = 0; jj < 32; jj += 2) {
+          const float2 ds = __fmul2_rn(make_float2(p[32 * c + jj], p[32 * c + jj + 1]),
+                                       __fadd2_rn(make_float2(w[jj], w[jj + 1]), make_float2(-Dr, -Dr)));
+          pd[jj >> 1] = pack_bf16x2(ds.x, ds.y);
+        }
 #pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4)
-          st_shared_v4(sdSa + p_off(r, c0 + q4 * 8), pd[4 * q4], pd[4 * q4 + 1], pd[4 * q4 + 2], pd[4 * q4 + 3]);
+        for (int q = 0; q < 4; ++q)
+          st_shared_v4(sdSa + p_off(r, c0 + q * 8), pd[4 * q], pd[4 * q + 1], pd[4 * q + 2], pd[4 * q + 3]);
       }
       sm100::fence_proxy_async_smem();
       sm100::tc_fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(elem_done);
-      sm100::mbar_wait(acc_full, i & 1);
-      sm100::tc_fence_after();
-      // dQ (row = query r), dK (row = key r), dV (row = key r): this thread's 32 of the 64 columns.
-      // A warp whose 32 rows all lie inside the sequence stages its [32 x 32] bf16 block in its own
-      // P / dS slab (64-byte swizzle, conflict-free) and one lane TMA-stores it; the ragged last
-      // quarter of a short sequence stores its valid rows directly.
+      lse_next = lse_of(un);  // in flight while the MMAs run
+      // dV (row = key r), then dQ (row = query r), dK (row = key r): this thread's 32 of the 64
+      // columns.  A warp whose 32 rows all lie inside the sequence stages its [32 x 32] bf16 block
+      // in its own P / dS slab (64-byte swizzle, conflict-free) and one lane TMA-stores it; the
+      // ragged last quarter of a short sequence stores its valid rows directly.
       const bool ok = r < len;
-      const bool col_ok = 32 * ch < d;
-      const int q4 = warp & 3;
       const bool full = q4 * 32 + 32 <= len;  // warp-uniform
-      const uint32_t slabP = sPa + ch * (TILE * 128) + q4 * 4096, slabS = sdSa + ch * (TILE * 128) + q4 * 4096;
+      sm100::mbar_wait(dv_full, i & 1);
 #pragma unroll 1
-      for (int which = 0; which < 3; ++which) {
+      for (int k3 = 0; k3 < 3; ++k3) {
+        const int which = k3 == 0 ? 2 : k3 - 1;  // V, Q, K
+        if (k3 == 1) sm100::mbar_wait(acc_full, i & 1);
+        sm100::tc_fence_after();
         float v[32];
         const uint32_t src = which == 0 ? tdQ : (which == 1 ? tdK : tdV);
         sm100::tmem_ld32(src + lane_off + 32 * ch, v);
@@ -840,7 +921,9 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
         for (int e = 0; e < 32; ++e) v[e] = ok ? v[e] * sc : 0.f;
         if (col_ok) {
           if (full) {
-            const uint32_t stg = which == 2 ? slabS : slabP + which * 2048;
+            // staging: dV -> P slab [0, 2K) (P was consumed by dV's MMA), dQ -> P slab [2K, 4K),
+            // dK -> dS slab (all MMAs done once acc_full has been waited)
+            const uint32_t stg = which == 2 ? slabP : (which == 0 ? slabP + 2048 : slabS);
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
               const uint4 pk = f32_to_bf16x8(v + 8 * c);
@@ -868,7 +951,7 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
         }
       }
       sm100::tc_fence_before();
-      u = next_unit(cu, heads, total, u);
+      u = un;
     }
     if (lane == 0) sm100::bulk_wait0();
   }
@@ -896,9 +979,11 @@ mb_status attention_fwd(const bf16* qkv, const int* cu, int batch, int nnz, int 
         return MB_ERR_CUDA;
       attr_s = true;
     }
+    CUtensorMap tmo;  // [32 rows x 32 columns] output blocks, 64-byte swizzle
+    MB_REQUIRE(make_tmap_bf16_2d(&tmo, O, H, nnz, H, 32, 32, 64), MB_ERR_CUDA);
     const int units = batch * heads;
     const int grid = std::max(1, std::min(units, num_sms()));
-    attn_fwd_short_kernel<<<grid, SH_FWD_THREADS, SH_FWD_SMEM2, s>>>(tm, cu, batch, heads, d, slopes, O, lse, nnz);
+    attn_fwd_short_kernel<<<grid, SH_FWD_THREADS, SH_FWD_SMEM2, s>>>(tm, tmo, cu, batch, heads, d, slopes, O, lse, nnz);
     MB_CHECK_LAUNCH();
     return MB_OK;
   }
