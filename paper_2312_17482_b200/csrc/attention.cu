@@ -671,25 +671,26 @@ __device__ __forceinline__ float warp_colsum32(float* v, int lane) {
 
 // Backward pass 1 for this thread's 64 keys [64 ch, 64 ch + 64) of query row r:
 //   P_rj = 2^(S_rj log2e / sqrt(d) - m_h log2e |r - j| - LSE_r log2e)
-// (fp32, kept in p[]; bf16 copy into the swizzled P tile) and the partial row sum of P * dP (D_r =
-// dO_r . O_r = sum_j P_rj dP_rj, so D needs neither O nor dO from memory).  Two keys per
-// instruction on the paired fp32 pipe; MASK = false for units of exactly 128 rows (no masking).
+// in fp32, written back over S in TMEM (pass 2 reloads it; keeps 64 registers free) and as bf16
+// into the swizzled P tile, plus the partial row sum of P * dP (D_r = dO_r . O_r = sum_j P_rj
+// dP_rj, so D needs neither O nor dO from memory).  Two keys per instruction on the paired fp32
+// pipe; MASK = false for units of exactly 128 rows (no masking).
 template <bool MASK>
 __device__ __forceinline__ float bwd_pass1(uint32_t tS, uint32_t tdP, uint32_t sPa, int r, int ch, int len, float sc2,
-                                          float sl2, float lse2, float (&p)[64]) {
+                                          float sl2, float lse2) {
   float2 Dp = make_float2(0.f, 0.f);
   const float rc = (float)(r - 64 * ch);
 #pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    const int c0 = 64 * ch + 32 * c;
-    float v[32], w[32];
-    sm100::tmem_ld32(tS + c0, v);
-    sm100::tmem_ld32(tdP + c0, w);
+  for (int c = 0; c < 4; ++c) {
+    const int c0 = 64 * ch + 16 * c;
+    float v[16], w[16];
+    sm100::tmem_ld16(tS + c0, v);
+    sm100::tmem_ld16(tdP + c0, w);
     sm100::tmem_ld_wait();
-    uint32_t pp[16];
+    uint32_t pp[8];
 #pragma unroll
-    for (int jj = 0; jj < 32; jj += 2) {
-      const float j0 = (float)(32 * c + jj);
+    for (int jj = 0; jj < 16; jj += 2) {
+      const float j0 = (float)(16 * c + jj);
       const float2 dd = __fadd2_rn(make_float2(rc, rc), make_float2(-j0, -j0 - 1.f));
       const float2 t = __ffma2_rn(make_float2(fabsf(dd.x), fabsf(dd.y)), make_float2(-sl2, -sl2),
                                   make_float2(-lse2, -lse2));
@@ -699,15 +700,16 @@ __device__ __forceinline__ float bwd_pass1(uint32_t tS, uint32_t tdP, uint32_t s
         pv.x = (r < len && c0 + jj < len) ? pv.x : 0.f;
         pv.y = (r < len && c0 + jj + 1 < len) ? pv.y : 0.f;
       }
-      p[32 * c + jj] = pv.x;
-      p[32 * c + jj + 1] = pv.y;
+      v[jj] = pv.x;
+      v[jj + 1] = pv.y;
       Dp = __ffma2_rn(pv, make_float2(w[jj], w[jj + 1]), Dp);
       pp[jj >> 1] = pack_bf16x2(pv.x, pv.y);
     }
-#pragma unroll
-    for (int q4 = 0; q4 < 4; ++q4)
-      st_shared_v4(sPa + p_off(r, c0 + q4 * 8), pp[4 * q4], pp[4 * q4 + 1], pp[4 * q4 + 2], pp[4 * q4 + 3]);
+    sm100::tmem_st16(tS + c0, v);
+    st_shared_v4(sPa + p_off(r, c0), pp[0], pp[1], pp[2], pp[3]);
+    st_shared_v4(sPa + p_off(r, c0 + 8), pp[4], pp[5], pp[6], pp[7]);
   }
+  sm100::tmem_st_wait();
   return Dp.x + Dp.y;
 }
 
@@ -867,9 +869,8 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
       __syncwarp();
       sm100::mbar_wait(sp_full, i & 1);
       sm100::tc_fence_after();
-      float p[64];
-      const float Dp = len == TILE ? bwd_pass1<false>(tS + lane_off, tdP + lane_off, sPa, r, ch, len, sc2, sl2, lse2, p)
-                                   : bwd_pass1<true>(tS + lane_off, tdP + lane_off, sPa, r, ch, len, sc2, sl2, lse2, p);
+      const float Dp = len == TILE ? bwd_pass1<false>(tS + lane_off, tdP + lane_off, sPa, r, ch, len, sc2, sl2, lse2)
+                                   : bwd_pass1<true>(tS + lane_off, tdP + lane_off, sPa, r, ch, len, sc2, sl2, lse2);
       sm100::fence_proxy_async_smem();
       sm100::tc_fence_before();
       __syncwarp();
@@ -877,18 +878,22 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
       dred[ch * 128 + r] = Dp;
       named_bar_sync(1, SH_THREADS);
       const float Dr = dred[r] + dred[128 + r];
-      // pass 2: dS = P (dP - D)
+      // pass 2: dS/sqrt(d) = P (dP - D)/sqrt(d) — the 1/sqrt(d) of dQ = dS K / sqrt(d) and
+      // dK = dS^T Q / sqrt(d) is folded in here (exact for d = 64), so the readout does no scaling
+      const float Drs = -Dr * rsd;
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const int c0 = 64 * ch + 32 * c;
-        float w[32];
+        float w[32], pf[32];
+        sm100::tmem_ld32(tS + lane_off + c0, pf);  // fp32 P from pass 1
         sm100::tmem_ld32(tdP + lane_off + c0, w);
         sm100::tmem_ld_wait();
         uint32_t pd[16];
 #pragma unroll
         for (int jj = 0; jj < 32; jj += 2) {
-          const float2 ds = __fmul2_rn(make_float2(p[32 * c + jj], p[32 * c + jj + 1]),
-                                       __fadd2_rn(make_float2(w[jj], w[jj + 1]), make_float2(-Dr, -Dr)));
+          const float2 ds = __fmul2_rn(make_float2(pf[jj], pf[jj + 1]),
+                                       __ffma2_rn(make_float2(w[jj], w[jj + 1]), make_float2(rsd, rsd),
+                                                  make_float2(Drs, Drs)));
           pd[jj >> 1] = pack_bf16x2(ds.x, ds.y);
         }
 #pragma unroll
@@ -916,9 +921,10 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
         const uint32_t src = which == 0 ? tdQ : (which == 1 ? tdK : tdV);
         sm100::tmem_ld32(src + lane_off + 32 * ch, v);
         sm100::tmem_ld_wait();
-        const float sc = which == 2 ? 1.f : rsd;
+        if (!full) {  // rows past the sequence hold garbage accumulations: zero them for the column sums
 #pragma unroll
-        for (int e = 0; e < 32; ++e) v[e] = ok ? v[e] * sc : 0.f;
+          for (int e = 0; e < 32; ++e) v[e] = ok ? v[e] : 0.f;
+        }
         if (col_ok) {
           if (full) {
             // staging: dV -> P slab [0, 2K) (P was consumed by dV's MMA), dQ -> P slab [2K, 4K),
