@@ -10,6 +10,8 @@ import math
 import numpy as np
 from scipy.special import erf
 
+from .philox import dropout_keep
+
 __all__ = [
     "MB_OK", "MB_ERR_MASK_LAYOUT", "IGNORE",
     "alibi_slopes", "alibi_bias", "unpad_index", "unpad", "pad",
@@ -17,7 +19,7 @@ __all__ = [
     "attention_forward", "attention_backward",
     "encoder_layer_forward", "encoder_layer_backward",
     "embed_forward", "embed_backward", "mlm_head_forward_backward",
-    "model_forward_backward", "param_count", "mfu",
+    "model_forward_backward", "param_count", "mfu", "dropout_masks",
 ]
 
 MB_OK = 0
@@ -193,17 +195,37 @@ def _split_heads(x, n):
     return x.reshape(B, L, n, H // n)
 
 
-def encoder_layer_forward(X, mask, slopes, p, eps=1e-12):
+def dropout_masks(mask, H, dropout):
+    """Padded [B, L, H] keep/(1-p) multipliers of the two F2 dropout sites (R32) for one layer:
+    the packed row of real position (b, l) is its rank in row-major order (P:147 packing), pad
+    positions get 0.  dropout = dict(p, seed, stream) (stream = layer index) or None -> (1, 1)."""
+    if not dropout or dropout.get("p", 0.0) == 0.0:
+        return 1.0, 1.0
+    mk = np.asarray(mask).astype(bool)
+    T = int(mk.sum())
+    out = []
+    for site in (0, 1):
+        keep = dropout_keep(T, H, dropout["p"], dropout["seed"], dropout["stream"], site)
+        d = np.zeros(mk.shape + (H,))
+        d[mk] = keep / (1.0 - dropout["p"])
+        out.append(d)
+    return out[0], out[1]
+
+
+def encoder_layer_forward(X, mask, slopes, p, eps=1e-12, dropout=None):
     """X [B, L, H] padded; p = dict of W[out,in] / bias / LN params (float arrays).
       QKV = X W_qkv^T + b_qkv, columns (3, heads, d)                       (R9)
       C = ALiBi attention (Eq. 1); A = C W_o^T + b_o
-      Y1 = LN(A + X; gamma1, beta1)                                         (post-LN, R1)
+      Y1 = LN(drop_0(A) + X; gamma1, beta1)                                 (post-LN, R1)
       U = Y1 W_1v^T + b_1v; a = U[:, :I] (W1 half), g = U[:, I:] (V half)   (fused GLU P:685, R8)
       Z = GeLU(a) * g; F = Z W_2^T + b_2                                   (Eq. 2)
-      Y = LN(F + Y1; gamma2, beta2)
-    Returns Y and a cache for the backward."""
+      Y = LN(drop_1(F) + Y1; gamma2, beta2)
+    drop_s = the F2 dropout of site s ("0.1 dropout to the feedforward layers"; placement
+    after each output projection, before the residual: SURVEY §8f F2, R32); identity when
+    dropout is None or p = 0 (R13).  Returns Y and a cache for the backward."""
     X = f64(X)
     B, L, H = X.shape
+    D0, D1 = dropout_masks(mask, H, dropout)
     n = len(slopes)
     P = {k_: f64(v_) for k_, v_ in p.items()}
     QKV = X @ P["w_qkv"].T + P["b_qkv"]
@@ -212,17 +234,17 @@ def encoder_layer_forward(X, mask, slopes, p, eps=1e-12):
                                    mask, slopes)
     C = C4.reshape(B, L, H)
     A = C @ P["w_o"].T + P["b_o"]
-    S1 = A + X
+    S1 = A * D0 + X
     Y1, ln1 = layer_norm(S1, P["ln1_g"], P["ln1_b"], eps)
     U = Y1 @ P["w_1v"].T + P["b_1v"]
     I = U.shape[-1] // 2
     a, g = U[..., :I], U[..., I:]
     Z = gelu(a) * g
     F = Z @ P["w_2"].T + P["b_2"]
-    S2 = F + Y1
+    S2 = F * D1 + Y1
     Y, ln2 = layer_norm(S2, P["ln2_g"], P["ln2_b"], eps)
     cache = dict(X=X, mask=np.asarray(mask), n=n, P=P, QKV=QKV, C=C, acache=acache, S1=S1,
-                 ln1=ln1, Y1=Y1, U=U, Z=Z, S2=S2, ln2=ln2)
+                 ln1=ln1, Y1=Y1, U=U, Z=Z, S2=S2, ln2=ln2, D0=D0, D1=D1)
     return Y, cache
 
 
@@ -241,10 +263,11 @@ def encoder_layer_backward(dY, cache):
     # Y = LN2(S2)
     dS2, g_["ln2_g"], g_["ln2_b"] = layer_norm_backward(dY, cache["ln2"], P["ln2_g"])
     dS2 = dS2 * m
-    # F = Z W2^T + b2
-    g_["w_2"] = flat(dS2).T @ flat(cache["Z"])
-    g_["b_2"] = flat(dS2).sum(axis=0)
-    dZ = dS2 @ P["w_2"]
+    # S2 = drop_1(F) + Y1, F = Z W2^T + b2
+    dF = dS2 * cache["D1"]
+    g_["w_2"] = flat(dF).T @ flat(cache["Z"])
+    g_["b_2"] = flat(dF).sum(axis=0)
+    dZ = dF @ P["w_2"]
     U = cache["U"]
     a, g = U[..., :I], U[..., I:]
     da = dZ * g * gelu_grad(a)
@@ -256,9 +279,11 @@ def encoder_layer_backward(dY, cache):
     # Y1 = LN1(S1)
     dS1, g_["ln1_g"], g_["ln1_b"] = layer_norm_backward(dY1, cache["ln1"], P["ln1_g"])
     dS1 = dS1 * m
-    g_["w_o"] = flat(dS1).T @ flat(cache["C"])
-    g_["b_o"] = flat(dS1).sum(axis=0)
-    dC = dS1 @ P["w_o"]
+    # S1 = drop_0(A) + X, A = C Wo^T + bo
+    dA = dS1 * cache["D0"]
+    g_["w_o"] = flat(dA).T @ flat(cache["C"])
+    g_["b_o"] = flat(dA).sum(axis=0)
+    dC = dA @ P["w_o"]
     dq, dk, dv = attention_backward(_split_heads(dC, n), cache["acache"])
     dQKV = np.concatenate([dq.reshape(B, L, H), dk.reshape(B, L, H), dv.reshape(B, L, H)], axis=-1)
     dQKV = dQKV * m
@@ -336,8 +361,9 @@ def mlm_head_forward_backward(Y, labels, mask, hp, emb, inv_norm, eps=1e-12):
 # ---------------------------------------------------------------------------------------------
 # the whole step: embedding -> layers -> MLM head+CE -> backward
 # ---------------------------------------------------------------------------------------------
-def model_forward_backward(batch, params, slopes, eps=1e-12, inv_norm=None):
+def model_forward_backward(batch, params, slopes, eps=1e-12, inv_norm=None, dropout=None):
     """One micro-step of MosaicBERT pretraining on the padded batch (SURVEY §3 call stack 1).
+    dropout = dict(p, seed) or None: layer li uses stream li (R32).
     Returns loss and gradients for every parameter (tied E_tok receives decoder + embedding)."""
     ids, mask, labels = batch["input_ids"], batch["attention_mask"], batch["labels"]
     V = params["emb"].shape[0]
@@ -347,8 +373,9 @@ def model_forward_backward(batch, params, slopes, eps=1e-12, inv_norm=None):
     X, ecache = embed_forward(ids, params["emb"], params["type_emb"], params["lne_g"],
                               params["lne_b"], eps)
     caches = []
-    for lp in params["layers"]:
-        X, c = encoder_layer_forward(X, mask, slopes, lp, eps)
+    for li, lp in enumerate(params["layers"]):
+        dli = dict(dropout, stream=li) if dropout else None
+        X, c = encoder_layer_forward(X, mask, slopes, lp, eps, dli)
         caches.append(c)
     hp = {k: params[k] for k in ("w_t", "b_t", "lnh_g", "lnh_b", "b_dec")}
     loss, dY, hg, _ = mlm_head_forward_backward(X, labels, mask, hp, params["emb"], inv_norm, eps)
