@@ -206,15 +206,36 @@ typedef struct {
   float *w_qkv, *b_qkv, *w_o, *b_o, *ln1_g, *ln1_b, *w_1v, *b_1v, *w_2, *b_2, *ln2_g, *ln2_b;
 } mb_layer_grads;
 
+/* F2 — feed-forward dropout ("we applied 0.1 dropout to the feedforward layers"; placement
+ * and generator per reading R32): S1 = X + drop_0(C Wo^T + bo), S2 = Y1 + drop_1(Z W2^T + b2),
+ * drop_s(v)[t, f] = v[t, f] * keep_s(t, f) / (1 - p).  keep is a pure function of (seed, stream,
+ * site s, packed row t, feature f): Philox-4x32-10 (Salmon et al., SC'11) with counter
+ * (f >> 3, t, 2*stream + s, 0), key (seed & 0xffffffff, seed >> 32); the uniform of f is 16-bit
+ * field (f & 1) of output word (f & 7) >> 1; kept iff >= round(65536 p).  The backward regenerates
+ * the same mask (nothing is saved).  NULL or p == 0: no dropout.  p must be in [0, 1). */
+typedef struct {
+  float p;
+  uint64_t seed;   /* one per micro-step (and rank) */
+  int32_t stream;  /* layer index */
+} mb_dropout;
+
 MB_API size_t mb_layer_saved_bytes(const mb_dims* d, int32_t nnz);
 MB_API size_t mb_layer_workspace_bytes(const mb_dims* d, int32_t nnz, int32_t max_seqlen);
 
+/* drop: optional F2 dropout (NULL = none).  Errors: p outside [0, 1) -> MB_ERR_INVALID_ARG. */
 MB_API mb_status mb_encoder_forward(const mb_dims* d, const mb_layer_params* p, const mb_packed* pk, const float* slopes,
-                             const mb_bf16* x, mb_bf16* y, void* saved, mb_stream_t s);
-/* dx = dL/dx; dy is consumed (used as scratch).  Gradients accumulate into g (+=). */
+                             const mb_bf16* x, mb_bf16* y, void* saved, const mb_dropout* drop, mb_stream_t s);
+/* dx = dL/dx; dy is consumed (used as scratch).  Gradients accumulate into g (+=).  drop must be
+ * the forward's (same seed / stream / p): the masks are regenerated, not saved. */
 MB_API mb_status mb_encoder_backward(const mb_dims* d, const mb_layer_params* p, const mb_packed* pk, const float* slopes,
                               const mb_bf16* x, const void* saved, mb_bf16* dy, mb_bf16* dx,
-                              const mb_layer_grads* g, void* ws, size_t ws_bytes, mb_stream_t s);
+                              const mb_layer_grads* g, void* ws, size_t ws_bytes, const mb_dropout* drop,
+                              mb_stream_t s);
+/* The F2 keep mask of one site as bytes (1 = kept): out[t * cols + f] for t < rows, f < cols —
+ * exactly what the fused epilogues apply (a test hook for bit-exact mask parity).  out: device
+ * uint8 [rows, cols]; cols % 8 == 0. */
+MB_API mb_status mb_dropout_mask(const mb_dropout* drop, int32_t site, int32_t rows, int32_t cols, uint8_t* out,
+                                 mb_stream_t s);
 
 /* ---------------------------------------------------------------------------------------------
  * A3 — embedding (no position table): x0[t] = LN_e(E_tok[ids[indices[t]]] + E_type[0]).

@@ -35,6 +35,11 @@ class Packed(C.Structure):
     _fields_ = [("cu_seqlens", P), ("batch", I32), ("nnz", I32), ("max_seqlen", I32)]
 
 
+class Dropout(C.Structure):
+    """mb_dropout (F2, R32): p, seed (one per micro-step and rank), stream (layer index)."""
+    _fields_ = [("p", F32), ("seed", C.c_uint64), ("stream", I32)]
+
+
 LAYER_FIELDS = ("w_qkv", "b_qkv", "w_o", "b_o", "ln1_g", "ln1_b", "w_1v", "b_1v", "w_2", "b_2", "ln2_g", "ln2_b")
 HEAD_FIELDS = ("w_t", "b_t", "ln_g", "ln_b", "emb", "b_dec")
 
@@ -69,9 +74,11 @@ _SIGS = {
     "mb_colsum": (C.c_int, [P, I32, I32, P, P]),
     "mb_layer_saved_bytes": (SZ, [C.POINTER(Dims), I32]),
     "mb_layer_workspace_bytes": (SZ, [C.POINTER(Dims), I32, I32]),
-    "mb_encoder_forward": (C.c_int, [C.POINTER(Dims), C.POINTER(LayerPtrs), C.POINTER(Packed), P, P, P, P, P]),
+    "mb_encoder_forward": (C.c_int, [C.POINTER(Dims), C.POINTER(LayerPtrs), C.POINTER(Packed), P, P, P, P,
+                                     C.POINTER(Dropout), P]),
     "mb_encoder_backward": (C.c_int, [C.POINTER(Dims), C.POINTER(LayerPtrs), C.POINTER(Packed), P, P, P, P, P,
-                                      C.POINTER(LayerPtrs), P, SZ, P]),
+                                      C.POINTER(LayerPtrs), P, SZ, C.POINTER(Dropout), P]),
+    "mb_dropout_mask": (C.c_int, [C.POINTER(Dropout), I32, I32, I32, P, P]),
     "mb_embed_forward": (C.c_int, [C.POINTER(Dims), P, P, I32, P, P, P, P, P, P, P]),
     "mb_embed_backward": (C.c_int, [C.POINTER(Dims), P, P, I32, P, P, P, P, P, P, P, P, P, P]),
     "mb_mlm_workspace_bytes": (SZ, [C.POINTER(Dims), I32]),
@@ -276,20 +283,30 @@ def head_ptrs(p: dict) -> HeadPtrs:
     return HeadPtrs(*[_p(p[f]) for f in HEAD_FIELDS])
 
 
-def encoder_forward(d: Dims, params, packed: Packed, slopes, x, y, saved):
+def _drop(drop):
+    return C.byref(drop) if drop is not None else None
+
+
+def encoder_forward(d: Dims, params, packed: Packed, slopes, x, y, saved, drop: Dropout | None = None):
     lp = params if isinstance(params, LayerPtrs) else layer_ptrs(params)
     _ck("mb_encoder_forward", lib().mb_encoder_forward(C.byref(d), C.byref(lp), C.byref(packed), _p(slopes), _p(x),
-                                                       _p(y), _p(saved), _stream()))
+                                                       _p(y), _p(saved), _drop(drop), _stream()))
     return y
 
 
-def encoder_backward(d: Dims, params, packed: Packed, slopes, x, saved, dy, dx, grads, ws):
+def encoder_backward(d: Dims, params, packed: Packed, slopes, x, saved, dy, dx, grads, ws,
+                     drop: Dropout | None = None):
     lp = params if isinstance(params, LayerPtrs) else layer_ptrs(params)
     lg = grads if isinstance(grads, LayerPtrs) else layer_ptrs(grads)
     _ck("mb_encoder_backward", lib().mb_encoder_backward(C.byref(d), C.byref(lp), C.byref(packed), _p(slopes), _p(x),
                                                          _p(saved), _p(dy), _p(dx), C.byref(lg), _p(ws), ws.numel(),
-                                                         _stream()))
+                                                         _drop(drop), _stream()))
     return dx
+
+
+def dropout_mask(drop: Dropout, site: int, rows: int, cols: int, out):
+    _ck("mb_dropout_mask", lib().mb_dropout_mask(C.byref(drop), site, rows, cols, _p(out), _stream()))
+    return out
 
 
 def embed_forward(d: Dims, ids, indices, nnz, emb, type_emb, ln_g, ln_b, x0, stats):

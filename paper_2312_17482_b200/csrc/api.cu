@@ -70,7 +70,34 @@ mb_status check_dims(const mb_dims* d) {
 
 inline const bf16* B(const mb_bf16* p) { return reinterpret_cast<const bf16*>(p); }
 
+bool drop_ok(const mb_dropout* dr) { return !dr || (dr->p >= 0.f && dr->p < 1.f && dr->stream >= 0); }
+
+__global__ void dropout_mask_kernel(DropArgs d, int rows, int cols, uint8_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one 8-feature group
+  const int gpr = cols / 8;
+  if (i >= (int64_t)rows * gpr) return;
+  const int t = (int)(i / gpr), f0 = (int)(i - (int64_t)t * gpr) * 8;
+  const uint32_t bits = dropout_keep8(d, (uint32_t)t, (uint32_t)f0);
+  uint2 v;
+  v.x = (bits & 1u) | ((bits >> 1) & 1u) << 8 | ((bits >> 2) & 1u) << 16 | ((bits >> 3) & 1u) << 24;
+  v.y = ((bits >> 4) & 1u) | ((bits >> 5) & 1u) << 8 | ((bits >> 6) & 1u) << 16 | ((bits >> 7) & 1u) << 24;
+  *reinterpret_cast<uint2*>(out + (int64_t)t * cols + f0) = v;
+}
+
 }  // namespace
+
+// F2 (R32): host-side dropout parameters of one site; thr = 0 (off) for NULL / p == 0
+DropArgs make_drop_args(const mb_dropout* dr, int site) {
+  DropArgs a;
+  if (!dr || dr->p <= 0.f) return a;
+  a.key0 = (uint32_t)(dr->seed & 0xFFFFFFFFull);
+  a.key1 = (uint32_t)(dr->seed >> 32);
+  a.site = 2u * (uint32_t)dr->stream + (uint32_t)site;
+  a.thr = (uint32_t)std::lround((double)dr->p * 65536.0);
+  a.scale = 1.0f / (1.0f - dr->p);
+  return a;
+}
+
 }  // namespace mb
 
 extern "C" {
@@ -85,12 +112,25 @@ size_t mb_layer_workspace_bytes(const mb_dims* d, int32_t nnz, int32_t max_seqle
   return mb::Ws(nullptr, std::max(nnz, 1), d->hidden, d->intermediate, d->heads, max_seqlen).bytes;
 }
 
+mb_status mb_dropout_mask(const mb_dropout* drop, int32_t site, int32_t rows, int32_t cols, uint8_t* out,
+                          mb_stream_t s_) {
+  using namespace mb;
+  if (!drop || !out || rows < 0 || cols < 0 || site < 0 || site > 1 || !drop_ok(drop)) return MB_ERR_INVALID_ARG;
+  if (cols % 8) return MB_ERR_CONFIG;
+  if (rows == 0 || cols == 0) return MB_OK;
+  const int64_t groups = (int64_t)rows * (cols / 8);
+  dropout_mask_kernel<<<(unsigned)((groups + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(s_)>>>(
+      make_drop_args(drop, site), rows, cols, out);
+  MB_CHECK_LAUNCH();
+  return MB_OK;
+}
+
 mb_status mb_encoder_forward(const mb_dims* d, const mb_layer_params* p, const mb_packed* pk, const float* slopes,
-                             const mb_bf16* x, mb_bf16* y, void* saved, mb_stream_t s_) {
+                             const mb_bf16* x, mb_bf16* y, void* saved, const mb_dropout* drop, mb_stream_t s_) {
   using namespace mb;
   mb_status st = check_dims(d);
   if (st != MB_OK) return st;
-  if (!p || !pk || !slopes || !x || !y || !saved || !pk->cu_seqlens) return MB_ERR_INVALID_ARG;
+  if (!p || !pk || !slopes || !x || !y || !saved || !pk->cu_seqlens || !drop_ok(drop)) return MB_ERR_INVALID_ARG;
   if (pk->nnz < 0 || pk->batch < 0) return MB_ERR_INVALID_ARG;
   if (pk->max_seqlen > 512) return MB_ERR_SHAPE;
   if (pk->nnz == 0) return MB_OK;
@@ -115,6 +155,7 @@ mb_status mb_encoder_forward(const mb_dims* d, const mb_layer_params* p, const m
     GemmArgs a;
     a.M = T, a.N = H, a.K = H, a.A = sv.o, a.lda = H, a.B = B(p->w_o), a.ldb = H;
     a.ep.mode = E_BF16, a.ep.C = sv.s1, a.ep.ldc = H, a.ep.bias = B(p->b_o), a.ep.res = B(x), a.ep.ldr = H;
+    a.ep.drop = make_drop_args(drop, 0);  // F2 site 0: S1 = X + drop(O Wo^T + bo)
     TRY(gemm(a, s));
   }
   // A7: Y1 = LN1(S1)
@@ -134,6 +175,7 @@ mb_status mb_encoder_forward(const mb_dims* d, const mb_layer_params* p, const m
     GemmArgs a;
     a.M = T, a.N = H, a.K = I, a.A = sv.z, a.lda = I, a.B = B(p->w_2), a.ldb = I;
     a.ep.mode = E_BF16, a.ep.C = sv.s2, a.ep.ldc = H, a.ep.bias = B(p->b_2), a.ep.res = sv.y1, a.ep.ldr = H;
+    a.ep.drop = make_drop_args(drop, 1);  // F2 site 1: S2 = Y1 + drop(Z W2^T + b2)
     TRY(gemm(a, s));
   }
   // A7: Y = LN2(S2)
@@ -143,11 +185,12 @@ mb_status mb_encoder_forward(const mb_dims* d, const mb_layer_params* p, const m
 
 mb_status mb_encoder_backward(const mb_dims* d, const mb_layer_params* p, const mb_packed* pk, const float* slopes,
                               const mb_bf16* x, const void* saved, mb_bf16* dy, mb_bf16* dx, const mb_layer_grads* g,
-                              void* ws, size_t ws_bytes, mb_stream_t s_) {
+                              void* ws, size_t ws_bytes, const mb_dropout* drop, mb_stream_t s_) {
   using namespace mb;
   mb_status st = check_dims(d);
   if (st != MB_OK) return st;
-  if (!p || !pk || !slopes || !x || !saved || !dy || !dx || !g || !ws || !pk->cu_seqlens) return MB_ERR_INVALID_ARG;
+  if (!p || !pk || !slopes || !x || !saved || !dy || !dx || !g || !ws || !pk->cu_seqlens || !drop_ok(drop))
+    return MB_ERR_INVALID_ARG;
   if (pk->nnz < 0 || pk->batch < 0) return MB_ERR_INVALID_ARG;
   if (pk->max_seqlen > 512) return MB_ERR_SHAPE;
   if (pk->nnz == 0) return MB_OK;
@@ -156,19 +199,26 @@ mb_status mb_encoder_backward(const mb_dims* d, const mb_layer_params* p, const 
   Saved sv(reinterpret_cast<char*>(const_cast<void*>(saved)), T, H, I, nh);
   Ws w(reinterpret_cast<char*>(ws), T, H, I, nh, pk->max_seqlen);
   if (ws_bytes < w.bytes) return MB_ERR_WORKSPACE;
-  // LN2 backward: dS2; dgamma2, dbeta2; db2 = column sums of dS2 (same pass)
+  // F2: with dropout the projection branches see dF = dS2 * keep / (1 - p) (dp2) and dA = dS1 * keep
+  // / (1 - p) (dp1), while the residual branches keep dS2 / dS1.  dp2 lives in w.dy1 (written only
+  // after its last reader, dW2) and dp1 in the front of w.dqkv (written only by the attention
+  // backward, after dWo).  Without dropout dp = dS.
+  const DropArgs dr2 = make_drop_args(drop, 1), dr1 = make_drop_args(drop, 0);
+  bf16* dp2 = dr2.thr ? w.dy1 : w.ds2;
+  bf16* dp1 = dr1.thr ? w.dqkv : w.ds1;
+  // LN2 backward: dS2 (and dp2); dgamma2, dbeta2; db2 = column sums of dp2 (same pass)
   TRY(layernorm_bwd(reinterpret_cast<bf16*>(dy), sv.s2, sv.st2, B(p->ln2_g), T, H, nullptr, w.ds2, g->ln2_g,
-                    g->ln2_b, g->b_2, s));
-  {  // dZ = dS2 W2 fused with the GeGLU backward -> dU = dZ * Gd = [dZ g GeLU'(a) | dZ GeLU(a)]
+                    g->ln2_b, g->b_2, s, &dr2, dr2.thr ? dp2 : nullptr));
+  {  // dZ = dF W2 fused with the GeGLU backward -> dU = dZ * Gd = [dZ g GeLU'(a) | dZ GeLU(a)]
     GemmArgs a;
-    a.M = T, a.N = I, a.K = H, a.A = w.ds2, a.lda = H, a.B = B(p->w_2), a.ldb = I, a.b_t = true;
+    a.M = T, a.N = I, a.K = H, a.A = dp2, a.lda = H, a.B = B(p->w_2), a.ldb = I, a.b_t = true;
     a.ep.mode = E_GEGLU_BWD, a.ep.C = w.du, a.ep.ldc = 2 * I, a.ep.U = sv.u, a.ep.ldu = 2 * I, a.ep.I = I;
     a.ep.dbias = g->b_1v;  // db1v = column sums of dU, from the smem tile before its TMA store
     TRY(gemm(a, s));
   }
-  {  // dW2 += dS2^T Z
+  {  // dW2 += dF^T Z
     GemmArgs a;
-    a.M = H, a.N = I, a.K = T, a.A = w.ds2, a.lda = H, a.a_t = true, a.B = sv.z, a.ldb = I, a.b_t = true;
+    a.M = H, a.N = I, a.K = T, a.A = dp2, a.lda = H, a.a_t = true, a.B = sv.z, a.ldb = I, a.b_t = true;
     a.ep.mode = E_F32_ACC, a.ep.C = g->w_2, a.ep.ldc = I;
     TRY(gemm(a, s));
   }
@@ -184,17 +234,18 @@ mb_status mb_encoder_backward(const mb_dims* d, const mb_layer_params* p, const 
     a.ep.mode = E_F32_ACC, a.ep.C = g->w_1v, a.ep.ldc = H;
     TRY(gemm(a, s));
   }
-  // LN1 backward: dS1; dgamma1, dbeta1; dbo = column sums of dS1 (same pass)
-  TRY(layernorm_bwd(w.dy1, sv.s1, sv.st1, B(p->ln1_g), T, H, nullptr, w.ds1, g->ln1_g, g->ln1_b, g->b_o, s));
-  {  // dO = dS1 Wo
+  // LN1 backward: dS1 (and dp1); dgamma1, dbeta1; dbo = column sums of dp1 (same pass)
+  TRY(layernorm_bwd(w.dy1, sv.s1, sv.st1, B(p->ln1_g), T, H, nullptr, w.ds1, g->ln1_g, g->ln1_b, g->b_o, s, &dr1,
+                    dr1.thr ? dp1 : nullptr));
+  {  // dO = dA Wo
     GemmArgs a;
-    a.M = T, a.N = H, a.K = H, a.A = w.ds1, a.lda = H, a.B = B(p->w_o), a.ldb = H, a.b_t = true;
+    a.M = T, a.N = H, a.K = H, a.A = dp1, a.lda = H, a.B = B(p->w_o), a.ldb = H, a.b_t = true;
     a.ep.mode = E_BF16, a.ep.C = w.dO, a.ep.ldc = H;
     TRY(gemm(a, s));
   }
-  {  // dWo += dS1^T O
+  {  // dWo += dA^T O
     GemmArgs a;
-    a.M = H, a.N = H, a.K = T, a.A = w.ds1, a.lda = H, a.a_t = true, a.B = sv.o, a.ldb = H, a.b_t = true;
+    a.M = H, a.N = H, a.K = T, a.A = dp1, a.lda = H, a.a_t = true, a.B = sv.o, a.ldb = H, a.b_t = true;
     a.ep.mode = E_F32_ACC, a.ep.C = g->w_o, a.ep.ldc = H;
     TRY(gemm(a, s));
   }

@@ -118,6 +118,44 @@ __device__ __forceinline__ void norm_cdf_pdf2(float2 x, float2& cdf, float2& pdf
   cdf = __ffma2_rn(sg, h, make_float2(0.5f, 0.5f));
   pdf = __fmul2_rn(e, make_float2(0.3989422804014327f, 0.3989422804014327f));
 }
+// ---- F2 dropout (reading R32): Philox-4x32-10 (Salmon et al., SC'11) keyed by the seed,
+// counter (f >> 3, packed row t, 2*stream + site, 0); 16-bit field (f & 1) of word (f & 7) >> 1 is
+// the uniform of feature f; kept iff >= thr = round(65536 p).
+struct DropArgs {
+  uint32_t key0 = 0, key1 = 0;  // seed mod 2^32, seed >> 32
+  uint32_t site = 0;            // 2 * stream + {0: attention out-proj, 1: FFN down-proj}
+  uint32_t thr = 0;             // 0 = dropout off
+  float scale = 1.f;            // 1 / (1 - p)
+};
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+  }
+  return c;
+}
+// keep bits of features [f0, f0 + 8) (f0 % 8 == 0) of packed row t: bit j <-> feature f0 + j
+__device__ __forceinline__ uint32_t dropout_keep8(const DropArgs& d, uint32_t t, uint32_t f0) {
+  const uint4 w = philox4x32_10(make_uint4(f0 >> 3, t, d.site, 0u), d.key0, d.key1);
+  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+  uint32_t bits = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) bits |= (uint32_t)(((ws[j >> 1] >> (16 * (j & 1))) & 0xFFFFu) >= d.thr) << j;
+  return bits;
+}
+// v[0..8) of features f0.. of row t -> v * keep * scale
+__device__ __forceinline__ void dropout_apply8(const DropArgs& d, uint32_t t, uint32_t f0, float* v) {
+  const uint32_t bits = dropout_keep8(d, t, f0);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v[j] = ((bits >> j) & 1u) ? v[j] * d.scale : 0.f;
+}
+
 __device__ __forceinline__ float gelu_f(float x) {
   float c, p;
   norm_cdf_pdf(x, c, p);

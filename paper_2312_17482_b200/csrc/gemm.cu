@@ -524,6 +524,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] += b[j];
             }
+            if (CE == 2 && row_ok) {  // F2 dropout of the projection output, before the residual
+#pragma unroll
+              for (int g8 = 0; g8 < 4; ++g8) dropout_apply8(ep.drop, (uint32_t)row, (uint32_t)(col + 8 * g8), v + 8 * g8);
+            }
             if (ep.res) {
               float r[32];
               scr_row_read(scrA, lane, r);
@@ -853,7 +857,8 @@ mb_status gemm(const GemmArgs& g, cudaStream_t s) {
   // W1 + the matching 128 of V).
   const bool geglu_bwd = g.ep.mode == E_GEGLU_BWD;
   const bool ce_mode = g.ep.mode == E_LSE || g.ep.mode == E_DZ;  // partial-statistics layout assumes 256
-  const int BN = (paired || ce_mode) ? 256 : ((g.N <= 128 || geglu_bwd) ? 128 : 256);
+  const bool drop_mode = g.ep.mode == E_BF16 && g.ep.drop.thr;  // F2 variant exists for BN = 256 only
+  const int BN = (paired || ce_mode || drop_mode) ? 256 : ((g.N <= 128 || geglu_bwd) ? 128 : 256);
   // CG = 2 (generic kernel): pair tiles of 256 rows; each CTA loads 128 rows of A and BN/2 of B's N.
   constexpr int CGV = 2;
   CUtensorMap ta, tb;
@@ -933,6 +938,10 @@ mb_status gemm(const GemmArgs& g, cudaStream_t s) {
     MB_REQUIRE(!g.a_t && !g.b_t && g.ep.labels && g.ep.bias && BN == 256, MB_ERR_CONFIG);
     MB_REQUIRE(g.ep.mode == E_DZ ? g.ep.lse != nullptr : (g.ep.part && g.ep.zlab), MB_ERR_INVALID_ARG);
     return launch<256, 6, 0, 0, 0, 1, 2, 2, 1>(g, ta, tb, sc, s);
+  }
+  if (g.ep.mode == E_BF16 && g.ep.drop.thr) {  // F2: bias -> dropout -> residual (forward projections)
+    MB_REQUIRE(!g.a_t && !g.b_t && BN == 256, MB_ERR_CONFIG);
+    return launch<256, 6, 0, 0, 0, 1, 2, 2, 2>(g, ta, tb, sc, s);
   }
   if (BN == 256) return dispatch_majors<256, 6, 1>(g, ta, tb, sc, s);
   return dispatch_majors<128, 8, 1>(g, ta, tb, sc, s);

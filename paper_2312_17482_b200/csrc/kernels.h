@@ -29,6 +29,8 @@ struct Epi {
   float* zlab = nullptr;
   int npart = 0;
   float inv_norm = 1.f;
+  // F2 dropout between bias and residual (E_BF16 with drop.thr > 0; compiled into one variant)
+  DropArgs drop;
 };
 
 struct GemmArgs {
@@ -46,8 +48,12 @@ mb_status gemm(const GemmArgs& g, cudaStream_t s);
 
 mb_status layernorm_fwd(const bf16* x, const bf16* gamma, const bf16* beta, int n, int H, float eps, bf16* y,
                         float* stats, cudaStream_t s);
+// drop.thr > 0 (F2 backward): dx = dL/d(LN input) (the residual path) and dxd = dx * keep * scale
+// (the gradient of the dropped projection output); dsum then sums dxd
 mb_status layernorm_bwd(const bf16* dy, const bf16* x, const float* stats, const bf16* gamma, int n, int H,
-                        const bf16* gelu_pre, bf16* dx, float* dgamma, float* dbeta, float* dsum, cudaStream_t s);
+                        const bf16* gelu_pre, bf16* dx, float* dgamma, float* dbeta, float* dsum, cudaStream_t s,
+                        const DropArgs* drop = nullptr, bf16* dxd = nullptr);
+DropArgs make_drop_args(const mb_dropout* d, int site);
 mb_status gather_rows(const bf16* src, const int* idx, int n, int H, bf16* dst, cudaStream_t s);
 mb_status scatter_rows(const bf16* src, const int* idx, int n, int H, int rows, bf16* dst, cudaStream_t s);
 

@@ -117,12 +117,12 @@ __device__ __forceinline__ void cta_column_reduce(const float* acc, float* sbuf,
   }
 }
 
-template <int VPL, bool EMBED, bool GELU, bool DSUM>
+template <int VPL, bool EMBED, bool GELU, bool DSUM, bool DROP = false>
 __global__ void __launch_bounds__(LN_THREADS, VPL <= 3 ? 2 : 1)
     ln_bwd_kernel(RowSrc src, const bf16* __restrict__ dy, const float* __restrict__ stats,
                   const bf16* __restrict__ gamma, const bf16* __restrict__ gelu_pre, int n, int H, bf16* dx,
                   float* __restrict__ d_emb, float* __restrict__ dgamma, float* __restrict__ dbeta,
-                  float* __restrict__ dsum) {
+                  float* __restrict__ dsum, DropArgs drop, bf16* __restrict__ dxd) {
   // Register budget (2 CTAs x 8 warps per SM): per lane only x-hat and the three column
   // accumulators stay live; dy and gamma are re-read (L1 hits) in the second pass.
   extern __shared__ float sbuf[];
@@ -178,11 +178,17 @@ __global__ void __launch_bounds__(LN_THREADS, VPL <= 3 ? 2 : 1)
 #pragma unroll
           for (int j = 0; j < 8; ++j) o[j] *= gelu_grad_f(p[j]);
         }
+        if (DROP) {  // F2: dx is the residual-path gradient; dxd = dx * keep / (1 - p) feeds the projection
+          *reinterpret_cast<uint4*>(dx + (size_t)row * H + c) = f32_to_bf16x8(o);
+          dropout_apply8(drop, (uint32_t)row, (uint32_t)c, o);
+        }
         if (DSUM) {
 #pragma unroll
           for (int j = 0; j < 8; ++j) acc_s[i * 8 + j] += o[j];
         }
-        if (EMBED) {
+        if (DROP) {
+          *reinterpret_cast<uint4*>(dxd + (size_t)row * H + c) = f32_to_bf16x8(o);
+        } else if (EMBED) {
           float* dst = d_emb + (size_t)id * H + c;
           red_add_v4(dst, o[0], o[1], o[2], o[3]);
           red_add_v4(dst + 4, o[4], o[5], o[6], o[7]);
@@ -221,12 +227,12 @@ __global__ void colsum_kernel(const bf16* __restrict__ x, int n, int C, int rows
 // shared memory (double-buffered by row parity, one named barrier per row).
 constexpr int LNW_GROUPS = 4;  // row groups (rows in flight) per CTA
 
-template <int W, bool EMBED, bool GELU, bool DSUM>
+template <int W, bool EMBED, bool GELU, bool DSUM, bool DROP = false>
 __global__ void __launch_bounds__(LNW_GROUPS * W * 32)
     ln_bwd_w_kernel(RowSrc src, const bf16* __restrict__ dy, const float* __restrict__ stats,
                     const bf16* __restrict__ gamma, const bf16* __restrict__ gelu_pre, int n, int H, bf16* dx,
                     float* __restrict__ d_emb, float* __restrict__ dgamma, float* __restrict__ dbeta,
-                    float* __restrict__ dsum) {
+                    float* __restrict__ dsum, DropArgs drop, bf16* __restrict__ dxd) {
   __shared__ float red[LNW_GROUPS][2][W][2];
   extern __shared__ float sbuf[];  // [LNW_GROUPS][H] for the final column reduction
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -309,11 +315,17 @@ __global__ void __launch_bounds__(LNW_GROUPS * W * 32)
 #pragma unroll
       for (int j = 0; j < 8; ++j) o[j] *= gelu_grad_f(p[j]);
     }
+    if (DROP) {  // F2: dx is the residual-path gradient; dxd = dx * keep / (1 - p) feeds the projection
+      *reinterpret_cast<uint4*>(dx + (size_t)row * H + c) = f32_to_bf16x8(o);
+      dropout_apply8(drop, (uint32_t)row, (uint32_t)c, o);
+    }
     if (DSUM) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) as[j] += o[j];
     }
-    if (EMBED) {
+    if (DROP) {
+      *reinterpret_cast<uint4*>(dxd + (size_t)row * H + c) = f32_to_bf16x8(o);
+    } else if (EMBED) {
       float* dst = d_emb + (size_t)id * H + c;
       red_add_v4(dst, o[0], o[1], o[2], o[3]);
       red_add_v4(dst + 4, o[4], o[5], o[6], o[7]);
@@ -342,15 +354,19 @@ __global__ void __launch_bounds__(LNW_GROUPS * W * 32)
 template <int W, bool EMBED>
 mb_status ln_bwd_w_launch(const RowSrc& src, const bf16* dy, const float* stats, const bf16* gamma,
                           const bf16* gelu_pre, int n, int H, bf16* dx, float* d_emb, float* dg, float* db,
-                          float* dsum, cudaStream_t s) {
+                          float* dsum, cudaStream_t s, const DropArgs& drop, bf16* dxd) {
   const int threads = LNW_GROUPS * W * 32;
   const int smem = LNW_GROUPS * H * sizeof(float);
   const int blocks_per_sm = std::max(1, 2048 / threads);
   const int grid = std::max(1, std::min((n + LNW_GROUPS - 1) / LNW_GROUPS, blocks_per_sm * num_sms()));
 #define LNW_GO(G, D)                                                                                          \
   ln_bwd_w_kernel<W, EMBED, G, D><<<grid, threads, smem, s>>>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, \
-                                                               dg, db, dsum)
-  if (gelu_pre && dsum) LNW_GO(true, true);
+                                                               dg, db, dsum, drop, dxd)
+  if (!EMBED && drop.thr) {
+    if (gelu_pre || !dsum || !dxd) return MB_ERR_INVALID_ARG;
+    ln_bwd_w_kernel<W, false, false, true, true><<<grid, threads, smem, s>>>(src, dy, stats, gamma, gelu_pre, n, H,
+                                                                             dx, d_emb, dg, db, dsum, drop, dxd);
+  } else if (gelu_pre && dsum) LNW_GO(true, true);
   else if (gelu_pre) LNW_GO(true, false);
   else if (dsum) LNW_GO(false, true);
   else LNW_GO(false, false);
@@ -379,21 +395,26 @@ mb_status ln_fwd_dispatch(const RowSrc& src, const bf16* gamma, const bf16* beta
 template <int VPL, bool EMBED>
 mb_status ln_bwd_launch(const RowSrc& src, const bf16* dy, const float* stats, const bf16* gamma,
                         const bf16* gelu_pre, int n, int H, bf16* dx, float* d_emb, float* dg, float* db,
-                        float* dsum, cudaStream_t s) {
+                        float* dsum, cudaStream_t s, const DropArgs& drop, bf16* dxd) {
   const int smem = LN_WARPS * H * sizeof(float);
   const int grid = std::max(1, std::min((n + LN_WARPS - 1) / LN_WARPS, (VPL <= 3 ? 2 : 1) * num_sms()));
-  if (gelu_pre && dsum)
+  if (!EMBED && drop.thr) {
+    if (gelu_pre || !dsum || !dxd) return MB_ERR_INVALID_ARG;
+    ln_bwd_kernel<VPL, false, false, true, true><<<grid, LN_THREADS, smem, s>>>(src, dy, stats, gamma, gelu_pre, n,
+                                                                                H, dx, d_emb, dg, db, dsum, drop,
+                                                                                dxd);
+  } else if (gelu_pre && dsum)
     ln_bwd_kernel<VPL, EMBED, true, true><<<grid, LN_THREADS, smem, s>>>(src, dy, stats, gamma, gelu_pre, n, H, dx,
-                                                                          d_emb, dg, db, dsum);
+                                                                          d_emb, dg, db, dsum, drop, dxd);
   else if (gelu_pre)
     ln_bwd_kernel<VPL, EMBED, true, false><<<grid, LN_THREADS, smem, s>>>(src, dy, stats, gamma, gelu_pre, n, H, dx,
-                                                                           d_emb, dg, db, dsum);
+                                                                           d_emb, dg, db, dsum, drop, dxd);
   else if (dsum)
     ln_bwd_kernel<VPL, EMBED, false, true><<<grid, LN_THREADS, smem, s>>>(src, dy, stats, gamma, gelu_pre, n, H,
-                                                                           dx, d_emb, dg, db, dsum);
+                                                                           dx, d_emb, dg, db, dsum, drop, dxd);
   else
     ln_bwd_kernel<VPL, EMBED, false, false><<<grid, LN_THREADS, smem, s>>>(src, dy, stats, gamma, gelu_pre, n, H,
-                                                                            dx, d_emb, dg, db, dsum);
+                                                                            dx, d_emb, dg, db, dsum, drop, dxd);
   MB_CHECK_LAUNCH();
   return MB_OK;
 }
@@ -401,17 +422,17 @@ mb_status ln_bwd_launch(const RowSrc& src, const bf16* dy, const float* stats, c
 template <bool EMBED>
 mb_status ln_bwd_dispatch(const RowSrc& src, const bf16* dy, const float* stats, const bf16* gamma,
                           const bf16* gelu_pre, int n, int H, bf16* dx, float* d_emb, float* dg, float* db,
-                          float* dsum, cudaStream_t s) {
+                          float* dsum, cudaStream_t s, const DropArgs& drop = DropArgs(), bf16* dxd = nullptr) {
   if (n == 0) return MB_OK;
-  if (H == 768) return ln_bwd_w_launch<3, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s);
-  if (H == 1024) return ln_bwd_w_launch<4, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s);
-  if (H == 512) return ln_bwd_w_launch<2, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s);
-  if (H == 256) return ln_bwd_w_launch<1, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s);
+  if (H == 768) return ln_bwd_w_launch<3, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s, drop, dxd);
+  if (H == 1024) return ln_bwd_w_launch<4, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s, drop, dxd);
+  if (H == 512) return ln_bwd_w_launch<2, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s, drop, dxd);
+  if (H == 256) return ln_bwd_w_launch<1, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s, drop, dxd);
   switch ((H / 8 + 31) / 32) {
-    case 1: return ln_bwd_launch<1, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s);
-    case 2: return ln_bwd_launch<2, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s);
-    case 3: return ln_bwd_launch<3, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s);
-    case 4: return ln_bwd_launch<4, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s);
+    case 1: return ln_bwd_launch<1, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s, drop, dxd);
+    case 2: return ln_bwd_launch<2, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s, drop, dxd);
+    case 3: return ln_bwd_launch<3, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s, drop, dxd);
+    case 4: return ln_bwd_launch<4, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s, drop, dxd);
   }
   return MB_ERR_CONFIG;
 }
@@ -425,9 +446,12 @@ mb_status layernorm_fwd(const bf16* x, const bf16* gamma, const bf16* beta, int 
 }
 
 mb_status layernorm_bwd(const bf16* dy, const bf16* x, const float* stats, const bf16* gamma, int n, int H,
-                        const bf16* gelu_pre, bf16* dx, float* dgamma, float* dbeta, float* dsum, cudaStream_t s) {
+                        const bf16* gelu_pre, bf16* dx, float* dgamma, float* dbeta, float* dsum, cudaStream_t s,
+                        const DropArgs* drop, bf16* dxd) {
   RowSrc src{x, nullptr, nullptr, nullptr, nullptr};
-  return ln_bwd_dispatch<false>(src, dy, stats, gamma, gelu_pre, n, H, dx, nullptr, dgamma, dbeta, dsum, s);
+  const DropArgs none;
+  return ln_bwd_dispatch<false>(src, dy, stats, gamma, gelu_pre, n, H, dx, nullptr, dgamma, dbeta, dsum, s,
+                                drop ? *drop : none, dxd);
 }
 
 mb_status embed_ln_fwd(const EmbedSrc& e, const bf16* gamma, const bf16* beta, int n, int H, float eps, bf16* y,

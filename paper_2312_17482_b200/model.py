@@ -93,7 +93,14 @@ class MosaicBert:
     """MosaicBERT encoder + MLM head whose forward/backward run in libmosaicbert.so."""
 
     def __init__(self, dims: ModelDims, params: dict | None = None, device: str | torch.device = "cuda",
-                 process_group=None):
+                 process_group=None, dropout: float = 0.0, seed: int = 0):
+        """dropout: F2 feed-forward dropout probability (P:152 uses 0.1; R13/R32).  Each micro-step
+        draws its masks from seed_of(micro-step), a pure function of (seed, rank, micro-step index)."""
+        if not 0.0 <= dropout < 1.0:
+            raise ValueError("dropout must be in [0, 1)")
+        self.dropout = float(dropout)
+        self.seed = int(seed)
+        self.micro_index = 0
         self.d = dims
         self.cd = dims.c()
         self.device = torch.device(device)
@@ -171,10 +178,22 @@ class MosaicBert:
         self._nm_cap = cap
 
     # ------------------------------------------------------------------ one micro-step
+    def seed_of(self, micro_index: int) -> int:
+        """64-bit dropout seed of one micro-step: a fixed mix of (seed, rank, micro-step index)."""
+        rank = dist.get_rank(self.pg) if self._dp() else 0
+        x = (self.seed * 0x9E3779B97F4A7C15 + rank * 0xBF58476D1CE4E5B9 + micro_index * 0x94D049BB133111EB)
+        return x & 0xFFFFFFFFFFFFFFFF
+
     def micro_step(self, ids: torch.Tensor, mask: torch.Tensor, labels: torch.Tensor, inv_norm: float = 1.0,
-                   allreduce: bool = False, timers: dict | None = None):
+                   allreduce: bool = False, timers: dict | None = None, drop_seed: int | None = None):
         """Forward + backward of one micro-batch (device int32 [B, L] tensors, right-padded).
-        Gradients accumulate (+=) into the buckets.  Returns (nnz, n_masked)."""
+        Gradients accumulate (+=) into the buckets.  With dropout, layer l uses mb_dropout(p,
+        drop_seed or seed_of(micro-step), stream=l).  Returns (nnz, n_masked)."""
+        if drop_seed is None:
+            drop_seed = self.seed_of(self.micro_index)
+        self.micro_index += 1
+        drops = ([L.Dropout(self.dropout, drop_seed, l) for l in range(self.d.layers)] if self.dropout > 0
+                 else [None] * self.d.layers)
         B, Lq = mask.shape
         self._ensure(B, Lq)
         cd = self.cd
@@ -199,7 +218,7 @@ class MosaicBert:
         # A4-A9: encoder layers
         lps = [L.layer_ptrs(b.p) for b in self.layer_buckets]
         for l in range(self.d.layers):
-            L.encoder_forward(cd, lps[l], packed, self.slopes, self.xs[l], self.xs[l + 1], self.saved[l])
+            L.encoder_forward(cd, lps[l], packed, self.slopes, self.xs[l], self.xs[l + 1], self.saved[l], drops[l])
         # A11: MLM head + CE (fwd + bwd)
         self._ensure_head(max(n_m, 1))
         dy, dx = self.dy
@@ -216,7 +235,7 @@ class MosaicBert:
         # backward through the layers; each bucket's allreduce is issued as soon as it is final
         for l in range(self.d.layers - 1, -1, -1):
             L.encoder_backward(cd, lps[l], packed, self.slopes, self.xs[l], self.saved[l], dy, dx,
-                               L.layer_ptrs(self.layer_buckets[l].gv), self.ws)
+                               L.layer_ptrs(self.layer_buckets[l].gv), self.ws, drops[l])
             dy, dx = dx, dy
             if allreduce:
                 handles.append(self._allreduce(self.layer_buckets[l]))

@@ -32,6 +32,7 @@ def declared_symbols():
 def test_header_declares_abi():
     syms = declared_symbols()
     for s in ("mb_unpad_index", "mb_encoder_forward", "mb_encoder_backward", "mb_mlm_loss", "mb_alibi_slopes",
+              "mb_dropout_mask",
               "mb_gather_rows", "mb_scatter_rows", "mb_embed_forward", "mb_embed_backward"):
         assert s in syms
 
@@ -70,10 +71,14 @@ def test_host_argument_errors(lib):
     d = _lib.dims(96, 5, 256, 128)  # hidden % heads != 0
     lp = _lib.LayerPtrs()
     pk = _lib.Packed(1, 1, 1, 1)
-    assert lib.mb_encoder_forward(ctypes.byref(d), ctypes.byref(lp), ctypes.byref(pk), 1, 1, 1, 1, None) == 2
+    assert lib.mb_encoder_forward(ctypes.byref(d), ctypes.byref(lp), ctypes.byref(pk), 1, 1, 1, 1, None, None) == 2
     d = _lib.dims(64, 1, 256, 128)  # head_dim 64 ok, but I=256 ok -> null ptrs -> invalid arg
     assert lib.mb_encoder_forward(ctypes.byref(d), ctypes.byref(lp), ctypes.byref(pk), None, None, None, None,
-                                  None) == 1
+                                  None, None) == 1
+    bad = _lib.Dropout(1.5, 0, 0)  # p outside [0, 1)
+    assert lib.mb_dropout_mask(ctypes.byref(bad), 0, 4, 8, 1, None) == 1
+    ok = _lib.Dropout(0.1, 0, 0)
+    assert lib.mb_dropout_mask(ctypes.byref(ok), 0, 4, 12, 1, None) == 2  # cols % 8 != 0
     assert lib.mb_status_string(4) == b"MB_ERR_MASK_LAYOUT"
 
 

@@ -24,13 +24,15 @@ def _need_gpu():
     mb.lib()
 
 
-def _layer_parity(dims, lens, Lmax, regime, seed):
+def _layer_parity(dims, lens, Lmax, regime, seed, dropout=None):
+    """dropout: None or dict(p, seed, stream) (F2, R32) — the same mask is regenerated on both sides."""
     H, n = dims.hidden, dims.heads
     p = synth.make_layer_params(dims, seed, regime)
     mask = synth.mask_from_lengths(np.array(lens), Lmax)
     X = synth.make_hidden(mask, H, seed + 1)
     dY = synth.make_grad(mask, H, seed + 2)
-    Y, c = O.encoder_layer_forward(X, mask, O.alibi_slopes(n), p, dims.ln_eps)
+    Y, c = O.encoder_layer_forward(X, mask, O.alibi_slopes(n), p, dims.ln_eps, dropout)
+    drop = L.Dropout(dropout["p"], dropout["seed"], dropout["stream"]) if dropout else None
     dX, g = O.encoder_layer_backward(dY, c)
     B = len(lens)
     cu, idx, meta = mb.unpad_index(to_dev(mask, I32))
@@ -44,12 +46,12 @@ def _layer_parity(dims, lens, Lmax, regime, seed):
     mb.gather_rows(to_dev(X.reshape(B * Lmax, H), torch.float32).to(BF), idx, nnz, x)
     y = torch.empty_like(x)
     saved = torch.empty(L.layer_saved_bytes(cd, nnz), dtype=torch.uint8, device="cuda")
-    mb.encoder_forward(cd, pd, pk, slopes, x, y, saved)
+    mb.encoder_forward(cd, pd, pk, slopes, x, y, saved, drop)
     dy = torch.empty_like(x)
     mb.gather_rows(to_dev(dY.reshape(B * Lmax, H), torch.float32).to(BF), idx, nnz, dy)
     dx = torch.empty_like(x)
     ws = torch.empty(L.layer_workspace_bytes(cd, nnz, maxlen), dtype=torch.uint8, device="cuda")
-    mb.encoder_backward(cd, pd, pk, slopes, x, saved, dy, dx, gd, ws)
+    mb.encoder_backward(cd, pd, pk, slopes, x, saved, dy, dx, gd, ws, drop)
     torch.cuda.synchronize()
     oidx = O.unpad_index(mask)[1]
     check("layer.Y", np64(y), O.unpad(Y, oidx))
@@ -79,16 +81,48 @@ def test_layer_large_dims():
     _layer_parity(synth.LARGE, [128, 128, 40], 128, "stress", 6)
 
 
-def _model_parity(dims, batch, params, tol_loss=1e-2):
+# ----------------------------------------------------------------------------- F2 dropout (R32)
+@pytest.mark.parametrize("site", [0, 1])
+@pytest.mark.parametrize("p", [0.1, 0.5])
+def test_dropout_mask_bitexact(site, p):
+    """The device Philox mask (the function the fused epilogues call) equals the oracle's, bit for
+    bit, including a 64-bit seed whose high word matters and a ragged row count."""
+    from oracle.philox import dropout_keep
+    rows, cols, seed, stream = 1003, 768, (1 << 40) + 12345, 7
+    out = torch.empty(rows, cols, dtype=torch.uint8, device="cuda")
+    L.dropout_mask(L.Dropout(p, seed, stream), site, rows, cols, out)
+    torch.cuda.synchronize()
+    ref = dropout_keep(rows, cols, p, seed, stream, site)
+    assert np.array_equal(out.cpu().numpy().astype(bool), ref)
+
+
+@pytest.mark.parametrize("regime", ["stress", "bert"])
+def test_layer_tiny_dropout(regime):
+    _layer_parity(synth.TINY, [16, 9, 3, 1], 16, regime, 2, dict(p=0.1, seed=77, stream=1))
+
+
+def test_layer_base_dropout_ragged():
+    lens = synth.make_lengths("lognormal", 12, 128, synth.rng_for(7))
+    lens[0] = 128
+    _layer_parity(synth.BASE, list(lens), 128, "bert", 8, dict(p=0.1, seed=(3 << 33) + 5, stream=11))
+
+
+def test_layer_base_dropout_high_p():
+    """p = 0.5 makes any mask disagreement between the epilogue / LN-backward and the oracle large."""
+    _layer_parity(synth.BASE, [128, 77, 128], 128, "stress", 9, dict(p=0.5, seed=4242, stream=0))
+
+
+def _model_parity(dims, batch, params, tol_loss=1e-2, dropout=None):
     model = mb.MosaicBert(mb.ModelDims(dims.hidden, dims.heads, dims.intermediate, dims.vocab,
-                                       len(params["layers"]), dims.ln_eps), params)
+                                       len(params["layers"]), dims.ln_eps), params,
+                          dropout=dropout["p"] if dropout else 0.0)
     n_lab = int(((batch["labels"] != -100) & (batch["attention_mask"] != 0)).sum())
     model.zero_grad()
     ids, mask, labels = (to_dev(batch[k], I32) for k in ("input_ids", "attention_mask", "labels"))
-    model.micro_step(ids, mask, labels, inv_norm=1.0 / n_lab)
+    model.micro_step(ids, mask, labels, inv_norm=1.0 / n_lab, drop_seed=dropout["seed"] if dropout else None)
     torch.cuda.synchronize()
     loss = float(model.loss_sum.item())
-    oloss, og = O.model_forward_backward(batch, params, O.alibi_slopes(dims.heads), dims.ln_eps)
+    oloss, og = O.model_forward_backward(batch, params, O.alibi_slopes(dims.heads), dims.ln_eps, dropout=dropout)
     assert abs(loss - oloss) <= tol_loss, (loss, oloss)
     gg = model.grads_numpy()
     for k in ("emb", "type_emb", "lne_g", "lne_b", "w_t", "b_t", "lnh_g", "lnh_b", "b_dec"):
@@ -112,6 +146,13 @@ def test_model_step_base_two_layers():
     params = synth.make_model_params(synth.BASE, 9, "bert", n_layers=2)
     batch = synth.make_batch("C5", 5001, B=6)
     _model_parity(synth.BASE, batch, params)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_model_step_c1_dropout(seed):
+    params = synth.make_model_params(synth.TINY, 20 + seed, "bert")
+    batch = synth.make_batch("C1", 300 + seed)
+    _model_parity(synth.TINY, batch, params, dropout=dict(p=0.1, seed=555 + seed))
 
 
 def test_loss_zero_decoder_is_lnV():
