@@ -176,6 +176,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--micro", type=int, default=None, help="override the per-GPU micro-batch")
+    ap.add_argument("--dropout", type=float, default=0.0,
+                    help="F2 feed-forward dropout p (P:152 trains with 0.1; the §8(a) hot path is p = 0, R13)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -197,7 +199,7 @@ def main():
     micro = args.micro or cfg.micro_batch
     dims = ModelDims(d.hidden, d.heads, d.intermediate, d.vocab, d.layers, d.ln_eps)
     params = synth.make_model_params(d, 0, "bert")  # random BERT init (never zeros: B200 is power-capped)
-    model = MosaicBert(dims, params, device=f"cuda:{local}", process_group=None)
+    model = MosaicBert(dims, params, device=f"cuda:{local}", process_group=None, dropout=args.dropout, seed=rank)
     del params
     n_params = param_count(dims)
 
@@ -320,7 +322,7 @@ def main():
                        "micro_batch_per_gpu": micro, "seq_len": cfg.seq_len, "parallelism": f"dp{world}",
                        "non_pad_tokens_per_step": tok_step, "l2": "working set >> L2 (weights 275 MB + "
                        "activations ~25 GB per step), no flush needed",
-                       "optimizer": "fused AdamW inside the step"},
+                       "optimizer": "fused AdamW inside the step", "ffn_dropout": args.dropout},
             "mfu": {"datasheet_2.25PF": mfu_ds, "measured_peak": mfu_meas, "n_params": n_params,
                     "formula": "6 N tok/s / (G peak) (Eq. 3, P:608)"},
             "loss": loss_val,
