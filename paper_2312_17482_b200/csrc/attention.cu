@@ -432,8 +432,11 @@ __device__ __forceinline__ int next_unit(const int* cu, int heads, int total, in
 // Forward scores of this thread's 64 keys [64 ch, 64 ch + 64) of query row r, in the exp2 domain:
 // x_j = S_rj log2e / sqrt(d) - m_h log2e |r - j| (-inf past the sequence when MASK); returns max_j.
 template <bool MASK>
-__device__ __forceinline__ float fwd_scores(float (&x)[64], int r, int ch, int len, float sc2, float sl2) {
-  const float rc = (float)(r - 64 * ch);
+__device__ __forceinline__ float fwd_scores(float (&x)[64], int r, int ch, int len, float sc2, float sl2,
+                                           int qk_off = 0) {
+  // query position - key position of this thread's first key = r + qk_off - 64 ch (qk_off = q0 - kv0);
+  // keys at or past len (relative to the tile) are masked
+  const float rc = (float)(r + qk_off - 64 * ch);
   float mx = -INFINITY;
 #pragma unroll
   for (int j = 0; j < 64; j += 2) {
@@ -634,6 +637,288 @@ __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const
       if (ch == 0 && r < len) lse[(size_t)h * nnz + start + r] = (mx + log2f(l)) * LN2;
       sm100::tc_fence_before();
       u = next_unit(cu, heads, total, u);
+    }
+    if (lane == 0) sm100::bulk_wait0();
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  if (warp == 0) sm100::tmem_dealloc(tbase, 512);
+}
+
+// ------------------------------------------------------------------------------------------
+// Long-sequence forward (128 < l <= 2048, SURVEY A5 at l = 512 and F4): one work unit = (128-row
+// query tile, head, sequence), iterating over the sequence's key tiles with the online softmax.
+// Warp 9 (one lane) streams Q (double-buffered per unit) and K/V tiles (LF_NS-stage ring) by TMA;
+// warp 8 (one lane) issues S_{g+1} = Q K_{g+1}^T into the other half of a double-buffered TMEM S
+// while the softmax warps work on S_g, then PV_g = P_g V_g into a double-buffered TMEM PV;
+// warps 0-7 (two threads per query row, 64 keys each) compute the exp2-domain online softmax and
+// fold PV_{g-1} into their fp32 registers (o = alpha_{g-1} o + PV_{g-1}) before writing P_g.
+// TMEM: S [0,256) (2 x 128), PV [256,384) (2 x 64).
+// ------------------------------------------------------------------------------------------
+constexpr int LF_NS = 3;
+constexpr int LF_THREADS = SH_THREADS + 64;
+constexpr int LF_SMEM = 2 * TILE_BYTES + LF_NS * 2 * TILE_BYTES + P_BYTES + 1024 + 256;
+
+struct LongUnits {  // unit u = (b * heads + h) * QT + qt, valid iff qt * 128 < len_b
+  const int* cu;
+  int heads, QT, total;
+  __device__ __forceinline__ bool valid(int u) const {
+    const int b = u / (heads * QT), qt = u % QT;
+    return qt * TILE < cu[b + 1] - cu[b];
+  }
+  __device__ __forceinline__ int next(int u) const {
+    for (u += gridDim.x; u < total; u += gridDim.x)
+      if (valid(u)) return u;
+    return total;
+  }
+  __device__ __forceinline__ int first() const {
+    int u = blockIdx.x;
+    if (u < total && !valid(u)) u = next(u);
+    return u;
+  }
+  __device__ __forceinline__ void decode(int u, int& b, int& h, int& qt) const {
+    b = u / (heads * QT);
+    const int rem = u - b * heads * QT;
+    h = rem / QT;
+    qt = rem - h * QT;
+  }
+};
+
+__global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __grid_constant__ CUtensorMap tm_qkv,
+                                                                     const __grid_constant__ CUtensorMap tm_o,
+                                                                     LongUnits U, int d,
+                                                                     const float* __restrict__ slopes,
+                                                                     bf16* __restrict__ O, float* __restrict__ lse,
+                                                                     int nnz) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;                              // 2 x Q
+  uint8_t* sKV = sQ + 2 * TILE_BYTES;              // LF_NS x (K, V)
+  uint8_t* sP = sKV + LF_NS * 2 * TILE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + P_BYTES);
+  uint64_t* q_full = bars;                         // [2]
+  uint64_t* q_empty = bars + 2;                    // [2]
+  uint64_t* kv_full = bars + 4;                    // [LF_NS]
+  uint64_t* kv_empty = bars + 4 + LF_NS;           // [LF_NS]
+  uint64_t* s_full = bars + 4 + 2 * LF_NS;         // [2]
+  uint64_t* pv_full = bars + 6 + 2 * LF_NS;        // [2]
+  uint64_t* p_ready = bars + 8 + 2 * LF_NS;        // 8 softmax warps
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 16);
+  __shared__ float rmax[2][2 * TILE], lsum[2 * TILE];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int H = U.heads * d;
+  if (tid == 0) {
+    sm100::tma_prefetch(&tm_qkv);
+    sm100::tma_prefetch(&tm_o);
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&q_full[i], 1);
+      sm100::mbar_init(&q_empty[i], 1);
+      sm100::mbar_init(&s_full[i], 1);
+      sm100::mbar_init(&pv_full[i], 1);
+    }
+    for (int i = 0; i < LF_NS; ++i) {
+      sm100::mbar_init(&kv_full[i], 1);
+      sm100::mbar_init(&kv_empty[i], 1);
+    }
+    sm100::mbar_init(p_ready, 8);
+    sm100::fence_barrier_init();
+  }
+  if (warp == 0) sm100::tmem_alloc(tslot, 512);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tbase = *tslot;
+  const uint32_t sQa = sm100::smem_u32(sQ), sKVa = sm100::smem_u32(sKV), sPa = sm100::smem_u32(sP);
+  auto nkv_of = [&](int u) {
+    int b, h, qt;
+    U.decode(u, b, h, qt);
+    return (U.cu[b + 1] - U.cu[b] + TILE - 1) / TILE;
+  };
+
+  if (warp == 9) {
+    // ------------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int uc = 0, g = 0;
+      for (int u = U.first(); u < U.total; u = U.next(u), ++uc) {
+        int b, h, qt;
+        U.decode(u, b, h, qt);
+        const int st = U.cu[b], nkv = (U.cu[b + 1] - st + TILE - 1) / TILE;
+        const int qb = uc & 1;
+        sm100::mbar_wait(&q_empty[qb], ((uc >> 1) & 1) ^ 1);
+        sm100::mbar_arrive_expect_tx(&q_full[qb], TILE_BYTES);
+        sm100::tma_load_2d(sQ + qb * TILE_BYTES, &tm_qkv, &q_full[qb], h * d, st + qt * TILE);
+        for (int j = 0; j < nkv; ++j, ++g) {
+          const int sg = g % LF_NS;
+          sm100::mbar_wait(&kv_empty[sg], ((g / LF_NS) & 1) ^ 1);
+          uint8_t* kv = sKV + sg * 2 * TILE_BYTES;
+          sm100::mbar_arrive_expect_tx(&kv_full[sg], 2 * TILE_BYTES);
+          sm100::tma_load_2d(kv, &tm_qkv, &kv_full[sg], H + h * d, st + j * TILE);
+          sm100::tma_load_2d(kv + TILE_BYTES, &tm_qkv, &kv_full[sg], 2 * H + h * d, st + j * TILE);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 8) {
+    // ------------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t id_s = sm100::idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t id_o = sm100::idesc_bf16(128, 64, 0, 1);
+      // (unit, tile) cursor over this CTA's flattened tile sequence
+      int u = U.first(), uc = 0, j = 0, nkv = u < U.total ? nkv_of(u) : 0;
+      auto issue_s = [&](int g, int uu_c, int last) {  // S_g = Q K_g^T into S buffer g & 1
+        const int sg = g % LF_NS;
+        sm100::mbar_wait(&kv_full[sg], (g / LF_NS) & 1);
+        sm100::tc_fence_after();
+        const uint32_t q = sQa + (uu_c & 1) * TILE_BYTES, k = sKVa + sg * 2 * TILE_BYTES;
+        for (int kk = 0; kk < d / 16; ++kk)
+          sm100::mma_bf16_ss(tbase + 128 * (g & 1), sm100::desc_kmajor_sw128(q + kk * 32),
+                             sm100::desc_kmajor_sw128(k + kk * 32), id_s, kk > 0);
+        sm100::mma_commit(&s_full[g & 1]);
+        if (last) sm100::mma_commit(&q_empty[uu_c & 1]);  // the unit's last read of its Q
+      };
+      if (u < U.total) {
+        sm100::mbar_wait(&q_full[0], 0);
+        issue_s(0, 0, nkv == 1);
+      }
+      for (int g = 0; u < U.total; ++g) {
+        // cursor of tile g + 1
+        int u2 = u, uc2 = uc, j2 = j + 1, nkv2 = nkv;
+        if (j2 == nkv) {
+          u2 = U.next(u);
+          ++uc2;
+          j2 = 0;
+          nkv2 = u2 < U.total ? nkv_of(u2) : 0;
+        }
+        if (u2 < U.total) {
+          if (j2 == 0) sm100::mbar_wait(&q_full[uc2 & 1], (uc2 >> 1) & 1);
+          issue_s(g + 1, uc2, j2 == nkv2 - 1);
+        }
+        sm100::mbar_wait(p_ready, g & 1);  // P_g in smem (S_g consumed)
+        sm100::tc_fence_after();
+        const uint32_t v = sKVa + (g % LF_NS) * 2 * TILE_BYTES + TILE_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < TILE / 16; ++kk)
+          sm100::mma_bf16_ss(tbase + 256 + 64 * (g & 1),
+                             sm100::desc_kmajor_sw128(sPa + (kk >> 2) * (TILE * 128) + (kk & 3) * 32),
+                             sm100::desc_mnmajor_sw128(v + kk * 2048, 8192), id_o, kk > 0);
+        sm100::mma_commit(&pv_full[g & 1]);
+        sm100::mma_commit(&kv_empty[g % LF_NS]);
+        u = u2, uc = uc2, j = j2, nkv = nkv2;
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------------ softmax warps 0-7
+    const int ch = warp >> 2, q4 = warp & 3;
+    const int r = q4 * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const float sc2 = rsqrtf((float)d) * LOG2E;
+    int g = 0;
+    for (int u = U.first(); u < U.total; u = U.next(u)) {
+      int b, h, qt;
+      U.decode(u, b, h, qt);
+      const int start = U.cu[b], len = U.cu[b + 1] - start, q0 = qt * TILE;
+      const int nkv = (len + TILE - 1) / TILE;
+      const float sl2 = slopes[h] * LOG2E;
+      float m = -INFINITY, l = 0.f, alpha_prev = 0.f;
+      float o[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) o[e] = 0.f;
+      // this warp's P slab doubles as O staging: the previous unit's TMA store must have read it
+      if (lane == 0) sm100::bulk_wait_read0();
+      __syncwarp();
+      for (int j = 0; j < nkv; ++j, ++g) {
+        const int kv0 = j * TILE;
+        sm100::mbar_wait(&s_full[g & 1], (g >> 1) & 1);
+        sm100::tc_fence_after();
+        float x[64];
+        const uint32_t tS = tbase + 128 * (g & 1) + lane_off + 64 * ch;
+        sm100::tmem_ld32(tS, x);
+        sm100::tmem_ld32(tS + 32, x + 32);
+        sm100::tmem_ld_wait();
+        const float mx = len - kv0 >= TILE ? fwd_scores<false>(x, r, ch, len - kv0, sc2, sl2, q0 - kv0)
+                                           : fwd_scores<true>(x, r, ch, len - kv0, sc2, sl2, q0 - kv0);
+        rmax[g & 1][ch * TILE + r] = mx;
+        named_bar_sync(1, SH_THREADS);
+        const float m_new = fmaxf(m, fmaxf(rmax[g & 1][r], rmax[g & 1][TILE + r]));
+        const float alpha = ex2_approx(m - m_new);
+        if (j > 0) {  // fold PV_{g-1}: o = alpha_{g-1} o + PV_{g-1}; its completion also frees sP
+          sm100::mbar_wait(&pv_full[(g - 1) & 1], ((g - 1) >> 1) & 1);
+          sm100::tc_fence_after();
+          float pv[32];
+          sm100::tmem_ld32(tbase + 256 + 64 * ((g - 1) & 1) + lane_off + 32 * ch, pv);
+          sm100::tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            const float2 t = __ffma2_rn(make_float2(o[e], o[e + 1]), make_float2(alpha_prev, alpha_prev),
+                                        make_float2(pv[e], pv[e + 1]));
+            o[e] = t.x;
+            o[e + 1] = t.y;
+          }
+        }
+        // P_g = 2^(x - m_new) rounded to bf16 (the PV operand); row sum over the rounded values
+        float2 sum2 = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int j8 = 0; j8 < 8; ++j8) {
+          uint32_t pk[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 t = __fadd2_rn(make_float2(x[j8 * 8 + 2 * e], x[j8 * 8 + 2 * e + 1]),
+                                        make_float2(-m_new, -m_new));
+            pk[e] = pack_bf16x2(ex2_approx(t.x), ex2_approx(t.y));
+            sum2 = __fadd2_rn(sum2, make_float2(__uint_as_float(pk[e] << 16), __uint_as_float(pk[e] & 0xffff0000u)));
+          }
+          st_shared_v4(sPa + p_off(r, 64 * ch + 8 * j8), pk[0], pk[1], pk[2], pk[3]);
+        }
+        l = l * alpha + (sum2.x + sum2.y);
+        m = m_new;
+        alpha_prev = alpha;
+        sm100::fence_proxy_async_smem();
+        sm100::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(p_ready);
+      }
+      // drain the unit's last PV, combine the two half-row sums, normalise, store O and LSE
+      sm100::mbar_wait(&pv_full[(g - 1) & 1], ((g - 1) >> 1) & 1);
+      sm100::tc_fence_after();
+      {
+        float pv[32];
+        sm100::tmem_ld32(tbase + 256 + 64 * ((g - 1) & 1) + lane_off + 32 * ch, pv);
+        sm100::tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; ++e) o[e] = fmaf(o[e], alpha_prev, pv[e]);
+      }
+      lsum[ch * TILE + r] = l;
+      named_bar_sync(1, SH_THREADS);
+      const float lt = lsum[r] + lsum[TILE + r];
+      const float inv = 1.f / lt;
+#pragma unroll
+      for (int e = 0; e < 32; ++e) o[e] *= inv;
+      const int qrow = q0 + r;
+      if (32 * ch < d) {
+        if (q0 + q4 * 32 + 32 <= len) {  // warp-uniform: all 32 rows valid -> swizzled staging + TMA store
+          const uint32_t stg = sPa + ch * (TILE * 128) + q4 * 4096;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const uint4 pk = f32_to_bf16x8(o + 8 * c);
+            st_shared_v4(stg + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4), pk.x, pk.y, pk.z, pk.w);
+          }
+          sm100::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            sm100::tma_store_2d(&tm_o, stg, h * d + 32 * ch, start + q0 + q4 * 32);
+            sm100::bulk_commit();
+          }
+        } else if (qrow < len) {
+          bf16* dst = O + (size_t)(start + qrow) * H + h * d + 32 * ch;
+#pragma unroll
+          for (int c = 0; c < 32; c += 8) *reinterpret_cast<uint4*>(dst + c) = f32_to_bf16x8(o + c);
+        }
+      }
+      if (ch == 0 && qrow < len) lse[(size_t)h * nnz + start + qrow] = (m + log2f(lt)) * LN2;
+      sm100::tc_fence_before();
     }
     if (lane == 0) sm100::bulk_wait0();
   }
@@ -993,14 +1278,19 @@ mb_status attention_fwd(const bf16* qkv, const int* cu, int batch, int nnz, int 
     MB_CHECK_LAUNCH();
     return MB_OK;
   }
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FWD_SMEM) != cudaSuccess)
+  static bool attr_l = false;
+  if (!attr_l) {
+    if (cudaFuncSetAttribute(attn_fwd_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, LF_SMEM) !=
+        cudaSuccess)
       return MB_ERR_CUDA;
-    attr = true;
+    attr_l = true;
   }
-  dim3 grid((max_seqlen + TILE - 1) / TILE, heads, batch);
-  attn_fwd_kernel<<<grid, 128, FWD_SMEM, s>>>(tm, cu, H, d, slopes, O, lse, nnz);
+  CUtensorMap tmo;
+  MB_REQUIRE(make_tmap_bf16_2d(&tmo, O, H, nnz, H, 32, 32, 64), MB_ERR_CUDA);
+  LongUnits U{cu, heads, (max_seqlen + TILE - 1) / TILE, 0};
+  U.total = batch * heads * U.QT;
+  const int grid = std::max(1, std::min(U.total, num_sms()));
+  attn_fwd_long_kernel<<<grid, LF_THREADS, LF_SMEM, s>>>(tm, tmo, U, d, slopes, O, lse, nnz);
   MB_CHECK_LAUNCH();
   return MB_OK;
 }
