@@ -42,7 +42,7 @@ typedef enum {
   MB_ERR_INVALID_ARG = 1, /* null pointer, negative size                                             */
   MB_ERR_CONFIG = 2,      /* heads<=0, hidden%heads!=0, head_dim not in {32,64},
                              odd fused GLU width, vocab<1, dims not multiples of 8           */
-  MB_ERR_SHAPE = 3,       /* nnz > B*L, max_seqlen > 512, n_masked > nnz                             */
+  MB_ERR_SHAPE = 3,       /* nnz > B*L, max_seqlen > 2048, n_masked > nnz                            */
   MB_ERR_MASK_LAYOUT = 4, /* device-reported: a mask row is not a right-padded prefix (R6)    */
   MB_ERR_LABEL_RANGE = 5, /* device-reported: label not in [0, V)                                    */
   MB_ERR_WORKSPACE = 6,   /* workspace smaller than mb_*_workspace_bytes(...)                        */
@@ -168,7 +168,7 @@ MB_API mb_status mb_geglu_backward(const mb_bf16* dF, int32_t n, int32_t H, int3
  *   O_i = sum_j softmax_j(s)_ij v_j,  LSE_i = log sum_j exp(s_ij)
  *   qkv bf16 [nnz, 3H] with columns (3, heads, d) (R9); cu_seqlens device int32[batch+1];
  *   slopes device fp32[heads]; O bf16 [nnz, H]; lse fp32 [heads, nnz] (saved for backward).
- * max_seqlen <= 512 (the longest workload, BASELINE config 4). */
+ * max_seqlen <= 2048 (BASELINE config 4 is 512; SURVEY F4 adds 1024 and 2048). */
 MB_API mb_status mb_attention_forward(const mb_bf16* qkv, const int32_t* cu_seqlens, int32_t batch, int32_t nnz,
                                int32_t max_seqlen, int32_t heads, int32_t head_dim, const float* slopes,
                                mb_bf16* O, float* lse, mb_stream_t s);

@@ -132,7 +132,7 @@ mb_status mb_encoder_forward(const mb_dims* d, const mb_layer_params* p, const m
   if (st != MB_OK) return st;
   if (!p || !pk || !slopes || !x || !y || !saved || !pk->cu_seqlens || !drop_ok(drop)) return MB_ERR_INVALID_ARG;
   if (pk->nnz < 0 || pk->batch < 0) return MB_ERR_INVALID_ARG;
-  if (pk->max_seqlen > 512) return MB_ERR_SHAPE;
+  if (pk->max_seqlen > kMaxSeqlen) return MB_ERR_SHAPE;
   if (pk->nnz == 0) return MB_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(s_);
   const int T = pk->nnz, H = d->hidden, I = d->intermediate, nh = d->heads;
@@ -192,7 +192,7 @@ mb_status mb_encoder_backward(const mb_dims* d, const mb_layer_params* p, const 
   if (!p || !pk || !slopes || !x || !saved || !dy || !dx || !g || !ws || !pk->cu_seqlens || !drop_ok(drop))
     return MB_ERR_INVALID_ARG;
   if (pk->nnz < 0 || pk->batch < 0) return MB_ERR_INVALID_ARG;
-  if (pk->max_seqlen > 512) return MB_ERR_SHAPE;
+  if (pk->max_seqlen > kMaxSeqlen) return MB_ERR_SHAPE;
   if (pk->nnz == 0) return MB_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(s_);
   const int T = pk->nnz, H = d->hidden, I = d->intermediate, nh = d->heads;

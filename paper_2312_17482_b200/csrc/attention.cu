@@ -1252,13 +1252,361 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
   if (warp == 0) sm100::tmem_dealloc(tbase, 512);
 }
 
+// ------------------------------------------------------------------------------------------
+// Long-sequence backward (128 < l <= 2048): one work unit = (128-key tile j, head, sequence),
+// iterating over the sequence's query tiles i.  D_i = dO_i . O_i comes from a pre-pass
+// (attn_bwd_prep_kernel), so each (i, j) block needs a single pass over S and dP:
+//   P = 2^(S log2e/sqrt(d) - m log2e |q - k| - LSE log2e),  dS/sqrt(d) = P (dP - D)/sqrt(d)
+//   dV_j += P^T dO_i, dK_j += dS^T Q_i  (TMEM accumulators across the unit's query tiles)
+//   dQ_i += dS K_j                        (per block, folded into an fp32 [nnz, H] buffer by
+//                                          vector reductions; dq_finish_kernel converts it)
+// Warp 9 streams K/V (double-buffered per unit) and Q/dO tiles (LB_NS-stage ring) by TMA; warp 8
+// issues S, dP of block i+1 as soon as the softmax warps have consumed block i, and dV/dK/dQ of
+// block i once P_i, dS_i are in smem.  TMEM: S [0,128), dP [128,256), dV [256,320),
+// dK [320,384), dQ [384,448).
+// ------------------------------------------------------------------------------------------
+constexpr int LB_NS = 2;
+constexpr int LB_THREADS = SH_THREADS + 64;
+constexpr int LB_SMEM = 2 * 2 * TILE_BYTES + LB_NS * 2 * TILE_BYTES + 2 * P_BYTES + 1024 + 256;
+
+// D[h, t] = sum_c dO[t, h d + c] O[t, h d + c]  (the rowsum(dO o O) of FlashAttention's backward)
+__global__ void attn_bwd_prep_kernel(const bf16* __restrict__ O, const bf16* __restrict__ dO, int nnz, int heads,
+                                     int d, float* __restrict__ D) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (t, h)
+  if (i >= (int64_t)nnz * heads) return;
+  const int t = (int)(i / heads), h = (int)(i - (int64_t)t * heads);
+  const bf16* o = O + (size_t)t * heads * d + h * d;
+  const bf16* g = dO + (size_t)t * heads * d + h * d;
+  float acc = 0.f;
+  for (int c = 0; c < d; c += 8) {
+    float a[8], b[8];
+    bf16x8_to_f32(ld_nc_v4(o + c), a);
+    bf16x8_to_f32(ld_nc_v4(g + c), b);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc = fmaf(a[e], b[e], acc);
+  }
+  D[(size_t)h * nnz + t] = acc;
+}
+
+// dq_acc fp32 [nnz, H] -> dqkv[:, :H] bf16, and db_q += column sums (block-local, one atomic per
+// column per block)
+__global__ void dq_finish_kernel(const float* __restrict__ dq_acc, int nnz, int H, int rows_per, bf16* __restrict__ dqkv,
+                                 float* __restrict__ db) {
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (c >= H) return;
+  const int r0 = blockIdx.y * rows_per, r1 = min(nnz, r0 + rows_per);
+  float cs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int r = r0; r < r1; ++r) {
+    const float4* src = reinterpret_cast<const float4*>(dq_acc + (size_t)r * H + c);
+    const float4 a = src[0], b = src[1];
+    const float t[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    const uint4 pk = f32_to_bf16x8(t);
+    *reinterpret_cast<uint4*>(dqkv + (size_t)r * 3 * H + c) = pk;
+    if (db) {
+      float f[8];
+      bf16x8_to_f32(pk, f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) cs[e] += f[e];
+    }
+  }
+  if (db) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) atomicAdd(db + c + e, cs[e]);
+  }
+}
+
+// single-pass P / dS of one (q tile, k tile) block for this thread's 64 keys: P -> sP, dS -> sdS
+template <bool MASK>
+__device__ __forceinline__ void bwd_block(uint32_t tS, uint32_t tdP, uint32_t sPa, uint32_t sdSa, int r, int ch,
+                                          int qk_off, int qrows, int keys, float sc2, float sl2, float lse2,
+                                          float rsd, float Drs) {
+  const float rc = (float)(r + qk_off - 64 * ch);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int c0 = 64 * ch + 16 * c;
+    float v[16], w[16];
+    sm100::tmem_ld16(tS + c0, v);
+    sm100::tmem_ld16(tdP + c0, w);
+    sm100::tmem_ld_wait();
+    uint32_t pp[8], pd[8];
+#pragma unroll
+    for (int jj = 0; jj < 16; jj += 2) {
+      const float j0 = (float)(16 * c + jj);
+      const float2 dd = __fadd2_rn(make_float2(rc, rc), make_float2(-j0, -j0 - 1.f));
+      const float2 t = __ffma2_rn(make_float2(fabsf(dd.x), fabsf(dd.y)), make_float2(-sl2, -sl2),
+                                  make_float2(-lse2, -lse2));
+      const float2 x = __ffma2_rn(make_float2(v[jj], v[jj + 1]), make_float2(sc2, sc2), t);
+      float2 pv = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+      if (MASK) {
+        pv.x = (r < qrows && c0 + jj < keys) ? pv.x : 0.f;
+        pv.y = (r < qrows && c0 + jj + 1 < keys) ? pv.y : 0.f;
+      }
+      const float2 ds = __fmul2_rn(pv, __ffma2_rn(make_float2(w[jj], w[jj + 1]), make_float2(rsd, rsd),
+                                                  make_float2(Drs, Drs)));
+      pp[jj >> 1] = pack_bf16x2(pv.x, pv.y);
+      pd[jj >> 1] = pack_bf16x2(ds.x, ds.y);
+    }
+    const uint32_t o0 = p_off(r, c0), o1 = p_off(r, c0 + 8);
+    st_shared_v4(sPa + o0, pp[0], pp[1], pp[2], pp[3]);
+    st_shared_v4(sPa + o1, pp[4], pp[5], pp[6], pp[7]);
+    st_shared_v4(sdSa + o0, pd[0], pd[1], pd[2], pd[3]);
+    st_shared_v4(sdSa + o1, pd[4], pd[5], pd[6], pd[7]);
+  }
+}
+
+__global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
+    const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+    const __grid_constant__ CUtensorMap tm_dqkv, LongUnits U, int d, const float* __restrict__ slopes,
+    const float* __restrict__ lse, const float* __restrict__ Dg, float* __restrict__ dq_acc,
+    bf16* __restrict__ dqkv, float* __restrict__ dbias, int nnz) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sKV = smem;                           // 2 x (K, V)
+  uint8_t* sQD = sKV + 2 * 2 * TILE_BYTES;       // LB_NS x (Q, dO)
+  uint8_t* sP = sQD + LB_NS * 2 * TILE_BYTES;
+  uint8_t* sdS = sP + P_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sdS + P_BYTES);
+  uint64_t* kv_full = bars;                      // [2]
+  uint64_t* kv_empty = bars + 2;                 // [2]
+  uint64_t* qd_full = bars + 4;                  // [LB_NS]
+  uint64_t* qd_empty = bars + 4 + LB_NS;         // [LB_NS]
+  uint64_t* sp_full = bars + 4 + 2 * LB_NS;
+  uint64_t* elem_done = bars + 5 + 2 * LB_NS;    // 8 warps
+  uint64_t* acc_full = bars + 6 + 2 * LB_NS;
+  uint64_t* out_free = bars + 7 + 2 * LB_NS;     // 8 warps: dK/dV of the unit read out
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 16);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int H = U.heads * d;
+  if (tid == 0) {
+    sm100::tma_prefetch(&tm_qkv);
+    sm100::tma_prefetch(&tm_do);
+    sm100::tma_prefetch(&tm_dqkv);
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&kv_full[i], 1);
+      sm100::mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < LB_NS; ++i) {
+      sm100::mbar_init(&qd_full[i], 1);
+      sm100::mbar_init(&qd_empty[i], 1);
+    }
+    sm100::mbar_init(sp_full, 1);
+    sm100::mbar_init(elem_done, 8);
+    sm100::mbar_init(acc_full, 1);
+    sm100::mbar_init(out_free, 8);
+    sm100::fence_barrier_init();
+  }
+  if (warp == 0) sm100::tmem_alloc(tslot, 512);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tbase = *tslot;
+  const uint32_t tS = tbase, tdP = tbase + 128, tdV = tbase + 256, tdK = tbase + 320, tdQ = tbase + 384;
+  const uint32_t sKVa = sm100::smem_u32(sKV), sQDa = sm100::smem_u32(sQD), sPa = sm100::smem_u32(sP),
+                 sdSa = sm100::smem_u32(sdS);
+  auto nq_of = [&](int u) {
+    int b, h, jt;
+    U.decode(u, b, h, jt);
+    return (U.cu[b + 1] - U.cu[b] + TILE - 1) / TILE;
+  };
+
+  if (warp == 9) {
+    // ------------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int uc = 0, g = 0;
+      for (int u = U.first(); u < U.total; u = U.next(u), ++uc) {
+        int b, h, jt;
+        U.decode(u, b, h, jt);
+        const int st = U.cu[b], nq = (U.cu[b + 1] - st + TILE - 1) / TILE;
+        const int kb = uc & 1;
+        sm100::mbar_wait(&kv_empty[kb], ((uc >> 1) & 1) ^ 1);
+        uint8_t* kv = sKV + kb * 2 * TILE_BYTES;
+        sm100::mbar_arrive_expect_tx(&kv_full[kb], 2 * TILE_BYTES);
+        sm100::tma_load_2d(kv, &tm_qkv, &kv_full[kb], H + h * d, st + jt * TILE);
+        sm100::tma_load_2d(kv + TILE_BYTES, &tm_qkv, &kv_full[kb], 2 * H + h * d, st + jt * TILE);
+        for (int i = 0; i < nq; ++i, ++g) {
+          const int sg = g % LB_NS;
+          sm100::mbar_wait(&qd_empty[sg], ((g / LB_NS) & 1) ^ 1);
+          uint8_t* qd = sQD + sg * 2 * TILE_BYTES;
+          sm100::mbar_arrive_expect_tx(&qd_full[sg], 2 * TILE_BYTES);
+          sm100::tma_load_2d(qd, &tm_qkv, &qd_full[sg], h * d, st + i * TILE);
+          sm100::tma_load_2d(qd + TILE_BYTES, &tm_do, &qd_full[sg], h * d, st + i * TILE);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 8) {
+    // ------------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t id_s = sm100::idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t id_t = sm100::idesc_bf16(128, 64, 1, 1);  // P^T dO, dS^T Q
+      constexpr uint32_t id_q = sm100::idesc_bf16(128, 64, 0, 1);  // dS K
+      int u = U.first(), uc = 0, i = 0, nq = u < U.total ? nq_of(u) : 0;
+      auto mma1 = [&](int g, int ucc) {  // S = Q_i K_j^T, dP = dO_i V_j^T
+        const int sg = g % LB_NS;
+        sm100::mbar_wait(&qd_full[sg], (g / LB_NS) & 1);
+        sm100::tc_fence_after();
+        const uint32_t q = sQDa + sg * 2 * TILE_BYTES, o = q + TILE_BYTES;
+        const uint32_t k = sKVa + (ucc & 1) * 2 * TILE_BYTES, v = k + TILE_BYTES;
+        for (int kk = 0; kk < d / 16; ++kk) {
+          sm100::mma_bf16_ss(tS, sm100::desc_kmajor_sw128(q + kk * 32), sm100::desc_kmajor_sw128(k + kk * 32), id_s,
+                             kk > 0);
+          sm100::mma_bf16_ss(tdP, sm100::desc_kmajor_sw128(o + kk * 32), sm100::desc_kmajor_sw128(v + kk * 32), id_s,
+                             kk > 0);
+        }
+        sm100::mma_commit(sp_full);
+      };
+      if (u < U.total) {
+        sm100::mbar_wait(&kv_full[0], 0);
+        mma1(0, 0);
+      }
+      for (int g = 0; u < U.total; ++g) {
+        sm100::mbar_wait(elem_done, g & 1);  // P_g, dS_g in smem; S/dP consumed
+        if (i == 0 && uc > 0) sm100::mbar_wait(out_free, (uc - 1) & 1);  // previous unit's dK/dV read out
+        sm100::tc_fence_after();
+        const int sg = g % LB_NS;
+        const uint32_t q = sQDa + sg * 2 * TILE_BYTES, o = q + TILE_BYTES;
+        const uint32_t k = sKVa + (uc & 1) * 2 * TILE_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < TILE / 16; ++kk) {
+          const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
+          sm100::mma_bf16_ss(tdV, sm100::desc_mnmajor_sw128(sPa + kk * 2048, TILE * 128),
+                             sm100::desc_mnmajor_sw128(o + kk * 2048, 8192), id_t, acc);
+          sm100::mma_bf16_ss(tdK, sm100::desc_mnmajor_sw128(sdSa + kk * 2048, TILE * 128),
+                             sm100::desc_mnmajor_sw128(q + kk * 2048, 8192), id_t, acc);
+          sm100::mma_bf16_ss(tdQ, sm100::desc_kmajor_sw128(sdSa + (kk >> 2) * (TILE * 128) + (kk & 3) * 32),
+                             sm100::desc_mnmajor_sw128(k + kk * 2048, 8192), id_q, kk > 0);
+        }
+        sm100::mma_commit(acc_full);
+        sm100::mma_commit(&qd_empty[sg]);
+        // cursor of block g + 1
+        int u2 = u, uc2 = uc, i2 = i + 1, nq2 = nq;
+        if (i2 == nq) {
+          sm100::mma_commit(&kv_empty[uc & 1]);  // the unit's last read of K_j, V_j
+          u2 = U.next(u);
+          ++uc2;
+          i2 = 0;
+          nq2 = u2 < U.total ? nq_of(u2) : 0;
+        }
+        if (u2 < U.total) {
+          if (i2 == 0) sm100::mbar_wait(&kv_full[uc2 & 1], (uc2 >> 1) & 1);
+          mma1(g + 1, uc2);
+        }
+        u = u2, uc = uc2, i = i2, nq = nq2;
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------------ compute warps 0-7
+    const int ch = warp >> 2, q4 = warp & 3;
+    const int r = q4 * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const float rsd = rsqrtf((float)d);
+    const float sc2 = rsd * LOG2E;
+    const bool col_ok = 32 * ch < d;
+    const uint32_t slabP = sPa + ch * (TILE * 128) + q4 * 4096, slabS = sdSa + ch * (TILE * 128) + q4 * 4096;
+    int g = 0;
+    auto dq_out = [&](int start, int q0, int len, int h) {  // fold the finished dQ block into dq_acc
+      float v[32];
+      sm100::tmem_ld32(tdQ + lane_off + 32 * ch, v);
+      sm100::tmem_ld_wait();
+      if (col_ok && q0 + r < len) {
+        float* dst = dq_acc + (size_t)(start + q0 + r) * H + h * d + 32 * ch;
+#pragma unroll
+        for (int e = 0; e < 32; e += 4) red_add_v4(dst + e, v[e], v[e + 1], v[e + 2], v[e + 3]);
+      }
+    };
+    for (int u = U.first(); u < U.total; u = U.next(u)) {
+      int b, h, jt;
+      U.decode(u, b, h, jt);
+      const int start = U.cu[b], len = U.cu[b + 1] - start, kv0 = jt * TILE;
+      const int nq = (len + TILE - 1) / TILE;
+      const float sl2 = slopes[h] * LOG2E;
+      // this warp's P / dS slabs double as dK/dV staging: the previous unit's stores must have read them
+      if (lane == 0) sm100::bulk_wait_read0();
+      __syncwarp();
+      for (int i = 0; i < nq; ++i, ++g) {
+        const int q0 = i * TILE;
+        const bool rv = q0 + r < len;
+        const float lse2 = rv ? lse[(size_t)h * nnz + start + q0 + r] * LOG2E : 0.f;
+        const float Drs = rv ? -Dg[(size_t)h * nnz + start + q0 + r] * rsd : 0.f;
+        sm100::mbar_wait(sp_full, g & 1);
+        sm100::tc_fence_after();
+        if (i > 0) {  // block g-1's MMAs finished (P/dS free); its dQ is ready
+          sm100::mbar_wait(acc_full, (g - 1) & 1);
+          sm100::tc_fence_after();
+          dq_out(start, q0 - TILE, len, h);
+        }
+        if (len - q0 >= TILE && len - kv0 >= TILE)
+          bwd_block<false>(tS + lane_off, tdP + lane_off, sPa, sdSa, r, ch, q0 - kv0, len - q0, len - kv0, sc2, sl2,
+                           lse2, rsd, Drs);
+        else
+          bwd_block<true>(tS + lane_off, tdP + lane_off, sPa, sdSa, r, ch, q0 - kv0, len - q0, len - kv0, sc2, sl2,
+                          lse2, rsd, Drs);
+        sm100::fence_proxy_async_smem();
+        sm100::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(elem_done);
+      }
+      // unit end: last dQ block, then dV / dK of the key tile (rows = keys kv0 + r)
+      sm100::mbar_wait(acc_full, (g - 1) & 1);
+      sm100::tc_fence_after();
+      dq_out(start, (nq - 1) * TILE, len, h);
+      const bool ok = kv0 + r < len;
+      const bool full = kv0 + q4 * 32 + 32 <= len;  // warp-uniform
+#pragma unroll 1
+      for (int which = 2; which >= 1; --which) {  // V then K
+        float v[32];
+        sm100::tmem_ld32((which == 2 ? tdV : tdK) + lane_off + 32 * ch, v);
+        sm100::tmem_ld_wait();
+        if (!full) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = ok ? v[e] : 0.f;
+        }
+        if (col_ok) {
+          if (full) {
+            const uint32_t stg = which == 2 ? slabP : slabS;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const uint4 pk = f32_to_bf16x8(v + 8 * c);
+              st_shared_v4(stg + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4), pk.x, pk.y, pk.z, pk.w);
+            }
+            sm100::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              sm100::tma_store_2d(&tm_dqkv, stg, which * H + h * d + 32 * ch, start + kv0 + q4 * 32);
+              sm100::bulk_commit();
+            }
+          } else if (ok) {
+            bf16* dst = dqkv + (size_t)(start + kv0 + r) * 3 * H + which * H + h * d + 32 * ch;
+#pragma unroll
+            for (int c = 0; c < 32; c += 8) *reinterpret_cast<uint4*>(dst + c) = f32_to_bf16x8(v + c);
+          }
+        }
+        if (dbias && which == 2) {  // db_v = column sums of dV (db_k = 0, R31; db_q in dq_finish_kernel)
+          const float cs = warp_colsum32(v, lane);
+          if (col_ok && 32 * ch + lane < d) atomicAdd(dbias + 2 * H + h * d + 32 * ch + lane, cs);
+        }
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(out_free);
+    }
+    if (lane == 0) sm100::bulk_wait0();
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  if (warp == 0) sm100::tmem_dealloc(tbase, 512);
+}
+
 }  // namespace
 
 mb_status attention_fwd(const bf16* qkv, const int* cu, int batch, int nnz, int max_seqlen, int heads, int d,
                         const float* slopes, bf16* O, float* lse, cudaStream_t s) {
   if (nnz == 0 || batch == 0) return MB_OK;
   MB_REQUIRE(d == 32 || d == 64, MB_ERR_CONFIG);
-  MB_REQUIRE(max_seqlen >= 1 && max_seqlen <= 512, MB_ERR_SHAPE);
+  MB_REQUIRE(max_seqlen >= 1 && max_seqlen <= kMaxSeqlen, MB_ERR_SHAPE);
   const int H = heads * d;
   CUtensorMap tm;
   MB_REQUIRE(make_tmap_bf16_2d(&tm, qkv, 3 * H, nnz, 3 * H, DT, TILE), MB_ERR_CUDA);
@@ -1295,8 +1643,11 @@ mb_status attention_fwd(const bf16* qkv, const int* cu, int batch, int nnz, int 
   return MB_OK;
 }
 
+// long path: dq_acc fp32 [nnz, H] followed by D fp32 [heads, nnz]
 size_t attention_ws_bytes(int nnz, int heads, int d, int max_seqlen) {
-  return max_seqlen > TILE ? (size_t)nnz * heads * d * sizeof(float) : 0;
+  if (max_seqlen <= TILE) return 0;
+  const size_t dq = ((size_t)nnz * heads * d * sizeof(float) + 255) & ~size_t(255);
+  return dq + (size_t)heads * nnz * sizeof(float);
 }
 
 mb_status attention_bwd(const bf16* qkv, const bf16* O, const bf16* dO, const float* lse, const int* cu, int batch,
@@ -1304,7 +1655,7 @@ mb_status attention_bwd(const bf16* qkv, const bf16* O, const bf16* dO, const fl
                         void* ws, size_t ws_bytes, cudaStream_t s) {
   if (nnz == 0 || batch == 0) return MB_OK;
   MB_REQUIRE(d == 32 || d == 64, MB_ERR_CONFIG);
-  MB_REQUIRE(max_seqlen >= 1 && max_seqlen <= 512, MB_ERR_SHAPE);
+  MB_REQUIRE(max_seqlen >= 1 && max_seqlen <= kMaxSeqlen, MB_ERR_SHAPE);
   const int H = heads * d;
   const size_t need = attention_ws_bytes(nnz, heads, d, max_seqlen);
   MB_REQUIRE(ws_bytes >= need && (need == 0 || ws), MB_ERR_WORKSPACE);
@@ -1328,24 +1679,37 @@ mb_status attention_bwd(const bf16* qkv, const bf16* O, const bf16* dO, const fl
     MB_CHECK_LAUNCH();
     return MB_OK;
   }
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_SMEM) != cudaSuccess)
+  static bool attr_l = false;
+  if (!attr_l) {
+    if (cudaFuncSetAttribute(attn_bwd_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, LB_SMEM) !=
+        cudaSuccess)
       return MB_ERR_CUDA;
-    attr = true;
+    attr_l = true;
   }
   float* dq_acc = reinterpret_cast<float*>(ws);
-  if (need) {
-    if (cudaMemsetAsync(dq_acc, 0, need, s) != cudaSuccess) return MB_ERR_CUDA;
-  }
-  dim3 grid((max_seqlen + TILE - 1) / TILE, heads, batch);
-  attn_bwd_kernel<<<grid, 128, BWD_SMEM, s>>>(tq, tdo, cu, H, d, slopes, O, dO, lse, dqkv, dq_acc, nnz);
-  MB_CHECK_LAUNCH();
-  if (need) {
-    dq_convert_kernel<<<nnz, 64, 0, s>>>(dq_acc, cu, batch, nnz, H, dqkv);
+  float* Dg = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) +
+                                       (((size_t)nnz * H * sizeof(float) + 255) & ~size_t(255)));
+  if (cudaMemsetAsync(dq_acc, 0, (size_t)nnz * H * sizeof(float), s) != cudaSuccess) return MB_ERR_CUDA;
+  {
+    const int64_t n = (int64_t)nnz * heads;
+    attn_bwd_prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(O, dO, nnz, heads, d, Dg);
     MB_CHECK_LAUNCH();
   }
-  if (dbias) return colsum(dqkv, nnz, 3 * H, dbias, s);
+  CUtensorMap tdq;  // [32 rows x 32 columns] dK / dV blocks, 64-byte swizzle
+  MB_REQUIRE(make_tmap_bf16_2d(&tdq, dqkv, 3 * H, nnz, 3 * H, 32, 32, 64), MB_ERR_CUDA);
+  LongUnits U{cu, heads, (max_seqlen + TILE - 1) / TILE, 0};
+  U.total = batch * heads * U.QT;
+  const int grid = std::max(1, std::min(U.total, num_sms()));
+  attn_bwd_long_kernel<<<grid, LB_THREADS, LB_SMEM, s>>>(tq, tdo, tdq, U, d, slopes, lse, Dg, dq_acc, dqkv, dbias,
+                                                         nnz);
+  MB_CHECK_LAUNCH();
+  {
+    const int bx = (H / 8 + 127) / 128;
+    const int rows_per = 16;  // ~4K CTAs at C4: enough loads in flight for HBM
+    const int by = (nnz + rows_per - 1) / rows_per;
+    dq_finish_kernel<<<dim3(bx, by), 128, 0, s>>>(dq_acc, nnz, H, rows_per, dqkv, dbias);
+    MB_CHECK_LAUNCH();
+  }
   return MB_OK;
 }
 

@@ -5,6 +5,9 @@
 
 namespace mb {
 
+constexpr int kMaxSeqlen = 2048;  // longest sequence the attention kernels accept (F4)
+
+
 enum EpiMode { E_BF16 = 0, E_F32_ACC = 1, E_F32 = 2, E_GELU_AUX = 3, E_GEGLU_FWD = 4, E_GEGLU_BWD = 5, E_LSE = 6, E_DZ = 7 };
 
 struct Epi {

@@ -232,6 +232,8 @@ ATTN_CASES = {
     "full128": (12, 64, [128] * 6),
     "multi_tile_512": (4, 64, [512, 300, 129, 128, 1]),
     "d32_multi": (2, 32, [200, 17]),
+    "long_1024": (2, 64, [1024, 700, 5, 129]),   # F4
+    "long_2048_d32": (1, 32, [2048, 1100]),      # F4
 }
 
 

@@ -77,6 +77,11 @@ def test_layer_base_seq512():
     _layer_parity(synth.BASE, [512, 300, 129], 512, "stress", 4)
 
 
+def test_layer_base_seq1024():
+    """F4: a Base layer at l = 1024 (ragged second sequence)."""
+    _layer_parity(synth.BASE, [1024, 517], 1024, "bert", 12)
+
+
 def test_layer_large_dims():
     _layer_parity(synth.LARGE, [128, 128, 40], 128, "stress", 6)
 
