@@ -3,14 +3,19 @@
 //
 //   s_ij = q_i . k_j / sqrt(d) - m_h |i - j|      (i, j = positions inside one sequence; R2, R4)
 //
-// Work unit = (128-row tile, head, sequence).  Q/K/V/dO tiles come straight out of the packed
-// buffers by TMA (128-byte swizzle, rows past the sequence are masked, rows past nnz read as 0);
-// S = Q K^T, dP = dO V^T, O = P V, dV = P^T dO, dK = dS^T Q, dQ = dS K all run as
-// tcgen05.mma kind::f16 with fp32 accumulators in TMEM.  One thread owns one tile row: it reads its
-// row of S from TMEM (tcgen05.ld), adds the ALiBi bias computed from the two positions (never
-// materialised), does the exp2-domain softmax in fp32, and writes P / dS as bf16 into shared memory
+// All kernels are persistent and warp-specialised: TMA producer / MMA issuer lanes plus 8 softmax
+// warps (two threads per 128-row tile row, 64 keys each).  Q/K/V/dO tiles come straight out of the
+// packed buffers by TMA (128-byte swizzle, rows past the sequence are masked, rows past nnz read as
+// 0); S = Q K^T, dP = dO V^T, O = P V, dV = P^T dO, dK = dS^T Q, dQ = dS K all run as tcgen05.mma
+// kind::f16 with fp32 accumulators in TMEM.  A thread reads its half-row of S from TMEM
+// (tcgen05.ld), adds the ALiBi bias computed from the two positions (never materialised), does the
+// exp2-domain softmax in fp32 on the paired fp32 pipe, and writes P / dS as bf16 into shared memory
 // in the same swizzled layout the next MMA consumes (K-major for P V and dS K, MN-major for the
-// transposed P^T dO and dS^T Q — the same bytes serve both views).
+// transposed P^T dO and dS^T Q — the same bytes serve both views).  Outputs leave by per-warp TMA
+// stores of 64B-swizzled [32 x 32] blocks.
+//   l <= 128 (C1/C2/C3/C5): one unit = (sequence, head), single-pass softmax.
+//   128 < l <= 2048 (C4, F4): forward units = (query tile, head, sequence) with the online softmax
+//   over key tiles; backward units = (key tile, head, sequence) over query tiles, dQ reduced in fp32.
 #include <algorithm>
 #include "common.cuh"
 #include "kernels.h"
@@ -36,378 +41,6 @@ __device__ __forceinline__ uint32_t p_off(int r, int c) {
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
-
-// ------------------------------------------------------------------------------------------ forward
-constexpr int FWD_SMEM = 3 * TILE_BYTES + P_BYTES + 1024 + 64;
-
-__global__ void __launch_bounds__(128) attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv,
-                                                       const int* __restrict__ cu, int H, int d,
-                                                       const float* __restrict__ slopes, bf16* __restrict__ O,
-                                                       float* __restrict__ lse, int nnz) {
-  const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int start = cu[b];
-  const int len = cu[b + 1] - start;
-  const int q0 = qt * TILE;
-  if (q0 >= len) return;
-
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sK = sQ + TILE_BYTES;
-  uint8_t* sV = sK + TILE_BYTES;
-  uint8_t* sP = sV + TILE_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + P_BYTES);  // q, kv, s, o
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) {
-    sm100::tma_prefetch(&tm_qkv);
-    for (int i = 0; i < 4; ++i) sm100::mbar_init(&bars[i], 1);
-    sm100::fence_barrier_init();
-  }
-  if (warp == 0) sm100::tmem_alloc(tslot, 256);
-  sm100::tc_fence_before();
-  __syncthreads();
-  sm100::tc_fence_after();
-  const uint32_t tbase = *tslot;
-  const uint32_t tS = tbase, tO = tbase + 128;
-  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-
-  if (tid == 0) {
-    sm100::mbar_arrive_expect_tx(&bars[0], TILE_BYTES);
-    sm100::tma_load_2d(sQ, &tm_qkv, &bars[0], h * d, start + q0);
-  }
-  const float sc2 = rsqrtf((float)d) * LOG2E;
-  const float sl2 = slopes[h] * LOG2E;
-  const int qi = q0 + tid;
-  float m = -INFINITY, l = 0.f;
-  float o[DT];
-#pragma unroll
-  for (int c = 0; c < DT; ++c) o[c] = 0.f;
-
-  const uint32_t sQa = sm100::smem_u32(sQ), sKa = sm100::smem_u32(sK), sVa = sm100::smem_u32(sV),
-                 sPa = sm100::smem_u32(sP);
-  int j = 0;
-  for (int kv0 = 0; kv0 < len; kv0 += TILE, ++j) {
-    const uint32_t ph = j & 1;
-    if (tid == 0) {
-      sm100::mbar_arrive_expect_tx(&bars[1], 2 * TILE_BYTES);
-      sm100::tma_load_2d(sK, &tm_qkv, &bars[1], H + h * d, start + kv0);
-      sm100::tma_load_2d(sV, &tm_qkv, &bars[1], 2 * H + h * d, start + kv0);
-      if (j == 0) sm100::mbar_wait(&bars[0], 0);
-      sm100::mbar_wait(&bars[1], ph);
-      sm100::tc_fence_after();
-      constexpr uint32_t id_s = sm100::idesc_bf16(128, 128, 0, 0);
-      for (int k = 0; k < d / 16; ++k)
-        sm100::mma_bf16_ss(tS, sm100::desc_kmajor_sw128(sQa + k * 32), sm100::desc_kmajor_sw128(sKa + k * 32), id_s,
-                           k > 0);
-      sm100::mma_commit(&bars[2]);
-    }
-    __syncwarp();
-    sm100::mbar_wait(&bars[2], ph);
-    sm100::tc_fence_after();
-    // pass 1: row max of the biased, scaled scores (log2 domain)
-    float mx = m;
-    float v[32];
-#pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
-      sm100::tmem_ld32(tS + lane_off + c * 32, v);
-      sm100::tmem_ld_wait();
-#pragma unroll
-      for (int jj = 0; jj < 32; ++jj) {
-        const int key = kv0 + c * 32 + jj;
-        const float x = v[jj] * sc2 - sl2 * fabsf((float)(qi - key));
-        if (key < len) mx = fmaxf(mx, x);
-      }
-    }
-    const float alpha = exp2f(m - mx);
-    // pass 2: P = exp2(x - max) -> bf16 -> swizzled smem; row sum
-    float rs = 0.f;
-#pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
-      sm100::tmem_ld32(tS + lane_off + c * 32, v);
-      sm100::tmem_ld_wait();
-      uint32_t pk[16];
-#pragma unroll
-      for (int jj = 0; jj < 32; jj += 2) {
-        const int key = kv0 + c * 32 + jj;
-        float p0 = key < len ? exp2f(v[jj] * sc2 - sl2 * fabsf((float)(qi - key)) - mx) : 0.f;
-        float p1 = key + 1 < len ? exp2f(v[jj + 1] * sc2 - sl2 * fabsf((float)(qi - key - 1)) - mx) : 0.f;
-        const bf162 hp = __floats2bfloat162_rn(p0, p1);
-        const float2 pr = __bfloat1622float2(hp);
-        rs += pr.x + pr.y;
-        pk[jj >> 1] = *reinterpret_cast<const uint32_t*>(&hp);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        st_shared_v4(sPa + p_off(tid, c * 32 + u * 8), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
-    }
-    l = l * alpha + rs;
-    m = mx;
-    sm100::fence_proxy_async_smem();
-    sm100::tc_fence_before();
-    __syncthreads();
-    if (tid == 0) {
-      sm100::tc_fence_after();
-      constexpr uint32_t id_o = sm100::idesc_bf16(128, 64, 0, 1);
-#pragma unroll
-      for (int k = 0; k < TILE / 16; ++k)
-        sm100::mma_bf16_ss(tO, sm100::desc_kmajor_sw128(sPa + (k >> 2) * (TILE * 128) + (k & 3) * 32),
-                           sm100::desc_mnmajor_sw128(sVa + k * 2048, 8192), id_o, k > 0);
-      sm100::mma_commit(&bars[3]);
-    }
-    __syncwarp();
-    sm100::mbar_wait(&bars[3], ph);
-    sm100::tc_fence_after();
-#pragma unroll
-    for (int c = 0; c < DT / 32; ++c) {
-      sm100::tmem_ld32(tO + lane_off + c * 32, v);
-      sm100::tmem_ld_wait();
-#pragma unroll
-      for (int jj = 0; jj < 32; ++jj) o[c * 32 + jj] = o[c * 32 + jj] * alpha + v[jj];
-    }
-    sm100::tc_fence_before();
-    __syncthreads();
-  }
-  if (qi < len) {
-    const float inv = 1.f / l;
-    bf16* dst = O + (size_t)(start + qi) * H + h * d;
-#pragma unroll
-    for (int c = 0; c < DT; c += 8) {
-      if (c < d) {
-        float t[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) t[u] = o[c + u] * inv;
-        *reinterpret_cast<uint4*>(dst + c) = f32_to_bf16x8(t);
-      }
-    }
-    lse[(size_t)h * nnz + start + qi] = (m + log2f(l)) * LN2;
-  }
-  sm100::tc_fence_before();
-  __syncthreads();
-  if (warp == 0) sm100::tmem_dealloc(tbase, 256);
-}
-
-// ------------------------------------------------------------------------------------------ backward
-constexpr int BWD_SMEM = 4 * TILE_BYTES + 2 * P_BYTES + 1024 + 64;
-
-__global__ void __launch_bounds__(128) attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv,
-                                                       const __grid_constant__ CUtensorMap tm_do,
-                                                       const int* __restrict__ cu, int H, int d,
-                                                       const float* __restrict__ slopes, const bf16* __restrict__ O,
-                                                       const bf16* __restrict__ dO, const float* __restrict__ lse,
-                                                       bf16* __restrict__ dqkv, float* __restrict__ dq_acc, int nnz) {
-  const int jt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int start = cu[b];
-  const int len = cu[b + 1] - start;
-  const int kv0 = jt * TILE;
-  if (kv0 >= len) return;
-  const int nq = (len + TILE - 1) / TILE;
-  const bool multi = nq > 1;
-
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sK = sQ + TILE_BYTES;
-  uint8_t* sV = sK + TILE_BYTES;
-  uint8_t* sdO = sV + TILE_BYTES;
-  uint8_t* sP = sdO + TILE_BYTES;
-  uint8_t* sdS = sP + P_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sdS + P_BYTES);  // kv, q, sp, acc
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
-
-  const int tid = threadIdx.x, warp = tid >> 5;
-  if (tid == 0) {
-    sm100::tma_prefetch(&tm_qkv);
-    sm100::tma_prefetch(&tm_do);
-    for (int i = 0; i < 4; ++i) sm100::mbar_init(&bars[i], 1);
-    sm100::fence_barrier_init();
-  }
-  if (warp == 0) sm100::tmem_alloc(tslot, 512);
-  sm100::tc_fence_before();
-  __syncthreads();
-  sm100::tc_fence_after();
-  const uint32_t tbase = *tslot;
-  const uint32_t tS = tbase, tdP = tbase + 128, tdV = tbase + 256, tdK = tbase + 320, tdQ = tbase + 384;
-  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-  const uint32_t sQa = sm100::smem_u32(sQ), sKa = sm100::smem_u32(sK), sVa = sm100::smem_u32(sV),
-                 sdOa = sm100::smem_u32(sdO), sPa = sm100::smem_u32(sP), sdSa = sm100::smem_u32(sdS);
-
-  if (tid == 0) {
-    sm100::mbar_arrive_expect_tx(&bars[0], 2 * TILE_BYTES);
-    sm100::tma_load_2d(sK, &tm_qkv, &bars[0], H + h * d, start + kv0);
-    sm100::tma_load_2d(sV, &tm_qkv, &bars[0], 2 * H + h * d, start + kv0);
-  }
-  const float rsd = rsqrtf((float)d);
-  const float sc2 = rsd * LOG2E;
-  const float sl2 = slopes[h] * LOG2E;
-  float v[32], w[32];
-
-  for (int it = 0; it < nq; ++it) {
-    const uint32_t ph = it & 1;
-    const int q0 = it * TILE;
-    const int qi = q0 + tid;
-    if (tid == 0) {
-      sm100::mbar_arrive_expect_tx(&bars[1], 2 * TILE_BYTES);
-      sm100::tma_load_2d(sQ, &tm_qkv, &bars[1], h * d, start + q0);
-      sm100::tma_load_2d(sdO, &tm_do, &bars[1], h * d, start + q0);
-    }
-    // per-row LSE and D_i = dO_i . O_i
-    float lse2 = 0.f, Dr = 0.f;
-    if (qi < len) {
-      lse2 = lse[(size_t)h * nnz + start + qi] * LOG2E;
-      const bf16* o_row = O + (size_t)(start + qi) * H + h * d;
-      const bf16* do_row = dO + (size_t)(start + qi) * H + h * d;
-      for (int c = 0; c < d; c += 8) {
-        float a[8], g[8];
-        bf16x8_to_f32(*reinterpret_cast<const uint4*>(o_row + c), a);
-        bf16x8_to_f32(*reinterpret_cast<const uint4*>(do_row + c), g);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) Dr += a[u] * g[u];
-      }
-    }
-    if (tid == 0) {
-      if (it == 0) sm100::mbar_wait(&bars[0], 0);
-      sm100::mbar_wait(&bars[1], ph);
-      sm100::tc_fence_after();
-      constexpr uint32_t id_s = sm100::idesc_bf16(128, 128, 0, 0);
-      for (int k = 0; k < d / 16; ++k) {
-        sm100::mma_bf16_ss(tS, sm100::desc_kmajor_sw128(sQa + k * 32), sm100::desc_kmajor_sw128(sKa + k * 32), id_s,
-                           k > 0);
-        sm100::mma_bf16_ss(tdP, sm100::desc_kmajor_sw128(sdOa + k * 32), sm100::desc_kmajor_sw128(sVa + k * 32),
-                           id_s, k > 0);
-      }
-      sm100::mma_commit(&bars[2]);
-    }
-    __syncwarp();
-    sm100::mbar_wait(&bars[2], ph);
-    sm100::tc_fence_after();
-#pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
-      sm100::tmem_ld32(tS + lane_off + c * 32, v);
-      sm100::tmem_ld32(tdP + lane_off + c * 32, w);
-      sm100::tmem_ld_wait();
-      uint32_t pp[16], pd[16];
-#pragma unroll
-      for (int jj = 0; jj < 32; jj += 2) {
-        float p2[2], ds2[2];
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int key = kv0 + c * 32 + jj + e;
-          const bool ok = (qi < len) && (key < len);
-          const float p = ok ? exp2f(v[jj + e] * sc2 - sl2 * fabsf((float)(qi - key)) - lse2) : 0.f;
-          p2[e] = p;
-          ds2[e] = p * (w[jj + e] - Dr);
-        }
-        pp[jj >> 1] = pack_bf16x2(p2[0], p2[1]);
-        pd[jj >> 1] = pack_bf16x2(ds2[0], ds2[1]);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t off = p_off(tid, c * 32 + u * 8);
-        st_shared_v4(sPa + off, pp[4 * u], pp[4 * u + 1], pp[4 * u + 2], pp[4 * u + 3]);
-        st_shared_v4(sdSa + off, pd[4 * u], pd[4 * u + 1], pd[4 * u + 2], pd[4 * u + 3]);
-      }
-    }
-    sm100::fence_proxy_async_smem();
-    sm100::tc_fence_before();
-    __syncthreads();
-    if (tid == 0) {
-      sm100::tc_fence_after();
-      constexpr uint32_t id_t = sm100::idesc_bf16(128, 64, 1, 1);  // P^T dO, dS^T Q
-      constexpr uint32_t id_q = sm100::idesc_bf16(128, 64, 0, 1);  // dS K
-#pragma unroll
-      for (int k = 0; k < TILE / 16; ++k) {
-        const uint32_t acc = (it > 0 || k > 0) ? 1u : 0u;
-        sm100::mma_bf16_ss(tdV, sm100::desc_mnmajor_sw128(sPa + k * 2048, TILE * 128),
-                           sm100::desc_mnmajor_sw128(sdOa + k * 2048, 8192), id_t, acc);
-        sm100::mma_bf16_ss(tdK, sm100::desc_mnmajor_sw128(sdSa + k * 2048, TILE * 128),
-                           sm100::desc_mnmajor_sw128(sQa + k * 2048, 8192), id_t, acc);
-        sm100::mma_bf16_ss(tdQ, sm100::desc_kmajor_sw128(sdSa + (k >> 2) * (TILE * 128) + (k & 3) * 32),
-                           sm100::desc_mnmajor_sw128(sKa + k * 2048, 8192), id_q, k > 0);
-      }
-      sm100::mma_commit(&bars[3]);
-    }
-    __syncwarp();
-    sm100::mbar_wait(&bars[3], ph);
-    sm100::tc_fence_after();
-    // dQ rows (query = qi)
-#pragma unroll 1
-    for (int c = 0; c < DT / 32; ++c) {
-      sm100::tmem_ld32(tdQ + lane_off + c * 32, v);
-      sm100::tmem_ld_wait();
-      if (qi < len) {
-        if (!multi) {
-          bf16* dst = dqkv + (size_t)(start + qi) * 3 * H + h * d + c * 32;
-#pragma unroll
-          for (int u = 0; u < 32; u += 8) {
-            if (c * 32 + u < d) {
-              float t[8];
-#pragma unroll
-              for (int e = 0; e < 8; ++e) t[e] = v[u + e] * rsd;
-              *reinterpret_cast<uint4*>(dst + u) = f32_to_bf16x8(t);
-            }
-          }
-        } else {
-          float* dst = dq_acc + (size_t)(start + qi) * H + h * d + c * 32;
-#pragma unroll
-          for (int u = 0; u < 32; u += 4)
-            if (c * 32 + u < d) red_add_v4(dst + u, v[u] * rsd, v[u + 1] * rsd, v[u + 2] * rsd, v[u + 3] * rsd);
-        }
-      }
-    }
-    sm100::tc_fence_before();
-    __syncthreads();
-  }
-  // dK, dV rows (key = kv0 + tid)
-  const int kj = kv0 + tid;
-#pragma unroll 1
-  for (int c = 0; c < DT / 32; ++c) {
-    sm100::tmem_ld32(tdK + lane_off + c * 32, v);
-    sm100::tmem_ld32(tdV + lane_off + c * 32, w);
-    sm100::tmem_ld_wait();
-    if (kj < len) {
-      bf16* dk = dqkv + (size_t)(start + kj) * 3 * H + H + h * d + c * 32;
-      bf16* dv = dk + H;
-#pragma unroll
-      for (int u = 0; u < 32; u += 8) {
-        if (c * 32 + u < d) {
-          float t[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) t[e] = v[u + e] * rsd;
-          *reinterpret_cast<uint4*>(dk + u) = f32_to_bf16x8(t);
-          *reinterpret_cast<uint4*>(dv + u) = f32_to_bf16x8(w + u);
-        }
-      }
-    }
-  }
-  sm100::tc_fence_before();
-  __syncthreads();
-  if (warp == 0) sm100::tmem_dealloc(tbase, 512);
-}
-
-// dq_acc fp32 [nnz, H] -> dqkv[:, :H] bf16 (multi-tile sequences only; single-tile rows were
-// written directly and have dq_acc == 0 rows that are skipped via the per-row length test)
-__global__ void dq_convert_kernel(const float* __restrict__ dq_acc, const int* __restrict__ cu, int batch, int nnz,
-                                  int H, bf16* __restrict__ dqkv) {
-  const int row = blockIdx.x;
-  // binary search the sequence of this row
-  int lo = 0, hi = batch;
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (cu[mid] <= row) lo = mid;
-    else hi = mid;
-  }
-  if (cu[lo + 1] - cu[lo] <= TILE) return;
-  for (int c = threadIdx.x * 8; c < H; c += blockDim.x * 8) {
-    const float* s = dq_acc + (size_t)row * H + c;
-    float t[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) t[e] = s[e];
-    *reinterpret_cast<uint4*>(dqkv + (size_t)row * 3 * H + c) = f32_to_bf16x8(t);
-  }
-}
-
 
 // ------------------------------------------------------------------------------------------
 // Short-sequence path (l <= 128: every workload of BASELINE configs 1, 2, 3, 5): one (sequence,
