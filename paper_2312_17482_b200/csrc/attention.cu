@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const
       sm100::tmem_ld_wait();
       float mx = len == TILE ? fwd_scores<false>(x, r, ch, len, sc2, sl2) : fwd_scores<true>(x, r, ch, len, sc2, sl2);
       rmax[ch * 128 + r] = mx;
-      named_bar_sync(1, SH_THREADS);
+      named_bar_sync(1 + (warp & 3), 64);  // the two half-row warps only
       mx = fmaxf(rmax[r], rmax[128 + r]);
       // P = 2^(x - max) rounded to bf16 (the operand of O = P V); the row sum is taken over the
       // rounded values so that the normalisation matches the product exactly
@@ -280,18 +280,45 @@ __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const
 }
 
 // ------------------------------------------------------------------------------------------
+// Long-forward scores in the unscaled domain y = S - (m_h / sc) |q - k| (sc = log2e / sqrt(d) is
+// applied inside the exponent, P = 2^(sc y - sc max y)); distances stepped by -2 per key pair so
+// no per-pair constants are materialised.  Returns max_j y (-inf past the sequence when MASK).
+template <bool MASK>
+__device__ __forceinline__ float lf_scores(float (&x)[64], int r, int ch, int keys, float slr, int qk_off) {
+  const float rc = (float)(r + qk_off - 64 * ch);
+  float2 dd = make_float2(rc, rc - 1.f);
+  float mx = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < 64; j += 2) {
+    const float2 t = __ffma2_rn(make_float2(fabsf(dd.x), fabsf(dd.y)), make_float2(-slr, -slr),
+                                make_float2(x[j], x[j + 1]));
+    dd = __fadd2_rn(dd, make_float2(-2.f, -2.f));
+    x[j] = t.x;
+    x[j + 1] = t.y;
+    if (MASK) {
+      x[j] = 64 * ch + j < keys ? x[j] : -INFINITY;
+      x[j + 1] = 64 * ch + j + 1 < keys ? x[j + 1] : -INFINITY;
+    }
+    mx = fmaxf(mx, fmaxf(x[j], x[j + 1]));
+  }
+  return mx;
+}
+
 // Long-sequence forward (128 < l <= 2048, SURVEY A5 at l = 512 and F4): one work unit = (128-row
 // query tile, head, sequence), iterating over the sequence's key tiles with the online softmax.
 // Warp 9 (one lane) streams Q (double-buffered per unit) and K/V tiles (LF_NS-stage ring) by TMA;
 // warp 8 (one lane) issues S_{g+1} = Q K_{g+1}^T into the other half of a double-buffered TMEM S
 // while the softmax warps work on S_g, then PV_g = P_g V_g into a double-buffered TMEM PV;
 // warps 0-7 (two threads per query row, 64 keys each) compute the exp2-domain online softmax and
-// fold PV_{g-1} into their fp32 registers (o = alpha_{g-1} o + PV_{g-1}) before writing P_g.
-// TMEM: S [0,256) (2 x 128), PV [256,384) (2 x 64).
+// fold PV_{g-1} into their fp32 registers (o = alpha_{g-1} o + PV_{g-1}) before writing P_g.  The
+// softmax denominator comes from the tensor core too: an N=16 MMA of P_g against an all-ones tile
+// gives the row sums of the bf16 P the PV product used, folded like PV (l = alpha l + sum).
+// TMEM: S [0,256) (2 x 128), PV [256,384) (2 x 64), row sums [384,416) (2 x 16).
 // ------------------------------------------------------------------------------------------
 constexpr int LF_NS = 3;
 constexpr int LF_THREADS = SH_THREADS + 64;
-constexpr int LF_SMEM = 2 * TILE_BYTES + LF_NS * 2 * TILE_BYTES + P_BYTES + 1024 + 256;
+constexpr int ONES_BYTES = 16 * TILE * 2;  // [16 x 128] bf16 ones: B operand of the row-sum MMA
+constexpr int LF_SMEM = 2 * TILE_BYTES + LF_NS * 2 * TILE_BYTES + P_BYTES + ONES_BYTES + 1024 + 256;
 
 struct LongUnits {  // unit u = (b * heads + h) * QT + qt, valid iff qt * 128 < len_b
   const int* cu;
@@ -329,7 +356,8 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
   uint8_t* sQ = smem;                              // 2 x Q
   uint8_t* sKV = sQ + 2 * TILE_BYTES;              // LF_NS x (K, V)
   uint8_t* sP = sKV + LF_NS * 2 * TILE_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + P_BYTES);
+  uint8_t* sOnes = sP + P_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sOnes + ONES_BYTES);
   uint64_t* q_full = bars;                         // [2]
   uint64_t* q_empty = bars + 2;                    // [2]
   uint64_t* kv_full = bars + 4;                    // [LF_NS]
@@ -338,7 +366,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
   uint64_t* pv_full = bars + 6 + 2 * LF_NS;        // [2]
   uint64_t* p_ready = bars + 8 + 2 * LF_NS;        // 8 softmax warps
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 16);
-  __shared__ float rmax[2][2 * TILE], lsum[2 * TILE];
+  __shared__ float rmax[2][2 * TILE];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int H = U.heads * d;
@@ -358,12 +386,16 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
     sm100::mbar_init(p_ready, 8);
     sm100::fence_barrier_init();
   }
+  for (int i = tid; i < ONES_BYTES / 16; i += LF_THREADS)  // bf16 1.0 = 0x3F80 (any swizzle of ones is ones)
+    reinterpret_cast<uint4*>(sOnes)[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+  sm100::fence_proxy_async_smem();
   if (warp == 0) sm100::tmem_alloc(tslot, 512);
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tbase = *tslot;
-  const uint32_t sQa = sm100::smem_u32(sQ), sKVa = sm100::smem_u32(sKV), sPa = sm100::smem_u32(sP);
+  const uint32_t sQa = sm100::smem_u32(sQ), sKVa = sm100::smem_u32(sKV), sPa = sm100::smem_u32(sP),
+                 sOa = sm100::smem_u32(sOnes);
   auto nkv_of = [&](int u) {
     int b, h, qt;
     U.decode(u, b, h, qt);
@@ -398,6 +430,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
     if (lane == 0) {
       constexpr uint32_t id_s = sm100::idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t id_o = sm100::idesc_bf16(128, 64, 0, 1);
+      constexpr uint32_t id_l = sm100::idesc_bf16(128, 16, 0, 0);
       // (unit, tile) cursor over this CTA's flattened tile sequence
       int u = U.first(), uc = 0, j = 0, nkv = u < U.total ? nkv_of(u) : 0;
       auto issue_s = [&](int g, int uu_c, int last) {  // S_g = Q K_g^T into S buffer g & 1
@@ -432,10 +465,13 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
         sm100::tc_fence_after();
         const uint32_t v = sKVa + (g % LF_NS) * 2 * TILE_BYTES + TILE_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < TILE / 16; ++kk)
-          sm100::mma_bf16_ss(tbase + 256 + 64 * (g & 1),
-                             sm100::desc_kmajor_sw128(sPa + (kk >> 2) * (TILE * 128) + (kk & 3) * 32),
-                             sm100::desc_mnmajor_sw128(v + kk * 2048, 8192), id_o, kk > 0);
+        for (int kk = 0; kk < TILE / 16; ++kk) {
+          const uint64_t pa = sm100::desc_kmajor_sw128(sPa + (kk >> 2) * (TILE * 128) + (kk & 3) * 32);
+          sm100::mma_bf16_ss(tbase + 256 + 64 * (g & 1), pa, sm100::desc_mnmajor_sw128(v + kk * 2048, 8192), id_o,
+                             kk > 0);
+          sm100::mma_bf16_ss(tbase + 384 + 16 * (g & 1), pa,
+                             sm100::desc_kmajor_sw128(sOa + (kk >> 2) * 2048 + (kk & 3) * 32), id_l, kk > 0);
+        }
         sm100::mma_commit(&pv_full[g & 1]);
         sm100::mma_commit(&kv_empty[g % LF_NS]);
         u = u2, uc = uc2, j = j2, nkv = nkv2;
@@ -454,8 +490,8 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
       U.decode(u, b, h, qt);
       const int start = U.cu[b], len = U.cu[b + 1] - start, q0 = qt * TILE;
       const int nkv = (len + TILE - 1) / TILE;
-      const float sl2 = slopes[h] * LOG2E;
-      float m = -INFINITY, l = 0.f, alpha_prev = 0.f;
+      const float slr = slopes[h] * sqrtf((float)d);  // m_h / (1/sqrt(d)): bias in the unscaled domain
+      float m = -INFINITY, l = 0.f, alpha_prev = 0.f;  // m: running max of y; l: running sum (both rows' halves)
       float o[32];
 #pragma unroll
       for (int e = 0; e < 32; ++e) o[e] = 0.f;
@@ -471,17 +507,18 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
         sm100::tmem_ld32(tS, x);
         sm100::tmem_ld32(tS + 32, x + 32);
         sm100::tmem_ld_wait();
-        const float mx = len - kv0 >= TILE ? fwd_scores<false>(x, r, ch, len - kv0, sc2, sl2, q0 - kv0)
-                                           : fwd_scores<true>(x, r, ch, len - kv0, sc2, sl2, q0 - kv0);
+        const float mx = len - kv0 >= TILE ? lf_scores<false>(x, r, ch, len - kv0, slr, q0 - kv0)
+                                           : lf_scores<true>(x, r, ch, len - kv0, slr, q0 - kv0);
         rmax[g & 1][ch * TILE + r] = mx;
-        named_bar_sync(1, SH_THREADS);
+        named_bar_sync(1 + (warp & 3), 64);  // the two half-row warps only
         const float m_new = fmaxf(m, fmaxf(rmax[g & 1][r], rmax[g & 1][TILE + r]));
-        const float alpha = ex2_approx(m - m_new);
-        if (j > 0) {  // fold PV_{g-1}: o = alpha_{g-1} o + PV_{g-1}; its completion also frees sP
+        const float alpha = ex2_approx((m - m_new) * sc2);
+        if (j > 0) {  // fold PV_{g-1} and its row sum: o = alpha_{g-1} o + PV_{g-1}; frees sP
           sm100::mbar_wait(&pv_full[(g - 1) & 1], ((g - 1) >> 1) & 1);
           sm100::tc_fence_after();
           float pv[32];
           sm100::tmem_ld32(tbase + 256 + 64 * ((g - 1) & 1) + lane_off + 32 * ch, pv);
+          const float ls = sm100::tmem_ld1(tbase + 384 + 16 * ((g - 1) & 1) + lane_off);
           sm100::tmem_ld_wait();
 #pragma unroll
           for (int e = 0; e < 32; e += 2) {
@@ -490,22 +527,21 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
             o[e] = t.x;
             o[e + 1] = t.y;
           }
+          l = fmaf(l, alpha_prev, ls);
         }
-        // P_g = 2^(x - m_new) rounded to bf16 (the PV operand); row sum over the rounded values
-        float2 sum2 = make_float2(0.f, 0.f);
+        // P_g = 2^(sc (y - m_new)) rounded to bf16 (the PV operand; its row sums come from the MMA)
+        const float nm = -m_new * sc2;
 #pragma unroll
         for (int j8 = 0; j8 < 8; ++j8) {
           uint32_t pk[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const float2 t = __fadd2_rn(make_float2(x[j8 * 8 + 2 * e], x[j8 * 8 + 2 * e + 1]),
-                                        make_float2(-m_new, -m_new));
+            const float2 t = __ffma2_rn(make_float2(x[j8 * 8 + 2 * e], x[j8 * 8 + 2 * e + 1]), make_float2(sc2, sc2),
+                                        make_float2(nm, nm));
             pk[e] = pack_bf16x2(ex2_approx(t.x), ex2_approx(t.y));
-            sum2 = __fadd2_rn(sum2, make_float2(__uint_as_float(pk[e] << 16), __uint_as_float(pk[e] & 0xffff0000u)));
           }
           st_shared_v4(sPa + p_off(r, 64 * ch + 8 * j8), pk[0], pk[1], pk[2], pk[3]);
         }
-        l = l * alpha + (sum2.x + sum2.y);
         m = m_new;
         alpha_prev = alpha;
         sm100::fence_proxy_async_smem();
@@ -519,13 +555,13 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
       {
         float pv[32];
         sm100::tmem_ld32(tbase + 256 + 64 * ((g - 1) & 1) + lane_off + 32 * ch, pv);
+        const float ls = sm100::tmem_ld1(tbase + 384 + 16 * ((g - 1) & 1) + lane_off);
         sm100::tmem_ld_wait();
 #pragma unroll
         for (int e = 0; e < 32; ++e) o[e] = fmaf(o[e], alpha_prev, pv[e]);
+        l = fmaf(l, alpha_prev, ls);
       }
-      lsum[ch * TILE + r] = l;
-      named_bar_sync(1, SH_THREADS);
-      const float lt = lsum[r] + lsum[TILE + r];
+      const float lt = l;  // full-row sum (the MMA summed all 128 keys of each tile)
       const float inv = 1.f / lt;
 #pragma unroll
       for (int e = 0; e < 32; ++e) o[e] *= inv;
@@ -550,7 +586,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
           for (int c = 0; c < 32; c += 8) *reinterpret_cast<uint4*>(dst + c) = f32_to_bf16x8(o + c);
         }
       }
-      if (ch == 0 && qrow < len) lse[(size_t)h * nnz + start + qrow] = (m + log2f(lt)) * LN2;
+      if (ch == 0 && qrow < len) lse[(size_t)h * nnz + start + qrow] = (m * sc2 + log2f(lt)) * LN2;
       sm100::tc_fence_before();
     }
     if (lane == 0) sm100::bulk_wait0();
@@ -794,7 +830,7 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(p_ready);
       dred[ch * 128 + r] = Dp;
-      named_bar_sync(1, SH_THREADS);
+      named_bar_sync(1 + (warp & 3), 64);  // the two half-row warps only
       const float Dr = dred[r] + dred[128 + r];
       // pass 2: dS/sqrt(d) = P (dP - D)/sqrt(d) — the 1/sqrt(d) of dQ = dS K / sqrt(d) and
       // dK = dS^T Q / sqrt(d) is folded in here (exact for d = 64), so the readout does no scaling
@@ -921,30 +957,40 @@ __global__ void attn_bwd_prep_kernel(const bf16* __restrict__ O, const bf16* __r
   D[(size_t)h * nnz + t] = acc;
 }
 
-// dq_acc fp32 [nnz, H] -> dqkv[:, :H] bf16, and db_q += column sums (block-local, one atomic per
-// column per block)
+// dq_acc fp32 [nnz, H] -> dqkv[:, :H] bf16, and db_q += column sums: a CTA of DQF_GROUPS row groups x
+// (H / 8) column vectors covers rows_per rows, reduces its groups through smem and issues one
+// atomic per column (a few hundred per address instead of one per 16 rows)
+constexpr int DQF_GROUPS = 8;
 __global__ void dq_finish_kernel(const float* __restrict__ dq_acc, int nnz, int H, int rows_per, bf16* __restrict__ dqkv,
                                  float* __restrict__ db) {
-  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
-  if (c >= H) return;
-  const int r0 = blockIdx.y * rows_per, r1 = min(nnz, r0 + rows_per);
+  extern __shared__ float red[];  // [DQF_GROUPS][H]
+  const int cv = threadIdx.x, rg = threadIdx.y;
+  const int c = cv * 8;
+  const int r0 = blockIdx.x * rows_per, r1 = min(nnz, r0 + rows_per);
   float cs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int r = r0; r < r1; ++r) {
+  for (int r = r0 + rg; r < r1; r += DQF_GROUPS) {
     const float4* src = reinterpret_cast<const float4*>(dq_acc + (size_t)r * H + c);
     const float4 a = src[0], b = src[1];
     const float t[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
     const uint4 pk = f32_to_bf16x8(t);
     *reinterpret_cast<uint4*>(dqkv + (size_t)r * 3 * H + c) = pk;
-    if (db) {
-      float f[8];
-      bf16x8_to_f32(pk, f);
+    float f[8];
+    bf16x8_to_f32(pk, f);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) cs[e] += f[e];
-    }
+    for (int e = 0; e < 8; ++e) cs[e] += f[e];
   }
-  if (db) {
+  if (!db) return;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) atomicAdd(db + c + e, cs[e]);
+  for (int e = 0; e < 8; ++e) red[rg * H + c + e] = cs[e];
+  __syncthreads();
+  if (rg == 0) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      float t = 0.f;
+#pragma unroll
+      for (int k = 0; k < DQF_GROUPS; ++k) t += red[k * H + c + e];
+      atomicAdd(db + c + e, t);
+    }
   }
 }
 
@@ -1149,20 +1195,36 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
         for (int e = 0; e < 32; e += 4) red_add_v4(dst + e, v[e], v[e + 1], v[e + 2], v[e + 3]);
       }
     };
+    // LSE and D of row r of query tile ii of unit uu, loaded one block ahead of their use
+    auto row_stats = [&](int uu, int ii, float& l_, float& d_) {
+      l_ = 0.f, d_ = 0.f;
+      if (uu >= U.total) return;
+      int bb, hh, jj;
+      U.decode(uu, bb, hh, jj);
+      const int st = U.cu[bb], q = ii * TILE + r;
+      if (q < U.cu[bb + 1] - st) {
+        l_ = lse[(size_t)hh * nnz + st + q];
+        d_ = Dg[(size_t)hh * nnz + st + q];
+      }
+    };
+    float lse_c, D_c;
+    row_stats(U.first(), 0, lse_c, D_c);
     for (int u = U.first(); u < U.total; u = U.next(u)) {
       int b, h, jt;
       U.decode(u, b, h, jt);
       const int start = U.cu[b], len = U.cu[b + 1] - start, kv0 = jt * TILE;
       const int nq = (len + TILE - 1) / TILE;
       const float sl2 = slopes[h] * LOG2E;
+      const int un = U.next(u);
       // this warp's P / dS slabs double as dK/dV staging: the previous unit's stores must have read them
       if (lane == 0) sm100::bulk_wait_read0();
       __syncwarp();
       for (int i = 0; i < nq; ++i, ++g) {
         const int q0 = i * TILE;
-        const bool rv = q0 + r < len;
-        const float lse2 = rv ? lse[(size_t)h * nnz + start + q0 + r] * LOG2E : 0.f;
-        const float Drs = rv ? -Dg[(size_t)h * nnz + start + q0 + r] * rsd : 0.f;
+        const float lse2 = lse_c * LOG2E;
+        const float Drs = -D_c * rsd;
+        if (i + 1 < nq) row_stats(u, i + 1, lse_c, D_c);
+        else row_stats(un, 0, lse_c, D_c);
         sm100::mbar_wait(sp_full, g & 1);
         sm100::tc_fence_after();
         if (i > 0) {  // block g-1's MMAs finished (P/dS free); its dQ is ready
@@ -1337,10 +1399,9 @@ mb_status attention_bwd(const bf16* qkv, const bf16* O, const bf16* dO, const fl
                                                          nnz);
   MB_CHECK_LAUNCH();
   {
-    const int bx = (H / 8 + 127) / 128;
-    const int rows_per = 16;  // ~4K CTAs at C4: enough loads in flight for HBM
-    const int by = (nnz + rows_per - 1) / rows_per;
-    dq_finish_kernel<<<dim3(bx, by), 128, 0, s>>>(dq_acc, nnz, H, rows_per, dqkv, dbias);
+    const int rows_per = 128;
+    dq_finish_kernel<<<(nnz + rows_per - 1) / rows_per, dim3(H / 8, DQF_GROUPS), DQF_GROUPS * H * sizeof(float),
+                       s>>>(dq_acc, nnz, H, rows_per, dqkv, dbias);
     MB_CHECK_LAUNCH();
   }
   return MB_OK;
