@@ -7,6 +7,7 @@
 // output is rounded once to bf16.  Backward column sums (dgamma, dbeta, and the preceding linear's
 // bias gradient sum dx) accumulate per warp in registers, reduce per CTA through shared memory and
 // reach global fp32 with one atomic per column per CTA.
+#include <algorithm>
 #include "common.cuh"
 #include "kernels.h"
 
@@ -48,6 +49,68 @@ __device__ __forceinline__ void load_row(const RowSrc& src, int row, int H, int 
 #pragma unroll
       for (int j = 0; j < 8; ++j) v[i * 8 + j] = 0.f;
     }
+  }
+}
+
+// Persistent variant for the encoder LNs: each warp walks rows with a grid stride, keeps gamma and
+// beta in registers and has the next row's loads in flight while it reduces the current one (twice
+// the bytes in flight per SM of the one-row-per-warp launch).
+constexpr int LNP_BLOCKS = 3;  // resident CTAs per SM of the persistent forward
+template <int VPL>
+__global__ void __launch_bounds__(LN_THREADS, LNP_BLOCKS) ln_fwd_persist_kernel(const bf16* __restrict__ x,
+                                                                                const bf16* __restrict__ gamma,
+                                                                                const bf16* __restrict__ beta, int n,
+                                                                                int H, float eps,
+                                                                                bf16* __restrict__ y,
+                                                                                float* __restrict__ stats) {
+  const int lane = threadIdx.x & 31;
+  const int step = gridDim.x * LN_WARPS;
+  uint4 nx[VPL];
+  int row = blockIdx.x * LN_WARPS + (threadIdx.x >> 5);
+  auto fetch = [&](int r) {
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const int c = (i * 32 + lane) * 8;
+      nx[i] = c < H ? ld_nc_v4(x + (size_t)r * H + c) : make_uint4(0, 0, 0, 0);
+    }
+  };
+  if (row < n) fetch(row);
+  const float inv_h = __frcp_rn((float)H);
+  for (; row < n; row += step) {
+    float v[VPL * 8];
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) bf16x8_to_f32(nx[i], v + i * 8);
+    if (row + step < n) fetch(row + step);
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < VPL * 8; ++i) s += v[i];
+    const float mean = warp_sum(s) * inv_h;
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const int c = (i * 32 + lane) * 8;
+      if (c < H) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float d = v[i * 8 + j] - mean;
+          q += d * d;
+        }
+      }
+    }
+    const float rstd = rsqrtf(warp_sum(q) * inv_h + eps);
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const int c = (i * 32 + lane) * 8;
+      if (c < H) {
+        float g[8], bt[8], o[8];
+        bf16x8_to_f32(*reinterpret_cast<const uint4*>(gamma + c), g);
+        bf16x8_to_f32(*reinterpret_cast<const uint4*>(beta + c), bt);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = (v[i * 8 + j] - mean) * rstd * g[j] + bt[j];
+        *reinterpret_cast<uint4*>(y + (size_t)row * H + c) = f32_to_bf16x8(o);
+      }
+    }
+    if (lane == 0) *reinterpret_cast<float2*>(stats + 2 * (size_t)row) = make_float2(mean, rstd);
   }
 }
 
@@ -381,6 +444,15 @@ mb_status ln_fwd_dispatch(const RowSrc& src, const bf16* gamma, const bf16* beta
   if (n == 0) return MB_OK;
   const int grid = (n + LN_WARPS - 1) / LN_WARPS;
   const int vpl = (H / 8 + 31) / 32;
+  if (!EMBED && (vpl == 3 || vpl == 4) && n >= 4096) {
+    const int pgrid = std::min(grid, LNP_BLOCKS * num_sms());  // one resident wave, rows strided
+    if (vpl == 3)
+      ln_fwd_persist_kernel<3><<<pgrid, LN_THREADS, 0, s>>>(src.x, gamma, beta, n, H, eps, y, stats);
+    else
+      ln_fwd_persist_kernel<4><<<pgrid, LN_THREADS, 0, s>>>(src.x, gamma, beta, n, H, eps, y, stats);
+    MB_CHECK_LAUNCH();
+    return MB_OK;
+  }
   switch (vpl) {
     case 1: ln_fwd_kernel<1, EMBED><<<grid, LN_THREADS, 0, s>>>(src, gamma, beta, n, H, eps, y, stats); break;
     case 2: ln_fwd_kernel<2, EMBED><<<grid, LN_THREADS, 0, s>>>(src, gamma, beta, n, H, eps, y, stats); break;
