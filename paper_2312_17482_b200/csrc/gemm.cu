@@ -325,7 +325,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         } else {
           const int c = lane >> 2, seg = lane & 3;
           const int col = nb * BN + grp * (BN / 2) + c * 32 + seg * 8;
-          if (c < BN / 64 && col < N) cp_async16(sbias + c * 64 + seg * 16, ep.bias + col);
+          if (c < BN / 64 && col < N) {
+            if (col + 8 <= N) {
+              cp_async16(sbias + c * 64 + seg * 16, ep.bias + col);
+            } else {  // ragged last vector (N % 8 != 0): never read past the bias array
+              for (int e = 0; e < 8; ++e) {
+                const bf16 bv = col + e < N ? ep.bias[col + e] : __float2bfloat16(0.f);
+                asm volatile("st.shared.b16 [%0], %1;" ::"r"(sbias + c * 64 + seg * 16 + 2 * e),
+                             "h"(*reinterpret_cast<const unsigned short*>(&bv)));
+              }
+            }
+          }
         }
       }
       uint4 pa[4], pg[4];  // first input chunk (residual / Gd), prefetched before the accumulator is ready
@@ -847,7 +857,11 @@ mb_status gemm(const GemmArgs& g, cudaStream_t s) {
   MB_REQUIRE(g.M >= 0 && g.N >= 0 && g.K >= 0, MB_ERR_INVALID_ARG);
   if (g.M == 0 || g.N == 0) return MB_OK;
   MB_REQUIRE(g.K > 0, MB_ERR_INVALID_ARG);
-  MB_REQUIRE(g.N % 8 == 0 && g.lda % 8 == 0 && g.ldb % 8 == 0, MB_ERR_CONFIG);
+  // N % 8 != 0 only for the decoder's fused-CE GEMMs (any vocabulary, F3): their bf16 output rows
+  // are padded (ldc >= N rounded up to 8), so the last 16-byte vector of a row stays inside it
+  const bool ce_any = g.ep.mode == E_LSE || g.ep.mode == E_DZ;
+  MB_REQUIRE(g.lda % 8 == 0 && g.ldb % 8 == 0, MB_ERR_CONFIG);
+  MB_REQUIRE(g.N % 8 == 0 || (ce_any && g.ep.ldc >= ((g.N + 7) & ~7)), MB_ERR_CONFIG);
   const bool paired = g.ep.mode == E_GEGLU_FWD;
   if (paired) MB_REQUIRE(g.ep.I % 128 == 0 && g.N == 2 * g.ep.I && !g.a_t && !g.b_t, MB_ERR_CONFIG);
   if (g.ep.mode == E_GEGLU_BWD) MB_REQUIRE(g.N == g.ep.I, MB_ERR_CONFIG);

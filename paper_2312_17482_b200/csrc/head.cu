@@ -99,7 +99,7 @@ struct HeadWs {
     row_loss = (float*)take((size_t)n * 4);
     zlab = (float*)take((size_t)n * 4);
     part = (float2*)take((size_t)n * npart_of(V) * 8);
-    dz = (bf16*)take((size_t)n * V * 2);
+    dz = (bf16*)take((size_t)n * ((V + 7) & ~7) * 2);  // rows padded to 8 elements (any V, F3)
     bytes = o;
   }
 };
@@ -122,7 +122,8 @@ mb_status mb_mlm_loss(const mb_dims* d, const mb_head_params* p, const mb_bf16* 
   if (n_masked < 0 || nnz < 0) return MB_ERR_INVALID_ARG;
   if (n_masked > nnz) return MB_ERR_SHAPE;
   const int H = d->hidden, V = d->vocab;
-  if (V < 1 || H % 8 || V % 8) return MB_ERR_CONFIG;
+  if (V < 1 || H % 8) return MB_ERR_CONFIG;
+  const int Vp = (V + 7) & ~7;  // dz row stride (P:174's 30522 is allowed; 30528 = 64 x 477 is the paper's choice)
   cudaStream_t s = reinterpret_cast<cudaStream_t>(s_);
   HeadWs w(reinterpret_cast<char*>(ws), std::max(n_masked, 1), H, V);
   if (ws_bytes < w.bytes) return MB_ERR_WORKSPACE;
@@ -153,7 +154,7 @@ mb_status mb_mlm_loss(const mb_dims* d, const mb_head_params* p, const mb_bf16* 
   {
     GemmArgs a;
     a.M = n, a.N = V, a.K = H, a.A = w.u, a.lda = H, a.B = B(p->emb), a.ldb = H;
-    a.ep.mode = E_LSE, a.ep.C = w.dz /* unused */, a.ep.ldc = V, a.ep.bias = B(p->b_dec);
+    a.ep.mode = E_LSE, a.ep.C = w.dz /* unused */, a.ep.ldc = Vp, a.ep.bias = B(p->b_dec);
     a.ep.labels = labels, a.ep.part = w.part, a.ep.zlab = w.zlab, a.ep.npart = npart;
     TRY(gemm(a, s));
   }
@@ -165,19 +166,19 @@ mb_status mb_mlm_loss(const mb_dims* d, const mb_head_params* p, const mb_bf16* 
   {
     GemmArgs a;
     a.M = n, a.N = V, a.K = H, a.A = w.u, a.lda = H, a.B = B(p->emb), a.ldb = H;
-    a.ep.mode = E_DZ, a.ep.C = w.dz, a.ep.ldc = V, a.ep.bias = B(p->b_dec);
+    a.ep.mode = E_DZ, a.ep.C = w.dz, a.ep.ldc = Vp, a.ep.bias = B(p->b_dec);
     a.ep.labels = labels, a.ep.lse = lse, a.ep.inv_norm = inv_norm;
     TRY(gemm(a, s));
   }
   {
     GemmArgs a;  // du = dz E   (E [V, H] = [K, N])
-    a.M = n, a.N = H, a.K = V, a.A = w.dz, a.lda = V, a.B = B(p->emb), a.ldb = H, a.b_t = true;
+    a.M = n, a.N = H, a.K = V, a.A = w.dz, a.lda = Vp, a.B = B(p->emb), a.ldb = H, a.b_t = true;
     a.ep.mode = E_BF16, a.ep.C = w.du, a.ep.ldc = H;
     TRY(gemm(a, s));
   }
   {
     GemmArgs a;  // dE += dz^T u
-    a.M = V, a.N = H, a.K = n, a.A = w.dz, a.lda = V, a.a_t = true, a.B = w.u, a.ldb = H, a.b_t = true;
+    a.M = V, a.N = H, a.K = n, a.A = w.dz, a.lda = Vp, a.a_t = true, a.B = w.u, a.ldb = H, a.b_t = true;
     a.ep.mode = E_F32_ACC, a.ep.C = g->emb, a.ep.ldc = H;
     a.ep.dbias = g->b_dec;  // db_dec = column sums of dz, from the A tiles of this GEMM
     TRY(gemm(a, s));

@@ -61,7 +61,8 @@ class Bucket:
 
     def __init__(self, shapes, device):
         self.shapes = shapes
-        self.numel = sum(int(np.prod(s)) for _, s in shapes)
+        # every view starts 16-byte aligned (TMA / vector loads): offsets rounded up to 8 elements
+        self.numel = sum((int(np.prod(s)) + 7) // 8 * 8 for _, s in shapes)
         pad = (self.numel + 63) // 64 * 64
         self.w = torch.zeros(pad, dtype=torch.bfloat16, device=device)
         self.g = torch.zeros(pad, dtype=torch.float32, device=device)
@@ -74,7 +75,7 @@ class Bucket:
             n = int(np.prod(s))
             self.p[name] = self.w[o:o + n].view(*s)
             self.gv[name] = self.g[o:o + n].view(*s)
-            o += n
+            o += (n + 7) // 8 * 8
         self._off = o
 
     def load(self, src: dict):

@@ -160,6 +160,17 @@ def test_model_step_c1_dropout(seed):
     _model_parity(synth.TINY, batch, params, dropout=dict(p=0.1, seed=555 + seed))
 
 
+def test_model_step_vocab_30522():
+    """F3: the unpadded BERT vocabulary (30522, not a multiple of 8 or 64 — P:174) through the
+    decoder/CE GEMMs (ragged last column vector, padded dz rows) and the bucket layout."""
+    import dataclasses
+    dims = dataclasses.replace(synth.BASE, vocab=30522)
+    params = synth.make_model_params(dims, 10, "bert", n_layers=2)
+    batch = synth.make_batch("C5", 5003, B=6)
+    assert batch["input_ids"].max() < 30522
+    _model_parity(dims, batch, params)
+
+
 def test_loss_zero_decoder_is_lnV():
     """Pin P12 on the GPU path: E_tok = 0 and b_dec = 0 give loss = ln V exactly (up to fp32)."""
     params = synth.make_model_params(synth.TINY, 3, "stress")
