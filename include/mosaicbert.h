@@ -279,6 +279,29 @@ MB_API mb_status mb_adamw_step(float* master, float* m, float* v, const float* g
                         float beta1, float beta2, float eps, float weight_decay, float grad_scale, int32_t step,
                         mb_stream_t s);
 
+/* ---------------------------------------------------------------------------------------------
+ * F3 — baselines for the paper's throughput ablations; not on the training path.
+ *
+ * fp32 LayerNorm (the alternative to P:145's bf16 LN, "only 2-bytes are required per-element"):
+ * the same forward / backward as mb_layernorm_forward / _backward with fp32 x, y, dy, dx
+ * [n, H] (gamma, beta bf16 as in the model).  Backward requires H % 256 == 0.  dsum may be NULL.
+ * Errors: NULL pointer / negative size -> MB_ERR_INVALID_ARG; H % 8 (fwd), H % 256 (bwd) or
+ * H > 1024 -> MB_ERR_CONFIG. */
+MB_API mb_status mb_layernorm_forward_f32(const float* x, const mb_bf16* gamma, const mb_bf16* beta, int32_t n,
+                                          int32_t H, float eps, float* y, float* stats, mb_stream_t s);
+MB_API mb_status mb_layernorm_backward_f32(const float* dy, const float* x, const float* stats,
+                                           const mb_bf16* gamma, int32_t n, int32_t H, float* dx, float* dgamma,
+                                           float* dbeta, float* dsum, mb_stream_t s);
+/* Naive (unfused) GLU, elementwise halves (Eq. 2): with U_a = x W1^T + b1 and
+ * U_g = x V^T + b_v computed by two separate mb_gemm calls,
+ *   forward:  Z = GeLU(U_a) * U_g                                  (exact-erf GeLU, R7)
+ *   backward: dU_a = dZ * U_g * GeLU'(U_a),  dU_g = dZ * GeLU(U_a)
+ * All bf16, `count` elements each (count % 8 == 0, contiguous). */
+MB_API mb_status mb_geglu_naive_forward(const mb_bf16* ua, const mb_bf16* ug, int64_t count, mb_bf16* z,
+                                        mb_stream_t s);
+MB_API mb_status mb_geglu_naive_backward(const mb_bf16* dz, const mb_bf16* ua, const mb_bf16* ug, int64_t count,
+                                         mb_bf16* dua, mb_bf16* dug, mb_stream_t s);
+
 #ifdef __cplusplus
 }
 #endif

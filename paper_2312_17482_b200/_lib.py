@@ -85,6 +85,10 @@ _SIGS = {
     "mb_mlm_loss": (C.c_int, [C.POINTER(Dims), C.POINTER(HeadPtrs), P, I32, P, P, I32, F32, P, P, P,
                               C.POINTER(HeadPtrs), P, SZ, P]),
     "mb_adamw_step": (C.c_int, [P, P, P, P, P, I64, F32, F32, F32, F32, F32, F32, I32, P]),
+    "mb_layernorm_forward_f32": (C.c_int, [P, P, P, I32, I32, F32, P, P, P]),
+    "mb_layernorm_backward_f32": (C.c_int, [P, P, P, P, I32, I32, P, P, P, P, P]),
+    "mb_geglu_naive_forward": (C.c_int, [P, P, I64, P, P]),
+    "mb_geglu_naive_backward": (C.c_int, [P, P, P, I64, P, P, P]),
 }
 
 _lib = None
@@ -336,3 +340,29 @@ def mlm_loss(d: Dims, head, y, nnz, masked_rows, labels, n_masked, inv_norm, los
 def adamw_step(master, m, v, g, w_bf16, lr, beta1, beta2, eps, weight_decay, grad_scale, step):
     _ck("mb_adamw_step", lib().mb_adamw_step(_p(master), _p(m), _p(v), _p(g), _p(w_bf16), master.numel(), lr, beta1,
                                              beta2, eps, weight_decay, grad_scale, step, _stream()))
+
+
+# ---- F3 ablation baselines (not on the training path)
+def layernorm_forward_f32(x, gamma, beta, eps, y, stats):
+    n, H = x.shape
+    _ck("mb_layernorm_forward_f32", lib().mb_layernorm_forward_f32(_p(x), _p(gamma), _p(beta), n, H, eps, _p(y),
+                                                                   _p(stats), _stream()))
+    return y, stats
+
+
+def layernorm_backward_f32(dy, x, stats, gamma, dx, dgamma, dbeta, dsum=None):
+    n, H = x.shape
+    _ck("mb_layernorm_backward_f32", lib().mb_layernorm_backward_f32(_p(dy), _p(x), _p(stats), _p(gamma), n, H, _p(dx),
+                                                                     _p(dgamma), _p(dbeta), _p(dsum), _stream()))
+    return dx
+
+
+def geglu_naive_forward(ua, ug, z):
+    _ck("mb_geglu_naive_forward", lib().mb_geglu_naive_forward(_p(ua), _p(ug), ua.numel(), _p(z), _stream()))
+    return z
+
+
+def geglu_naive_backward(dz, ua, ug, dua, dug):
+    _ck("mb_geglu_naive_backward", lib().mb_geglu_naive_backward(_p(dz), _p(ua), _p(ug), ua.numel(), _p(dua), _p(dug),
+                                                                 _stream()))
+    return dua, dug

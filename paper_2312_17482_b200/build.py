@@ -20,7 +20,7 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", 
          "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
 if os.environ.get("MB_WATCHDOG", "1") == "1":
     FLAGS.append("-DMB_WATCHDOG")
-SOURCES = ["runtime.cu", "unpad.cu", "layernorm.cu", "gemm.cu", "attention.cu", "head.cu", "api.cu"]
+SOURCES = ["runtime.cu", "unpad.cu", "layernorm.cu", "gemm.cu", "attention.cu", "head.cu", "api.cu", "ablation.cu"]
 
 
 def _deps():

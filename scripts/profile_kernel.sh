@@ -4,7 +4,7 @@
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 python -m paper_2312_17482_b200.build > /dev/null
-CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
+CMD="python bench.py --config ${CONFIG:-C2} --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
 $CMD > gpurun_out/plain_k.log 2>&1 || { echo "plain run failed"; tail gpurun_out/plain_k.log; exit 1; }
 name=$1; shift
 i=0

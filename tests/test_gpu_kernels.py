@@ -316,3 +316,46 @@ def test_attention_alibi_closed_form():
             assert abs(out[cu[b] + i, 0] - np.dot(w, np.arange(l))) < 1e-2 * max(1, l)
             assert abs(out[cu[b] + i, d] - 1.0) < 1e-2
     assert abs(out[0, 0] - 0.25) < 4e-3 and abs(out[1, 0] - 0.75) < 4e-3
+
+
+# ------------------------------------------------------------------------------------ F3 baselines
+@pytest.mark.parametrize("H", [768, 1024])
+def test_layernorm_f32_baseline(H):
+    """F3 ablation baseline: fp32-activation LayerNorm against the oracle (fp32 storage, so the
+    forward is checked at fp32 tolerance)."""
+    rng = np.random.default_rng(H + 1)
+    n = 517
+    x = rng.standard_normal((n, H)).astype(np.float32) * 3 + 1
+    g = synth.bf16_round(1 + 0.1 * rng.standard_normal(H))
+    b = synth.bf16_round(0.1 * rng.standard_normal(H))
+    dy = rng.standard_normal((n, H)).astype(np.float32)
+    xd = to_dev(x, torch.float32)
+    y = torch.empty(n, H, dtype=torch.float32, device="cuda")
+    st = torch.empty(n, 2, dtype=torch.float32, device="cuda")
+    mb._lib.layernorm_forward_f32(xd, _bf(g), _bf(b), 1e-12, y, st)
+    yo, cache = O.layer_norm(x, g, b, 1e-12)
+    check("lnf32.y", np64(y), yo, max_rel=1e-5)
+    dx = torch.empty(n, H, dtype=torch.float32, device="cuda")
+    dg, dbb, ds = (torch.zeros(H, device="cuda") for _ in range(3))
+    mb._lib.layernorm_backward_f32(to_dev(dy, torch.float32), xd, st, _bf(g), dx, dg, dbb, ds)
+    dxo, dgo, dbo = O.layer_norm_backward(dy, cache, g)
+    check("lnf32.dx", np64(dx), dxo, max_rel=1e-4)
+    check("lnf32.dgamma", np64(dg), dgo, max_rel=1e-4)
+    check("lnf32.dbeta", np64(dbb), dbo, max_rel=1e-4)
+    check("lnf32.dsum", np64(ds), dxo.sum(0), max_rel=1e-3)
+
+
+def test_geglu_naive_baseline():
+    """F3 ablation baseline: the unfused GLU's elementwise kernels against the oracle's GeLU (Eq. 2)."""
+    rng = np.random.default_rng(77)
+    n, I = 300, 3072
+    ua = synth.bf16_round(rng.standard_normal((n, I)) * 2)
+    ug = synth.bf16_round(rng.standard_normal((n, I)))
+    dz = synth.bf16_round(rng.standard_normal((n, I)))
+    z = torch.empty(n, I, dtype=BF, device="cuda")
+    mb._lib.geglu_naive_forward(_bf(ua), _bf(ug), z)
+    check("geglu_naive.z", np64(z), O.gelu(ua) * ug)
+    dua, dug = torch.empty_like(z), torch.empty_like(z)
+    mb._lib.geglu_naive_backward(_bf(dz), _bf(ua), _bf(ug), dua, dug)
+    check("geglu_naive.dua", np64(dua), dz * ug * O.gelu_grad(ua))
+    check("geglu_naive.dug", np64(dug), dz * O.gelu(ua))
