@@ -415,28 +415,44 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             load_bias32_smem(sbias + c * 64, b);
             sm100::tmem_ld_wait();
             if (ep.mode == E_LSE) {
+              // online (max, sum exp) over this chunk; exponentials in the log2 domain, two columns
+              // per instruction on the paired fp32 pipe
               float mx = -INFINITY;
 #pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                v[j] += b[j];
-                if (col + j < N) mx = fmaxf(mx, v[j]);
-                if (col + j == lab) {
-                  zl = v[j];
-                  has_lab = true;
-                }
+              for (int j = 0; j < 32; j += 2) {
+                const float2 z = __fadd2_rn(make_float2(v[j], v[j + 1]), make_float2(b[j], b[j + 1]));
+                v[j] = col + j < N ? z.x : -INFINITY;
+                v[j + 1] = col + j + 1 < N ? z.y : -INFINITY;
+                mx = fmaxf(mx, fmaxf(v[j], v[j + 1]));
+              }
+              if (lab >= col && lab < col + 32) {  // warp-divergent but rare: this row's label column
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                  if (col + j == lab) zl = v[j];
+                has_lab = true;
               }
               const float nm = fmaxf(run_m, mx);
-              float acc_s = 0.f;
+              const float nml = -nm * L2E;
+              float2 acc2 = make_float2(0.f, 0.f);
 #pragma unroll
-              for (int j = 0; j < 32; ++j) acc_s += (col + j < N) ? exp2f((v[j] - nm) * L2E) : 0.f;
-              run_s = run_s * exp2f((run_m - nm) * L2E) + acc_s;
+              for (int j = 0; j < 32; j += 2) {
+                const float2 t = __ffma2_rn(make_float2(v[j], v[j + 1]), make_float2(L2E, L2E), make_float2(nml, nml));
+                acc2 = __fadd2_rn(acc2, make_float2(ex2_approx(t.x), ex2_approx(t.y)));
+              }
+              run_s = run_s * ex2_approx((run_m - nm) * L2E) + (acc2.x + acc2.y);
               run_m = nm;
             } else {
+              const float nl = -lse_r * L2E;
 #pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                float pz = exp2f((v[j] + b[j] - lse_r) * L2E);
-                if (col + j == lab) pz -= 1.f;
-                v[j] = pz * ep.inv_norm;
+              for (int j = 0; j < 32; j += 2) {
+                const float2 z = __fadd2_rn(make_float2(v[j], v[j + 1]), make_float2(b[j], b[j + 1]));
+                const float2 t = __ffma2_rn(z, make_float2(L2E, L2E), make_float2(nl, nl));
+                float2 pz = make_float2(ex2_approx(t.x), ex2_approx(t.y));
+                if (col + j == lab) pz.x -= 1.f;
+                if (col + j + 1 == lab) pz.y -= 1.f;
+                pz = __fmul2_rn(pz, make_float2(ep.inv_norm, ep.inv_norm));
+                v[j] = pz.x;
+                v[j + 1] = pz.y;
               }
               emit_chunk(scrA, v, reinterpret_cast<bf16*>(ep.C), ep.ldc, row0, M, col, N, lane);
             }
