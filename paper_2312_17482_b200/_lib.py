@@ -14,7 +14,8 @@ import numpy as np
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmosaicbert.so")
+# MB_LIBRARY: an alternative build of the same library (A/B timing of two builds on one box)
+LIB_PATH = os.environ.get("MB_LIBRARY") or os.path.join(HERE, "libmosaicbert.so")
 
 P = C.c_void_p
 I32 = C.c_int32

@@ -213,7 +213,6 @@ mb_status mb_encoder_backward(const mb_dims* d, const mb_layer_params* p, const 
     GemmArgs a;
     a.M = T, a.N = I, a.K = H, a.A = dp2, a.lda = H, a.B = B(p->w_2), a.ldb = I, a.b_t = true;
     a.ep.mode = E_GEGLU_BWD, a.ep.C = w.du, a.ep.ldc = 2 * I, a.ep.U = sv.u, a.ep.ldu = 2 * I, a.ep.I = I;
-    a.ep.dbias = g->b_1v;  // db1v = column sums of dU, from the smem tile before its TMA store
     TRY(gemm(a, s));
   }
   {  // dW2 += dF^T Z
@@ -228,10 +227,10 @@ mb_status mb_encoder_backward(const mb_dims* d, const mb_layer_params* p, const 
     a.ep.mode = E_BF16, a.ep.C = w.dy1, a.ep.ldc = H, a.ep.res = w.ds2, a.ep.ldr = H;
     TRY(gemm(a, s));
   }
-  {  // dW1v += dU^T Y1
+  {  // dW1v += dU^T Y1; db1v += dU^T 1 (column sums of dU) by an extra N=16 MMA in the same k-loop
     GemmArgs a;
     a.M = 2 * I, a.N = H, a.K = T, a.A = w.du, a.lda = 2 * I, a.a_t = true, a.B = sv.y1, a.ldb = H, a.b_t = true;
-    a.ep.mode = E_F32_ACC, a.ep.C = g->w_1v, a.ep.ldc = H;
+    a.ep.mode = E_F32_ACC, a.ep.C = g->w_1v, a.ep.ldc = H, a.ep.dbias = g->b_1v;
     TRY(gemm(a, s));
   }
   // LN1 backward: dS1 (and dp1); dgamma1, dbeta1; dbo = column sums of dp1 (same pass)

@@ -600,33 +600,35 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 // ------------------------------------------------------------------------------------------------
 // GeGLU backward (A8 bwd, epilogue E4) as a dedicated kernel with asynchronous epilogue I/O:
 //   dZ = dF W2 (tcgen05, never stored);  dU = dZ * Gd,  Gd = [g GeLU'(a) | GeLU(a)] saved by the
-//   forward;  db_1v += column sums of dU.
-// The tile is 128 rows x 128 columns of dZ.  The producer warp TMA-loads the tile's Gd slice
-// ([128 x 128] of each half, 64 KB) into one of two smem slots while the tile's MMAs run; the 8
-// epilogue warps multiply in place (swizzled layout) and the tile leaves by TMA stores, so the
-// kernel streams Gd in / dU out at HBM rate with no per-thread global accesses.
+//   forward.  (db_1v = column sums of dU comes from the dW1v GEMM's tensor-core row sums.)
+// A CTA pair computes 256 rows x 256 columns of dZ (cta_group::2, each CTA 128 rows x all 256
+// columns in TMEM, double-buffered).  The wide tile halves the MMA operand ingest per FLOP of the
+// former 128-column tile, which matters because this kernel is bounded by the SM's shared-memory
+// bandwidth: operands + Gd in (TMA) + Gd read + dU write + dU out (TMA) all cross it.  The epilogue
+// walks the tile in four 64-column quarters; a dedicated producer warp streams each quarter's Gd
+// slice ([128 x 64] of each half, 32 KB) into a 4-slot ring ahead of use, the 8 epilogue warps
+// multiply in place (swizzled layout) and one thread TMA-stores the quarter, releasing its slot
+// once the store has read it.  Warps: 0 operand TMA, 1 MMA, 2 TMEM alloc, 3 Gd TMA, 4-11 epilogue.
 // ------------------------------------------------------------------------------------------------
-constexpr int GB_BN = 128, GB_STAGES = 4;
-constexpr int GB_STAGE_BYTES = BM * BK * 2 + (GB_BN / 2) * BK * 2;  // own 128 A rows + half of B (24 KB)
-constexpr int GB_SLOT_BYTES = 4 * 128 * 128;                        // 4 boxes of 128 rows x 64 cols bf16 (64 KB)
-constexpr int GB_SMEM = GB_STAGES * GB_STAGE_BYTES + 2 * GB_SLOT_BYTES + 1024 + 256;
+constexpr int GB_BN = 256, GB_STAGES = 3, GB_NSLOT = 4;
+constexpr int GB_STAGE_BYTES = BM * BK * 2 + (GB_BN / 2) * BK * 2;  // own 128 A rows + half of B (32 KB)
+constexpr int GB_SLOT_BYTES = 2 * BM * 64 * 2;                      // a and g boxes [128 x 64] bf16 (32 KB)
+constexpr int GB_SMEM = GB_STAGES * GB_STAGE_BYTES + GB_NSLOT * GB_SLOT_BYTES + 1024 + 256;
 
-// CTA pair (cta_group::2): the pair computes 256 rows x 128 columns of dZ; each CTA stages its 128
-// rows of dF and half (64 columns) of W2's tile, and owns the epilogue (Gd in, dU out) of its rows.
 __global__ void __launch_bounds__(NTHREADS, 1)
     geglu_bwd_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmGd, const __grid_constant__ CUtensorMap tmDU, int M, int I,
-                     Sched sc, float* __restrict__ dbias) {
+                     Sched sc) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* slots = smem + GB_STAGES * GB_STAGE_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(slots + 2 * GB_SLOT_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(slots + GB_NSLOT * GB_SLOT_BYTES);
   uint64_t* empty = full + GB_STAGES;
   uint64_t* tfull = empty + GB_STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* gfull = tempty + 2;   // [2] Gd slice landed (own CTA)
-  uint64_t* gempty = gfull + 2;   // [2] slot free (2 arrivals: one per epilogue group)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gempty + 2);
+  uint64_t* gfull = tempty + 2;        // [GB_NSLOT] Gd quarter landed (own CTA)
+  uint64_t* gempty = gfull + GB_NSLOT;  // [GB_NSLOT] slot's dU store has read it
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gempty + GB_NSLOT);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -644,8 +646,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&tfull[i], 1);
       sm100::mbar_init(&tempty[i], 2 * NUM_EPI_WARPS);
+    }
+    for (int i = 0; i < GB_NSLOT; ++i) {
       sm100::mbar_init(&gfull[i], 1);
-      sm100::mbar_init(&gempty[i], 2);
+      sm100::mbar_init(&gempty[i], 1);
     }
     sm100::fence_barrier_init();
   }
@@ -656,22 +660,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {
+    if (lane == 0) {  // operands: own 128 rows of dF, own half (128 columns) of W2's tile
       int stage = 0;
       uint32_t phase = 0;
-      int it = 0;
-      for (int u = cid; u < sc.total; u += ncl, ++it) {
+      for (int u = cid; u < sc.total; u += ncl) {
         int mb, nb, kb0, kb1;
         sc.decode(u, mb, nb, kb0, kb1);
         const int m_cta = (mb * 2 + rank) * BM;
-        // this CTA's Gd slice first, so it lands while the MMAs run
-        const int sl = it & 1;
-        sm100::mbar_wait(&gempty[sl], ((it >> 1) & 1) ^ 1);
-        uint8_t* slot = slots + sl * GB_SLOT_BYTES;
-        sm100::mbar_arrive_expect_tx(&gfull[sl], GB_SLOT_BYTES);
-#pragma unroll
-        for (int bx = 0; bx < 4; ++bx)
-          sm100::tma_load_2d(slot + bx * 16384, &tmGd, &gfull[sl], (bx >> 1) * I + nb * GB_BN + (bx & 1) * 64, m_cta);
         for (int kb = kb0; kb < kb1; ++kb) {
           sm100::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * GB_STAGE_BYTES;
@@ -679,11 +674,30 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           if (rank == 0) sm100::mbar_arrive_expect_tx(&full[stage], 2 * GB_STAGE_BYTES);
           const int k0 = kb * BK;
           sm100::tma_load_2d_pair(sa, &tmA, &full[stage], k0, m_cta);
-          sm100::tma_load_2d_pair(sb, &tmB, &full[stage], nb * GB_BN + rank * 64, k0);
+#pragma unroll
+          for (int i = 0; i < GB_BN / 2 / 64; ++i)
+            sm100::tma_load_2d_pair(sb + i * 8192, &tmB, &full[stage], nb * GB_BN + rank * (GB_BN / 2) + i * 64, k0);
           if (++stage == GB_STAGES) {
             stage = 0;
             phase ^= 1;
           }
+        }
+      }
+    }
+  } else if (warp == 3) {
+    if (lane == 0) {  // Gd quarters of this CTA's rows, GB_NSLOT ahead
+      int qi = 0;
+      for (int u = cid; u < sc.total; u += ncl) {
+        int mb, nb, kb0, kb1;
+        sc.decode(u, mb, nb, kb0, kb1);
+        const int m_cta = (mb * 2 + rank) * BM;
+        for (int qq = 0; qq < GB_BN / 64; ++qq, ++qi) {
+          const int sl = qi % GB_NSLOT;
+          sm100::mbar_wait(&gempty[sl], ((qi / GB_NSLOT) & 1) ^ 1);
+          uint8_t* slot = slots + sl * GB_SLOT_BYTES;
+          sm100::mbar_arrive_expect_tx(&gfull[sl], GB_SLOT_BYTES);
+          sm100::tma_load_2d(slot, &tmGd, &gfull[sl], nb * GB_BN + qq * 64, m_cta);
+          sm100::tma_load_2d(slot + BM * 128, &tmGd, &gfull[sl], I + nb * GB_BN + qq * 64, m_cta);
         }
       }
     }
@@ -726,101 +740,78 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   } else if (warp >= 4) {
     const int ew = warp - 4;
     const int q = warp & 3;   // TMEM lane quarter = rows [32q, 32q+32) of this CTA's half
-    const int grp = ew >> 2;  // column half: dZ columns [64 grp, 64 grp + 64) of the tile
-    const int gtid = threadIdx.x - 128 - grp * 128;  // 0..127 within the group
+    const int grp = ew >> 2;  // 32-column half of each 64-column quarter
+    const int gtid = threadIdx.x - 128;  // 0..255
     const int r = q * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
-    int it = 0;
-    for (int u = cid; u < sc.total; u += ncl, ++it) {
+    int qi = 0;
+    for (int u = cid; u < sc.total; u += ncl) {
       int mb, nb, kb0, kb1;
       sc.decode(u, mb, nb, kb0, kb1);
-      const int sl = it & 1;
-      const uint32_t slot = sm100::smem_u32(slots + sl * GB_SLOT_BYTES);
-      const uint32_t box_a = slot + grp * 16384, box_g = slot + (2 + grp) * 16384;
-      sm100::mbar_wait(&gfull[sl], (it >> 1) & 1);
+      const int row0 = (mb * 2 + rank) * BM;
       sm100::mbar_wait(&tfull[acc], acc_phase);
       sm100::tc_fence_after();
-      const uint32_t tb = tmem_base + acc * GB_BN + ((uint32_t)(q * 32) << 16) + grp * 64;
-      float v[32], w[32];
-      sm100::tmem_ld32(tb, v);
-      sm100::tmem_ld32(tb + 32, w);
-      sm100::tmem_ld_wait();
-      sm100::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) sm100::mbar_arrive_leader(&tempty[acc]);  // accumulator drained
+      for (int qq = 0; qq < GB_BN / 64; ++qq, ++qi) {
+        const int sl = qi % GB_NSLOT;
+        const uint32_t box_a = sm100::smem_u32(slots + sl * GB_SLOT_BYTES), box_g = box_a + BM * 128;
+        float v[32];
+        sm100::tmem_ld32(tmem_base + acc * GB_BN + ((uint32_t)(q * 32) << 16) + qq * 64 + grp * 32, v);
+        sm100::mbar_wait(&gfull[sl], (qi / GB_NSLOT) & 1);
+        sm100::tmem_ld_wait();
+        if (qq == GB_BN / 64 - 1) {  // accumulator fully read: the MMA may reuse it
+          sm100::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) sm100::mbar_arrive_leader(&tempty[acc]);
+        }
+        // dU = dZ * Gd in place: row r, 16-byte chunks grp*4 .. grp*4+3 of the 64-column box (swizzled)
+        uint4 A[4], G[4];
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int j = grp * 4 + jj;
+          const uint32_t off = r * 128 + ((j ^ (r & 7)) << 4);
+          A[jj] = lds128(box_a + off);
+          G[jj] = lds128(box_g + off);
+        }
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int j = grp * 4 + jj;
+          const uint32_t off = r * 128 + ((j ^ (r & 7)) << 4);
+          float ga[8], gg[8];
+          bf16x8_to_f32(A[jj], ga);
+          bf16x8_to_f32(G[jj], gg);
+#pragma unroll
+          for (int e = 0; e < 8; e += 2) {
+            const float2 dz = make_float2(v[8 * jj + e], v[8 * jj + e + 1]);
+            const float2 pa = __fmul2_rn(dz, make_float2(ga[e], ga[e + 1]));
+            const float2 pg = __fmul2_rn(dz, make_float2(gg[e], gg[e + 1]));
+            ga[e] = pa.x, ga[e + 1] = pa.y, gg[e] = pg.x, gg[e + 1] = pg.y;
+          }
+          sts128(box_a + off, f32_to_bf16x8(ga));
+          sts128(box_g + off, f32_to_bf16x8(gg));
+        }
+        sm100::fence_proxy_async_smem();
+        sm100::named_bar(1, 32 * NUM_EPI_WARPS);
+        if (gtid == 0) {
+          sm100::tma_store_2d(&tmDU, slots + sl * GB_SLOT_BYTES, nb * GB_BN + qq * 64, row0);
+          sm100::tma_store_2d(&tmDU, slots + sl * GB_SLOT_BYTES + BM * 128, I + nb * GB_BN + qq * 64, row0);
+          sm100::bulk_commit();
+          if (qi > 0) {  // the previous quarter's stores have read their slot: hand it back
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            sm100::mbar_arrive(&gempty[(qi - 1) % GB_NSLOT]);
+          }
+        }
+      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
       }
-      // dU = dZ * Gd in place; row r, 16-byte chunks j = 0..7 of the 64-column box (swizzled).
-      // All 16 loads are issued before any store (the volatile shared accesses keep program order).
-      uint4 A[8], G[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const uint32_t off = r * 128 + ((j ^ (r & 7)) << 4);
-        A[j] = lds128(box_a + off);
-        G[j] = lds128(box_g + off);
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const uint32_t off = r * 128 + ((j ^ (r & 7)) << 4);
-        const float* dz = j < 4 ? v + 8 * j : w + 8 * (j - 4);
-        float ga[8], gg[8];
-        bf16x8_to_f32(A[j], ga);
-        bf16x8_to_f32(G[j], gg);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          ga[e] *= dz[e];
-          gg[e] *= dz[e];
-        }
-        sts128(box_a + off, f32_to_bf16x8(ga));
-        sts128(box_g + off, f32_to_bf16x8(gg));
-      }
-      sm100::fence_proxy_async_smem();
-      sm100::named_bar(1 + grp, 128);
-      const int row0 = (mb * 2 + rank) * BM;
-      if (gtid == 0) {
-        sm100::tma_store_2d(&tmDU, slots + sl * GB_SLOT_BYTES + grp * 16384, nb * GB_BN + grp * 64, row0);
-        sm100::tma_store_2d(&tmDU, slots + sl * GB_SLOT_BYTES + (2 + grp) * 16384, I + nb * GB_BN + grp * 64, row0);
-        sm100::bulk_commit();
-      }
-      // db_1v: column sums of the tile's dU.  Thread gtid covers box (gtid >> 6), 8-column chunk
-      // ((gtid >> 3) & 7) and rows [16 (gtid & 7), +16): 16 independent 16-byte loads, then a
-      // 3-step shuffle reduction over the 8 row blocks (consecutive lanes).
-      if (dbias) {
-        const uint32_t box = (gtid >> 6) ? box_g : box_a;
-        const int cj = (gtid >> 3) & 7, rb = gtid & 7;
-        const int rows = min(BM, M - row0);
-        float cs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const int rr = rb * 16 + k;
-          float t[8];
-          bf16x8_to_f32(lds128(box + rr * 128 + ((cj ^ (rr & 7)) << 4)), t);
-          if (rr < rows) {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) cs[e] += t[e];
-          }
-        }
-#pragma unroll
-        for (int o = 1; o < 8; o <<= 1) {
-#pragma unroll
-          for (int e = 0; e < 8; ++e) cs[e] += __shfl_xor_sync(0xffffffffu, cs[e], o);
-        }
-        if (rb == 0 && rows > 0) {
-          float* dst = dbias + ((gtid >> 6) ? I : 0) + nb * GB_BN + grp * 64 + cj * 8;
-#pragma unroll
-          for (int e = 0; e < 8; ++e) atomicAdd(dst + e, cs[e]);
-        }
-      }
-      sm100::named_bar(1 + grp, 128);
-      if (gtid == 0) {
-        sm100::bulk_wait_read0();  // the stores have read the slot
-        sm100::mbar_arrive(&gempty[sl]);
-      }
     }
-    if (gtid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (gtid == 0) {
+      sm100::bulk_wait_read0();
+      if (qi > 0) sm100::mbar_arrive(&gempty[(qi - 1) % GB_NSLOT]);
+      sm100::bulk_wait0();
+    }
   }
   sm100::tc_fence_before();
   sm100::cluster_sync();
@@ -882,13 +873,12 @@ mb_status gemm(const GemmArgs& g, cudaStream_t s) {
   if (paired) MB_REQUIRE(g.ep.I % 128 == 0 && g.N == 2 * g.ep.I && !g.a_t && !g.b_t, MB_ERR_CONFIG);
   if (g.ep.mode == E_GEGLU_BWD) MB_REQUIRE(g.N == g.ep.I, MB_ERR_CONFIG);
 
-  // BN: 256 for wide outputs, 128 when N is small (tiny configs) or for the GeGLU backward (whose
-  // epilogue streams two input tiles); GeGLU fwd is always a 256-wide paired tile (128 columns of
-  // W1 + the matching 128 of V).
+  // BN: 256 for wide outputs, 128 when N is small (tiny configs); GeGLU fwd is always a 256-wide
+  // paired tile (128 columns of W1 + the matching 128 of V), GeGLU bwd a 256-wide tile.
   const bool geglu_bwd = g.ep.mode == E_GEGLU_BWD;
   const bool ce_mode = g.ep.mode == E_LSE || g.ep.mode == E_DZ;  // partial-statistics layout assumes 256
   const bool drop_mode = g.ep.mode == E_BF16 && g.ep.drop.thr;  // F2 variant exists for BN = 256 only
-  const int BN = (paired || ce_mode || drop_mode) ? 256 : ((g.N <= 128 || geglu_bwd) ? 128 : 256);
+  const int BN = (paired || ce_mode || drop_mode || geglu_bwd) ? 256 : (g.N <= 128 ? 128 : 256);
   // CG = 2 (generic kernel): pair tiles of 256 rows; each CTA loads 128 rows of A and BN/2 of B's N.
   constexpr int CGV = 2;
   CUtensorMap ta, tb;
@@ -954,7 +944,7 @@ mb_status gemm(const GemmArgs& g, cudaStream_t s) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, geglu_bwd_kernel, ta, tb, tg, tdu, g.M, g.ep.I, sg, g.ep.dbias) != cudaSuccess)
+    if (cudaLaunchKernelEx(&cfg, geglu_bwd_kernel, ta, tb, tg, tdu, g.M, g.ep.I, sg) != cudaSuccess)
       return MB_ERR_CUDA;
     MB_CHECK_LAUNCH();
     return MB_OK;
