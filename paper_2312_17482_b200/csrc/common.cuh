@@ -168,6 +168,7 @@ __device__ __forceinline__ float gelu_grad_f(float x) {
 }
 
 int num_sms();  // cached per device (host)
+int* device_scratch(size_t n_ints);  // library-owned device scratch (host; nullptr on failure)
 void count_launch();  // host-side counter of kernel launches (mb_launch_count)
 // optional timing probe around one kernel site (mb_probe_set): records caller-provided CUDA events
 enum ProbeSite { PROBE_NONE = 0, PROBE_GEGLU_FWD = 1, PROBE_ATTN_FWD = 2, PROBE_ATTN_BWD = 3, PROBE_LN_FWD = 4 };

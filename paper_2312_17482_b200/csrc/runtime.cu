@@ -25,6 +25,27 @@ int num_sms() {
   return g_sms[dev];
 }
 
+// small library-owned device scratch (per device, grown on demand, never freed): per-block
+// counts of the multi-CTA scans.  Grown outside any stream capture (first calls of a process).
+static std::mutex g_scratch_mu;
+static int* g_scratch[64] = {};
+static size_t g_scratch_n[64] = {};
+int* device_scratch(size_t n_ints) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(g_scratch_mu);
+  if (g_scratch_n[dev] < n_ints) {
+    if (g_scratch[dev]) cudaFree(g_scratch[dev]);
+    g_scratch[dev] = nullptr;
+    g_scratch_n[dev] = 0;
+    const size_t n = std::max<size_t>(n_ints, 1 << 16);
+    if (cudaMalloc(&g_scratch[dev], n * sizeof(int)) != cudaSuccess) return nullptr;
+    g_scratch_n[dev] = n;
+  }
+  return g_scratch[dev];
+}
+
 static std::atomic<unsigned long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 

@@ -138,6 +138,152 @@ __global__ void __launch_bounds__(SCAN_THREADS) mlm_select_kernel(const int* __r
   }
 }
 
+// ---- multi-CTA unpad: (1) per-row counts + prefix check, warp per row; (2) every CTA sums the
+// counts of the rows before its own (a few hundred ints) and writes its rows' indices, while CTA 0
+// also writes cu_seqlens and meta.  Two short launches instead of one latency-bound CTA.
+constexpr int UP_ROWS = 8;  // rows (warps) per CTA
+__global__ void __launch_bounds__(UP_ROWS * 32) unpad_count_kernel(const int* __restrict__ mask, int B, int L,
+                                                                   int* __restrict__ cnt, int* __restrict__ bad) {
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x * UP_ROWS + (threadIdx.x >> 5);
+  if (b >= B) return;
+  const int* row = mask + (size_t)b * L;
+  int c = 0;
+  for (int l0 = 0; l0 < L; l0 += 32) {
+    const int l = l0 + lane;
+    c += __popc(__ballot_sync(0xffffffffu, l < L && row[l] != 0));
+  }
+  int nb = 0;  // right-padded prefix <=> every position l < c is on (R6)
+  for (int l0 = 0; l0 < c; l0 += 32) {
+    const int l = l0 + lane;
+    if (l < c && row[l] == 0) nb = 1;
+  }
+  nb = __any_sync(0xffffffffu, nb);
+  if (lane == 0) {
+    cnt[b] = c;
+    bad[b] = nb;
+  }
+}
+
+__global__ void __launch_bounds__(UP_ROWS * 32) unpad_write_kernel(const int* __restrict__ mask, int B, int L,
+                                                                   const int* __restrict__ cnt,
+                                                                   const int* __restrict__ bad, int* __restrict__ cu,
+                                                                   int* __restrict__ indices, int* __restrict__ meta) {
+  __shared__ int s_part[UP_ROWS * 32 / 32];
+  __shared__ int s_row[UP_ROWS + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int b0 = blockIdx.x * UP_ROWS;
+  // exclusive prefix of this CTA's first row: sum of cnt[0 .. b0)
+  int part = 0;
+  for (int i = threadIdx.x; i < b0; i += blockDim.x) part += cnt[i];
+  part = warp_sum_i(part);
+  if (lane == 0) s_part[warp] = part;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int base = 0;
+    for (int w = 0; w < UP_ROWS; ++w) base += s_part[w];
+    s_row[0] = base;
+    for (int r = 0; r < UP_ROWS; ++r) s_row[r + 1] = s_row[r] + (b0 + r < B ? cnt[b0 + r] : 0);
+  }
+  __syncthreads();
+  const int b = b0 + warp;
+  if (b < B) {
+    const int* row = mask + (size_t)b * L;
+    int out = s_row[warp];
+    for (int l0 = 0; l0 < L; l0 += 32) {
+      const int l = l0 + lane;
+      const bool on = l < L && row[l] != 0;
+      const unsigned bal = __ballot_sync(0xffffffffu, on);
+      if (on) indices[out + __popc(bal & ((1u << lane) - 1u))] = b * L + l;
+      out += __popc(bal);
+    }
+  }
+  if (blockIdx.x == 0) {  // cu_seqlens, nnz, max_seqlen, status
+    __shared__ int s_warp[32];
+    __shared__ int s_max, s_bad;
+    if (threadIdx.x == 0) {
+      s_max = 0;
+      s_bad = 0;
+    }
+    __syncthreads();
+    int carry = 0;
+    for (int base = 0; base < B; base += blockDim.x) {
+      const int i = base + threadIdx.x;
+      const int v = i < B ? cnt[i] : 0;
+      if (i < B) {
+        atomicMax(&s_max, v);
+        if (bad[i]) atomicOr(&s_bad, 1);
+      }
+      // block inclusive scan (blockDim.x = 256 = 8 warps)
+      int x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += t;
+      }
+      if (lane == 31) s_warp[warp] = x;
+      __syncthreads();
+      int off = 0, tot = 0;
+      for (int w = 0; w < UP_ROWS; ++w) {
+        if (w < warp) off += s_warp[w];
+        tot += s_warp[w];
+      }
+      if (i < B) cu[i + 1] = carry + off + x;
+      carry += tot;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      cu[0] = 0;
+      meta[0] = carry;
+      meta[1] = s_max;
+      meta[2] = s_bad ? MB_ERR_MASK_LAYOUT : MB_OK;
+    }
+  }
+}
+
+// ---- multi-CTA MLM selection: (1) per-block counts of labelled tokens, (2) each block's prefix from
+// the counts before it, block scan, ordered writes; the last block writes meta[3]
+constexpr int SEL_THREADS = 1024;
+__global__ void __launch_bounds__(SEL_THREADS) sel_count_kernel(const int* __restrict__ labels,
+                                                                const int* __restrict__ indices, int capacity,
+                                                                const int* __restrict__ meta, int* __restrict__ cnt) {
+  __shared__ int s_warp[32];
+  const int nnz = min(meta[0], capacity);
+  const int t = blockIdx.x * SEL_THREADS + threadIdx.x;
+  const int f = (t < nnz && labels[indices[t]] != -100) ? 1 : 0;
+  int tot;
+  block_scan_incl(f, s_warp, tot);
+  if (threadIdx.x == 0) cnt[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(SEL_THREADS) sel_write_kernel(const int* __restrict__ labels,
+                                                                const int* __restrict__ indices, int capacity,
+                                                                int vocab, const int* __restrict__ cnt,
+                                                                int* __restrict__ rows, int* __restrict__ out_labels,
+                                                                int* __restrict__ meta) {
+  __shared__ int s_warp[32];
+  __shared__ int s_base;
+  const int nnz = min(meta[0], capacity);
+  if (threadIdx.x < 32) {
+    int p = 0;
+    for (int i = threadIdx.x; i < (int)blockIdx.x; i += 32) p += cnt[i];
+    p = warp_sum_i(p);
+    if (threadIdx.x == 0) s_base = p;
+  }
+  const int t = blockIdx.x * SEL_THREADS + threadIdx.x;
+  const int lab = t < nnz ? labels[indices[t]] : -100;
+  const int f = lab != -100;
+  int tot;
+  const int inc = block_scan_incl(f, s_warp, tot);  // includes a __syncthreads after s_base is set
+  const int base = s_base;
+  if (f) {
+    rows[base + inc - 1] = t;
+    out_labels[base + inc - 1] = lab;
+    if (lab < 0 || lab >= vocab) meta[2] = MB_ERR_LABEL_RANGE;
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) meta[3] = base + tot;
+}
+
 // warp per row, 16-byte vectors
 __global__ void gather_rows_kernel(const uint4* __restrict__ src, const int* __restrict__ idx, int n, int vec,
                                    uint4* __restrict__ dst) {
@@ -187,8 +333,17 @@ mb_status mb_unpad_index(const int32_t* mask, int32_t B, int32_t L, int32_t* cu_
                          int32_t* meta, mb_stream_t s) {
   if (!mask || !cu_seqlens || !indices || !meta) return MB_ERR_INVALID_ARG;
   if (B <= 0 || L <= 0 || B > 65536 || L > 65536) return MB_ERR_INVALID_ARG;
-  mb::unpad_index_kernel<<<1, mb::SCAN_THREADS, 0, reinterpret_cast<cudaStream_t>(s)>>>(mask, B, L, cu_seqlens,
-                                                                                        indices, meta);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
+  int* scr = mb::device_scratch(2 * (size_t)B);
+  if (!scr) {  // no scratch: the single-CTA kernel
+    mb::unpad_index_kernel<<<1, mb::SCAN_THREADS, 0, st>>>(mask, B, L, cu_seqlens, indices, meta);
+    MB_CHECK_LAUNCH();
+    return MB_OK;
+  }
+  const int grid = (B + mb::UP_ROWS - 1) / mb::UP_ROWS;
+  mb::unpad_count_kernel<<<grid, mb::UP_ROWS * 32, 0, st>>>(mask, B, L, scr, scr + B);
+  MB_CHECK_LAUNCH();
+  mb::unpad_write_kernel<<<grid, mb::UP_ROWS * 32, 0, st>>>(mask, B, L, scr, scr + B, cu_seqlens, indices, meta);
   MB_CHECK_LAUNCH();
   return MB_OK;
 }
@@ -198,8 +353,19 @@ mb_status mb_mlm_select(const int32_t* labels, const int32_t* indices, int32_t c
   if (!labels || !indices || !masked_rows || !masked_labels || !meta) return MB_ERR_INVALID_ARG;
   if (capacity < 0) return MB_ERR_INVALID_ARG;
   if (vocab < 1) return MB_ERR_CONFIG;
-  mb::mlm_select_kernel<<<1, mb::SCAN_THREADS, 0, reinterpret_cast<cudaStream_t>(s)>>>(
-      labels, indices, capacity, vocab, masked_rows, masked_labels, meta);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
+  const int blocks = (capacity + mb::SEL_THREADS - 1) / mb::SEL_THREADS;
+  int* scr = (blocks >= 1 && blocks <= 4096) ? mb::device_scratch(blocks) : nullptr;
+  if (!scr) {  // empty / huge capacity: the single-CTA kernel
+    mb::mlm_select_kernel<<<1, mb::SCAN_THREADS, 0, st>>>(labels, indices, capacity, vocab, masked_rows,
+                                                         masked_labels, meta);
+    MB_CHECK_LAUNCH();
+    return MB_OK;
+  }
+  mb::sel_count_kernel<<<blocks, mb::SEL_THREADS, 0, st>>>(labels, indices, capacity, meta, scr);
+  MB_CHECK_LAUNCH();
+  mb::sel_write_kernel<<<blocks, mb::SEL_THREADS, 0, st>>>(labels, indices, capacity, vocab, scr, masked_rows,
+                                                          masked_labels, meta);
   MB_CHECK_LAUNCH();
   return MB_OK;
 }

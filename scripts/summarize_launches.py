@@ -17,7 +17,7 @@ for r in csv.DictReader(lines):
     scale = {"ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "nsecond": 1e-3}.get(unit, 1e-3)
     rows.append((r["Kernel Name"], v * scale))
 # last step = from the last unpad_index_kernel
-starts = [i for i, (k, _) in enumerate(rows) if "unpad_index" in k]
+starts = [i for i, (k, _) in enumerate(rows) if "unpad_index" in k or "unpad_count" in k]
 step = rows[starts[-1]:] if starts else rows
 tot = sum(t for _, t in step)
 agg = defaultdict(lambda: [0, 0.0])
