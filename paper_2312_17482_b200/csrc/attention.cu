@@ -89,10 +89,13 @@ __device__ __forceinline__ float fwd_scores(float (&x)[64], int r, int ch, int l
 
 // Forward, software-pipelined: warp 8 (one lane) issues the TMA loads of units i+1, i+2 into two
 // smem buffers and S(i+1) = Q K^T into the second TMEM S buffer while warps 0-7 run the softmax of
-// unit i; then O(i) = P V.  TMEM: S[0] [0,128), S[1] [128,256), O [256,320).
+// unit i; then O(i) = P V into one of two TMEM O buffers.  The softmax warps read O(i) out only
+// after the softmax of unit i+1, so the PV latency hides behind useful work (P is double-buffered
+// in smem for that).  TMEM: S[0] [0,128), S[1] [128,256), O[0] [256,320), O[1] [320,384).
 constexpr int SH_FWD_THREADS = SH_THREADS + 32;
 constexpr int FWD_BUF_BYTES = 3 * TILE_BYTES;  // Q, K, V
-constexpr int SH_FWD_SMEM2 = 2 * FWD_BUF_BYTES + P_BYTES + 1024 + 256;
+constexpr int O_STG_BYTES = 8 * 2048;          // per-warp [32 x 32] bf16 O staging blocks
+constexpr int SH_FWD_SMEM2 = 2 * FWD_BUF_BYTES + 2 * P_BYTES + O_STG_BYTES + 1024 + 256;
 
 __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const __grid_constant__ CUtensorMap tm_qkv,
                                                                           const __grid_constant__ CUtensorMap tm_o,
@@ -104,28 +107,31 @@ __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* bufs = smem;  // 2 x (Q, K, V)
-  uint8_t* sP = smem + 2 * FWD_BUF_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + P_BYTES);
+  uint8_t* sP = smem + 2 * FWD_BUF_BYTES;  // 2 x P
+  uint8_t* sStg = sP + 2 * P_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + O_STG_BYTES);
   uint64_t* load_full = bars;     // [2]
   // one S barrier per TMEM S buffer: S(i+1) is committed before the softmax of unit i ends, so a
-  // single barrier could run two phases ahead of a slow waiter (parity aliasing)
+  // single barrier could run two phases ahead of a slow waiter (parity aliasing); same for O
   uint64_t* s_full = bars + 2;    // [2]
   uint64_t* p_ready = bars + 4;   // 8 compute warps arrive per unit
-  uint64_t* o_full = bars + 5;
+  uint64_t* o_full = bars + 5;    // [2]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 8);
-  __shared__ float rmax[2 * 128], rsum[2 * 128];
+  __shared__ float rmax[2 * 128], rsum[2 * 128];  // half-row max / sum exchange of the two row threads
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int H = heads * d;
   const int total = batch * heads;
   if (tid == 0) {
     sm100::tma_prefetch(&tm_qkv);
+    sm100::tma_prefetch(&tm_o);
     sm100::mbar_init(&load_full[0], 1);
     sm100::mbar_init(&load_full[1], 1);
     sm100::mbar_init(&s_full[0], 1);
     sm100::mbar_init(&s_full[1], 1);
     sm100::mbar_init(p_ready, 8);
-    sm100::mbar_init(o_full, 1);
+    sm100::mbar_init(&o_full[0], 1);
+    sm100::mbar_init(&o_full[1], 1);
     sm100::fence_barrier_init();
   }
   if (warp == 0) sm100::tmem_alloc(tslot, 512);
@@ -159,12 +165,13 @@ __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const
       };
       auto mma_o = [&](int b) {
         const uint32_t v = sm100::smem_u32(bufs + b * FWD_BUF_BYTES) + 2 * TILE_BYTES;
+        const uint32_t p = sPa + b * P_BYTES;
         constexpr uint32_t id_o = sm100::idesc_bf16(128, 64, 0, 1);
 #pragma unroll
         for (int kk = 0; kk < TILE / 16; ++kk)
-          sm100::mma_bf16_ss(tbase + 256, sm100::desc_kmajor_sw128(sPa + (kk >> 2) * (TILE * 128) + (kk & 3) * 32),
+          sm100::mma_bf16_ss(tbase + 256 + 64 * b, sm100::desc_kmajor_sw128(p + (kk >> 2) * (TILE * 128) + (kk & 3) * 32),
                              sm100::desc_mnmajor_sw128(v + kk * 2048, 8192), id_o, kk > 0);
-        sm100::mma_commit(o_full);
+        sm100::mma_commit(&o_full[b]);
       };
       int u_cur = u0;
       int u_nxt = u_cur < total ? next_unit(cu, heads, total, u_cur) : total;
@@ -185,7 +192,7 @@ __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const
         sm100::mbar_wait(p_ready, i & 1);
         sm100::tc_fence_after();
         mma_o(b);
-        sm100::mbar_wait(o_full, i & 1);  // P V(i) done: buffer b and sP are free
+        sm100::mbar_wait(&o_full[b], (i >> 1) & 1);  // P V(i) done: Q/K/V buffer b is free
         const int u_n2 = u_nxt < total ? next_unit(cu, heads, total, u_nxt) : total;
         if (u_n2 < total) issue_loads(u_n2, b);
         u_cur = u_nxt;
@@ -195,61 +202,28 @@ __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const
     __syncwarp();
   } else {
     const int ch = warp >> 2;
-    const int r = (warp & 3) * 32 + lane;
-    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     const float sc2 = rsqrtf((float)d) * LOG2E;
-    for (int i = 0, u = u0; u < total; ++i) {
+    const uint32_t stg = sm100::smem_u32(sStg) + warp * 2048;
+    // the deferred readout of unit i's O (issued as PV(i) into TMEM buffer i & 1)
+    auto readout = [&](int i, int u, float mx, float l) {
       const int b = u / heads, h = u - b * heads;
       const int start = cu[b];
       const int len = cu[b + 1] - start;
-      const float sl2 = slopes[h] * LOG2E;
-      // this warp's P slab doubles as its O staging: the previous unit's TMA store must have read it
-      if (lane == 0) sm100::bulk_wait_read0();
-      __syncwarp();
-      sm100::mbar_wait(&s_full[i & 1], (i >> 1) & 1);
-      sm100::tc_fence_after();
-      const uint32_t tS = tbase + 128 * (i & 1) + lane_off + 64 * ch;
-      float x[64];
-      sm100::tmem_ld32(tS, x);
-      sm100::tmem_ld32(tS + 32, x + 32);
-      sm100::tmem_ld_wait();
-      float mx = len == TILE ? fwd_scores<false>(x, r, ch, len, sc2, sl2) : fwd_scores<true>(x, r, ch, len, sc2, sl2);
-      rmax[ch * 128 + r] = mx;
-      named_bar_sync(1 + (warp & 3), 64);  // the two half-row warps only
-      mx = fmaxf(rmax[r], rmax[128 + r]);
-      // P = 2^(x - max) rounded to bf16 (the operand of O = P V); the row sum is taken over the
-      // rounded values so that the normalisation matches the product exactly
-      float2 sum2 = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int j8 = 0; j8 < 8; ++j8) {
-        uint32_t pk[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 t = __fadd2_rn(make_float2(x[j8 * 8 + 2 * e], x[j8 * 8 + 2 * e + 1]), make_float2(-mx, -mx));
-          pk[e] = pack_bf16x2(ex2_approx(t.x), ex2_approx(t.y));
-          sum2 = __fadd2_rn(sum2, make_float2(__uint_as_float(pk[e] << 16), __uint_as_float(pk[e] & 0xffff0000u)));
-        }
-        st_shared_v4(sPa + p_off(r, 64 * ch + 8 * j8), pk[0], pk[1], pk[2], pk[3]);
-      }
-      const float sum = sum2.x + sum2.y;
-      rsum[ch * 128 + r] = sum;
-      sm100::fence_proxy_async_smem();
-      sm100::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) sm100::mbar_arrive(p_ready);
-      sm100::mbar_wait(o_full, i & 1);
+      sm100::mbar_wait(&o_full[i & 1], (i >> 1) & 1);
       sm100::tc_fence_after();
       float v[32];
-      sm100::tmem_ld32(tbase + 256 + lane_off + 32 * ch, v);
+      sm100::tmem_ld32(tbase + 256 + 64 * (i & 1) + lane_off + 32 * ch, v);
       sm100::tmem_ld_wait();
-      const float l = rsum[r] + rsum[128 + r];
       const float inv = 1.f / l;
 #pragma unroll
       for (int e = 0; e < 32; ++e) v[e] *= inv;
-      const int q4 = warp & 3;
       if (32 * ch < d) {
         if (q4 * 32 + 32 <= len) {  // warp-uniform: all 32 rows valid -> swizzled staging + TMA store
-          const uint32_t stg = sPa + ch * (TILE * 128) + q4 * 4096;
+          if (lane == 0) sm100::bulk_wait_read0();  // this warp's previous store has read its staging
+          __syncwarp();
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             const uint4 pk = f32_to_bf16x8(v + 8 * c);
@@ -269,8 +243,57 @@ __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const
       }
       if (ch == 0 && r < len) lse[(size_t)h * nnz + start + r] = (mx + log2f(l)) * LN2;
       sm100::tc_fence_before();
+    };
+    int u_prev = -1;
+    float mx_prev = 0.f, l_prev = 1.f;
+    int i = 0;
+    for (int u = u0; u < total; ++i) {
+      const int b = u / heads, h = u - b * heads;
+      const int start = cu[b];
+      const int len = cu[b + 1] - start;
+      const float sl2 = slopes[h] * LOG2E;
+      sm100::mbar_wait(&s_full[i & 1], (i >> 1) & 1);
+      sm100::tc_fence_after();
+      const uint32_t tS = tbase + 128 * (i & 1) + lane_off + 64 * ch;
+      float x[64];
+      sm100::tmem_ld32(tS, x);
+      sm100::tmem_ld32(tS + 32, x + 32);
+      sm100::tmem_ld_wait();
+      float mx = len == TILE ? fwd_scores<false>(x, r, ch, len, sc2, sl2) : fwd_scores<true>(x, r, ch, len, sc2, sl2);
+      rmax[ch * 128 + r] = mx;
+      named_bar_sync(1 + (warp & 3), 64);  // the two half-row warps only
+      mx = fmaxf(rmax[r], rmax[128 + r]);
+      // P = 2^(x - max) rounded to bf16 (the operand of O = P V) into P buffer i & 1 (PV(i-2), its
+      // last reader, finished before unit i-1's readout); the row sum is taken over the rounded values
+      const uint32_t pbuf = sPa + (i & 1) * P_BYTES;
+      float2 sum2 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int j8 = 0; j8 < 8; ++j8) {
+        uint32_t pk[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 t = __fadd2_rn(make_float2(x[j8 * 8 + 2 * e], x[j8 * 8 + 2 * e + 1]), make_float2(-mx, -mx));
+          pk[e] = pack_bf16x2(ex2_approx(t.x), ex2_approx(t.y));
+          sum2 = __fadd2_rn(sum2, make_float2(__uint_as_float(pk[e] << 16), __uint_as_float(pk[e] & 0xffff0000u)));
+        }
+        st_shared_v4(pbuf + p_off(r, 64 * ch + 8 * j8), pk[0], pk[1], pk[2], pk[3]);
+      }
+      sm100::fence_proxy_async_smem();
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(p_ready);
+      // row sum of both halves; the two pair barriers per unit separate every rmax / rsum write
+      // from the partner's previous read of it
+      rsum[ch * 128 + r] = sum2.x + sum2.y;
+      if (u_prev >= 0) readout(i - 1, u_prev, mx_prev, l_prev);
+      named_bar_sync(1 + (warp & 3), 64);
+      const float l = rsum[r] + rsum[128 + r];
+      u_prev = u;
+      mx_prev = mx;
+      l_prev = l;
       u = next_unit(cu, heads, total, u);
     }
+    if (u_prev >= 0) readout(i - 1, u_prev, mx_prev, l_prev);
     if (lane == 0) sm100::bulk_wait0();
   }
   sm100::tc_fence_before();
@@ -279,7 +302,6 @@ __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const
   if (warp == 0) sm100::tmem_dealloc(tbase, 512);
 }
 
-// ------------------------------------------------------------------------------------------
 // Long-forward scores in the unscaled domain y = S - (m_h / sc) |q - k| (sc = log2e / sqrt(d) is
 // applied inside the exponent, P = 2^(sc y - sc max y)); distances stepped by -2 per key pair so
 // no per-pair constants are materialised.  Returns max_j y (-inf past the sequence when MASK).
