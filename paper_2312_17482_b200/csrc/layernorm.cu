@@ -288,7 +288,7 @@ __global__ void colsum_kernel(const bf16* __restrict__ x, int n, int C, int rows
 // row, so the three column accumulators cost 24 registers and the SM runs at full occupancy (the
 // one-warp-per-row variant needed ~128 registers).  Row sums combine across the W warps through
 // shared memory (double-buffered by row parity, one named barrier per row).
-constexpr int LNW_GROUPS = 4;  // row groups (rows in flight) per CTA
+constexpr int LNW_GROUPS = 8;  // row groups (rows in flight) per CTA (8: half the CTAs, reductions and atomics of 4)
 
 template <int W, bool EMBED, bool GELU, bool DSUM, bool DROP = false>
 __global__ void __launch_bounds__(LNW_GROUPS * W * 32)
@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(LNW_GROUPS * W * 32)
       *reinterpret_cast<uint4*>(dx + (size_t)row * H + c) = f32_to_bf16x8(o);
     }
   }
-  // column sums: reduce the 4 row groups through smem, one atomic per column per CTA
+  // column sums: reduce the row groups through smem, one atomic per column per CTA
   auto reduce = [&](const float* acc, float* out) {
     __syncthreads();
 #pragma unroll
