@@ -94,8 +94,8 @@ __device__ __forceinline__ float fwd_scores(float (&x)[64], int r, int ch, int l
 // in smem for that).  TMEM: S[0] [0,128), S[1] [128,256), O[0] [256,320), O[1] [320,384).
 constexpr int SH_FWD_THREADS = SH_THREADS + 32;
 constexpr int FWD_BUF_BYTES = 3 * TILE_BYTES;  // Q, K, V
-constexpr int O_STG_BYTES = 8 * 2048;          // per-warp [32 x 32] bf16 O staging blocks
-constexpr int SH_FWD_SMEM2 = 2 * FWD_BUF_BYTES + 2 * P_BYTES + O_STG_BYTES + 1024 + 256;
+constexpr int FWD_NBUF = 3;                    // Q/K/V buffers: loads run two units ahead
+constexpr int SH_FWD_SMEM2 = FWD_NBUF * FWD_BUF_BYTES + 2 * P_BYTES + 1024 + 256;
 
 __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const __grid_constant__ CUtensorMap tm_qkv,
                                                                           const __grid_constant__ CUtensorMap tm_o,
@@ -106,16 +106,15 @@ __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const
                                                                           float* __restrict__ lse, int nnz) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* bufs = smem;  // 2 x (Q, K, V)
-  uint8_t* sP = smem + 2 * FWD_BUF_BYTES;  // 2 x P
-  uint8_t* sStg = sP + 2 * P_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + O_STG_BYTES);
-  uint64_t* load_full = bars;     // [2]
+  uint8_t* bufs = smem;  // FWD_NBUF x (Q, K, V)
+  uint8_t* sP = smem + FWD_NBUF * FWD_BUF_BYTES;  // 2 x P (unit i's P buffer also stages O(i))
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * P_BYTES);
+  uint64_t* load_full = bars;     // [FWD_NBUF]
   // one S barrier per TMEM S buffer: S(i+1) is committed before the softmax of unit i ends, so a
   // single barrier could run two phases ahead of a slow waiter (parity aliasing); same for O
-  uint64_t* s_full = bars + 2;    // [2]
-  uint64_t* p_ready = bars + 4;   // 8 compute warps arrive per unit
-  uint64_t* o_full = bars + 5;    // [2]
+  uint64_t* s_full = bars + 3;    // [2]
+  uint64_t* p_ready = bars + 5;   // 8 compute warps arrive per unit
+  uint64_t* o_full = bars + 6;    // [2]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 8);
   __shared__ float rmax[2 * 128], rsum[2 * 128];  // half-row max / sum exchange of the two row threads
 
@@ -125,8 +124,7 @@ __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const
   if (tid == 0) {
     sm100::tma_prefetch(&tm_qkv);
     sm100::tma_prefetch(&tm_o);
-    sm100::mbar_init(&load_full[0], 1);
-    sm100::mbar_init(&load_full[1], 1);
+    for (int k = 0; k < FWD_NBUF; ++k) sm100::mbar_init(&load_full[k], 1);
     sm100::mbar_init(&s_full[0], 1);
     sm100::mbar_init(&s_full[1], 1);
     sm100::mbar_init(p_ready, 8);
@@ -155,48 +153,51 @@ __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const
         sm100::tma_load_2d(base + TILE_BYTES, &tm_qkv, &load_full[b], H + h * d, st);
         sm100::tma_load_2d(base + 2 * TILE_BYTES, &tm_qkv, &load_full[b], 2 * H + h * d, st);
       };
-      auto mma_s = [&](int b) {
-        const uint32_t q = sm100::smem_u32(bufs + b * FWD_BUF_BYTES), k = q + TILE_BYTES;
+      auto mma_s = [&](int i) {  // S(i): data buffer i % FWD_NBUF, TMEM S buffer i & 1
+        const uint32_t q = sm100::smem_u32(bufs + (i % FWD_NBUF) * FWD_BUF_BYTES), k = q + TILE_BYTES;
         constexpr uint32_t id_s = sm100::idesc_bf16(128, 128, 0, 0);
         for (int kk = 0; kk < d / 16; ++kk)
-          sm100::mma_bf16_ss(tbase + 128 * b, sm100::desc_kmajor_sw128(q + kk * 32),
+          sm100::mma_bf16_ss(tbase + 128 * (i & 1), sm100::desc_kmajor_sw128(q + kk * 32),
                              sm100::desc_kmajor_sw128(k + kk * 32), id_s, kk > 0);
-        sm100::mma_commit(&s_full[b]);
+        sm100::mma_commit(&s_full[i & 1]);
       };
-      auto mma_o = [&](int b) {
-        const uint32_t v = sm100::smem_u32(bufs + b * FWD_BUF_BYTES) + 2 * TILE_BYTES;
-        const uint32_t p = sPa + b * P_BYTES;
+      auto mma_o = [&](int i) {  // O(i) = P(i) V(i): P buffer i & 1, TMEM O buffer i & 1
+        const uint32_t v = sm100::smem_u32(bufs + (i % FWD_NBUF) * FWD_BUF_BYTES) + 2 * TILE_BYTES;
+        const uint32_t p = sPa + (i & 1) * P_BYTES;
         constexpr uint32_t id_o = sm100::idesc_bf16(128, 64, 0, 1);
 #pragma unroll
         for (int kk = 0; kk < TILE / 16; ++kk)
-          sm100::mma_bf16_ss(tbase + 256 + 64 * b, sm100::desc_kmajor_sw128(p + (kk >> 2) * (TILE * 128) + (kk & 3) * 32),
+          sm100::mma_bf16_ss(tbase + 256 + 64 * (i & 1),
+                             sm100::desc_kmajor_sw128(p + (kk >> 2) * (TILE * 128) + (kk & 3) * 32),
                              sm100::desc_mnmajor_sw128(v + kk * 2048, 8192), id_o, kk > 0);
-        sm100::mma_commit(&o_full[b]);
+        sm100::mma_commit(&o_full[i & 1]);
       };
-      int u_cur = u0;
-      int u_nxt = u_cur < total ? next_unit(cu, heads, total, u_cur) : total;
-      if (u_cur < total) issue_loads(u_cur, 0);
-      if (u_nxt < total) issue_loads(u_nxt, 1);
-      if (u_cur < total) {
+      // units i, i+1, i+2 of this CTA: loads run two units ahead of the MMAs
+      int un[3];
+      un[0] = u0;
+      un[1] = un[0] < total ? next_unit(cu, heads, total, un[0]) : total;
+      un[2] = un[1] < total ? next_unit(cu, heads, total, un[1]) : total;
+      for (int k = 0; k < FWD_NBUF; ++k)
+        if (un[k] < total) issue_loads(un[k], k);
+      if (un[0] < total) {
         sm100::mbar_wait(&load_full[0], 0);
         sm100::tc_fence_after();
         mma_s(0);
       }
-      for (int i = 0; u_cur < total; ++i) {
-        const int b = i & 1;
-        if (u_nxt < total) {  // S(i+1) into the other TMEM buffer while the softmax of unit i runs
-          sm100::mbar_wait(&load_full[b ^ 1], ((i + 1) >> 1) & 1);
+      for (int i = 0; un[0] < total; ++i) {
+        const int nb = (i + 1) % FWD_NBUF;
+        if (un[1] < total) {  // S(i+1) into the other TMEM buffer while the softmax of unit i runs
+          sm100::mbar_wait(&load_full[nb], ((i + 1) / FWD_NBUF) & 1);
           sm100::tc_fence_after();
-          mma_s(b ^ 1);
+          mma_s(i + 1);
         }
         sm100::mbar_wait(p_ready, i & 1);
         sm100::tc_fence_after();
-        mma_o(b);
-        sm100::mbar_wait(&o_full[b], (i >> 1) & 1);  // P V(i) done: Q/K/V buffer b is free
-        const int u_n2 = u_nxt < total ? next_unit(cu, heads, total, u_nxt) : total;
-        if (u_n2 < total) issue_loads(u_n2, b);
-        u_cur = u_nxt;
-        u_nxt = u_n2;
+        mma_o(i);
+        sm100::mbar_wait(&o_full[i & 1], (i >> 1) & 1);  // P V(i) done: data buffer i % FWD_NBUF is free
+        const int u3 = un[2] < total ? next_unit(cu, heads, total, un[2]) : total;
+        if (u3 < total) issue_loads(u3, i % FWD_NBUF);
+        un[0] = un[1], un[1] = un[2], un[2] = u3;
       }
     }
     __syncwarp();
@@ -206,9 +207,11 @@ __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const
     const int r = q4 * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     const float sc2 = rsqrtf((float)d) * LOG2E;
-    const uint32_t stg = sm100::smem_u32(sStg) + warp * 2048;
-    // the deferred readout of unit i's O (issued as PV(i) into TMEM buffer i & 1)
+    // the deferred readout of unit i's O (issued as PV(i) into TMEM buffer i & 1); the O block is
+    // staged in this warp's slab of P buffer i & 1, free once PV(i) has completed and until unit
+    // i + 2 writes its P there (which first waits for this store to have read it)
     auto readout = [&](int i, int u, float mx, float l) {
+      const uint32_t stg = sPa + (i & 1) * P_BYTES + ch * (TILE * 128) + q4 * 4096;
       const int b = u / heads, h = u - b * heads;
       const int start = cu[b];
       const int len = cu[b + 1] - start;
@@ -222,8 +225,6 @@ __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const
       for (int e = 0; e < 32; ++e) v[e] *= inv;
       if (32 * ch < d) {
         if (q4 * 32 + 32 <= len) {  // warp-uniform: all 32 rows valid -> swizzled staging + TMA store
-          if (lane == 0) sm100::bulk_wait_read0();  // this warp's previous store has read its staging
-          __syncwarp();
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             const uint4 pk = f32_to_bf16x8(v + 8 * c);
@@ -264,8 +265,11 @@ __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const
       named_bar_sync(1 + (warp & 3), 64);  // the two half-row warps only
       mx = fmaxf(rmax[r], rmax[128 + r]);
       // P = 2^(x - max) rounded to bf16 (the operand of O = P V) into P buffer i & 1 (PV(i-2), its
-      // last reader, finished before unit i-1's readout); the row sum is taken over the rounded values
+      // last MMA reader, finished before unit i-1's readout, whose O staging store must also have
+      // read it); the row sum is taken over the rounded values
       const uint32_t pbuf = sPa + (i & 1) * P_BYTES;
+      if (lane == 0) sm100::bulk_wait_read0();
+      __syncwarp();
       float2 sum2 = make_float2(0.f, 0.f);
 #pragma unroll
       for (int j8 = 0; j8 < 8; ++j8) {
