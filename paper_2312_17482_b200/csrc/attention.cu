@@ -1020,12 +1020,15 @@ __global__ void dq_finish_kernel(const float* __restrict__ dq_acc, int nnz, int 
   }
 }
 
-// single-pass P / dS of one (q tile, k tile) block for this thread's 64 keys: P -> sP, dS -> sdS
+// single-pass P / dS of one (q tile, k tile) block for this thread's 64 keys: P -> sP as computed;
+// dS/sqrt(d) is kept packed in registers and written to sdS after this warp's pending bulk copies
+// (the previous block's dQ reduction staged in the dS slab) have read it
 template <bool MASK>
 __device__ __forceinline__ void bwd_block(uint32_t tS, uint32_t tdP, uint32_t sPa, uint32_t sdSa, int r, int ch,
-                                          int qk_off, int qrows, int keys, float sc2, float sl2, float lse2,
+                                          int lane, int qk_off, int qrows, int keys, float sc2, float sl2, float lse2,
                                           float rsd, float Drs) {
   const float rc = (float)(r + qk_off - 64 * ch);
+  uint32_t pd[32];
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     const int c0 = 64 * ch + 16 * c;
@@ -1033,7 +1036,7 @@ __device__ __forceinline__ void bwd_block(uint32_t tS, uint32_t tdP, uint32_t sP
     sm100::tmem_ld16(tS + c0, v);
     sm100::tmem_ld16(tdP + c0, w);
     sm100::tmem_ld_wait();
-    uint32_t pp[8], pd[8];
+    uint32_t pp[8];
 #pragma unroll
     for (int jj = 0; jj < 16; jj += 2) {
       const float j0 = (float)(16 * c + jj);
@@ -1049,19 +1052,22 @@ __device__ __forceinline__ void bwd_block(uint32_t tS, uint32_t tdP, uint32_t sP
       const float2 ds = __fmul2_rn(pv, __ffma2_rn(make_float2(w[jj], w[jj + 1]), make_float2(rsd, rsd),
                                                   make_float2(Drs, Drs)));
       pp[jj >> 1] = pack_bf16x2(pv.x, pv.y);
-      pd[jj >> 1] = pack_bf16x2(ds.x, ds.y);
+      pd[8 * c + (jj >> 1)] = pack_bf16x2(ds.x, ds.y);
     }
-    const uint32_t o0 = p_off(r, c0), o1 = p_off(r, c0 + 8);
-    st_shared_v4(sPa + o0, pp[0], pp[1], pp[2], pp[3]);
-    st_shared_v4(sPa + o1, pp[4], pp[5], pp[6], pp[7]);
-    st_shared_v4(sdSa + o0, pd[0], pd[1], pd[2], pd[3]);
-    st_shared_v4(sdSa + o1, pd[4], pd[5], pd[6], pd[7]);
+    st_shared_v4(sPa + p_off(r, c0), pp[0], pp[1], pp[2], pp[3]);
+    st_shared_v4(sPa + p_off(r, c0 + 8), pp[4], pp[5], pp[6], pp[7]);
   }
+  if (lane == 0) sm100::bulk_wait_read0();
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    st_shared_v4(sdSa + p_off(r, 64 * ch + 8 * c), pd[4 * c], pd[4 * c + 1], pd[4 * c + 2], pd[4 * c + 3]);
 }
 
 __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
     const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-    const __grid_constant__ CUtensorMap tm_dqkv, LongUnits U, int d, const float* __restrict__ slopes,
+    const __grid_constant__ CUtensorMap tm_dqkv, const __grid_constant__ CUtensorMap tm_dq, LongUnits U, int d,
+    const float* __restrict__ slopes,
     const float* __restrict__ lse, const float* __restrict__ Dg, float* __restrict__ dq_acc,
     bf16* __restrict__ dqkv, float* __restrict__ dbias, int nnz) {
   extern __shared__ uint8_t smem_raw[];
@@ -1211,11 +1217,26 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
     const bool col_ok = 32 * ch < d;
     const uint32_t slabP = sPa + ch * (TILE * 128) + q4 * 4096, slabS = sdSa + ch * (TILE * 128) + q4 * 4096;
     int g = 0;
-    auto dq_out = [&](int start, int q0, int len, int h) {  // fold the finished dQ block into dq_acc
+    // fold the finished dQ block into dq_acc: a warp whose 32 query rows are all inside the sequence
+    // stages its [32 x 32] fp32 block in its dS slab (128B swizzle) and one lane hands it to the TMA
+    // engine as a bulk reduce-add; a ragged quarter adds its valid rows with vector reductions
+    auto dq_out = [&](int start, int q0, int len, int h) {
       float v[32];
       sm100::tmem_ld32(tdQ + lane_off + 32 * ch, v);
       sm100::tmem_ld_wait();
-      if (col_ok && q0 + r < len) {
+      if (!col_ok) return;
+      if (q0 + q4 * 32 + 32 <= len) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          st_shared_v4(slabS + lane * 128 + ((c ^ (lane & 7)) << 4), __float_as_uint(v[4 * c]),
+                       __float_as_uint(v[4 * c + 1]), __float_as_uint(v[4 * c + 2]), __float_as_uint(v[4 * c + 3]));
+        sm100::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          sm100::tma_reduce_add_2d(&tm_dq, slabS, h * d + 32 * ch, start + q0 + q4 * 32);
+          sm100::bulk_commit();
+        }
+      } else if (q0 + r < len) {
         float* dst = dq_acc + (size_t)(start + q0 + r) * H + h * d + 32 * ch;
 #pragma unroll
         for (int e = 0; e < 32; e += 4) red_add_v4(dst + e, v[e], v[e + 1], v[e + 2], v[e + 3]);
@@ -1259,11 +1280,11 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
           dq_out(start, q0 - TILE, len, h);
         }
         if (len - q0 >= TILE && len - kv0 >= TILE)
-          bwd_block<false>(tS + lane_off, tdP + lane_off, sPa, sdSa, r, ch, q0 - kv0, len - q0, len - kv0, sc2, sl2,
-                           lse2, rsd, Drs);
+          bwd_block<false>(tS + lane_off, tdP + lane_off, sPa, sdSa, r, ch, lane, q0 - kv0, len - q0, len - kv0, sc2,
+                           sl2, lse2, rsd, Drs);
         else
-          bwd_block<true>(tS + lane_off, tdP + lane_off, sPa, sdSa, r, ch, q0 - kv0, len - q0, len - kv0, sc2, sl2,
-                          lse2, rsd, Drs);
+          bwd_block<true>(tS + lane_off, tdP + lane_off, sPa, sdSa, r, ch, lane, q0 - kv0, len - q0, len - kv0, sc2,
+                          sl2, lse2, rsd, Drs);
         sm100::fence_proxy_async_smem();
         sm100::tc_fence_before();
         __syncwarp();
@@ -1287,6 +1308,10 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
         if (col_ok) {
           if (full) {
             const uint32_t stg = which == 2 ? slabP : slabS;
+            if (which == 1) {  // the last dQ reduction may still be reading the dS slab
+              if (lane == 0) sm100::bulk_wait_read0();
+              __syncwarp();
+            }
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
               const uint4 pk = f32_to_bf16x8(v + 8 * c);
@@ -1416,13 +1441,14 @@ mb_status attention_bwd(const bf16* qkv, const bf16* O, const bf16* dO, const fl
     attn_bwd_prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(O, dO, nnz, heads, d, Dg);
     MB_CHECK_LAUNCH();
   }
-  CUtensorMap tdq;  // [32 rows x 32 columns] dK / dV blocks, 64-byte swizzle
+  CUtensorMap tdq, tdqa;  // [32 x 32] dK / dV bf16 blocks (64B swizzle); [32 x 32] fp32 dQ blocks (128B swizzle)
   MB_REQUIRE(make_tmap_bf16_2d(&tdq, dqkv, 3 * H, nnz, 3 * H, 32, 32, 64), MB_ERR_CUDA);
+  MB_REQUIRE(make_tmap_f32_2d(&tdqa, dq_acc, H, nnz, H, 32, 32, 128), MB_ERR_CUDA);
   LongUnits U{cu, heads, (max_seqlen + TILE - 1) / TILE, 0};
   U.total = batch * heads * U.QT;
   const int grid = std::max(1, std::min(U.total, num_sms()));
-  attn_bwd_long_kernel<<<grid, LB_THREADS, LB_SMEM, s>>>(tq, tdo, tdq, U, d, slopes, lse, Dg, dq_acc, dqkv, dbias,
-                                                         nnz);
+  attn_bwd_long_kernel<<<grid, LB_THREADS, LB_SMEM, s>>>(tq, tdo, tdq, tdqa, U, d, slopes, lse, Dg, dq_acc, dqkv,
+                                                         dbias, nnz);
   MB_CHECK_LAUNCH();
   {
     const int rows_per = 128;

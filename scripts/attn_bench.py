@@ -1,0 +1,39 @@
+"""Time the attention forward / backward kernels alone at a config's shape (default C4: 128 x 512,
+12 heads, d = 64).  Tuning aid.   usage: attn_bench.py [B] [L]"""
+import sys
+import numpy as np
+import torch
+from paper_2312_17482_b200 import _lib as L
+
+B = int(sys.argv[1]) if len(sys.argv) > 1 else 128
+Lq = int(sys.argv[2]) if len(sys.argv) > 2 else 512
+heads, d = 12, 64
+H = heads * d
+nnz = B * Lq
+cu = torch.arange(0, nnz + 1, Lq, dtype=torch.int32, device="cuda")
+qkv = (torch.randn(nnz, 3 * H, device="cuda") * 0.5).to(torch.bfloat16)
+dO = torch.randn(nnz, H, device="cuda").to(torch.bfloat16)
+O = torch.empty(nnz, H, dtype=torch.bfloat16, device="cuda")
+lse = torch.empty(heads, nnz, device="cuda")
+dqkv = torch.empty(nnz, 3 * H, dtype=torch.bfloat16, device="cuda")
+db = torch.zeros(3 * H, device="cuda")
+sl = torch.from_numpy(L.alibi_slopes(heads)).cuda()
+ws = torch.empty(L.attention_workspace_bytes(nnz, heads, d, Lq), dtype=torch.uint8, device="cuda")
+
+
+def timed(fn, reps=20):
+    for _ in range(3):
+        fn()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps * 1e3
+
+
+tf = timed(lambda: L.attention_forward(qkv, cu, B, nnz, Lq, heads, d, sl, O, lse))
+tb = timed(lambda: L.attention_backward(qkv, O, dO, lse, cu, B, nnz, Lq, heads, d, sl, dqkv, ws=ws, db_qkv=db))
+print(f"B={B} L={Lq}: attention fwd {tf:.1f} us, bwd (incl. prep/finish) {tb:.1f} us")
