@@ -344,7 +344,7 @@ __device__ __forceinline__ float lf_scores(float (&x)[64], int r, int ch, int ke
 constexpr int LF_NS = 3;
 constexpr int LF_THREADS = SH_THREADS + 64;
 constexpr int ONES_BYTES = 16 * TILE * 2;  // [16 x 128] bf16 ones: B operand of the row-sum MMA
-constexpr int LF_SMEM = 2 * TILE_BYTES + LF_NS * 2 * TILE_BYTES + P_BYTES + ONES_BYTES + 1024 + 256;
+constexpr int LF_SMEM = 2 * TILE_BYTES + LF_NS * 2 * TILE_BYTES + 2 * P_BYTES + ONES_BYTES + 1024 + 256;
 
 struct LongUnits {  // unit u = (b * heads + h) * QT + qt, valid iff qt * 128 < len_b
   const int* cu;
@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
   uint8_t* sQ = smem;                              // 2 x Q
   uint8_t* sKV = sQ + 2 * TILE_BYTES;              // LF_NS x (K, V)
   uint8_t* sP = sKV + LF_NS * 2 * TILE_BYTES;
-  uint8_t* sOnes = sP + P_BYTES;
+  uint8_t* sOnes = sP + 2 * P_BYTES;  // sP: two P buffers (tile g uses g & 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sOnes + ONES_BYTES);
   uint64_t* q_full = bars;                         // [2]
   uint64_t* q_empty = bars + 2;                    // [2]
@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
         const uint32_t v = sKVa + (g % LF_NS) * 2 * TILE_BYTES + TILE_BYTES;
 #pragma unroll
         for (int kk = 0; kk < TILE / 16; ++kk) {
-          const uint64_t pa = sm100::desc_kmajor_sw128(sPa + (kk >> 2) * (TILE * 128) + (kk & 3) * 32);
+          const uint64_t pa = sm100::desc_kmajor_sw128(sPa + (g & 1) * P_BYTES + (kk >> 2) * (TILE * 128) + (kk & 3) * 32);
           sm100::mma_bf16_ss(tbase + 256 + 64 * (g & 1), pa, sm100::desc_mnmajor_sw128(v + kk * 2048, 8192), id_o,
                              kk > 0);
           sm100::mma_bf16_ss(tbase + 384 + 16 * (g & 1), pa,
@@ -517,11 +517,29 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
       const int start = U.cu[b], len = U.cu[b + 1] - start, q0 = qt * TILE;
       const int nkv = (len + TILE - 1) / TILE;
       const float slr = slopes[h] * sqrtf((float)d);  // m_h / (1/sqrt(d)): bias in the unscaled domain
-      float m = -INFINITY, l = 0.f, alpha_prev = 0.f;  // m: running max of y; l: running sum (both rows' halves)
+      // m: running max of y; l: running row sum; o: this thread's 32 output columns.  PV / row-sum
+      // tile k is folded two tiles late (o = alpha_k o + PV_k, l = alpha_k l + sum_k) so that its MMA
+      // latency hides behind the next tile; P is double-buffered in smem and PV in TMEM for that.
+      float m = -INFINITY, l = 0.f, a_m1 = 0.f, a_m2 = 0.f;  // alpha of tiles j-1, j-2
       float o[32];
 #pragma unroll
       for (int e = 0; e < 32; ++e) o[e] = 0.f;
-      // this warp's P slab doubles as O staging: the previous unit's TMA store must have read it
+      auto fold = [&](int gk, float a) {
+        sm100::mbar_wait(&pv_full[gk & 1], (gk >> 1) & 1);
+        sm100::tc_fence_after();
+        float pv[32];
+        sm100::tmem_ld32(tbase + 256 + 64 * (gk & 1) + lane_off + 32 * ch, pv);
+        const float ls = sm100::tmem_ld1(tbase + 384 + 16 * (gk & 1) + lane_off);
+        sm100::tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          const float2 t = __ffma2_rn(make_float2(o[e], o[e + 1]), make_float2(a, a), make_float2(pv[e], pv[e + 1]));
+          o[e] = t.x;
+          o[e + 1] = t.y;
+        }
+        l = fmaf(l, a, ls);
+      };
+      // this warp's P slabs double as O staging: the previous unit's TMA store must have read them
       if (lane == 0) sm100::bulk_wait_read0();
       __syncwarp();
       for (int j = 0; j < nkv; ++j, ++g) {
@@ -539,24 +557,10 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
         named_bar_sync(1 + (warp & 3), 64);  // the two half-row warps only
         const float m_new = fmaxf(m, fmaxf(rmax[g & 1][r], rmax[g & 1][TILE + r]));
         const float alpha = ex2_approx((m - m_new) * sc2);
-        if (j > 0) {  // fold PV_{g-1} and its row sum: o = alpha_{g-1} o + PV_{g-1}; frees sP
-          sm100::mbar_wait(&pv_full[(g - 1) & 1], ((g - 1) >> 1) & 1);
-          sm100::tc_fence_after();
-          float pv[32];
-          sm100::tmem_ld32(tbase + 256 + 64 * ((g - 1) & 1) + lane_off + 32 * ch, pv);
-          const float ls = sm100::tmem_ld1(tbase + 384 + 16 * ((g - 1) & 1) + lane_off);
-          sm100::tmem_ld_wait();
-#pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            const float2 t = __ffma2_rn(make_float2(o[e], o[e + 1]), make_float2(alpha_prev, alpha_prev),
-                                        make_float2(pv[e], pv[e + 1]));
-            o[e] = t.x;
-            o[e + 1] = t.y;
-          }
-          l = fmaf(l, alpha_prev, ls);
-        }
+        if (j >= 2) fold(g - 2, a_m2);  // PV(g-2) done: its P buffer (= this tile's) is free
         // P_g = 2^(sc (y - m_new)) rounded to bf16 (the PV operand; its row sums come from the MMA)
         const float nm = -m_new * sc2;
+        const uint32_t pbuf = sPa + (g & 1) * P_BYTES;
 #pragma unroll
         for (int j8 = 0; j8 < 8; ++j8) {
           uint32_t pk[4];
@@ -566,27 +570,19 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
                                         make_float2(nm, nm));
             pk[e] = pack_bf16x2(ex2_approx(t.x), ex2_approx(t.y));
           }
-          st_shared_v4(sPa + p_off(r, 64 * ch + 8 * j8), pk[0], pk[1], pk[2], pk[3]);
+          st_shared_v4(pbuf + p_off(r, 64 * ch + 8 * j8), pk[0], pk[1], pk[2], pk[3]);
         }
         m = m_new;
-        alpha_prev = alpha;
+        a_m2 = a_m1;
+        a_m1 = alpha;
         sm100::fence_proxy_async_smem();
         sm100::tc_fence_before();
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive(p_ready);
       }
-      // drain the unit's last PV, combine the two half-row sums, normalise, store O and LSE
-      sm100::mbar_wait(&pv_full[(g - 1) & 1], ((g - 1) >> 1) & 1);
-      sm100::tc_fence_after();
-      {
-        float pv[32];
-        sm100::tmem_ld32(tbase + 256 + 64 * ((g - 1) & 1) + lane_off + 32 * ch, pv);
-        const float ls = sm100::tmem_ld1(tbase + 384 + 16 * ((g - 1) & 1) + lane_off);
-        sm100::tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 32; ++e) o[e] = fmaf(o[e], alpha_prev, pv[e]);
-        l = fmaf(l, alpha_prev, ls);
-      }
+      // drain the unit's last two PVs (tiles nkv-2, nkv-1), normalise, store O and LSE
+      if (nkv >= 2) fold(g - 2, a_m2);
+      fold(g - 1, a_m1);
       const float lt = l;  // full-row sum (the MMA summed all 128 keys of each tile)
       const float inv = 1.f / lt;
 #pragma unroll
@@ -594,7 +590,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
       const int qrow = q0 + r;
       if (32 * ch < d) {
         if (q0 + q4 * 32 + 32 <= len) {  // warp-uniform: all 32 rows valid -> swizzled staging + TMA store
-          const uint32_t stg = sPa + ch * (TILE * 128) + q4 * 4096;
+          const uint32_t stg = sPa + ((g - 1) & 1) * P_BYTES + ch * (TILE * 128) + q4 * 4096;
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             const uint4 pk = f32_to_bf16x8(o + 8 * c);
