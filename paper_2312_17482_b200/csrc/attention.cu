@@ -331,15 +331,16 @@ __device__ __forceinline__ float lf_scores(float (&x)[64], int r, int ch, int ke
 }
 
 // Long-sequence forward (128 < l <= 2048, SURVEY A5 at l = 512 and F4): one work unit = (128-row
-// query tile, head, sequence), iterating over the sequence's key tiles with the online softmax.
-// Warp 9 (one lane) streams Q (double-buffered per unit) and K/V tiles (LF_NS-stage ring) by TMA;
-// warp 8 (one lane) issues S_{g+1} = Q K_{g+1}^T into the other half of a double-buffered TMEM S
-// while the softmax warps work on S_g, then PV_g = P_g V_g into a double-buffered TMEM PV;
-// warps 0-7 (two threads per query row, 64 keys each) compute the exp2-domain online softmax and
-// fold PV_{g-1} into their fp32 registers (o = alpha_{g-1} o + PV_{g-1}) before writing P_g.  The
-// softmax denominator comes from the tensor core too: an N=16 MMA of P_g against an all-ones tile
-// gives the row sums of the bf16 P the PV product used, folded like PV (l = alpha l + sum).
-// TMEM: S [0,256) (2 x 128), PV [256,384) (2 x 64), row sums [384,416) (2 x 16).
+// query tile, head, sequence), iterating over the sequence's key tiles with the online softmax,
+// starting at the diagonal tile (where ALiBi puts the row maxima).  Warp 9 (one lane) streams Q
+// (double-buffered per unit) and K/V tiles (LF_NS-stage ring) by TMA; warp 8 (one lane) issues
+// S_{g+1} = Q K_{g+1}^T into the other half of a double-buffered TMEM S while the softmax warps work
+// on S_g, then O += P_g V_g and l += P_g 1 (an N=16 MMA against an all-ones tile) straight into the
+// unit's TMEM accumulators (double-buffered per unit).  Warps 0-7 (two threads per query row, 64
+// keys each) keep the running max the P tiles were computed against and rescale the TMEM
+// accumulators only when a row's max grows by more than 2^8 (rare once the diagonal tile has set
+// it); a unit's O is normalised and stored during the next unit's first tile, so no MMA latency is
+// exposed at unit boundaries.  TMEM: S [0,256) (2 x 128), O [256,384) (2 x 64), l [384,416) (2 x 16).
 // ------------------------------------------------------------------------------------------
 constexpr int LF_NS = 3;
 constexpr int LF_THREADS = SH_THREADS + 64;
@@ -389,8 +390,9 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
   uint64_t* kv_full = bars + 4;                    // [LF_NS]
   uint64_t* kv_empty = bars + 4 + LF_NS;           // [LF_NS]
   uint64_t* s_full = bars + 4 + 2 * LF_NS;         // [2]
-  uint64_t* pv_full = bars + 6 + 2 * LF_NS;        // [2]
+  uint64_t* pv_full = bars + 6 + 2 * LF_NS;        // [2] per tile: PV_g (and l_g) accumulated
   uint64_t* p_ready = bars + 8 + 2 * LF_NS;        // 8 softmax warps
+  uint64_t* o_done = bars + 9 + 2 * LF_NS;         // [2] per unit: its last PV accumulated
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 16);
   __shared__ float rmax[2][2 * TILE];
 
@@ -404,6 +406,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
       sm100::mbar_init(&q_empty[i], 1);
       sm100::mbar_init(&s_full[i], 1);
       sm100::mbar_init(&pv_full[i], 1);
+      sm100::mbar_init(&o_done[i], 1);
     }
     for (int i = 0; i < LF_NS; ++i) {
       sm100::mbar_init(&kv_full[i], 1);
@@ -440,7 +443,8 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
         sm100::mbar_wait(&q_empty[qb], ((uc >> 1) & 1) ^ 1);
         sm100::mbar_arrive_expect_tx(&q_full[qb], TILE_BYTES);
         sm100::tma_load_2d(sQ + qb * TILE_BYTES, &tm_qkv, &q_full[qb], h * d, st + qt * TILE);
-        for (int j = 0; j < nkv; ++j, ++g) {
+        for (int jj = 0; jj < nkv; ++jj, ++g) {
+          const int j = (qt + jj) % nkv;  // diagonal tile first
           const int sg = g % LF_NS;
           sm100::mbar_wait(&kv_empty[sg], ((g / LF_NS) & 1) ^ 1);
           uint8_t* kv = sKV + sg * 2 * TILE_BYTES;
@@ -491,15 +495,17 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
         sm100::tc_fence_after();
         const uint32_t v = sKVa + (g % LF_NS) * 2 * TILE_BYTES + TILE_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < TILE / 16; ++kk) {
+        for (int kk = 0; kk < TILE / 16; ++kk) {  // O += P V, l += P 1 into the unit's accumulators
           const uint64_t pa = sm100::desc_kmajor_sw128(sPa + (g & 1) * P_BYTES + (kk >> 2) * (TILE * 128) + (kk & 3) * 32);
-          sm100::mma_bf16_ss(tbase + 256 + 64 * (g & 1), pa, sm100::desc_mnmajor_sw128(v + kk * 2048, 8192), id_o,
-                             kk > 0);
-          sm100::mma_bf16_ss(tbase + 384 + 16 * (g & 1), pa,
-                             sm100::desc_kmajor_sw128(sOa + (kk >> 2) * 2048 + (kk & 3) * 32), id_l, kk > 0);
+          const uint32_t acc = (j > 0 || kk > 0) ? 1u : 0u;
+          sm100::mma_bf16_ss(tbase + 256 + 64 * (uc & 1), pa, sm100::desc_mnmajor_sw128(v + kk * 2048, 8192), id_o,
+                             acc);
+          sm100::mma_bf16_ss(tbase + 384 + 16 * (uc & 1), pa,
+                             sm100::desc_kmajor_sw128(sOa + (kk >> 2) * 2048 + (kk & 3) * 32), id_l, acc);
         }
         sm100::mma_commit(&pv_full[g & 1]);
         sm100::mma_commit(&kv_empty[g % LF_NS]);
+        if (j + 1 == nkv) sm100::mma_commit(&o_done[uc & 1]);
         u = u2, uc = uc2, j = j2, nkv = nkv2;
       }
     }
@@ -510,87 +516,27 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
     const int r = q4 * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     const float sc2 = rsqrtf((float)d) * LOG2E;
-    int g = 0;
-    for (int u = U.first(); u < U.total; u = U.next(u)) {
+    const float tau = 8.f / sc2;  // rescale only when a row max grows by more than 2^8 in P
+    // the deferred epilogue of a finished unit: O / l from its TMEM accumulators, stored as bf16 O
+    // (staged in the retired P buffer `pb`) and the LSE
+    auto epilogue = [&](int uu, int ucc, float m_used, uint32_t pb) {
       int b, h, qt;
-      U.decode(u, b, h, qt);
+      U.decode(uu, b, h, qt);
       const int start = U.cu[b], len = U.cu[b + 1] - start, q0 = qt * TILE;
-      const int nkv = (len + TILE - 1) / TILE;
-      const float slr = slopes[h] * sqrtf((float)d);  // m_h / (1/sqrt(d)): bias in the unscaled domain
-      // m: running max of y; l: running row sum; o: this thread's 32 output columns.  PV / row-sum
-      // tile k is folded two tiles late (o = alpha_k o + PV_k, l = alpha_k l + sum_k) so that its MMA
-      // latency hides behind the next tile; P is double-buffered in smem and PV in TMEM for that.
-      float m = -INFINITY, l = 0.f, a_m1 = 0.f, a_m2 = 0.f;  // alpha of tiles j-1, j-2
+      sm100::mbar_wait(&o_done[ucc & 1], (ucc >> 1) & 1);
+      sm100::tc_fence_after();
       float o[32];
-#pragma unroll
-      for (int e = 0; e < 32; ++e) o[e] = 0.f;
-      auto fold = [&](int gk, float a) {
-        sm100::mbar_wait(&pv_full[gk & 1], (gk >> 1) & 1);
-        sm100::tc_fence_after();
-        float pv[32];
-        sm100::tmem_ld32(tbase + 256 + 64 * (gk & 1) + lane_off + 32 * ch, pv);
-        const float ls = sm100::tmem_ld1(tbase + 384 + 16 * (gk & 1) + lane_off);
-        sm100::tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          const float2 t = __ffma2_rn(make_float2(o[e], o[e + 1]), make_float2(a, a), make_float2(pv[e], pv[e + 1]));
-          o[e] = t.x;
-          o[e + 1] = t.y;
-        }
-        l = fmaf(l, a, ls);
-      };
-      // this warp's P slabs double as O staging: the previous unit's TMA store must have read them
-      if (lane == 0) sm100::bulk_wait_read0();
-      __syncwarp();
-      for (int j = 0; j < nkv; ++j, ++g) {
-        const int kv0 = j * TILE;
-        sm100::mbar_wait(&s_full[g & 1], (g >> 1) & 1);
-        sm100::tc_fence_after();
-        float x[64];
-        const uint32_t tS = tbase + 128 * (g & 1) + lane_off + 64 * ch;
-        sm100::tmem_ld32(tS, x);
-        sm100::tmem_ld32(tS + 32, x + 32);
-        sm100::tmem_ld_wait();
-        const float mx = len - kv0 >= TILE ? lf_scores<false>(x, r, ch, len - kv0, slr, q0 - kv0)
-                                           : lf_scores<true>(x, r, ch, len - kv0, slr, q0 - kv0);
-        rmax[g & 1][ch * TILE + r] = mx;
-        named_bar_sync(1 + (warp & 3), 64);  // the two half-row warps only
-        const float m_new = fmaxf(m, fmaxf(rmax[g & 1][r], rmax[g & 1][TILE + r]));
-        const float alpha = ex2_approx((m - m_new) * sc2);
-        if (j >= 2) fold(g - 2, a_m2);  // PV(g-2) done: its P buffer (= this tile's) is free
-        // P_g = 2^(sc (y - m_new)) rounded to bf16 (the PV operand; its row sums come from the MMA)
-        const float nm = -m_new * sc2;
-        const uint32_t pbuf = sPa + (g & 1) * P_BYTES;
-#pragma unroll
-        for (int j8 = 0; j8 < 8; ++j8) {
-          uint32_t pk[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 t = __ffma2_rn(make_float2(x[j8 * 8 + 2 * e], x[j8 * 8 + 2 * e + 1]), make_float2(sc2, sc2),
-                                        make_float2(nm, nm));
-            pk[e] = pack_bf16x2(ex2_approx(t.x), ex2_approx(t.y));
-          }
-          st_shared_v4(pbuf + p_off(r, 64 * ch + 8 * j8), pk[0], pk[1], pk[2], pk[3]);
-        }
-        m = m_new;
-        a_m2 = a_m1;
-        a_m1 = alpha;
-        sm100::fence_proxy_async_smem();
-        sm100::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) sm100::mbar_arrive(p_ready);
-      }
-      // drain the unit's last two PVs (tiles nkv-2, nkv-1), normalise, store O and LSE
-      if (nkv >= 2) fold(g - 2, a_m2);
-      fold(g - 1, a_m1);
-      const float lt = l;  // full-row sum (the MMA summed all 128 keys of each tile)
+      sm100::tmem_ld32(tbase + 256 + 64 * (ucc & 1) + lane_off + 32 * ch, o);
+      const float lt = sm100::tmem_ld1(tbase + 384 + 16 * (ucc & 1) + lane_off);
+      sm100::tmem_ld_wait();
+      sm100::tc_fence_before();
       const float inv = 1.f / lt;
 #pragma unroll
       for (int e = 0; e < 32; ++e) o[e] *= inv;
       const int qrow = q0 + r;
       if (32 * ch < d) {
         if (q0 + q4 * 32 + 32 <= len) {  // warp-uniform: all 32 rows valid -> swizzled staging + TMA store
-          const uint32_t stg = sPa + ((g - 1) & 1) * P_BYTES + ch * (TILE * 128) + q4 * 4096;
+          const uint32_t stg = pb + ch * (TILE * 128) + q4 * 4096;
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             const uint4 pk = f32_to_bf16x8(o + 8 * c);
@@ -608,9 +554,86 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
           for (int c = 0; c < 32; c += 8) *reinterpret_cast<uint4*>(dst + c) = f32_to_bf16x8(o + c);
         }
       }
-      if (ch == 0 && qrow < len) lse[(size_t)h * nnz + start + qrow] = (m * sc2 + log2f(lt)) * LN2;
-      sm100::tc_fence_before();
+      if (ch == 0 && qrow < len) lse[(size_t)h * nnz + start + qrow] = (m_used * sc2 + log2f(lt)) * LN2;
+    };
+    int g = 0, uc = 0;
+    int pend_u = -1, pend_uc = 0;  // unit whose epilogue is pending
+    float pend_m = 0.f;
+    for (int u = U.first(); u < U.total; u = U.next(u), ++uc) {
+      int b, h, qt;
+      U.decode(u, b, h, qt);
+      const int start = U.cu[b], len = U.cu[b + 1] - start, q0 = qt * TILE;
+      (void)start;
+      const int nkv = (len + TILE - 1) / TILE;
+      const float slr = slopes[h] * sqrtf((float)d);  // m_h / (1/sqrt(d)): bias in the unscaled domain
+      float m = -INFINITY;  // the max the unit's P tiles are computed against (unscaled domain)
+      for (int jj = 0; jj < nkv; ++jj, ++g) {
+        const int kv0 = ((qt + jj) % nkv) * TILE;
+        sm100::mbar_wait(&s_full[g & 1], (g >> 1) & 1);
+        sm100::tc_fence_after();
+        float x[64];
+        const uint32_t tS = tbase + 128 * (g & 1) + lane_off + 64 * ch;
+        sm100::tmem_ld32(tS, x);
+        sm100::tmem_ld32(tS + 32, x + 32);
+        sm100::tmem_ld_wait();
+        const float mx = len - kv0 >= TILE ? lf_scores<false>(x, r, ch, len - kv0, slr, q0 - kv0)
+                                           : lf_scores<true>(x, r, ch, len - kv0, slr, q0 - kv0);
+        rmax[g & 1][ch * TILE + r] = mx;
+        named_bar_sync(1 + (warp & 3), 64);  // the two half-row warps only
+        const float m_row = fmaxf(rmax[g & 1][r], rmax[g & 1][TILE + r]);
+        if (jj == 0) {
+          m = m_row;
+        } else if (__any_sync(0xffffffffu, m_row > m + tau)) {
+          // some row of this warp outgrew its max: rescale its O / l accumulators (after PV_{g-1})
+          const float m_new = fmaxf(m, m_row);
+          const float alpha = ex2_approx((m - m_new) * sc2);
+          sm100::mbar_wait(&pv_full[(g - 1) & 1], ((g - 1) >> 1) & 1);
+          sm100::tc_fence_after();
+          float o[32];
+          const uint32_t to = tbase + 256 + 64 * (uc & 1) + lane_off + 32 * ch;
+          sm100::tmem_ld32(to, o);
+          float lv[1];
+          lv[0] = sm100::tmem_ld1(tbase + 384 + 16 * (uc & 1) + lane_off);
+          sm100::tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] *= alpha;
+          sm100::tmem_st32(to, o);
+          if (ch == 0) sm100::tmem_st1(tbase + 384 + 16 * (uc & 1) + lane_off, lv[0] * alpha);  // warp-uniform
+          sm100::tmem_st_wait();
+          m = m_new;
+        }
+        // P_g = 2^(sc (y - m)) rounded to bf16 into P buffer g & 1 (PV_{g-2}, its last reader, done;
+        // any O staging store from it has been read)
+        if (g >= 2) sm100::mbar_wait(&pv_full[g & 1], ((g - 2) >> 1) & 1);
+        if (lane == 0) sm100::bulk_wait_read0();
+        __syncwarp();
+        const float nm = -m * sc2;
+        const uint32_t pbuf = sPa + (g & 1) * P_BYTES;
+#pragma unroll
+        for (int j8 = 0; j8 < 8; ++j8) {
+          uint32_t pk[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 t = __ffma2_rn(make_float2(x[j8 * 8 + 2 * e], x[j8 * 8 + 2 * e + 1]), make_float2(sc2, sc2),
+                                        make_float2(nm, nm));
+            pk[e] = pack_bf16x2(ex2_approx(t.x), ex2_approx(t.y));
+          }
+          st_shared_v4(pbuf + p_off(r, 64 * ch + 8 * j8), pk[0], pk[1], pk[2], pk[3]);
+        }
+        sm100::fence_proxy_async_smem();
+        sm100::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(p_ready);
+        if (jj == 0 && pend_u >= 0) {  // the previous unit's epilogue, its O staged in its last P buffer
+          epilogue(pend_u, pend_uc, pend_m, sPa + ((g - 1) & 1) * P_BYTES);
+          pend_u = -1;
+        }
+      }
+      pend_u = u;
+      pend_uc = uc;
+      pend_m = m;
     }
+    if (pend_u >= 0) epilogue(pend_u, pend_uc, pend_m, sPa + ((g - 1) & 1) * P_BYTES);
     if (lane == 0) sm100::bulk_wait0();
   }
   sm100::tc_fence_before();
