@@ -37,6 +37,8 @@ MASK_CASES = {
     "zero_rows": lambda: synth.mask_from_lengths(np.array([0, 5, 0, 3, 0]), 7),
     "L1": lambda: synth.mask_from_lengths(np.array([1, 0, 1, 1]), 1),
     "big_ragged": lambda: synth.mask_from_lengths(np.random.default_rng(0).integers(0, 301, 3000), 300),
+    "all_zero": lambda: np.zeros((4, 9), dtype=np.int32),
+    "many_rows": lambda: synth.mask_from_lengths(np.random.default_rng(1).integers(0, 65, 20000), 64),
 }
 
 

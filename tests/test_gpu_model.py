@@ -171,6 +171,28 @@ def test_model_step_vocab_30522():
     _model_parity(dims, batch, params)
 
 
+def test_model_step_degenerate_batches():
+    """Edge cases of one micro-step: no labelled token (loss 0, every gradient exactly 0 — the
+    head writes a zero upstream gradient) and an all-padding batch (nothing to do)."""
+    params = synth.make_model_params(synth.TINY, 4, "stress")
+    dims = synth.TINY
+    model = mb.MosaicBert(mb.ModelDims(dims.hidden, dims.heads, dims.intermediate, dims.vocab, 1, dims.ln_eps), params)
+    batch = synth.make_batch("C1", 77)
+    labels = np.full_like(batch["labels"], -100)
+    model.zero_grad()
+    nnz, n_m = model.micro_step(*(to_dev(x, I32) for x in (batch["input_ids"], batch["attention_mask"], labels)))
+    torch.cuda.synchronize()
+    assert nnz == int(batch["attention_mask"].sum()) and n_m == 0
+    assert float(model.loss_sum.item()) == 0.0
+    assert all(float(b.g.abs().max().item()) == 0.0 for b in model.buckets)
+    empty = np.zeros_like(batch["attention_mask"])
+    model.zero_grad()
+    nnz, n_m = model.micro_step(*(to_dev(x, I32) for x in (batch["input_ids"], empty, batch["labels"])))
+    torch.cuda.synchronize()
+    assert (nnz, n_m) == (0, 0)
+    assert all(float(b.g.abs().max().item()) == 0.0 for b in model.buckets)
+
+
 def test_loss_zero_decoder_is_lnV():
     """Pin P12 on the GPU path: E_tok = 0 and b_dec = 0 give loss = ln V exactly (up to fp32)."""
     params = synth.make_model_params(synth.TINY, 3, "stress")
