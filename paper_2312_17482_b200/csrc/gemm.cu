@@ -56,6 +56,14 @@ struct Sched {
     kb0 = s * kb_per;
     kb1 = min(nkb, kb0 + kb_per);
   }
+  // k-block range [d0, d1) of a unit whose A tiles also feed the bias-gradient MMA: the unit's range
+  // is split evenly over the num_n column tiles of its m-block (db does not depend on n), so every
+  // tile pays 1/num_n of the extra N = 16 MMA instead of the n = 0 tiles paying all of it
+  __device__ __forceinline__ void db_range(int n, int kb0, int kb1, int& d0, int& d1) const {
+    const int len = (kb1 - kb0 + num_n - 1) / num_n;
+    d0 = min(kb1, kb0 + n * len);
+    d1 = min(kb1, d0 + len);
+  }
 };
 
 __device__ __forceinline__ void load_bf16x32(const bf16* src, float* v, int ncols_valid) {
@@ -264,8 +272,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         sm100::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         // bias gradient of a weight-gradient GEMM: db[m] = sum_k A[m, k] comes from the A tiles
-        // already in smem, as an extra N = 16 MMA against an all-ones B tile (only once per m-block)
-        const bool do_db = ACC == 1 && ep.dbias != nullptr && nb == 0;
+        // already in smem, as an extra N = 16 MMA against an all-ones B tile; each of the m-block's
+        // num_n tiles covers 1/num_n of the k-range (Sched::db_range)
+        int dkb0 = 0, dkb1 = 0;
+        if (ACC == 1 && ep.dbias != nullptr) sc.db_range(nb, kb0, kb1, dkb0, dkb1);
         constexpr uint32_t idesc_db = sm100::idesc_bf16(BM * CG, 16, A_MN, 0);
         const uint32_t d_db = tmem_base + C::TMEM_DB + acc * 16;
         const uint32_t s_ones = sm100::smem_u32(ones);
@@ -280,10 +290,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const uint64_t bd = B_MN ? sm100::desc_mnmajor_sw128(sb + k * 2048, 8192) : sm100::desc_kmajor_sw128(sb + k * 32);
             if (CG == 2) sm100::mma_bf16_ss_pair(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
             else sm100::mma_bf16_ss(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-            if (ACC == 1 && do_db) {
+            if (ACC == 1 && kb >= dkb0 && kb < dkb1) {
               const uint64_t od = sm100::desc_kmajor_sw128(s_ones + k * 32);
-              if (CG == 2) sm100::mma_bf16_ss_pair(d_db, ad, od, idesc_db, (kb > kb0 || k > 0) ? 1u : 0u);
-              else sm100::mma_bf16_ss(d_db, ad, od, idesc_db, (kb > kb0 || k > 0) ? 1u : 0u);
+              if (CG == 2) sm100::mma_bf16_ss_pair(d_db, ad, od, idesc_db, (kb > dkb0 || k > 0) ? 1u : 0u);
+              else sm100::mma_bf16_ss(d_db, ad, od, idesc_db, (kb > dkb0 || k > 0) ? 1u : 0u);
             }
           }
           if (CG == 2) sm100::mma_commit_pair(&empty[stage]);
@@ -457,7 +467,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               emit_chunk(scrA, v, reinterpret_cast<bf16*>(ep.C), ep.ldc, row0, M, col, N, lane);
             }
           } else if (ep.mode == E_F32_ACC) {
-            if (ACC == 1 && c == 0 && grp == 0 && ep.dbias && nb == 0) {
+            int dkb0 = 0, dkb1 = 0;
+            if (ACC == 1 && ep.dbias) sc.db_range(nb, kb0, kb1, dkb0, dkb1);
+            if (ACC == 1 && c == 0 && grp == 0 && dkb0 < dkb1) {
               float dbv[16];
               sm100::tmem_ld16(tmem_base + C::TMEM_DB + acc * 16 + ((uint32_t)(q * 32) << 16), dbv);
               sm100::tmem_ld_wait();
