@@ -37,12 +37,9 @@ struct Cfg {
   static constexpr int DATA = STAGE_BYTES * STAGES;
   static constexpr int SCR = NUM_EPI_WARPS * NSCR * SCR_BYTES;
   static constexpr int BIAS = NUM_EPI_WARPS * 256;  // per-warp staged bias slice of the current tile
-  static constexpr int ONES = 2048;                  // all-ones K-major B tile (16 rows x 64) for db MMAs
-  static constexpr int SMEM = DATA + SCR + BIAS + ONES + 1024 + 256;
-  // ACC accumulator stages of BN columns (+ ACC x 16 columns of bias-gradient accumulators)
-  static constexpr int TMEM_NEED = ACC * BN + ACC * 16;
+  static constexpr int SMEM = DATA + SCR + BIAS + 1024 + 384;
+  static constexpr int TMEM_NEED = ACC * BN;  // ACC accumulator stages of BN fp32 columns
   static constexpr int TMEM_COLS = TMEM_NEED <= 256 ? 256 : 512;
-  static constexpr int TMEM_DB = ACC * BN;  // first column of the db accumulators
 };
 
 struct Sched {
@@ -56,9 +53,9 @@ struct Sched {
     kb0 = s * kb_per;
     kb1 = min(nkb, kb0 + kb_per);
   }
-  // k-block range [d0, d1) of a unit whose A tiles also feed the bias-gradient MMA: the unit's range
-  // is split evenly over the num_n column tiles of its m-block (db does not depend on n), so every
-  // tile pays 1/num_n of the extra N = 16 MMA instead of the n = 0 tiles paying all of it
+  // k-block range [d0, d1) of a unit whose A tiles also feed the bias gradient: the unit's range is
+  // split evenly over the num_n column tiles of its m-block (db does not depend on n), so every
+  // tile reads 1/num_n of its A tiles a second time instead of the n = 0 tiles reading all
   __device__ __forceinline__ void db_range(int n, int kb0, int kb1, int& d0, int& d1) const {
     const int len = (kb1 - kb0 + num_n - 1) / num_n;
     d0 = min(kb1, kb0 + n * len);
@@ -170,16 +167,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                 Sched sc, Epi ep) {
   using C = Cfg<BN, STAGES, NSCR, CG, ACC>;
+  static_assert(ACC == 2 || A_MN == 1, "the fused bias gradient reads MN-major A tiles");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* scr_base = smem + C::DATA;
   uint8_t* bias_base = smem + C::DATA + C::SCR;
-  uint8_t* ones = smem + C::DATA + C::SCR + C::BIAS;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATA + C::SCR + C::BIAS + C::ONES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATA + C::SCR + C::BIAS);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* mdone = tempty + 2;  // [STAGES] (ACC == 1) the MMAs have consumed the stage
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mdone + STAGES);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -189,9 +187,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch(&tmA);
     sm100::tma_prefetch(&tmB);
+    // ACC == 1 (weight gradients with a fused bias gradient): the MMA's commit goes to mdone and the
+    // epilogue warps, after reading the stage's A tile for db, release it to the producer (empty)
     for (int i = 0; i < STAGES; ++i) {
       sm100::mbar_init(&full[i], 1);
-      sm100::mbar_init(&empty[i], 1);
+      sm100::mbar_init(&empty[i], ACC == 1 ? NUM_EPI_WARPS : 1);
+      if (ACC == 1) sm100::mbar_init(&mdone[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&tfull[i], 1);
@@ -202,11 +203,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp == 2) {
     if (CG == 2) sm100::tmem_alloc_pair(tmem_slot, C::TMEM_COLS);
     else sm100::tmem_alloc(tmem_slot, C::TMEM_COLS);
-  }
-  if (ACC == 1 && warp == 3) {  // bf16 1.0 everywhere (the swizzle of an all-ones tile is irrelevant)
-    for (int i = lane; i < C::ONES / 16; i += 32)
-      sts128(sm100::smem_u32(ones) + i * 16, make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u));
-    sm100::fence_proxy_async_smem();
   }
   sm100::tc_fence_before();
   if (CG == 2) sm100::cluster_sync();
@@ -271,14 +267,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         sm100::mbar_wait(&tempty[acc], acc_phase ^ 1);
         sm100::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        // bias gradient of a weight-gradient GEMM: db[m] = sum_k A[m, k] comes from the A tiles
-        // already in smem, as an extra N = 16 MMA against an all-ones B tile; each of the m-block's
-        // num_n tiles covers 1/num_n of the k-range (Sched::db_range)
-        int dkb0 = 0, dkb1 = 0;
-        if (ACC == 1 && ep.dbias != nullptr) sc.db_range(nb, kb0, kb1, dkb0, dkb1);
-        constexpr uint32_t idesc_db = sm100::idesc_bf16(BM * CG, 16, A_MN, 0);
-        const uint32_t d_db = tmem_base + C::TMEM_DB + acc * 16;
-        const uint32_t s_ones = sm100::smem_u32(ones);
         for (int kb = kb0; kb < kb1; ++kb) {
           sm100::mbar_wait(&full[stage], phase);
           sm100::tc_fence_after();
@@ -290,14 +278,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const uint64_t bd = B_MN ? sm100::desc_mnmajor_sw128(sb + k * 2048, 8192) : sm100::desc_kmajor_sw128(sb + k * 32);
             if (CG == 2) sm100::mma_bf16_ss_pair(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
             else sm100::mma_bf16_ss(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-            if (ACC == 1 && kb >= dkb0 && kb < dkb1) {
-              const uint64_t od = sm100::desc_kmajor_sw128(s_ones + k * 32);
-              if (CG == 2) sm100::mma_bf16_ss_pair(d_db, ad, od, idesc_db, (kb > dkb0 || k > 0) ? 1u : 0u);
-              else sm100::mma_bf16_ss(d_db, ad, od, idesc_db, (kb > dkb0 || k > 0) ? 1u : 0u);
-            }
           }
-          if (CG == 2) sm100::mma_commit_pair(&empty[stage]);
-          else sm100::mma_commit(&empty[stage]);
+          uint64_t* rel = ACC == 1 ? &mdone[stage] : &empty[stage];
+          if (CG == 2) sm100::mma_commit_pair(rel);
+          else sm100::mma_commit(rel);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -319,9 +303,52 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const uint32_t scrB = scrA + (NSCR > 1 ? SCR_BYTES : 0);
     int acc = 0;
     uint32_t acc_phase = 0;
+    int rstage = 0;  // ACC == 1: position in the operand ring, in step with the MMA warp
+    uint32_t rphase = 0;
     for (int u = cid; u < sc.total; u += ncl) {
       int mb, nb, kb0, kb1;
       sc.decode(u, mb, nb, kb0, kb1);
+      if (ACC == 1) {
+        // bias gradient of a weight-gradient GEMM, db[m] = sum_k A[m, k], on the CUDA cores from the
+        // A tiles the MMAs have just consumed (MN-major: two 128B-swizzled boxes of 64 m x 64 k per
+        // stage).  Thread t sums 16-byte chunk (t & 15) = 8 consecutive m over k-rows (t >> 4) + 16j.
+        int dkb0 = 0, dkb1 = 0;
+        if (ep.dbias) sc.db_range(nb, kb0, kb1, dkb0, dkb1);
+        const int t = threadIdx.x - 128, ch = t & 15, r0 = t >> 4;
+        float dbs[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) dbs[e] = 0.f;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          sm100::mbar_wait(&mdone[rstage], rphase);
+          if (kb >= dkb0 && kb < dkb1) {
+            const uint32_t sa = sm100::smem_u32(smem + rstage * C::STAGE_BYTES) + (ch >> 3) * 8192;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int r = r0 + 16 * j;
+              float f[8];
+              bf16x8_to_f32(lds128(sa + r * 128 + (((ch & 7) ^ (r & 7)) << 4)), f);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) dbs[e] += f[e];
+            }
+          }
+          __syncwarp();
+          if (lane == 0) sm100::mbar_arrive(&empty[rstage]);
+          if (++rstage == STAGES) {
+            rstage = 0;
+            rphase ^= 1;
+          }
+        }
+        if (dkb0 < dkb1) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) dbs[e] += __shfl_xor_sync(0xffffffffu, dbs[e], 16);
+          const int m0 = (mb * CG + rank) * BM + ch * 8;
+          if (lane < 16) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (m0 + e < M) atomicAdd(ep.dbias + m0 + e, dbs[e]);
+          }
+        }
+      }
       const int row0 = (mb * CG + rank) * BM + q * 32;
       const int row = row0 + lane;
       const bool row_ok = row < M;
@@ -467,14 +494,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               emit_chunk(scrA, v, reinterpret_cast<bf16*>(ep.C), ep.ldc, row0, M, col, N, lane);
             }
           } else if (ep.mode == E_F32_ACC) {
-            int dkb0 = 0, dkb1 = 0;
-            if (ACC == 1 && ep.dbias) sc.db_range(nb, kb0, kb1, dkb0, dkb1);
-            if (ACC == 1 && c == 0 && grp == 0 && dkb0 < dkb1) {
-              float dbv[16];
-              sm100::tmem_ld16(tmem_base + C::TMEM_DB + acc * 16 + ((uint32_t)(q * 32) << 16), dbv);
-              sm100::tmem_ld_wait();
-              if (row_ok) atomicAdd(ep.dbias + row, dbv[0]);
-            }
             sm100::tmem_ld_wait();
             if (row_ok) {
               float* dst = reinterpret_cast<float*>(ep.C) + (int64_t)row * ep.ldc + col;
