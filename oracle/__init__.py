@@ -15,4 +15,7 @@ full-depth (12/24-layer) activations, for which the paper prints nothing (pin P1
 unpinned" beyond the per-layer pins.
 """
 from .mosaicbert import *  # noqa: F401,F403
-from .mosaicbert import __all__  # noqa: F401
+from .mosaicbert import __all__ as _mb_all
+from .optim import adamw_step, lr_at  # noqa: F401  (F1, reading R34)
+
+__all__ = [*_mb_all, "adamw_step", "lr_at"]
