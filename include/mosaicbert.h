@@ -272,9 +272,15 @@ MB_API mb_status mb_mlm_loss(const mb_dims* d, const mb_head_params* p, const mb
 
 /* ---------------------------------------------------------------------------------------------
  * F1 — fused decoupled AdamW update (Table A1: beta=(0.9,0.98), eps=1e-6, wd 1e-5):
- *   m = b1 m + (1-b1) g; v = b2 v + (1-b2) g^2; p -= lr (m_hat/(sqrt(v_hat)+eps) + wd p)
- * master fp32 [n] in/out, m, v fp32 [n] in/out, g fp32 [n] (gradient, scaled by grad_scale),
- * w_bf16 [n] out (the bf16 weight copy the kernels read).  step >= 1 (bias correction). */
+ *   g' = grad_scale g; m = b1 m + (1-b1) g'; v = b2 v + (1-b2) g'^2;
+ *   m_hat = m / (1 - b1^step); v_hat = v / (1 - b2^step);
+ *   p = p - lr m_hat / (sqrt(v_hat) + eps) - weight_decay p
+ * "Decoupled" (reading R34, Loshchilov & Hutter): the decay never enters the gradient and is NOT
+ * multiplied by lr; weight_decay is the per-step factor (lr_t / lr_peak) * wd that the caller
+ * derives from the schedule (warmup 6 %, linear decay to 0.02 lr).
+ * master fp32 [n] in/out, m, v fp32 [n] in/out, g fp32 [n], w_bf16 [n] out (RNE of the new master:
+ * the bf16 weight copy the kernels read).  step >= 1.  Stream-ordered, allocates nothing.
+ * Errors: NULL pointer, n < 0 or step < 1 -> MB_ERR_INVALID_ARG; launch failure -> MB_ERR_CUDA. */
 MB_API mb_status mb_adamw_step(float* master, float* m, float* v, const float* g, mb_bf16* w_bf16, int64_t n, float lr,
                         float beta1, float beta2, float eps, float weight_decay, float grad_scale, int32_t step,
                         mb_stream_t s);

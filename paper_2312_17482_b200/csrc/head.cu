@@ -64,9 +64,37 @@ __global__ void adamw_kernel(float* __restrict__ p, float* __restrict__ m, float
     v[i] = vi;
     const float mh = mi / bc1, vh = vi / bc2;
     float pi = p[i];
-    pi -= lr * (mh / (sqrtf(vh) + eps) + wd * pi);
+    pi -= lr * (mh / (sqrtf(vh) + eps)) + wd * pi;  // decoupled decay: wd is the per-step factor (R34)
     p[i] = pi;
     w[i] = __float2bfloat16_rn(pi);
+  }
+}
+
+// the same update on 4 consecutive parameters per thread: 16-byte loads/stores of p, m, v, g and an
+// 8-byte store of the bf16 weights (4x the bytes in flight per thread of the scalar loop)
+__device__ __forceinline__ float adamw_one(float& p, float& m, float& v, float g, float lr, float b1, float b2,
+                                           float eps, float wd, float gscale, float bc1, float bc2) {
+  g *= gscale;
+  m = b1 * m + (1.f - b1) * g;
+  v = b2 * v + (1.f - b2) * g * g;
+  p -= lr * ((m / bc1) / (sqrtf(v / bc2) + eps)) + wd * p;
+  return p;
+}
+__global__ void adamw4_kernel(float4* __restrict__ p, float4* __restrict__ m, float4* __restrict__ v,
+                              const float4* __restrict__ g, uint2* __restrict__ w, int64_t n4, float lr, float b1,
+                              float b2, float eps, float wd, float gscale, float bc1, float bc2) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 pi = p[i], mi = m[i], vi = v[i];
+    const float4 gi = g[i];
+    adamw_one(pi.x, mi.x, vi.x, gi.x, lr, b1, b2, eps, wd, gscale, bc1, bc2);
+    adamw_one(pi.y, mi.y, vi.y, gi.y, lr, b1, b2, eps, wd, gscale, bc1, bc2);
+    adamw_one(pi.z, mi.z, vi.z, gi.z, lr, b1, b2, eps, wd, gscale, bc1, bc2);
+    adamw_one(pi.w, mi.w, vi.w, gi.w, lr, b1, b2, eps, wd, gscale, bc1, bc2);
+    p[i] = pi;
+    m[i] = mi;
+    v[i] = vi;
+    const __nv_bfloat162 lo = __floats2bfloat162_rn(pi.x, pi.y), hi = __floats2bfloat162_rn(pi.z, pi.w);
+    w[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
   }
 }
 
@@ -237,9 +265,27 @@ mb_status mb_adamw_step(float* master, float* m, float* v, const float* g, mb_bf
   if (!master || !m || !v || !g || !w_bf16 || n < 0 || step < 1) return MB_ERR_INVALID_ARG;
   if (n == 0) return MB_OK;
   const float bc1 = 1.f - powf(beta1, (float)step), bc2 = 1.f - powf(beta2, (float)step);
-  const int grid = (int)std::min<int64_t>((n + 255) / 256, 8 * mb::num_sms());
-  mb::adamw_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(
-      master, m, v, g, reinterpret_cast<bf16*>(w_bf16), n, lr, beta1, beta2, eps, weight_decay, grad_scale, bc1, bc2);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
+  const bool vec = ((reinterpret_cast<uintptr_t>(master) | reinterpret_cast<uintptr_t>(m) |
+                     reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(g)) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(w_bf16) & 7) == 0;
+  int64_t done = 0;
+  if (vec && n >= 4) {
+    const int64_t n4 = n / 4;
+    const int grid = (int)std::min<int64_t>((n4 + 255) / 256, 8 * mb::num_sms());
+    mb::adamw4_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<float4*>(master), reinterpret_cast<float4*>(m),
+                                            reinterpret_cast<float4*>(v), reinterpret_cast<const float4*>(g),
+                                            reinterpret_cast<uint2*>(w_bf16), n4, lr, beta1, beta2, eps,
+                                            weight_decay, grad_scale, bc1, bc2);
+    MB_CHECK_LAUNCH();
+    done = n4 * 4;
+  }
+  if (done == n) return MB_OK;
+  const int64_t rest = n - done;
+  const int grid = (int)std::min<int64_t>((rest + 255) / 256, 8 * mb::num_sms());
+  mb::adamw_kernel<<<grid, 256, 0, st>>>(master + done, m + done, v + done, g + done,
+                                         reinterpret_cast<bf16*>(w_bf16) + done, rest, lr, beta1, beta2, eps,
+                                         weight_decay, grad_scale, bc1, bc2);
   MB_CHECK_LAUNCH();
   return MB_OK;
 }

@@ -289,6 +289,12 @@ __global__ void colsum_kernel(const bf16* __restrict__ x, int n, int C, int rows
 // one-warp-per-row variant needed ~128 registers).  Row sums combine across the W warps through
 // shared memory (double-buffered by row parity, one named barrier per row).
 constexpr int LNW_GROUPS = 8;  // row groups (rows in flight) per CTA (8: half the CTAs, reductions and atomics of 4)
+// Embedding backward (A3): dE_tok[id] += dx0 for every token.  A few ids occur thousands of times
+// per batch ([MASK] is ~80 % of the 30 % masked positions, [CLS]/[SEP] open/close every sequence), and
+// fp32 atomics on one row serialise in its L2 slice.  Each CTA therefore owns a contiguous range of
+// <= EMB_ROWS rows, finds the ids that repeat >= EMB_HOT_MIN times inside it, accumulates those rows
+// in shared memory (EMB_HOT slots) and flushes each slot once; all other rows go straight to L2.
+constexpr int EMB_ROWS = 256, EMB_HOT = 4, EMB_HOT_MIN = 3;
 
 template <int W, bool EMBED, bool GELU, bool DSUM, bool DROP = false>
 __global__ void __launch_bounds__(LNW_GROUPS * W * 32)
@@ -297,11 +303,43 @@ __global__ void __launch_bounds__(LNW_GROUPS * W * 32)
                     float* __restrict__ d_emb, float* __restrict__ dgamma, float* __restrict__ dbeta,
                     float* __restrict__ dsum, DropArgs drop, bf16* __restrict__ dxd) {
   __shared__ float red[LNW_GROUPS][2][W][2];
-  extern __shared__ float sbuf[];  // [LNW_GROUPS][H] for the final column reduction
+  extern __shared__ float sbuf[];  // [LNW_GROUPS][H] for the final column reduction (+ EMBED: [EMB_HOT][H])
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int rg = warp / W, w = warp - rg * W;
   const int c = (w * 32 + lane) * 8;  // this lane's 8 columns
   const float inv_h = __frcp_rn((float)H);
+  // EMBED: contiguous row range, its ids staged in smem, repeated ids given a shared-memory slot
+  __shared__ int sid[EMBED ? EMB_ROWS : 1];
+  __shared__ int hot[EMB_HOT];
+  float* hacc = sbuf + LNW_GROUPS * H;
+  int r_begin = 0, r_end = n;
+  if (EMBED) {
+    const int per = (n + gridDim.x - 1) / gridDim.x;
+    r_begin = min(n, blockIdx.x * per);
+    r_end = min(n, r_begin + per);
+    const int cnt = r_end - r_begin;
+    if (threadIdx.x < EMB_HOT) hot[threadIdx.x] = -1;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) sid[i] = src.ids[src.indices[r_begin + i]];
+    for (int i = threadIdx.x; i < EMB_HOT * H; i += blockDim.x) hacc[i] = 0.f;
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const int id = sid[i];
+      int m = 0, first = i;
+      for (int j = 0; j < cnt; ++j) {
+        const bool eq = sid[j] == id;
+        m += eq;
+        if (eq && j < first) first = j;
+      }
+      if (m >= EMB_HOT_MIN && first == i) {  // one inserter per distinct id
+        for (int k = 0; k < EMB_HOT; ++k)
+          if (atomicCAS(&hot[k], -1, id) == -1) break;
+      }
+    }
+    __syncthreads();
+  }
+  int hid[EMB_HOT];
+#pragma unroll
+  for (int k = 0; k < EMB_HOT; ++k) hid[k] = EMBED ? hot[k] : -1;
   float gm[8];
   bf16x8_to_f32(*reinterpret_cast<const uint4*>(gamma + c), gm);
   float ag[8], ab[8], as[8];
@@ -309,11 +347,11 @@ __global__ void __launch_bounds__(LNW_GROUPS * W * 32)
   for (int j = 0; j < 8; ++j) ag[j] = ab[j] = as[j] = 0.f;
   int par = 0;
   // one-row-ahead prefetch of x, dy, stats (doubles the bytes in flight per SM)
-  const int step = gridDim.x * LNW_GROUPS;
+  const int step = EMBED ? LNW_GROUPS : gridDim.x * LNW_GROUPS;
   auto fetch = [&](int r, uint4& xv, uint4& dv, float2& sv, int& idv) {
     const bf16* base;
     if (EMBED) {
-      idv = src.ids[src.indices[r]];
+      idv = sid[r - r_begin];
       base = src.emb + (size_t)idv * H;
     } else {
       base = src.x + (size_t)r * H;
@@ -325,13 +363,13 @@ __global__ void __launch_bounds__(LNW_GROUPS * W * 32)
   uint4 nx = make_uint4(0, 0, 0, 0), nd = make_uint4(0, 0, 0, 0);
   float2 nst = make_float2(0.f, 0.f);
   int nid = 0;
-  int row = blockIdx.x * LNW_GROUPS + rg;
-  if (row < n) fetch(row, nx, nd, nst, nid);
-  for (; row < n; row += step, par ^= 1) {
+  int row = EMBED ? r_begin + rg : blockIdx.x * LNW_GROUPS + rg;
+  if (row < r_end) fetch(row, nx, nd, nst, nid);
+  for (; row < r_end; row += step, par ^= 1) {
     const uint4 cx = nx, cd = nd;
     const float2 st = nst;
     const int id = nid;
-    if (row + step < n) fetch(row + step, nx, nd, nst, nid);
+    if (row + step < r_end) fetch(row + step, nx, nd, nst, nid);
     float xh[8], d[8];
     bf16x8_to_f32(cx, xh);
     if (EMBED) {
@@ -389,9 +427,18 @@ __global__ void __launch_bounds__(LNW_GROUPS * W * 32)
     if (DROP) {
       *reinterpret_cast<uint4*>(dxd + (size_t)row * H + c) = f32_to_bf16x8(o);
     } else if (EMBED) {
-      float* dst = d_emb + (size_t)id * H + c;
-      red_add_v4(dst, o[0], o[1], o[2], o[3]);
-      red_add_v4(dst + 4, o[4], o[5], o[6], o[7]);
+      int slot = -1;
+#pragma unroll
+      for (int k = 0; k < EMB_HOT; ++k)
+        if (hid[k] == id) slot = k;
+      if (slot >= 0) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) atomicAdd(hacc + slot * H + c + j, o[j]);
+      } else {
+        float* dst = d_emb + (size_t)id * H + c;
+        red_add_v4(dst, o[0], o[1], o[2], o[3]);
+        red_add_v4(dst + 4, o[4], o[5], o[6], o[7]);
+      }
     } else {
       *reinterpret_cast<uint4*>(dx + (size_t)row * H + c) = f32_to_bf16x8(o);
     }
@@ -412,6 +459,16 @@ __global__ void __launch_bounds__(LNW_GROUPS * W * 32)
   reduce(ag, dgamma);
   reduce(ab, dbeta);
   if (DSUM) reduce(as, dsum);
+  if (EMBED) {  // flush the shared-memory rows of the repeated ids (written by every warp: barrier first)
+    __syncthreads();
+#pragma unroll 1
+    for (int k = 0; k < EMB_HOT; ++k) {
+      if (hid[k] < 0) continue;
+      for (int cc = threadIdx.x * 4; cc < H; cc += blockDim.x * 4)
+        red_add_v4(d_emb + (size_t)hid[k] * H + cc, hacc[k * H + cc], hacc[k * H + cc + 1], hacc[k * H + cc + 2],
+                   hacc[k * H + cc + 3]);
+    }
+  }
 }
 
 template <int W, bool EMBED>
@@ -419,9 +476,21 @@ mb_status ln_bwd_w_launch(const RowSrc& src, const bf16* dy, const float* stats,
                           const bf16* gelu_pre, int n, int H, bf16* dx, float* d_emb, float* dg, float* db,
                           float* dsum, cudaStream_t s, const DropArgs& drop, bf16* dxd) {
   const int threads = LNW_GROUPS * W * 32;
-  const int smem = LNW_GROUPS * H * sizeof(float);
+  const int smem = (LNW_GROUPS + (EMBED ? EMB_HOT : 0)) * H * sizeof(float);
   const int blocks_per_sm = std::max(1, 2048 / threads);
-  const int grid = std::max(1, std::min((n + LNW_GROUPS - 1) / LNW_GROUPS, blocks_per_sm * num_sms()));
+  int grid = std::max(1, std::min((n + LNW_GROUPS - 1) / LNW_GROUPS, blocks_per_sm * num_sms()));
+  if (EMBED) {
+    grid = std::max(grid, (n + EMB_ROWS - 1) / EMB_ROWS);  // <= EMB_ROWS rows per CTA
+    static bool attr = false;  // H = 1024: 48 KB dynamic + static smem exceeds the default window
+    if (!attr) {
+      if (cudaFuncSetAttribute(ln_bwd_w_kernel<W, true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               smem) != cudaSuccess ||
+          cudaFuncSetAttribute(ln_bwd_w_kernel<W, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               smem) != cudaSuccess)
+        return MB_ERR_CUDA;
+      attr = true;
+    }
+  }
 #define LNW_GO(G, D)                                                                                          \
   ln_bwd_w_kernel<W, EMBED, G, D><<<grid, threads, smem, s>>>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, \
                                                                dg, db, dsum, drop, dxd)

@@ -94,13 +94,17 @@ class MosaicBert:
     """MosaicBERT encoder + MLM head whose forward/backward run in libmosaicbert.so."""
 
     def __init__(self, dims: ModelDims, params: dict | None = None, device: str | torch.device = "cuda",
-                 process_group=None, dropout: float = 0.0, seed: int = 0):
+                 process_group=None, dropout: float = 0.0, seed: int = 0, lr_peak: float = 5e-4,
+                 total_steps: int | None = None):
         """dropout: F2 feed-forward dropout probability (P:152 uses 0.1; R13/R32).  Each micro-step
-        draws its masks from seed_of(micro-step), a pure function of (seed, rank, micro-step index)."""
+        draws its masks from seed_of(micro-step), a pure function of (seed, rank, micro-step index).
+        lr_peak / total_steps: the F1 schedule (Table A1: 5e-4 Base, 2e-4 Large)."""
         if not 0.0 <= dropout < 1.0:
             raise ValueError("dropout must be in [0, 1)")
         self.dropout = float(dropout)
         self.seed = int(seed)
+        self.lr_peak = float(lr_peak)
+        self.total_steps = total_steps
         self.micro_index = 0
         self.d = dims
         self.cd = dims.c()
@@ -275,18 +279,36 @@ class MosaicBert:
         self._handles = []
 
     # ------------------------------------------------------------------ optimizer (F1)
-    def optimizer_step(self, grad_scale: float, lr: float = 5e-4, betas=(0.9, 0.98), eps=1e-6,
+    def lr_at(self, step: int) -> float:
+        """Warmup + linear decay (Table A1): 0 -> lr_peak over the first 6 % of
+        total_steps, then linearly to 0.02 lr_peak at total_steps; constant lr_peak if total_steps
+        is None."""
+        if self.total_steps is None:
+            return self.lr_peak
+        T = self.total_steps
+        step = min(max(step, 0), T)
+        w = 0.06 * T
+        if step <= w:
+            return self.lr_peak * step / w if w > 0 else self.lr_peak
+        return self.lr_peak * (1.0 - 0.98 * (step - w) / (T - w))
+
+    def optimizer_step(self, grad_scale: float, lr: float | None = None, betas=(0.9, 0.98), eps=1e-6,
                        weight_decay: float = 1e-5):
-        """Decoupled AdamW (Table A1) over every bucket; rewrites the bf16 weights."""
+        """Decoupled AdamW (Table A1) over every bucket; rewrites the bf16 weights.  lr
+        defaults to the schedule's value at this step; the decay factor handed to the kernel is
+        (lr / lr_peak) * weight_decay, not multiplied by lr (reading R34)."""
         self.step_count += 1
+        if lr is None:
+            lr = self.lr_at(self.step_count)
+        wd_step = (lr / self.lr_peak) * weight_decay
         for b in self.buckets:
             if b.master is None:
                 b.init_optimizer()
-            L.adamw_step(b.master, b.m, b.v, b.g, b.w, lr, betas[0], betas[1], eps, weight_decay, grad_scale,
+            L.adamw_step(b.master, b.m, b.v, b.g, b.w, lr, betas[0], betas[1], eps, wd_step, grad_scale,
                          self.step_count)
 
     # ------------------------------------------------------------------ whole optimizer step
-    def train_step(self, micro_batches: Sequence[tuple], global_masked: int | None = None, lr: float = 5e-4,
+    def train_step(self, micro_batches: Sequence[tuple], global_masked: int | None = None, lr: float | None = None,
                    optimizer: bool = True):
         """micro_batches: [(ids, mask, labels), ...] device int32 tensors.  Gradients are summed over
         micro-steps (+= contract) and ranks (allreduce on the last micro-step), then scaled by

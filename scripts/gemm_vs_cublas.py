@@ -61,3 +61,14 @@ dZ = torch.empty(T, I, device=dev, dtype=bf)
 o = timeit(lambda: _lib.geglu_backward(dF, W2, Gd, dU))
 r = timeit(lambda: torch.matmul(dF, W2, out=dZ))
 report("geglu_bwd", 2 * T * I * Hd, o, r)
+
+# mainloop-efficiency probe: the same N with growing K (epilogue cost per FLOP shrinks as K grows)
+if __import__("os").environ.get("MB_GEMM_KSWEEP"):
+    for N, K in ((2304, 768), (2304, 3072), (2304, 12288), (768, 768), (768, 6144), (4096, 4096)):
+        A = torch.randn(T // 4 if K > 4096 else T, K, device=dev, dtype=bf)
+        M = A.shape[0]
+        W = torch.randn(N, K, device=dev, dtype=bf) * 0.02
+        C = torch.empty(M, N, device=dev, dtype=bf)
+        o = timeit(lambda: _lib.gemm(M, N, K, A, K, 0, W, K, 0, C, N))
+        r = timeit(lambda: torch.matmul(A, W.t(), out=C))
+        report(f"k{M}x{N}x{K}", 2 * M * N * K, o, r)

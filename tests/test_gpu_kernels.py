@@ -361,3 +361,40 @@ def test_geglu_naive_baseline():
     mb._lib.geglu_naive_backward(_bf(dz), _bf(ua), _bf(ug), dua, dug)
     check("geglu_naive.dua", np64(dua), dz * ug * O.gelu_grad(ua))
     check("geglu_naive.dug", np64(dug), dz * O.gelu(ua))
+
+
+# ------------------------------------------------------------------------------------ F1 AdamW
+@pytest.mark.parametrize("n", [1, 7, 1000, 9450243])
+def test_adamw_step_vs_oracle(n):
+    """mb_adamw_step (decoupled AdamW, R34) against the fp64 oracle over three steps with a changing
+    lr / decay factor and a grad_scale: fp32 master, moments within fp32 rounding of the oracle; the
+    bf16 weight copy is exactly the RNE of the kernel's own master.  n covers the scalar tail and a
+    full Base layer bucket (+3); offset views exercise the unaligned (scalar) path."""
+    from paper_2312_17482_b200 import _lib as L
+    rng = np.random.default_rng(n)
+    w0 = (0.02 * rng.standard_normal(n)).astype(np.float32)
+    for off in (0, 1):
+        N = n + off
+        master = torch.zeros(N, dtype=torch.float32, device="cuda")
+        m = torch.zeros_like(master)
+        v = torch.zeros_like(master)
+        g = torch.zeros_like(master)
+        wb = torch.zeros(N, dtype=BF, device="cuda")
+        mv, vv, gv, wv = m[off:], v[off:], g[off:], wb[off:]
+        pv = master[off:]
+        pv.copy_(torch.from_numpy(w0))
+        ow, om, ov = w0.astype(np.float64), np.zeros(n), np.zeros(n)
+        gmax = 0.0  # moments are sums of terms of size |g'| (g'^2): fp32 rounding is relative to those
+        for t in range(1, 4):
+            gr = (rng.standard_normal(n) * 10.0 ** rng.integers(-2, 3)).astype(np.float32)
+            gmax = max(gmax, float(np.abs(gr).max()) / 3.0)
+            gv.copy_(torch.from_numpy(gr))
+            lr, wd, gs = 5e-4 * t, 1e-5 * t, 1.0 / 3.0
+            L.adamw_step(pv, mv, vv, gv, wv, lr, 0.9, 0.98, 1e-6, wd, gs, t)
+            ow, om, ov = O.adamw_step(ow, om, ov, gr.astype(np.float64), t, lr=lr, wd_step=wd, grad_scale=np.float32(gs))
+        torch.cuda.synchronize()
+        pg = pv.double().cpu().numpy()
+        assert np.allclose(pg, ow, rtol=2e-6, atol=1e-9), float(np.max(np.abs(pg - ow)))
+        assert np.allclose(mv.double().cpu().numpy(), om, rtol=2e-6, atol=1e-6 * gmax)
+        assert np.allclose(vv.double().cpu().numpy(), ov, rtol=2e-6, atol=1e-6 * gmax * gmax)
+        assert torch.equal(wv.cpu(), pv.cpu().to(BF))
