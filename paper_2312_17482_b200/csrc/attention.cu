@@ -137,6 +137,8 @@ __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tbase = *tslot;
+  pdl_wait();  // (PDL) the setup above touched only shared memory, TMEM and kernel parameters
+  pdl_trigger();
   const uint32_t sPa = sm100::smem_u32(sP);
 
   int u0 = blockIdx.x;
@@ -423,6 +425,8 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tbase = *tslot;
+  pdl_wait();  // (PDL) the setup above touched only shared memory, TMEM and kernel parameters
+  pdl_trigger();
   const uint32_t sQa = sm100::smem_u32(sQ), sKVa = sm100::smem_u32(sKV), sPa = sm100::smem_u32(sP),
                  sOa = sm100::smem_u32(sOnes);
   auto nkv_of = [&](int u) {
@@ -754,6 +758,8 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tbase = *tslot;
+  pdl_wait();  // (PDL) the setup above touched only shared memory, TMEM and kernel parameters
+  pdl_trigger();
   const uint32_t tS = tbase, tdP = tbase + 128, tdV = tbase + 256, tdK = tbase + 320, tdQ = tbase + 384;
   const uint32_t sPa = sm100::smem_u32(sP), sdSa = sm100::smem_u32(sdS);
 
@@ -1131,6 +1137,8 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tbase = *tslot;
+  pdl_wait();  // (PDL) the setup above touched only shared memory, TMEM and kernel parameters
+  pdl_trigger();
   const uint32_t tS = tbase, tdP = tbase + 128, tdV = tbase + 256, tdK = tbase + 320, tdQ = tbase + 384;
   const uint32_t sKVa = sm100::smem_u32(sKV), sQDa = sm100::smem_u32(sQD), sPa = sm100::smem_u32(sP),
                  sdSa = sm100::smem_u32(sdS);
@@ -1387,7 +1395,9 @@ mb_status attention_fwd(const bf16* qkv, const int* cu, int batch, int nnz, int 
     MB_REQUIRE(make_tmap_bf16_2d(&tmo, O, H, nnz, H, 32, 32, 64), MB_ERR_CUDA);
     const int units = batch * heads;
     const int grid = std::max(1, std::min(units, num_sms()));
-    attn_fwd_short_kernel<<<grid, SH_FWD_THREADS, SH_FWD_SMEM2, s>>>(tm, tmo, cu, batch, heads, d, slopes, O, lse, nnz);
+    if (launch_pdl(attn_fwd_short_kernel, dim3(grid), dim3(SH_FWD_THREADS), SH_FWD_SMEM2, s, 1, tm, tmo, cu, batch,
+                   heads, d, slopes, O, lse, nnz) != cudaSuccess)
+      return MB_ERR_CUDA;
     MB_CHECK_LAUNCH();
     return MB_OK;
   }
@@ -1403,7 +1413,9 @@ mb_status attention_fwd(const bf16* qkv, const int* cu, int batch, int nnz, int 
   LongUnits U{cu, heads, (max_seqlen + TILE - 1) / TILE, 0};
   U.total = batch * heads * U.QT;
   const int grid = std::max(1, std::min(U.total, num_sms()));
-  attn_fwd_long_kernel<<<grid, LF_THREADS, LF_SMEM, s>>>(tm, tmo, U, d, slopes, O, lse, nnz);
+  if (launch_pdl(attn_fwd_long_kernel, dim3(grid), dim3(LF_THREADS), LF_SMEM, s, 1, tm, tmo, U, d, slopes, O, lse,
+                 nnz) != cudaSuccess)
+    return MB_ERR_CUDA;
   MB_CHECK_LAUNCH();
   return MB_OK;
 }
@@ -1439,8 +1451,9 @@ mb_status attention_bwd(const bf16* qkv, const bf16* O, const bf16* dO, const fl
     }
     const int units = batch * heads;
     const int grid = std::max(1, std::min(units, num_sms()));
-    attn_bwd_short_kernel<<<grid, SH_BWD_THREADS, SH_BWD_SMEM, s>>>(tq, tdo, tdq, cu, batch, heads, d, slopes, O, dO,
-                                                                     lse, dqkv, dbias, nnz);
+    if (launch_pdl(attn_bwd_short_kernel, dim3(grid), dim3(SH_BWD_THREADS), SH_BWD_SMEM, s, 1, tq, tdo, tdq, cu,
+                   batch, heads, d, slopes, O, dO, lse, dqkv, dbias, nnz) != cudaSuccess)
+      return MB_ERR_CUDA;
     MB_CHECK_LAUNCH();
     return MB_OK;
   }
@@ -1466,8 +1479,9 @@ mb_status attention_bwd(const bf16* qkv, const bf16* O, const bf16* dO, const fl
   LongUnits U{cu, heads, (max_seqlen + TILE - 1) / TILE, 0};
   U.total = batch * heads * U.QT;
   const int grid = std::max(1, std::min(U.total, num_sms()));
-  attn_bwd_long_kernel<<<grid, LB_THREADS, LB_SMEM, s>>>(tq, tdo, tdq, tdqa, U, d, slopes, lse, Dg, dq_acc, dqkv,
-                                                         dbias, nnz);
+  if (launch_pdl(attn_bwd_long_kernel, dim3(grid), dim3(LB_THREADS), LB_SMEM, s, 1, tq, tdo, tdq, tdqa, U, d, slopes,
+                 lse, Dg, dq_acc, dqkv, dbias, nnz) != cudaSuccess)
+    return MB_ERR_CUDA;
   MB_CHECK_LAUNCH();
   {
     const int rows_per = 128;

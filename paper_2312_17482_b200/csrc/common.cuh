@@ -167,6 +167,42 @@ __device__ __forceinline__ float gelu_grad_f(float x) {
   return c + x * p;
 }
 
+// Programmatic dependent launch (PDL).  A kernel launched through launch_pdl() may become resident
+// while its predecessor in the stream is still draining (its prologue — barrier init, TMEM alloc,
+// tensor-map prefetch — overlaps the predecessor's tail).  It must call pdl_wait() before it
+// touches global memory that earlier kernels write; pdl_trigger() then lets its own successor
+// start launching.  Both are no-ops for a kernel launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+bool pdl_enabled();  // host: true unless the environment sets MB_NO_PDL (A/B measurements)
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, int cluster,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (cluster > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = cluster;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 int num_sms();  // cached per device (host)
 int* device_scratch(size_t n_ints);  // library-owned device scratch (host; nullptr on failure)
 void count_launch();  // host-side counter of kernel launches (mb_launch_count)

@@ -209,6 +209,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   else __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // everything above touched only shared memory, TMEM and kernel parameters
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -689,6 +691,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   sm100::cluster_sync();
   sm100::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // everything above touched only shared memory, TMEM and kernel parameters
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {  // operands: own 128 rows of dF, own half (128 columns) of W2's tile
@@ -862,19 +866,8 @@ mb_status launch(const GemmArgs& g, const CUtensorMap& ta, const CUtensorMap& tb
     attr_set = true;
   }
   const int clusters = std::max(1, std::min(sc.total, num_sms() / CG));
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(clusters * CG);
-  cfg.blockDim = dim3(NTHREADS);
-  cfg.dynamicSmemBytes = C::SMEM;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CG;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, k, ta, tb, g.M, g.N, sc, g.ep) != cudaSuccess) return MB_ERR_CUDA;
+  if (launch_pdl(k, dim3(clusters * CG), dim3(NTHREADS), C::SMEM, s, CG, ta, tb, g.M, g.N, sc, g.ep) != cudaSuccess)
+    return MB_ERR_CUDA;
   MB_CHECK_LAUNCH();
   return MB_OK;
 }
@@ -963,19 +956,8 @@ mb_status gemm(const GemmArgs& g, cudaStream_t s) {
     sg.num_m = (g.M + 2 * BM - 1) / (2 * BM);
     sg.total = sg.num_m * sg.num_n * sg.splits;
     const int clusters = std::max(1, std::min(sg.total, num_sms() / 2));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * clusters);
-    cfg.blockDim = dim3(NTHREADS);
-    cfg.dynamicSmemBytes = GB_SMEM;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, geglu_bwd_kernel, ta, tb, tg, tdu, g.M, g.ep.I, sg) != cudaSuccess)
+    if (launch_pdl(geglu_bwd_kernel, dim3(2 * clusters), dim3(NTHREADS), GB_SMEM, s, 2, ta, tb, tg, tdu, g.M, g.ep.I,
+                   sg) != cudaSuccess)
       return MB_ERR_CUDA;
     MB_CHECK_LAUNCH();
     return MB_OK;

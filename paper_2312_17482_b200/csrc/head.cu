@@ -83,6 +83,8 @@ __device__ __forceinline__ float adamw_one(float& p, float& m, float& v, float g
 __global__ void adamw4_kernel(float4* __restrict__ p, float4* __restrict__ m, float4* __restrict__ v,
                               const float4* __restrict__ g, uint2* __restrict__ w, int64_t n4, float lr, float b1,
                               float b2, float eps, float wd, float gscale, float bc1, float bc2) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
     float4 pi = p[i], mi = m[i], vi = v[i];
     const float4 gi = g[i];
@@ -273,10 +275,11 @@ mb_status mb_adamw_step(float* master, float* m, float* v, const float* g, mb_bf
   if (vec && n >= 4) {
     const int64_t n4 = n / 4;
     const int grid = (int)std::min<int64_t>((n4 + 255) / 256, 8 * mb::num_sms());
-    mb::adamw4_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<float4*>(master), reinterpret_cast<float4*>(m),
-                                            reinterpret_cast<float4*>(v), reinterpret_cast<const float4*>(g),
-                                            reinterpret_cast<uint2*>(w_bf16), n4, lr, beta1, beta2, eps,
-                                            weight_decay, grad_scale, bc1, bc2);
+    if (mb::launch_pdl(mb::adamw4_kernel, dim3(grid), dim3(256), 0, st, 1, reinterpret_cast<float4*>(master),
+                       reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v),
+                       reinterpret_cast<const float4*>(g), reinterpret_cast<uint2*>(w_bf16), n4, lr, beta1, beta2,
+                       eps, weight_decay, grad_scale, bc1, bc2) != cudaSuccess)
+      return MB_ERR_CUDA;
     MB_CHECK_LAUNCH();
     done = n4 * 4;
   }

@@ -63,6 +63,8 @@ __global__ void __launch_bounds__(LN_THREADS, LNP_BLOCKS) ln_fwd_persist_kernel(
                                                                                 int H, float eps,
                                                                                 bf16* __restrict__ y,
                                                                                 float* __restrict__ stats) {
+  pdl_wait();
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int step = gridDim.x * LN_WARPS;
   uint4 nx[VPL];
@@ -302,6 +304,8 @@ __global__ void __launch_bounds__(LNW_GROUPS * W * 32)
                     const bf16* __restrict__ gamma, const bf16* __restrict__ gelu_pre, int n, int H, bf16* dx,
                     float* __restrict__ d_emb, float* __restrict__ dgamma, float* __restrict__ dbeta,
                     float* __restrict__ dsum, DropArgs drop, bf16* __restrict__ dxd) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float red[LNW_GROUPS][2][W][2];
   extern __shared__ float sbuf[];  // [LNW_GROUPS][H] for the final column reduction (+ EMBED: [EMB_HOT][H])
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -491,18 +495,20 @@ mb_status ln_bwd_w_launch(const RowSrc& src, const bf16* dy, const float* stats,
       attr = true;
     }
   }
-#define LNW_GO(G, D)                                                                                          \
-  ln_bwd_w_kernel<W, EMBED, G, D><<<grid, threads, smem, s>>>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, \
-                                                               dg, db, dsum, drop, dxd)
+#define LNW_GO(G, D)                                                                                           \
+  ok = launch_pdl(ln_bwd_w_kernel<W, EMBED, G, D>, dim3(grid), dim3(threads), smem, s, 1, src, dy, stats, gamma, \
+                  gelu_pre, n, H, dx, d_emb, dg, db, dsum, drop, dxd) == cudaSuccess
+  bool ok = true;
   if (!EMBED && drop.thr) {
     if (gelu_pre || !dsum || !dxd) return MB_ERR_INVALID_ARG;
-    ln_bwd_w_kernel<W, false, false, true, true><<<grid, threads, smem, s>>>(src, dy, stats, gamma, gelu_pre, n, H,
-                                                                             dx, d_emb, dg, db, dsum, drop, dxd);
+    ok = launch_pdl(ln_bwd_w_kernel<W, false, false, true, true>, dim3(grid), dim3(threads), smem, s, 1, src, dy, stats,
+                    gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, drop, dxd) == cudaSuccess;
   } else if (gelu_pre && dsum) LNW_GO(true, true);
   else if (gelu_pre) LNW_GO(true, false);
   else if (dsum) LNW_GO(false, true);
   else LNW_GO(false, false);
 #undef LNW_GO
+  if (!ok) return MB_ERR_CUDA;
   MB_CHECK_LAUNCH();
   return MB_OK;
 }
@@ -515,10 +521,14 @@ mb_status ln_fwd_dispatch(const RowSrc& src, const bf16* gamma, const bf16* beta
   const int vpl = (H / 8 + 31) / 32;
   if (!EMBED && (vpl == 3 || vpl == 4) && n >= 4096) {
     const int pgrid = std::min(grid, LNP_BLOCKS * num_sms());  // one resident wave, rows strided
+    bool ok;
     if (vpl == 3)
-      ln_fwd_persist_kernel<3><<<pgrid, LN_THREADS, 0, s>>>(src.x, gamma, beta, n, H, eps, y, stats);
+      ok = launch_pdl(ln_fwd_persist_kernel<3>, dim3(pgrid), dim3(LN_THREADS), 0, s, 1, src.x, gamma, beta, n, H, eps,
+                      y, stats) == cudaSuccess;
     else
-      ln_fwd_persist_kernel<4><<<pgrid, LN_THREADS, 0, s>>>(src.x, gamma, beta, n, H, eps, y, stats);
+      ok = launch_pdl(ln_fwd_persist_kernel<4>, dim3(pgrid), dim3(LN_THREADS), 0, s, 1, src.x, gamma, beta, n, H, eps,
+                      y, stats) == cudaSuccess;
+    if (!ok) return MB_ERR_CUDA;
     MB_CHECK_LAUNCH();
     return MB_OK;
   }

@@ -13,6 +13,11 @@ namespace mb {
 static int g_sms[64];
 static std::once_flag g_sms_once[64];
 
+bool pdl_enabled() {
+  static const bool on = std::getenv("MB_NO_PDL") == nullptr;
+  return on;
+}
+
 int num_sms() {
   int dev = 0;
   cudaGetDevice(&dev);
