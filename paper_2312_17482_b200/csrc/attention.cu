@@ -113,9 +113,12 @@ __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const
   // one S barrier per TMEM S buffer: S(i+1) is committed before the softmax of unit i ends, so a
   // single barrier could run two phases ahead of a slow waiter (parity aliasing); same for O
   uint64_t* s_full = bars + 3;    // [2]
-  uint64_t* p_ready = bars + 5;   // 8 compute warps arrive per unit
-  uint64_t* o_full = bars + 6;    // [2]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 8);
+  // [2] by unit parity, 8 compute warps arrive per unit: S(i+1) is in TMEM before unit i's P is
+  // complete, so a fast warp pair can arrive for unit i+1 while a slow pair is still on unit i; a
+  // single barrier would count that arrival towards unit i's phase
+  uint64_t* p_ready = bars + 5;
+  uint64_t* o_full = bars + 7;    // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 9);
   __shared__ float rmax[2 * 128], rsum[2 * 128];  // half-row max / sum exchange of the two row threads
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -127,7 +130,8 @@ __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const
     for (int k = 0; k < FWD_NBUF; ++k) sm100::mbar_init(&load_full[k], 1);
     sm100::mbar_init(&s_full[0], 1);
     sm100::mbar_init(&s_full[1], 1);
-    sm100::mbar_init(p_ready, 8);
+    sm100::mbar_init(&p_ready[0], 8);
+    sm100::mbar_init(&p_ready[1], 8);
     sm100::mbar_init(&o_full[0], 1);
     sm100::mbar_init(&o_full[1], 1);
     sm100::fence_barrier_init();
@@ -193,7 +197,7 @@ __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const
           sm100::tc_fence_after();
           mma_s(i + 1);
         }
-        sm100::mbar_wait(p_ready, i & 1);
+        sm100::mbar_wait(&p_ready[i & 1], (i >> 1) & 1);
         sm100::tc_fence_after();
         mma_o(i);
         sm100::mbar_wait(&o_full[i & 1], (i >> 1) & 1);  // P V(i) done: data buffer i % FWD_NBUF is free
@@ -287,7 +291,7 @@ __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const
       sm100::fence_proxy_async_smem();
       sm100::tc_fence_before();
       __syncwarp();
-      if (lane == 0) sm100::mbar_arrive(p_ready);
+      if (lane == 0) sm100::mbar_arrive(&p_ready[i & 1]);
       // row sum of both halves; the two pair barriers per unit separate every rmax / rsum write
       // from the partner's previous read of it
       rsum[ch * 128 + r] = sum2.x + sum2.y;
@@ -393,9 +397,9 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
   uint64_t* kv_empty = bars + 4 + LF_NS;           // [LF_NS]
   uint64_t* s_full = bars + 4 + 2 * LF_NS;         // [2]
   uint64_t* pv_full = bars + 6 + 2 * LF_NS;        // [2] per tile: PV_g (and l_g) accumulated
-  uint64_t* p_ready = bars + 8 + 2 * LF_NS;        // 8 softmax warps
-  uint64_t* o_done = bars + 9 + 2 * LF_NS;         // [2] per unit: its last PV accumulated
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint64_t* p_ready = bars + 8 + 2 * LF_NS;        // [2] by tile parity, 8 softmax warps (see the short kernel)
+  uint64_t* o_done = bars + 10 + 2 * LF_NS;        // [2] per unit: its last PV accumulated
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 12 + 2 * LF_NS);
   __shared__ float rmax[2][2 * TILE];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -414,7 +418,8 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
       sm100::mbar_init(&kv_full[i], 1);
       sm100::mbar_init(&kv_empty[i], 1);
     }
-    sm100::mbar_init(p_ready, 8);
+    sm100::mbar_init(&p_ready[0], 8);
+    sm100::mbar_init(&p_ready[1], 8);
     sm100::fence_barrier_init();
   }
   for (int i = tid; i < ONES_BYTES / 16; i += LF_THREADS)  // bf16 1.0 = 0x3F80 (any swizzle of ones is ones)
@@ -495,7 +500,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
           if (j2 == 0) sm100::mbar_wait(&q_full[uc2 & 1], (uc2 >> 1) & 1);
           issue_s(g + 1, uc2, j2 == nkv2 - 1);
         }
-        sm100::mbar_wait(p_ready, g & 1);  // P_g in smem (S_g consumed)
+        sm100::mbar_wait(&p_ready[g & 1], (g >> 1) & 1);  // P_g in smem (S_g consumed)
         sm100::tc_fence_after();
         const uint32_t v = sKVa + (g % LF_NS) * 2 * TILE_BYTES + TILE_BYTES;
 #pragma unroll
@@ -627,7 +632,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
         sm100::fence_proxy_async_smem();
         sm100::tc_fence_before();
         __syncwarp();
-        if (lane == 0) sm100::mbar_arrive(p_ready);
+        if (lane == 0) sm100::mbar_arrive(&p_ready[g & 1]);
         if (jj == 0 && pend_u >= 0) {  // the previous unit's epilogue, its O staged in its last P buffer
           epilogue(pend_u, pend_uc, pend_m, sPa + ((g - 1) & 1) * P_BYTES);
           pend_u = -1;
