@@ -26,8 +26,14 @@ constexpr int BM = 128, BK = 64;
 constexpr int kSplitOverheadKb = 4;  // split-K cost model: one unit's fp32 flush ~ this many k-blocks
 constexpr int NUM_EPI_WARPS = 8;                     // two warps per TMEM lane quarter
 constexpr int NTHREADS = 128 + 32 * NUM_EPI_WARPS;  // warps 0-3: TMA, MMA, TMEM alloc, spare
-constexpr int SCR_ROW = 80;                          // scratch row: 32 bf16 (64 B) + 16 B pad (conflict-free)
+// per-warp epilogue scratch: 32 rows x 32 bf16 (64 B), 16-byte unit u of row r stored at unit
+// u ^ ((r >> 1) & 3): conflict-free both for row-wise access (lane = row, 8 rows per 128-byte phase)
+// and for the coalescing pattern (8 lanes = 2 rows x 4 units per phase)
+constexpr int SCR_ROW = 64;
 constexpr int SCR_BYTES = 32 * SCR_ROW;
+__device__ __forceinline__ uint32_t scr_at(uint32_t scr, int row, int unit) {
+  return scr + row * SCR_ROW + ((unit ^ ((row >> 1) & 3)) << 4);
+}
 
 template <int BN, int STAGES, int NSCR, int CG = 1, int ACC = 2>
 struct Cfg {
@@ -101,15 +107,15 @@ __device__ __forceinline__ void sts128(uint32_t a, const uint4& v) {
 }
 __device__ __forceinline__ void chunk_to_scr(uint32_t scr, const uint4 (&r)[4], int lane) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) sts128(scr + ((lane >> 2) + 8 * i) * SCR_ROW + (lane & 3) * 16, r[i]);
+  for (int i = 0; i < 4; ++i) sts128(scr_at(scr, (lane >> 2) + 8 * i, lane & 3), r[i]);
 }
 __device__ __forceinline__ void scr_row_read(uint32_t scr, int lane, float* v) {
 #pragma unroll
-  for (int j = 0; j < 4; ++j) bf16x8_to_f32(lds128(scr + lane * SCR_ROW + j * 16), v + 8 * j);
+  for (int j = 0; j < 4; ++j) bf16x8_to_f32(lds128(scr_at(scr, lane, j)), v + 8 * j);
 }
 __device__ __forceinline__ void scr_row_write(uint32_t scr, int lane, const float* v) {
 #pragma unroll
-  for (int j = 0; j < 4; ++j) sts128(scr + lane * SCR_ROW + j * 16, f32_to_bf16x8(v + 8 * j));
+  for (int j = 0; j < 4; ++j) sts128(scr_at(scr, lane, j), f32_to_bf16x8(v + 8 * j));
 }
 __device__ __forceinline__ void scr_to_global(uint32_t scr, bf16* base, int64_t ld, int row0, int M, int col, int N,
                                               int lane) {
@@ -118,7 +124,7 @@ __device__ __forceinline__ void scr_to_global(uint32_t scr, bf16* base, int64_t 
   for (int i = 0; i < 4; ++i) {
     const int rr = (lane >> 2) + 8 * i;
     const int row = row0 + rr;
-    const uint4 v = lds128(scr + rr * SCR_ROW + (lane & 3) * 16);
+    const uint4 v = lds128(scr_at(scr, rr, lane & 3));
     if (row < M && c < N) *reinterpret_cast<uint4*>(base + (int64_t)row * ld + c) = v;
   }
 }
@@ -533,8 +539,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               float a[16], g[16];
 #pragma unroll
               for (int j = 0; j < 2; ++j) {
-                bf16x8_to_f32(lds128(scrA + lane * SCR_ROW + (2 * h + j) * 16), a + 8 * j);
-                bf16x8_to_f32(lds128(scrB + lane * SCR_ROW + (2 * h + j) * 16), g + 8 * j);
+                bf16x8_to_f32(lds128(scr_at(scrA, lane, 2 * h + j)), a + 8 * j);
+                bf16x8_to_f32(lds128(scr_at(scrB, lane, 2 * h + j)), g + 8 * j);
               }
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
@@ -544,8 +550,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               }
 #pragma unroll
               for (int j = 0; j < 2; ++j) {
-                sts128(scrA + lane * SCR_ROW + (2 * h + j) * 16, f32_to_bf16x8(a + 8 * j));
-                sts128(scrB + lane * SCR_ROW + (2 * h + j) * 16, f32_to_bf16x8(g + 8 * j));
+                sts128(scr_at(scrA, lane, 2 * h + j), f32_to_bf16x8(a + 8 * j));
+                sts128(scr_at(scrB, lane, 2 * h + j), f32_to_bf16x8(g + 8 * j));
               }
             }
             __syncwarp();
