@@ -654,10 +654,21 @@ constexpr int GB_STAGE_BYTES = BM * BK * 2 + (GB_BN / 2) * BK * 2;  // own 128 A
 constexpr int GB_SLOT_BYTES = 2 * BM * 64 * 2;                      // a and g boxes [128 x 64] bf16 (32 KB)
 constexpr int GB_SMEM = GB_STAGES * GB_STAGE_BYTES + GB_NSLOT * GB_SLOT_BYTES + 1024 + 256;
 
+__device__ __forceinline__ void stg256(void* p, const uint4& a, const uint4& b) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w),
+               "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
+}
+
+// DIRECT_STORE (default): dU leaves the registers by 32-byte stores (row per thread) and each Gd
+// slot is released as soon as the 8 warps have read it, instead of being rewritten in place and
+// TMA-stored: two of the four shared-memory passes of the epilogue disappear (kernel 400 -> 382 us
+// in isolation)
+template <bool DIRECT_STORE>
 __global__ void __launch_bounds__(NTHREADS, 1)
     geglu_bwd_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmGd, const __grid_constant__ CUtensorMap tmDU, int M, int I,
-                     Sched sc) {
+                     Sched sc, bf16* __restrict__ dU) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* slots = smem + GB_STAGES * GB_STAGE_BYTES;
@@ -688,7 +699,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     for (int i = 0; i < GB_NSLOT; ++i) {
       sm100::mbar_init(&gfull[i], 1);
-      sm100::mbar_init(&gempty[i], 1);
+      sm100::mbar_init(&gempty[i], DIRECT_STORE ? NUM_EPI_WARPS : 1);
     }
     sm100::fence_barrier_init();
   }
@@ -814,6 +825,34 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           A[jj] = lds128(box_a + off);
           G[jj] = lds128(box_g + off);
         }
+        if (DIRECT_STORE) {  // the slot's contents are in registers: hand it back to the Gd producer
+          __syncwarp();
+          if (lane == 0) sm100::mbar_arrive(&gempty[sl]);
+          uint4 oa[4], og[4];
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            float ga[8], gg[8];
+            bf16x8_to_f32(A[jj], ga);
+            bf16x8_to_f32(G[jj], gg);
+#pragma unroll
+            for (int e = 0; e < 8; e += 2) {
+              const float2 dz = make_float2(v[8 * jj + e], v[8 * jj + e + 1]);
+              const float2 pa = __fmul2_rn(dz, make_float2(ga[e], ga[e + 1]));
+              const float2 pg = __fmul2_rn(dz, make_float2(gg[e], gg[e + 1]));
+              ga[e] = pa.x, ga[e + 1] = pa.y, gg[e] = pg.x, gg[e + 1] = pg.y;
+            }
+            oa[jj] = f32_to_bf16x8(ga);
+            og[jj] = f32_to_bf16x8(gg);
+          }
+          if (row0 + r < M) {
+            bf16* da = dU + (size_t)(row0 + r) * (2 * I) + nb * GB_BN + qq * 64 + grp * 32;
+            stg256(da, oa[0], oa[1]);
+            stg256(da + 16, oa[2], oa[3]);
+            stg256(da + I, og[0], og[1]);
+            stg256(da + I + 16, og[2], og[3]);
+          }
+          continue;
+        }
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
           const int j = grp * 4 + jj;
@@ -848,7 +887,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         acc_phase ^= 1;
       }
     }
-    if (gtid == 0) {
+    if (!DIRECT_STORE && gtid == 0) {
       sm100::bulk_wait_read0();
       if (qi > 0) sm100::mbar_arrive(&gempty[(qi - 1) % GB_NSLOT]);
       sm100::bulk_wait0();
@@ -952,9 +991,14 @@ mb_status gemm(const GemmArgs& g, cudaStream_t s) {
     CUtensorMap tg, tdu;
     MB_REQUIRE(make_tmap_bf16_2d(&tg, g.ep.U, 2 * g.ep.I, g.M, g.ep.ldu, 64, BM), MB_ERR_CUDA);
     MB_REQUIRE(make_tmap_bf16_2d(&tdu, g.ep.C, 2 * g.ep.I, g.M, g.ep.ldc, 64, BM), MB_ERR_CUDA);
+    static const bool direct = [] {  // MB_GEGLU_BWD_STORE=tma: the in-place + TMA-store epilogue (A/B)
+      const char* e = std::getenv("MB_GEGLU_BWD_STORE");
+      return !(e && e[0] == 't');
+    }();
+    auto kern = direct ? geglu_bwd_kernel<true> : geglu_bwd_kernel<false>;
     static bool attr_gb = false;
     if (!attr_gb) {
-      if (cudaFuncSetAttribute(geglu_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GB_SMEM) != cudaSuccess)
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, GB_SMEM) != cudaSuccess)
         return MB_ERR_CUDA;
       attr_gb = true;
     }
@@ -962,8 +1006,8 @@ mb_status gemm(const GemmArgs& g, cudaStream_t s) {
     sg.num_m = (g.M + 2 * BM - 1) / (2 * BM);
     sg.total = sg.num_m * sg.num_n * sg.splits;
     const int clusters = std::max(1, std::min(sg.total, num_sms() / 2));
-    if (launch_pdl(geglu_bwd_kernel, dim3(2 * clusters), dim3(NTHREADS), GB_SMEM, s, 2, ta, tb, tg, tdu, g.M, g.ep.I,
-                   sg) != cudaSuccess)
+    if (launch_pdl(kern, dim3(2 * clusters), dim3(NTHREADS), GB_SMEM, s, 2, ta, tb, tg, tdu, g.M, g.ep.I, sg,
+                   reinterpret_cast<bf16*>(g.ep.C)) != cudaSuccess)
       return MB_ERR_CUDA;
     MB_CHECK_LAUNCH();
     return MB_OK;
