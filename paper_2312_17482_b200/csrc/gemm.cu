@@ -137,6 +137,12 @@ __device__ __forceinline__ void emit_chunk(uint32_t scr, const float* v, bf16* b
   __syncwarp();
 }
 
+__device__ __forceinline__ void stg256(void* p, const uint4& a, const uint4& b) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w),
+               "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
+}
+
 __device__ __forceinline__ void cp_async16(uint32_t smem_dst, const void* gsrc) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_dst), "l"(gsrc) : "memory");
 }
@@ -339,6 +345,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               for (int e = 0; e < 8; ++e) dbs[e] += f[e];
             }
           }
+          sm100::fence_proxy_async_smem();  // generic reads of the stage before the producer's next TMA write
           __syncwarp();
           if (lane == 0) sm100::mbar_arrive(&empty[rstage]);
           if (++rstage == STAGES) {
@@ -654,12 +661,6 @@ constexpr int GB_STAGE_BYTES = BM * BK * 2 + (GB_BN / 2) * BK * 2;  // own 128 A
 constexpr int GB_SLOT_BYTES = 2 * BM * 64 * 2;                      // a and g boxes [128 x 64] bf16 (32 KB)
 constexpr int GB_SMEM = GB_STAGES * GB_STAGE_BYTES + GB_NSLOT * GB_SLOT_BYTES + 1024 + 256;
 
-__device__ __forceinline__ void stg256(void* p, const uint4& a, const uint4& b) {
-  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w),
-               "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
-               : "memory");
-}
-
 // DIRECT_STORE (default): dU leaves the registers by 32-byte stores (row per thread) and each Gd
 // slot is released as soon as the 8 warps have read it, instead of being rewritten in place and
 // TMA-stored: two of the four shared-memory passes of the epilogue disappear (kernel 400 -> 382 us
@@ -825,9 +826,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           A[jj] = lds128(box_a + off);
           G[jj] = lds128(box_g + off);
         }
-        if (DIRECT_STORE) {  // the slot's contents are in registers: hand it back to the Gd producer
-          __syncwarp();
-          if (lane == 0) sm100::mbar_arrive(&gempty[sl]);
+        if (DIRECT_STORE) {
           uint4 oa[4], og[4];
 #pragma unroll
           for (int jj = 0; jj < 4; ++jj) {
@@ -844,6 +843,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             oa[jj] = f32_to_bf16x8(ga);
             og[jj] = f32_to_bf16x8(gg);
           }
+          // the slot's values have been consumed (the products depend on every loaded register):
+          // order the generic-proxy reads before the producer's next TMA write, then hand it back
+          sm100::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) sm100::mbar_arrive(&gempty[sl]);
           if (row0 + r < M) {
             bf16* da = dU + (size_t)(row0 + r) * (2 * I) + nb * GB_BN + qq * 64 + grp * 32;
             stg256(da, oa[0], oa[1]);
