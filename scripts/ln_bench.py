@@ -2,7 +2,8 @@
 import torch
 from paper_2312_17482_b200 import _lib as L
 
-T, H = 65536, 768
+import os
+T, H = int(os.environ.get("LN_T", 65536)), 768
 x = torch.randn(T, H, device="cuda").to(torch.bfloat16)
 dy = torch.randn(T, H, device="cuda").to(torch.bfloat16)
 g = torch.ones(H, dtype=torch.bfloat16, device="cuda")
