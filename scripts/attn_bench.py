@@ -36,4 +36,8 @@ def timed(fn, reps=20):
 
 tf = timed(lambda: L.attention_forward(qkv, cu, B, nnz, Lq, heads, d, sl, O, lse))
 tb = timed(lambda: L.attention_backward(qkv, O, dO, lse, cu, B, nnz, Lq, heads, d, sl, dqkv, ws=ws, db_qkv=db))
-print(f"B={B} L={Lq}: attention fwd {tf:.1f} us, bwd (incl. prep/finish) {tb:.1f} us")
+fl_f = 4.0 * B * heads * Lq * Lq * d  # QK^T and PV: 2 L^2 d MACs per (sequence, head)
+fl_b = 2.5 * fl_f                      # S, dP, dV, dK, dQ
+byt_f = nnz * (3 * H * 2 + H * 2 + heads * 4)  # QKV in, O + LSE out
+print(f"B={B} L={Lq}: attention fwd {tf:.1f} us ({fl_f / tf / 1e6:.0f} TF/s, {byt_f / tf / 1e3:.0f} GB/s), "
+      f"bwd (incl. prep/finish) {tb:.1f} us ({fl_b / tb / 1e6:.0f} TF/s)")
