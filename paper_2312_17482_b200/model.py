@@ -189,8 +189,33 @@ class MosaicBert:
         x = (self.seed * 0x9E3779B97F4A7C15 + rank * 0xBF58476D1CE4E5B9 + micro_index * 0x94D049BB133111EB)
         return x & 0xFFFFFFFFFFFFFFFF
 
+    @staticmethod
+    def batch_meta(mask, labels) -> tuple[int, int, int]:
+        """(nnz, max_seqlen, n_masked) of a right-padded batch from HOST arrays (numpy or CPU
+        tensors): what mb_unpad_index / mb_mlm_select report, known before the batch is uploaded."""
+        m = torch.as_tensor(mask) != 0
+        lab = torch.as_tensor(labels)
+        return int(m.sum()), int(m.sum(1).max()) if m.numel() else 0, int(((lab != -100) & m).sum())
+
+    def check_meta(self):
+        """Verify the device-side index results of the last micro-step run with host_meta against
+        the host's numbers (deferred: called at the next micro-step and by train_step's caller at
+        its own sync points).  Raises on a mismatch or a device-reported error status."""
+        pend = getattr(self, "_meta_pending", None)
+        if pend is None:
+            return
+        self._meta_pending = None
+        ev, want = pend
+        ev.synchronize()
+        nnz, max_seqlen, status, n_m = (int(x) for x in self.meta_host.tolist())
+        if status != 0:
+            raise RuntimeError(f"batch rejected: {L.STATUS.get(status, status)}")
+        if (nnz, max_seqlen, n_m) != tuple(want):
+            raise RuntimeError(f"host batch metadata {tuple(want)} != device {(nnz, max_seqlen, n_m)}")
+
     def micro_step(self, ids: torch.Tensor, mask: torch.Tensor, labels: torch.Tensor, inv_norm: float = 1.0,
-                   allreduce: bool = False, timers: dict | None = None, drop_seed: int | None = None):
+                   allreduce: bool = False, timers: dict | None = None, drop_seed: int | None = None,
+                   host_meta: tuple[int, int, int] | None = None):
         """Forward + backward of one micro-batch (device int32 [B, L] tensors, right-padded).
         Gradients accumulate (+=) into the buckets.  With dropout, layer l uses mb_dropout(p,
         drop_seed or seed_of(micro-step), stream=l).  Returns (nnz, n_masked)."""
@@ -207,11 +232,21 @@ class MosaicBert:
                                                         L._p(self.meta), L._stream()))
         L._ck("mb_mlm_select", L.lib().mb_mlm_select(L._p(labels), L._p(self.indices), B * Lq, self.d.vocab,
                                                       L._p(self.rows), L._p(self.labs), L._p(self.meta), L._stream()))
+        self.check_meta()  # the previous micro-step's deferred check (its copy is long complete)
         self.meta_host.copy_(self.meta, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        nnz, max_seqlen, status, n_m = (int(x) for x in self.meta_host.tolist())
-        if status != 0:
-            raise RuntimeError(f"batch rejected: {L.STATUS.get(status, status)}")
+        if host_meta is None:  # read {nnz, max_seqlen, status, n_masked} back (one 16-byte D2H sync)
+            torch.cuda.current_stream().synchronize()
+            nnz, max_seqlen, status, n_m = (int(x) for x in self.meta_host.tolist())
+            if status != 0:
+                raise RuntimeError(f"batch rejected: {L.STATUS.get(status, status)}")
+        else:  # sizes known on the host: no sync; the device's numbers are verified later.  They must
+            # be exact (batch_meta of the same host arrays): kernels are sized by them
+            nnz, max_seqlen, n_m = (int(x) for x in host_meta)
+            if not (0 <= n_m <= nnz <= B * Lq and 0 <= max_seqlen <= Lq):
+                raise ValueError(f"host_meta {tuple(host_meta)} impossible for a {B}x{Lq} batch")
+            ev = torch.cuda.Event()
+            ev.record()
+            self._meta_pending = (ev, (nnz, max_seqlen, n_m))
         self.masked_count += n_m
         if nnz == 0:
             return 0, 0
@@ -309,14 +344,18 @@ class MosaicBert:
 
     # ------------------------------------------------------------------ whole optimizer step
     def train_step(self, micro_batches: Sequence[tuple], global_masked: int | None = None, lr: float | None = None,
-                   optimizer: bool = True):
+                   optimizer: bool = True, host_meta: Sequence[tuple] | None = None):
         """micro_batches: [(ids, mask, labels), ...] device int32 tensors.  Gradients are summed over
         micro-steps (+= contract) and ranks (allreduce on the last micro-step), then scaled by
-        1/N_masked_global in the optimizer.  Returns the device loss tensor (mean CE)."""
+        1/N_masked_global in the optimizer.  Returns the device loss tensor (mean CE).
+        host_meta: optional [batch_meta(mask, labels), ...] computed from the host copy of each
+        micro-batch; the step then never waits for the device (its index results are verified one
+        micro-step later, check_meta())."""
         self.zero_grad()
         n = len(micro_batches)
         for i, (ids, mask, labels) in enumerate(micro_batches):
-            self.micro_step(ids, mask, labels, inv_norm=1.0, allreduce=(i == n - 1))
+            self.micro_step(ids, mask, labels, inv_norm=1.0, allreduce=(i == n - 1),
+                            host_meta=host_meta[i] if host_meta is not None else None)
         if global_masked is None:
             global_masked = self.global_masked(self.masked_count)
         self.wait_grads()

@@ -201,3 +201,27 @@ def test_loss_zero_decoder_is_lnV():
     batch = synth.make_batch("C1", 8)
     loss, _ = _model_parity(synth.TINY, batch, params, tol_loss=1e-5)
     assert abs(loss - np.log(128)) < 1e-5
+
+
+def test_host_meta_path_matches_and_is_checked():
+    """train_step(host_meta=...) skips the device->host read of the unpad results: same loss and
+    gradients as the synchronising path; a wrong host value is caught by the deferred check."""
+    params = synth.make_model_params(synth.TINY, 6, "stress")
+    dims = synth.TINY
+    model = mb.MosaicBert(mb.ModelDims(dims.hidden, dims.heads, dims.intermediate, dims.vocab, 1, dims.ln_eps), params)
+    batch = synth.make_batch("C1", 41)
+    dev = tuple(to_dev(batch[k], I32) for k in ("input_ids", "attention_mask", "labels"))
+    meta = mb.MosaicBert.batch_meta(batch["attention_mask"], batch["labels"])
+    assert meta[0] == int(batch["attention_mask"].sum())
+    l0 = float(model.train_step([dev], optimizer=False).item())
+    g0 = model.grads_numpy()
+    l1 = float(model.train_step([dev], optimizer=False, host_meta=[meta]).item())
+    model.check_meta()
+    g1 = model.grads_numpy()
+    assert abs(l0 - l1) <= 1e-6 * abs(l0)
+    for k in ("emb", "w_t", "b_dec"):
+        check(f"host_meta.d{k}", g1[k], g0[k], max_rel=1e-5, min_cos=0.999999)
+    # (one masked row fewer: a wrong value that still only touches valid rows)
+    model.train_step([dev], optimizer=False, host_meta=[(meta[0], meta[1], meta[2] - 1)])
+    with pytest.raises(RuntimeError, match="host batch metadata"):
+        model.check_meta()
