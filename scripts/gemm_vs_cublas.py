@@ -31,6 +31,16 @@ for name, N, K in (("fwd_qkv", 2304, Hd), ("fwd_o", Hd, Hd), ("fwd_2", Hd, I)):
     o = timeit(lambda: _lib.gemm(T, N, K, A, K, 0, W, K, 0, C, N))
     r = timeit(lambda: torch.matmul(A, W.t(), out=C))
     report(name, 2 * T * N * K, o, r)
+# out-proj / down-proj as in the layer: + bias + residual (E2)
+for name, N, K in (("fwd_o+res", Hd, Hd), ("fwd_2+res", Hd, I)):
+    A = torch.randn(T, K, device=dev, dtype=bf)
+    W = torch.randn(N, K, device=dev, dtype=bf) * 0.02
+    bias = torch.randn(N, device=dev, dtype=bf)
+    R = torch.randn(T, N, device=dev, dtype=bf)
+    C = torch.empty(T, N, device=dev, dtype=bf)
+    o = timeit(lambda: _lib.gemm(T, N, K, A, K, 0, W, K, 0, C, N, bias=bias, residual=R, ldr=N))
+    r = timeit(lambda: torch.addmm(bias, A, W.t(), out=C).add_(R))
+    report(name, 2 * T * N * K, o, r)
 for name, N, K in (("dx_qkv", Hd, 2304), ("dx_1v", Hd, 2 * I), ("dx_o", Hd, Hd)):
     dY = torch.randn(T, K, device=dev, dtype=bf)
     W = torch.randn(K, N, device=dev, dtype=bf) * 0.02
