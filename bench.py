@@ -317,8 +317,8 @@ def main():
 
     if rank == 0:
         tok_s = value
-        mfu_ds = 6.0 * n_params * tok_s / (args.gpus * PEAK_DATASHEET)
-        mfu_meas = 6.0 * n_params * tok_s / (args.gpus * pk["bf16_tflops"] * 1e12)
+        mfu_ds = 6.0 * n_params * tok_s / (world * PEAK_DATASHEET)
+        mfu_meas = 6.0 * n_params * tok_s / (world * pk["bf16_tflops"] * 1e12)
         line = {
             "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
