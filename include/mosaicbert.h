@@ -284,6 +284,12 @@ MB_API mb_status mb_mlm_loss(const mb_dims* d, const mb_head_params* p, const mb
 MB_API mb_status mb_adamw_step(float* master, float* m, float* v, const float* g, mb_bf16* w_bf16, int64_t n, float lr,
                         float beta1, float beta2, float eps, float weight_decay, float grad_scale, int32_t step,
                         mb_stream_t s);
+/* The same update with the gradient scale read from DEVICE memory: g' = grad_scale * (*grad_scale_dev) g.
+ * Lets a data-parallel step normalise by the global masked-token count (R18) that an in-stream
+ * allreduce produced, without reading it back to the host.  grad_scale_dev: device fp32 scalar. */
+MB_API mb_status mb_adamw_step_dev(float* master, float* m, float* v, const float* g, mb_bf16* w_bf16, int64_t n,
+                            float lr, float beta1, float beta2, float eps, float weight_decay, float grad_scale,
+                            const float* grad_scale_dev, int32_t step, mb_stream_t s);
 
 /* ---------------------------------------------------------------------------------------------
  * F3 — baselines for the paper's throughput ablations; not on the training path.

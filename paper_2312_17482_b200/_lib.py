@@ -86,6 +86,7 @@ _SIGS = {
     "mb_mlm_loss": (C.c_int, [C.POINTER(Dims), C.POINTER(HeadPtrs), P, I32, P, P, I32, F32, P, P, P,
                               C.POINTER(HeadPtrs), P, SZ, P]),
     "mb_adamw_step": (C.c_int, [P, P, P, P, P, I64, F32, F32, F32, F32, F32, F32, I32, P]),
+    "mb_adamw_step_dev": (C.c_int, [P, P, P, P, P, I64, F32, F32, F32, F32, F32, F32, P, I32, P]),
     "mb_layernorm_forward_f32": (C.c_int, [P, P, P, I32, I32, F32, P, P, P]),
     "mb_layernorm_backward_f32": (C.c_int, [P, P, P, P, I32, I32, P, P, P, P, P]),
     "mb_geglu_naive_forward": (C.c_int, [P, P, I64, P, P]),
@@ -338,7 +339,12 @@ def mlm_loss(d: Dims, head, y, nnz, masked_rows, labels, n_masked, inv_norm, los
                                          _stream()))
 
 
-def adamw_step(master, m, v, g, w_bf16, lr, beta1, beta2, eps, weight_decay, grad_scale, step):
+def adamw_step(master, m, v, g, w_bf16, lr, beta1, beta2, eps, weight_decay, grad_scale, step, grad_scale_dev=None):
+    if grad_scale_dev is not None:  # device fp32 scalar multiplying grad_scale (no host read-back)
+        _ck("mb_adamw_step_dev", lib().mb_adamw_step_dev(_p(master), _p(m), _p(v), _p(g), _p(w_bf16), master.numel(),
+                                                         lr, beta1, beta2, eps, weight_decay, grad_scale,
+                                                         _p(grad_scale_dev), step, _stream()))
+        return
     _ck("mb_adamw_step", lib().mb_adamw_step(_p(master), _p(m), _p(v), _p(g), _p(w_bf16), master.numel(), lr, beta1,
                                              beta2, eps, weight_decay, grad_scale, step, _stream()))
 

@@ -55,7 +55,9 @@ __global__ void sum_kernel(const float* __restrict__ x, int n, float scale, floa
 
 __global__ void adamw_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
                              const float* __restrict__ g, bf16* __restrict__ w, int64_t n, float lr, float b1, float b2,
-                             float eps, float wd, float gscale, float bc1, float bc2) {
+                             float eps, float wd, float gscale, const float* __restrict__ gscale_dev, float bc1,
+                             float bc2) {
+  if (gscale_dev) gscale *= *gscale_dev;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const float gi = g[i] * gscale;
     const float mi = b1 * m[i] + (1.f - b1) * gi;
@@ -82,9 +84,11 @@ __device__ __forceinline__ float adamw_one(float& p, float& m, float& v, float g
 }
 __global__ void adamw4_kernel(float4* __restrict__ p, float4* __restrict__ m, float4* __restrict__ v,
                               const float4* __restrict__ g, uint2* __restrict__ w, int64_t n4, float lr, float b1,
-                              float b2, float eps, float wd, float gscale, float bc1, float bc2) {
+                              float b2, float eps, float wd, float gscale, const float* __restrict__ gscale_dev,
+                              float bc1, float bc2) {
   pdl_wait();
   pdl_trigger();
+  if (gscale_dev) gscale *= *gscale_dev;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
     float4 pi = p[i], mi = m[i], vi = v[i];
     const float4 gi = g[i];
@@ -261,9 +265,9 @@ mb_status mb_embed_backward(const mb_dims* d, const int32_t* ids, const int32_t*
                           d->hidden, d_ln_g, d_ln_b, d_type_emb, reinterpret_cast<cudaStream_t>(s));
 }
 
-mb_status mb_adamw_step(float* master, float* m, float* v, const float* g, mb_bf16* w_bf16, int64_t n, float lr,
-                        float beta1, float beta2, float eps, float weight_decay, float grad_scale, int32_t step,
-                        mb_stream_t s) {
+mb_status mb_adamw_step_dev(float* master, float* m, float* v, const float* g, mb_bf16* w_bf16, int64_t n,
+                            float lr, float beta1, float beta2, float eps, float weight_decay, float grad_scale,
+                            const float* grad_scale_dev, int32_t step, mb_stream_t s) {
   if (!master || !m || !v || !g || !w_bf16 || n < 0 || step < 1) return MB_ERR_INVALID_ARG;
   if (n == 0) return MB_OK;
   const float bc1 = 1.f - powf(beta1, (float)step), bc2 = 1.f - powf(beta2, (float)step);
@@ -278,7 +282,7 @@ mb_status mb_adamw_step(float* master, float* m, float* v, const float* g, mb_bf
     if (mb::launch_pdl(mb::adamw4_kernel, dim3(grid), dim3(256), 0, st, 1, reinterpret_cast<float4*>(master),
                        reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v),
                        reinterpret_cast<const float4*>(g), reinterpret_cast<uint2*>(w_bf16), n4, lr, beta1, beta2,
-                       eps, weight_decay, grad_scale, bc1, bc2) != cudaSuccess)
+                       eps, weight_decay, grad_scale, grad_scale_dev, bc1, bc2) != cudaSuccess)
       return MB_ERR_CUDA;
     MB_CHECK_LAUNCH();
     done = n4 * 4;
@@ -288,9 +292,16 @@ mb_status mb_adamw_step(float* master, float* m, float* v, const float* g, mb_bf
   const int grid = (int)std::min<int64_t>((rest + 255) / 256, 8 * mb::num_sms());
   mb::adamw_kernel<<<grid, 256, 0, st>>>(master + done, m + done, v + done, g + done,
                                          reinterpret_cast<bf16*>(w_bf16) + done, rest, lr, beta1, beta2, eps,
-                                         weight_decay, grad_scale, bc1, bc2);
+                                         weight_decay, grad_scale, grad_scale_dev, bc1, bc2);
   MB_CHECK_LAUNCH();
   return MB_OK;
+}
+
+mb_status mb_adamw_step(float* master, float* m, float* v, const float* g, mb_bf16* w_bf16, int64_t n, float lr,
+                        float beta1, float beta2, float eps, float weight_decay, float grad_scale, int32_t step,
+                        mb_stream_t s) {
+  return mb_adamw_step_dev(master, m, v, g, w_bf16, n, lr, beta1, beta2, eps, weight_decay, grad_scale, nullptr, step,
+                           s);
 }
 
 }  // extern "C"

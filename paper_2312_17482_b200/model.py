@@ -328,7 +328,7 @@ class MosaicBert:
         return self.lr_peak * (1.0 - 0.98 * (step - w) / (T - w))
 
     def optimizer_step(self, grad_scale: float, lr: float | None = None, betas=(0.9, 0.98), eps=1e-6,
-                       weight_decay: float = 1e-5):
+                       weight_decay: float = 1e-5, grad_scale_dev: torch.Tensor | None = None):
         """Decoupled AdamW (Table A1) over every bucket; rewrites the bf16 weights.  lr
         defaults to the schedule's value at this step; the decay factor handed to the kernel is
         (lr / lr_peak) * weight_decay, not multiplied by lr (reading R34)."""
@@ -340,7 +340,7 @@ class MosaicBert:
             if b.master is None:
                 b.init_optimizer()
             L.adamw_step(b.master, b.m, b.v, b.g, b.w, lr, betas[0], betas[1], eps, wd_step, grad_scale,
-                         self.step_count)
+                         self.step_count, grad_scale_dev=grad_scale_dev)
 
     # ------------------------------------------------------------------ whole optimizer step
     def train_step(self, micro_batches: Sequence[tuple], global_masked: int | None = None, lr: float | None = None,
@@ -356,8 +356,18 @@ class MosaicBert:
         for i, (ids, mask, labels) in enumerate(micro_batches):
             self.micro_step(ids, mask, labels, inv_norm=1.0, allreduce=(i == n - 1),
                             host_meta=host_meta[i] if host_meta is not None else None)
+        if global_masked is None and self._dp():
+            # R18 normaliser = the global masked count: summed by an in-stream allreduce and applied
+            # from device memory (AdamW's grad_scale_dev, the returned loss), never read back
+            t = torch.tensor([float(self.masked_count)], dtype=torch.float32, device=self.device)
+            dist.all_reduce(t, group=self.pg)
+            inv = 1.0 / t.clamp_(min=1.0)
+            self.wait_grads()
+            if optimizer:
+                self.optimizer_step(1.0, lr=lr, grad_scale_dev=inv)
+            return self.loss_sum * inv
         if global_masked is None:
-            global_masked = self.global_masked(self.masked_count)
+            global_masked = self.masked_count
         self.wait_grads()
         scale = 1.0 / max(global_masked, 1)
         if optimizer:

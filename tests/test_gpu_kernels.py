@@ -364,8 +364,9 @@ def test_geglu_naive_baseline():
 
 
 # ------------------------------------------------------------------------------------ F1 AdamW
+@pytest.mark.parametrize("dev_scale", [False, True])
 @pytest.mark.parametrize("n", [1, 7, 1000, 9450243])
-def test_adamw_step_vs_oracle(n):
+def test_adamw_step_vs_oracle(n, dev_scale):
     """mb_adamw_step (decoupled AdamW, R34) against the fp64 oracle over three steps with a changing
     lr / decay factor and a grad_scale: fp32 master, moments within fp32 rounding of the oracle; the
     bf16 weight copy is exactly the RNE of the kernel's own master.  n covers the scalar tail and a
@@ -390,7 +391,11 @@ def test_adamw_step_vs_oracle(n):
             gmax = max(gmax, float(np.abs(gr).max()) / 3.0)
             gv.copy_(torch.from_numpy(gr))
             lr, wd, gs = 5e-4 * t, 1e-5 * t, 1.0 / 3.0
-            L.adamw_step(pv, mv, vv, gv, wv, lr, 0.9, 0.98, 1e-6, wd, gs, t)
+            if dev_scale:  # the data-parallel form: scale read from device memory (mb_adamw_step_dev)
+                L.adamw_step(pv, mv, vv, gv, wv, lr, 0.9, 0.98, 1e-6, wd, 1.0, t,
+                             grad_scale_dev=torch.tensor([gs], dtype=torch.float32, device="cuda"))
+            else:
+                L.adamw_step(pv, mv, vv, gv, wv, lr, 0.9, 0.98, 1e-6, wd, gs, t)
             ow, om, ov = O.adamw_step(ow, om, ov, gr.astype(np.float64), t, lr=lr, wd_step=wd, grad_scale=np.float32(gs))
         torch.cuda.synchronize()
         pg = pv.double().cpu().numpy()
