@@ -225,3 +225,21 @@ def test_host_meta_path_matches_and_is_checked():
     model.train_step([dev], optimizer=False, host_meta=[(meta[0], meta[1], meta[2] - 1)])
     with pytest.raises(RuntimeError, match="host batch metadata"):
         model.check_meta()
+
+
+def test_training_memorises_one_batch():
+    """End-to-end sanity of the whole train step (forward, backward, allreduce-free DP path,
+    decoupled AdamW with the bf16 weight copy): repeated steps on one tiny batch drive its MLM
+    loss far below the initial ln(V)-level value."""
+    params = synth.make_model_params(synth.TINY, 11, "bert")
+    dims = synth.TINY
+    model = mb.MosaicBert(mb.ModelDims(dims.hidden, dims.heads, dims.intermediate, dims.vocab, 1, dims.ln_eps),
+                          params, lr_peak=3e-3)
+    batch = synth.make_batch("C1", 2024, B=8)
+    dev = tuple(to_dev(batch[k], I32) for k in ("input_ids", "attention_mask", "labels"))
+    meta = mb.MosaicBert.batch_meta(batch["attention_mask"], batch["labels"])
+    losses = [float(model.train_step([dev], host_meta=[meta]).item()) for _ in range(80)]
+    model.check_meta()
+    assert all(np.isfinite(losses))
+    assert losses[0] > 0.8 * np.log(dims.vocab), losses[0]
+    assert losses[-1] < 0.25 * losses[0], (losses[0], losses[-1])
