@@ -270,6 +270,11 @@ class MosaicBert:
         if t is not None:
             t[1].record()
         handles = []
+        if allreduce and self._dp():
+            # the R18 normaliser first (known since the index step): its allreduce precedes the
+            # gradient buckets in NCCL's order, so the optimizer never waits behind the last bucket
+            t = torch.tensor([float(self.masked_count)], dtype=torch.float32, device=self.device)
+            self._count = (t, dist.all_reduce(t, group=self.pg, async_op=True))
         if allreduce:
             handles.append(self._allreduce(self.head_bucket))
         # backward through the layers; each bucket's allreduce is issued as soon as it is final
@@ -291,10 +296,11 @@ class MosaicBert:
         return dist.is_available() and dist.is_initialized() and dist.get_world_size(self.pg) > 1
 
     def _allreduce(self, b: Bucket):
-        """Sum one fp32 gradient bucket over the data-parallel ranks (async; A12)."""
+        """Sum one fp32 gradient bucket over the data-parallel ranks (async; A12).  Returns
+        (bucket, work) or None."""
         if not self._dp():
             return None
-        return dist.all_reduce(b.g, op=dist.ReduceOp.SUM, group=self.pg, async_op=True)
+        return b, dist.all_reduce(b.g, op=dist.ReduceOp.SUM, group=self.pg, async_op=True)
 
     def allreduce_grads(self):
         """Issue the allreduce of every bucket (used when gradients were produced elsewhere)."""
@@ -309,7 +315,7 @@ class MosaicBert:
         return int(t.item())
 
     def wait_grads(self):
-        for h in getattr(self, "_handles", []):
+        for _, h in getattr(self, "_handles", []):
             h.wait()
         self._handles = []
 
@@ -336,7 +342,16 @@ class MosaicBert:
         if lr is None:
             lr = self.lr_at(self.step_count)
         wd_step = (lr / self.lr_peak) * weight_decay
-        for b in self.buckets:
+        # buckets whose allreduce is still in flight are updated in the order it was issued, each
+        # right after its own reduction (stream wait, no host sync): the last bucket's transfer
+        # overlaps the other buckets' updates
+        pending = getattr(self, "_handles", [])
+        self._handles = []
+        order = [b for b, _ in pending] + [b for b in self.buckets if all(b is not pb for pb, _ in pending)]
+        works = {id(b): w for b, w in pending}
+        for b in order:
+            if id(b) in works:
+                works[id(b)].wait()
             if b.master is None:
                 b.init_optimizer()
             L.adamw_step(b.master, b.m, b.v, b.g, b.w, lr, betas[0], betas[1], eps, wd_step, grad_scale,
@@ -357,14 +372,15 @@ class MosaicBert:
             self.micro_step(ids, mask, labels, inv_norm=1.0, allreduce=(i == n - 1),
                             host_meta=host_meta[i] if host_meta is not None else None)
         if global_masked is None and self._dp():
-            # R18 normaliser = the global masked count: summed by an in-stream allreduce and applied
-            # from device memory (AdamW's grad_scale_dev, the returned loss), never read back
-            t = torch.tensor([float(self.masked_count)], dtype=torch.float32, device=self.device)
-            dist.all_reduce(t, group=self.pg)
-            inv = 1.0 / t.clamp_(min=1.0)
-            self.wait_grads()
+            # R18 normaliser = the global masked count, allreduced in-stream by the last micro-step
+            # and applied from device memory (AdamW's grad_scale_dev, the returned loss): never read back
+            t, work = self._count
+            work.wait()
+            inv = 1.0 / t.clamp(min=1.0)
             if optimizer:
-                self.optimizer_step(1.0, lr=lr, grad_scale_dev=inv)
+                self.optimizer_step(1.0, lr=lr, grad_scale_dev=inv)  # waits each bucket's reduction
+            else:
+                self.wait_grads()
             return self.loss_sum * inv
         if global_masked is None:
             global_masked = self.masked_count

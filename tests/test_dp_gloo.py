@@ -74,3 +74,32 @@ def test_dp_world2_gradient_equivalence(tmp_path):
         assert np.array_equal(r0[f"L0_{k}"], r1[f"L0_{k}"]), k  # every rank holds the same reduced gradient
     for k in ("emb", "type_emb", "lne_g", "w_t", "b_t", "lnh_g", "b_dec"):
         assert np.allclose(r0[k], full[k], rtol=1e-5, atol=1e-6 * np.abs(full[k]).max()), k
+
+
+def test_optimizer_waits_each_bucket_in_issue_order(monkeypatch):
+    """The DP optimizer step updates the buckets in the order their allreduces were issued (head,
+    layers last to first, embedding), each only after waiting for its own reduction, so the last
+    bucket's transfer overlaps the other updates; buckets without a pending reduction follow."""
+    from paper_2312_17482_b200 import _lib as L
+    from paper_2312_17482_b200.model import ModelDims, MosaicBert
+    d = synth.TINY
+    model = MosaicBert(ModelDims(d.hidden, d.heads, d.intermediate, d.vocab, 2), synth.make_model_params(d, 1, n_layers=2),
+                       device="cpu")
+    log = []
+
+    class Work:
+        def __init__(self, name):
+            self.name = name
+
+        def wait(self):
+            log.append(("wait", self.name))
+
+    names = {id(model.head_bucket): "head", id(model.emb_bucket): "emb",
+             id(model.layer_buckets[0]): "L0", id(model.layer_buckets[1]): "L1"}
+    model._handles = [(b, Work(names[id(b)])) for b in (model.head_bucket, model.layer_buckets[1], model.emb_bucket)]
+    monkeypatch.setattr(L, "adamw_step", lambda master, *a, **k: log.append(("adam", next(
+        n for b in model.buckets for n in [names[id(b)]] if b.master is master))))
+    model.optimizer_step(1.0)
+    assert log == [("wait", "head"), ("adam", "head"), ("wait", "L1"), ("adam", "L1"), ("wait", "emb"), ("adam", "emb"),
+                   ("adam", "L0")]
+    assert model._handles == []
