@@ -190,7 +190,11 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # NCCL on a high-priority stream: when a persistent kernel's CTAs retire, the block scheduler
+        # hands the freed SMs to a pending bucket allreduce before the next compute kernel
+        opts = dist.ProcessGroupNCCL.Options()
+        opts.is_high_priority_stream = True
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local), pg_options=opts)
     from paper_2312_17482_b200 import _lib as L
     from paper_2312_17482_b200.model import ModelDims, MosaicBert, param_count
 
