@@ -188,13 +188,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    backend = os.environ.get("MB_DIST_BACKEND", "nccl")  # "gloo": functional test of the N > 1 path only
+    if backend != "nccl":
+        local %= torch.cuda.device_count()  # (ranks may share a GPU; gloo kernels never wait on each other)
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 and backend == "nccl":
         # NCCL on a high-priority stream: when a persistent kernel's CTAs retire, the block scheduler
         # hands the freed SMs to a pending bucket allreduce before the next compute kernel
         opts = dist.ProcessGroupNCCL.Options()
         opts.is_high_priority_stream = True
         dist.init_process_group("nccl", device_id=torch.device("cuda", local), pg_options=opts)
+    elif world > 1:
+        dist.init_process_group(backend)
     from paper_2312_17482_b200 import _lib as L
     from paper_2312_17482_b200.model import ModelDims, MosaicBert, param_count
 
@@ -269,7 +274,7 @@ def main():
     tok_step = sum_over_ranks(float(np.mean([tokens[i % nb] for i in range(args.steps)])))
     value = tok_step * args.steps / (ms_max / 1e3)
     clocks = clk.summary()
-    loss_val = float(loss.item())
+    loss_val = sum_over_ranks(float(loss.item()))  # each rank holds its share of the global mean (R18)
 
     # ---- roofline of the dominant kernel (GeGLU up-projection GEMM, A8), timed inside the steps
     pk, src = peaks()
