@@ -39,3 +39,60 @@ def test_bench_two_ranks_gloo():
     # the loss is the global mean over both ranks' masked tokens: near ln V at BERT init
     assert 9.0 < line["loss"] < 11.5, line["loss"]
     assert line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
+
+
+def _dp_worker(rank, world, port, out_dir):
+    import numpy as np
+    import torch.distributed as dist
+    import synth
+    import paper_2312_17482_b200 as mb
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    d = synth.TINY
+    params = synth.make_model_params(d, 5, "stress", n_layers=2)
+    batch = synth.make_batch("C1", 91, B=8)
+    per = 8 // world
+    sh = {k: v[rank * per:(rank + 1) * per] for k, v in batch.items()}
+    model = mb.MosaicBert(mb.ModelDims(d.hidden, d.heads, d.intermediate, d.vocab, 2, d.ln_eps), params)
+    dev = tuple(torch.from_numpy(sh[k]).cuda() for k in ("input_ids", "attention_mask", "labels"))
+    loss = model.train_step([dev], optimizer=False)
+    torch.cuda.synchronize()
+    model.wait_grads()
+    n_all = int(((batch["labels"] != -100) & (batch["attention_mask"] != 0)).sum())
+    g = model.grads_numpy(scale=1.0 / n_all)
+    np.savez(os.path.join(out_dir, f"g{rank}.npz"), loss=float(loss.item()),
+             **{f"L{i}_{k}": v for i, lg in enumerate(g["layers"]) for k, v in lg.items()},
+             **{k: v for k, v in g.items() if k != "layers"})
+    dist.destroy_process_group()
+
+
+def test_dp_two_ranks_gradient_equals_full_batch(tmp_path):
+    """SURVEY §8e invariant with the real kernels: two ranks (gloo, one GPU) on half a batch each,
+    gradients summed by the product's bucket allreduce and normalised by the global masked count,
+    equal the single-process gradient of the whole batch (fp32 reassociation only)."""
+    import numpy as np
+    import torch.multiprocessing as mp
+    import synth
+    import paper_2312_17482_b200 as mb
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    mp.start_processes(_dp_worker, args=(2, _port(), str(tmp_path)), nprocs=2, start_method="spawn")
+    d = synth.TINY
+    params = synth.make_model_params(d, 5, "stress", n_layers=2)
+    batch = synth.make_batch("C1", 91, B=8)
+    model = mb.MosaicBert(mb.ModelDims(d.hidden, d.heads, d.intermediate, d.vocab, 2, d.ln_eps), params)
+    dev = tuple(torch.from_numpy(batch[k]).cuda() for k in ("input_ids", "attention_mask", "labels"))
+    loss = float(model.train_step([dev], optimizer=False).item())
+    n_all = int(((batch["labels"] != -100) & (batch["attention_mask"] != 0)).sum())
+    full = model.grads_numpy(scale=1.0 / n_all)
+    r0, r1 = (np.load(tmp_path / f"g{r}.npz") for r in range(2))
+    assert abs(float(r0["loss"]) + float(r1["loss"]) - loss) <= 1e-5 * abs(loss)
+    for i, lg in enumerate(full["layers"]):
+        for k, v in lg.items():
+            assert np.array_equal(r0[f"L{i}_{k}"], r1[f"L{i}_{k}"]), k  # both ranks hold the same sum
+            scale = max(float(np.abs(v).max()), 1e-30)
+            assert float(np.abs(r0[f"L{i}_{k}"] - v).max()) <= 2e-5 * scale, (i, k)
+    for k in ("emb", "type_emb", "lne_g", "lne_b", "w_t", "b_t", "lnh_g", "lnh_b", "b_dec"):
+        scale = max(float(np.abs(full[k]).max()), 1e-30)
+        assert float(np.abs(r0[k] - full[k]).max()) <= 2e-5 * scale, k
