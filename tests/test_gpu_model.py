@@ -243,3 +243,12 @@ def test_training_memorises_one_batch():
     assert all(np.isfinite(losses))
     assert losses[0] > 0.8 * np.log(dims.vocab), losses[0]
     assert losses[-1] < 0.25 * losses[0], (losses[0], losses[-1])
+
+
+def test_model_step_with_empty_rows():
+    """Zero-length rows inside a batch (R5: allowed, they have no queries): the packed stream skips
+    them in every kernel (attention units, index scans, head) and the step matches the oracle."""
+    params = synth.make_model_params(synth.TINY, 12, "stress")
+    batch = synth.make_batch("C1", 512, B=6, lengths=np.array([16, 0, 5, 0, 1, 9]))
+    assert batch["attention_mask"][1].sum() == 0 and batch["attention_mask"][3].sum() == 0
+    _model_parity(synth.TINY, batch, params)
