@@ -252,3 +252,11 @@ def test_model_step_with_empty_rows():
     batch = synth.make_batch("C1", 512, B=6, lengths=np.array([16, 0, 5, 0, 1, 9]))
     assert batch["attention_mask"][1].sum() == 0 and batch["attention_mask"][3].sum() == 0
     _model_parity(synth.TINY, batch, params)
+
+
+def test_model_step_large_dims_one_layer():
+    """MosaicBERT-Large widths (H = 1024, 16 heads, GLU 4096, V = 30528) through embedding (the
+    H = 1024 embedding backward with its 48 KB shared-memory accumulators), one layer and the head."""
+    params = synth.make_model_params(synth.LARGE, 13, "bert", n_layers=1)
+    batch = synth.make_batch("C3", 5013, B=4)
+    _model_parity(synth.LARGE, batch, params)
