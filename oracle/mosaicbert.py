@@ -10,7 +10,7 @@ import math
 import numpy as np
 from scipy.special import erf
 
-from .philox import dropout_keep
+from .philox import dropout_keep, dropout_scale
 
 __all__ = [
     "MB_OK", "MB_ERR_MASK_LAYOUT", "IGNORE",
@@ -196,18 +196,20 @@ def _split_heads(x, n):
 
 
 def dropout_masks(mask, H, dropout):
-    """Padded [B, L, H] keep/(1-p) multipliers of the two F2 dropout sites (R32) for one layer:
+    """Padded [B, L, H] keep/P(keep) multipliers of the two F2 dropout sites (R32) for one layer:
     the packed row of real position (b, l) is its rank in row-major order (P:147 packing), pad
-    positions get 0.  dropout = dict(p, seed, stream) (stream = layer index) or None -> (1, 1)."""
+    positions get 0.  dropout = dict(p, seed, stream) (stream = layer index) or None -> (1, 1);
+    an optional dropout["rows"] gives the packed row of each real position (row-major order) when
+    the batch is a subset of a larger packed micro-batch."""
     if not dropout or dropout.get("p", 0.0) == 0.0:
         return 1.0, 1.0
     mk = np.asarray(mask).astype(bool)
     T = int(mk.sum())
     out = []
     for site in (0, 1):
-        keep = dropout_keep(T, H, dropout["p"], dropout["seed"], dropout["stream"], site)
+        keep = dropout_keep(T, H, dropout["p"], dropout["seed"], dropout["stream"], site, dropout.get("rows"))
         d = np.zeros(mk.shape + (H,))
-        d[mk] = keep / (1.0 - dropout["p"])
+        d[mk] = keep * dropout_scale(dropout["p"])
         out.append(d)
     return out[0], out[1]
 

@@ -10,7 +10,10 @@ regenerate exactly the mask the kernels use:
     counter = (f >> 3, t, 2*stream + site, 0),  key = (seed mod 2^32, seed >> 32)
     w = Philox4x32_10(counter, key)                   (4 x 32-bit words -> 8 features)
     u = 16-bit field (f & 1) of word (f & 7) >> 1     (uniform on 0..65535)
-    keep(t, f) = u >= round(p * 65536);  dropout(v) = v * keep / (1 - p)
+    keep(t, f) = u >= thr = round(p * 65536);  dropout(v) = v * keep * 65536 / (65536 - thr)
+
+The rescale is 1 / P(keep) for u uniform on 0..65535 (inverted dropout: E[dropout(v)] = v); it
+equals 1 / (1 - p) exactly when 65536 p is an integer.
 
 site 0 = attention output projection (A6), site 1 = FFN down-projection (A9).
 """
@@ -51,10 +54,16 @@ def dropout_threshold(p: float) -> int:
     return int(round(p * 65536.0))
 
 
-def dropout_keep(T: int, H: int, p: float, seed: int, stream: int, site: int) -> np.ndarray:
-    """bool [T, H]: keep(t, f) for packed rows t = 0..T-1 and features f = 0..H-1 (R32)."""
+def dropout_scale(p: float) -> float:
+    """Inverted-dropout rescale 1 / P(keep) = 65536 / (65536 - thr) (so E[keep * scale] = 1)."""
+    return 65536.0 / (65536.0 - dropout_threshold(p))
+
+
+def dropout_keep(T: int, H: int, p: float, seed: int, stream: int, site: int, rows=None) -> np.ndarray:
+    """bool [T, H]: keep(t, f) for packed rows t = 0..T-1 (or t = rows[i], i < T, when the rows are
+    a subset of a larger packed stream) and features f = 0..H-1 (R32)."""
     thr = dropout_threshold(p)
-    t = np.arange(T, dtype=np.uint64)[:, None]
+    t = (np.arange(T, dtype=np.uint64) if rows is None else np.asarray(rows, dtype=np.uint64))[:, None]
     fb = np.arange((H + 7) // 8, dtype=np.uint64)[None, :]
     ctr = np.stack(np.broadcast_arrays(fb, t, np.uint64(2 * stream + site), np.uint64(0)), axis=-1)
     key = np.array([seed & MASK32, (seed >> 32) & MASK32], dtype=np.uint64)

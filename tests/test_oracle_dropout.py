@@ -102,3 +102,20 @@ def test_dropout_layer_fd_and_mask_effect():
             fd = (fp - fm) / 2e-5
             worst = max(worst, abs(g[k][ix] - fd) / max(1.0, abs(fd)))
     assert worst < 1e-6, worst
+
+
+def test_dropout_scale_is_inverse_keep_probability():
+    """Inverted dropout (R32): a kept value is scaled by 1 / P(keep), P(keep) = (65536 - thr) / 65536
+    for a uniform 16-bit u, so E[drop(v)] = v for every p; equal to 1 / (1 - p) when 65536 p is an
+    integer (p = 1/2, 1/4), and 65536 / 58982 (not 1 / 0.9) at the paper's p = 0.1."""
+    from oracle.philox import dropout_scale
+    assert dropout_scale(0.5) == 2.0 and dropout_scale(0.25) == 65536.0 / 49152.0
+    assert dropout_scale(0.1) == 65536.0 / 58982.0 and dropout_scale(0.0) == 1.0
+    u = np.arange(65536)
+    for p in (0.1, 0.3, 1.0 / 3.0):
+        assert abs(float(np.sum(u >= dropout_threshold(p))) * dropout_scale(p) - 65536.0) < 1e-9
+    # the oracle layer applies exactly keep * scale
+    mask = synth.mask_from_lengths(np.array([5, 3]), 5)
+    D0, _ = O.dropout_masks(mask, 16, dict(p=0.1, seed=3, stream=0))
+    vals = np.unique(D0[mask.astype(bool)])
+    assert set(vals.tolist()) <= {0.0, 65536.0 / 58982.0}
