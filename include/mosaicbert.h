@@ -5,7 +5,8 @@
  *
  * Conventions (all entry points):
  *  - Pointers marked "device" are CUDA device pointers owned by the caller (allocated by torch in
- *    the Python layer).  The library keeps no device state and allocates nothing.
+ *    the Python layer).  The library keeps no device state and allocates nothing: every scratch
+ *    buffer is a caller workspace sized by an mb_*_workspace_bytes() query.
  *  - Every device call is ordered on the given stream `s` (a cudaStream_t; NULL = legacy default)
  *    and never synchronises the host.  Results are visible after the stream reaches them.
  *  - bf16 tensors are raw bfloat16 bit patterns (uint16_t), row-major, densely packed unless a
@@ -13,10 +14,14 @@
  *  - Gradients are fp32 and ACCUMULATED (+=): the caller zeroes them once per optimizer step, so
  *    gradient accumulation over micro-steps is free ("float32 for gradient accumulation").
  *  - Host-checkable argument errors return a status immediately and launch nothing.  Data-dependent
- *    errors (mask layout, label range) are written to a device status word (meta[2]) that the caller
- *    reads at its own sync point.  Launch failures return MB_ERR_CUDA.  No C++ exception crosses
+ *    errors (mask layout, token-id range, label range) are written to a device status word (meta[2])
+ *    that the caller reads at its own sync point.  Launch failures return MB_ERR_CUDA.  Every entry
+ *    point that touches the device returns MB_ERR_ARCH (and launches nothing) when the current
+ *    device is not sm_100 (B200): the library carries sm_100a SASS only.  No C++ exception crosses
  *    the ABI.
- *  - Calls are reentrant; the only global state is a per-device attribute cache (SM count).
+ *  - Calls are reentrant and may run concurrently on different streams (each call uses only the
+ *    buffers passed to it); the only global state is a per-device attribute cache (SM count,
+ *    architecture) and the instrumentation counters below.
  */
 #ifndef MOSAICBERT_H_
 #define MOSAICBERT_H_
@@ -47,7 +52,8 @@ typedef enum {
   MB_ERR_LABEL_RANGE = 5, /* device-reported: label not in [0, V)                                    */
   MB_ERR_WORKSPACE = 6,   /* workspace smaller than mb_*_workspace_bytes(...)                        */
   MB_ERR_ARCH = 7,        /* device is not sm_100 (B200)                                             */
-  MB_ERR_CUDA = 8         /* CUDA launch / runtime error                                             */
+  MB_ERR_CUDA = 8,        /* CUDA launch / runtime error                                             */
+  MB_ERR_TOKEN_RANGE = 9  /* device-reported: a real token's id is not in [0, V) (A3 reads E_tok[id]) */
 } mb_status;
 
 MB_API const char* mb_status_string(int status);
@@ -81,24 +87,40 @@ MB_API mb_status mb_alibi_slopes(int32_t heads, float* host_out);
  * A1 — unpad index ("concatenate all the examples from a minibatch into a single sequence of
  * batch size 1").
  *   mask       device int32[B*L], 1 = real token, right-padded rows (R6).
+ *   ids        device int32[B*L] token ids, or NULL: if given, every REAL position's id is checked
+ *              against [0, vocab) (the embedding gathers E_tok[id]; upstream nn.Embedding
+ *              raises on such ids) — a violation sets status MB_ERR_TOKEN_RANGE.
  *   cu_seqlens device int32[B+1] out: [0, cumsum(seqlen)]  (non-decreasing; zero-length rows OK, R5)
  *   indices    device int32[B*L] out (capacity): first nnz entries = ascending flat positions b*L+l
  *              with mask==1 (the flash-attention `unpad_input` convention)
- *   meta       device int32[4] out: {nnz, max_seqlen, status, (unchanged)}; status = MB_OK or
- *              MB_ERR_MASK_LAYOUT if some row is not a prefix of ones (indices are still the
- *              positions of the ones).
- * Bit-exact by construction (integer work).  Limits: B <= 65536, L <= 65536. */
-MB_API mb_status mb_unpad_index(const int32_t* mask, int32_t B, int32_t L, int32_t* cu_seqlens, int32_t* indices,
-                         int32_t* meta, mb_stream_t s);
+ *   meta       device int32[4] out: {nnz, max_seqlen, status, (unchanged)}; status = MB_OK,
+ *              MB_ERR_MASK_LAYOUT if some row is not a prefix of ones (precedence; indices are still
+ *              the positions of the ones), else MB_ERR_TOKEN_RANGE for a bad id.
+ *   ws         device workspace of mb_unpad_workspace_bytes(B) bytes (per-row counts and status), or
+ *              NULL (then a single-CTA kernel does the whole scan: same results, slower at large B).
+ * Bit-exact by construction (integer work).  Limits: B <= 65536, L <= 65536.
+ * Errors: NULL mask/cu/indices/meta or B, L outside [1, 65536] -> MB_ERR_INVALID_ARG; ids given with
+ * vocab < 1 -> MB_ERR_CONFIG; ws_bytes too small -> MB_ERR_WORKSPACE. */
+MB_API size_t mb_unpad_workspace_bytes(int32_t B);
+MB_API mb_status mb_unpad_index(const int32_t* mask, const int32_t* ids, int32_t vocab, int32_t B, int32_t L,
+                                int32_t* cu_seqlens, int32_t* indices, int32_t* meta, void* ws, size_t ws_bytes,
+                                mb_stream_t s);
 
 /* MLM selection: among the packed tokens t < meta[0] (device nnz), select those
  * whose padded label labels[indices[t]] != -100.
  *   masked_rows   device int32[capacity] out: packed row ids t (ascending)
  *   masked_labels device int32[capacity] out: their labels
  *   meta          device int32[4] in/out: reads meta[0] (nnz); writes meta[3] = n_masked and sets
- *                 meta[2] = MB_ERR_LABEL_RANGE if a selected label is outside [0, vocab). */
+ *                 meta[2] = MB_ERR_LABEL_RANGE if a selected label is outside [0, vocab).
+ *   count_accum   device fp32 scalar or NULL: += n_masked (the R18 normaliser of an optimizer step is
+ *                 this sum over its micro-steps — and over the data-parallel ranks after an allreduce —
+ *                 so the loss scale never needs a device->host read).
+ *   ws            device workspace of mb_select_workspace_bytes(capacity) bytes, or NULL (single-CTA
+ *                 kernel).  Errors: ws_bytes too small -> MB_ERR_WORKSPACE. */
+MB_API size_t mb_select_workspace_bytes(int32_t capacity);
 MB_API mb_status mb_mlm_select(const int32_t* labels, const int32_t* indices, int32_t capacity, int32_t vocab,
-                        int32_t* masked_rows, int32_t* masked_labels, int32_t* meta, mb_stream_t s);
+                               int32_t* masked_rows, int32_t* masked_labels, int32_t* meta, float* count_accum,
+                               void* ws, size_t ws_bytes, mb_stream_t s);
 
 /* A2 — row gather / scatter between the padded [rows, H] and packed [n, H] layouts.
  *   gather : dst[t,:] = src[idx[t],:]                       (unpad)
@@ -208,11 +230,12 @@ typedef struct {
 
 /* F2 — feed-forward dropout ("we applied 0.1 dropout to the feedforward layers"; placement
  * and generator per reading R32): S1 = X + drop_0(C Wo^T + bo), S2 = Y1 + drop_1(Z W2^T + b2),
- * drop_s(v)[t, f] = v[t, f] * keep_s(t, f) / (1 - p).  keep is a pure function of (seed, stream,
+ * drop_s(v)[t, f] = v[t, f] * keep_s(t, f) / P(keep).  keep is a pure function of (seed, stream,
  * site s, packed row t, feature f): Philox-4x32-10 (Salmon et al., SC'11) with counter
  * (f >> 3, t, 2*stream + s, 0), key (seed & 0xffffffff, seed >> 32); the uniform of f is 16-bit
- * field (f & 1) of output word (f & 7) >> 1; kept iff >= round(65536 p).  The backward regenerates
- * the same mask (nothing is saved).  NULL or p == 0: no dropout.  p must be in [0, 1). */
+ * field (f & 1) of output word (f & 7) >> 1; kept iff >= thr = round(65536 p), and a kept value is
+ * scaled by 1 / P(keep) = 65536 / (65536 - thr) (inverted dropout, unbiased for every p).  The
+ * backward regenerates the same mask (nothing is saved).  NULL or p == 0: no dropout.  p in [0, 1). */
 typedef struct {
   float p;
   uint64_t seed;   /* one per micro-step (and rank) */
@@ -239,7 +262,9 @@ MB_API mb_status mb_dropout_mask(const mb_dropout* drop, int32_t site, int32_t r
 
 /* ---------------------------------------------------------------------------------------------
  * A3 — embedding (no position table): x0[t] = LN_e(E_tok[ids[indices[t]]] + E_type[0]).
- * ids device int32[B*L] (padded layout); x0 bf16 [nnz, H]; stats fp32 [nnz, 2] saved for backward. */
+ * ids device int32[B*L] (padded layout); x0 bf16 [nnz, H]; stats fp32 [nnz, 2] saved for backward.
+ * Ids outside [0, V) (V = d->vocab) are clamped so no access leaves E_tok / d_emb; mb_unpad_index
+ * reports them (MB_ERR_TOKEN_RANGE) when given the ids. */
 MB_API mb_status mb_embed_forward(const mb_dims* d, const int32_t* ids, const int32_t* indices, int32_t nnz,
                            const mb_bf16* emb, const mb_bf16* type_emb, const mb_bf16* ln_g, const mb_bf16* ln_b,
                            mb_bf16* x0, float* stats, mb_stream_t s);
@@ -269,6 +294,13 @@ MB_API mb_status mb_mlm_loss(const mb_dims* d, const mb_head_params* p, const mb
                       const int32_t* masked_rows, const int32_t* labels, int32_t n_masked, float inv_norm,
                       float* loss_sum, float* lse, mb_bf16* dy_top, const mb_head_grads* g, void* ws,
                       size_t ws_bytes, mb_stream_t s);
+
+/* R18 loss normaliser ("mean over labelled positions"; the mean is over the GLOBAL masked count
+ * N of the optimizer step): inv_out = 1 / max(N, 1), loss_out = loss_sum * inv_out, with N read from
+ * the device scalar `count` (mb_mlm_select's count_accum, allreduced over ranks) or, if count is
+ * NULL, the host value count_host.  Device fp32 scalars; either output may be NULL (not both). */
+MB_API mb_status mb_loss_normalize(const float* loss_sum, const float* count, float count_host, float* inv_out,
+                                   float* loss_out, mb_stream_t s);
 
 /* ---------------------------------------------------------------------------------------------
  * F1 — fused decoupled AdamW update (Table A1: beta=(0.9,0.98), eps=1e-6, wd 1e-5):

@@ -8,11 +8,11 @@ north_star entry points are re-exported under the paper's names: ``encoder_forwa
 from ._lib import (  # noqa: F401
     alibi_slopes, attention_backward, attention_forward, colsum, embed_backward, embed_forward, encoder_backward,
     encoder_forward, gather_rows, gemm, geglu_backward, geglu_forward, layernorm_backward, layernorm_forward, lib,
-    mlm_loss, mlm_select, scatter_rows, unpad_index,
+    loss_normalize, mlm_loss, mlm_select, scatter_rows, unpad_index,
 )
 from .model import ModelDims, MosaicBert, param_count  # noqa: F401
 
 __all__ = ["alibi_slopes", "unpad_index", "mlm_select", "gather_rows", "scatter_rows", "layernorm_forward",
            "layernorm_backward", "gemm", "geglu_forward", "geglu_backward", "attention_forward",
            "attention_backward", "colsum", "encoder_forward", "encoder_backward", "embed_forward",
-           "embed_backward", "mlm_loss", "ModelDims", "MosaicBert", "param_count", "lib"]
+           "embed_backward", "mlm_loss", "loss_normalize", "ModelDims", "MosaicBert", "param_count", "lib"]

@@ -25,7 +25,8 @@ SZ = C.c_size_t
 
 EPI_BF16, EPI_F32_ACC, EPI_F32, EPI_GELU_AUX = 0, 1, 2, 3
 STATUS = {0: "MB_OK", 1: "MB_ERR_INVALID_ARG", 2: "MB_ERR_CONFIG", 3: "MB_ERR_SHAPE", 4: "MB_ERR_MASK_LAYOUT",
-          5: "MB_ERR_LABEL_RANGE", 6: "MB_ERR_WORKSPACE", 7: "MB_ERR_ARCH", 8: "MB_ERR_CUDA"}
+          5: "MB_ERR_LABEL_RANGE", 6: "MB_ERR_WORKSPACE", 7: "MB_ERR_ARCH", 8: "MB_ERR_CUDA",
+          9: "MB_ERR_TOKEN_RANGE"}
 
 
 class Dims(C.Structure):
@@ -59,8 +60,11 @@ _SIGS = {
     "mb_launch_count": (C.c_ulonglong, []),
     "mb_probe_set": (C.c_int, [I32, P, I32, P]),
     "mb_alibi_slopes": (C.c_int, [I32, P]),
-    "mb_unpad_index": (C.c_int, [P, I32, I32, P, P, P, P]),
-    "mb_mlm_select": (C.c_int, [P, P, I32, I32, P, P, P, P]),
+    "mb_unpad_workspace_bytes": (SZ, [I32]),
+    "mb_unpad_index": (C.c_int, [P, P, I32, I32, I32, P, P, P, P, SZ, P]),
+    "mb_select_workspace_bytes": (SZ, [I32]),
+    "mb_mlm_select": (C.c_int, [P, P, I32, I32, P, P, P, P, P, SZ, P]),
+    "mb_loss_normalize": (C.c_int, [P, P, F32, P, P, P]),
     "mb_gather_rows": (C.c_int, [P, P, I32, I32, P, P]),
     "mb_scatter_rows": (C.c_int, [P, P, I32, I32, I32, P, P]),
     "mb_layernorm_forward": (C.c_int, [P, P, P, I32, I32, F32, P, P, P]),
@@ -176,24 +180,61 @@ def alibi_slopes(heads: int) -> np.ndarray:
     return out[:heads]
 
 
-def unpad_index(mask: torch.Tensor, meta: torch.Tensor | None = None):
-    """mask: cuda int32 [B, L] -> (cu_seqlens [B+1], indices [B*L] (first nnz valid), meta [4])."""
+def unpad_workspace_bytes(B: int) -> int:
+    return int(lib().mb_unpad_workspace_bytes(B))
+
+
+def select_workspace_bytes(capacity: int) -> int:
+    return int(lib().mb_select_workspace_bytes(capacity))
+
+
+def _ws(nbytes: int, device, ws):
+    """The caller-owned workspace of one call: `ws` if given (must be large enough), else a new one;
+    ws=False passes NULL (the single-CTA kernels)."""
+    if ws is False or nbytes == 0:
+        return None, 0
+    if ws is None:
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    return ws, ws.numel()
+
+
+def unpad_index(mask: torch.Tensor, meta: torch.Tensor | None = None, ids: torch.Tensor | None = None,
+                vocab: int = 0, ws=None, out=None):
+    """mask: cuda int32 [B, L] -> (cu_seqlens [B+1], indices [B*L] (first nnz valid), meta [4]).
+    ids (optional): token ids checked against [0, vocab) (MB_ERR_TOKEN_RANGE in meta[2])."""
     B, L = mask.shape
-    cu = torch.empty(B + 1, dtype=torch.int32, device=mask.device)
-    idx = torch.empty(B * L, dtype=torch.int32, device=mask.device)
+    if out is None:
+        cu = torch.empty(B + 1, dtype=torch.int32, device=mask.device)
+        idx = torch.empty(B * L, dtype=torch.int32, device=mask.device)
+    else:
+        cu, idx = out
     if meta is None:
         meta = torch.zeros(4, dtype=torch.int32, device=mask.device)
-    _ck("mb_unpad_index", lib().mb_unpad_index(_p(mask), B, L, _p(cu), _p(idx), _p(meta), _stream()))
+    w, nb = _ws(unpad_workspace_bytes(B), mask.device, ws)
+    _ck("mb_unpad_index", lib().mb_unpad_index(_p(mask), _p(ids), vocab, B, L, _p(cu), _p(idx), _p(meta), _p(w), nb,
+                                               _stream()))
     return cu, idx, meta
 
 
-def mlm_select(labels: torch.Tensor, indices: torch.Tensor, vocab: int, meta: torch.Tensor):
+def mlm_select(labels: torch.Tensor, indices: torch.Tensor, vocab: int, meta: torch.Tensor, count=None, ws=None,
+               out=None):
     cap = indices.numel()
-    rows = torch.empty(cap, dtype=torch.int32, device=labels.device)
-    labs = torch.empty(cap, dtype=torch.int32, device=labels.device)
+    if out is None:
+        rows = torch.empty(cap, dtype=torch.int32, device=labels.device)
+        labs = torch.empty(cap, dtype=torch.int32, device=labels.device)
+    else:
+        rows, labs = out
+    w, nb = _ws(select_workspace_bytes(cap), labels.device, ws)
     _ck("mb_mlm_select", lib().mb_mlm_select(_p(labels), _p(indices), cap, vocab, _p(rows), _p(labs), _p(meta),
-                                             _stream()))
+                                             _p(count), _p(w), nb, _stream()))
     return rows, labs
+
+
+def loss_normalize(loss_sum, count=None, count_host: float = 0.0, inv_out=None, loss_out=None):
+    """R18: inv_out = 1 / max(N, 1), loss_out = loss_sum * inv_out (N from the device `count` or
+    count_host)."""
+    _ck("mb_loss_normalize", lib().mb_loss_normalize(_p(loss_sum), _p(count), float(count_host), _p(inv_out),
+                                                     _p(loss_out), _stream()))
 
 
 def gather_rows(src, idx, n, dst):

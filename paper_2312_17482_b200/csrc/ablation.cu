@@ -208,6 +208,7 @@ mb_status mb_layernorm_forward_f32(const float* x, const mb_bf16* gamma, const m
   if (!x || !gamma || !beta || !y || !stats || n < 0 || H <= 0) return MB_ERR_INVALID_ARG;
   if (H % 8 || H > 1024) return MB_ERR_CONFIG;
   if (n == 0) return MB_OK;
+  MB_REQUIRE_ARCH();
   cudaStream_t s = reinterpret_cast<cudaStream_t>(s_);
   const int grid = std::max(1, std::min((n + AB_WARPS - 1) / AB_WARPS, 2 * num_sms()));
   const auto g = reinterpret_cast<const bf16*>(gamma);
@@ -229,6 +230,7 @@ mb_status mb_layernorm_backward_f32(const float* dy, const float* x, const float
   if (!dy || !x || !stats || !gamma || !dx || !dgamma || !dbeta || n < 0 || H <= 0) return MB_ERR_INVALID_ARG;
   if (H % 256 || H > 1024) return MB_ERR_CONFIG;
   if (n == 0) return MB_OK;
+  MB_REQUIRE_ARCH();
   cudaStream_t s = reinterpret_cast<cudaStream_t>(s_);
   const auto g = reinterpret_cast<const bf16*>(gamma);
   const int W = H / 256, threads = ABW_GROUPS * W * 32;
@@ -249,6 +251,7 @@ mb_status mb_geglu_naive_forward(const mb_bf16* ua, const mb_bf16* ug, int64_t c
   if (!ua || !ug || !z || count < 0) return MB_ERR_INVALID_ARG;
   if (count % 8) return MB_ERR_CONFIG;
   if (count == 0) return MB_OK;
+  MB_REQUIRE_ARCH();
   const int64_t n8 = count / 8;
   const int grid = (int)std::min<int64_t>((n8 + 255) / 256, 8 * num_sms());
   geglu_ew_fwd_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(s_)>>>(
@@ -263,6 +266,7 @@ mb_status mb_geglu_naive_backward(const mb_bf16* dz, const mb_bf16* ua, const mb
   if (!dz || !ua || !ug || !dua || !dug || count < 0) return MB_ERR_INVALID_ARG;
   if (count % 8) return MB_ERR_CONFIG;
   if (count == 0) return MB_OK;
+  MB_REQUIRE_ARCH();
   const int64_t n8 = count / 8;
   const int grid = (int)std::min<int64_t>((n8 + 255) / 256, 8 * num_sms());
   geglu_ew_bwd_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(s_)>>>(

@@ -94,7 +94,9 @@ DropArgs make_drop_args(const mb_dropout* dr, int site) {
   a.key1 = (uint32_t)(dr->seed >> 32);
   a.site = 2u * (uint32_t)dr->stream + (uint32_t)site;
   a.thr = (uint32_t)std::lround((double)dr->p * 65536.0);
-  a.scale = 1.0f / (1.0f - dr->p);
+  // inverted dropout: the scale is 1 / P(keep) with P(keep) = (65536 - thr) / 65536 exactly, so
+  // E[drop(v)] = v for every p (not only those with 65536 p integral)
+  a.scale = (float)(65536.0 / (65536.0 - (double)a.thr));
   return a;
 }
 
@@ -118,6 +120,7 @@ mb_status mb_dropout_mask(const mb_dropout* drop, int32_t site, int32_t rows, in
   if (!drop || !out || rows < 0 || cols < 0 || site < 0 || site > 1 || !drop_ok(drop)) return MB_ERR_INVALID_ARG;
   if (cols % 8) return MB_ERR_CONFIG;
   if (rows == 0 || cols == 0) return MB_OK;
+  MB_REQUIRE_ARCH();
   const int64_t groups = (int64_t)rows * (cols / 8);
   dropout_mask_kernel<<<(unsigned)((groups + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(s_)>>>(
       make_drop_args(drop, site), rows, cols, out);
@@ -134,6 +137,7 @@ mb_status mb_encoder_forward(const mb_dims* d, const mb_layer_params* p, const m
   if (pk->nnz < 0 || pk->batch < 0) return MB_ERR_INVALID_ARG;
   if (pk->max_seqlen > kMaxSeqlen) return MB_ERR_SHAPE;
   if (pk->nnz == 0) return MB_OK;
+  MB_REQUIRE_ARCH();
   cudaStream_t s = reinterpret_cast<cudaStream_t>(s_);
   const int T = pk->nnz, H = d->hidden, I = d->intermediate, nh = d->heads;
   Saved sv(reinterpret_cast<char*>(saved), T, H, I, nh);
@@ -194,6 +198,7 @@ mb_status mb_encoder_backward(const mb_dims* d, const mb_layer_params* p, const 
   if (pk->nnz < 0 || pk->batch < 0) return MB_ERR_INVALID_ARG;
   if (pk->max_seqlen > kMaxSeqlen) return MB_ERR_SHAPE;
   if (pk->nnz == 0) return MB_OK;
+  MB_REQUIRE_ARCH();
   cudaStream_t s = reinterpret_cast<cudaStream_t>(s_);
   const int T = pk->nnz, H = d->hidden, I = d->intermediate, nh = d->heads;
   Saved sv(reinterpret_cast<char*>(const_cast<void*>(saved)), T, H, I, nh);

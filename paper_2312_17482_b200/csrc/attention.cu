@@ -1506,6 +1506,7 @@ mb_status mb_attention_forward(const mb_bf16* qkv, const int32_t* cu_seqlens, in
                                float* lse, mb_stream_t s) {
   if (!qkv || !cu_seqlens || !slopes || !O || !lse || batch < 0 || nnz < 0) return MB_ERR_INVALID_ARG;
   if (heads <= 0) return MB_ERR_CONFIG;
+  MB_REQUIRE_ARCH();
   return mb::attention_fwd(reinterpret_cast<const bf16*>(qkv), cu_seqlens, batch, nnz, max_seqlen, heads, head_dim,
                            slopes, reinterpret_cast<bf16*>(O), lse, reinterpret_cast<cudaStream_t>(s));
 }
@@ -1521,6 +1522,7 @@ mb_status mb_attention_backward(const mb_bf16* qkv, const mb_bf16* O, const mb_b
   if (!qkv || !O || !dO || !lse || !cu_seqlens || !slopes || !dqkv || batch < 0 || nnz < 0)
     return MB_ERR_INVALID_ARG;
   if (heads <= 0) return MB_ERR_CONFIG;
+  MB_REQUIRE_ARCH();
   return mb::attention_bwd(reinterpret_cast<const bf16*>(qkv), reinterpret_cast<const bf16*>(O),
                            reinterpret_cast<const bf16*>(dO), lse, cu_seqlens, batch, nnz, max_seqlen, heads,
                            head_dim, slopes, reinterpret_cast<bf16*>(dqkv), db_qkv, ws, ws_bytes,

@@ -15,6 +15,12 @@ typedef __nv_bfloat162 bf162;
     if (e__ != cudaSuccess) return MB_ERR_CUDA;             \
   } while (0)
 
+// every entry point that touches the device: MB_ERR_ARCH on anything but sm_100 (B200)
+#define MB_REQUIRE_ARCH()                     \
+  do {                                        \
+    if (!mb::arch_ok()) return MB_ERR_ARCH;   \
+  } while (0)
+
 #define MB_REQUIRE(cond, code) \
   do {                         \
     if (!(cond)) return (code);\
@@ -204,7 +210,7 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 }
 
 int num_sms();  // cached per device (host)
-int* device_scratch(size_t n_ints);  // library-owned device scratch (host; nullptr on failure)
+bool arch_ok();  // host: the current device is sm_100 (the only SASS this library carries)
 void count_launch();  // host-side counter of kernel launches (mb_launch_count)
 // optional timing probe around one kernel site (mb_probe_set): records caller-provided CUDA events
 enum ProbeSite { PROBE_NONE = 0, PROBE_GEGLU_FWD = 1, PROBE_ATTN_FWD = 2, PROBE_ATTN_BWD = 3, PROBE_LN_FWD = 4 };

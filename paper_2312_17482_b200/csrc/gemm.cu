@@ -1040,6 +1040,8 @@ extern "C" mb_status mb_gemm(int32_t M, int32_t N, int32_t K, const mb_bf16* A, 
                              const mb_bf16* B, int64_t ldb, int32_t b_t, void* C, int64_t ldc, int32_t epilogue,
                              const mb_bf16* bias, const mb_bf16* residual, int64_t ldr, mb_bf16* aux, int64_t ldaux,
                              mb_stream_t s) {
+  MB_REQUIRE(A && B && C, MB_ERR_INVALID_ARG);
+  MB_REQUIRE_ARCH();
   mb::GemmArgs g;
   g.M = M, g.N = N, g.K = K;
   g.A = reinterpret_cast<const bf16*>(A), g.lda = lda, g.a_t = a_t != 0;
@@ -1061,6 +1063,7 @@ extern "C" mb_status mb_gemm(int32_t M, int32_t N, int32_t K, const mb_bf16* A, 
 extern "C" mb_status mb_gemm_wgrad(int32_t M, int32_t N, int32_t K, const mb_bf16* dY, int64_t lda, const mb_bf16* X,
                                    int64_t ldb, float* dW, int64_t ldc, float* db, mb_stream_t s) {
   MB_REQUIRE(dY && X && dW, MB_ERR_INVALID_ARG);
+  MB_REQUIRE_ARCH();
   mb::GemmArgs g;
   g.M = M, g.N = N, g.K = K;
   g.A = reinterpret_cast<const bf16*>(dY), g.lda = lda, g.a_t = true;
@@ -1072,6 +1075,7 @@ extern "C" mb_status mb_gemm_wgrad(int32_t M, int32_t N, int32_t K, const mb_bf1
 extern "C" mb_status mb_geglu_forward(const mb_bf16* X, int32_t n, int32_t H, int32_t I, const mb_bf16* w_1v,
                                       const mb_bf16* b_1v, mb_bf16* Gd, mb_bf16* Z, mb_stream_t s) {
   MB_REQUIRE(X && w_1v && b_1v && Gd && Z, MB_ERR_INVALID_ARG);
+  MB_REQUIRE_ARCH();
   mb::GemmArgs g;
   g.M = n, g.N = 2 * I, g.K = H;
   g.A = reinterpret_cast<const bf16*>(X), g.lda = H;
@@ -1087,6 +1091,7 @@ extern "C" mb_status mb_geglu_forward(const mb_bf16* X, int32_t n, int32_t H, in
 extern "C" mb_status mb_geglu_backward(const mb_bf16* dF, int32_t n, int32_t H, int32_t I, const mb_bf16* w_2,
                                        const mb_bf16* Gd, mb_bf16* dU, mb_stream_t s) {
   MB_REQUIRE(dF && w_2 && Gd && dU, MB_ERR_INVALID_ARG);
+  MB_REQUIRE_ARCH();
   mb::GemmArgs g;
   g.M = n, g.N = I, g.K = H;
   g.A = reinterpret_cast<const bf16*>(dF), g.lda = H;

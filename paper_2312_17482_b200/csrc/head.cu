@@ -53,6 +53,15 @@ __global__ void sum_kernel(const float* __restrict__ x, int n, float scale, floa
   }
 }
 
+// R18: the step's loss and gradient scale from the device-resident global masked count
+__global__ void loss_normalize_kernel(const float* __restrict__ loss_sum, const float* __restrict__ count,
+                                      float count_host, float* __restrict__ inv_out, float* __restrict__ loss_out) {
+  const float c = count ? *count : count_host;
+  const float inv = 1.f / fmaxf(c, 1.f);
+  if (inv_out) *inv_out = inv;
+  if (loss_out) *loss_out = *loss_sum * inv;
+}
+
 __global__ void adamw_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
                              const float* __restrict__ g, bf16* __restrict__ w, int64_t n, float lr, float b1, float b2,
                              float eps, float wd, float gscale, const float* __restrict__ gscale_dev, float bc1,
@@ -155,6 +164,7 @@ mb_status mb_mlm_loss(const mb_dims* d, const mb_head_params* p, const mb_bf16* 
   if (!d || !p || !y || !masked_rows || !labels || !loss_sum || !lse || !dy_top || !g || !ws) return MB_ERR_INVALID_ARG;
   if (n_masked < 0 || nnz < 0) return MB_ERR_INVALID_ARG;
   if (n_masked > nnz) return MB_ERR_SHAPE;
+  MB_REQUIRE_ARCH();
   const int H = d->hidden, V = d->vocab;
   if (V < 1 || H % 8) return MB_ERR_CONFIG;
   const int Vp = (V + 7) & ~7;  // dz row stride (P:174's 30522 is allowed; 30528 = 64 x 477 is the paper's choice)
@@ -241,10 +251,12 @@ mb_status mb_embed_forward(const mb_dims* d, const int32_t* ids, const int32_t* 
                            mb_bf16* x0, float* stats, mb_stream_t s) {
   if (!d || !ids || !indices || !emb || !type_emb || !ln_g || !ln_b || !x0 || !stats || nnz < 0)
     return MB_ERR_INVALID_ARG;
-  if (d->hidden % 8 || d->hidden > 1024) return MB_ERR_CONFIG;
+  if (d->hidden % 8 || d->hidden > 1024 || d->vocab < 1) return MB_ERR_CONFIG;
+  MB_REQUIRE_ARCH();
   mb::EmbedSrc e;
   e.ids = ids, e.indices = indices, e.emb = reinterpret_cast<const bf16*>(emb);
   e.type_emb = reinterpret_cast<const bf16*>(type_emb);
+  e.vocab = d->vocab;
   return mb::embed_ln_fwd(e, reinterpret_cast<const bf16*>(ln_g), reinterpret_cast<const bf16*>(ln_b), nnz, d->hidden,
                           d->ln_eps, reinterpret_cast<bf16*>(x0), stats, reinterpret_cast<cudaStream_t>(s));
 }
@@ -256,10 +268,12 @@ mb_status mb_embed_backward(const mb_dims* d, const int32_t* ids, const int32_t*
   if (!d || !ids || !indices || !emb || !type_emb || !ln_g || !stats || !dx0 || !d_emb || !d_type_emb || !d_ln_g ||
       !d_ln_b || nnz < 0)
     return MB_ERR_INVALID_ARG;
-  if (d->hidden % 8 || d->hidden > 1024) return MB_ERR_CONFIG;
+  if (d->hidden % 8 || d->hidden > 1024 || d->vocab < 1) return MB_ERR_CONFIG;
+  MB_REQUIRE_ARCH();
   mb::EmbedSrc e;
   e.ids = ids, e.indices = indices, e.emb = reinterpret_cast<const bf16*>(emb);
   e.type_emb = reinterpret_cast<const bf16*>(type_emb), e.d_emb = d_emb;
+  e.vocab = d->vocab;
   // d_type_emb[0] = sum over tokens of dv (every token has type 0, R17) == the LN "dsum"
   return mb::embed_ln_bwd(e, reinterpret_cast<const bf16*>(dx0), stats, reinterpret_cast<const bf16*>(ln_g), nnz,
                           d->hidden, d_ln_g, d_ln_b, d_type_emb, reinterpret_cast<cudaStream_t>(s));
@@ -270,6 +284,7 @@ mb_status mb_adamw_step_dev(float* master, float* m, float* v, const float* g, m
                             const float* grad_scale_dev, int32_t step, mb_stream_t s) {
   if (!master || !m || !v || !g || !w_bf16 || n < 0 || step < 1) return MB_ERR_INVALID_ARG;
   if (n == 0) return MB_OK;
+  MB_REQUIRE_ARCH();
   const float bc1 = 1.f - powf(beta1, (float)step), bc2 = 1.f - powf(beta2, (float)step);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
   const bool vec = ((reinterpret_cast<uintptr_t>(master) | reinterpret_cast<uintptr_t>(m) |
@@ -293,6 +308,16 @@ mb_status mb_adamw_step_dev(float* master, float* m, float* v, const float* g, m
   mb::adamw_kernel<<<grid, 256, 0, st>>>(master + done, m + done, v + done, g + done,
                                          reinterpret_cast<bf16*>(w_bf16) + done, rest, lr, beta1, beta2, eps,
                                          weight_decay, grad_scale, grad_scale_dev, bc1, bc2);
+  MB_CHECK_LAUNCH();
+  return MB_OK;
+}
+
+mb_status mb_loss_normalize(const float* loss_sum, const float* count, float count_host, float* inv_out,
+                            float* loss_out, mb_stream_t s) {
+  if (!loss_sum || (!inv_out && !loss_out)) return MB_ERR_INVALID_ARG;
+  MB_REQUIRE_ARCH();
+  mb::loss_normalize_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(s)>>>(loss_sum, count, count_host, inv_out,
+                                                                          loss_out);
   MB_CHECK_LAUNCH();
   return MB_OK;
 }

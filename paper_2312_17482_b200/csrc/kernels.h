@@ -67,6 +67,7 @@ struct EmbedSrc {
   const bf16* emb = nullptr;
   const bf16* type_emb = nullptr;
   float* d_emb = nullptr;  // backward: dv is red-added into d_emb[id]
+  int vocab = 1;           // ids are clamped to [0, vocab)
 };
 mb_status embed_ln_fwd(const EmbedSrc& e, const bf16* gamma, const bf16* beta, int n, int H, float eps, bf16* y,
                        float* stats, cudaStream_t s);

@@ -23,13 +23,15 @@ struct RowSrc {
   const int* indices;
   const bf16* emb;
   const bf16* type_emb;
+  int vocab;              // embed mode: ids are clamped to [0, vocab) (out-of-range ids are reported
+                          // by mb_unpad_index as MB_ERR_TOKEN_RANGE; the clamp keeps every access in bounds)
 };
 
 template <int VPL, bool EMBED>
 __device__ __forceinline__ void load_row(const RowSrc& src, int row, int H, int lane, float* v, int& id) {
   const bf16* base;
   if (EMBED) {
-    id = src.ids[src.indices[row]];
+    id = min(max(src.ids[src.indices[row]], 0), src.vocab - 1);
     base = src.emb + (size_t)id * H;
   } else {
     base = src.x + (size_t)row * H;
@@ -323,7 +325,8 @@ __global__ void __launch_bounds__(LNW_GROUPS * W * 32)
     r_end = min(n, r_begin + per);
     const int cnt = r_end - r_begin;
     if (threadIdx.x < EMB_HOT) hot[threadIdx.x] = -1;
-    for (int i = threadIdx.x; i < cnt; i += blockDim.x) sid[i] = src.ids[src.indices[r_begin + i]];
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x)
+      sid[i] = min(max(src.ids[src.indices[r_begin + i]], 0), src.vocab - 1);
     for (int i = threadIdx.x; i < EMB_HOT * H; i += blockDim.x) hacc[i] = 0.f;
     __syncthreads();
     for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
@@ -592,14 +595,14 @@ mb_status ln_bwd_dispatch(const RowSrc& src, const bf16* dy, const float* stats,
 
 mb_status layernorm_fwd(const bf16* x, const bf16* gamma, const bf16* beta, int n, int H, float eps, bf16* y,
                         float* stats, cudaStream_t s) {
-  RowSrc src{x, nullptr, nullptr, nullptr, nullptr};
+  RowSrc src{x, nullptr, nullptr, nullptr, nullptr, 0};
   return ln_fwd_dispatch<false>(src, gamma, beta, n, H, eps, y, stats, s);
 }
 
 mb_status layernorm_bwd(const bf16* dy, const bf16* x, const float* stats, const bf16* gamma, int n, int H,
                         const bf16* gelu_pre, bf16* dx, float* dgamma, float* dbeta, float* dsum, cudaStream_t s,
                         const DropArgs* drop, bf16* dxd) {
-  RowSrc src{x, nullptr, nullptr, nullptr, nullptr};
+  RowSrc src{x, nullptr, nullptr, nullptr, nullptr, 0};
   const DropArgs none;
   return ln_bwd_dispatch<false>(src, dy, stats, gamma, gelu_pre, n, H, dx, nullptr, dgamma, dbeta, dsum, s,
                                 drop ? *drop : none, dxd);
@@ -607,13 +610,13 @@ mb_status layernorm_bwd(const bf16* dy, const bf16* x, const float* stats, const
 
 mb_status embed_ln_fwd(const EmbedSrc& e, const bf16* gamma, const bf16* beta, int n, int H, float eps, bf16* y,
                        float* stats, cudaStream_t s) {
-  RowSrc src{nullptr, e.ids, e.indices, e.emb, e.type_emb};
+  RowSrc src{nullptr, e.ids, e.indices, e.emb, e.type_emb, e.vocab};
   return ln_fwd_dispatch<true>(src, gamma, beta, n, H, eps, y, stats, s);
 }
 
 mb_status embed_ln_bwd(const EmbedSrc& e, const bf16* dy, const float* stats, const bf16* gamma, int n, int H,
                        float* dgamma, float* dbeta, float* dsum, cudaStream_t s) {
-  RowSrc src{nullptr, e.ids, e.indices, e.emb, e.type_emb};
+  RowSrc src{nullptr, e.ids, e.indices, e.emb, e.type_emb, e.vocab};
   return ln_bwd_dispatch<true>(src, dy, stats, gamma, nullptr, n, H, nullptr, e.d_emb, dgamma, dbeta, dsum, s);
 }
 
@@ -639,6 +642,7 @@ mb_status mb_layernorm_forward(const mb_bf16* x, const mb_bf16* gamma, const mb_
                                float eps, mb_bf16* y, float* stats, mb_stream_t s) {
   if (!x || !gamma || !beta || !y || !stats || n < 0 || H <= 0) return MB_ERR_INVALID_ARG;
   if (H % 8 || H > 1024) return MB_ERR_CONFIG;
+  MB_REQUIRE_ARCH();
   return mb::layernorm_fwd(reinterpret_cast<const bf16*>(x), reinterpret_cast<const bf16*>(gamma),
                            reinterpret_cast<const bf16*>(beta), n, H, eps, reinterpret_cast<bf16*>(y), stats,
                            reinterpret_cast<cudaStream_t>(s));
@@ -649,6 +653,7 @@ mb_status mb_layernorm_backward(const mb_bf16* dy, const mb_bf16* x, const float
                                 float* dbeta, float* dsum, mb_stream_t s) {
   if (!dy || !x || !stats || !gamma || !dx || !dgamma || !dbeta || n < 0 || H <= 0) return MB_ERR_INVALID_ARG;
   if (H % 8 || H > 1024) return MB_ERR_CONFIG;
+  MB_REQUIRE_ARCH();
   return mb::layernorm_bwd(reinterpret_cast<const bf16*>(dy), reinterpret_cast<const bf16*>(x), stats,
                            reinterpret_cast<const bf16*>(gamma), n, H, reinterpret_cast<const bf16*>(gelu_pre),
                            reinterpret_cast<bf16*>(dx), dgamma, dbeta, dsum, reinterpret_cast<cudaStream_t>(s));
@@ -656,6 +661,7 @@ mb_status mb_layernorm_backward(const mb_bf16* dy, const mb_bf16* x, const float
 
 mb_status mb_colsum(const mb_bf16* x, int32_t n, int32_t C, float* out, mb_stream_t s) {
   if (!x || !out || n < 0 || C < 0) return MB_ERR_INVALID_ARG;
+  MB_REQUIRE_ARCH();
   return mb::colsum(reinterpret_cast<const bf16*>(x), n, C, out, reinterpret_cast<cudaStream_t>(s));
 }
 

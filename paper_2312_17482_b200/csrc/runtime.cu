@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <atomic>
+#include <cstdlib>
 #include <mutex>
 #include "common.cuh"
 #include "tma.h"
@@ -30,25 +31,19 @@ int num_sms() {
   return g_sms[dev];
 }
 
-// small library-owned device scratch (per device, grown on demand, never freed): per-block
-// counts of the multi-CTA scans.  Grown outside any stream capture (first calls of a process).
-static std::mutex g_scratch_mu;
-static int* g_scratch[64] = {};
-static size_t g_scratch_n[64] = {};
-int* device_scratch(size_t n_ints) {
+// MB_ERR_ARCH: the SASS in this library is sm_100a only (B200).  Cached per device.
+static int g_arch[64];
+static std::once_flag g_arch_once[64];
+bool arch_ok() {
   int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return nullptr;
-  std::lock_guard<std::mutex> lk(g_scratch_mu);
-  if (g_scratch_n[dev] < n_ints) {
-    if (g_scratch[dev]) cudaFree(g_scratch[dev]);
-    g_scratch[dev] = nullptr;
-    g_scratch_n[dev] = 0;
-    const size_t n = std::max<size_t>(n_ints, 1 << 16);
-    if (cudaMalloc(&g_scratch[dev], n * sizeof(int)) != cudaSuccess) return nullptr;
-    g_scratch_n[dev] = n;
-  }
-  return g_scratch[dev];
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
+  std::call_once(g_arch_once[dev], [dev] {
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    g_arch[dev] = (major == 10 && minor == 0) ? 1 : 0;
+  });
+  return g_arch[dev] == 1;
 }
 
 static std::atomic<unsigned long long> g_launches{0};
@@ -140,6 +135,7 @@ const char* mb_status_string(int s) {
     case MB_ERR_WORKSPACE: return "MB_ERR_WORKSPACE";
     case MB_ERR_ARCH: return "MB_ERR_ARCH";
     case MB_ERR_CUDA: return "MB_ERR_CUDA";
+    case MB_ERR_TOKEN_RANGE: return "MB_ERR_TOKEN_RANGE";
   }
   return "MB_ERR_UNKNOWN";
 }

@@ -37,7 +37,18 @@ __device__ __forceinline__ int block_scan_incl(int v, int* s_warp, int& total) {
 
 // one CTA: phase 1 row counts + prefix check (warp per row, ballot/popc over 32-wide chunks),
 // phase 2 exclusive scan over rows, phase 3 indices by rank.
-__global__ void __launch_bounds__(SCAN_THREADS) unpad_index_kernel(const int* __restrict__ mask, int B, int L,
+// token-id range check of one real position (A3 reads E_tok[id]): bit 1 of the row's status
+__device__ __forceinline__ int id_bad(const int* ids, int vocab, size_t pos) {
+  if (!ids) return 0;
+  const int id = ids[pos];
+  return (id < 0 || id >= vocab) ? 2 : 0;
+}
+__device__ __forceinline__ int status_of(int bad) {
+  return (bad & 1) ? MB_ERR_MASK_LAYOUT : (bad & 2) ? MB_ERR_TOKEN_RANGE : MB_OK;
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) unpad_index_kernel(const int* __restrict__ mask,
+                                                                   const int* __restrict__ ids, int vocab, int B, int L,
                                                                    int* __restrict__ cu, int* __restrict__ indices,
                                                                    int* __restrict__ meta) {
   __shared__ int s_warp[32];
@@ -51,10 +62,11 @@ __global__ void __launch_bounds__(SCAN_THREADS) unpad_index_kernel(const int* __
   int my_max = 0, my_bad = 0;
   for (int b = warp; b < B; b += SCAN_THREADS / 32) {
     const int* row = mask + (size_t)b * L;
-    int cnt = 0;
+    int cnt = 0, tok = 0;
     for (int l0 = 0; l0 < L; l0 += 32) {
       const int l = l0 + lane;
       const bool on = l < L && row[l] != 0;
+      if (on) tok |= id_bad(ids, vocab, (size_t)b * L + l);
       cnt += __popc(__ballot_sync(0xffffffffu, on));
     }
     // right-padded prefix <=> every position l < cnt is on (R6)
@@ -63,7 +75,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) unpad_index_kernel(const int* __
       const int l = l0 + lane;
       if (l < cnt && row[l] == 0) bad = 1;
     }
-    bad = __any_sync(0xffffffffu, bad);
+    bad = __any_sync(0xffffffffu, bad) | (__any_sync(0xffffffffu, tok) ? 2 : 0);
     if (lane == 0) {
       cu[b + 1] = cnt;
       my_max = max(my_max, cnt);
@@ -72,7 +84,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) unpad_index_kernel(const int* __
   }
   if (lane == 0) {
     atomicMax(&s_max, my_max);
-    if (my_bad) atomicOr(&s_bad, 1);
+    if (my_bad) atomicOr(&s_bad, my_bad);
   }
   __syncthreads();
   // phase 2: scan cu[1..B] in chunks of 1024
@@ -102,14 +114,15 @@ __global__ void __launch_bounds__(SCAN_THREADS) unpad_index_kernel(const int* __
   if (threadIdx.x == 0) {
     meta[0] = carry;
     meta[1] = s_max;
-    meta[2] = s_bad ? MB_ERR_MASK_LAYOUT : MB_OK;
+    meta[2] = status_of(s_bad);
   }
 }
 
 __global__ void __launch_bounds__(SCAN_THREADS) mlm_select_kernel(const int* __restrict__ labels,
                                                                   const int* __restrict__ indices, int capacity,
                                                                   int vocab, int* __restrict__ rows,
-                                                                  int* __restrict__ out_labels, int* __restrict__ meta) {
+                                                                  int* __restrict__ out_labels, int* __restrict__ meta,
+                                                                  float* __restrict__ count_accum) {
   __shared__ int s_warp[32];
   __shared__ int s_bad;
   if (threadIdx.x == 0) s_bad = 0;
@@ -135,6 +148,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) mlm_select_kernel(const int* __r
   if (threadIdx.x == 0) {
     meta[3] = carry;
     if (s_bad) meta[2] = MB_ERR_LABEL_RANGE;
+    if (count_accum) *count_accum += (float)carry;
   }
 }
 
@@ -142,23 +156,26 @@ __global__ void __launch_bounds__(SCAN_THREADS) mlm_select_kernel(const int* __r
 // counts of the rows before its own (a few hundred ints) and writes its rows' indices, while CTA 0
 // also writes cu_seqlens and meta.  Two short launches instead of one latency-bound CTA.
 constexpr int UP_ROWS = 8;  // rows (warps) per CTA
-__global__ void __launch_bounds__(UP_ROWS * 32) unpad_count_kernel(const int* __restrict__ mask, int B, int L,
+__global__ void __launch_bounds__(UP_ROWS * 32) unpad_count_kernel(const int* __restrict__ mask,
+                                                                   const int* __restrict__ ids, int vocab, int B, int L,
                                                                    int* __restrict__ cnt, int* __restrict__ bad) {
   const int lane = threadIdx.x & 31;
   const int b = blockIdx.x * UP_ROWS + (threadIdx.x >> 5);
   if (b >= B) return;
   const int* row = mask + (size_t)b * L;
-  int c = 0;
+  int c = 0, tok = 0;
   for (int l0 = 0; l0 < L; l0 += 32) {
     const int l = l0 + lane;
-    c += __popc(__ballot_sync(0xffffffffu, l < L && row[l] != 0));
+    const bool on = l < L && row[l] != 0;
+    if (on) tok |= id_bad(ids, vocab, (size_t)b * L + l);
+    c += __popc(__ballot_sync(0xffffffffu, on));
   }
   int nb = 0;  // right-padded prefix <=> every position l < c is on (R6)
   for (int l0 = 0; l0 < c; l0 += 32) {
     const int l = l0 + lane;
     if (l < c && row[l] == 0) nb = 1;
   }
-  nb = __any_sync(0xffffffffu, nb);
+  nb = __any_sync(0xffffffffu, nb) | (__any_sync(0xffffffffu, tok) ? 2 : 0);
   if (lane == 0) {
     cnt[b] = c;
     bad[b] = nb;
@@ -212,7 +229,7 @@ __global__ void __launch_bounds__(UP_ROWS * 32) unpad_write_kernel(const int* __
       const int v = i < B ? cnt[i] : 0;
       if (i < B) {
         atomicMax(&s_max, v);
-        if (bad[i]) atomicOr(&s_bad, 1);
+        if (bad[i]) atomicOr(&s_bad, bad[i]);
       }
       // block inclusive scan (blockDim.x = 256 = 8 warps)
       int x = v;
@@ -236,7 +253,7 @@ __global__ void __launch_bounds__(UP_ROWS * 32) unpad_write_kernel(const int* __
       cu[0] = 0;
       meta[0] = carry;
       meta[1] = s_max;
-      meta[2] = s_bad ? MB_ERR_MASK_LAYOUT : MB_OK;
+      meta[2] = status_of(s_bad);
     }
   }
 }
@@ -260,7 +277,7 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_write_kernel(const int* __res
                                                                 const int* __restrict__ indices, int capacity,
                                                                 int vocab, const int* __restrict__ cnt,
                                                                 int* __restrict__ rows, int* __restrict__ out_labels,
-                                                                int* __restrict__ meta) {
+                                                                int* __restrict__ meta, float* __restrict__ count_accum) {
   __shared__ int s_warp[32];
   __shared__ int s_base;
   const int nnz = min(meta[0], capacity);
@@ -281,7 +298,10 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_write_kernel(const int* __res
     out_labels[base + inc - 1] = lab;
     if (lab < 0 || lab >= vocab) meta[2] = MB_ERR_LABEL_RANGE;
   }
-  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) meta[3] = base + tot;
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+    meta[3] = base + tot;
+    if (count_accum) *count_accum += (float)(base + tot);
+  }
 }
 
 // warp per row, 16-byte vectors
@@ -329,19 +349,29 @@ mb_status scatter_rows(const bf16* src, const int* idx, int n, int H, int rows, 
 
 extern "C" {
 
-mb_status mb_unpad_index(const int32_t* mask, int32_t B, int32_t L, int32_t* cu_seqlens, int32_t* indices,
-                         int32_t* meta, mb_stream_t s) {
+size_t mb_unpad_workspace_bytes(int32_t B) { return B > 0 ? 2 * (size_t)B * sizeof(int) : 0; }
+
+size_t mb_select_workspace_bytes(int32_t capacity) {
+  return capacity > 0 ? (size_t)((capacity + mb::SEL_THREADS - 1) / mb::SEL_THREADS) * sizeof(int) : 0;
+}
+
+mb_status mb_unpad_index(const int32_t* mask, const int32_t* ids, int32_t vocab, int32_t B, int32_t L,
+                         int32_t* cu_seqlens, int32_t* indices, int32_t* meta, void* ws, size_t ws_bytes,
+                         mb_stream_t s) {
   if (!mask || !cu_seqlens || !indices || !meta) return MB_ERR_INVALID_ARG;
   if (B <= 0 || L <= 0 || B > 65536 || L > 65536) return MB_ERR_INVALID_ARG;
+  if (ids && vocab < 1) return MB_ERR_CONFIG;
+  MB_REQUIRE_ARCH();
   cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
-  int* scr = mb::device_scratch(2 * (size_t)B);
-  if (!scr) {  // no scratch: the single-CTA kernel
-    mb::unpad_index_kernel<<<1, mb::SCAN_THREADS, 0, st>>>(mask, B, L, cu_seqlens, indices, meta);
+  if (!ws) {  // no workspace: the single-CTA kernel
+    mb::unpad_index_kernel<<<1, mb::SCAN_THREADS, 0, st>>>(mask, ids, vocab, B, L, cu_seqlens, indices, meta);
     MB_CHECK_LAUNCH();
     return MB_OK;
   }
+  if (ws_bytes < mb_unpad_workspace_bytes(B)) return MB_ERR_WORKSPACE;
+  int* scr = reinterpret_cast<int*>(ws);  // [0, B): row counts, [B, 2B): row status bits
   const int grid = (B + mb::UP_ROWS - 1) / mb::UP_ROWS;
-  mb::unpad_count_kernel<<<grid, mb::UP_ROWS * 32, 0, st>>>(mask, B, L, scr, scr + B);
+  mb::unpad_count_kernel<<<grid, mb::UP_ROWS * 32, 0, st>>>(mask, ids, vocab, B, L, scr, scr + B);
   MB_CHECK_LAUNCH();
   mb::unpad_write_kernel<<<grid, mb::UP_ROWS * 32, 0, st>>>(mask, B, L, scr, scr + B, cu_seqlens, indices, meta);
   MB_CHECK_LAUNCH();
@@ -349,23 +379,26 @@ mb_status mb_unpad_index(const int32_t* mask, int32_t B, int32_t L, int32_t* cu_
 }
 
 mb_status mb_mlm_select(const int32_t* labels, const int32_t* indices, int32_t capacity, int32_t vocab,
-                        int32_t* masked_rows, int32_t* masked_labels, int32_t* meta, mb_stream_t s) {
+                        int32_t* masked_rows, int32_t* masked_labels, int32_t* meta, float* count_accum, void* ws,
+                        size_t ws_bytes, mb_stream_t s) {
   if (!labels || !indices || !masked_rows || !masked_labels || !meta) return MB_ERR_INVALID_ARG;
   if (capacity < 0) return MB_ERR_INVALID_ARG;
   if (vocab < 1) return MB_ERR_CONFIG;
+  MB_REQUIRE_ARCH();
   cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
   const int blocks = (capacity + mb::SEL_THREADS - 1) / mb::SEL_THREADS;
-  int* scr = (blocks >= 1 && blocks <= 4096) ? mb::device_scratch(blocks) : nullptr;
-  if (!scr) {  // empty / huge capacity: the single-CTA kernel
+  if (!ws || blocks < 1) {  // no workspace / empty: the single-CTA kernel
     mb::mlm_select_kernel<<<1, mb::SCAN_THREADS, 0, st>>>(labels, indices, capacity, vocab, masked_rows,
-                                                         masked_labels, meta);
+                                                         masked_labels, meta, count_accum);
     MB_CHECK_LAUNCH();
     return MB_OK;
   }
+  if (ws_bytes < mb_select_workspace_bytes(capacity)) return MB_ERR_WORKSPACE;
+  int* scr = reinterpret_cast<int*>(ws);  // per-block label counts
   mb::sel_count_kernel<<<blocks, mb::SEL_THREADS, 0, st>>>(labels, indices, capacity, meta, scr);
   MB_CHECK_LAUNCH();
   mb::sel_write_kernel<<<blocks, mb::SEL_THREADS, 0, st>>>(labels, indices, capacity, vocab, scr, masked_rows,
-                                                          masked_labels, meta);
+                                                          masked_labels, meta, count_accum);
   MB_CHECK_LAUNCH();
   return MB_OK;
 }
@@ -373,6 +406,7 @@ mb_status mb_mlm_select(const int32_t* labels, const int32_t* indices, int32_t c
 mb_status mb_gather_rows(const mb_bf16* src, const int32_t* idx, int32_t n, int32_t H, mb_bf16* dst, mb_stream_t s) {
   if (!src || !idx || !dst || n < 0 || H <= 0) return MB_ERR_INVALID_ARG;
   if (H % 8) return MB_ERR_CONFIG;
+  MB_REQUIRE_ARCH();
   return mb::gather_rows(reinterpret_cast<const bf16*>(src), idx, n, H, reinterpret_cast<bf16*>(dst),
                          reinterpret_cast<cudaStream_t>(s));
 }
@@ -381,6 +415,7 @@ mb_status mb_scatter_rows(const mb_bf16* src, const int32_t* idx, int32_t n, int
                           mb_stream_t s) {
   if (!src || !idx || !dst || n < 0 || H <= 0 || rows < n) return MB_ERR_INVALID_ARG;
   if (H % 8) return MB_ERR_CONFIG;
+  MB_REQUIRE_ARCH();
   return mb::scatter_rows(reinterpret_cast<const bf16*>(src), idx, n, H, rows, reinterpret_cast<bf16*>(dst),
                           reinterpret_cast<cudaStream_t>(s));
 }

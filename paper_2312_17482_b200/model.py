@@ -124,6 +124,12 @@ class MosaicBert:
         self._nm_cap = 0
         self.step_count = 0
         self.loss_sum = torch.zeros(1, dtype=torch.float32, device=self.device)
+        # R18 on the device: count_dev accumulates n_masked over the micro-steps (mb_mlm_select), is
+        # allreduced over the ranks, and mb_loss_normalize turns it into the optimizer's gradient
+        # scale (inv_dev) and the returned mean loss (loss_dev) — no host read-back, no torch kernel
+        self.count_dev = torch.zeros(1, dtype=torch.float32, device=self.device)
+        self.inv_dev = torch.zeros(1, dtype=torch.float32, device=self.device)
+        self.loss_dev = torch.zeros(1, dtype=torch.float32, device=self.device)
         self.masked_count = 0
         if params is not None:
             self.load(params)
@@ -149,6 +155,7 @@ class MosaicBert:
         for b in self.buckets:
             b.g.zero_()
         self.loss_sum.zero_()
+        self.count_dev.zero_()
         self.masked_count = 0
 
     # ------------------------------------------------------------------ buffers
@@ -163,7 +170,8 @@ class MosaicBert:
         self.cu = torch.empty(B + 1, dtype=torch.int32, device=dev)
         self.indices = torch.empty(T, dtype=torch.int32, device=dev)
         self.meta = torch.zeros(4, dtype=torch.int32, device=dev)
-        self.meta_host = torch.zeros(4, dtype=torch.int32).pin_memory()
+        self.idx_ws = torch.empty(max(L.unpad_workspace_bytes(B), 1), dtype=torch.uint8, device=dev)
+        self.sel_ws = torch.empty(max(L.select_workspace_bytes(T), 1), dtype=torch.uint8, device=dev)
         self.rows = torch.empty(T, dtype=torch.int32, device=dev)
         self.labs = torch.empty(T, dtype=torch.int32, device=dev)
         self.xs = [torch.empty(T, H, dtype=torch.bfloat16, device=dev) for _ in range(self.d.layers + 1)]
@@ -205,9 +213,9 @@ class MosaicBert:
         if pend is None:
             return
         self._meta_pending = None
-        ev, want = pend
+        ev, want, host = pend
         ev.synchronize()
-        nnz, max_seqlen, status, n_m = (int(x) for x in self.meta_host.tolist())
+        nnz, max_seqlen, status, n_m = (int(x) for x in host.tolist())
         if status != 0:
             raise RuntimeError(f"batch rejected: {L.STATUS.get(status, status)}")
         if (nnz, max_seqlen, n_m) != tuple(want):
@@ -225,18 +233,23 @@ class MosaicBert:
         drops = ([L.Dropout(self.dropout, drop_seed, l) for l in range(self.d.layers)] if self.dropout > 0
                  else [None] * self.d.layers)
         B, Lq = mask.shape
+        self.check_meta()  # the previous micro-step's deferred check (before _ensure may regrow buffers)
         self._ensure(B, Lq)
         cd = self.cd
-        # A1: unpad index + MLM selection; one 16-byte D2H read of {nnz, max_seqlen, status, n_masked}
-        L._ck("mb_unpad_index", L.lib().mb_unpad_index(L._p(mask), B, Lq, L._p(self.cu), L._p(self.indices),
-                                                        L._p(self.meta), L._stream()))
+        # A1: unpad index (+ token-id range check) + MLM selection; n_masked is also accumulated on
+        # the device (count_dev, the R18 normaliser)
+        L._ck("mb_unpad_index", L.lib().mb_unpad_index(L._p(mask), L._p(ids), self.d.vocab, B, Lq, L._p(self.cu),
+                                                        L._p(self.indices), L._p(self.meta), L._p(self.idx_ws),
+                                                        self.idx_ws.numel(), L._stream()))
         L._ck("mb_mlm_select", L.lib().mb_mlm_select(L._p(labels), L._p(self.indices), B * Lq, self.d.vocab,
-                                                      L._p(self.rows), L._p(self.labs), L._p(self.meta), L._stream()))
-        self.check_meta()  # the previous micro-step's deferred check (its copy is long complete)
-        self.meta_host.copy_(self.meta, non_blocking=True)
+                                                      L._p(self.rows), L._p(self.labs), L._p(self.meta),
+                                                      L._p(self.count_dev), L._p(self.sel_ws), self.sel_ws.numel(),
+                                                      L._stream()))
+        meta_host = self._meta_host()  # the previous micro-step's copy was consumed by check_meta above
+        meta_host.copy_(self.meta, non_blocking=True)
         if host_meta is None:  # read {nnz, max_seqlen, status, n_masked} back (one 16-byte D2H sync)
             torch.cuda.current_stream().synchronize()
-            nnz, max_seqlen, status, n_m = (int(x) for x in self.meta_host.tolist())
+            nnz, max_seqlen, status, n_m = (int(x) for x in meta_host.tolist())
             if status != 0:
                 raise RuntimeError(f"batch rejected: {L.STATUS.get(status, status)}")
         else:  # sizes known on the host: no sync; the device's numbers are verified later.  They must
@@ -246,9 +259,14 @@ class MosaicBert:
                 raise ValueError(f"host_meta {tuple(host_meta)} impossible for a {B}x{Lq} batch")
             ev = torch.cuda.Event()
             ev.record()
-            self._meta_pending = (ev, (nnz, max_seqlen, n_m))
+            self._meta_pending = (ev, (nnz, max_seqlen, n_m), meta_host)
         self.masked_count += n_m
         if nnz == 0:
+            # nothing to compute; a data-parallel rank must still join every collective its peers
+            # issue on this micro-step (zero gradients reduce to the right sum)
+            if allreduce and self._dp():
+                self._count_work = dist.all_reduce(self.count_dev, group=self.pg, async_op=True)
+                self._handles = [h for h in (self._allreduce(b) for b in self._reduce_order()) if h is not None]
             return 0, 0
         packed = L.Packed(L._p(self.cu), B, nnz, max_seqlen)
         e = self.emb_bucket.p
@@ -271,10 +289,10 @@ class MosaicBert:
             t[1].record()
         handles = []
         if allreduce and self._dp():
-            # the R18 normaliser first (known since the index step): its allreduce precedes the
-            # gradient buckets in NCCL's order, so the optimizer never waits behind the last bucket
-            t = torch.tensor([float(self.masked_count)], dtype=torch.float32, device=self.device)
-            self._count = (t, dist.all_reduce(t, group=self.pg, async_op=True))
+            # the R18 normaliser first (device count of every micro-step so far): its allreduce
+            # precedes the gradient buckets in NCCL's order, so the optimizer never waits behind
+            # the last bucket; no host value is involved, so nothing synchronises the host
+            self._count_work = dist.all_reduce(self.count_dev, group=self.pg, async_op=True)
         if allreduce:
             handles.append(self._allreduce(self.head_bucket))
         # backward through the layers; each bucket's allreduce is issued as soon as it is final
@@ -291,6 +309,15 @@ class MosaicBert:
             handles.append(self._allreduce(self.emb_bucket))
         self._handles = [h for h in handles if h is not None]
         return nnz, n_m
+
+    def _meta_host(self):
+        if getattr(self, "_meta_pinned", None) is None:
+            self._meta_pinned = torch.zeros(4, dtype=torch.int32).pin_memory()
+        return self._meta_pinned
+
+    def _reduce_order(self):
+        """Buckets in the order micro_step issues their allreduce (head, layers L-1..0, embedding)."""
+        return [self.head_bucket, *self.layer_buckets[::-1], self.emb_bucket]
 
     def _dp(self) -> bool:
         return dist.is_available() and dist.is_initialized() and dist.get_world_size(self.pg) > 1
@@ -372,23 +399,25 @@ class MosaicBert:
             self.micro_step(ids, mask, labels, inv_norm=1.0, allreduce=(i == n - 1),
                             host_meta=host_meta[i] if host_meta is not None else None)
         if global_masked is None and self._dp():
-            # R18 normaliser = the global masked count, allreduced in-stream by the last micro-step
-            # and applied from device memory (AdamW's grad_scale_dev, the returned loss): never read back
-            t, work = self._count
-            work.wait()
-            inv = 1.0 / t.clamp(min=1.0)
+            # R18 normaliser = the global masked count, allreduced in-stream by the last micro-step;
+            # mb_loss_normalize turns it into AdamW's device gradient scale and the returned loss
+            self._count_work.wait()
+            self._count_work = None
+            L.loss_normalize(self.loss_sum, count=self.count_dev, inv_out=self.inv_dev, loss_out=self.loss_dev)
             if optimizer:
-                self.optimizer_step(1.0, lr=lr, grad_scale_dev=inv)  # waits each bucket's reduction
+                self.optimizer_step(1.0, lr=lr, grad_scale_dev=self.inv_dev)  # waits each bucket's reduction
             else:
                 self.wait_grads()
-            return self.loss_sum * inv
-        if global_masked is None:
-            global_masked = self.masked_count
+            return self.loss_dev
         self.wait_grads()
-        scale = 1.0 / max(global_masked, 1)
+        if global_masked is None:  # one rank: the device count of this step's micro-steps
+            L.loss_normalize(self.loss_sum, count=self.count_dev, inv_out=self.inv_dev, loss_out=self.loss_dev)
+        else:
+            L.loss_normalize(self.loss_sum, count_host=float(global_masked), inv_out=self.inv_dev,
+                             loss_out=self.loss_dev)
         if optimizer:
-            self.optimizer_step(scale, lr=lr)
-        return self.loss_sum * scale
+            self.optimizer_step(1.0, lr=lr, grad_scale_dev=self.inv_dev)
+        return self.loss_dev
 
     def grads_numpy(self, scale: float = 1.0) -> dict:
         """All gradients as float64 numpy arrays in the synth/oracle naming (tests)."""

@@ -65,7 +65,10 @@ def test_host_argument_errors(lib):
     out = np.zeros(4, np.float32)
     assert lib.mb_alibi_slopes(0, out.ctypes.data) == 2  # MB_ERR_CONFIG
     assert lib.mb_alibi_slopes(4, None) == 1
-    assert lib.mb_unpad_index(None, 1, 1, None, None, None, None) == 1
+    assert lib.mb_unpad_index(None, None, 0, 1, 1, None, None, None, None, 0, None) == 1
+    assert lib.mb_unpad_index(1, 1, 0, 1, 1, 1, 1, 1, None, 0, None) == 2  # ids given, vocab < 1
+    assert lib.mb_mlm_select(None, None, 0, 1, None, None, None, None, None, 0, None) == 1
+    assert lib.mb_loss_normalize(None, None, 1.0, None, None, None) == 1
     assert lib.mb_gemm(4, 4, 4, None, 8, 0, None, 8, 0, None, 8, 0, None, None, 0, None, 0, None) == 1
     from paper_2312_17482_b200 import _lib
     d = _lib.dims(96, 5, 256, 128)  # hidden % heads != 0
@@ -80,10 +83,35 @@ def test_host_argument_errors(lib):
     ok = _lib.Dropout(0.1, 0, 0)
     assert lib.mb_dropout_mask(ctypes.byref(ok), 0, 4, 12, 1, None) == 2  # cols % 8 != 0
     assert lib.mb_status_string(4) == b"MB_ERR_MASK_LAYOUT"
+    assert lib.mb_status_string(9) == b"MB_ERR_TOKEN_RANGE"
+
+
+def test_arch_error_without_b200(lib):
+    """Well-formed calls on a machine whose current device is not sm_100 (here: no device at all)
+    return MB_ERR_ARCH and launch nothing (the library carries sm_100a SASS only)."""
+    import torch
+    if torch.cuda.is_available() and torch.cuda.get_device_capability() == (10, 0):
+        pytest.skip("running on a B200")
+    n0 = lib.mb_launch_count()
+    assert lib.mb_layernorm_forward(8, 8, 8, 4, 64, ctypes.c_float(1e-5), 8, 8, None) == 7
+    assert lib.mb_unpad_index(8, None, 0, 2, 4, 8, 8, 8, None, 0, None) == 7
+    assert lib.mb_loss_normalize(8, None, ctypes.c_float(1.0), 8, None, None) == 7
+    assert lib.mb_launch_count() == n0
+
+
+def test_library_holds_no_device_allocation():
+    """The header's contract: the library allocates nothing (every scratch is a caller workspace)."""
+    csrc = os.path.join(ROOT, "paper_2312_17482_b200", "csrc")
+    for f in os.listdir(csrc):
+        txt = open(os.path.join(csrc, f)).read()
+        for call in ("cudaMalloc", "cudaFree", "cudaHostAlloc", "malloc("):
+            assert call not in txt, (f, call)
 
 
 def test_workspace_queries(lib):
     from paper_2312_17482_b200 import _lib
+    assert _lib.unpad_workspace_bytes(512) == 2 * 512 * 4 and _lib.unpad_workspace_bytes(0) == 0
+    assert _lib.select_workspace_bytes(65536) == 64 * 4 and _lib.select_workspace_bytes(1) == 4
     d = _lib.dims(768, 12, 3072, 30528)
     sb = _lib.layer_saved_bytes(d, 65536)
     # QKV 3H + O H + S1 H + Y1 H + U 2I + Z I + S2 H (bf16) + LSE heads + 2x stats (fp32) per token

@@ -96,3 +96,73 @@ def test_dp_two_ranks_gradient_equals_full_batch(tmp_path):
     for k in ("emb", "type_emb", "lne_g", "lne_b", "w_t", "b_t", "lnh_g", "lnh_b", "b_dec"):
         scale = max(float(np.abs(full[k]).max()), 1e-30)
         assert float(np.abs(r0[k] - full[k]).max()) <= 2e-5 * scale, k
+
+
+def _dp_empty_worker(rank, world, port, out_dir):
+    import numpy as np
+    import torch.distributed as dist
+    import synth
+    import paper_2312_17482_b200 as mb
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    d = synth.TINY
+    params = synth.make_model_params(d, 5, "stress", n_layers=2)
+    mbs = _empty_case_batches()[rank]
+    model = mb.MosaicBert(mb.ModelDims(d.hidden, d.heads, d.intermediate, d.vocab, 2, d.ln_eps), params)
+    dev = [tuple(torch.from_numpy(b[k]).cuda() for k in ("input_ids", "attention_mask", "labels")) for b in mbs]
+    loss = model.train_step(dev, optimizer=False)
+    torch.cuda.synchronize()
+    g = model.grads_numpy(scale=float(model.inv_dev.item()))
+    np.savez(os.path.join(out_dir, f"e{rank}.npz"), loss=float(loss.item()),
+             **{f"L{i}_{k}": v for i, lg in enumerate(g["layers"]) for k, v in lg.items()},
+             **{k: v for k, v in g.items() if k != "layers"})
+    dist.destroy_process_group()
+
+
+def _empty_case_batches():
+    import numpy as np
+    import synth
+    a = synth.make_batch("C1", 301, B=4)
+    b = synth.make_batch("C1", 302, B=4)
+    c = synth.make_batch("C1", 303, B=4)
+    empty = {k: v.copy() for k, v in c.items()}
+    empty["attention_mask"][:] = 0  # an all-padding micro-batch: nnz == 0
+    return [[a, b], [c, empty]]
+
+
+def test_dp_last_microbatch_all_padding(tmp_path):
+    """a rank whose LAST micro-batch is all padding (nnz = 0) must still join the
+    masked-count and every bucket allreduce its peer issues (else the job deadlocks), and the
+    reduced gradient equals the single-process gradient of all real micro-batches."""
+    import time
+    import numpy as np
+    import torch.multiprocessing as mp
+    import synth
+    import paper_2312_17482_b200 as mb
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = mp.start_processes(_dp_empty_worker, args=(2, _port(), str(tmp_path)), nprocs=2, start_method="spawn",
+                             join=False)
+    deadline = time.time() + 300
+    while not ctx.join(timeout=5):
+        if time.time() > deadline:
+            for p in ctx.processes:
+                p.kill()
+            pytest.fail("data-parallel step with an empty last micro-batch did not finish (deadlock)")
+    d = synth.TINY
+    params = synth.make_model_params(d, 5, "stress", n_layers=2)
+    model = mb.MosaicBert(mb.ModelDims(d.hidden, d.heads, d.intermediate, d.vocab, 2, d.ln_eps), params)
+    a, b = _empty_case_batches()[0]
+    c, _ = _empty_case_batches()[1]
+    dev = [tuple(torch.from_numpy(x[k]).cuda() for k in ("input_ids", "attention_mask", "labels")) for x in (a, b, c)]
+    loss = float(model.train_step(dev, optimizer=False).item())
+    full = model.grads_numpy(scale=float(model.inv_dev.item()))
+    r0, r1 = (np.load(tmp_path / f"e{r}.npz") for r in range(2))
+    assert abs(float(r0["loss"]) + float(r1["loss"]) - loss) <= 1e-5 * abs(loss)
+    for i, lg in enumerate(full["layers"]):
+        for k, v in lg.items():
+            assert np.array_equal(r0[f"L{i}_{k}"], r1[f"L{i}_{k}"]), k
+            assert float(np.abs(r0[f"L{i}_{k}"] - v).max()) <= 2e-5 * max(float(np.abs(v).max()), 1e-30), (i, k)
+    for k in ("emb", "w_t", "b_dec"):
+        assert float(np.abs(r0[k] - full[k]).max()) <= 2e-5 * max(float(np.abs(full[k]).max()), 1e-30), k

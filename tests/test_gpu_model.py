@@ -260,3 +260,97 @@ def test_model_step_large_dims_one_layer():
     params = synth.make_model_params(synth.LARGE, 13, "bert", n_layers=1)
     batch = synth.make_batch("C3", 5013, B=4)
     _model_parity(synth.LARGE, batch, params)
+
+
+def test_host_meta_growing_batch():
+    """with host_meta, a later micro-batch larger than any earlier one regrows the
+    buffers; the deferred check of the previous micro-step must still read ITS metadata."""
+    params = synth.make_model_params(synth.TINY, 6, "stress")
+    dims = synth.TINY
+    model = mb.MosaicBert(mb.ModelDims(dims.hidden, dims.heads, dims.intermediate, dims.vocab, 1, dims.ln_eps), params)
+    small = synth.make_batch("C1", 41, B=4, L=16)
+    big = synth.make_batch("C1", 42, B=8, L=24)
+    mbs, metas = [], []
+    for b in (small, big, small):
+        mbs.append(tuple(to_dev(b[k], I32) for k in ("input_ids", "attention_mask", "labels")))
+        metas.append(mb.MosaicBert.batch_meta(b["attention_mask"], b["labels"]))
+    loss = float(model.train_step(mbs, optimizer=False, host_meta=metas).item())
+    model.check_meta()
+    ref = float(mb.MosaicBert(mb.ModelDims(dims.hidden, dims.heads, dims.intermediate, dims.vocab, 1, dims.ln_eps),
+                              params).train_step(mbs, optimizer=False).item())
+    assert abs(loss - ref) <= 1e-6 * abs(ref)
+
+
+def test_token_id_range_reported_and_clamped():
+    """an id outside [0, V) at a REAL position is reported by mb_unpad_index
+    (MB_ERR_TOKEN_RANGE in meta[2]); at a pad position it is ignored; the embedding kernels clamp, so
+    nothing outside E_tok / dE_tok is touched, and the model step rejects the batch."""
+    dims = synth.TINY
+    batch = synth.make_batch("C1", 77)
+    mask = batch["attention_mask"]
+    ids = batch["input_ids"].copy()
+    b = int(np.argmin(mask.sum(1)))
+    ids[b, -1] = 10_000 if mask[b, -1] == 0 else ids[b, -1]  # pad position: ignored
+    _, _, meta = mb.unpad_index(to_dev(mask, I32), ids=to_dev(ids, I32), vocab=dims.vocab)
+    assert int(meta[2]) == 0
+    for bad in (-1, dims.vocab):
+        ids2 = ids.copy()
+        ids2[0, 0] = bad  # row 0 is a full row: position 0 is real
+        _, _, meta = mb.unpad_index(to_dev(mask, I32), ids=to_dev(ids2, I32), vocab=dims.vocab)
+        assert L.STATUS[int(meta[2])] == "MB_ERR_TOKEN_RANGE"
+        # the mask-layout error takes precedence
+        m2 = mask.copy()
+        m2[0, 1] = 0
+        _, _, meta = mb.unpad_index(to_dev(m2, I32), ids=to_dev(ids2, I32), vocab=dims.vocab)
+        assert L.STATUS[int(meta[2])] == "MB_ERR_MASK_LAYOUT"
+    params = synth.make_model_params(dims, 1, "stress")
+    model = mb.MosaicBert(mb.ModelDims(dims.hidden, dims.heads, dims.intermediate, dims.vocab, 1, dims.ln_eps), params)
+    ids2 = ids.copy()
+    ids2[0, 0] = dims.vocab + 5
+    guard = model.emb_bucket.g.clone()
+    with pytest.raises(RuntimeError, match="TOKEN_RANGE"):
+        model.train_step([(to_dev(ids2, I32), to_dev(mask, I32), to_dev(batch["labels"], I32))], optimizer=False)
+    assert torch.equal(model.emb_bucket.g, guard)  # rejected before any kernel wrote a gradient
+
+
+def test_unpad_select_workspace_and_concurrent_streams():
+    """The index scans use only the caller's workspace: the single-CTA (no workspace) and multi-CTA
+    kernels agree bit for bit, and two streams running mb_unpad_index / mb_mlm_select concurrently on
+    different batches (their own workspaces) both stay bit-exact vs the oracle."""
+    cases = [synth.make_batch("C5", 3100 + i, B=512) for i in range(2)]
+    s = [torch.cuda.Stream() for _ in cases]
+    dev = [(to_dev(c["attention_mask"], I32), to_dev(c["labels"], I32).reshape(-1)) for c in cases]
+    outs = [None, None]
+    torch.cuda.synchronize()
+    for i, (m, lab) in enumerate(dev):
+        with torch.cuda.stream(s[i]):
+            count = torch.zeros(1, dtype=torch.float32, device="cuda")
+            cu, idx, meta = mb.unpad_index(m)
+            rows, labs = mb.mlm_select(lab, idx, synth.BASE.vocab, meta, count=count)
+            outs[i] = (cu, idx, meta, rows, labs, count)
+    torch.cuda.synchronize()
+    for c, (cu, idx, meta, rows, labs, count) in zip(cases, outs):
+        ocu, oidx, omax, ost = O.unpad_index(c["attention_mask"])
+        nnz, mx, st, n_m = (int(v) for v in meta.tolist())
+        assert (nnz, mx, st) == (len(oidx), omax, ost)
+        assert np.array_equal(cu.cpu().numpy(), ocu) and np.array_equal(idx.cpu().numpy()[:nnz], oidx)
+        lab = c["labels"].reshape(-1)[oidx]
+        sel = np.flatnonzero(lab != -100)
+        assert n_m == len(sel) and float(count.item()) == n_m
+        assert np.array_equal(rows.cpu().numpy()[:n_m], sel) and np.array_equal(labs.cpu().numpy()[:n_m], lab[sel])
+        # the workspace-free single-CTA kernels give the same bits
+        m = to_dev(c["attention_mask"], I32)
+        cu1, idx1, meta1 = mb.unpad_index(m, ws=False)
+        rows1, labs1 = mb.mlm_select(to_dev(c["labels"], I32).reshape(-1), idx1, synth.BASE.vocab, meta1, ws=False)
+        assert torch.equal(cu1, cu) and torch.equal(idx1[:nnz], idx[:nnz]) and torch.equal(meta1, meta)
+        assert torch.equal(rows1[:n_m], rows[:n_m]) and torch.equal(labs1[:n_m], labs[:n_m])
+
+
+def test_loss_normalize_device_count():
+    """R18 on the device: inv = 1 / max(N, 1), loss = loss_sum * inv, N from a device scalar or the host."""
+    ls = torch.tensor([12.5], device="cuda")
+    inv, out = torch.zeros(1, device="cuda"), torch.zeros(1, device="cuda")
+    mb.loss_normalize(ls, count=torch.tensor([5.0], device="cuda"), inv_out=inv, loss_out=out)
+    assert float(inv) == np.float32(1 / 5.0) and abs(float(out) - 2.5) < 1e-6
+    mb.loss_normalize(ls, count_host=0.0, inv_out=inv, loss_out=out)
+    assert float(inv) == 1.0 and float(out) == 12.5
