@@ -70,10 +70,19 @@ MB_API const char* mb_version(void);
 MB_API unsigned long long mb_launch_count(void);
 MB_API mb_status mb_probe_set(int32_t site, void* events, int32_t capacity, int32_t* count);
 
-/* Model dimensions.  d = hidden/heads (head_dim, 32 or 64).  ln_eps: LayerNorm epsilon (R11). */
+/* Model dimensions.  d = hidden/heads (head_dim, 32 or 64).  ln_eps: LayerNorm epsilon (R11).
+ * flags: MB_FLAG_DETERMINISTIC makes every gradient reduction of mb_encoder_backward, mb_mlm_loss and
+ *   mb_embed_backward bitwise reproducible from run to run: split-K weight-
+ *   gradient partials are added split by split in split order (per-tile turnstiles), per-CTA column
+ *   partials (LN dgamma/dbeta, bias gradients) are summed in a fixed order by a second pass, the
+ *   long-sequence dQ is kept per key tile and summed in key-tile order, and the embedding-table
+ *   scatter-add sums the rows of each token id in token order.  The default (0) uses fp32 atomics:
+ *   faster, equal up to fp32 reassociation.  The workspace queries take the flag into account. */
+enum { MB_FLAG_DETERMINISTIC = 1 };
 typedef struct {
   int32_t hidden, heads, intermediate, vocab;
   float ln_eps;
+  int32_t flags;
 } mb_dims;
 
 /* ---------------------------------------------------------------------------------------------
@@ -268,11 +277,14 @@ MB_API mb_status mb_dropout_mask(const mb_dropout* drop, int32_t site, int32_t r
 MB_API mb_status mb_embed_forward(const mb_dims* d, const int32_t* ids, const int32_t* indices, int32_t nnz,
                            const mb_bf16* emb, const mb_bf16* type_emb, const mb_bf16* ln_g, const mb_bf16* ln_b,
                            mb_bf16* x0, float* stats, mb_stream_t s);
-/* Backward: d_emb[id] += dv, d_type_emb[0] += sum dv, d_ln_g/d_ln_b += (fp32).  dx0 is consumed. */
+/* Backward: d_emb[id] += dv, d_type_emb[0] += sum dv, d_ln_g/d_ln_b += (fp32).  dx0 is consumed.
+ * ws: device workspace of mb_embed_workspace_bytes(d, nnz) bytes (0 unless d->flags has
+ * MB_FLAG_DETERMINISTIC: then the dv rows, the (id, token) sort keys and the LN column partials). */
+MB_API size_t mb_embed_workspace_bytes(const mb_dims* d, int32_t nnz);
 MB_API mb_status mb_embed_backward(const mb_dims* d, const int32_t* ids, const int32_t* indices, int32_t nnz,
                             const mb_bf16* emb, const mb_bf16* type_emb, const mb_bf16* ln_g, const float* stats,
-                            mb_bf16* dx0, float* d_emb, float* d_type_emb, float* d_ln_g, float* d_ln_b,
-                            mb_stream_t s);
+                            mb_bf16* dx0, float* d_emb, float* d_type_emb, float* d_ln_g, float* d_ln_b, void* ws,
+                            size_t ws_bytes, mb_stream_t s);
 
 /* ---------------------------------------------------------------------------------------------
  * A11 — sparse MLM head + softmax cross-entropy on the masked tokens only (P:150 30% MLM; vocab

@@ -29,8 +29,12 @@ STATUS = {0: "MB_OK", 1: "MB_ERR_INVALID_ARG", 2: "MB_ERR_CONFIG", 3: "MB_ERR_SH
           9: "MB_ERR_TOKEN_RANGE"}
 
 
+FLAG_DETERMINISTIC = 1  # mb_dims.flags: bitwise-reproducible gradient reductions
+
+
 class Dims(C.Structure):
-    _fields_ = [("hidden", I32), ("heads", I32), ("intermediate", I32), ("vocab", I32), ("ln_eps", F32)]
+    _fields_ = [("hidden", I32), ("heads", I32), ("intermediate", I32), ("vocab", I32), ("ln_eps", F32),
+                ("flags", I32)]
 
 
 class Packed(C.Structure):
@@ -85,7 +89,8 @@ _SIGS = {
                                       C.POINTER(LayerPtrs), P, SZ, C.POINTER(Dropout), P]),
     "mb_dropout_mask": (C.c_int, [C.POINTER(Dropout), I32, I32, I32, P, P]),
     "mb_embed_forward": (C.c_int, [C.POINTER(Dims), P, P, I32, P, P, P, P, P, P, P]),
-    "mb_embed_backward": (C.c_int, [C.POINTER(Dims), P, P, I32, P, P, P, P, P, P, P, P, P, P]),
+    "mb_embed_workspace_bytes": (SZ, [C.POINTER(Dims), I32]),
+    "mb_embed_backward": (C.c_int, [C.POINTER(Dims), P, P, I32, P, P, P, P, P, P, P, P, P, P, SZ, P]),
     "mb_mlm_workspace_bytes": (SZ, [C.POINTER(Dims), I32]),
     "mb_mlm_loss": (C.c_int, [C.POINTER(Dims), C.POINTER(HeadPtrs), P, I32, P, P, I32, F32, P, P, P,
                               C.POINTER(HeadPtrs), P, SZ, P]),
@@ -169,8 +174,8 @@ class Probe:
         return [self.events[2 * i].elapsed_time(self.events[2 * i + 1]) for i in range(n)]
 
 
-def dims(hidden, heads, intermediate, vocab, ln_eps=1e-12) -> Dims:
-    return Dims(hidden, heads, intermediate, vocab, ln_eps)
+def dims(hidden, heads, intermediate, vocab, ln_eps=1e-12, deterministic=False) -> Dims:
+    return Dims(hidden, heads, intermediate, vocab, ln_eps, FLAG_DETERMINISTIC if deterministic else 0)
 
 
 # --------------------------------------------------------------------------------------- wrappers
@@ -362,10 +367,19 @@ def embed_forward(d: Dims, ids, indices, nnz, emb, type_emb, ln_g, ln_b, x0, sta
     return x0
 
 
-def embed_backward(d: Dims, ids, indices, nnz, emb, type_emb, ln_g, stats, dx0, d_emb, d_type_emb, d_ln_g, d_ln_b):
+def embed_workspace_bytes(d: Dims, nnz: int) -> int:
+    return int(lib().mb_embed_workspace_bytes(C.byref(d), nnz))
+
+
+def embed_backward(d: Dims, ids, indices, nnz, emb, type_emb, ln_g, stats, dx0, d_emb, d_type_emb, d_ln_g, d_ln_b,
+                   ws=None):
+    nb = embed_workspace_bytes(d, nnz)
+    if ws is None and nb:
+        ws = torch.empty(nb, dtype=torch.uint8, device=dx0.device)
     _ck("mb_embed_backward", lib().mb_embed_backward(C.byref(d), _p(ids), _p(indices), nnz, _p(emb), _p(type_emb),
                                                      _p(ln_g), _p(stats), _p(dx0), _p(d_emb), _p(d_type_emb),
-                                                     _p(d_ln_g), _p(d_ln_b), _stream()))
+                                                     _p(d_ln_g), _p(d_ln_b), _p(ws), ws.numel() if ws is not None else 0,
+                                                     _stream()))
 
 
 def mlm_workspace_bytes(d: Dims, n_masked: int) -> int:

@@ -20,7 +20,8 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", 
          "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
 if os.environ.get("MB_WATCHDOG", "0") == "1":  # debug build: mbarrier waits trap after a timeout
     FLAGS.append("-DMB_WATCHDOG")
-SOURCES = ["runtime.cu", "unpad.cu", "layernorm.cu", "gemm.cu", "attention.cu", "head.cu", "api.cu", "ablation.cu"]
+SOURCES = ["runtime.cu", "unpad.cu", "layernorm.cu", "gemm.cu", "attention.cu", "head.cu", "api.cu", "ablation.cu",
+           "reduce.cu"]
 
 
 def _deps():

@@ -40,7 +40,8 @@ struct Ws {  // backward scratch
   bf16 *ds2, *du, *dy1, *ds1, *dO, *dqkv;
   void* attn;
   size_t attn_bytes, bytes;
-  Ws(char* base, int T, int H, int I, int heads, int max_seqlen) {
+  Det det;  // deterministic mode (MB_FLAG_DETERMINISTIC): partial slab + split-K turnstiles
+  Ws(char* base, int T, int H, int I, int heads, int max_seqlen, bool deterministic) {
     size_t off = 0;
     auto take = [&](size_t b) {
       char* p = base ? base + off : nullptr;
@@ -53,11 +54,20 @@ struct Ws {  // backward scratch
     ds1 = (bf16*)take((size_t)T * H * 2);
     dO = (bf16*)take((size_t)T * H * 2);
     dqkv = (bf16*)take((size_t)T * 3 * H * 2);
-    attn_bytes = attention_ws_bytes(T, heads, H / heads, max_seqlen);
+    attn_bytes = attention_ws_bytes(T, heads, H / heads, max_seqlen, deterministic);
     attn = take(attn_bytes);
+    if (deterministic) {
+      det.part_floats = std::max({layernorm_bwd_det_floats(T, H), gemm_det_floats(2 * I, H, T), colsum_det_floats(T, H)});
+      det.part = (float*)take(det.part_floats * 4);
+      det.sem_count = std::max({gemm_det_sems(H, I), gemm_det_sems(2 * I, H), gemm_det_sems(H, H), gemm_det_sems(3 * H, H)});
+      det.sem = (int*)take((size_t)det.sem_count * 4);
+      if (!base) det.part = nullptr;
+    }
     bytes = off;
   }
 };
+
+inline bool det_of(const mb_dims* d) { return d && (d->flags & MB_FLAG_DETERMINISTIC); }
 
 mb_status check_dims(const mb_dims* d) {
   if (!d) return MB_ERR_INVALID_ARG;
@@ -111,7 +121,7 @@ size_t mb_layer_saved_bytes(const mb_dims* d, int32_t nnz) {
 
 size_t mb_layer_workspace_bytes(const mb_dims* d, int32_t nnz, int32_t max_seqlen) {
   if (!d || d->heads <= 0) return 0;
-  return mb::Ws(nullptr, std::max(nnz, 1), d->hidden, d->intermediate, d->heads, max_seqlen).bytes;
+  return mb::Ws(nullptr, std::max(nnz, 1), d->hidden, d->intermediate, d->heads, max_seqlen, mb::det_of(d)).bytes;
 }
 
 mb_status mb_dropout_mask(const mb_dropout* drop, int32_t site, int32_t rows, int32_t cols, uint8_t* out,
@@ -202,8 +212,11 @@ mb_status mb_encoder_backward(const mb_dims* d, const mb_layer_params* p, const 
   cudaStream_t s = reinterpret_cast<cudaStream_t>(s_);
   const int T = pk->nnz, H = d->hidden, I = d->intermediate, nh = d->heads;
   Saved sv(reinterpret_cast<char*>(const_cast<void*>(saved)), T, H, I, nh);
-  Ws w(reinterpret_cast<char*>(ws), T, H, I, nh, pk->max_seqlen);
+  Ws w(reinterpret_cast<char*>(ws), T, H, I, nh, pk->max_seqlen, det_of(d));
   if (ws_bytes < w.bytes) return MB_ERR_WORKSPACE;
+  const Det* det = w.det ? &w.det : nullptr;
+  // the turnstiles start at zero (each GEMM's last split resets its own counters)
+  if (det && cudaMemsetAsync(w.det.sem, 0, (size_t)w.det.sem_count * 4, s) != cudaSuccess) return MB_ERR_CUDA;
   // F2: with dropout the projection branches see dF = dS2 * keep / (1 - p) (dp2) and dA = dS1 * keep
   // / (1 - p) (dp1), while the residual branches keep dS2 / dS1.  dp2 lives in w.dy1 (written only
   // after its last reader, dW2) and dp1 in the front of w.dqkv (written only by the attention
@@ -213,7 +226,7 @@ mb_status mb_encoder_backward(const mb_dims* d, const mb_layer_params* p, const 
   bf16* dp1 = dr1.thr ? w.dqkv : w.ds1;
   // LN2 backward: dS2 (and dp2); dgamma2, dbeta2; db2 = column sums of dp2 (same pass)
   TRY(layernorm_bwd(reinterpret_cast<bf16*>(dy), sv.s2, sv.st2, B(p->ln2_g), T, H, nullptr, w.ds2, g->ln2_g,
-                    g->ln2_b, g->b_2, s, &dr2, dr2.thr ? dp2 : nullptr));
+                    g->ln2_b, g->b_2, s, &dr2, dr2.thr ? dp2 : nullptr, det));
   {  // dZ = dF W2 fused with the GeGLU backward -> dU = dZ * Gd = [dZ g GeLU'(a) | dZ GeLU(a)]
     GemmArgs a;
     a.M = T, a.N = I, a.K = H, a.A = dp2, a.lda = H, a.B = B(p->w_2), a.ldb = I, a.b_t = true;
@@ -224,6 +237,7 @@ mb_status mb_encoder_backward(const mb_dims* d, const mb_layer_params* p, const 
     GemmArgs a;
     a.M = H, a.N = I, a.K = T, a.A = dp2, a.lda = H, a.a_t = true, a.B = sv.z, a.ldb = I, a.b_t = true;
     a.ep.mode = E_F32_ACC, a.ep.C = g->w_2, a.ep.ldc = I;
+    a.det = det;
     TRY(gemm(a, s));
   }
   {  // dY1 = dU W1v + dS2
@@ -236,11 +250,12 @@ mb_status mb_encoder_backward(const mb_dims* d, const mb_layer_params* p, const 
     GemmArgs a;
     a.M = 2 * I, a.N = H, a.K = T, a.A = w.du, a.lda = 2 * I, a.a_t = true, a.B = sv.y1, a.ldb = H, a.b_t = true;
     a.ep.mode = E_F32_ACC, a.ep.C = g->w_1v, a.ep.ldc = H, a.ep.dbias = g->b_1v;
+    a.det = det;
     TRY(gemm(a, s));
   }
   // LN1 backward: dS1 (and dp1); dgamma1, dbeta1; dbo = column sums of dp1 (same pass)
   TRY(layernorm_bwd(w.dy1, sv.s1, sv.st1, B(p->ln1_g), T, H, nullptr, w.ds1, g->ln1_g, g->ln1_b, g->b_o, s, &dr1,
-                    dr1.thr ? dp1 : nullptr));
+                    dr1.thr ? dp1 : nullptr, det));
   {  // dO = dA Wo
     GemmArgs a;
     a.M = T, a.N = H, a.K = H, a.A = dp1, a.lda = H, a.B = B(p->w_o), a.ldb = H, a.b_t = true;
@@ -251,12 +266,13 @@ mb_status mb_encoder_backward(const mb_dims* d, const mb_layer_params* p, const 
     GemmArgs a;
     a.M = H, a.N = H, a.K = T, a.A = dp1, a.lda = H, a.a_t = true, a.B = sv.o, a.ldb = H, a.b_t = true;
     a.ep.mode = E_F32_ACC, a.ep.C = g->w_o, a.ep.ldc = H;
+    a.det = det;
     TRY(gemm(a, s));
   }
   // A10: attention backward -> dQKV
   probe_begin(PROBE_ATTN_BWD, s);
   TRY(attention_bwd(sv.qkv, sv.o, w.dO, sv.lse, pk->cu_seqlens, pk->batch, T, pk->max_seqlen, nh, H / nh, slopes,
-                    w.dqkv, g->b_qkv, w.attn, w.attn_bytes, s));  // also dbqkv = column sums of dQKV
+                    w.dqkv, g->b_qkv, w.attn, w.attn_bytes, s, det));  // also dbqkv = column sums of dQKV
   probe_end(PROBE_ATTN_BWD, s);
   {  // dX = dQKV Wqkv + dS1
     GemmArgs a;
@@ -268,6 +284,7 @@ mb_status mb_encoder_backward(const mb_dims* d, const mb_layer_params* p, const 
     GemmArgs a;
     a.M = 3 * H, a.N = H, a.K = T, a.A = w.dqkv, a.lda = 3 * H, a.a_t = true, a.B = B(x), a.ldb = H, a.b_t = true;
     a.ep.mode = E_F32_ACC, a.ep.C = g->w_qkv, a.ep.ldc = H;
+    a.det = det;
     TRY(gemm(a, s));
   }
 #undef TRY

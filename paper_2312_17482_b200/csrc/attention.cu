@@ -1050,6 +1050,29 @@ __global__ void dq_finish_kernel(const float* __restrict__ dq_acc, int nnz, int 
   }
 }
 
+// deterministic mode: dQ row r = sum over the key tiles kt < ceil(len_b / 128) of its sequence b of
+// slab kt, in kt order; written as bf16 into the Q third of dqkv (db_q then comes from colsum_det)
+__global__ void dq_finish_det_kernel(const float* __restrict__ dq_part, const int* __restrict__ cu, int batch, int nnz,
+                                     int H, bf16* __restrict__ dqkv) {
+  const int r = blockIdx.x * blockDim.y + threadIdx.y;
+  const int c = threadIdx.x * 8;
+  if (r >= nnz || c >= H) return;
+  int lo = 0, hi = batch;  // sequence b with cu[b] <= r < cu[b + 1]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (cu[mid] <= r) lo = mid;
+    else hi = mid;
+  }
+  const int nt = (cu[lo + 1] - cu[lo] + TILE - 1) / TILE;
+  float t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int kt = 0; kt < nt; ++kt) {
+    const float4* src = reinterpret_cast<const float4*>(dq_part + ((size_t)kt * nnz + r) * H + c);
+    const float4 a = src[0], b = src[1];
+    t[0] += a.x, t[1] += a.y, t[2] += a.z, t[3] += a.w, t[4] += b.x, t[5] += b.y, t[6] += b.z, t[7] += b.w;
+  }
+  *reinterpret_cast<uint4*>(dqkv + (size_t)r * 3 * H + c) = f32_to_bf16x8(t);
+}
+
 // single-pass P / dS of one (q tile, k tile) block for this thread's 64 keys: P -> sP as computed;
 // dS/sqrt(d) is kept packed in registers and written to sdS after this warp's pending bulk copies
 // (the previous block's dQ reduction staged in the dS slab) have read it
@@ -1099,7 +1122,10 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
     const __grid_constant__ CUtensorMap tm_dqkv, const __grid_constant__ CUtensorMap tm_dq, LongUnits U, int d,
     const float* __restrict__ slopes,
     const float* __restrict__ lse, const float* __restrict__ Dg, float* __restrict__ dq_acc,
-    bf16* __restrict__ dqkv, float* __restrict__ dbias, int nnz) {
+    bf16* __restrict__ dqkv, float* __restrict__ dbias, int nnz, int det) {
+  // det (deterministic mode): each key tile kt stores its dQ contribution into its own slab
+  // dq_acc[kt * nnz + row] (tm_dq spans [QT * nnz, H]) instead of reduce-adding into one buffer;
+  // dq_finish_det_kernel then sums the slabs in key-tile order
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sKV = smem;                           // 2 x (K, V)
@@ -1252,7 +1278,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
     // fold the finished dQ block into dq_acc: a warp whose 32 query rows are all inside the sequence
     // stages its [32 x 32] fp32 block in its dS slab (128B swizzle) and one lane hands it to the TMA
     // engine as a bulk reduce-add; a ragged quarter adds its valid rows with vector reductions
-    auto dq_out = [&](int start, int q0, int len, int h) {
+    auto dq_out = [&](int start, int q0, int len, int h, int kt) {
       float v[32];
       sm100::tmem_ld32(tdQ + lane_off + 32 * ch, v);
       sm100::tmem_ld_wait();
@@ -1265,13 +1291,19 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
         sm100::fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          sm100::tma_reduce_add_2d(&tm_dq, slabS, h * d + 32 * ch, start + q0 + q4 * 32);
+          if (det) sm100::tma_store_2d(&tm_dq, slabS, h * d + 32 * ch, kt * nnz + start + q0 + q4 * 32);
+          else sm100::tma_reduce_add_2d(&tm_dq, slabS, h * d + 32 * ch, start + q0 + q4 * 32);
           sm100::bulk_commit();
         }
       } else if (q0 + r < len) {
-        float* dst = dq_acc + (size_t)(start + q0 + r) * H + h * d + 32 * ch;
+        float* dst = dq_acc + ((size_t)(det ? kt * nnz : 0) + start + q0 + r) * H + h * d + 32 * ch;
+        if (det) {
 #pragma unroll
-        for (int e = 0; e < 32; e += 4) red_add_v4(dst + e, v[e], v[e + 1], v[e + 2], v[e + 3]);
+          for (int e = 0; e < 32; e += 4) *reinterpret_cast<float4*>(dst + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; e += 4) red_add_v4(dst + e, v[e], v[e + 1], v[e + 2], v[e + 3]);
+        }
       }
     };
     // LSE and D of row r of query tile ii of unit uu, loaded one block ahead of their use
@@ -1309,7 +1341,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
         if (i > 0) {  // block g-1's MMAs finished (P/dS free); its dQ is ready
           sm100::mbar_wait(acc_full, (g - 1) & 1);
           sm100::tc_fence_after();
-          dq_out(start, q0 - TILE, len, h);
+          dq_out(start, q0 - TILE, len, h, jt);
         }
         if (len - q0 >= TILE && len - kv0 >= TILE)
           bwd_block<false>(tS + lane_off, tdP + lane_off, sPa, sdSa, r, ch, lane, q0 - kv0, len - q0, len - kv0, sc2,
@@ -1325,7 +1357,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
       // unit end: last dQ block, then dV / dK of the key tile (rows = keys kv0 + r)
       sm100::mbar_wait(acc_full, (g - 1) & 1);
       sm100::tc_fence_after();
-      dq_out(start, (nq - 1) * TILE, len, h);
+      dq_out(start, (nq - 1) * TILE, len, h, jt);
       const bool ok = kv0 + r < len;
       const bool full = kv0 + q4 * 32 + 32 <= len;  // warp-uniform
 #pragma unroll 1
@@ -1425,22 +1457,33 @@ mb_status attention_fwd(const bf16* qkv, const int* cu, int batch, int nnz, int 
   return MB_OK;
 }
 
-// long path: dq_acc fp32 [nnz, H] followed by D fp32 [heads, nnz]
-size_t attention_ws_bytes(int nnz, int heads, int d, int max_seqlen) {
+// long path: dq_acc fp32 [nnz, H] (deterministic mode: one such slab per key tile) followed by D
+// fp32 [heads, nnz]
+size_t attention_ws_bytes(int nnz, int heads, int d, int max_seqlen, bool det) {
   if (max_seqlen <= TILE) return 0;
-  const size_t dq = ((size_t)nnz * heads * d * sizeof(float) + 255) & ~size_t(255);
+  const size_t slabs = det ? (size_t)((max_seqlen + TILE - 1) / TILE) : 1;
+  const size_t dq = (slabs * nnz * heads * d * sizeof(float) + 255) & ~size_t(255);
   return dq + (size_t)heads * nnz * sizeof(float);
 }
 
 mb_status attention_bwd(const bf16* qkv, const bf16* O, const bf16* dO, const float* lse, const int* cu, int batch,
                         int nnz, int max_seqlen, int heads, int d, const float* slopes, bf16* dqkv, float* dbias,
-                        void* ws, size_t ws_bytes, cudaStream_t s) {
+                        void* ws, size_t ws_bytes, cudaStream_t s, const Det* det) {
   if (nnz == 0 || batch == 0) return MB_OK;
   MB_REQUIRE(d == 32 || d == 64, MB_ERR_CONFIG);
   MB_REQUIRE(max_seqlen >= 1 && max_seqlen <= kMaxSeqlen, MB_ERR_SHAPE);
   const int H = heads * d;
-  const size_t need = attention_ws_bytes(nnz, heads, d, max_seqlen);
+  const bool dm = det && *det;
+  const size_t need = attention_ws_bytes(nnz, heads, d, max_seqlen, dm);
   MB_REQUIRE(ws_bytes >= need && (need == 0 || ws), MB_ERR_WORKSPACE);
+  if (dm && dbias) {  // deterministic mode: the kernels skip db_qkv; ordered column sums of dQ, dV afterwards
+    MB_REQUIRE(det->part_floats >= colsum_det_floats(nnz, H), MB_ERR_WORKSPACE);
+    mb_status st = attention_bwd(qkv, O, dO, lse, cu, batch, nnz, max_seqlen, heads, d, slopes, dqkv, nullptr, ws,
+                                 ws_bytes, s, det);
+    if (st != MB_OK) return st;
+    if ((st = colsum_det(dqkv, 3 * H, nnz, H, dbias, det->part, s)) != MB_OK) return st;  // db_q (db_k = 0, R31)
+    return colsum_det(dqkv + 2 * H, 3 * H, nnz, H, dbias + 2 * H, det->part, s);          // db_v
+  }
   CUtensorMap tq, tdo;
   MB_REQUIRE(make_tmap_bf16_2d(&tq, qkv, 3 * H, nnz, 3 * H, DT, TILE), MB_ERR_CUDA);
   MB_REQUIRE(make_tmap_bf16_2d(&tdo, dO, H, nnz, H, DT, TILE), MB_ERR_CUDA);
@@ -1469,10 +1512,12 @@ mb_status attention_bwd(const bf16* qkv, const bf16* O, const bf16* dO, const fl
       return MB_ERR_CUDA;
     attr_l = true;
   }
+  const int QT = (max_seqlen + TILE - 1) / TILE;
+  const size_t slabs = dm ? (size_t)QT : 1;  // deterministic mode: one fp32 dQ slab per key tile
   float* dq_acc = reinterpret_cast<float*>(ws);
   float* Dg = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) +
-                                       (((size_t)nnz * H * sizeof(float) + 255) & ~size_t(255)));
-  if (cudaMemsetAsync(dq_acc, 0, (size_t)nnz * H * sizeof(float), s) != cudaSuccess) return MB_ERR_CUDA;
+                                       ((slabs * nnz * H * sizeof(float) + 255) & ~size_t(255)));
+  if (!dm && cudaMemsetAsync(dq_acc, 0, (size_t)nnz * H * sizeof(float), s) != cudaSuccess) return MB_ERR_CUDA;
   {
     const int64_t n = (int64_t)nnz * heads;
     attn_bwd_prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(O, dO, nnz, heads, d, Dg);
@@ -1480,14 +1525,19 @@ mb_status attention_bwd(const bf16* qkv, const bf16* O, const bf16* dO, const fl
   }
   CUtensorMap tdq, tdqa;  // [32 x 32] dK / dV bf16 blocks (64B swizzle); [32 x 32] fp32 dQ blocks (128B swizzle)
   MB_REQUIRE(make_tmap_bf16_2d(&tdq, dqkv, 3 * H, nnz, 3 * H, 32, 32, 64), MB_ERR_CUDA);
-  MB_REQUIRE(make_tmap_f32_2d(&tdqa, dq_acc, H, nnz, H, 32, 32, 128), MB_ERR_CUDA);
-  LongUnits U{cu, heads, (max_seqlen + TILE - 1) / TILE, 0};
+  MB_REQUIRE(make_tmap_f32_2d(&tdqa, dq_acc, H, slabs * nnz, H, 32, 32, 128), MB_ERR_CUDA);
+  LongUnits U{cu, heads, QT, 0};
   U.total = batch * heads * U.QT;
   const int grid = std::max(1, std::min(U.total, num_sms()));
   if (launch_pdl(attn_bwd_long_kernel, dim3(grid), dim3(LB_THREADS), LB_SMEM, s, 1, tq, tdo, tdq, tdqa, U, d, slopes,
-                 lse, Dg, dq_acc, dqkv, dbias, nnz) != cudaSuccess)
+                 lse, Dg, dq_acc, dqkv, dbias, nnz, dm ? 1 : 0) != cudaSuccess)
     return MB_ERR_CUDA;
   MB_CHECK_LAUNCH();
+  if (dm) {
+    dq_finish_det_kernel<<<(nnz + 7) / 8, dim3(H / 8, 8), 0, s>>>(dq_acc, cu, batch, nnz, H, dqkv);
+    MB_CHECK_LAUNCH();
+    return MB_OK;
+  }
   {
     const int rows_per = 128;
     dq_finish_kernel<<<(nnz + rows_per - 1) / rows_per, dim3(H / 8, DQF_GROUPS), DQF_GROUPS * H * sizeof(float),
@@ -1512,7 +1562,7 @@ mb_status mb_attention_forward(const mb_bf16* qkv, const int32_t* cu_seqlens, in
 }
 
 size_t mb_attention_workspace_bytes(int32_t nnz, int32_t heads, int32_t head_dim, int32_t max_seqlen) {
-  return mb::attention_ws_bytes(nnz, heads, head_dim, max_seqlen);
+  return mb::attention_ws_bytes(nnz, heads, head_dim, max_seqlen, false);
 }
 
 mb_status mb_attention_backward(const mb_bf16* qkv, const mb_bf16* O, const mb_bf16* dO, const float* lse,

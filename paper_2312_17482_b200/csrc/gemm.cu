@@ -143,6 +143,12 @@ __device__ __forceinline__ void stg256(void* p, const uint4& a, const uint4& b) 
                : "memory");
 }
 
+__device__ __forceinline__ int ld_acquire_s32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void cp_async16(uint32_t smem_dst, const void* gsrc) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_dst), "l"(gsrc) : "memory");
 }
@@ -353,14 +359,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             rphase ^= 1;
           }
         }
-        if (dkb0 < dkb1) {
+        if (ep.dbias && (dkb0 < dkb1 || ep.dpart)) {
 #pragma unroll
           for (int e = 0; e < 8; ++e) dbs[e] += __shfl_xor_sync(0xffffffffu, dbs[e], 16);
           const int m0 = (mb * CG + rank) * BM + ch * 8;
           if (lane < 16) {
+            if (ep.dpart) {  // deterministic mode: one partial per (split, column tile), summed in order later
+              float* dp = ep.dpart + (int64_t)(kb0 / sc.kb_per * sc.num_n + nb) * M;
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
-              if (m0 + e < M) atomicAdd(ep.dbias + m0 + e, dbs[e]);
+              for (int e = 0; e < 8; ++e)
+                if (m0 + e < M) dp[m0 + e] = dbs[e];
+            } else {
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                if (m0 + e < M) atomicAdd(ep.dbias + m0 + e, dbs[e]);
+            }
           }
         }
       }
@@ -455,6 +468,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           if (ep.mode == E_DZ) lse_r = ep.lse[row];
         }
         constexpr float L2E = 1.4426950408889634f;
+        // deterministic split-K: this tile's splits add into C one after another, in split order
+        int* semp = nullptr;
+        if (ep.mode == E_F32_ACC && ep.sem && sc.splits > 1) {
+          const int tiles = sc.num_m * sc.num_n;
+          semp = ep.sem + (u % tiles) * CG + rank;
+          const int need = NUM_EPI_WARPS * (u / tiles);
+          if (lane == 0) {
+            // bounded wait: a turnstile that never opens (a scheduling bug) traps instead of hanging
+            for (long long spin = 0; ld_acquire_s32(semp) < need; ++spin) {
+              __nanosleep(64);
+              if (spin > (1ll << 27)) __trap();
+            }
+          }
+          __syncwarp();
+        }
 #pragma unroll 1
         for (int c = 0; c < HALF / 32; ++c) {
           const int crel = grp * HALF + c * 32;
@@ -512,9 +540,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             sm100::tmem_ld_wait();
             if (row_ok) {
               float* dst = reinterpret_cast<float*>(ep.C) + (int64_t)row * ep.ldc + col;
+              if (semp) {  // sole writer of these elements while this split holds the turnstile
 #pragma unroll
-              for (int j = 0; j < 32; j += 4)
-                if (j < nv) red_add_v4(dst + j, v[j], v[j + 1], v[j + 2], v[j + 3]);
+                for (int j = 0; j < 32; j += 4)
+                  if (j < nv) {
+                    float4 o = __ldcg(reinterpret_cast<const float4*>(dst + j));
+                    o.x += v[j], o.y += v[j + 1], o.z += v[j + 2], o.w += v[j + 3];
+                    __stcg(reinterpret_cast<float4*>(dst + j), o);
+                  }
+              } else {
+#pragma unroll
+                for (int j = 0; j < 32; j += 4)
+                  if (j < nv) red_add_v4(dst + j, v[j], v[j + 1], v[j + 2], v[j + 3]);
+              }
             }
           } else if (ep.mode == E_F32) {
             float b[32];
@@ -618,6 +656,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (CE && ep.mode == E_LSE && row_ok) {
           ep.part[(int64_t)row * ep.npart + nb * 2 + grp] = make_float2(run_m, run_s);
           if (has_lab) ep.zlab[row] = zl;
+        }
+        if (semp) {  // pass the turnstile on; the last split's last warp resets it for the next GEMM
+          __syncwarp();
+          if (lane == 0) {
+            __threadfence();
+            if (atomicAdd(semp, 1) == NUM_EPI_WARPS * sc.splits - 1) atomicExch(semp, 0);
+          }
         }
       }
       sm100::tc_fence_before();
@@ -988,6 +1033,18 @@ mb_status gemm(const GemmArgs& g, cudaStream_t s) {
   sc.kb_per = (sc.nkb + splits - 1) / splits;
   sc.splits = (sc.nkb + sc.kb_per - 1) / sc.kb_per;
   sc.total = sc.num_m * sc.num_n * sc.splits;
+  GemmArgs gd = g;  // deterministic mode: turnstile counters for split-K, partial slab for the fused db
+  const bool det = g.det && *g.det && g.ep.mode == E_F32_ACC;
+  if (det) {
+    if (sc.splits > 1) {
+      MB_REQUIRE(g.det->sem && g.det->sem_count >= sc.num_m * sc.num_n * CGV, MB_ERR_WORKSPACE);
+      gd.ep.sem = g.det->sem;
+    }
+    if (g.ep.dbias) {
+      MB_REQUIRE(g.det->part_floats >= (size_t)sc.splits * sc.num_n * g.M, MB_ERR_WORKSPACE);
+      gd.ep.dpart = g.det->part;
+    }
+  }
 
   if (paired) return launch<256, 6, 0, 0, 1, 1>(g, ta, tb, sc, s);
   if (geglu_bwd) {
@@ -1017,8 +1074,10 @@ mb_status gemm(const GemmArgs& g, cudaStream_t s) {
     return MB_OK;
   }
   if (g.ep.mode == E_F32_ACC && g.a_t && g.b_t && g.ep.dbias) {  // wgrad + fused db: 1 accumulator
-    if (BN == 256) return launch<256, 6, 1, 1, 0, 1, 2, 1>(g, ta, tb, sc, s);
-    return launch<128, 8, 1, 1, 0, 1, 2, 1>(g, ta, tb, sc, s);
+    const mb_status st = BN == 256 ? launch<256, 6, 1, 1, 0, 1, 2, 1>(gd, ta, tb, sc, s)
+                                   : launch<128, 8, 1, 1, 0, 1, 2, 1>(gd, ta, tb, sc, s);
+    if (st != MB_OK || !gd.ep.dpart) return st;
+    return ordered_sum(gd.ep.dpart, sc.splits * sc.num_n, g.M, g.M, g.ep.dbias, s);
   }
   MB_REQUIRE(g.ep.dbias == nullptr, MB_ERR_INVALID_ARG);
   if (g.ep.mode == E_LSE || g.ep.mode == E_DZ) {  // decoder GEMM with fused softmax-cross-entropy
@@ -1030,9 +1089,16 @@ mb_status gemm(const GemmArgs& g, cudaStream_t s) {
     MB_REQUIRE(!g.a_t && !g.b_t && BN == 256, MB_ERR_CONFIG);
     return launch<256, 6, 0, 0, 0, 1, 2, 2, 2>(g, ta, tb, sc, s);
   }
-  if (BN == 256) return dispatch_majors<256, 6, 1>(g, ta, tb, sc, s);
-  return dispatch_majors<128, 8, 1>(g, ta, tb, sc, s);
+  if (BN == 256) return dispatch_majors<256, 6, 1>(gd, ta, tb, sc, s);
+  return dispatch_majors<128, 8, 1>(gd, ta, tb, sc, s);
 }
+
+size_t gemm_det_floats(int M, int N, int K) {
+  // fused-db partial slab bound: splits <= 64 (the split-K search), column tiles of 128
+  (void)K;
+  return (size_t)64 * (size_t)((N + 127) / 128) * (size_t)M;
+}
+int gemm_det_sems(int M, int N) { return 2 * ((M + 255) / 256) * ((N + 127) / 128); }
 
 }  // namespace mb
 

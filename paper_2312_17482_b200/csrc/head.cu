@@ -125,8 +125,9 @@ struct HeadWs {
   float *stats, *row_loss, *zlab;
   float2* part;
   bf16* dz;
+  Det det;
   size_t bytes;
-  HeadWs(char* base, int n, int H, int V) {
+  HeadWs(char* base, int n, int H, int V, bool deterministic) {
     size_t o = 0;
     auto take = [&](size_t b) {
       char* p = base ? base + o : nullptr;
@@ -143,6 +144,12 @@ struct HeadWs {
     zlab = (float*)take((size_t)n * 4);
     part = (float2*)take((size_t)n * npart_of(V) * 8);
     dz = (bf16*)take((size_t)n * ((V + 7) & ~7) * 2);  // rows padded to 8 elements (any V, F3)
+    if (deterministic) {
+      det.part_floats = std::max(layernorm_bwd_det_floats(n, H), gemm_det_floats(V, H, n));
+      det.part = (float*)take(det.part_floats * 4);
+      det.sem_count = std::max(gemm_det_sems(V, H), gemm_det_sems(H, H));
+      det.sem = (int*)take((size_t)det.sem_count * 4);
+    }
     bytes = o;
   }
 };
@@ -153,7 +160,8 @@ extern "C" {
 
 size_t mb_mlm_workspace_bytes(const mb_dims* d, int32_t n_masked) {
   if (!d) return 0;
-  return mb::HeadWs(nullptr, std::max(n_masked, 1), d->hidden, d->vocab).bytes;
+  return mb::HeadWs(nullptr, std::max(n_masked, 1), d->hidden, d->vocab, (d->flags & MB_FLAG_DETERMINISTIC) != 0)
+      .bytes;
 }
 
 mb_status mb_mlm_loss(const mb_dims* d, const mb_head_params* p, const mb_bf16* y, int32_t nnz,
@@ -169,14 +177,16 @@ mb_status mb_mlm_loss(const mb_dims* d, const mb_head_params* p, const mb_bf16* 
   if (V < 1 || H % 8) return MB_ERR_CONFIG;
   const int Vp = (V + 7) & ~7;  // dz row stride (P:174's 30522 is allowed; 30528 = 64 x 477 is the paper's choice)
   cudaStream_t s = reinterpret_cast<cudaStream_t>(s_);
-  HeadWs w(reinterpret_cast<char*>(ws), std::max(n_masked, 1), H, V);
+  HeadWs w(reinterpret_cast<char*>(ws), std::max(n_masked, 1), H, V, (d->flags & MB_FLAG_DETERMINISTIC) != 0);
   if (ws_bytes < w.bytes) return MB_ERR_WORKSPACE;
+  const Det* det = w.det ? &w.det : nullptr;
   bf16* dyt = reinterpret_cast<bf16*>(dy_top);
   if (n_masked == 0) {
     if (cudaMemsetAsync(dyt, 0, (size_t)nnz * H * 2, s) != cudaSuccess) return MB_ERR_CUDA;
     return MB_OK;
   }
   const int n = n_masked;
+  if (det && cudaMemsetAsync(w.det.sem, 0, (size_t)w.det.sem_count * 4, s) != cudaSuccess) return MB_ERR_CUDA;
   auto B = [](const mb_bf16* q) { return reinterpret_cast<const bf16*>(q); };
   mb_status st;
 #define TRY(x)                      \
@@ -225,10 +235,12 @@ mb_status mb_mlm_loss(const mb_dims* d, const mb_head_params* p, const mb_bf16* 
     a.M = V, a.N = H, a.K = n, a.A = w.dz, a.lda = Vp, a.a_t = true, a.B = w.u, a.ldb = H, a.b_t = true;
     a.ep.mode = E_F32_ACC, a.ep.C = g->emb, a.ep.ldc = H;
     a.ep.dbias = g->b_dec;  // db_dec = column sums of dz, from the A tiles of this GEMM
+    a.det = det;
     TRY(gemm(a, s));
   }
   // LN_h backward fused with the GeLU' of the transform: du -> dt_pre (in place); db_t = sum dt_pre
-  TRY(layernorm_bwd(w.du, w.t, w.stats, B(p->ln_g), n, H, w.tpre, w.du, g->ln_g, g->ln_b, g->b_t, s));
+  TRY(layernorm_bwd(w.du, w.t, w.stats, B(p->ln_g), n, H, w.tpre, w.du, g->ln_g, g->ln_b, g->b_t, s, nullptr, nullptr,
+                    det));
   {
     GemmArgs a;  // dh = dt_pre W_t  (W_t [H_out, H_in] = [K, N]) -> reuse t
     a.M = n, a.N = H, a.K = H, a.A = w.du, a.lda = H, a.B = B(p->w_t), a.ldb = H, a.b_t = true;
@@ -239,6 +251,7 @@ mb_status mb_mlm_loss(const mb_dims* d, const mb_head_params* p, const mb_bf16* 
     GemmArgs a;  // dW_t += dt_pre^T h
     a.M = H, a.N = H, a.K = n, a.A = w.du, a.lda = H, a.a_t = true, a.B = w.h, a.ldb = H, a.b_t = true;
     a.ep.mode = E_F32_ACC, a.ep.C = g->w_t, a.ep.ldc = H;
+    a.det = det;
     TRY(gemm(a, s));
   }
   TRY(scatter_rows(w.t, masked_rows, n, H, nnz, dyt, s));
@@ -261,22 +274,39 @@ mb_status mb_embed_forward(const mb_dims* d, const int32_t* ids, const int32_t* 
                           d->ln_eps, reinterpret_cast<bf16*>(x0), stats, reinterpret_cast<cudaStream_t>(s));
 }
 
+size_t mb_embed_workspace_bytes(const mb_dims* d, int32_t nnz) {
+  if (!d || !(d->flags & MB_FLAG_DETERMINISTIC) || nnz <= 0) return 0;
+  const size_t ln = (mb::layernorm_bwd_det_floats(nnz, d->hidden) * 4 + 255) & ~size_t(255);
+  return ln + mb::embed_det_bytes(nnz, d->hidden);
+}
+
 mb_status mb_embed_backward(const mb_dims* d, const int32_t* ids, const int32_t* indices, int32_t nnz,
                             const mb_bf16* emb, const mb_bf16* type_emb, const mb_bf16* ln_g, const float* stats,
-                            mb_bf16* dx0, float* d_emb, float* d_type_emb, float* d_ln_g, float* d_ln_b,
-                            mb_stream_t s) {
+                            mb_bf16* dx0, float* d_emb, float* d_type_emb, float* d_ln_g, float* d_ln_b, void* ws,
+                            size_t ws_bytes, mb_stream_t s) {
   if (!d || !ids || !indices || !emb || !type_emb || !ln_g || !stats || !dx0 || !d_emb || !d_type_emb || !d_ln_g ||
       !d_ln_b || nnz < 0)
     return MB_ERR_INVALID_ARG;
   if (d->hidden % 8 || d->hidden > 1024 || d->vocab < 1) return MB_ERR_CONFIG;
   MB_REQUIRE_ARCH();
+  if (ws_bytes < mb_embed_workspace_bytes(d, nnz) || (ws_bytes && !ws)) return MB_ERR_WORKSPACE;
   mb::EmbedSrc e;
   e.ids = ids, e.indices = indices, e.emb = reinterpret_cast<const bf16*>(emb);
   e.type_emb = reinterpret_cast<const bf16*>(type_emb), e.d_emb = d_emb;
   e.vocab = d->vocab;
+  mb::Det det;
+  if ((d->flags & MB_FLAG_DETERMINISTIC) && nnz > 0) {
+    char* w = reinterpret_cast<char*>(ws);
+    det.part_floats = mb::layernorm_bwd_det_floats(nnz, d->hidden);
+    det.part = reinterpret_cast<float*>(w);
+    w += (det.part_floats * 4 + 255) & ~size_t(255);
+    e.dv_out = reinterpret_cast<float*>(w);
+    e.keys = reinterpret_cast<unsigned long long*>(w + (((size_t)nnz * d->hidden * 4 + 255) & ~size_t(255)));
+  }
   // d_type_emb[0] = sum over tokens of dv (every token has type 0, R17) == the LN "dsum"
   return mb::embed_ln_bwd(e, reinterpret_cast<const bf16*>(dx0), stats, reinterpret_cast<const bf16*>(ln_g), nnz,
-                          d->hidden, d_ln_g, d_ln_b, d_type_emb, reinterpret_cast<cudaStream_t>(s));
+                          d->hidden, d_ln_g, d_ln_b, d_type_emb, reinterpret_cast<cudaStream_t>(s),
+                          det ? &det : nullptr);
 }
 
 mb_status mb_adamw_step_dev(float* master, float* m, float* v, const float* g, mb_bf16* w_bf16, int64_t n,

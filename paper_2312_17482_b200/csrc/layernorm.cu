@@ -25,6 +25,7 @@ struct RowSrc {
   const bf16* type_emb;
   int vocab;              // embed mode: ids are clamped to [0, vocab) (out-of-range ids are reported
                           // by mb_unpad_index as MB_ERR_TOKEN_RANGE; the clamp keeps every access in bounds)
+  float* dv_out;          // embed backward, deterministic mode: dv rows [n, H] fp32 instead of the scatter-add
 };
 
 template <int VPL, bool EMBED>
@@ -164,7 +165,8 @@ __global__ void __launch_bounds__(LN_THREADS) ln_fwd_kernel(RowSrc src, const bf
 // Reduce one per-lane register vector (the same column layout in every warp) across the CTA and
 // atomically add it to out[H].
 template <int VPL>
-__device__ __forceinline__ void cta_column_reduce(const float* acc, float* sbuf, int H, float* out) {
+__device__ __forceinline__ void cta_column_reduce(const float* acc, float* sbuf, int H, float* out, float* part,
+                                                  int j3) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __syncthreads();
 #pragma unroll
@@ -180,7 +182,8 @@ __device__ __forceinline__ void cta_column_reduce(const float* acc, float* sbuf,
     float t = 0.f;
 #pragma unroll
     for (int w = 0; w < LN_WARPS; ++w) t += sbuf[w * H + c];
-    atomicAdd(out + c, t);
+    if (part) part[((size_t)blockIdx.x * 3 + j3) * H + c] = t;  // deterministic mode: ordered second pass
+    else atomicAdd(out + c, t);
   }
 }
 
@@ -189,7 +192,7 @@ __global__ void __launch_bounds__(LN_THREADS, VPL <= 3 ? 2 : 1)
     ln_bwd_kernel(RowSrc src, const bf16* __restrict__ dy, const float* __restrict__ stats,
                   const bf16* __restrict__ gamma, const bf16* __restrict__ gelu_pre, int n, int H, bf16* dx,
                   float* __restrict__ d_emb, float* __restrict__ dgamma, float* __restrict__ dbeta,
-                  float* __restrict__ dsum, DropArgs drop, bf16* __restrict__ dxd) {
+                  float* __restrict__ dsum, DropArgs drop, bf16* __restrict__ dxd, float* __restrict__ part) {
   // Register budget (2 CTAs x 8 warps per SM): per lane only x-hat and the three column
   // accumulators stay live; dy and gamma are re-read (L1 hits) in the second pass.
   extern __shared__ float sbuf[];
@@ -256,18 +259,23 @@ __global__ void __launch_bounds__(LN_THREADS, VPL <= 3 ? 2 : 1)
         if (DROP) {
           *reinterpret_cast<uint4*>(dxd + (size_t)row * H + c) = f32_to_bf16x8(o);
         } else if (EMBED) {
-          float* dst = d_emb + (size_t)id * H + c;
-          red_add_v4(dst, o[0], o[1], o[2], o[3]);
-          red_add_v4(dst + 4, o[4], o[5], o[6], o[7]);
+          float* dst = src.dv_out ? src.dv_out + (size_t)row * H + c : d_emb + (size_t)id * H + c;
+          if (src.dv_out) {
+            *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1], o[2], o[3]);
+            *reinterpret_cast<float4*>(dst + 4) = make_float4(o[4], o[5], o[6], o[7]);
+          } else {
+            red_add_v4(dst, o[0], o[1], o[2], o[3]);
+            red_add_v4(dst + 4, o[4], o[5], o[6], o[7]);
+          }
         } else {
           *reinterpret_cast<uint4*>(dx + (size_t)row * H + c) = f32_to_bf16x8(o);
         }
       }
     }
   }
-  cta_column_reduce<VPL>(acc_g, sbuf, H, dgamma);
-  cta_column_reduce<VPL>(acc_b, sbuf, H, dbeta);
-  if (DSUM) cta_column_reduce<VPL>(acc_s, sbuf, H, dsum);
+  cta_column_reduce<VPL>(acc_g, sbuf, H, dgamma, part, 0);
+  cta_column_reduce<VPL>(acc_b, sbuf, H, dbeta, part, 1);
+  if (DSUM) cta_column_reduce<VPL>(acc_s, sbuf, H, dsum, part, 2);
 }
 
 // out[c] += sum_r x[r, c]; thread = one 8-column vector, blockIdx.y = row chunk
@@ -305,7 +313,7 @@ __global__ void __launch_bounds__(LNW_GROUPS * W * 32)
     ln_bwd_w_kernel(RowSrc src, const bf16* __restrict__ dy, const float* __restrict__ stats,
                     const bf16* __restrict__ gamma, const bf16* __restrict__ gelu_pre, int n, int H, bf16* dx,
                     float* __restrict__ d_emb, float* __restrict__ dgamma, float* __restrict__ dbeta,
-                    float* __restrict__ dsum, DropArgs drop, bf16* __restrict__ dxd) {
+                    float* __restrict__ dsum, DropArgs drop, bf16* __restrict__ dxd, float* __restrict__ part) {
   pdl_wait();
   pdl_trigger();
   __shared__ float red[LNW_GROUPS][2][W][2];
@@ -433,6 +441,10 @@ __global__ void __launch_bounds__(LNW_GROUPS * W * 32)
     }
     if (DROP) {
       *reinterpret_cast<uint4*>(dxd + (size_t)row * H + c) = f32_to_bf16x8(o);
+    } else if (EMBED && src.dv_out) {  // deterministic mode: rows out, summed per id in token order later
+      float* dst = src.dv_out + (size_t)row * H + c;
+      *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1], o[2], o[3]);
+      *reinterpret_cast<float4*>(dst + 4) = make_float4(o[4], o[5], o[6], o[7]);
     } else if (EMBED) {
       int slot = -1;
 #pragma unroll
@@ -451,7 +463,7 @@ __global__ void __launch_bounds__(LNW_GROUPS * W * 32)
     }
   }
   // column sums: reduce the row groups through smem, one atomic per column per CTA
-  auto reduce = [&](const float* acc, float* out) {
+  auto reduce = [&](const float* acc, float* out, int j3) {
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < 8; ++j) sbuf[rg * H + c + j] = acc[j];
@@ -460,13 +472,14 @@ __global__ void __launch_bounds__(LNW_GROUPS * W * 32)
       float t = 0.f;
 #pragma unroll
       for (int g = 0; g < LNW_GROUPS; ++g) t += sbuf[g * H + cc];
-      atomicAdd(out + cc, t);
+      if (part) part[((size_t)blockIdx.x * 3 + j3) * H + cc] = t;  // deterministic mode: ordered second pass
+      else atomicAdd(out + cc, t);
     }
   };
-  reduce(ag, dgamma);
-  reduce(ab, dbeta);
-  if (DSUM) reduce(as, dsum);
-  if (EMBED) {  // flush the shared-memory rows of the repeated ids (written by every warp: barrier first)
+  reduce(ag, dgamma, 0);
+  reduce(ab, dbeta, 1);
+  if (DSUM) reduce(as, dsum, 2);
+  if (EMBED && !src.dv_out) {  // flush the shared-memory rows of the repeated ids (every warp wrote: barrier first)
     __syncthreads();
 #pragma unroll 1
     for (int k = 0; k < EMB_HOT; ++k) {
@@ -478,10 +491,20 @@ __global__ void __launch_bounds__(LNW_GROUPS * W * 32)
   }
 }
 
+// deterministic mode: the per-CTA column partials [grid][3][H] are summed in CTA order afterwards
+mb_status ln_det_finish(const Det* det, int grid, int H, float* dg, float* db, float* dsum, cudaStream_t s) {
+  if (!det || !*det) return MB_OK;
+  mb_status st;
+  if ((st = ordered_sum(det->part, grid, 3 * (int64_t)H, H, dg, s)) != MB_OK) return st;
+  if ((st = ordered_sum(det->part + H, grid, 3 * (int64_t)H, H, db, s)) != MB_OK) return st;
+  if (dsum) return ordered_sum(det->part + 2 * H, grid, 3 * (int64_t)H, H, dsum, s);
+  return MB_OK;
+}
+
 template <int W, bool EMBED>
 mb_status ln_bwd_w_launch(const RowSrc& src, const bf16* dy, const float* stats, const bf16* gamma,
                           const bf16* gelu_pre, int n, int H, bf16* dx, float* d_emb, float* dg, float* db,
-                          float* dsum, cudaStream_t s, const DropArgs& drop, bf16* dxd) {
+                          float* dsum, cudaStream_t s, const DropArgs& drop, bf16* dxd, const Det* det) {
   const int threads = LNW_GROUPS * W * 32;
   const int smem = (LNW_GROUPS + (EMBED ? EMB_HOT : 0)) * H * sizeof(float);
   const int blocks_per_sm = std::max(1, 2048 / threads);
@@ -498,14 +521,16 @@ mb_status ln_bwd_w_launch(const RowSrc& src, const bf16* dy, const float* stats,
       attr = true;
     }
   }
+  float* part = det && *det ? det->part : nullptr;
+  if (part && det->part_floats < (size_t)grid * 3 * H) return MB_ERR_WORKSPACE;
 #define LNW_GO(G, D)                                                                                           \
   ok = launch_pdl(ln_bwd_w_kernel<W, EMBED, G, D>, dim3(grid), dim3(threads), smem, s, 1, src, dy, stats, gamma, \
-                  gelu_pre, n, H, dx, d_emb, dg, db, dsum, drop, dxd) == cudaSuccess
+                  gelu_pre, n, H, dx, d_emb, dg, db, dsum, drop, dxd, part) == cudaSuccess
   bool ok = true;
   if (!EMBED && drop.thr) {
     if (gelu_pre || !dsum || !dxd) return MB_ERR_INVALID_ARG;
     ok = launch_pdl(ln_bwd_w_kernel<W, false, false, true, true>, dim3(grid), dim3(threads), smem, s, 1, src, dy, stats,
-                    gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, drop, dxd) == cudaSuccess;
+                    gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, drop, dxd, part) == cudaSuccess;
   } else if (gelu_pre && dsum) LNW_GO(true, true);
   else if (gelu_pre) LNW_GO(true, false);
   else if (dsum) LNW_GO(false, true);
@@ -513,7 +538,7 @@ mb_status ln_bwd_w_launch(const RowSrc& src, const bf16* dy, const float* stats,
 #undef LNW_GO
   if (!ok) return MB_ERR_CUDA;
   MB_CHECK_LAUNCH();
-  return MB_OK;
+  return ln_det_finish(det, grid, H, dg, db, dsum, s);
 }
 
 template <bool EMBED>
@@ -549,44 +574,47 @@ mb_status ln_fwd_dispatch(const RowSrc& src, const bf16* gamma, const bf16* beta
 template <int VPL, bool EMBED>
 mb_status ln_bwd_launch(const RowSrc& src, const bf16* dy, const float* stats, const bf16* gamma,
                         const bf16* gelu_pre, int n, int H, bf16* dx, float* d_emb, float* dg, float* db,
-                        float* dsum, cudaStream_t s, const DropArgs& drop, bf16* dxd) {
+                        float* dsum, cudaStream_t s, const DropArgs& drop, bf16* dxd, const Det* det) {
   const int smem = LN_WARPS * H * sizeof(float);
   const int grid = std::max(1, std::min((n + LN_WARPS - 1) / LN_WARPS, (VPL <= 3 ? 2 : 1) * num_sms()));
+  float* part = det && *det ? det->part : nullptr;
+  if (part && det->part_floats < (size_t)grid * 3 * H) return MB_ERR_WORKSPACE;
   if (!EMBED && drop.thr) {
     if (gelu_pre || !dsum || !dxd) return MB_ERR_INVALID_ARG;
     ln_bwd_kernel<VPL, false, false, true, true><<<grid, LN_THREADS, smem, s>>>(src, dy, stats, gamma, gelu_pre, n,
                                                                                 H, dx, d_emb, dg, db, dsum, drop,
-                                                                                dxd);
+                                                                                dxd, part);
   } else if (gelu_pre && dsum)
     ln_bwd_kernel<VPL, EMBED, true, true><<<grid, LN_THREADS, smem, s>>>(src, dy, stats, gamma, gelu_pre, n, H, dx,
-                                                                          d_emb, dg, db, dsum, drop, dxd);
+                                                                          d_emb, dg, db, dsum, drop, dxd, part);
   else if (gelu_pre)
     ln_bwd_kernel<VPL, EMBED, true, false><<<grid, LN_THREADS, smem, s>>>(src, dy, stats, gamma, gelu_pre, n, H, dx,
-                                                                           d_emb, dg, db, dsum, drop, dxd);
+                                                                           d_emb, dg, db, dsum, drop, dxd, part);
   else if (dsum)
     ln_bwd_kernel<VPL, EMBED, false, true><<<grid, LN_THREADS, smem, s>>>(src, dy, stats, gamma, gelu_pre, n, H,
-                                                                           dx, d_emb, dg, db, dsum, drop, dxd);
+                                                                           dx, d_emb, dg, db, dsum, drop, dxd, part);
   else
     ln_bwd_kernel<VPL, EMBED, false, false><<<grid, LN_THREADS, smem, s>>>(src, dy, stats, gamma, gelu_pre, n, H,
-                                                                            dx, d_emb, dg, db, dsum, drop, dxd);
+                                                                            dx, d_emb, dg, db, dsum, drop, dxd, part);
   MB_CHECK_LAUNCH();
-  return MB_OK;
+  return ln_det_finish(det, grid, H, dg, db, dsum, s);
 }
 
 template <bool EMBED>
 mb_status ln_bwd_dispatch(const RowSrc& src, const bf16* dy, const float* stats, const bf16* gamma,
                           const bf16* gelu_pre, int n, int H, bf16* dx, float* d_emb, float* dg, float* db,
-                          float* dsum, cudaStream_t s, const DropArgs& drop = DropArgs(), bf16* dxd = nullptr) {
+                          float* dsum, cudaStream_t s, const DropArgs& drop = DropArgs(), bf16* dxd = nullptr,
+                          const Det* det = nullptr) {
   if (n == 0) return MB_OK;
-  if (H == 768) return ln_bwd_w_launch<3, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s, drop, dxd);
-  if (H == 1024) return ln_bwd_w_launch<4, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s, drop, dxd);
-  if (H == 512) return ln_bwd_w_launch<2, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s, drop, dxd);
-  if (H == 256) return ln_bwd_w_launch<1, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s, drop, dxd);
+  if (H == 768) return ln_bwd_w_launch<3, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s, drop, dxd, det);
+  if (H == 1024) return ln_bwd_w_launch<4, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s, drop, dxd, det);
+  if (H == 512) return ln_bwd_w_launch<2, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s, drop, dxd, det);
+  if (H == 256) return ln_bwd_w_launch<1, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s, drop, dxd, det);
   switch ((H / 8 + 31) / 32) {
-    case 1: return ln_bwd_launch<1, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s, drop, dxd);
-    case 2: return ln_bwd_launch<2, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s, drop, dxd);
-    case 3: return ln_bwd_launch<3, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s, drop, dxd);
-    case 4: return ln_bwd_launch<4, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s, drop, dxd);
+    case 1: return ln_bwd_launch<1, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s, drop, dxd, det);
+    case 2: return ln_bwd_launch<2, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s, drop, dxd, det);
+    case 3: return ln_bwd_launch<3, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s, drop, dxd, det);
+    case 4: return ln_bwd_launch<4, EMBED>(src, dy, stats, gamma, gelu_pre, n, H, dx, d_emb, dg, db, dsum, s, drop, dxd, det);
   }
   return MB_ERR_CONFIG;
 }
@@ -595,29 +623,41 @@ mb_status ln_bwd_dispatch(const RowSrc& src, const bf16* dy, const float* stats,
 
 mb_status layernorm_fwd(const bf16* x, const bf16* gamma, const bf16* beta, int n, int H, float eps, bf16* y,
                         float* stats, cudaStream_t s) {
-  RowSrc src{x, nullptr, nullptr, nullptr, nullptr, 0};
+  RowSrc src{x, nullptr, nullptr, nullptr, nullptr, 0, nullptr};
   return ln_fwd_dispatch<false>(src, gamma, beta, n, H, eps, y, stats, s);
 }
 
 mb_status layernorm_bwd(const bf16* dy, const bf16* x, const float* stats, const bf16* gamma, int n, int H,
                         const bf16* gelu_pre, bf16* dx, float* dgamma, float* dbeta, float* dsum, cudaStream_t s,
-                        const DropArgs* drop, bf16* dxd) {
-  RowSrc src{x, nullptr, nullptr, nullptr, nullptr, 0};
+                        const DropArgs* drop, bf16* dxd, const Det* det) {
+  RowSrc src{x, nullptr, nullptr, nullptr, nullptr, 0, nullptr};
   const DropArgs none;
   return ln_bwd_dispatch<false>(src, dy, stats, gamma, gelu_pre, n, H, dx, nullptr, dgamma, dbeta, dsum, s,
-                                drop ? *drop : none, dxd);
+                                drop ? *drop : none, dxd, det);
+}
+
+size_t layernorm_bwd_det_floats(int n, int H) {
+  // bound on every LN-backward grid (ln_bwd_w_launch: <= 8 CTAs/SM or n / EMB_ROWS; ln_bwd_launch: 2/SM)
+  const size_t grid = (size_t)8 * num_sms() + (size_t)n / EMB_ROWS + 8;
+  return grid * 3 * (size_t)H;
 }
 
 mb_status embed_ln_fwd(const EmbedSrc& e, const bf16* gamma, const bf16* beta, int n, int H, float eps, bf16* y,
                        float* stats, cudaStream_t s) {
-  RowSrc src{nullptr, e.ids, e.indices, e.emb, e.type_emb, e.vocab};
+  RowSrc src{nullptr, e.ids, e.indices, e.emb, e.type_emb, e.vocab, nullptr};
   return ln_fwd_dispatch<true>(src, gamma, beta, n, H, eps, y, stats, s);
 }
 
 mb_status embed_ln_bwd(const EmbedSrc& e, const bf16* dy, const float* stats, const bf16* gamma, int n, int H,
-                       float* dgamma, float* dbeta, float* dsum, cudaStream_t s) {
-  RowSrc src{nullptr, e.ids, e.indices, e.emb, e.type_emb, e.vocab};
-  return ln_bwd_dispatch<true>(src, dy, stats, gamma, nullptr, n, H, nullptr, e.d_emb, dgamma, dbeta, dsum, s);
+                       float* dgamma, float* dbeta, float* dsum, cudaStream_t s, const Det* det) {
+  const bool dm = det && *det;
+  if (dm) MB_REQUIRE(e.dv_out && e.keys, MB_ERR_WORKSPACE);
+  RowSrc src{nullptr, e.ids, e.indices, e.emb, e.type_emb, e.vocab, dm ? e.dv_out : nullptr};
+  mb_status st = ln_bwd_dispatch<true>(src, dy, stats, gamma, nullptr, n, H, nullptr, e.d_emb, dgamma, dbeta, dsum,
+                                       s, DropArgs(), nullptr, det);
+  if (st != MB_OK || !dm) return st;
+  // deterministic scatter-add: sort the (id, token) pairs, then each id's rows are summed in token order
+  return embed_scatter_det(e.dv_out, e.ids, e.indices, n, H, e.vocab, e.keys, e.d_emb, s);
 }
 
 mb_status colsum(const bf16* x, int n, int C, float* out, cudaStream_t s) {

@@ -26,7 +26,13 @@ int num_sms() {
   std::call_once(g_sms_once[dev], [dev] {
     int n = 0;
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    g_sms[dev] = n > 0 ? n : 148;
+    n = n > 0 ? n : 148;
+    // MB_SM_CARVEOUT=k: the persistent grids leave k SMs idle (kept even for the CTA pairs), where a
+    // concurrent NCCL bucket reduction runs without waiting for a kernel boundary (data parallelism)
+    const char* c = std::getenv("MB_SM_CARVEOUT");
+    const int k = c ? std::atoi(c) : 0;
+    if (k > 0 && k < n - 2) n = (n - k) & ~1;
+    g_sms[dev] = n;
   });
   return g_sms[dev];
 }

@@ -45,8 +45,8 @@ class ModelDims:
     layers: int
     ln_eps: float = 1e-12
 
-    def c(self) -> L.Dims:
-        return L.dims(self.hidden, self.heads, self.intermediate, self.vocab, self.ln_eps)
+    def c(self, deterministic: bool = False) -> L.Dims:
+        return L.dims(self.hidden, self.heads, self.intermediate, self.vocab, self.ln_eps, deterministic)
 
 
 def param_count(d: ModelDims) -> int:
@@ -95,10 +95,11 @@ class MosaicBert:
 
     def __init__(self, dims: ModelDims, params: dict | None = None, device: str | torch.device = "cuda",
                  process_group=None, dropout: float = 0.0, seed: int = 0, lr_peak: float = 5e-4,
-                 total_steps: int | None = None):
+                 total_steps: int | None = None, deterministic: bool = False):
         """dropout: F2 feed-forward dropout probability (P:152 uses 0.1; R13/R32).  Each micro-step
         draws its masks from seed_of(micro-step), a pure function of (seed, rank, micro-step index).
-        lr_peak / total_steps: the F1 schedule (Table A1: 5e-4 Base, 2e-4 Large)."""
+        lr_peak / total_steps: the F1 schedule (Table A1: 5e-4 Base, 2e-4 Large).
+        deterministic: bitwise-reproducible gradient reductions (MB_FLAG_DETERMINISTIC; slower)."""
         if not 0.0 <= dropout < 1.0:
             raise ValueError("dropout must be in [0, 1)")
         self.dropout = float(dropout)
@@ -107,7 +108,8 @@ class MosaicBert:
         self.total_steps = total_steps
         self.micro_index = 0
         self.d = dims
-        self.cd = dims.c()
+        self.deterministic = bool(deterministic)
+        self.cd = dims.c(self.deterministic)
         self.device = torch.device(device)
         L.lib()  # fail loudly now if the library is missing
         H, I, V = dims.hidden, dims.intermediate, dims.vocab
@@ -180,6 +182,8 @@ class MosaicBert:
         self.saved = [torch.empty(sb, dtype=torch.uint8, device=dev) for _ in range(self.d.layers)]
         self.ws = torch.empty(L.layer_workspace_bytes(self.cd, T, Lmax), dtype=torch.uint8, device=dev)
         self.dy = [torch.empty(T, H, dtype=torch.bfloat16, device=dev) for _ in range(2)]
+        eb = L.embed_workspace_bytes(self.cd, T)
+        self.emb_ws = torch.empty(eb, dtype=torch.uint8, device=dev) if eb else None
         self.lse = torch.empty(T, dtype=torch.float32, device=dev)
         self._cap = (B, Lmax)
 
@@ -304,7 +308,7 @@ class MosaicBert:
                 handles.append(self._allreduce(self.layer_buckets[l]))
         g = self.emb_bucket.gv
         L.embed_backward(cd, ids, self.indices, nnz, e["emb"], e["type_emb"], e["lne_g"], self.estats, dy, g["emb"],
-                         g["type_emb"][0], g["lne_g"], g["lne_b"])
+                         g["type_emb"][0], g["lne_g"], g["lne_b"], ws=self.emb_ws)
         if allreduce:
             handles.append(self._allreduce(self.emb_bucket))
         self._handles = [h for h in handles if h is not None]
