@@ -5,10 +5,13 @@
 One step = one optimizer step of the whole hot path on every rank: unpad index + MLM select (A1),
 embedding (A3), 12 encoder layers forward (A4-A9), MLM head + CE forward/backward (A11), 12 layers
 backward (A10, A4-A9 bwd), embedding backward, NCCL gradient allreduce overlapped with the backward
-(A12), fused AdamW (F1).  Per GPU one micro-batch of 512 sequences x 128, so the global
-batch is 512*N (4096 at N = 8): weak scaling.
+(A12), fused AdamW (F1).  The global batch is 4096 sequences at every N: each
+rank runs accumulation = 4096 / (N x micro) micro-batches of 512 sequences x 128 per
+optimizer step (8/N at C2), the gradient allreduce overlapping the last micro-step's backward.
+Per-GPU work per micro-step is the same at every N: weak scaling.  (--accum 1: one micro-batch per
+optimizer step, global batch 512 N.)
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--accum A] [--impl ours|reference]
 
 Prints ONE JSON line on rank 0.  `--impl reference` times the fp64 CPU oracle (the reference arm of
 this tier) on a bounded sample of the same workload.
@@ -138,6 +141,43 @@ def cpu_cores():
         return os.cpu_count()
 
 
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def oracle_baseline(cfg: str, n_seq: int):
+    """the oracle as it stands, 1 warm-up + 3 timed runs, median, on the host cores."""
+    time_oracle(cfg, n_seq, reps=1)
+    ntok, ts = time_oracle(cfg, n_seq, reps=3)
+    med = statistics.median(ts)
+    return {"value": ntok / med, "unit": "tokens/s", "cores": cpu_cores(), "cpu_model": cpu_model(), "kind": "oracle",
+            "sample": f"first {n_seq} sequences of the rank-0 {cfg} micro-batch ({ntok} non-pad tokens), full-depth "
+                      f"fp64 step (embedding, {synth.CONFIGS[cfg].dims.layers} layers fwd+bwd, head+CE); 1 warm-up "
+                      f"+ median of 3 runs ({', '.join(f'{t:.1f}' for t in ts)} s)",
+            "note": "unoptimised fp64 correctness oracle (numpy/OpenBLAS on the host cores), not a tuned baseline"}
+
+
+def step_flops(cfg: str, lens, n_masked: int):
+    """Algorithmic FLOPs of one micro-step: encoder GEMMs 6 (3H^2 + H^2 + 2IH + IH) per
+    token and layer, attention 12 H l_b per token of a length-l_b sequence and layer (QK^T, PV forward
+    + 4 backward products), MLM head 6 (H^2 + H V) per masked token.  (MFU instead credits 6 N per
+    token, Eq. 3.)"""
+    d = synth.CONFIGS[cfg].dims
+    H, I, V, nl = d.hidden, d.intermediate, d.vocab, d.layers
+    T = float(np.sum(lens))
+    gemm = 6.0 * nl * (3 * H * H + H * H + 2 * I * H + I * H) * T
+    attn = 12.0 * nl * H * float(np.sum(np.asarray(lens, dtype=np.float64) ** 2))
+    head = 6.0 * (H * H + H * V) * n_masked
+    return gemm + attn + head
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -156,7 +196,7 @@ def run_reference(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_name(args.config), "sample": f"first {n_seq} sequences of the rank-0 "
                    f"micro-batch ({ntok} non-pad tokens), full-depth model", "parallelism": "host cores"},
-        "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+        "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "cpu_model": cpu_model(), "kind": "oracle",
                          "sample": f"{n_seq} sequences x {synth.CONFIGS[args.config].seq_len}, {ntok} tokens"},
         "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -172,7 +212,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--oracle-seqs", type=int, default=16)
+    ap.add_argument("--oracle-seqs", type=int, default=8)
+    ap.add_argument("--accum", type=int, default=None,
+                    help="micro-steps per optimizer step (default: global batch 4096 sequences, P:177)")
+    ap.add_argument("--nccl-sm-carveout", type=int, default=0,
+                    help="leave this many SMs out of the persistent kernels' grids (NCCL kernels run there)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--micro", type=int, default=None, help="override the per-GPU micro-batch")
@@ -181,6 +225,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.nccl_sm_carveout:
+        os.environ["MB_SM_CARVEOUT"] = str(args.nccl_sm_carveout)  # read by the library at first launch
 
     import torch
     import torch.distributed as dist
@@ -212,25 +258,35 @@ def main():
     del params
     n_params = param_count(dims)
 
-    # synthetic batches for this rank (inputs resident in HBM for the device-timed value)
-    nb = 2
+    accum = args.accum or max(1, 4096 // (world * micro))  # global batch 4096
+
+    # synthetic micro-batches for this rank (inputs resident in HBM for the device-timed value)
+    nb = max(2, accum)
     host = []
     for i in range(nb):
         b = synth.make_batch(cfg, 1000 * int(args.config[1]) + 17 * rank + i, B=micro)
         host.append({k: torch.from_numpy(b[k]).pin_memory() for k in ("input_ids", "attention_mask", "labels")})
     dev = [{k: v.cuda() for k, v in h.items()} for h in host]
     tokens = [int(h["attention_mask"].sum()) for h in host]
+    lens = [h["attention_mask"].sum(1).numpy() for h in host]
 
     # (nnz, max_seqlen, n_masked) of each batch from its host copy: the step then needs no device->host
     # read of the unpad results (they are still computed on the device and verified one step later)
     metas = [MosaicBert.batch_meta(h["attention_mask"], h["labels"]) for h in host]
+    flops = [step_flops(args.config, lens[i], metas[i][2]) for i in range(nb)]
+
+    def micro_ids(i):
+        return [(i * accum + j) % nb for j in range(accum)]
 
     def step(i, hostcopy=False):
-        b = dev[i % nb]
-        if hostcopy:
-            for k in b:
-                b[k].copy_(host[i % nb][k], non_blocking=True)
-        return model.train_step([(b["input_ids"], b["attention_mask"], b["labels"])], host_meta=[metas[i % nb]])
+        mbs = []
+        for j in micro_ids(i):
+            b = dev[j]
+            if hostcopy:
+                for k in b:
+                    b[k].copy_(host[j][k], non_blocking=True)
+            mbs.append((b["input_ids"], b["attention_mask"], b["labels"]))
+        return model.train_step(mbs, host_meta=[metas[j] for j in micro_ids(i)])
 
     def barrier():
         if world > 1:
@@ -256,22 +312,29 @@ def main():
     barrier()
 
     # ---- device-timed value: inputs resident, K steps between CUDA events, max over ranks
-    probe = L.Probe(1, capacity=2 * d.layers * args.steps + 8)
+    probe = L.Probe(1, capacity=2 * d.layers * accum * args.steps + 8)
     n0 = L.launch_count()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    profile_range = os.environ.get("MB_PROFILE_RANGE") == "1"  # nsys --capture-range=cudaProfilerApi
     with Clocks(local) as clk, probe:
         barrier()
-        ev0.record()
+        if profile_range:
+            torch.cuda.profiler.start()
+        evs[0].record()
         loss = None
         for i in range(args.steps):
             loss = step(i)
-        ev1.record()
+            evs[i + 1].record()
         barrier()
+        if profile_range:
+            torch.cuda.profiler.stop()
     model.check_meta()
     launches = (L.launch_count() - n0) // args.steps
-    ms = ev0.elapsed_time(ev1)
+    ms = evs[0].elapsed_time(evs[-1])
+    per_step = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
     ms_max = max_over_ranks(ms)
-    tok_step = sum_over_ranks(float(np.mean([tokens[i % nb] for i in range(args.steps)])))
+    tok_step = sum_over_ranks(float(np.mean([sum(tokens[j] for j in micro_ids(i)) for i in range(args.steps)])))
+    flop_step = sum_over_ranks(float(np.mean([sum(flops[j] for j in micro_ids(i)) for i in range(args.steps)])))
     value = tok_step * args.steps / (ms_max / 1e3)
     clocks = clk.summary()
     loss_val = sum_over_ranks(float(loss.item()))  # each rank holds its share of the global mean (R18)
@@ -312,34 +375,41 @@ def main():
         barrier()
         model.check_meta()
         ems = max_over_ranks(e0.elapsed_time(e1))
-        h2d = sum(int(v.numel() * v.element_size()) for v in host[0].values())
+        h2d = accum * sum(int(v.numel() * v.element_size()) for v in host[0].values())
         e2e = {"value": tok_step * args.steps / (ems / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": 4, "ms_per_step": ems / args.steps}
 
     # ---- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        ntok, ts = time_oracle(args.config, args.oracle_seqs, reps=1)
-        cpu = {"value": ntok / ts[0], "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
-               "sample": f"first {args.oracle_seqs} sequences of the rank-0 micro-batch ({ntok} tokens), "
-                         f"full 12-layer fp64 step, {ts[0]:.1f} s"}
+        cpu = oracle_baseline(args.config, args.oracle_seqs)
 
     if rank == 0:
         tok_s = value
         mfu_ds = 6.0 * n_params * tok_s / (world * PEAK_DATASHEET)
         mfu_meas = 6.0 * n_params * tok_s / (world * pk["bf16_tflops"] * 1e12)
+        flop_s = flop_step * args.steps / (ms_max / 1e3)
+        q = np.quantile(per_step, [0.1, 0.5, 0.9])
         line = {
             "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": (tok_s / PAPER_TOKS) if (world == 8 and args.config == "C2") else None,
+            "vs_baseline": None,  # BASELINE.md has no number for this metric on B200 (the paper's 8xA100 row is context)
+            "step_ms_p10_p50_p90": [float(x) for x in q],
             "dtype": "bf16", "data": "synthetic (seeded; random BERT-init weights)",
-            "config": {"workload": workload_name(args.config), "global_batch": micro * world,
-                       "micro_batch_per_gpu": micro, "seq_len": cfg.seq_len, "parallelism": f"dp{world}",
+            "config": {"workload": workload_name(args.config), "global_batch": micro * world * accum,
+                       "micro_batch_per_gpu": micro, "accumulation": accum, "seq_len": cfg.seq_len,
+                       "parallelism": f"dp{world}", "nccl_sm_carveout": args.nccl_sm_carveout,
                        "non_pad_tokens_per_step": tok_step, "l2": "working set >> L2 (weights 275 MB + "
                        "activations ~25 GB per step), no flush needed",
                        "optimizer": "fused AdamW inside the step", "ffn_dropout": args.dropout},
             "mfu": {"datasheet_2.25PF": mfu_ds, "measured_peak": mfu_meas, "n_params": n_params,
                     "formula": "6 N tok/s / (G peak) (Eq. 3, P:608)"},
+            "hfu": {"datasheet_2.25PF": flop_s / (world * PEAK_DATASHEET),
+                    "measured_peak": flop_s / (world * pk["bf16_tflops"] * 1e12),
+                    "measured_sustained": flop_s / (world * pk["bf16_tflops_sustained"] * 1e12),
+                    "algorithmic_tflop_per_step": flop_step / 1e12,
+                    "formula": "SURVEY 8(d) algorithmic FLOPs (GEMMs + attention at each sequence's own l + head on "
+                               "the masked rows) / time / (G peak)"},
             "loss": loss_val,
             "clocks": clocks,
             "gpu_launches": int(launches),

@@ -359,21 +359,43 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             rphase ^= 1;
           }
         }
-        if (ep.dbias && (dkb0 < dkb1 || ep.dpart)) {
+        if (ep.dbias && ep.dpart) {
+          // deterministic mode: the 8 warps' partials (same 128 rows, different k-rows) meet in shared
+          // memory and warp 4 writes one partial per (split, column tile), summed in order later
+#pragma unroll
+          for (int e = 0; e < 8; ++e) dbs[e] += __shfl_xor_sync(0xffffffffu, dbs[e], 16);
+          if (lane < 16) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              asm volatile("st.shared.f32 [%0], %1;" ::"r"(scrA + (lane * 8 + e) * 4), "f"(dbs[e]) : "memory");
+          }
+          asm volatile("bar.sync 1, %0;" ::"r"(32 * NUM_EPI_WARPS) : "memory");
+          if (ew == 0 && lane < 16) {
+            const uint32_t s0 = sm100::smem_u32(scr_base);
+            float acc8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            for (int w = 0; w < NUM_EPI_WARPS; ++w) {
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                float x;
+                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(s0 + w * NSCR * SCR_BYTES + (lane * 8 + e) * 4));
+                acc8[e] += x;
+              }
+            }
+            const int m0 = (mb * CG + rank) * BM + lane * 8;
+            float* dp = ep.dpart + (int64_t)(kb0 / sc.kb_per * sc.num_n + nb) * M;
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (m0 + e < M) dp[m0 + e] = acc8[e];
+          }
+          asm volatile("bar.sync 1, %0;" ::"r"(32 * NUM_EPI_WARPS) : "memory");
+        } else if (ep.dbias && dkb0 < dkb1) {
 #pragma unroll
           for (int e = 0; e < 8; ++e) dbs[e] += __shfl_xor_sync(0xffffffffu, dbs[e], 16);
           const int m0 = (mb * CG + rank) * BM + ch * 8;
           if (lane < 16) {
-            if (ep.dpart) {  // deterministic mode: one partial per (split, column tile), summed in order later
-              float* dp = ep.dpart + (int64_t)(kb0 / sc.kb_per * sc.num_n + nb) * M;
 #pragma unroll
-              for (int e = 0; e < 8; ++e)
-                if (m0 + e < M) dp[m0 + e] = dbs[e];
-            } else {
-#pragma unroll
-              for (int e = 0; e < 8; ++e)
-                if (m0 + e < M) atomicAdd(ep.dbias + m0 + e, dbs[e]);
-            }
+            for (int e = 0; e < 8; ++e)
+              if (m0 + e < M) atomicAdd(ep.dbias + m0 + e, dbs[e]);
           }
         }
       }

@@ -30,12 +30,13 @@ def test_bench_two_ranks_gloo():
     env = dict(os.environ, MB_DIST_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"),
-           "--gpus", "2", "--steps", "2", "--warmup", "3", "--micro", "32", "--no-cpu-baseline"]
+           "--gpus", "2", "--steps", "2", "--warmup", "3", "--micro", "32", "--accum", "2", "--no-cpu-baseline"]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["config"]["parallelism"] == "dp2"
-    assert line["config"]["global_batch"] == 64 and line["value"] > 0
+    # 2 ranks x 2 accumulated micro-steps x 32 sequences per optimizer step
+    assert line["config"]["global_batch"] == 128 and line["config"]["accumulation"] == 2 and line["value"] > 0
     # the loss is the global mean over both ranks' masked tokens: near ln V at BERT init
     assert 9.0 < line["loss"] < 11.5, line["loss"]
     assert line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
