@@ -12,14 +12,15 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
-OBJ = os.path.join(HERE, "build")
-LIB = os.path.join(HERE, "libmosaicbert.so")
+OBJ = os.path.join(HERE, "build" + os.environ.get("MB_OBJ_SUFFIX", ""))
+LIB = os.environ.get("MB_LIB_OUT") or os.path.join(HERE, "libmosaicbert.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
 if os.environ.get("MB_WATCHDOG", "0") == "1":  # debug build: mbarrier waits trap after a timeout
     FLAGS.append("-DMB_WATCHDOG")
+FLAGS += os.environ.get("MB_EXTRA_FLAGS", "").split()  # diagnostic builds only (scripts/build_diag.sh)
 SOURCES = ["runtime.cu", "unpad.cu", "layernorm.cu", "gemm.cu", "attention.cu", "head.cu", "api.cu", "ablation.cu",
            "reduce.cu"]
 
