@@ -17,6 +17,7 @@
 //   128 < l <= 2048 (C4, F4): forward units = (query tile, head, sequence) with the online softmax
 //   over key tiles; backward units = (key tile, head, sequence) over query tiles, dQ reduced in fp32.
 #include <algorithm>
+#include <cstdlib>
 #include "common.cuh"
 #include "kernels.h"
 #include "sm100.cuh"
@@ -644,6 +645,346 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
     }
     if (pend_u >= 0) epilogue(pend_u, pend_uc, pend_m, sPa + ((g - 1) & 1) * P_BYTES);
     if (lane == 0) sm100::bulk_wait0();
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  if (warp == 0) sm100::tmem_dealloc(tbase, 512);
+}
+
+// Long-sequence forward, v2: two query tiles per unit, ping-ponged (the FlashAttention-4 schedule
+// on sm_100a).  A unit = (query tiles 2p and 2p+1, head, sequence); the two tiles share every K/V
+// tile the TMA warp streams in.  Softmax warpgroup t (warps 4t..4t+3) owns query tile t with ONE
+// thread per query row (128 keys per thread: no cross-thread row-max exchange).  The MMA warp issues
+// S_t = Q_t K^T into TMEM; warpgroup t reads S_t (tcgen05.ld), adds the ALiBi bias, exponentiates in
+// the exp2 domain and writes P_t back as packed bf16 over the first 64 columns of S_t (tcgen05.st);
+// O_t += P_t V then runs with A = P_t straight from tensor memory (tcgen05.mma A-in-TMEM), so P never
+// touches shared memory.  While warpgroup 0 works on tile g the MMAs of warpgroup 1's tile
+// (PV_1(g-1), S_1(g)) run, and vice versa.  The row sum l stays in registers (fp32); the O
+// accumulators are rescaled only when a row max grows by more than 2^8 (rare with the diagonal key
+// tile first).  O is double-buffered per unit parity so a unit's normalisation + store overlaps the
+// next unit's first tile.  TMEM: S_0 [0,128), S_1 [128,256), O[parity][t] at 256 + 64 (2 parity + t).
+constexpr int L2_NS = 3;
+constexpr int L2_THREADS = SH_THREADS + 128;  // softmax warpgroups 0, 1; warpgroup 2: MMA warp 8, TMA warp 9
+constexpr int L2_SMEM = 4 * TILE_BYTES + L2_NS * 2 * TILE_BYTES + 1024 + 256;
+
+struct PairUnits {  // unit u = (b * heads + h) * QP + p, valid iff 256 p < len_b
+  const int* cu;
+  int heads, QP, total;
+  __device__ __forceinline__ bool valid(int u) const {
+    const int b = u / (heads * QP), p = u % QP;
+    return p * 2 * TILE < cu[b + 1] - cu[b];
+  }
+  __device__ __forceinline__ int next(int u) const {
+    for (u += gridDim.x; u < total; u += gridDim.x)
+      if (valid(u)) return u;
+    return total;
+  }
+  __device__ __forceinline__ int first() const {
+    int u = blockIdx.x;
+    if (u < total && !valid(u)) u = next(u);
+    return u;
+  }
+  __device__ __forceinline__ void decode(int u, int& b, int& h, int& p) const {
+    b = u / (heads * QP);
+    const int rem = u - b * heads * QP;
+    h = rem / QP;
+    p = rem - h * QP;
+  }
+};
+
+// ALiBi-biased scores of one full query row (128 keys, one thread per row), unscaled domain:
+// x_j += -slr |(r + qk_off) - j|, keys at or past `keys` masked when MASK; returns max_j
+template <bool MASK>
+__device__ __forceinline__ float row_scores128(float (&x)[128], int r, int keys, float slr, int qk_off) {
+  const float rc = (float)(r + qk_off);
+  float2 dd = make_float2(rc, rc - 1.f);
+  float2 mx2 = make_float2(-INFINITY, -INFINITY);
+#pragma unroll
+  for (int j = 0; j < 128; j += 2) {
+    float2 t = __ffma2_rn(make_float2(fabsf(dd.x), fabsf(dd.y)), make_float2(-slr, -slr), make_float2(x[j], x[j + 1]));
+    dd = __fadd2_rn(dd, make_float2(-2.f, -2.f));
+    if (MASK) {
+      t.x = j < keys ? t.x : -INFINITY;
+      t.y = j + 1 < keys ? t.y : -INFINITY;
+    }
+    x[j] = t.x;
+    x[j + 1] = t.y;
+    mx2 = make_float2(fmaxf(mx2.x, t.x), fmaxf(mx2.y, t.y));
+  }
+  return fmaxf(mx2.x, mx2.y);
+}
+
+__global__ void __launch_bounds__(L2_THREADS, 1) attn_fwd_long2_kernel(const __grid_constant__ CUtensorMap tm_qkv,
+                                                                      PairUnits U, int d,
+                                                                      const float* __restrict__ slopes,
+                                                                      bf16* __restrict__ O, float* __restrict__ lse,
+                                                                      int nnz) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;                  // [unit parity][tile] Q
+  uint8_t* sKV = sQ + 4 * TILE_BYTES;  // L2_NS x (K, V)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + L2_NS * 2 * TILE_BYTES);
+  uint64_t* q_full = bars;                  // [2] per unit parity
+  uint64_t* q_empty = bars + 2;             // [2]
+  uint64_t* kv_full = bars + 4;             // [L2_NS]
+  uint64_t* kv_empty = bars + 4 + L2_NS;    // [L2_NS]
+  uint64_t* s_full = bars + 4 + 2 * L2_NS;  // [2] per query tile t
+  uint64_t* p_ready = s_full + 2;           // [2] per t, 4 warps arrive
+  uint64_t* pv_done = s_full + 4;           // [2] per t, one phase per PV_t
+  uint64_t* o_full = s_full + 6;            // [2] per unit parity: the unit's last PVs are done
+  uint64_t* o_empty = s_full + 8;           // [2] per unit parity: 8 softmax warps have read O
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(s_full + 10);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int H = U.heads * d;
+  if (tid == 0) {
+    sm100::tma_prefetch(&tm_qkv);
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&q_full[i], 1);
+      sm100::mbar_init(&q_empty[i], 1);
+      sm100::mbar_init(&s_full[i], 1);
+      sm100::mbar_init(&p_ready[i], 4);
+      sm100::mbar_init(&pv_done[i], 1);
+      sm100::mbar_init(&o_full[i], 1);
+      sm100::mbar_init(&o_empty[i], 8);
+    }
+    for (int i = 0; i < L2_NS; ++i) {
+      sm100::mbar_init(&kv_full[i], 1);
+      sm100::mbar_init(&kv_empty[i], 1);
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 0) sm100::tmem_alloc(tslot, 512);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tbase = *tslot;
+  pdl_wait();
+  pdl_trigger();
+  const uint32_t sQa = sm100::smem_u32(sQ), sKVa = sm100::smem_u32(sKV);
+  // geometry of unit u: first token st, length len, key tiles nkv, second query tile present
+  auto geom = [&](int u, int& b, int& h, int& p, int& st, int& len, int& nkv, bool& two) {
+    U.decode(u, b, h, p);
+    st = U.cu[b];
+    len = U.cu[b + 1] - st;
+    nkv = (len + TILE - 1) / TILE;
+    two = (2 * p + 1) * TILE < len;
+  };
+
+  // registers: 12 warps leave 168 per thread; the producer/issuer warpgroup (warps 8-11) hands most
+  // of its share to the two softmax warpgroups (a full 128-key score row per thread lives in registers)
+  if (warp >= 8) {
+    sm100::setmaxnreg_dec<64>();
+    if (warp == 9) {
+    // ------------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int uc = 0, g = 0;
+      for (int u = U.first(); u < U.total; u = U.next(u), ++uc) {
+        int b, h, p, st, len, nkv;
+        bool two;
+        geom(u, b, h, p, st, len, nkv, two);
+        const int qb = uc & 1;
+        sm100::mbar_wait(&q_empty[qb], ((uc >> 1) & 1) ^ 1);
+        sm100::mbar_arrive_expect_tx(&q_full[qb], (two ? 2 : 1) * TILE_BYTES);
+        sm100::tma_load_2d(sQ + 2 * qb * TILE_BYTES, &tm_qkv, &q_full[qb], h * d, st + 2 * p * TILE);
+        if (two) sm100::tma_load_2d(sQ + (2 * qb + 1) * TILE_BYTES, &tm_qkv, &q_full[qb], h * d, st + (2 * p + 1) * TILE);
+        for (int jj = 0; jj < nkv; ++jj, ++g) {
+          const int j = (2 * p + jj) % nkv;  // query tile 0's diagonal key tile first
+          const int sg = g % L2_NS;
+          sm100::mbar_wait(&kv_empty[sg], ((g / L2_NS) & 1) ^ 1);
+          uint8_t* kv = sKV + sg * 2 * TILE_BYTES;
+          sm100::mbar_arrive_expect_tx(&kv_full[sg], 2 * TILE_BYTES);
+          sm100::tma_load_2d(kv, &tm_qkv, &kv_full[sg], H + h * d, st + j * TILE);
+          sm100::tma_load_2d(kv + TILE_BYTES, &tm_qkv, &kv_full[sg], 2 * H + h * d, st + j * TILE);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 8) {
+    // ------------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t id_s = sm100::idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t id_o = sm100::idesc_bf16(128, 64, 0, 1);
+      int uc = 0, g = 0, c0 = 0, c1 = 0;
+      auto issue_s = [&](int t, uint32_t q, int sg) {  // S_t = Q_t K_sg^T
+        const uint32_t k = sKVa + sg * 2 * TILE_BYTES;
+        for (int kk = 0; kk < d / 16; ++kk)
+          sm100::mma_bf16_ss(tbase + 128 * t, sm100::desc_kmajor_sw128(q + kk * 32), sm100::desc_kmajor_sw128(k + kk * 32),
+                             id_s, kk > 0);
+        sm100::mma_commit(&s_full[t]);
+      };
+      auto issue_pv = [&](int t, int qb, int sg, bool acc) {  // O[qb][t] += P_t V_sg, P_t from TMEM
+        const uint32_t v = sKVa + sg * 2 * TILE_BYTES + TILE_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < TILE / 16; ++kk)
+          sm100::mma_bf16_ts(tbase + 256 + 64 * (2 * qb + t), tbase + 128 * t + 8 * kk,
+                             sm100::desc_mnmajor_sw128(v + kk * 2048, 8192), id_o, (acc || kk > 0) ? 1u : 0u);
+        sm100::mma_commit(&pv_done[t]);
+      };
+      for (int u = U.first(); u < U.total; u = U.next(u), ++uc) {
+        int b, h, p, st, len, nkv;
+        bool two;
+        geom(u, b, h, p, st, len, nkv, two);
+        const int qb = uc & 1;
+        const uint32_t q0 = sQa + 2 * qb * TILE_BYTES, q1 = q0 + TILE_BYTES;
+        sm100::mbar_wait(&q_full[qb], (uc >> 1) & 1);
+        sm100::mbar_wait(&o_empty[qb], ((uc >> 1) & 1) ^ 1);  // unit uc-2's O has been read out
+        sm100::tc_fence_after();
+        for (int jj = 0; jj < nkv; ++jj, ++g) {
+          const int sg = g % L2_NS, sg2 = (g + 1) % L2_NS;
+          if (jj == 0) {
+            sm100::mbar_wait(&kv_full[sg], (g / L2_NS) & 1);
+            sm100::tc_fence_after();
+            issue_s(0, q0, sg);
+            if (two) issue_s(1, q1, sg);
+          }
+          sm100::mbar_wait(&p_ready[0], c0 & 1);
+          sm100::tc_fence_after();
+          issue_pv(0, qb, sg, jj > 0);
+          ++c0;
+          if (jj + 1 < nkv) {
+            sm100::mbar_wait(&kv_full[sg2], ((g + 1) / L2_NS) & 1);
+            sm100::tc_fence_after();
+            issue_s(0, q0, sg2);  // after PV_0 in issue order: overwrites P_0 only once it is read
+          }
+          if (two) {
+            sm100::mbar_wait(&p_ready[1], c1 & 1);
+            sm100::tc_fence_after();
+            issue_pv(1, qb, sg, jj > 0);
+            ++c1;
+          }
+          sm100::mma_commit(&kv_empty[sg]);
+          if (two && jj + 1 < nkv) issue_s(1, q1, sg2);
+        }
+        sm100::mma_commit(&q_empty[qb]);
+        sm100::mma_commit(&o_full[qb]);
+      }
+    }
+    __syncwarp();
+    }
+  } else {
+    // ------------------------------------------------------------------ softmax warpgroups
+    sm100::setmaxnreg_inc<216>();  // 2 x 128 x 216 + 128 x 64 <= 384 x 168
+    const int t = warp >> 2, q4 = warp & 3;
+    const int r = q4 * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const float sc2 = rsqrtf((float)d) * LOG2E;
+    const float tau = 8.f / sc2;  // rescale only when a row max grows by more than 2^8 in P
+    const uint32_t tS = tbase + 128 * t + lane_off;
+    auto epilogue = [&](int uu, int ucc, float m_used, float l_used, bool act) {
+      int b, h, p, st, len, nkv;
+      bool two;
+      geom(uu, b, h, p, st, len, nkv, two);
+      const int qrow = (2 * p + t) * TILE + r;
+      sm100::mbar_wait(&o_full[ucc & 1], (ucc >> 1) & 1);
+      sm100::tc_fence_after();
+      if (act) {
+        const uint32_t to = tbase + 256 + 64 * (2 * (ucc & 1) + t) + lane_off;
+        const float inv = 1.f / l_used;
+        bf16* dst = O + (size_t)(st + qrow) * H + h * d;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          float o[32];
+          sm100::tmem_ld32(to + 32 * hh, o);
+          sm100::tmem_ld_wait();
+          if (32 * hh < d && qrow < len) {
+#pragma unroll
+            for (int c = 0; c < 32; c += 8) {
+              float w[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) w[e] = o[c + e] * inv;
+              *reinterpret_cast<uint4*>(dst + 32 * hh + c) = f32_to_bf16x8(w);
+            }
+          }
+        }
+        if (qrow < len) lse[(size_t)h * nnz + st + qrow] = (m_used * sc2 + log2f(l_used)) * LN2;
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&o_empty[ucc & 1]);
+    };
+    int uc = 0, c = 0;
+    int pend_u = -1, pend_uc = 0;
+    float pend_m = 0.f, pend_l = 1.f;
+    bool pend_act = false;
+    for (int u = U.first(); u < U.total; u = U.next(u), ++uc) {
+      int b, h, p, st, len, nkv;
+      bool two;
+      geom(u, b, h, p, st, len, nkv, two);
+      const bool act = t == 0 || two;
+      const int q0 = (2 * p + t) * TILE;
+      const float slr = slopes[h] * sqrtf((float)d);  // m_h / (1/sqrt(d)): bias in the unscaled domain
+      float m = -INFINITY, l = 0.f;
+      for (int jj = 0; jj < nkv; ++jj) {
+        if (act) {
+          const int kv0 = ((2 * p + jj) % nkv) * TILE;
+          sm100::mbar_wait(&s_full[t], c & 1);
+          sm100::tc_fence_after();
+          float x[128];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) sm100::tmem_ld32(tS + 32 * i, x + 32 * i);
+          sm100::tmem_ld_wait();
+          const int keys = len - kv0;
+          const float mx = keys >= TILE ? row_scores128<false>(x, r, keys, slr, q0 - kv0)
+                                        : row_scores128<true>(x, r, keys, slr, q0 - kv0);
+          if (jj == 0) {
+            m = mx;
+          } else if (__any_sync(0xffffffffu, mx > m + tau)) {
+            // rescale this warp's O rows (after PV_t of the previous key tile has landed)
+            const float m_new = fmaxf(m, mx);
+            const float alpha = ex2_approx((m - m_new) * sc2);
+            sm100::mbar_wait(&pv_done[t], (c - 1) & 1);
+            sm100::tc_fence_after();
+            const uint32_t to = tbase + 256 + 64 * (2 * (uc & 1) + t) + lane_off;
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              float o[32];
+              sm100::tmem_ld32(to + 32 * hh, o);
+              sm100::tmem_ld_wait();
+#pragma unroll
+              for (int e = 0; e < 32; ++e) o[e] *= alpha;
+              sm100::tmem_st32(to + 32 * hh, o);
+            }
+            sm100::tmem_st_wait();
+            l *= alpha;
+            m = m_new;
+          }
+          // P = 2^(sc (s - m)) as packed bf16 pairs written in place over x[0..63] -> S_t columns [0, 64)
+          const float nm = -m * sc2;
+          float2 ls = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {  // keys [64 hh, 64 hh + 64) -> P columns [32 hh, 32 hh + 32)
+            float pk[32];  // packed bf16 pairs (bit patterns)
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int k = 64 * hh + 2 * j;
+              const float2 tt = __ffma2_rn(make_float2(x[k], x[k + 1]), make_float2(sc2, sc2), make_float2(nm, nm));
+              const float2 e = make_float2(ex2_approx(tt.x), ex2_approx(tt.y));
+              ls = __fadd2_rn(ls, e);
+              pk[j] = __uint_as_float(pack_bf16x2(e.x, e.y));
+            }
+            sm100::tmem_st32(tS + 32 * hh, pk);
+          }
+          l += ls.x + ls.y;
+          sm100::tmem_st_wait();
+          sm100::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) sm100::mbar_arrive(&p_ready[t]);
+          ++c;
+        }
+        if (jj == 0 && pend_u >= 0) {  // the previous unit's O: normalise and store
+          epilogue(pend_u, pend_uc, pend_m, pend_l, pend_act);
+          pend_u = -1;
+        }
+      }
+      pend_u = u;
+      pend_uc = uc;
+      pend_m = m;
+      pend_l = l;
+      pend_act = act;
+    }
+    if (pend_u >= 0) epilogue(pend_u, pend_uc, pend_m, pend_l, pend_act);
   }
   sm100::tc_fence_before();
   __syncthreads();
@@ -1434,6 +1775,27 @@ mb_status attention_fwd(const bf16* qkv, const int* cu, int batch, int nnz, int 
     const int grid = std::max(1, std::min(units, num_sms()));
     if (launch_pdl(attn_fwd_short_kernel, dim3(grid), dim3(SH_FWD_THREADS), SH_FWD_SMEM2, s, 1, tm, tmo, cu, batch,
                    heads, d, slopes, O, lse, nnz) != cudaSuccess)
+      return MB_ERR_CUDA;
+    MB_CHECK_LAUNCH();
+    return MB_OK;
+  }
+  static const bool v1 = [] {  // MB_ATTN_LONG_FWD=v1: the round-1 one-query-tile kernel (A/B)
+    const char* e = std::getenv("MB_ATTN_LONG_FWD");
+    return e && e[0] == 'v' && e[1] == '1';
+  }();
+  if (!v1) {
+    static bool attr_2 = false;
+    if (!attr_2) {
+      if (cudaFuncSetAttribute(attn_fwd_long2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L2_SMEM) !=
+          cudaSuccess)
+        return MB_ERR_CUDA;
+      attr_2 = true;
+    }
+    PairUnits P{cu, heads, (max_seqlen + 2 * TILE - 1) / (2 * TILE), 0};
+    P.total = batch * heads * P.QP;
+    const int grid = std::max(1, std::min(P.total, num_sms()));
+    if (launch_pdl(attn_fwd_long2_kernel, dim3(grid), dim3(L2_THREADS), L2_SMEM, s, 1, tm, P, d, slopes, O, lse,
+                   nnz) != cudaSuccess)
       return MB_ERR_CUDA;
     MB_CHECK_LAUNCH();
     return MB_OK;

@@ -3,7 +3,9 @@
 import sys
 import numpy as np
 import torch
-from paper_2312_17482_b200 import _lib as L
+import os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2312_17482_b200 import _lib as L  # noqa: E402
 
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 128
 Lq = int(sys.argv[2]) if len(sys.argv) > 2 else 512

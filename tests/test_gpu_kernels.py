@@ -294,6 +294,50 @@ def test_attention_fwd_bwd(case):
     assert np.max(np.abs(np64(db)[H:2 * H])) <= 2e-2 * np.max(np.abs(dbref))
 
 
+@pytest.mark.parametrize("lo,hi,nseq", [(129, 512, 180), (257, 1024, 60)])
+def test_attention_long_many_units(lo, hi, nseq):
+    """Long path with several work units per persistent CTA (units > SMs), ragged lengths including
+    odd query-tile counts: exercises the cross-unit pipeline (deferred O epilogue, O double-buffering,
+    barrier phases across units).  Oracle per sequence (B = 1) to keep host memory small."""
+    heads, d = 4, 64
+    H = heads * d
+    rng = np.random.default_rng(lo + hi)
+    lens = rng.integers(lo, hi + 1, size=nseq)
+    lens[:3] = [hi, lo, 2 * 128 + 1]
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    nnz = int(cu[-1])
+    qkv_np = synth.bf16_round(rng.standard_normal((nnz, 3 * H)) * 1.5)
+    do_np = synth.bf16_round(rng.standard_normal((nnz, H)))
+    sl_np = mb.alibi_slopes(heads)
+    qkv, dO, cud, sl = _bf(qkv_np), _bf(do_np), to_dev(cu, I32), to_dev(sl_np, torch.float32)
+    Od = torch.empty(nnz, H, dtype=BF, device="cuda")
+    lse = torch.empty(heads, nnz, dtype=torch.float32, device="cuda")
+    mb.attention_forward(qkv, cud, nseq, nnz, int(lens.max()), heads, d, sl, Od, lse)
+    dqkv = torch.zeros(nnz, 3 * H, dtype=BF, device="cuda")
+    db = torch.zeros(3 * H, dtype=torch.float32, device="cuda")
+    mb.attention_backward(qkv, Od, dO, lse, cud, nseq, nnz, int(lens.max()), heads, d, sl, dqkv, db_qkv=db)
+    Og, lg, dg = np64(Od), np64(lse), np64(dqkv)
+    ref_o, ref_d = np.zeros((nnz, H)), np.zeros((nnz, 3 * H))
+    ref_l = np.zeros((heads, nnz))
+    for b in range(nseq):
+        a, e, L_ = cu[b], cu[b + 1], int(lens[b])
+        sp = lambda t: t[a:e].reshape(1, L_, heads, d)  # noqa: E731
+        C, cache = O.attention_forward(sp(qkv_np[:, :H]), sp(qkv_np[:, H:2 * H]), sp(qkv_np[:, 2 * H:]),
+                                       np.ones((1, L_)), sl_np.astype(np.float64))
+        ref_o[a:e] = C.reshape(L_, H)
+        q, k = cache[0][0], cache[1][0]
+        i = np.arange(L_)
+        s_ = np.einsum("lhd,mhd->hlm", q, k) / np.sqrt(d) - sl_np[:, None, None] * np.abs(i[:, None] - i[None, :])
+        mx = s_.max(-1)
+        ref_l[:, a:e] = np.log(np.exp(s_ - mx[..., None]).sum(-1)) + mx
+        dq, dk, dv = O.attention_backward(do_np[a:e].reshape(1, L_, heads, d), cache)
+        ref_d[a:e] = np.concatenate([x.reshape(L_, H) for x in (dq, dk, dv)], -1)
+    check(f"many{hi}.O", Og, ref_o, max_rel=2e-2)
+    assert np.max(np.abs(lg - ref_l)) < 2e-2
+    for nm, sl_ in (("dq", slice(0, H)), ("dk", slice(H, 2 * H)), ("dv", slice(2 * H, 3 * H))):
+        check(f"many{hi}.{nm}", dg[:, sl_], ref_d[:, sl_])
+
+
 def test_attention_alibi_closed_form():
     """Pin P4b on the kernel: Q = K = 0 -> weights e^{-m|i-j|}/sum (in-kernel bias, masking and the
     per-sequence position restart); l=2, m=ln 3 -> [3/4, 1/4]."""
