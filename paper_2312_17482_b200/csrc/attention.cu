@@ -313,6 +313,294 @@ __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const
   if (warp == 0) sm100::tmem_dealloc(tbase, 512);
 }
 
+// Short-sequence forward, v2 (l <= 128): the two softmax warpgroups take alternate work units
+// (unit j -> warpgroup j & 1) with one thread per query row, ping-ponged on the tensor core like the
+// long kernel v2: S_t = Q K^T into TMEM, P_t written back over S_t as packed bf16, O = P_t V with P
+// from tensor memory, O double-buffered per warpgroup so a unit's readout runs after the next
+// unit's softmax.  Q/K/V of up to four units are in flight (4 x 48 KB slots).
+// A unit is one head of a GROUP of consecutive sequences whose total length fits one 128-row tile
+// (several short sequences share a tile): sequences 4g..4g+3 form one group when their
+// lengths sum to <= 128, else pairs 2g, 2g+1 when they fit, else single sequences.  Consecutive
+// sequences are adjacent in the unpadded stream, so a group is one contiguous [<=128 x d] tile;
+// each query row attends only to the key window of its own sequence (block-diagonal mask) and the
+// ALiBi distance is the in-tile distance (positions restart with each sequence and both operands
+// of a row-key pair are in the same sequence).
+constexpr int S2_NSLOT = 4;
+constexpr int S2_THREADS = SH_THREADS + 128;
+constexpr int S2_CU_MAX = 4096;  // cu_seqlens entries cached in shared memory (batch + 1 <= this)
+constexpr int S2_UMAX = 1024;    // work units per CTA (host falls back to the v1 kernel beyond)
+constexpr int S2_SMEM = S2_NSLOT * 3 * TILE_BYTES + 1024 + 256 + 4 * S2_CU_MAX + 16 * S2_UMAX;
+
+struct GroupUnits {  // unit u = b * heads + h, valid iff a group starts at sequence b
+  const int* cu;
+  int batch, heads, total;
+  __device__ __forceinline__ int span(int b) const {  // sequences in the group starting at b, 0 if none
+    const int b4 = b & ~3;
+    if (b4 + 3 < batch && cu[b4 + 4] - cu[b4] <= TILE) return b == b4 && cu[b4 + 4] > cu[b4] ? 4 : 0;
+    const int b2 = b & ~1;
+    if (b2 + 1 < batch && cu[b2 + 2] - cu[b2] <= TILE) return b == b2 && cu[b2 + 2] > cu[b2] ? 2 : 0;
+    return cu[b + 1] > cu[b] ? 1 : 0;
+  }
+  __device__ __forceinline__ bool valid(int u) const { return span(u / heads) > 0; }
+  __device__ __forceinline__ int next(int u) const {
+    for (u += gridDim.x; u < total; u += gridDim.x)
+      if (valid(u)) return u;
+    return total;
+  }
+  __device__ __forceinline__ int first() const {
+    int u = blockIdx.x;
+    if (u < total && !valid(u)) u = next(u);
+    return u;
+  }
+};
+
+// ALiBi-biased scores of one query row r of a short tile, unscaled domain; keys outside the row's
+// window [lo, hi) are masked when MASK; returns max_j
+template <bool MASK>
+__device__ __forceinline__ float row_scores_win(float (&x)[128], int r, int lo, int hi, float slr) {
+  float rc = (float)r;
+  asm volatile("" : "+f"(rc));  // keep the distance ramp inside the unit loop (hoisted, it spills)
+  float2 dd = make_float2(rc, rc - 1.f);
+  float2 mx2 = make_float2(-INFINITY, -INFINITY);
+  const uint32_t w = (uint32_t)(hi - lo);
+#pragma unroll
+  for (int j = 0; j < 128; j += 2) {
+    float2 t = __ffma2_rn(make_float2(fabsf(dd.x), fabsf(dd.y)), make_float2(-slr, -slr), make_float2(x[j], x[j + 1]));
+    dd = __fadd2_rn(dd, make_float2(-2.f, -2.f));
+    if (MASK) {
+      t.x = (uint32_t)(j - lo) < w ? t.x : -INFINITY;
+      t.y = (uint32_t)(j + 1 - lo) < w ? t.y : -INFINITY;
+    }
+    x[j] = t.x;
+    x[j + 1] = t.y;
+    mx2 = make_float2(fmaxf(mx2.x, t.x), fmaxf(mx2.y, t.y));
+  }
+  return fmaxf(mx2.x, mx2.y);
+}
+
+__global__ void __launch_bounds__(S2_THREADS, 1) attn_fwd_short2_kernel(const __grid_constant__ CUtensorMap tm_qkv,
+                                                                       GroupUnits U, int d,
+                                                                       const float* __restrict__ slopes,
+                                                                       bf16* __restrict__ O, float* __restrict__ lse,
+                                                                       int nnz) {
+  // TMEM per warpgroup t: S_t [128 t, +128) fp32, P_t [256 + 64 t, +64) packed bf16, O_t [384 + 64 t, +64).
+  // S_t is released (s_free) as soon as the warpgroup has it in registers, so S of its next unit is
+  // computed during this unit's exponentials; the previous unit's O is read out after that load.
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* slots = smem;  // S2_NSLOT x (Q, K, V)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(slots + S2_NSLOT * 3 * TILE_BYTES);
+  uint64_t* ld_full = bars;                  // [S2_NSLOT]
+  uint64_t* ld_empty = bars + S2_NSLOT;      // [S2_NSLOT]
+  uint64_t* s_full = bars + 2 * S2_NSLOT;    // [2] per warpgroup
+  uint64_t* s_free = s_full + 2;             // [2] per warpgroup, 4 warps arrive
+  uint64_t* p_ready = s_full + 4;            // [2] per warpgroup, 4 warps arrive
+  uint64_t* o_full = s_full + 6;             // [2] per warpgroup
+  uint64_t* o_empty = s_full + 8;            // [2] per warpgroup, 4 warps arrive
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(s_full + 10);
+  int* cu_s = reinterpret_cast<int*>(s_full + 12);
+  int4* ulist = reinterpret_cast<int4*>(cu_s + S2_CU_MAX);  // this CTA's units {st, glen, h | span << 16, b}
+  __shared__ int wcount[S2_THREADS / 32 + 1];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int H = U.heads * d;
+  if (tid == 0) {
+    sm100::tma_prefetch(&tm_qkv);
+    for (int i = 0; i < S2_NSLOT; ++i) {
+      sm100::mbar_init(&ld_full[i], 1);
+      sm100::mbar_init(&ld_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&s_full[i], 1);
+      sm100::mbar_init(&s_free[i], 4);
+      sm100::mbar_init(&p_ready[i], 4);
+      sm100::mbar_init(&o_full[i], 1);
+      sm100::mbar_init(&o_empty[i], 4);
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 0) sm100::tmem_alloc(tslot, 512);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tbase = *tslot;
+  pdl_wait();
+  pdl_trigger();
+  const uint32_t slots_a = sm100::smem_u32(slots);
+  // this CTA's work-unit list, built once in shared memory by all threads (candidates u = blockIdx.x
+  // + c gridDim.x; a group span needs up to six dependent cu reads, too slow for the roles' loops)
+  for (int i = tid; i <= U.batch; i += S2_THREADS) cu_s[i] = U.cu[i];
+  __syncthreads();
+  U.cu = cu_s;
+  const int ncand = U.total > (int)blockIdx.x ? (U.total - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+  int nunits = 0;
+  for (int c0 = 0; c0 < ncand; c0 += S2_THREADS) {
+    const int c = c0 + tid;
+    const int u = (int)blockIdx.x + c * (int)gridDim.x;
+    int span = 0, b = 0;
+    if (c < ncand) {
+      b = u / U.heads;
+      span = U.span(b);
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, span > 0);
+    if (lane == 0) wcount[warp] = __popc(bal);
+    __syncthreads();
+    int off = nunits;
+    for (int w = 0; w < warp; ++w) off += wcount[w];
+    if (span > 0) {
+      const int st = cu_s[b];
+      ulist[off + __popc(bal & ((1u << lane) - 1))] = make_int4(st, cu_s[b + span] - st, (u - b * U.heads) | (span << 16), b);
+    }
+    for (int w = 0; w < S2_THREADS / 32; ++w) nunits += wcount[w];
+    __syncthreads();
+  }
+
+  if (warp >= 8) {
+    sm100::setmaxnreg_dec<64>();
+    if (warp == 9 && lane == 0) {
+      // ------------------------------------------------------------------ TMA producer
+      for (int j = 0; j < nunits; ++j) {
+        const int4 e = ulist[j];
+        const int h = e.z & 0xffff;
+#if defined(MB_DIAG_SAMELOAD)  // diagnostic builds only: every unit reads the first tile (L2-resident)
+        const int st = 0;
+#else
+        const int st = e.x;
+#endif
+        const int sl = j % S2_NSLOT;
+        sm100::mbar_wait(&ld_empty[sl], ((j / S2_NSLOT) & 1) ^ 1);
+        uint8_t* base = slots + sl * 3 * TILE_BYTES;
+        sm100::mbar_arrive_expect_tx(&ld_full[sl], 3 * TILE_BYTES);
+        sm100::tma_load_2d(base, &tm_qkv, &ld_full[sl], h * d, st);
+        sm100::tma_load_2d(base + TILE_BYTES, &tm_qkv, &ld_full[sl], H + h * d, st);
+        sm100::tma_load_2d(base + 2 * TILE_BYTES, &tm_qkv, &ld_full[sl], 2 * H + h * d, st);
+      }
+    } else if (warp == 8 && lane == 0) {
+      // ------------------------------------------------------------------ MMA issuer
+      constexpr uint32_t id_s = sm100::idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t id_o = sm100::idesc_bf16(128, 64, 0, 1);
+      auto do_pv = [&](int i) {  // O_t = P_t V of unit i (warpgroup t = i & 1, its k-th unit)
+        const int t = i & 1, k = i >> 1, sl = i % S2_NSLOT;
+        sm100::mbar_wait(&o_empty[t], (k & 1) ^ 1);  // the warpgroup's previous O has been read out
+        sm100::mbar_wait(&p_ready[t], k & 1);
+        sm100::tc_fence_after();
+        const uint32_t v = slots_a + sl * 3 * TILE_BYTES + 2 * TILE_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < TILE / 16; ++kk)
+          sm100::mma_bf16_ts(tbase + 384 + 64 * t, tbase + 256 + 64 * t + 8 * kk,
+                             sm100::desc_mnmajor_sw128(v + kk * 2048, 8192), id_o, kk > 0 ? 1u : 0u);
+        sm100::mma_commit(&ld_empty[sl]);
+        sm100::mma_commit(&o_full[t]);
+      };
+      int j = 0;
+      for (; j < nunits; ++j) {
+        const int t = j & 1, k = j >> 1, sl = j % S2_NSLOT;
+        sm100::mbar_wait(&ld_full[sl], (j / S2_NSLOT) & 1);
+        sm100::mbar_wait(&s_free[t], (k & 1) ^ 1);  // S_t of the warpgroup's previous unit is in registers
+        sm100::tc_fence_after();
+        const uint32_t q = slots_a + sl * 3 * TILE_BYTES, kt = q + TILE_BYTES;
+        for (int kk = 0; kk < d / 16; ++kk)
+          sm100::mma_bf16_ss(tbase + 128 * t, sm100::desc_kmajor_sw128(q + kk * 32),
+                             sm100::desc_kmajor_sw128(kt + kk * 32), id_s, kk > 0);
+        sm100::mma_commit(&s_full[t]);
+        if (j >= 1) do_pv(j - 1);
+      }
+      if (j >= 1) do_pv(j - 1);
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------------ softmax warpgroups
+    sm100::setmaxnreg_inc<216>();
+    const int t = warp >> 2, q4 = warp & 3;
+    const int r = q4 * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const float sc2 = rsqrtf((float)d) * LOG2E;
+    const uint32_t tS = tbase + 128 * t + lane_off, tP = tbase + 256 + 64 * t + lane_off,
+                   tO = tbase + 384 + 64 * t + lane_off;
+    // the previous unit's O: normalise, store, LSE; then O_t may be overwritten
+    auto readout = [&](int kk, int st, int h, int glen, float m_used, float l_used) {
+      sm100::mbar_wait(&o_full[t], kk & 1);
+      sm100::tc_fence_after();
+      const float inv = 1.f / l_used;
+      bf16* dst = O + (size_t)(st + r) * H + h * d;
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        float o[32];
+        sm100::tmem_ld32(tO + 32 * hh, o);
+        sm100::tmem_ld_wait();
+        if (hh == 1) {
+          sm100::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) sm100::mbar_arrive(&o_empty[t]);
+        }
+        if (32 * hh < d && r < glen) {
+#pragma unroll
+          for (int c = 0; c < 32; c += 8) {
+            float w8[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) w8[e] = o[c + e] * inv;
+            *reinterpret_cast<uint4*>(dst + 32 * hh + c) = f32_to_bf16x8(w8);
+          }
+        }
+      }
+      if (r < glen) lse[(size_t)h * nnz + st + r] = (m_used * sc2 + __log2f(l_used)) * LN2;  // l >= 1
+    };
+    int j = 0, k = 0;
+    int pk_k = -1, pk_st = 0, pk_h = 0, pk_glen = 0;
+    float pk_m = 0.f, pk_l = 1.f;
+    for (j = t; j < nunits; j += 2) {
+      const int4 ue = ulist[j];
+      const int st = ue.x, glen = ue.y, h = ue.z & 0xffff, span = ue.z >> 16, b = ue.w;
+      // this row's key window: its own sequence inside the group (rows past the group: [0, 1))
+      int lo = 0, hi = 1;
+      for (int e = 0; e < span; ++e) {
+        const int a = cu_s[b + e] - st, z = cu_s[b + e + 1] - st;
+        if (r >= a && r < z) lo = a, hi = z;
+      }
+      const float slr = slopes[h] * sqrtf((float)d);
+      sm100::mbar_wait(&s_full[t], k & 1);
+      sm100::tc_fence_after();
+      float x[128];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) sm100::tmem_ld32(tS + 32 * i, x + 32 * i);
+      sm100::tmem_ld_wait();
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&s_free[t]);  // S of the next unit may now be computed
+      if (pk_k >= 0) readout(pk_k, pk_st, pk_h, pk_glen, pk_m, pk_l);  // also frees P_t (PV done)
+      float m;
+      if (span == 1 && glen == TILE) m = row_scores_win<false>(x, r, 0, TILE, slr);
+      else m = row_scores_win<true>(x, r, lo, hi, slr);
+      const float nm = -m * sc2;
+      float2 ls = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        float pk[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const int c = 64 * hh + 2 * q;
+          const float2 tt = __ffma2_rn(make_float2(x[c], x[c + 1]), make_float2(sc2, sc2), make_float2(nm, nm));
+          const float2 e = make_float2(ex2_approx(tt.x), ex2_approx(tt.y));
+          ls = __fadd2_rn(ls, e);
+          pk[q] = __uint_as_float(pack_bf16x2(e.x, e.y));
+        }
+        sm100::tmem_st32(tP + 32 * hh, pk);
+      }
+      sm100::tmem_st_wait();
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&p_ready[t]);
+      pk_k = k, pk_st = st, pk_h = h, pk_glen = glen, pk_m = m, pk_l = ls.x + ls.y;
+      ++k;
+    }
+    if (pk_k >= 0) readout(pk_k, pk_st, pk_h, pk_glen, pk_m, pk_l);
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  if (warp == 0) sm100::tmem_dealloc(tbase, 512);
+}
+
 // Long-forward scores in the unscaled domain y = S - (m_h / sc) |q - k| (sc = log2e / sqrt(d) is
 // applied inside the exponent, P = 2^(sc y - sc max y)); distances stepped by -2 per key pair so
 // no per-pair constants are materialised.  Returns max_j y (-inf past the sequence when MASK).
@@ -1761,6 +2049,27 @@ mb_status attention_fwd(const bf16* qkv, const int* cu, int batch, int nnz, int 
   const int H = heads * d;
   CUtensorMap tm;
   MB_REQUIRE(make_tmap_bf16_2d(&tm, qkv, 3 * H, nnz, 3 * H, DT, TILE), MB_ERR_CUDA);
+  static const bool short_v1 = [] {  // MB_ATTN_SHORT_FWD=v1: the round-1 short kernel (A/B)
+    const char* e = std::getenv("MB_ATTN_SHORT_FWD");
+    return e && e[0] == 'v' && e[1] == '1';
+  }();
+  const bool short2_fits = batch + 1 <= S2_CU_MAX && batch * heads <= num_sms() * S2_UMAX;
+  if (max_seqlen <= TILE && !short_v1 && short2_fits) {
+    static bool attr_s2 = false;
+    if (!attr_s2) {
+      if (cudaFuncSetAttribute(attn_fwd_short2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, S2_SMEM) !=
+          cudaSuccess)
+        return MB_ERR_CUDA;
+      attr_s2 = true;
+    }
+    GroupUnits G{cu, batch, heads, batch * heads};
+    const int grid = std::max(1, std::min(G.total, num_sms()));
+    if (launch_pdl(attn_fwd_short2_kernel, dim3(grid), dim3(S2_THREADS), S2_SMEM, s, 1, tm, G, d, slopes, O, lse,
+                   nnz) != cudaSuccess)
+      return MB_ERR_CUDA;
+    MB_CHECK_LAUNCH();
+    return MB_OK;
+  }
   if (max_seqlen <= TILE) {
     static bool attr_s = false;
     if (!attr_s) {

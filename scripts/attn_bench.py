@@ -9,10 +9,17 @@ from paper_2312_17482_b200 import _lib as L  # noqa: E402
 
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 128
 Lq = int(sys.argv[2]) if len(sys.argv) > 2 else 512
+kind = sys.argv[3] if len(sys.argv) > 3 else "full"  # "full" | "lognormal" (the C5 length recipe)
 heads, d = 12, 64
 H = heads * d
-nnz = B * Lq
-cu = torch.arange(0, nnz + 1, Lq, dtype=torch.int32, device="cuda")
+if kind == "full":
+    lens = np.full(B, Lq)
+else:
+    import synth  # noqa: E402
+    lens = synth.make_lengths(kind, B, Lq, synth.rng_for(5))
+nnz = int(lens.sum())
+cu = torch.from_numpy(np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)).cuda()
+Lq = int(lens.max())
 qkv = (torch.randn(nnz, 3 * H, device="cuda") * 0.5).to(torch.bfloat16)
 dO = torch.randn(nnz, H, device="cuda").to(torch.bfloat16)
 O = torch.empty(nnz, H, dtype=torch.bfloat16, device="cuda")
@@ -38,8 +45,8 @@ def timed(fn, reps=20):
 
 tf = timed(lambda: L.attention_forward(qkv, cu, B, nnz, Lq, heads, d, sl, O, lse))
 tb = timed(lambda: L.attention_backward(qkv, O, dO, lse, cu, B, nnz, Lq, heads, d, sl, dqkv, ws=ws, db_qkv=db))
-fl_f = 4.0 * B * heads * Lq * Lq * d  # QK^T and PV: 2 L^2 d MACs per (sequence, head)
+fl_f = 4.0 * heads * float((lens.astype(np.float64) ** 2).sum()) * d  # QK^T, PV: 2 l^2 d MACs per (seq, head)
 fl_b = 2.5 * fl_f                      # S, dP, dV, dK, dQ
 byt_f = nnz * (3 * H * 2 + H * 2 + heads * 4)  # QKV in, O + LSE out
-print(f"B={B} L={Lq}: attention fwd {tf:.1f} us ({fl_f / tf / 1e6:.0f} TF/s, {byt_f / tf / 1e3:.0f} GB/s), "
+print(f"B={B} L={Lq} {kind} nnz={nnz}: attention fwd {tf:.1f} us ({fl_f / tf / 1e6:.0f} TF/s, {byt_f / tf / 1e3:.0f} GB/s), "
       f"bwd (incl. prep/finish) {tb:.1f} us ({fl_b / tb / 1e6:.0f} TF/s)")

@@ -294,16 +294,21 @@ def test_attention_fwd_bwd(case):
     assert np.max(np.abs(np64(db)[H:2 * H])) <= 2e-2 * np.max(np.abs(dbref))
 
 
-@pytest.mark.parametrize("lo,hi,nseq", [(129, 512, 180), (257, 1024, 60)])
+@pytest.mark.parametrize("lo,hi,nseq", [(129, 512, 180), (257, 1024, 60), (1, 128, 400), (1, 40, 500)])
 def test_attention_long_many_units(lo, hi, nseq):
-    """Long path with several work units per persistent CTA (units > SMs), ragged lengths including
-    odd query-tile counts: exercises the cross-unit pipeline (deferred O epilogue, O double-buffering,
-    barrier phases across units).  Oracle per sequence (B = 1) to keep host memory small."""
+    """Several work units per persistent CTA (units > SMs) with ragged lengths: long path with odd
+    query-tile counts, and the short path with groups of 4 / pairs / single sequences sharing one
+    tile (block-diagonal key windows), zero-length sequences included: exercises the cross-unit
+    pipelines (deferred O epilogue, O double-buffering, barrier phases across units).  Oracle per
+    sequence (B = 1) to keep host memory small."""
     heads, d = 4, 64
     H = heads * d
     rng = np.random.default_rng(lo + hi)
     lens = rng.integers(lo, hi + 1, size=nseq)
-    lens[:3] = [hi, lo, 2 * 128 + 1]
+    lens[:3] = [hi, lo, 2 * 128 + 1] if hi > 128 else [hi, lo, 0]
+    if hi <= 128:
+        lens[10:14] = 0  # a whole empty group
+        lens[20] = 0
     cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
     nnz = int(cu[-1])
     qkv_np = synth.bf16_round(rng.standard_normal((nnz, 3 * H)) * 1.5)
@@ -321,6 +326,8 @@ def test_attention_long_many_units(lo, hi, nseq):
     ref_l = np.zeros((heads, nnz))
     for b in range(nseq):
         a, e, L_ = cu[b], cu[b + 1], int(lens[b])
+        if L_ == 0:
+            continue
         sp = lambda t: t[a:e].reshape(1, L_, heads, d)  # noqa: E731
         C, cache = O.attention_forward(sp(qkv_np[:, :H]), sp(qkv_np[:, H:2 * H]), sp(qkv_np[:, 2 * H:]),
                                        np.ones((1, L_)), sl_np.astype(np.float64))
