@@ -944,41 +944,23 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
 // on sm_100a).  A unit = (query tiles 2p and 2p+1, head, sequence); the two tiles share every K/V
 // tile the TMA warp streams in.  Softmax warpgroup t (warps 4t..4t+3) owns query tile t with ONE
 // thread per query row (128 keys per thread: no cross-thread row-max exchange).  The MMA warp issues
-// S_t = Q_t K^T into TMEM; warpgroup t reads S_t (tcgen05.ld), adds the ALiBi bias, exponentiates in
-// the exp2 domain and writes P_t back as packed bf16 over the first 64 columns of S_t (tcgen05.st);
-// O_t += P_t V then runs with A = P_t straight from tensor memory (tcgen05.mma A-in-TMEM), so P never
-// touches shared memory.  While warpgroup 0 works on tile g the MMAs of warpgroup 1's tile
-// (PV_1(g-1), S_1(g)) run, and vice versa.  The row sum l stays in registers (fp32); the O
-// accumulators are rescaled only when a row max grows by more than 2^8 (rare with the diagonal key
-// tile first).  O is double-buffered per unit parity so a unit's normalisation + store overlaps the
-// next unit's first tile.  TMEM: S_0 [0,128), S_1 [128,256), O[parity][t] at 256 + 64 (2 parity + t).
+// S_t = Q_t K^T into TMEM; warpgroup t loads S_t into registers and releases it at once (so S_t of
+// the next key tile is computed while this tile's exponentials run), adds the ALiBi bias,
+// exponentiates in the exp2 domain and writes P_t as packed bf16 into its own TMEM columns; O_t +=
+// P_t V then runs with A = P_t straight from tensor memory (tcgen05.mma A-in-TMEM), so P never
+// touches shared memory.  The row sum l stays in registers (fp32); the O accumulators are rescaled
+// only when a row max grows by more than 2^8 (rare with the diagonal key tile first).  A unit's O is
+// normalised and stored right after the first key tile of the next unit has been loaded.  Each CTA
+// builds its unit list once in shared memory.
+// TMEM: S_t [128 t, +128), P_t [256 + 64 t, +64) (bf16 pairs), O_t [384 + 64 t, +64).
 constexpr int L2_NS = 3;
 constexpr int L2_THREADS = SH_THREADS + 128;  // softmax warpgroups 0, 1; warpgroup 2: MMA warp 8, TMA warp 9
-constexpr int L2_SMEM = 4 * TILE_BYTES + L2_NS * 2 * TILE_BYTES + 1024 + 256;
+constexpr int L2_UMAX = 2048;                 // work units per CTA (host falls back to v1 beyond)
+constexpr int L2_SMEM = 4 * TILE_BYTES + L2_NS * 2 * TILE_BYTES + 1024 + 256 + 16 * L2_UMAX;
 
 struct PairUnits {  // unit u = (b * heads + h) * QP + p, valid iff 256 p < len_b
   const int* cu;
   int heads, QP, total;
-  __device__ __forceinline__ bool valid(int u) const {
-    const int b = u / (heads * QP), p = u % QP;
-    return p * 2 * TILE < cu[b + 1] - cu[b];
-  }
-  __device__ __forceinline__ int next(int u) const {
-    for (u += gridDim.x; u < total; u += gridDim.x)
-      if (valid(u)) return u;
-    return total;
-  }
-  __device__ __forceinline__ int first() const {
-    int u = blockIdx.x;
-    if (u < total && !valid(u)) u = next(u);
-    return u;
-  }
-  __device__ __forceinline__ void decode(int u, int& b, int& h, int& p) const {
-    b = u / (heads * QP);
-    const int rem = u - b * heads * QP;
-    h = rem / QP;
-    p = rem - h * QP;
-  }
 };
 
 // ALiBi-biased scores of one full query row (128 keys, one thread per row), unscaled domain:
@@ -1018,11 +1000,12 @@ __global__ void __launch_bounds__(L2_THREADS, 1) attn_fwd_long2_kernel(const __g
   uint64_t* kv_full = bars + 4;             // [L2_NS]
   uint64_t* kv_empty = bars + 4 + L2_NS;    // [L2_NS]
   uint64_t* s_full = bars + 4 + 2 * L2_NS;  // [2] per query tile t
-  uint64_t* p_ready = s_full + 2;           // [2] per t, 4 warps arrive
-  uint64_t* pv_done = s_full + 4;           // [2] per t, one phase per PV_t
-  uint64_t* o_full = s_full + 6;            // [2] per unit parity: the unit's last PVs are done
-  uint64_t* o_empty = s_full + 8;           // [2] per unit parity: 8 softmax warps have read O
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(s_full + 10);
+  uint64_t* s_free = s_full + 2;            // [2] per t, 4 warps arrive: S_t is in registers
+  uint64_t* p_ready = s_full + 4;           // [2] per t, 4 warps arrive
+  uint64_t* pv_done = s_full + 6;           // [2] per t, one phase per PV_t
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(s_full + 8);
+  int4* ulist = reinterpret_cast<int4*>(s_full + 10);  // {st, len, h | p << 16, two}
+  __shared__ int wcount[L2_THREADS / 32];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int H = U.heads * d;
@@ -1032,10 +1015,9 @@ __global__ void __launch_bounds__(L2_THREADS, 1) attn_fwd_long2_kernel(const __g
       sm100::mbar_init(&q_full[i], 1);
       sm100::mbar_init(&q_empty[i], 1);
       sm100::mbar_init(&s_full[i], 1);
+      sm100::mbar_init(&s_free[i], 4);
       sm100::mbar_init(&p_ready[i], 4);
       sm100::mbar_init(&pv_done[i], 1);
-      sm100::mbar_init(&o_full[i], 1);
-      sm100::mbar_init(&o_empty[i], 8);
     }
     for (int i = 0; i < L2_NS; ++i) {
       sm100::mbar_init(&kv_full[i], 1);
@@ -1051,27 +1033,45 @@ __global__ void __launch_bounds__(L2_THREADS, 1) attn_fwd_long2_kernel(const __g
   pdl_wait();
   pdl_trigger();
   const uint32_t sQa = sm100::smem_u32(sQ), sKVa = sm100::smem_u32(sKV);
-  // geometry of unit u: first token st, length len, key tiles nkv, second query tile present
-  auto geom = [&](int u, int& b, int& h, int& p, int& st, int& len, int& nkv, bool& two) {
-    U.decode(u, b, h, p);
-    st = U.cu[b];
-    len = U.cu[b + 1] - st;
-    nkv = (len + TILE - 1) / TILE;
-    two = (2 * p + 1) * TILE < len;
-  };
+  // this CTA's unit list (candidates blockIdx.x + c gridDim.x), compacted once by all threads
+  const int ncand = U.total > (int)blockIdx.x ? (U.total - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+  int nunits = 0;
+  for (int c0 = 0; c0 < ncand; c0 += L2_THREADS) {
+    const int c = c0 + tid;
+    const int u = (int)blockIdx.x + c * (int)gridDim.x;
+    int st = 0, len = 0, h = 0, p = 0;
+    bool ok = false;
+    if (c < ncand) {
+      const int b = u / (U.heads * U.QP);
+      const int rem = u - b * U.heads * U.QP;
+      h = rem / U.QP;
+      p = rem - h * U.QP;
+      st = U.cu[b];
+      len = U.cu[b + 1] - st;
+      ok = p * 2 * TILE < len;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, ok);
+    if (lane == 0) wcount[warp] = __popc(bal);
+    __syncthreads();
+    int off = nunits;
+    for (int w = 0; w < warp; ++w) off += wcount[w];
+    if (ok) ulist[off + __popc(bal & ((1u << lane) - 1))] = make_int4(st, len, h | (p << 16), (2 * p + 1) * TILE < len);
+    for (int w = 0; w < L2_THREADS / 32; ++w) nunits += wcount[w];
+    __syncthreads();
+  }
 
   // registers: 12 warps leave 168 per thread; the producer/issuer warpgroup (warps 8-11) hands most
   // of its share to the two softmax warpgroups (a full 128-key score row per thread lives in registers)
   if (warp >= 8) {
     sm100::setmaxnreg_dec<64>();
-    if (warp == 9) {
-    // ------------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      int uc = 0, g = 0;
-      for (int u = U.first(); u < U.total; u = U.next(u), ++uc) {
-        int b, h, p, st, len, nkv;
-        bool two;
-        geom(u, b, h, p, st, len, nkv, two);
+    if (warp == 9 && lane == 0) {
+      // ------------------------------------------------------------------ TMA producer
+      int g = 0;
+      for (int uc = 0; uc < nunits; ++uc) {
+        const int4 e = ulist[uc];
+        const int st = e.x, len = e.y, h = e.z & 0xffff, p = e.z >> 16;
+        const bool two = e.w;
+        const int nkv = (len + TILE - 1) / TILE;
         const int qb = uc & 1;
         sm100::mbar_wait(&q_empty[qb], ((uc >> 1) & 1) ^ 1);
         sm100::mbar_arrive_expect_tx(&q_full[qb], (two ? 2 : 1) * TILE_BYTES);
@@ -1087,70 +1087,75 @@ __global__ void __launch_bounds__(L2_THREADS, 1) attn_fwd_long2_kernel(const __g
           sm100::tma_load_2d(kv + TILE_BYTES, &tm_qkv, &kv_full[sg], 2 * H + h * d, st + j * TILE);
         }
       }
-    }
-    __syncwarp();
-  } else if (warp == 8) {
-    // ------------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    } else if (warp == 8 && lane == 0) {
+      // ------------------------------------------------------------------ MMA issuer
       constexpr uint32_t id_s = sm100::idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t id_o = sm100::idesc_bf16(128, 64, 0, 1);
-      int uc = 0, g = 0, c0 = 0, c1 = 0;
-      auto issue_s = [&](int t, uint32_t q, int sg) {  // S_t = Q_t K_sg^T
+      int c[2] = {0, 0}, sc[2] = {0, 0};  // PVs / S issued per query tile t
+      auto issue_s = [&](int t, uint32_t q, int sg) {  // S_t = Q_t K_sg^T, once S_t's last tile is in registers
+        sm100::mbar_wait(&s_free[t], (sc[t] & 1) ^ 1);
+        ++sc[t];
+        sm100::tc_fence_after();
         const uint32_t k = sKVa + sg * 2 * TILE_BYTES;
         for (int kk = 0; kk < d / 16; ++kk)
           sm100::mma_bf16_ss(tbase + 128 * t, sm100::desc_kmajor_sw128(q + kk * 32), sm100::desc_kmajor_sw128(k + kk * 32),
                              id_s, kk > 0);
         sm100::mma_commit(&s_full[t]);
       };
-      auto issue_pv = [&](int t, int qb, int sg, bool acc) {  // O[qb][t] += P_t V_sg, P_t from TMEM
+      auto issue_pv = [&](int t, int sg, bool acc) {  // O_t += P_t V_sg (P_t from TMEM), after P_t is written
+        sm100::mbar_wait(&p_ready[t], c[t] & 1);
+        sm100::tc_fence_after();
         const uint32_t v = sKVa + sg * 2 * TILE_BYTES + TILE_BYTES;
 #pragma unroll
         for (int kk = 0; kk < TILE / 16; ++kk)
-          sm100::mma_bf16_ts(tbase + 256 + 64 * (2 * qb + t), tbase + 128 * t + 8 * kk,
+          sm100::mma_bf16_ts(tbase + 384 + 64 * t, tbase + 256 + 64 * t + 8 * kk,
                              sm100::desc_mnmajor_sw128(v + kk * 2048, 8192), id_o, (acc || kk > 0) ? 1u : 0u);
         sm100::mma_commit(&pv_done[t]);
+        ++c[t];
       };
-      for (int u = U.first(); u < U.total; u = U.next(u), ++uc) {
-        int b, h, p, st, len, nkv;
-        bool two;
-        geom(u, b, h, p, st, len, nkv, two);
-        const int qb = uc & 1;
-        const uint32_t q0 = sQa + 2 * qb * TILE_BYTES, q1 = q0 + TILE_BYTES;
-        sm100::mbar_wait(&q_full[qb], (uc >> 1) & 1);
-        sm100::mbar_wait(&o_empty[qb], ((uc >> 1) & 1) ^ 1);  // unit uc-2's O has been read out
-        sm100::tc_fence_after();
-        for (int jj = 0; jj < nkv; ++jj, ++g) {
-          const int sg = g % L2_NS, sg2 = (g + 1) % L2_NS;
-          if (jj == 0) {
-            sm100::mbar_wait(&kv_full[sg], (g / L2_NS) & 1);
-            sm100::tc_fence_after();
-            issue_s(0, q0, sg);
-            if (two) issue_s(1, q1, sg);
-          }
-          sm100::mbar_wait(&p_ready[0], c0 & 1);
+      // flattened key-tile sequence over this CTA's units: S_t of tile g + 1 is issued as soon as
+      // warpgroup t holds S_t(g) in registers (before PV_t(g)), so it overlaps the exponentials
+      auto unit_two = [&](int uc) { return ulist[uc].w != 0; };
+      auto unit_nkv = [&](int uc) { return (ulist[uc].y + TILE - 1) / TILE; };
+      auto issue_s_tile = [&](int t, int uc, int g) {  // S_t of global tile g (unit uc)
+        const int sg = g % L2_NS;
+        if (t == 0) {
+          sm100::mbar_wait(&kv_full[sg], (g / L2_NS) & 1);
           sm100::tc_fence_after();
-          issue_pv(0, qb, sg, jj > 0);
-          ++c0;
-          if (jj + 1 < nkv) {
-            sm100::mbar_wait(&kv_full[sg2], ((g + 1) / L2_NS) & 1);
-            sm100::tc_fence_after();
-            issue_s(0, q0, sg2);  // after PV_0 in issue order: overwrites P_0 only once it is read
-          }
-          if (two) {
-            sm100::mbar_wait(&p_ready[1], c1 & 1);
-            sm100::tc_fence_after();
-            issue_pv(1, qb, sg, jj > 0);
-            ++c1;
-          }
-          sm100::mma_commit(&kv_empty[sg]);
-          if (two && jj + 1 < nkv) issue_s(1, q1, sg2);
         }
-        sm100::mma_commit(&q_empty[qb]);
-        sm100::mma_commit(&o_full[qb]);
+        issue_s(t, sQa + (2 * (uc & 1) + t) * TILE_BYTES, sg);
+      };
+      if (nunits > 0) {
+        sm100::mbar_wait(&q_full[0], 0);
+        issue_s_tile(0, 0, 0);
+        if (unit_two(0)) issue_s_tile(1, 0, 0);
+      }
+      int g = 0;
+      for (int uc = 0; uc < nunits; ++uc) {
+        const bool two = unit_two(uc);
+        const int nkv = unit_nkv(uc);
+        for (int jj = 0; jj < nkv; ++jj, ++g) {
+          // the next tile of the flattened sequence
+          int nu = uc, nj = jj + 1;
+          if (nj == nkv) {
+            nu = uc + 1;
+            nj = 0;
+          }
+          const bool has_next = nu < nunits;
+          const bool next_two = has_next && unit_two(nu);
+          if (has_next) {
+            if (nj == 0) sm100::mbar_wait(&q_full[nu & 1], (nu >> 1) & 1);
+            issue_s_tile(0, nu, g + 1);
+          }
+          issue_pv(0, g % L2_NS, jj > 0);
+          if (next_two) issue_s_tile(1, nu, g + 1);
+          if (two) issue_pv(1, g % L2_NS, jj > 0);
+          sm100::mma_commit(&kv_empty[g % L2_NS]);
+        }
+        sm100::mma_commit(&q_empty[uc & 1]);  // every S of this unit has been issued
       }
     }
     __syncwarp();
-    }
   } else {
     // ------------------------------------------------------------------ softmax warpgroups
     sm100::setmaxnreg_inc<216>();  // 2 x 128 x 216 + 128 x 64 <= 384 x 168
@@ -1159,120 +1164,110 @@ __global__ void __launch_bounds__(L2_THREADS, 1) attn_fwd_long2_kernel(const __g
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     const float sc2 = rsqrtf((float)d) * LOG2E;
     const float tau = 8.f / sc2;  // rescale only when a row max grows by more than 2^8 in P
-    const uint32_t tS = tbase + 128 * t + lane_off;
-    auto epilogue = [&](int uu, int ucc, float m_used, float l_used, bool act) {
-      int b, h, p, st, len, nkv;
-      bool two;
-      geom(uu, b, h, p, st, len, nkv, two);
-      const int qrow = (2 * p + t) * TILE + r;
-      sm100::mbar_wait(&o_full[ucc & 1], (ucc >> 1) & 1);
+    const uint32_t tS = tbase + 128 * t + lane_off, tP = tbase + 256 + 64 * t + lane_off,
+                   tO = tbase + 384 + 64 * t + lane_off;
+    int c = 0;  // key tiles processed by this warpgroup (all units)
+    // a finished unit's O: normalise, store, LSE (its last PV is pv_done phase c - 1)
+    auto readout = [&](int st, int len, int h, int qrow, float m_used, float l_used) {
+      sm100::mbar_wait(&pv_done[t], (c - 1) & 1);
       sm100::tc_fence_after();
-      if (act) {
-        const uint32_t to = tbase + 256 + 64 * (2 * (ucc & 1) + t) + lane_off;
-        const float inv = 1.f / l_used;
-        bf16* dst = O + (size_t)(st + qrow) * H + h * d;
+      const float inv = 1.f / l_used;
+      bf16* dst = O + (size_t)(st + qrow) * H + h * d;
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          float o[32];
-          sm100::tmem_ld32(to + 32 * hh, o);
-          sm100::tmem_ld_wait();
-          if (32 * hh < d && qrow < len) {
+      for (int hh = 0; hh < 2; ++hh) {
+        float o[32];
+        sm100::tmem_ld32(tO + 32 * hh, o);
+        sm100::tmem_ld_wait();
+        if (32 * hh < d && qrow < len) {
 #pragma unroll
-            for (int c = 0; c < 32; c += 8) {
-              float w[8];
+          for (int cc = 0; cc < 32; cc += 8) {
+            float w8[8];
 #pragma unroll
-              for (int e = 0; e < 8; ++e) w[e] = o[c + e] * inv;
-              *reinterpret_cast<uint4*>(dst + 32 * hh + c) = f32_to_bf16x8(w);
-            }
+            for (int e = 0; e < 8; ++e) w8[e] = o[cc + e] * inv;
+            *reinterpret_cast<uint4*>(dst + 32 * hh + cc) = f32_to_bf16x8(w8);
           }
         }
-        if (qrow < len) lse[(size_t)h * nnz + st + qrow] = (m_used * sc2 + log2f(l_used)) * LN2;
       }
-      sm100::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) sm100::mbar_arrive(&o_empty[ucc & 1]);
+      if (qrow < len) lse[(size_t)h * nnz + st + qrow] = (m_used * sc2 + __log2f(l_used)) * LN2;  // l >= 1
     };
-    int uc = 0, c = 0;
-    int pend_u = -1, pend_uc = 0;
-    float pend_m = 0.f, pend_l = 1.f;
-    bool pend_act = false;
-    for (int u = U.first(); u < U.total; u = U.next(u), ++uc) {
-      int b, h, p, st, len, nkv;
-      bool two;
-      geom(u, b, h, p, st, len, nkv, two);
-      const bool act = t == 0 || two;
+    bool pend = false;
+    int pd_st = 0, pd_len = 0, pd_h = 0, pd_row = 0;
+    float pd_m = 0.f, pd_l = 1.f;
+    for (int uc = 0; uc < nunits; ++uc) {
+      const int4 e = ulist[uc];
+      const int st = e.x, len = e.y, h = e.z & 0xffff, p = e.z >> 16;
+      if (t == 1 && !e.w) continue;  // no second query tile in this unit
+      const int nkv = (len + TILE - 1) / TILE;
       const int q0 = (2 * p + t) * TILE;
       const float slr = slopes[h] * sqrtf((float)d);  // m_h / (1/sqrt(d)): bias in the unscaled domain
       float m = -INFINITY, l = 0.f;
       for (int jj = 0; jj < nkv; ++jj) {
-        if (act) {
-          const int kv0 = ((2 * p + jj) % nkv) * TILE;
-          sm100::mbar_wait(&s_full[t], c & 1);
-          sm100::tc_fence_after();
-          float x[128];
+        const int kv0 = ((2 * p + jj) % nkv) * TILE;
+        sm100::mbar_wait(&s_full[t], c & 1);
+        sm100::tc_fence_after();
+        float x[128];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) sm100::tmem_ld32(tS + 32 * i, x + 32 * i);
-          sm100::tmem_ld_wait();
-          const int keys = len - kv0;
-          const float mx = keys >= TILE ? row_scores128<false>(x, r, keys, slr, q0 - kv0)
-                                        : row_scores128<true>(x, r, keys, slr, q0 - kv0);
-          if (jj == 0) {
-            m = mx;
-          } else if (__any_sync(0xffffffffu, mx > m + tau)) {
-            // rescale this warp's O rows (after PV_t of the previous key tile has landed)
+        for (int i = 0; i < 4; ++i) sm100::tmem_ld32(tS + 32 * i, x + 32 * i);
+        sm100::tmem_ld_wait();
+        sm100::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(&s_free[t]);
+        if (jj == 0 && pend) {  // the previous unit's O (its PVs are done once this tile's S is in)
+          readout(pd_st, pd_len, pd_h, pd_row, pd_m, pd_l);
+          pend = false;
+        }
+        const int keys = len - kv0;
+        const float mx = keys >= TILE ? row_scores128<false>(x, r, keys, slr, q0 - kv0)
+                                      : row_scores128<true>(x, r, keys, slr, q0 - kv0);
+        if (jj > 0) {
+          // P_t of the previous key tile must have been consumed before P_t is rewritten, and a
+          // rescale of O_t must follow that PV
+          sm100::mbar_wait(&pv_done[t], (c - 1) & 1);
+          if (__any_sync(0xffffffffu, mx > m + tau)) {
             const float m_new = fmaxf(m, mx);
             const float alpha = ex2_approx((m - m_new) * sc2);
-            sm100::mbar_wait(&pv_done[t], (c - 1) & 1);
             sm100::tc_fence_after();
-            const uint32_t to = tbase + 256 + 64 * (2 * (uc & 1) + t) + lane_off;
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
               float o[32];
-              sm100::tmem_ld32(to + 32 * hh, o);
+              sm100::tmem_ld32(tO + 32 * hh, o);
               sm100::tmem_ld_wait();
 #pragma unroll
-              for (int e = 0; e < 32; ++e) o[e] *= alpha;
-              sm100::tmem_st32(to + 32 * hh, o);
+              for (int q = 0; q < 32; ++q) o[q] *= alpha;
+              sm100::tmem_st32(tO + 32 * hh, o);
             }
-            sm100::tmem_st_wait();
             l *= alpha;
             m = m_new;
           }
-          // P = 2^(sc (s - m)) as packed bf16 pairs written in place over x[0..63] -> S_t columns [0, 64)
-          const float nm = -m * sc2;
-          float2 ls = make_float2(0.f, 0.f);
+        } else {
+          m = mx;
+        }
+        const float nm = -m * sc2;
+        float2 ls = make_float2(0.f, 0.f);
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {  // keys [64 hh, 64 hh + 64) -> P columns [32 hh, 32 hh + 32)
-            float pk[32];  // packed bf16 pairs (bit patterns)
+        for (int hh = 0; hh < 2; ++hh) {
+          float pk[32];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const int k = 64 * hh + 2 * j;
-              const float2 tt = __ffma2_rn(make_float2(x[k], x[k + 1]), make_float2(sc2, sc2), make_float2(nm, nm));
-              const float2 e = make_float2(ex2_approx(tt.x), ex2_approx(tt.y));
-              ls = __fadd2_rn(ls, e);
-              pk[j] = __uint_as_float(pack_bf16x2(e.x, e.y));
-            }
-            sm100::tmem_st32(tS + 32 * hh, pk);
+          for (int q = 0; q < 32; ++q) {
+            const int cc = 64 * hh + 2 * q;
+            const float2 tt = __ffma2_rn(make_float2(x[cc], x[cc + 1]), make_float2(sc2, sc2), make_float2(nm, nm));
+            const float2 ee = make_float2(ex2_approx(tt.x), ex2_approx(tt.y));
+            ls = __fadd2_rn(ls, ee);
+            pk[q] = __uint_as_float(pack_bf16x2(ee.x, ee.y));
           }
-          l += ls.x + ls.y;
-          sm100::tmem_st_wait();
-          sm100::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) sm100::mbar_arrive(&p_ready[t]);
-          ++c;
+          sm100::tmem_st32(tP + 32 * hh, pk);
         }
-        if (jj == 0 && pend_u >= 0) {  // the previous unit's O: normalise and store
-          epilogue(pend_u, pend_uc, pend_m, pend_l, pend_act);
-          pend_u = -1;
-        }
+        l += ls.x + ls.y;
+        sm100::tmem_st_wait();
+        sm100::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(&p_ready[t]);
+        ++c;
       }
-      pend_u = u;
-      pend_uc = uc;
-      pend_m = m;
-      pend_l = l;
-      pend_act = act;
+      pend = true;
+      pd_st = st, pd_len = len, pd_h = h, pd_row = q0 + r, pd_m = m, pd_l = l;
     }
-    if (pend_u >= 0) epilogue(pend_u, pend_uc, pend_m, pend_l, pend_act);
+    if (pend) readout(pd_st, pd_len, pd_h, pd_row, pd_m, pd_l);
   }
   sm100::tc_fence_before();
   __syncthreads();
@@ -2092,7 +2087,7 @@ mb_status attention_fwd(const bf16* qkv, const int* cu, int batch, int nnz, int 
     const char* e = std::getenv("MB_ATTN_LONG_FWD");
     return e && e[0] == 'v' && e[1] == '1';
   }();
-  if (!v1) {
+  if (!v1 && (size_t)batch * heads * ((max_seqlen + 2 * TILE - 1) / (2 * TILE)) <= (size_t)num_sms() * L2_UMAX) {
     static bool attr_2 = false;
     if (!attr_2) {
       if (cudaFuncSetAttribute(attn_fwd_long2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L2_SMEM) !=
