@@ -327,32 +327,65 @@ __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const
 // of a row-key pair are in the same sequence).
 constexpr int S2_NSLOT = 4;
 constexpr int S2_THREADS = SH_THREADS + 128;
-constexpr int S2_CU_MAX = 4096;  // cu_seqlens entries cached in shared memory (batch + 1 <= this)
-constexpr int S2_UMAX = 1024;    // work units per CTA (host falls back to the v1 kernel beyond)
-constexpr int S2_SMEM = S2_NSLOT * 3 * TILE_BYTES + 1024 + 256 + 4 * S2_CU_MAX + 16 * S2_UMAX;
+constexpr int S2_UMAX = 1024;  // work units per CTA (host falls back to the v1 kernel beyond)
+constexpr int S2_SMEM = S2_NSLOT * 3 * TILE_BYTES + 1024 + 256 + 16 * S2_UMAX;
 
-struct GroupUnits {  // unit u = b * heads + h, valid iff a group starts at sequence b
-  const int* cu;
-  int batch, heads, total;
-  __device__ __forceinline__ int span(int b) const {  // sequences in the group starting at b, 0 if none
-    const int b4 = b & ~3;
-    if (b4 + 3 < batch && cu[b4 + 4] - cu[b4] <= TILE) return b == b4 && cu[b4 + 4] > cu[b4] ? 4 : 0;
-    const int b2 = b & ~1;
-    if (b2 + 1 < batch && cu[b2 + 2] - cu[b2] <= TILE) return b == b2 && cu[b2 + 2] > cu[b2] ? 2 : 0;
-    return cu[b + 1] > cu[b] ? 1 : 0;
+// Short-path work units: one head of a GROUP of consecutive sequences fitting one 128-row tile —
+// sequences 4g..4g+3 when their lengths sum to <= 128, else the pair 2g, 2g+1 when it fits, else
+// one sequence; empty groups are skipped.  span(b) = sequences in the group starting at b (0: none).
+__device__ __forceinline__ int group_span(const int* cu, int batch, int b) {
+  const int b4 = b & ~3;
+  if (b4 + 3 < batch && cu[b4 + 4] - cu[b4] <= TILE) return b == b4 && cu[b4 + 4] > cu[b4] ? 4 : 0;
+  const int b2 = b & ~1;
+  if (b2 + 1 < batch && cu[b2 + 2] - cu[b2] <= TILE) return b == b2 && cu[b2 + 2] > cu[b2] ? 2 : 0;
+  return cu[b + 1] > cu[b] ? 1 : 0;
+}
+// This CTA's units (candidates u = blockIdx.x + c gridDim.x, u = b * heads + h), compacted in order
+// into shared memory by all NT threads: {first token, group length, h | span << 16, in-group
+// sequence boundaries b1 | b2 << 8 | b3 << 16 (tile-relative, 0 when absent)}.  Walking cu per
+// unit inside the roles' loops (up to six dependent reads per candidate) stalled every role.
+template <int NT>
+__device__ int build_group_list(const int* __restrict__ cu, int batch, int heads, int4* ulist, int* wcount) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int total = batch * heads;
+  const int ncand = total > (int)blockIdx.x ? (total - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+  int n = 0;
+  for (int c0 = 0; c0 < ncand; c0 += NT) {
+    const int c = c0 + tid;
+    const int u = (int)blockIdx.x + c * (int)gridDim.x;
+    int span = 0, b = 0;
+    if (c < ncand) {
+      b = u / heads;
+      span = group_span(cu, batch, b);
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, span > 0);
+    if (lane == 0) wcount[warp] = __popc(bal);
+    __syncthreads();
+    int off = n;
+    for (int w = 0; w < warp; ++w) off += wcount[w];
+    if (span > 0) {
+      const int st = cu[b];
+      int bnd = 0;
+      for (int e = 1; e < span; ++e) bnd |= (cu[b + e] - st) << (8 * (e - 1));
+      ulist[off + __popc(bal & ((1u << lane) - 1))] = make_int4(st, cu[b + span] - st, (u - b * heads) | (span << 16), bnd);
+    }
+    for (int w = 0; w < NT / 32; ++w) n += wcount[w];
+    __syncthreads();
   }
-  __device__ __forceinline__ bool valid(int u) const { return span(u / heads) > 0; }
-  __device__ __forceinline__ int next(int u) const {
-    for (u += gridDim.x; u < total; u += gridDim.x)
-      if (valid(u)) return u;
-    return total;
+  return n;
+}
+// key window [lo, hi) of tile row r in a unit entry (its own sequence; rows past the group: [0, 1))
+__device__ __forceinline__ void group_window(const int4& e, int r, int& lo, int& hi) {
+  const int span = e.z >> 16;
+  lo = 0;
+  hi = e.y;
+  for (int k = 1; k < span; ++k) {
+    const int bk = (e.w >> (8 * (k - 1))) & 0xff;
+    if (r >= bk) lo = bk;
+    else if (hi == e.y && r < bk) hi = bk;
   }
-  __device__ __forceinline__ int first() const {
-    int u = blockIdx.x;
-    if (u < total && !valid(u)) u = next(u);
-    return u;
-  }
-};
+  if (r >= e.y) lo = 0, hi = 1;
+}
 
 // ALiBi-biased scores of one query row r of a short tile, unscaled domain; keys outside the row's
 // window [lo, hi) are masked when MASK; returns max_j
@@ -379,8 +412,8 @@ __device__ __forceinline__ float row_scores_win(float (&x)[128], int r, int lo, 
 }
 
 __global__ void __launch_bounds__(S2_THREADS, 1) attn_fwd_short2_kernel(const __grid_constant__ CUtensorMap tm_qkv,
-                                                                       GroupUnits U, int d,
-                                                                       const float* __restrict__ slopes,
+                                                                       const int* __restrict__ cu, int batch, int heads,
+                                                                       int d, const float* __restrict__ slopes,
                                                                        bf16* __restrict__ O, float* __restrict__ lse,
                                                                        int nnz) {
   // TMEM per warpgroup t: S_t [128 t, +128) fp32, P_t [256 + 64 t, +64) packed bf16, O_t [384 + 64 t, +64).
@@ -398,12 +431,11 @@ __global__ void __launch_bounds__(S2_THREADS, 1) attn_fwd_short2_kernel(const __
   uint64_t* o_full = s_full + 6;             // [2] per warpgroup
   uint64_t* o_empty = s_full + 8;            // [2] per warpgroup, 4 warps arrive
   uint32_t* tslot = reinterpret_cast<uint32_t*>(s_full + 10);
-  int* cu_s = reinterpret_cast<int*>(s_full + 12);
-  int4* ulist = reinterpret_cast<int4*>(cu_s + S2_CU_MAX);  // this CTA's units {st, glen, h | span << 16, b}
-  __shared__ int wcount[S2_THREADS / 32 + 1];
+  int4* ulist = reinterpret_cast<int4*>(s_full + 12);  // this CTA's units (build_group_list)
+  __shared__ int wcount[S2_THREADS / 32];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int H = U.heads * d;
+  const int H = heads * d;
   if (tid == 0) {
     sm100::tma_prefetch(&tm_qkv);
     for (int i = 0; i < S2_NSLOT; ++i) {
@@ -427,33 +459,7 @@ __global__ void __launch_bounds__(S2_THREADS, 1) attn_fwd_short2_kernel(const __
   pdl_wait();
   pdl_trigger();
   const uint32_t slots_a = sm100::smem_u32(slots);
-  // this CTA's work-unit list, built once in shared memory by all threads (candidates u = blockIdx.x
-  // + c gridDim.x; a group span needs up to six dependent cu reads, too slow for the roles' loops)
-  for (int i = tid; i <= U.batch; i += S2_THREADS) cu_s[i] = U.cu[i];
-  __syncthreads();
-  U.cu = cu_s;
-  const int ncand = U.total > (int)blockIdx.x ? (U.total - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
-  int nunits = 0;
-  for (int c0 = 0; c0 < ncand; c0 += S2_THREADS) {
-    const int c = c0 + tid;
-    const int u = (int)blockIdx.x + c * (int)gridDim.x;
-    int span = 0, b = 0;
-    if (c < ncand) {
-      b = u / U.heads;
-      span = U.span(b);
-    }
-    const unsigned bal = __ballot_sync(0xffffffffu, span > 0);
-    if (lane == 0) wcount[warp] = __popc(bal);
-    __syncthreads();
-    int off = nunits;
-    for (int w = 0; w < warp; ++w) off += wcount[w];
-    if (span > 0) {
-      const int st = cu_s[b];
-      ulist[off + __popc(bal & ((1u << lane) - 1))] = make_int4(st, cu_s[b + span] - st, (u - b * U.heads) | (span << 16), b);
-    }
-    for (int w = 0; w < S2_THREADS / 32; ++w) nunits += wcount[w];
-    __syncthreads();
-  }
+  const int nunits = build_group_list<S2_THREADS>(cu, batch, heads, ulist, wcount);
 
   if (warp >= 8) {
     sm100::setmaxnreg_dec<64>();
@@ -550,13 +556,9 @@ __global__ void __launch_bounds__(S2_THREADS, 1) attn_fwd_short2_kernel(const __
     float pk_m = 0.f, pk_l = 1.f;
     for (j = t; j < nunits; j += 2) {
       const int4 ue = ulist[j];
-      const int st = ue.x, glen = ue.y, h = ue.z & 0xffff, span = ue.z >> 16, b = ue.w;
-      // this row's key window: its own sequence inside the group (rows past the group: [0, 1))
-      int lo = 0, hi = 1;
-      for (int e = 0; e < span; ++e) {
-        const int a = cu_s[b + e] - st, z = cu_s[b + e + 1] - st;
-        if (r >= a && r < z) lo = a, hi = z;
-      }
+      const int st = ue.x, glen = ue.y, h = ue.z & 0xffff, span = ue.z >> 16;
+      int lo, hi;
+      group_window(ue, r, lo, hi);
       const float slr = slopes[h] * sqrtf((float)d);
       sm100::mbar_wait(&s_full[t], k & 1);
       sm100::tc_fence_after();
@@ -1284,7 +1286,8 @@ __global__ void __launch_bounds__(L2_THREADS, 1) attn_fwd_long2_kernel(const __g
 // TMEM: S [0,128), dP [128,256), dV [256,320), dK [320,384), dQ [384,448).
 constexpr int BWD_BUF_BYTES = 4 * TILE_BYTES;  // Q, K, V, dO
 constexpr int SH_BWD_THREADS = SH_THREADS + 32;
-constexpr int SH_BWD_SMEM = 2 * BWD_BUF_BYTES + 2 * P_BYTES + 1024 + 256;
+constexpr int BW_UMAX = 512;  // work units per CTA (build_group_list)
+constexpr int SH_BWD_SMEM = 2 * BWD_BUF_BYTES + 2 * P_BYTES + 1024 + 256 + 16 * BW_UMAX;
 
 // per-warp transpose-reduce: lane l ends with sum over the warp's 32 rows of column l of v[32]
 __device__ __forceinline__ float warp_colsum32(float* v, int lane) {
@@ -1308,8 +1311,9 @@ __device__ __forceinline__ float warp_colsum32(float* v, int lane) {
 // dP_rj, so D needs neither O nor dO from memory).  Two keys per instruction on the paired fp32
 // pipe; MASK = false for units of exactly 128 rows (no masking).
 template <bool MASK>
-__device__ __forceinline__ float bwd_pass1(uint32_t tS, uint32_t tdP, uint32_t sPa, int r, int ch, int len, float sc2,
-                                          float sl2, float lse2) {
+__device__ __forceinline__ float bwd_pass1(uint32_t tS, uint32_t tdP, uint32_t sPa, int r, int ch, int lo, int hi,
+                                          bool row_ok, float sc2, float sl2, float lse2) {
+  const uint32_t wwin = (uint32_t)(hi - lo);
   float2 Dp = make_float2(0.f, 0.f);
   const float rc = (float)(r - 64 * ch);
 #pragma unroll
@@ -1328,9 +1332,9 @@ __device__ __forceinline__ float bwd_pass1(uint32_t tS, uint32_t tdP, uint32_t s
                                   make_float2(-lse2, -lse2));
       const float2 x = __ffma2_rn(make_float2(v[jj], v[jj + 1]), make_float2(sc2, sc2), t);
       float2 pv = make_float2(ex2_approx(x.x), ex2_approx(x.y));
-      if (MASK) {
-        pv.x = (r < len && c0 + jj < len) ? pv.x : 0.f;
-        pv.y = (r < len && c0 + jj + 1 < len) ? pv.y : 0.f;
+      if (MASK) {  // keys outside the row's own sequence, rows past the unit
+        pv.x = (row_ok && (uint32_t)(c0 + jj - lo) < wwin) ? pv.x : 0.f;
+        pv.y = (row_ok && (uint32_t)(c0 + jj + 1 - lo) < wwin) ? pv.y : 0.f;
       }
       v[jj] = pv.x;
       v[jj + 1] = pv.y;
@@ -1364,11 +1368,12 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
   uint64_t* p_ready = bars + 5;    // 8 compute warps: P in smem
   uint64_t* dv_full = bars + 6;    // dV of the unit in TMEM
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 8);
+  int4* ulist = reinterpret_cast<int4*>(bars + 10);  // this CTA's units (build_group_list)
   __shared__ float dred[2 * 128];  // partial D of the two half-row threads
+  __shared__ int wcount[SH_BWD_THREADS / 32];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int H = heads * d;
-  const int total = batch * heads;
   if (tid == 0) {
     sm100::tma_prefetch(&tm_qkv);
     sm100::tma_prefetch(&tm_do);
@@ -1392,16 +1397,15 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
   const uint32_t tS = tbase, tdP = tbase + 128, tdV = tbase + 256, tdK = tbase + 320, tdQ = tbase + 384;
   const uint32_t sPa = sm100::smem_u32(sP), sdSa = sm100::smem_u32(sdS);
 
-  int u0 = blockIdx.x;
-  if (u0 < total && unit_len(cu, heads, u0) == 0) u0 = next_unit(cu, heads, total, u0);
+  const int nunits = build_group_list<SH_BWD_THREADS>(cu, batch, heads, ulist, wcount);
 
   if (warp == 8) {
     // ------------------------------------------------------------------ producer / MMA issuer
     if (lane == 0) {
       auto buf_addr = [&](int b) { return bufs + b * BWD_BUF_BYTES; };
-      auto issue_loads = [&](int u, int b) {
-        const int bb = u / heads, h = u - bb * heads;
-        const int st = cu[bb];
+      auto issue_loads = [&](int i, int b) {
+        const int4 e = ulist[i];
+        const int h = e.z & 0xffff, st = e.x;
         uint8_t* base = buf_addr(b);
         sm100::mbar_arrive_expect_tx(&load_full[b], BWD_BUF_BYTES);
         sm100::tma_load_2d(base, &tm_qkv, &load_full[b], h * d, st);
@@ -1443,16 +1447,14 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
         }
         sm100::mma_commit(acc_full);
       };
-      int u_cur = u0;
-      int u_nxt = u_cur < total ? next_unit(cu, heads, total, u_cur) : total;
-      if (u_cur < total) issue_loads(u_cur, 0);
-      if (u_nxt < total) issue_loads(u_nxt, 1);
-      if (u_cur < total) {
+      if (nunits > 0) issue_loads(0, 0);
+      if (nunits > 1) issue_loads(1, 1);
+      if (nunits > 0) {
         sm100::mbar_wait(&load_full[0], 0);
         sm100::tc_fence_after();
         mma1(0);
       }
-      for (int i = 0; u_cur < total; ++i) {
+      for (int i = 0; i < nunits; ++i) {
         const int b = i & 1;
         sm100::mbar_wait(p_ready, i & 1);  // P(i) in smem (and dV(i-1) read out)
         sm100::tc_fence_after();
@@ -1460,16 +1462,13 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
         sm100::mbar_wait(elem_done, i & 1);  // S/dP(i) consumed, dS(i) in smem
         sm100::tc_fence_after();
         mma_dkq(b);
-        if (u_nxt < total) {
+        if (i + 1 < nunits) {
           sm100::mbar_wait(&load_full[b ^ 1], ((i + 1) >> 1) & 1);
           sm100::tc_fence_after();
           mma1(b ^ 1);
         }
         sm100::mbar_wait(acc_full, i & 1);  // all MMAs of unit i done: buffer b is free
-        const int u_n2 = u_nxt < total ? next_unit(cu, heads, total, u_nxt) : total;
-        if (u_n2 < total) issue_loads(u_n2, b);
-        u_cur = u_nxt;
-        u_nxt = u_n2;
+        if (i + 2 < nunits) issue_loads(i + 2, b);
       }
     }
     __syncwarp();
@@ -1484,27 +1483,29 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
     const bool col_ok = 32 * ch < d;
     // this warp's P / dS slabs (rows [32 q4, +32), columns [64 ch, +64)) double as output staging
     const uint32_t slabP = sPa + ch * (TILE * 128) + q4 * 4096, slabS = sdSa + ch * (TILE * 128) + q4 * 4096;
-    auto lse_of = [&](int uu) {  // LSE of row r of unit uu, prefetched one unit ahead (scaled at use)
-      if (uu >= total) return 0.f;
-      const int bb = uu / heads, hh = uu - bb * heads;
-      const int st = cu[bb];
-      return (r < cu[bb + 1] - st) ? lse[(size_t)hh * nnz + st + r] : 0.f;
+    auto lse_of = [&](int ii) {  // LSE of row r of unit ii, prefetched one unit ahead (scaled at use)
+      if (ii >= nunits) return 0.f;
+      const int4 e = ulist[ii];
+      return r < e.y ? lse[(size_t)(e.z & 0xffff) * nnz + e.x + r] : 0.f;
     };
-    float lse_next = lse_of(u0);
-    for (int i = 0, u = u0; u < total; ++i) {
-      const int b = u / heads, h = u - b * heads;
-      const int start = cu[b];
-      const int len = cu[b + 1] - start;
+    float lse_next = lse_of(0);
+    for (int i = 0; i < nunits; ++i) {
+      const int4 ue = ulist[i];
+      const int h = ue.z & 0xffff, span = ue.z >> 16;
+      const int start = ue.x;
+      const int len = ue.y;  // rows of the unit (the whole group)
+      int lo, hi;
+      group_window(ue, r, lo, hi);
       const float sl2 = slopes[h] * LOG2E;
       const float lse2 = lse_next * LOG2E;
-      const int un = next_unit(cu, heads, total, u);
       // the previous unit's TMA stores must have read this warp's slabs before they are rewritten
       if (lane == 0) sm100::bulk_wait_read0();
       __syncwarp();
       sm100::mbar_wait(sp_full, i & 1);
       sm100::tc_fence_after();
-      const float Dp = len == TILE ? bwd_pass1<false>(tS + lane_off, tdP + lane_off, sPa, r, ch, len, sc2, sl2, lse2)
-                                   : bwd_pass1<true>(tS + lane_off, tdP + lane_off, sPa, r, ch, len, sc2, sl2, lse2);
+      const float Dp = (len == TILE && span == 1)
+                           ? bwd_pass1<false>(tS + lane_off, tdP + lane_off, sPa, r, ch, 0, TILE, true, sc2, sl2, lse2)
+                           : bwd_pass1<true>(tS + lane_off, tdP + lane_off, sPa, r, ch, lo, hi, r < len, sc2, sl2, lse2);
       sm100::fence_proxy_async_smem();
       sm100::tc_fence_before();
       __syncwarp();
@@ -1538,7 +1539,7 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
       sm100::tc_fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(elem_done);
-      lse_next = lse_of(un);  // in flight while the MMAs run
+      lse_next = lse_of(i + 1);  // in flight while the MMAs run
       // dV (row = key r), then dQ (row = query r), dK (row = key r): this thread's 32 of the 64
       // columns.  A warp whose 32 rows all lie inside the sequence stages its [32 x 32] bf16 block
       // in its own P / dS slab (64-byte swizzle, conflict-free) and one lane TMA-stores it; the
@@ -1591,7 +1592,6 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
         }
       }
       sm100::tc_fence_before();
-      u = un;
     }
     if (lane == 0) sm100::bulk_wait0();
   }
@@ -2048,7 +2048,7 @@ mb_status attention_fwd(const bf16* qkv, const int* cu, int batch, int nnz, int 
     const char* e = std::getenv("MB_ATTN_SHORT_FWD");
     return e && e[0] == 'v' && e[1] == '1';
   }();
-  const bool short2_fits = batch + 1 <= S2_CU_MAX && batch * heads <= num_sms() * S2_UMAX;
+  const bool short2_fits = batch * heads <= num_sms() * S2_UMAX;
   if (max_seqlen <= TILE && !short_v1 && short2_fits) {
     static bool attr_s2 = false;
     if (!attr_s2) {
@@ -2057,10 +2057,9 @@ mb_status attention_fwd(const bf16* qkv, const int* cu, int batch, int nnz, int 
         return MB_ERR_CUDA;
       attr_s2 = true;
     }
-    GroupUnits G{cu, batch, heads, batch * heads};
-    const int grid = std::max(1, std::min(G.total, num_sms()));
-    if (launch_pdl(attn_fwd_short2_kernel, dim3(grid), dim3(S2_THREADS), S2_SMEM, s, 1, tm, G, d, slopes, O, lse,
-                   nnz) != cudaSuccess)
+    const int grid = std::max(1, std::min(batch * heads, num_sms()));
+    if (launch_pdl(attn_fwd_short2_kernel, dim3(grid), dim3(S2_THREADS), S2_SMEM, s, 1, tm, cu, batch, heads, d, slopes,
+                   O, lse, nnz) != cudaSuccess)
       return MB_ERR_CUDA;
     MB_CHECK_LAUNCH();
     return MB_OK;
@@ -2153,7 +2152,8 @@ mb_status attention_bwd(const bf16* qkv, const bf16* O, const bf16* dO, const fl
   CUtensorMap tq, tdo;
   MB_REQUIRE(make_tmap_bf16_2d(&tq, qkv, 3 * H, nnz, 3 * H, DT, TILE), MB_ERR_CUDA);
   MB_REQUIRE(make_tmap_bf16_2d(&tdo, dO, H, nnz, H, DT, TILE), MB_ERR_CUDA);
-  if (max_seqlen <= TILE) {
+  // short path: per-CTA unit lists hold BW_UMAX units (beyond: the long kernel, which takes any l)
+  if (max_seqlen <= TILE && batch * heads <= std::max(1, std::min(batch * heads, num_sms())) * BW_UMAX) {
     CUtensorMap tdq;  // [32 rows x 32 columns] output blocks, 64-byte swizzle
     MB_REQUIRE(make_tmap_bf16_2d(&tdq, dqkv, 3 * H, nnz, 3 * H, 32, 32, 64), MB_ERR_CUDA);
     static bool attr_s = false;
