@@ -1615,7 +1615,7 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
 // dK [320,384), dQ [384,448).
 // ------------------------------------------------------------------------------------------
 constexpr int LB_NS = 2;
-constexpr int LB_THREADS = SH_THREADS + 64;
+constexpr int LB_THREADS = SH_THREADS + 128;  // compute warps 0-7; warpgroup 2: MMA warp 8, TMA warp 9
 constexpr int LB_SMEM = 2 * 2 * TILE_BYTES + LB_NS * 2 * TILE_BYTES + 2 * P_BYTES + 1024 + 256;
 
 // D[h, t] = sum_c dO[t, h d + c] O[t, h d + c]  (the rowsum(dO o O) of FlashAttention's backward)
@@ -1741,6 +1741,44 @@ __device__ __forceinline__ void bwd_block(uint32_t tS, uint32_t tdP, uint32_t sP
     st_shared_v4(sdSa + p_off(r, 64 * ch + 8 * c), pd[4 * c], pd[4 * c + 1], pd[4 * c + 2], pd[4 * c + 3]);
 }
 
+// the same block computation from S / dP already in registers (v = S, w = dP: this thread's 64 keys)
+template <bool MASK>
+__device__ __forceinline__ void bwd_block_regs(const float (&v)[64], const float (&w)[64], uint32_t sPa, uint32_t sdSa,
+                                               int r, int ch, int lane, int qk_off, int qrows, int keys, float sc2,
+                                               float sl2, float lse2, float rsd, float Drs) {
+  const float rc = (float)(r + qk_off - 64 * ch);
+  uint32_t pd[32];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int c0 = 64 * ch + 16 * c;
+    uint32_t pp[8];
+#pragma unroll
+    for (int jj = 0; jj < 16; jj += 2) {
+      const int j = 16 * c + jj;
+      const float2 dd = __fadd2_rn(make_float2(rc, rc), make_float2(-(float)j, -(float)j - 1.f));
+      const float2 t = __ffma2_rn(make_float2(fabsf(dd.x), fabsf(dd.y)), make_float2(-sl2, -sl2),
+                                  make_float2(-lse2, -lse2));
+      const float2 x = __ffma2_rn(make_float2(v[j], v[j + 1]), make_float2(sc2, sc2), t);
+      float2 pv = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+      if (MASK) {
+        pv.x = (r < qrows && c0 + jj < keys) ? pv.x : 0.f;
+        pv.y = (r < qrows && c0 + jj + 1 < keys) ? pv.y : 0.f;
+      }
+      const float2 ds = __fmul2_rn(pv, __ffma2_rn(make_float2(w[j], w[j + 1]), make_float2(rsd, rsd),
+                                                  make_float2(Drs, Drs)));
+      pp[jj >> 1] = pack_bf16x2(pv.x, pv.y);
+      pd[8 * c + (jj >> 1)] = pack_bf16x2(ds.x, ds.y);
+    }
+    st_shared_v4(sPa + p_off(r, c0), pp[0], pp[1], pp[2], pp[3]);
+    st_shared_v4(sPa + p_off(r, c0 + 8), pp[4], pp[5], pp[6], pp[7]);
+  }
+  if (lane == 0) sm100::bulk_wait_read0();
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    st_shared_v4(sdSa + p_off(r, 64 * ch + 8 * c), pd[4 * c], pd[4 * c + 1], pd[4 * c + 2], pd[4 * c + 3]);
+}
+
 __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
     const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
     const __grid_constant__ CUtensorMap tm_dqkv, const __grid_constant__ CUtensorMap tm_dq, LongUnits U, int d,
@@ -1765,6 +1803,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
   uint64_t* elem_done = bars + 5 + 2 * LB_NS;    // 8 warps
   uint64_t* acc_full = bars + 6 + 2 * LB_NS;
   uint64_t* out_free = bars + 7 + 2 * LB_NS;     // 8 warps: dK/dV of the unit read out
+  uint64_t* sp_free = bars + 8 + 2 * LB_NS;      // 8 warps: S / dP of the block are in registers
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1785,6 +1824,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
     sm100::mbar_init(elem_done, 8);
     sm100::mbar_init(acc_full, 1);
     sm100::mbar_init(out_free, 8);
+    sm100::mbar_init(sp_free, 8);
     sm100::fence_barrier_init();
   }
   if (warp == 0) sm100::tmem_alloc(tslot, 512);
@@ -1803,7 +1843,11 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
     return (U.cu[b + 1] - U.cu[b] + TILE - 1) / TILE;
   };
 
-  if (warp == 9) {
+  // registers: 12 warps leave 168 per thread; warpgroup 2 (producer, MMA issuer, two idle warps) hands
+  // most of its share to the compute warps, which hold a block's S and dP rows in registers
+  if (warp >= 8) {
+    sm100::setmaxnreg_dec<64>();
+    if (warp == 9) {
     // ------------------------------------------------------------------ TMA producer
     if (lane == 0) {
       int uc = 0, g = 0;
@@ -1854,7 +1898,21 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
         mma1(0, 0);
       }
       for (int g = 0; u < U.total; ++g) {
-        sm100::mbar_wait(elem_done, g & 1);  // P_g, dS_g in smem; S/dP consumed
+        // cursor of block g + 1; its S / dP go into TMEM as soon as block g's are in registers, so
+        // they overlap block g's elementwise work and its dV / dK / dQ MMAs
+        int u2 = u, uc2 = uc, i2 = i + 1, nq2 = nq;
+        if (i2 == nq) {
+          u2 = U.next(u);
+          ++uc2;
+          i2 = 0;
+          nq2 = u2 < U.total ? nq_of(u2) : 0;
+        }
+        sm100::mbar_wait(sp_free, g & 1);
+        if (u2 < U.total) {
+          if (i2 == 0) sm100::mbar_wait(&kv_full[uc2 & 1], (uc2 >> 1) & 1);
+          mma1(g + 1, uc2);
+        }
+        sm100::mbar_wait(elem_done, g & 1);  // P_g, dS_g in smem
         if (i == 0 && uc > 0) sm100::mbar_wait(out_free, (uc - 1) & 1);  // previous unit's dK/dV read out
         sm100::tc_fence_after();
         const int sg = g % LB_NS;
@@ -1872,25 +1930,15 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
         }
         sm100::mma_commit(acc_full);
         sm100::mma_commit(&qd_empty[sg]);
-        // cursor of block g + 1
-        int u2 = u, uc2 = uc, i2 = i + 1, nq2 = nq;
-        if (i2 == nq) {
-          sm100::mma_commit(&kv_empty[uc & 1]);  // the unit's last read of K_j, V_j
-          u2 = U.next(u);
-          ++uc2;
-          i2 = 0;
-          nq2 = u2 < U.total ? nq_of(u2) : 0;
-        }
-        if (u2 < U.total) {
-          if (i2 == 0) sm100::mbar_wait(&kv_full[uc2 & 1], (uc2 >> 1) & 1);
-          mma1(g + 1, uc2);
-        }
+        if (i2 == 0) sm100::mma_commit(&kv_empty[uc & 1]);  // the unit's last read of K_j, V_j
         u = u2, uc = uc2, i = i2, nq = nq2;
       }
     }
     __syncwarp();
+    }
   } else {
     // ------------------------------------------------------------------ compute warps 0-7
+    sm100::setmaxnreg_inc<216>();  // 2 x 128 x 216 + 128 x 64 <= 384 x 168
     const int ch = warp >> 2, q4 = warp & 3;
     const int r = q4 * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
@@ -1962,17 +2010,26 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
         else row_stats(un, 0, lse_c, D_c);
         sm100::mbar_wait(sp_full, g & 1);
         sm100::tc_fence_after();
+        float sv[64], dpv[64];
+        sm100::tmem_ld32(tS + lane_off + 64 * ch, sv);
+        sm100::tmem_ld32(tS + lane_off + 64 * ch + 32, sv + 32);
+        sm100::tmem_ld32(tdP + lane_off + 64 * ch, dpv);
+        sm100::tmem_ld32(tdP + lane_off + 64 * ch + 32, dpv + 32);
+        sm100::tmem_ld_wait();
+        sm100::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(sp_free);  // S / dP of the next block may overwrite TMEM
         if (i > 0) {  // block g-1's MMAs finished (P/dS free); its dQ is ready
           sm100::mbar_wait(acc_full, (g - 1) & 1);
           sm100::tc_fence_after();
           dq_out(start, q0 - TILE, len, h, jt);
         }
         if (len - q0 >= TILE && len - kv0 >= TILE)
-          bwd_block<false>(tS + lane_off, tdP + lane_off, sPa, sdSa, r, ch, lane, q0 - kv0, len - q0, len - kv0, sc2,
-                           sl2, lse2, rsd, Drs);
+          bwd_block_regs<false>(sv, dpv, sPa, sdSa, r, ch, lane, q0 - kv0, len - q0, len - kv0, sc2, sl2, lse2, rsd,
+                                Drs);
         else
-          bwd_block<true>(tS + lane_off, tdP + lane_off, sPa, sdSa, r, ch, lane, q0 - kv0, len - q0, len - kv0, sc2,
-                          sl2, lse2, rsd, Drs);
+          bwd_block_regs<true>(sv, dpv, sPa, sdSa, r, ch, lane, q0 - kv0, len - q0, len - kv0, sc2, sl2, lse2, rsd,
+                               Drs);
         sm100::fence_proxy_async_smem();
         sm100::tc_fence_before();
         __syncwarp();
