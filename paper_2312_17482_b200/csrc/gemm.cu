@@ -206,10 +206,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch(&tmA);
     sm100::tma_prefetch(&tmB);
-    if (PAIRED) {
-      sm100::tma_prefetch(&tmC);
-      sm100::tma_prefetch(&tmX);
-    }
+    if (PAIRED || NSCR == 2) sm100::tma_prefetch(&tmC);
+    if (PAIRED) sm100::tma_prefetch(&tmX);
     // ACC == 1 (weight gradients with a fused bias gradient): the MMA's commit goes to mdone and the
     // epilogue warps, after reading the stage's A tile for db, release it to the producer (empty)
     for (int i = 0; i < STAGES; ++i) {
@@ -716,7 +714,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
             }
-            emit_chunk(scrA, v, reinterpret_cast<bf16*>(ep.C), ep.ldc, row0, M, col, N, lane);
+            if (NSCR == 2 && ep.mode == E_BF16) {
+              // the output [32 x 32] block leaves by a TMA store from the warp's second scratch
+              // block (64B swizzle = the scr_at layout), once the previous chunk's store has read it
+              if (lane == 0) sm100::bulk_wait_read<0>();
+              __syncwarp();
+              scr_row_write(scrB, lane, v);
+              sm100::fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                sm100::tma_store_2d(&tmC, scrB, col, row0);
+                sm100::bulk_commit();
+              }
+            } else {
+              emit_chunk(scrA, v, reinterpret_cast<bf16*>(ep.C), ep.ldc, row0, M, col, N, lane);
+            }
           }
         }
         if (CE && ep.mode == E_LSE && row_ok) {
@@ -744,7 +756,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         acc_phase ^= 1;
       }
     }
-    if (PAIRED && lane == 0) sm100::bulk_wait0();  // the TMA stores have left shared memory
+    if ((PAIRED || NSCR == 2) && lane == 0) sm100::bulk_wait0();  // the TMA stores have left shared memory
   }
   sm100::tc_fence_before();
   if (CG == 2) sm100::cluster_sync();
@@ -1164,6 +1176,13 @@ mb_status gemm(const GemmArgs& g, cudaStream_t s) {
   if (g.ep.mode == E_BF16 && g.ep.drop.thr) {  // F2: bias -> dropout -> residual (forward projections)
     MB_REQUIRE(!g.a_t && !g.b_t && BN == 256, MB_ERR_CONFIG);
     return launch<256, 6, 0, 0, 0, 1, 2, 2, 2>(g, ta, tb, sc, s);
+  }
+  if (BN == 256 && g.ep.mode == E_BF16 && !g.a_t && g.ep.ldc % 8 == 0 &&
+      (reinterpret_cast<uintptr_t>(g.ep.C) & 15) == 0) {
+    // forward / dX GEMMs: output by TMA stores (5-stage ring, two scratch blocks per epilogue warp)
+    CUtensorMap tc;
+    MB_REQUIRE(make_tmap_bf16_2d(&tc, g.ep.C, g.N, g.M, g.ep.ldc, 32, 32, 64), MB_ERR_CUDA);
+    return g.b_t ? launch<256, 5, 0, 1, 0, 2>(gd, ta, tb, sc, s, &tc) : launch<256, 5, 0, 0, 0, 2>(gd, ta, tb, sc, s, &tc);
   }
   if (BN == 256) return dispatch_majors<256, 6, 1>(gd, ta, tb, sc, s);
   return dispatch_majors<128, 8, 1>(gd, ta, tb, sc, s);

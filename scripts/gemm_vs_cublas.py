@@ -1,7 +1,9 @@
 """Sustained throughput of the library's GEMMs vs cuBLAS (torch.matmul, bf16 out) on the MosaicBERT-Base
 layer shapes (65536 tokens).  Tuning aid only; both run back to back in one process."""
 import torch
-from paper_2312_17482_b200 import _lib
+import os, sys  # noqa: E401
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2312_17482_b200 import _lib  # noqa: E402
 
 T, Hd, I = 65536, 768, 3072
 dev = "cuda"
