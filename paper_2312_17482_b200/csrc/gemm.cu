@@ -782,7 +782,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 // multiply in place (swizzled layout) and one thread TMA-stores the quarter, releasing its slot
 // once the store has read it.  Warps: 0 operand TMA, 1 MMA, 2 TMEM alloc, 3 Gd TMA, 4-11 epilogue.
 // ------------------------------------------------------------------------------------------------
-constexpr int GB_BN = 256, GB_STAGES = 3, GB_NSLOT = 4;
+#ifndef MB_GB_STAGES
+#define MB_GB_STAGES 4
+#endif
+#ifndef MB_GB_NSLOT
+#define MB_GB_NSLOT 3
+#endif
+constexpr int GB_BN = 256, GB_STAGES = MB_GB_STAGES, GB_NSLOT = MB_GB_NSLOT;
 constexpr int GB_STAGE_BYTES = BM * BK * 2 + (GB_BN / 2) * BK * 2;  // own 128 A rows + half of B (32 KB)
 constexpr int GB_SLOT_BYTES = 2 * BM * 64 * 2;                      // a and g boxes [128 x 64] bf16 (32 KB)
 constexpr int GB_SMEM = GB_STAGES * GB_STAGE_BYTES + GB_NSLOT * GB_SLOT_BYTES + 1024 + 256;
