@@ -1618,23 +1618,43 @@ constexpr int LB_NS = 2;
 constexpr int LB_THREADS = SH_THREADS + 128;  // compute warps 0-7; warpgroup 2: MMA warp 8, TMA warp 9
 constexpr int LB_SMEM = 2 * 2 * TILE_BYTES + LB_NS * 2 * TILE_BYTES + 2 * P_BYTES + 1024 + 256;
 
-// D[h, t] = sum_c dO[t, h d + c] O[t, h d + c]  (the rowsum(dO o O) of FlashAttention's backward)
+// D[h, t] = sum_c dO[t, h d + c] O[t, h d + c]  (the rowsum(dO o O) of FlashAttention's backward).
+// One warp per token row: lane l reads the row's 16-byte chunks l, l + 32, ... (coalesced 512 B per
+// instruction, every load issued before the first use), the d / 8 chunks of a head are reduced
+// across their lanes with shuffles.
 __global__ void attn_bwd_prep_kernel(const bf16* __restrict__ O, const bf16* __restrict__ dO, int nnz, int heads,
                                      int d, float* __restrict__ D) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (t, h)
-  if (i >= (int64_t)nnz * heads) return;
-  const int t = (int)(i / heads), h = (int)(i - (int64_t)t * heads);
-  const bf16* o = O + (size_t)t * heads * d + h * d;
-  const bf16* g = dO + (size_t)t * heads * d + h * d;
-  float acc = 0.f;
-  for (int c = 0; c < d; c += 8) {
-    float a[8], b[8];
-    bf16x8_to_f32(ld_nc_v4(o + c), a);
-    bf16x8_to_f32(ld_nc_v4(g + c), b);
+  const int lane = threadIdx.x & 31;
+  const int H = heads * d, nch = H / 8, cph = d / 8;  // 16-byte chunks per row / per head
+  const int wpb = blockDim.x >> 5;
+  for (int t = blockIdx.x * wpb + (threadIdx.x >> 5); t < nnz; t += gridDim.x * wpb) {
+    const bf16* o = O + (size_t)t * H;
+    const bf16* g = dO + (size_t)t * H;
+    uint4 a[4], b[4];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) acc = fmaf(a[e], b[e], acc);
+    for (int k = 0; k < 4; ++k) {
+      const int i = lane + 32 * k;
+      if (i < nch) {
+        a[k] = ld_nc_v4(o + 8 * i);
+        b[k] = ld_nc_v4(g + 8 * i);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = lane + 32 * k;
+      if (32 * k >= nch) break;  // warp-uniform
+      float acc = 0.f;
+      if (i < nch) {
+        float fa[8], fb[8];
+        bf16x8_to_f32(a[k], fa);
+        bf16x8_to_f32(b[k], fb);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc = fmaf(fa[e], fb[e], acc);
+      }
+      for (int m = 1; m < cph; m <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);  // cph | 32: groups align
+      if (i < nch && (i % cph) == 0) D[(size_t)(i / cph) * nnz + t] = acc;
+    }
   }
-  D[(size_t)h * nnz + t] = acc;
 }
 
 // dq_acc fp32 [nnz, H] -> dqkv[:, :H] bf16, and db_q += column sums: a CTA of DQF_GROUPS row groups x
@@ -1648,16 +1668,30 @@ __global__ void dq_finish_kernel(const float* __restrict__ dq_acc, int nnz, int 
   const int c = cv * 8;
   const int r0 = blockIdx.x * rows_per, r1 = min(nnz, r0 + rows_per);
   float cs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int r = r0 + rg; r < r1; r += DQF_GROUPS) {
-    const float4* src = reinterpret_cast<const float4*>(dq_acc + (size_t)r * H + c);
-    const float4 a = src[0], b = src[1];
-    const float t[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-    const uint4 pk = f32_to_bf16x8(t);
-    *reinterpret_cast<uint4*>(dqkv + (size_t)r * 3 * H + c) = pk;
-    float f[8];
-    bf16x8_to_f32(pk, f);
+  constexpr int U = 4;  // rows in flight per thread: all loads issued before the first conversion
+  for (int rb = r0 + rg; rb < r1; rb += U * DQF_GROUPS) {
+    float4 a[U], b[U];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) cs[e] += f[e];
+    for (int k = 0; k < U; ++k) {
+      const int r = rb + k * DQF_GROUPS;
+      if (r < r1) {
+        const float4* src = reinterpret_cast<const float4*>(dq_acc + (size_t)r * H + c);
+        a[k] = __ldcs(src);
+        b[k] = __ldcs(src + 1);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int r = rb + k * DQF_GROUPS;
+      if (r >= r1) break;
+      const float t[8] = {a[k].x, a[k].y, a[k].z, a[k].w, b[k].x, b[k].y, b[k].z, b[k].w};
+      const uint4 pk = f32_to_bf16x8(t);
+      *reinterpret_cast<uint4*>(dqkv + (size_t)r * 3 * H + c) = pk;
+      float f[8];
+      bf16x8_to_f32(pk, f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) cs[e] += f[e];
+    }
   }
   if (!db) return;
 #pragma unroll
@@ -2242,8 +2276,9 @@ mb_status attention_bwd(const bf16* qkv, const bf16* O, const bf16* dO, const fl
                                        ((slabs * nnz * H * sizeof(float) + 255) & ~size_t(255)));
   if (!dm && cudaMemsetAsync(dq_acc, 0, (size_t)nnz * H * sizeof(float), s) != cudaSuccess) return MB_ERR_CUDA;
   {
-    const int64_t n = (int64_t)nnz * heads;
-    attn_bwd_prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(O, dO, nnz, heads, d, Dg);
+    MB_REQUIRE(H <= 1024, MB_ERR_CONFIG);  // the prep kernel's warp covers a row in at most 4 x 32 chunks
+    attn_bwd_prep_kernel<<<(unsigned)std::max(1, std::min((nnz + 7) / 8, 8 * num_sms())), 256, 0, s>>>(O, dO, nnz,
+                                                                                                       heads, d, Dg);
     MB_CHECK_LAUNCH();
   }
   CUtensorMap tdq, tdqa;  // [32 x 32] dK / dV bf16 blocks (64B swizzle); [32 x 32] fp32 dQ blocks (128B swizzle)
