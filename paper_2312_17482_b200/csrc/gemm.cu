@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch(&tmA);
     sm100::tma_prefetch(&tmB);
-    if (PAIRED || NSCR == 2) sm100::tma_prefetch(&tmC);
+    if (PAIRED || ep.tma_store) sm100::tma_prefetch(&tmC);
     if (PAIRED) sm100::tma_prefetch(&tmX);
     // ACC == 1 (weight gradients with a fused bias gradient): the MMA's commit goes to mdone and the
     // epilogue warps, after reading the stage's A tile for db, release it to the producer (empty)
@@ -714,9 +714,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
             }
-            if (NSCR == 2 && ep.mode == E_BF16) {
-              // the output [32 x 32] block leaves by a TMA store from the warp's second scratch
-              // block (64B swizzle = the scr_at layout), once the previous chunk's store has read it
+            if (ep.tma_store && ep.mode == E_BF16) {
+              // the output [32 x 32] block leaves by a TMA store from the warp's last scratch block
+              // (64B swizzle = the scr_at layout; the first one stages the residual when NSCR == 2),
+              // once the previous chunk's store has read it
               if (lane == 0) sm100::bulk_wait_read<0>();
               __syncwarp();
               scr_row_write(scrB, lane, v);
@@ -756,7 +757,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         acc_phase ^= 1;
       }
     }
-    if ((PAIRED || NSCR == 2) && lane == 0) sm100::bulk_wait0();  // the TMA stores have left shared memory
+    if ((PAIRED || ep.tma_store) && lane == 0) sm100::bulk_wait0();  // the TMA stores have left shared memory
   }
   sm100::tc_fence_before();
   if (CG == 2) sm100::cluster_sync();
@@ -1185,10 +1186,15 @@ mb_status gemm(const GemmArgs& g, cudaStream_t s) {
   }
   if (BN == 256 && g.ep.mode == E_BF16 && !g.a_t && g.ep.ldc % 8 == 0 &&
       (reinterpret_cast<uintptr_t>(g.ep.C) & 15) == 0) {
-    // forward / dX GEMMs: output by TMA stores (5-stage ring, two scratch blocks per epilogue warp)
+    // forward / dX GEMMs: output by TMA stores; with a residual two scratch blocks per epilogue warp
+    // (5-stage ring), without one a single block (6-stage ring)
     CUtensorMap tc;
     MB_REQUIRE(make_tmap_bf16_2d(&tc, g.ep.C, g.N, g.M, g.ep.ldc, 32, 32, 64), MB_ERR_CUDA);
-    return g.b_t ? launch<256, 5, 0, 1, 0, 2>(gd, ta, tb, sc, s, &tc) : launch<256, 5, 0, 0, 0, 2>(gd, ta, tb, sc, s, &tc);
+    GemmArgs gt = gd;
+    gt.ep.tma_store = 1;
+    if (g.ep.res) return g.b_t ? launch<256, 5, 0, 1, 0, 2>(gt, ta, tb, sc, s, &tc)
+                                : launch<256, 5, 0, 0, 0, 2>(gt, ta, tb, sc, s, &tc);
+    return g.b_t ? launch<256, 6, 0, 1, 0, 1>(gt, ta, tb, sc, s, &tc) : launch<256, 6, 0, 0, 0, 1>(gt, ta, tb, sc, s, &tc);
   }
   if (BN == 256) return dispatch_majors<256, 6, 1>(gd, ta, tb, sc, s);
   return dispatch_majors<128, 8, 1>(gd, ta, tb, sc, s);

@@ -51,6 +51,9 @@ struct Epi {
   // the bias-gradient partial slab [splits * num_n, M] (ACC == 1 kernels)
   int* sem = nullptr;
   float* dpart = nullptr;
+  // E_BF16: the output leaves by TMA stores through tmC (host-checked: 16-byte aligned C, ldc % 8 == 0,
+  // and with NSCR == 1 no residual, whose staging would share the single scratch block)
+  int tma_store = 0;
 };
 
 struct GemmArgs {
