@@ -598,7 +598,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 v[j] = pz.x;
                 v[j + 1] = pz.y;
               }
-              emit_chunk(scrA, v, reinterpret_cast<bf16*>(ep.C), ep.ldc, row0, M, col, N, lane);
+              if (ep.tma_store) {  // dz block by TMA store from the warp's scratch (see E_BF16)
+                if (lane == 0) sm100::bulk_wait_read<0>();
+                __syncwarp();
+                scr_row_write(scrA, lane, v);
+                sm100::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                  sm100::tma_store_2d(&tmC, scrA, col, row0);
+                  sm100::bulk_commit();
+                }
+              } else {
+                emit_chunk(scrA, v, reinterpret_cast<bf16*>(ep.C), ep.ldc, row0, M, col, N, lane);
+              }
             }
           } else if (ep.mode == E_F32_ACC) {
             sm100::tmem_ld_wait();
@@ -1178,6 +1190,13 @@ mb_status gemm(const GemmArgs& g, cudaStream_t s) {
   if (g.ep.mode == E_LSE || g.ep.mode == E_DZ) {  // decoder GEMM with fused softmax-cross-entropy
     MB_REQUIRE(!g.a_t && !g.b_t && g.ep.labels && g.ep.bias && BN == 256, MB_ERR_CONFIG);
     MB_REQUIRE(g.ep.mode == E_DZ ? g.ep.lse != nullptr : (g.ep.part && g.ep.zlab), MB_ERR_INVALID_ARG);
+    if (g.ep.mode == E_DZ && g.ep.ldc % 8 == 0 && (reinterpret_cast<uintptr_t>(g.ep.C) & 15) == 0) {
+      CUtensorMap tc;  // dz [M, N] (row stride ldc): [32 x 32] blocks, 64-byte swizzle; columns >= N clipped
+      MB_REQUIRE(make_tmap_bf16_2d(&tc, g.ep.C, g.N, g.M, g.ep.ldc, 32, 32, 64), MB_ERR_CUDA);
+      GemmArgs gt = g;
+      gt.ep.tma_store = 1;
+      return launch<256, 6, 0, 0, 0, 1, 2, 2, 1>(gt, ta, tb, sc, s, &tc);
+    }
     return launch<256, 6, 0, 0, 0, 1, 2, 2, 1>(g, ta, tb, sc, s);
   }
   if (g.ep.mode == E_BF16 && g.ep.drop.thr) {  // F2: bias -> dropout -> residual (forward projections)
