@@ -278,7 +278,7 @@ def main():
     def micro_ids(i):
         return [(i * accum + j) % nb for j in range(accum)]
 
-    def step(i, hostcopy=False):
+    def step(i, hostcopy=False, use_meta=True):
         mbs = []
         for j in micro_ids(i):
             b = dev[j]
@@ -286,7 +286,7 @@ def main():
                 for k in b:
                     b[k].copy_(host[j][k], non_blocking=True)
             mbs.append((b["input_ids"], b["attention_mask"], b["labels"]))
-        return model.train_step(mbs, host_meta=[metas[j] for j in micro_ids(i)])
+        return model.train_step(mbs, host_meta=[metas[j] for j in micro_ids(i)] if use_meta else None)
 
     def barrier():
         if world > 1:
@@ -375,9 +375,24 @@ def main():
         barrier()
         model.check_meta()
         ems = max_over_ranks(e0.elapsed_time(e1))
+        # the same, for a loader that does not know (nnz, max_seqlen, n_masked) on the host: every
+        # micro-step then reads the device index results back (one 16-byte D2H sync per micro-step)
+        barrier()
+        e0.record()
+        for i in range(args.steps):
+            l_ = step(i, hostcopy=True, use_meta=False)
+            float(l_.item())
+        e1.record()
+        barrier()
+        ems_sync = max_over_ranks(e0.elapsed_time(e1))
         h2d = accum * sum(int(v.numel() * v.element_size()) for v in host[0].values())
         e2e = {"value": tok_step * args.steps / (ems / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": 4, "ms_per_step": ems / args.steps}
+               "d2h_bytes_per_step": 4, "ms_per_step": ems / args.steps,
+               "host_meta": "batch (nnz, max_seqlen, n_masked) from the host copy of each micro-batch (the "
+                            "device index results are still computed and checked one micro-step later)",
+               "without_host_meta": {"value": tok_step * args.steps / (ems_sync / 1e3), "unit": "tokens/s",
+                                     "ms_per_step": ems_sync / args.steps,
+                                     "d2h_bytes_per_step": 4 + 16 * accum}}
 
     # ---- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
