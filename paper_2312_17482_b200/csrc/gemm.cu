@@ -43,7 +43,9 @@ struct Cfg {
   static constexpr int DATA = STAGE_BYTES * STAGES;
   static constexpr int SCR = NUM_EPI_WARPS * NSCR * SCR_BYTES;
   static constexpr int BIAS = NUM_EPI_WARPS * 256;  // per-warp staged bias slice of the current tile
-  static constexpr int SMEM = DATA + SCR + BIAS + 1024 + 384;
+  // no alignment slack: the dynamic shared window of these kernels starts 1024-byte aligned (no
+  // static shared memory); the kernel traps if it ever does not
+  static constexpr int SMEM = DATA + SCR + BIAS + 384;
   static constexpr int TMEM_NEED = ACC * BN;  // ACC accumulator stages of BN fp32 columns
   static constexpr int TMEM_COLS = TMEM_NEED <= 256 ? 256 : 512;
 };
@@ -188,7 +190,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   using C = Cfg<BN, STAGES, NSCR, CG, ACC>;
   static_assert(ACC == 2 || A_MN == 1, "the fused bias gradient reads MN-major A tiles");
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  if (sm100::smem_u32(smem_raw) & 1023) __trap();  // Cfg::SMEM reserves no alignment slack
+  uint8_t* smem = smem_raw;
   uint8_t* scr_base = smem + C::DATA;
   uint8_t* bias_base = smem + C::DATA + C::SCR;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATA + C::SCR + C::BIAS);
@@ -1206,13 +1209,13 @@ mb_status gemm(const GemmArgs& g, cudaStream_t s) {
   if (BN == 256 && g.ep.mode == E_BF16 && !g.a_t && g.ep.ldc % 8 == 0 &&
       (reinterpret_cast<uintptr_t>(g.ep.C) & 15) == 0) {
     // forward / dX GEMMs: output by TMA stores; with a residual two scratch blocks per epilogue warp
-    // (5-stage ring), without one a single block (6-stage ring)
+    // and without one a single block, both with the 6-stage ring
     CUtensorMap tc;
     MB_REQUIRE(make_tmap_bf16_2d(&tc, g.ep.C, g.N, g.M, g.ep.ldc, 32, 32, 64), MB_ERR_CUDA);
     GemmArgs gt = gd;
     gt.ep.tma_store = 1;
-    if (g.ep.res) return g.b_t ? launch<256, 5, 0, 1, 0, 2>(gt, ta, tb, sc, s, &tc)
-                                : launch<256, 5, 0, 0, 0, 2>(gt, ta, tb, sc, s, &tc);
+    if (g.ep.res) return g.b_t ? launch<256, 6, 0, 1, 0, 2>(gt, ta, tb, sc, s, &tc)
+                                : launch<256, 6, 0, 0, 0, 2>(gt, ta, tb, sc, s, &tc);
     return g.b_t ? launch<256, 6, 0, 1, 0, 1>(gt, ta, tb, sc, s, &tc) : launch<256, 6, 0, 0, 0, 1>(gt, ta, tb, sc, s, &tc);
   }
   if (BN == 256) return dispatch_majors<256, 6, 1>(gd, ta, tb, sc, s);
