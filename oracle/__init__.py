@@ -10,9 +10,9 @@ follows (P:n = PAPER.md line n, S:n = SPEC.md line n; readings R1..R30 are liste
 
 Parity status: every function here is pinned by a ``-m "not gpu"`` test in tests/test_oracle_*.py
 (closed forms, worked examples, library special cases, finite differences, an independent torch
-fp64 autograd re-implementation).  The only unpinned statement is the absolute value of
-full-depth (12/24-layer) activations, for which the paper prints nothing (pin P17): "parity
-unpinned" beyond the per-layer pins.
+fp64 autograd re-implementation).  The whole-model step at full depth (12 and 24 layers) is pinned
+by P18 (tests/test_oracle_depth.py): an independent torch-fp64 autograd implementation of the entire
+model, loss and every parameter gradient within 1e-9.
 """
 from .mosaicbert import *  # noqa: F401,F403
 from .mosaicbert import __all__ as _mb_all
