@@ -207,7 +207,8 @@ MB_API mb_status mb_attention_forward(const mb_bf16* qkv, const int32_t* cu_seql
  *   dV = P^T dO, dP = dO V^T, dS = P (dP - D), D_i = dO_i . O_i, dQ = dS K/sqrt d, dK = dS^T Q/sqrt d
  * written into dqkv bf16 [nnz, 3H] in the qkv column layout.  If db_qkv != NULL, the column sums of
  * dqkv (the QKV-projection bias gradient) are accumulated into it (fp32 [3H], +=).
- * ws: mb_attention_workspace_bytes. */
+ * ws: mb_attention_workspace_bytes (non-zero for every max_seqlen: short batches with more
+ * (sequence, head) units than the short kernel's per-CTA unit lists hold run on the long kernel). */
 MB_API size_t mb_attention_workspace_bytes(int32_t nnz, int32_t heads, int32_t head_dim, int32_t max_seqlen);
 MB_API mb_status mb_attention_backward(const mb_bf16* qkv, const mb_bf16* O, const mb_bf16* dO, const float* lse,
                                 const int32_t* cu_seqlens, int32_t batch, int32_t nnz, int32_t max_seqlen,

@@ -2214,10 +2214,10 @@ mb_status attention_fwd(const bf16* qkv, const int* cu, int batch, int nnz, int 
 }
 
 // long path: dq_acc fp32 [nnz, H] (deterministic mode: one such slab per key tile) followed by D
-// fp32 [heads, nnz]
+// fp32 [heads, nnz].  Also sized for l <= 128: batches with more (sequence, head) units than the
+// short backward's per-CTA unit lists hold run on the long kernel.
 size_t attention_ws_bytes(int nnz, int heads, int d, int max_seqlen, bool det) {
-  if (max_seqlen <= TILE) return 0;
-  const size_t slabs = det ? (size_t)((max_seqlen + TILE - 1) / TILE) : 1;
+  const size_t slabs = det ? (size_t)((std::max(max_seqlen, 1) + TILE - 1) / TILE) : 1;
   const size_t dq = (slabs * nnz * heads * d * sizeof(float) + 255) & ~size_t(255);
   return dq + (size_t)heads * nnz * sizeof(float);
 }

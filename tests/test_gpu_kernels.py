@@ -502,3 +502,34 @@ def test_embedding_fwd_bwd_repeated_ids(H):
     check("emb.dtype", np64(dT), dTo[0])
     check("emb.dgamma", np64(dg), dgo)
     check("emb.dbeta", np64(dbb), dbo)
+
+
+def test_attention_short_huge_batch_fallbacks():
+    """More (sequence, head) units than the short kernels' per-CTA unit lists hold (forward: v1
+    kernel; backward: the long kernel, which takes any length): 80,000 sequences of length 1..3."""
+    heads, d = 2, 32
+    H = heads * d
+    rng = np.random.default_rng(80000)
+    B, Lmax = 80000, 3
+    lens = rng.integers(1, Lmax + 1, size=B)
+    mask = synth.mask_from_lengths(lens, Lmax)
+    qkv_p = synth.bf16_round(rng.standard_normal((B, Lmax, 3 * H)))
+    do_p = synth.bf16_round(rng.standard_normal((B, Lmax, H))) * mask[..., None]
+    cu, oidx, maxlen, _ = O.unpad_index(mask)
+    nnz = len(oidx)
+    sl_np = mb.alibi_slopes(heads)
+    qkv, dO, cud, sl = _bf(O.unpad(qkv_p, oidx)), _bf(O.unpad(do_p, oidx)), to_dev(cu, I32), to_dev(sl_np, torch.float32)
+    Od = torch.empty(nnz, H, dtype=BF, device="cuda")
+    lse = torch.empty(heads, nnz, dtype=torch.float32, device="cuda")
+    mb.attention_forward(qkv, cud, B, nnz, maxlen, heads, d, sl, Od, lse)
+    dqkv = torch.zeros(nnz, 3 * H, dtype=BF, device="cuda")
+    mb.attention_backward(qkv, Od, dO, lse, cud, B, nnz, maxlen, heads, d, sl, dqkv)
+    sp = lambda t: t.reshape(B, Lmax, heads, d)  # noqa: E731
+    C, cache = O.attention_forward(sp(qkv_p[..., :H]), sp(qkv_p[..., H:2 * H]), sp(qkv_p[..., 2 * H:]), mask,
+                                   sl_np.astype(np.float64))
+    check("huge.O", np64(Od), O.unpad(C.reshape(B, Lmax, H), oidx), max_rel=2e-2)
+    dq, dk, dv = O.attention_backward(sp(do_p), cache)
+    ref = O.unpad(np.concatenate([x.reshape(B, Lmax, H) for x in (dq, dk, dv)], -1), oidx)
+    got = np64(dqkv)
+    for nm, s_ in (("dq", slice(0, H)), ("dk", slice(H, 2 * H)), ("dv", slice(2 * H, 3 * H))):
+        check(f"huge.{nm}", got[:, s_], ref[:, s_])
