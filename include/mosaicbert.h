@@ -315,6 +315,11 @@ MB_API mb_status mb_mlm_loss(const mb_dims* d, const mb_head_params* p, const mb
 MB_API mb_status mb_loss_normalize(const float* loss_sum, const float* count, float count_host, float* inv_out,
                                    float* loss_out, mb_stream_t s);
 
+/* Zero-fill of an fp32 device buffer (n elements; caller-owned): the gradient buckets and scalars
+ * reset at the start of each optimizer step (the += contract of the backward calls, R18's count).
+ * p may have any 4-byte alignment; n == 0 is a no-op. */
+MB_API mb_status mb_zero_f32(float* p, int64_t n, mb_stream_t s);
+
 /* ---------------------------------------------------------------------------------------------
  * F1 — fused decoupled AdamW update (Table A1: beta=(0.9,0.98), eps=1e-6, wd 1e-5):
  *   g' = grad_scale g; m = b1 m + (1-b1) g'; v = b2 v + (1-b2) g'^2;

@@ -69,6 +69,7 @@ _SIGS = {
     "mb_select_workspace_bytes": (SZ, [I32]),
     "mb_mlm_select": (C.c_int, [P, P, I32, I32, P, P, P, P, P, SZ, P]),
     "mb_loss_normalize": (C.c_int, [P, P, F32, P, P, P]),
+    "mb_zero_f32": (C.c_int, [P, C.c_int64, P]),
     "mb_gather_rows": (C.c_int, [P, P, I32, I32, P, P]),
     "mb_scatter_rows": (C.c_int, [P, P, I32, I32, I32, P, P]),
     "mb_layernorm_forward": (C.c_int, [P, P, P, I32, I32, F32, P, P, P]),
@@ -240,6 +241,12 @@ def loss_normalize(loss_sum, count=None, count_host: float = 0.0, inv_out=None, 
     count_host)."""
     _ck("mb_loss_normalize", lib().mb_loss_normalize(_p(loss_sum), _p(count), float(count_host), _p(inv_out),
                                                      _p(loss_out), _stream()))
+
+
+def zero_f32(t):
+    """t (fp32 device tensor, contiguous) = 0 through the library (no torch kernel in the step)."""
+    _ck("mb_zero_f32", lib().mb_zero_f32(_p(t), t.numel(), _stream()))
+    return t
 
 
 def gather_rows(src, idx, n, dst):

@@ -54,6 +54,16 @@ __global__ void sum_kernel(const float* __restrict__ x, int n, float scale, floa
 }
 
 // R18: the step's loss and gradient scale from the device-resident global masked count
+// fp32 zero fill: the unaligned head element-wise, the aligned body in 16-byte stores, the tail
+__global__ void zero_f32_kernel(float* __restrict__ p, int64_t n, int64_t head, int64_t n4) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, step = (int64_t)gridDim.x * blockDim.x;
+  if (tid < head) p[tid] = 0.f;
+  float4* q = reinterpret_cast<float4*>(p + head);
+  for (int64_t i = tid; i < n4; i += step) q[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int64_t t0 = head + 4 * n4;
+  if (tid < n - t0) p[t0 + tid] = 0.f;
+}
+
 __global__ void loss_normalize_kernel(const float* __restrict__ loss_sum, const float* __restrict__ count,
                                       float count_host, float* __restrict__ inv_out, float* __restrict__ loss_out) {
   const float c = count ? *count : count_host;
@@ -348,6 +358,19 @@ mb_status mb_loss_normalize(const float* loss_sum, const float* count, float cou
   MB_REQUIRE_ARCH();
   mb::loss_normalize_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(s)>>>(loss_sum, count, count_host, inv_out,
                                                                           loss_out);
+  MB_CHECK_LAUNCH();
+  return MB_OK;
+}
+
+mb_status mb_zero_f32(float* p, int64_t n, mb_stream_t s) {
+  if (n < 0 || (n > 0 && !p)) return MB_ERR_INVALID_ARG;
+  if (n == 0) return MB_OK;
+  MB_REQUIRE_ARCH();
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
+  const int64_t head = std::min<int64_t>(n, (int64_t)((16 - (reinterpret_cast<uintptr_t>(p) & 15)) & 15) / 4);
+  const int64_t n4 = (n - head) / 4;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, 4 * mb::num_sms()));
+  mb::zero_f32_kernel<<<grid, 256, 0, st>>>(p, n, head, n4);
   MB_CHECK_LAUNCH();
   return MB_OK;
 }

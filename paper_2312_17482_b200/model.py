@@ -155,9 +155,9 @@ class MosaicBert:
 
     def zero_grad(self):
         for b in self.buckets:
-            b.g.zero_()
-        self.loss_sum.zero_()
-        self.count_dev.zero_()
+            L.zero_f32(b.g)
+        L.zero_f32(self.loss_sum)
+        L.zero_f32(self.count_dev)
         self.masked_count = 0
 
     # ------------------------------------------------------------------ buffers
