@@ -320,6 +320,13 @@ MB_API mb_status mb_loss_normalize(const float* loss_sum, const float* count, fl
  * p may have any 4-byte alignment; n == 0 is a no-op. */
 MB_API mb_status mb_zero_f32(float* p, int64_t n, mb_stream_t s);
 
+/* F1 learning-rate schedule (Table A1; reading R34), host function: lr at
+ * optimizer step `step` of `total_steps`: linear warmup 0 -> lr_peak over the first 6 % of the
+ * steps, then linear decay to 0.02 lr_peak at total_steps (step clamped to [0, total_steps]);
+ * lr_peak itself if total_steps <= 0.  The AdamW decay factor for that step is
+ * (lr / lr_peak) * weight_decay (mb_adamw_step's weight_decay argument). */
+MB_API float mb_lr_schedule(int64_t step, int64_t total_steps, float lr_peak);
+
 /* ---------------------------------------------------------------------------------------------
  * F1 — fused decoupled AdamW update (Table A1: beta=(0.9,0.98), eps=1e-6, wd 1e-5):
  *   g' = grad_scale g; m = b1 m + (1-b1) g'; v = b2 v + (1-b2) g'^2;

@@ -70,6 +70,7 @@ _SIGS = {
     "mb_mlm_select": (C.c_int, [P, P, I32, I32, P, P, P, P, P, SZ, P]),
     "mb_loss_normalize": (C.c_int, [P, P, F32, P, P, P]),
     "mb_zero_f32": (C.c_int, [P, C.c_int64, P]),
+    "mb_lr_schedule": (C.c_float, [C.c_int64, C.c_int64, F32]),
     "mb_gather_rows": (C.c_int, [P, P, I32, I32, P, P]),
     "mb_scatter_rows": (C.c_int, [P, P, I32, I32, I32, P, P]),
     "mb_layernorm_forward": (C.c_int, [P, P, P, I32, I32, F32, P, P, P]),
@@ -241,6 +242,11 @@ def loss_normalize(loss_sum, count=None, count_host: float = 0.0, inv_out=None, 
     count_host)."""
     _ck("mb_loss_normalize", lib().mb_loss_normalize(_p(loss_sum), _p(count), float(count_host), _p(inv_out),
                                                      _p(loss_out), _stream()))
+
+
+def lr_schedule(step: int, total_steps: int | None, lr_peak: float) -> float:
+    """F1 schedule (library host function): warmup 6 %, linear decay to 0.02 lr_peak."""
+    return float(lib().mb_lr_schedule(int(step), int(total_steps or 0), float(lr_peak)))
 
 
 def zero_f32(t):

@@ -352,17 +352,10 @@ class MosaicBert:
 
     # ------------------------------------------------------------------ optimizer (F1)
     def lr_at(self, step: int) -> float:
-        """Warmup + linear decay (Table A1): 0 -> lr_peak over the first 6 % of
-        total_steps, then linearly to 0.02 lr_peak at total_steps; constant lr_peak if total_steps
-        is None."""
-        if self.total_steps is None:
-            return self.lr_peak
-        T = self.total_steps
-        step = min(max(step, 0), T)
-        w = 0.06 * T
-        if step <= w:
-            return self.lr_peak * step / w if w > 0 else self.lr_peak
-        return self.lr_peak * (1.0 - 0.98 * (step - w) / (T - w))
+        """Warmup + linear decay (Table A1), computed by the library
+        (mb_lr_schedule): 0 -> lr_peak over the first 6 % of total_steps, then linearly to
+        0.02 lr_peak at total_steps; constant lr_peak if total_steps is None."""
+        return L.lr_schedule(step, self.total_steps, self.lr_peak)
 
     def optimizer_step(self, grad_scale: float, lr: float | None = None, betas=(0.9, 0.98), eps=1e-6,
                        weight_decay: float = 1e-5, grad_scale_dev: torch.Tensor | None = None):

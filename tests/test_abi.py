@@ -121,3 +121,16 @@ def test_workspace_queries(lib):
     # fused softmax-CE: no fp32 logits; the bf16 dz [n, V] (input of the two backward GEMMs) is the
     # largest buffer, and the workspace stays below the unfused logits + dz (6 B per logit)
     assert 100 * 30528 * 2 <= _lib.mlm_workspace_bytes(d, 100) < 100 * 30528 * 6
+
+
+def test_lr_schedule_matches_oracle():
+    """mb_lr_schedule (F1, a host function: callable without a GPU) vs the pinned oracle schedule."""
+    import oracle as O
+    from paper_2312_17482_b200 import _lib
+    pk = 5e-4
+    for T in (1, 7, 100, 70000):
+        for step in sorted({0, 1, T // 20, int(0.06 * T), int(0.06 * T) + 1, T // 2, T - 1, T}):
+            assert _lib.lr_schedule(step, T, pk) == pytest.approx(O.lr_at(step, T, pk), rel=2e-6, abs=1e-12), (T, step)
+        # past the end the library clamps to the final value (the oracle rejects the step)
+        assert _lib.lr_schedule(T + 5, T, pk) == pytest.approx(O.lr_at(T, T, pk), rel=2e-6)
+    assert _lib.lr_schedule(123, None, pk) == pytest.approx(pk, rel=1e-7)
