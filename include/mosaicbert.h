@@ -325,7 +325,7 @@ MB_API mb_status mb_zero_f32(float* p, int64_t n, mb_stream_t s);
  * steps, then linear decay to 0.02 lr_peak at total_steps (step clamped to [0, total_steps]);
  * lr_peak itself if total_steps <= 0.  The AdamW decay factor for that step is
  * (lr / lr_peak) * weight_decay (mb_adamw_step's weight_decay argument). */
-MB_API float mb_lr_schedule(int64_t step, int64_t total_steps, float lr_peak);
+MB_API double mb_lr_schedule(int64_t step, int64_t total_steps, double lr_peak);
 
 /* ---------------------------------------------------------------------------------------------
  * F1 — fused decoupled AdamW update (Table A1: beta=(0.9,0.98), eps=1e-6, wd 1e-5):

@@ -70,7 +70,7 @@ _SIGS = {
     "mb_mlm_select": (C.c_int, [P, P, I32, I32, P, P, P, P, P, SZ, P]),
     "mb_loss_normalize": (C.c_int, [P, P, F32, P, P, P]),
     "mb_zero_f32": (C.c_int, [P, C.c_int64, P]),
-    "mb_lr_schedule": (C.c_float, [C.c_int64, C.c_int64, F32]),
+    "mb_lr_schedule": (C.c_double, [C.c_int64, C.c_int64, C.c_double]),
     "mb_gather_rows": (C.c_int, [P, P, I32, I32, P, P]),
     "mb_scatter_rows": (C.c_int, [P, P, I32, I32, I32, P, P]),
     "mb_layernorm_forward": (C.c_int, [P, P, P, I32, I32, F32, P, P, P]),

@@ -362,13 +362,13 @@ mb_status mb_loss_normalize(const float* loss_sum, const float* count, float cou
   return MB_OK;
 }
 
-float mb_lr_schedule(int64_t step, int64_t total_steps, float lr_peak) {
+double mb_lr_schedule(int64_t step, int64_t total_steps, double lr_peak) {
   if (total_steps <= 0) return lr_peak;
   const double T = (double)total_steps;
   const double t = (double)std::min<int64_t>(std::max<int64_t>(step, 0), total_steps);
   const double w = 0.06 * T;  // warmup: the first 6 % of the steps
-  if (t <= w) return w > 0 ? (float)(lr_peak * t / w) : lr_peak;
-  return (float)(lr_peak * (1.0 - 0.98 * (t - w) / (T - w)));  // linear to 0.02 lr_peak at T
+  if (t <= w) return w > 0 ? lr_peak * t / w : lr_peak;
+  return lr_peak * (1.0 - 0.98 * (t - w) / (T - w));  // linear to 0.02 lr_peak at T
 }
 
 mb_status mb_zero_f32(float* p, int64_t n, mb_stream_t s) {
