@@ -43,12 +43,18 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C2")
     ap.add_argument("--accum", type=int, default=None)
+    ap.add_argument("--force-dp", action="store_true",
+                    help="one rank: still open an NCCL group and run the data-parallel path (bucket allreduces)")
     args = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count()
     torch.cuda.set_device(local)
     backend = os.environ.get("MB_DIST_BACKEND", "nccl")
-    if world > 1:
+    if world > 1 or args.force_dp:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         if backend == "nccl":
             opts = dist.ProcessGroupNCCL.Options()
             opts.is_high_priority_stream = True
@@ -60,6 +66,8 @@ def main():
     d = cfg.dims
     model = MosaicBert(ModelDims(d.hidden, d.heads, d.intermediate, d.vocab, d.layers, d.ln_eps),
                        synth.make_model_params(d, 0, "bert"), device=f"cuda:{local}", seed=rank)
+    if args.force_dp:
+        model._dp = lambda: True
     accum = args.accum or max(1, 4096 // (world * cfg.micro_batch))
     mbs, metas = [], []
     for i in range(accum):
@@ -69,7 +77,7 @@ def main():
     for _ in range(2):
         model.train_step(mbs, host_meta=metas)
     torch.cuda.synchronize()
-    if world > 1:
+    if world > 1 or args.force_dp:
         dist.barrier()
     with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
         model.train_step(mbs, host_meta=metas)
@@ -87,7 +95,7 @@ def main():
             "nccl_exposed_us": sum(e - s for s, e in nccl) - overlap(nccl, ours),
             "trace": os.path.relpath(path, ROOT)}
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1 or args.force_dp:
         dist.destroy_process_group()
 
 

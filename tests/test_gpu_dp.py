@@ -167,3 +167,55 @@ def test_dp_last_microbatch_all_padding(tmp_path):
             assert float(np.abs(r0[f"L{i}_{k}"] - v).max()) <= 2e-5 * max(float(np.abs(v).max()), 1e-30), (i, k)
     for k in ("emb", "w_t", "b_dec"):
         assert float(np.abs(r0[k] - full[k]).max()) <= 2e-5 * max(float(np.abs(full[k]).max()), 1e-30), k
+
+
+def _nccl_one_rank_worker(rank, port, out_dir):
+    import numpy as np
+    import torch.distributed as dist
+    import synth
+    import paper_2312_17482_b200 as mb
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    opts = dist.ProcessGroupNCCL.Options()
+    opts.is_high_priority_stream = True
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0), pg_options=opts)
+    d = synth.TINY
+    params = synth.make_model_params(d, 7, "stress", n_layers=2)
+    dims = mb.ModelDims(d.hidden, d.heads, d.intermediate, d.vocab, 2, d.ln_eps)
+    mbs = [synth.make_batch("C1", 400 + i, B=4) for i in range(3)]
+    dev = [tuple(torch.from_numpy(b[k]).cuda() for k in ("input_ids", "attention_mask", "labels")) for b in mbs]
+    out = {}
+    for tag, dp in (("plain", False), ("nccl", True)):
+        model = mb.MosaicBert(dims, params)
+        if dp:  # one rank, but the whole data-parallel path: count + 14 bucket allreduces through NCCL
+            model._dp = lambda: True
+        losses = [float(model.train_step(dev).item()) for _ in range(2)]  # two optimizer steps
+        torch.cuda.synchronize()
+        out[f"{tag}_loss"] = np.array(losses)
+        out[f"{tag}_w"] = np.concatenate([b.w.float().cpu().numpy() for b in model.buckets])
+    np.savez(os.path.join(out_dir, "nccl1.npz"), **out)
+    dist.destroy_process_group()
+
+
+def test_dp_path_through_nccl_one_rank(tmp_path):
+    """The data-parallel step's NCCL data plane on the B200 (one rank: this pool has one GPU): the
+    in-stream masked-count allreduce, the 14 per-bucket async allreduces issued during the last
+    micro-step's backward on NCCL's high-priority stream, and the optimizer's per-bucket waits.
+    Two optimizer steps give bit-identical losses and weights to the non-distributed path (a 1-rank
+    sum is exact), so every stream / handle ordering of the NCCL path is exercised end to end."""
+    import time
+    import numpy as np
+    import torch.multiprocessing as mp
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = mp.start_processes(_nccl_one_rank_worker, args=(_port(), str(tmp_path)), nprocs=1, start_method="spawn",
+                             join=False)
+    deadline = time.time() + 300
+    while not ctx.join(timeout=5):
+        if time.time() > deadline:
+            for p in ctx.processes:
+                p.kill()
+            pytest.fail("one-rank NCCL data-parallel step did not finish")
+    r = np.load(tmp_path / "nccl1.npz")
+    assert np.array_equal(r["plain_loss"], r["nccl_loss"]), (r["plain_loss"], r["nccl_loss"])
+    assert np.array_equal(r["plain_w"], r["nccl_w"])
