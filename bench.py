@@ -219,6 +219,8 @@ def main():
                     help="leave this many SMs out of the persistent kernels' grids (NCCL kernels run there)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-balance", action="store_true",
+                    help="N > 1: contiguous slices of the global batch instead of the LPT partition")
     ap.add_argument("--micro", type=int, default=None, help="override the per-GPU micro-batch")
     ap.add_argument("--dropout", type=float, default=0.0,
                     help="F2 feed-forward dropout p (P:152 trains with 0.1; the §8(a) hot path is p = 0, R13)")
@@ -260,12 +262,35 @@ def main():
 
     accum = args.accum or max(1, 4096 // (world * micro))  # global batch 4096
 
-    # synthetic micro-batches for this rank (inputs resident in HBM for the device-timed value)
+    # synthetic micro-batches for this rank (inputs resident in HBM for the device-timed value).
+    # N > 1: every rank draws the same global batch (world x accumulation x micro sequences) and
+    # takes its share of an LPT partition on the sequence lengths (per-rank nnz equal
+    # to < 0.5 % on ragged batches, so no rank straggles); --no-balance: contiguous slices.
     nb = max(2, accum)
     host = []
-    for i in range(nb):
-        b = synth.make_batch(cfg, 1000 * int(args.config[1]) + 17 * rank + i, B=micro)
-        host.append({k: torch.from_numpy(b[k]).pin_memory() for k in ("input_ids", "attention_mask", "labels")})
+    balance = None
+    if world > 1:
+        from paper_2312_17482_b200.balance import imbalance, lpt_partition
+        per_rank = accum * micro
+        imb = []
+        for gi in range((nb + accum - 1) // accum):
+            gb = synth.make_batch(cfg, 1000 * int(args.config[1]) + 7919 * gi, B=world * per_rank)
+            lens_g = gb["attention_mask"].sum(1)
+            parts = (lpt_partition(lens_g, world) if not args.no_balance else
+                     [np.arange(r * per_rank, (r + 1) * per_rank) for r in range(world)])
+            imb.append(imbalance(lens_g, parts))
+            mine = parts[rank]
+            for j in range(accum):
+                sel = mine[j * micro:(j + 1) * micro]
+                host.append({k: torch.from_numpy(np.ascontiguousarray(gb[k][sel])).pin_memory()
+                             for k in ("input_ids", "attention_mask", "labels")})
+        host = host[:nb]
+        balance = {"method": "contiguous" if args.no_balance else "LPT on sequence length",
+                   "max_rank_nnz_over_mean": 1.0 + max(imb)}
+    else:
+        for i in range(nb):
+            b = synth.make_batch(cfg, 1000 * int(args.config[1]) + 17 * rank + i, B=micro)
+            host.append({k: torch.from_numpy(b[k]).pin_memory() for k in ("input_ids", "attention_mask", "labels")})
     dev = [{k: v.cuda() for k, v in h.items()} for h in host]
     tokens = [int(h["attention_mask"].sum()) for h in host]
     lens = [h["attention_mask"].sum(1).numpy() for h in host]
@@ -414,6 +439,7 @@ def main():
             "config": {"workload": workload_name(args.config), "global_batch": micro * world * accum,
                        "micro_batch_per_gpu": micro, "accumulation": accum, "seq_len": cfg.seq_len,
                        "parallelism": f"dp{world}", "nccl_sm_carveout": args.nccl_sm_carveout,
+                       "shard_balance": balance,
                        "non_pad_tokens_per_step": tok_step, "l2": "working set >> L2 (weights 275 MB + "
                        "activations ~25 GB per step), no flush needed",
                        "optimizer": "fused AdamW inside the step", "ffn_dropout": args.dropout},
