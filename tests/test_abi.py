@@ -134,3 +134,19 @@ def test_lr_schedule_matches_oracle():
         # past the end the library clamps to the final value (the oracle rejects the step)
         assert _lib.lr_schedule(T + 5, T, pk) == pytest.approx(O.lr_at(T, T, pk), rel=2e-6)
     assert _lib.lr_schedule(123, None, pk) == pytest.approx(pk, rel=1e-7)
+
+
+def test_header_is_plain_c():
+    """include/mosaicbert.h is a C header (extern "C" ABI): it compiles as C99 with -Wall -Werror."""
+    import shutil
+    import tempfile
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    with tempfile.TemporaryDirectory() as d:
+        src = os.path.join(d, "t.c")
+        with open(src, "w") as f:
+            f.write('#include "mosaicbert.h"\nint main(void) { return 0; }\n')
+        r = subprocess.run([cc, "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), "-c", src, "-o",
+                            os.path.join(d, "t.o")], capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
