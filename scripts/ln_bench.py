@@ -1,6 +1,8 @@
 """Time the bf16 LayerNorm forward / backward at C2 size (T = 65536, H = 768).  Tuning aid."""
 import torch
-from paper_2312_17482_b200 import _lib as L
+import os, sys  # noqa: E401
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2312_17482_b200 import _lib as L  # noqa: E402
 
 import os
 T, H = int(os.environ.get("LN_T", 65536)), 768
