@@ -987,6 +987,28 @@ __device__ __forceinline__ float row_scores128(float (&x)[128], int r, int keys,
   return fmaxf(mx2.x, mx2.y);
 }
 
+#ifdef MB_TRACE_L2
+// diagnostic builds only: clock64 stamps of CTA 0's phases over key tiles [TR0, TR0 + 16)
+constexpr int TR0 = 40;
+__device__ long long l2_trace[2][16][8];  // per warpgroup: wait S, S in, S loaded, scores, pv waited, exps, p_ready
+__device__ long long l2_mtrace[2][6][16];  // per t: S_t issued, PV_t issued, S: enter, kv ok; PV: enter
+#define L2TR(t_, c_, ev_)                                                                  \
+  do {                                                                                     \
+    if (blockIdx.x == 0 && (c_) >= TR0 && (c_) < TR0 + 16) l2_trace[t_][(c_) - TR0][ev_] = clock64(); \
+  } while (0)
+#define L2MTR(t_, k_, c_)                                                                  \
+  do {                                                                                     \
+    if (blockIdx.x == 0 && (c_) >= TR0 && (c_) < TR0 + 16) l2_mtrace[t_][k_][(c_) - TR0] = clock64(); \
+  } while (0)
+#else
+#define L2TR(t_, c_, ev_) \
+  do {                    \
+  } while (0)
+#define L2MTR(t_, k_, c_) \
+  do {                    \
+  } while (0)
+#endif
+
 __global__ void __launch_bounds__(L2_THREADS, 1) attn_fwd_long2_kernel(const __grid_constant__ CUtensorMap tm_qkv,
                                                                       PairUnits U, int d,
                                                                       const float* __restrict__ slopes,
@@ -1095,7 +1117,9 @@ __global__ void __launch_bounds__(L2_THREADS, 1) attn_fwd_long2_kernel(const __g
       constexpr uint32_t id_o = sm100::idesc_bf16(128, 64, 0, 1);
       int c[2] = {0, 0}, sc[2] = {0, 0};  // PVs / S issued per query tile t
       auto issue_s = [&](int t, uint32_t q, int sg) {  // S_t = Q_t K_sg^T, once S_t's last tile is in registers
+        L2MTR(t, 3, sc[t]);
         sm100::mbar_wait(&s_free[t], (sc[t] & 1) ^ 1);
+        L2MTR(t, 0, sc[t]);
         ++sc[t];
         sm100::tc_fence_after();
         const uint32_t k = sKVa + sg * 2 * TILE_BYTES;
@@ -1105,7 +1129,9 @@ __global__ void __launch_bounds__(L2_THREADS, 1) attn_fwd_long2_kernel(const __g
         sm100::mma_commit(&s_full[t]);
       };
       auto issue_pv = [&](int t, int sg, bool acc) {  // O_t += P_t V_sg (P_t from TMEM), after P_t is written
+        L2MTR(t, 4, c[t]);
         sm100::mbar_wait(&p_ready[t], c[t] & 1);
+        L2MTR(t, 1, c[t]);
         sm100::tc_fence_after();
         const uint32_t v = sKVa + sg * 2 * TILE_BYTES + TILE_BYTES;
 #pragma unroll
@@ -1121,6 +1147,7 @@ __global__ void __launch_bounds__(L2_THREADS, 1) attn_fwd_long2_kernel(const __g
       auto unit_nkv = [&](int uc) { return (ulist[uc].y + TILE - 1) / TILE; };
       auto issue_s_tile = [&](int t, int uc, int g) {  // S_t of global tile g (unit uc)
         const int sg = g % L2_NS;
+        L2MTR(t, 2, sc[t]);
         if (t == 0) {
           sm100::mbar_wait(&kv_full[sg], (g / L2_NS) & 1);
           sm100::tc_fence_after();
@@ -1205,7 +1232,10 @@ __global__ void __launch_bounds__(L2_THREADS, 1) attn_fwd_long2_kernel(const __g
       float m = -INFINITY, l = 0.f;
       for (int jj = 0; jj < nkv; ++jj) {
         const int kv0 = ((2 * p + jj) % nkv) * TILE;
+        const bool trw = q4 == 0 && lane == 0;
+        if (trw) L2TR(t, c, 0);
         sm100::mbar_wait(&s_full[t], c & 1);
+        if (trw) L2TR(t, c, 1);
         sm100::tc_fence_after();
         float x[128];
 #pragma unroll
@@ -1214,6 +1244,7 @@ __global__ void __launch_bounds__(L2_THREADS, 1) attn_fwd_long2_kernel(const __g
         sm100::tc_fence_before();
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive(&s_free[t]);
+        if (trw) L2TR(t, c, 2);
         if (jj == 0 && pend) {  // the previous unit's O (its PVs are done once this tile's S is in)
           readout(pd_st, pd_len, pd_h, pd_row, pd_m, pd_l);
           pend = false;
@@ -1221,6 +1252,7 @@ __global__ void __launch_bounds__(L2_THREADS, 1) attn_fwd_long2_kernel(const __g
         const int keys = len - kv0;
         const float mx = keys >= TILE ? row_scores128<false>(x, r, keys, slr, q0 - kv0)
                                       : row_scores128<true>(x, r, keys, slr, q0 - kv0);
+        if (trw) L2TR(t, c, 3);
         if (jj > 0) {
           // P_t of the previous key tile must have been consumed before P_t is rewritten, and a
           // rescale of O_t must follow that PV
@@ -1245,6 +1277,7 @@ __global__ void __launch_bounds__(L2_THREADS, 1) attn_fwd_long2_kernel(const __g
           m = mx;
         }
         const float nm = -m * sc2;
+        if (trw) L2TR(t, c, 4);
         float2 ls = make_float2(0.f, 0.f);
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
@@ -1259,11 +1292,13 @@ __global__ void __launch_bounds__(L2_THREADS, 1) attn_fwd_long2_kernel(const __g
           }
           sm100::tmem_st32(tP + 32 * hh, pk);
         }
+        if (trw) L2TR(t, c, 5);
         l += ls.x + ls.y;
         sm100::tmem_st_wait();
         sm100::tc_fence_before();
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive(&p_ready[t]);
+        if (trw) L2TR(t, c, 6);
         ++c;
       }
       pend = true;
@@ -2338,3 +2373,10 @@ mb_status mb_attention_backward(const mb_bf16* qkv, const mb_bf16* O, const mb_b
 }
 
 }  // extern "C"
+
+#ifdef MB_TRACE_L2
+extern "C" MB_API int mb_diag_l2_trace(long long* host) {  // diagnostic builds only
+  if (cudaMemcpyFromSymbol(host, mb::l2_trace, sizeof(mb::l2_trace)) != cudaSuccess) return 1;
+  return cudaMemcpyFromSymbol(host + 2 * 16 * 8, mb::l2_mtrace, sizeof(mb::l2_mtrace)) != cudaSuccess;
+}
+#endif
