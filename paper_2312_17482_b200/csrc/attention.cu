@@ -393,22 +393,28 @@ template <bool MASK>
 __device__ __forceinline__ float row_scores_win(float (&x)[128], int r, int lo, int hi, float slr) {
   float rc = (float)r;
   asm volatile("" : "+f"(rc));  // keep the distance ramp inside the unit loop (hoisted, it spills)
-  float2 dd = make_float2(rc, rc - 1.f);
-  float2 mx2 = make_float2(-INFINITY, -INFINITY);
+  // two interleaved distance / max chains (key pairs j = 4i + 2q) instead of one 64-deep chain each
+  float2 dd[2] = {make_float2(rc, rc - 1.f), make_float2(rc - 2.f, rc - 3.f)};
+  float2 mx[2] = {make_float2(-INFINITY, -INFINITY), make_float2(-INFINITY, -INFINITY)};
   const uint32_t w = (uint32_t)(hi - lo);
 #pragma unroll
-  for (int j = 0; j < 128; j += 2) {
-    float2 t = __ffma2_rn(make_float2(fabsf(dd.x), fabsf(dd.y)), make_float2(-slr, -slr), make_float2(x[j], x[j + 1]));
-    dd = __fadd2_rn(dd, make_float2(-2.f, -2.f));
-    if (MASK) {
-      t.x = (uint32_t)(j - lo) < w ? t.x : -INFINITY;
-      t.y = (uint32_t)(j + 1 - lo) < w ? t.y : -INFINITY;
+  for (int j0 = 0; j0 < 128; j0 += 4) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int j = j0 + 2 * q;
+      float2 t = __ffma2_rn(make_float2(fabsf(dd[q].x), fabsf(dd[q].y)), make_float2(-slr, -slr),
+                            make_float2(x[j], x[j + 1]));
+      dd[q] = __fadd2_rn(dd[q], make_float2(-4.f, -4.f));
+      if (MASK) {
+        t.x = (uint32_t)(j - lo) < w ? t.x : -INFINITY;
+        t.y = (uint32_t)(j + 1 - lo) < w ? t.y : -INFINITY;
+      }
+      x[j] = t.x;
+      x[j + 1] = t.y;
+      mx[q] = make_float2(fmaxf(mx[q].x, t.x), fmaxf(mx[q].y, t.y));
     }
-    x[j] = t.x;
-    x[j + 1] = t.y;
-    mx2 = make_float2(fmaxf(mx2.x, t.x), fmaxf(mx2.y, t.y));
   }
-  return fmaxf(mx2.x, mx2.y);
+  return fmaxf(fmaxf(mx[0].x, mx[0].y), fmaxf(mx[1].x, mx[1].y));
 }
 
 __global__ void __launch_bounds__(S2_THREADS, 1) attn_fwd_short2_kernel(const __grid_constant__ CUtensorMap tm_qkv,
@@ -574,7 +580,7 @@ __global__ void __launch_bounds__(S2_THREADS, 1) attn_fwd_short2_kernel(const __
       if (span == 1 && glen == TILE) m = row_scores_win<false>(x, r, 0, TILE, slr);
       else m = row_scores_win<true>(x, r, lo, hi, slr);
       const float nm = -m * sc2;
-      float2 ls = make_float2(0.f, 0.f);
+      float2 ls[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};  // two row-sum chains
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         float pk[32];
@@ -583,7 +589,7 @@ __global__ void __launch_bounds__(S2_THREADS, 1) attn_fwd_short2_kernel(const __
           const int c = 64 * hh + 2 * q;
           const float2 tt = __ffma2_rn(make_float2(x[c], x[c + 1]), make_float2(sc2, sc2), make_float2(nm, nm));
           const float2 e = make_float2(ex2_approx(tt.x), ex2_approx(tt.y));
-          ls = __fadd2_rn(ls, e);
+          ls[q & 1] = __fadd2_rn(ls[q & 1], e);
           pk[q] = __uint_as_float(pack_bf16x2(e.x, e.y));
         }
         sm100::tmem_st32(tP + 32 * hh, pk);
@@ -592,7 +598,7 @@ __global__ void __launch_bounds__(S2_THREADS, 1) attn_fwd_short2_kernel(const __
       sm100::tc_fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&p_ready[t]);
-      pk_k = k, pk_st = st, pk_h = h, pk_glen = glen, pk_m = m, pk_l = ls.x + ls.y;
+      pk_k = k, pk_st = st, pk_h = h, pk_glen = glen, pk_m = m, pk_l = (ls[0].x + ls[1].x) + (ls[0].y + ls[1].y);
       ++k;
     }
     if (pk_k >= 0) readout(pk_k, pk_st, pk_h, pk_glen, pk_m, pk_l);
@@ -966,25 +972,36 @@ struct PairUnits {  // unit u = (b * heads + h) * QP + p, valid iff 256 p < len_
 };
 
 // ALiBi-biased scores of one full query row (128 keys, one thread per row), unscaled domain:
-// x_j += -slr |(r + qk_off) - j|, keys at or past `keys` masked when MASK; returns max_j
+// x_j += -slr |(r + qk_off) - j|, keys at or past `keys` masked when MASK; returns max_j.
+// Two interleaved distance / max chains (key pairs j = 4i + 2q, q = 0, 1) so that neither the
+// distance update nor the running max is a 64-deep dependency chain.
 template <bool MASK>
 __device__ __forceinline__ float row_scores128(float (&x)[128], int r, int keys, float slr, int qk_off) {
   const float rc = (float)(r + qk_off);
-  float2 dd = make_float2(rc, rc - 1.f);
-  float2 mx2 = make_float2(-INFINITY, -INFINITY);
+  float2 dd[2], mx[2];
 #pragma unroll
-  for (int j = 0; j < 128; j += 2) {
-    float2 t = __ffma2_rn(make_float2(fabsf(dd.x), fabsf(dd.y)), make_float2(-slr, -slr), make_float2(x[j], x[j + 1]));
-    dd = __fadd2_rn(dd, make_float2(-2.f, -2.f));
-    if (MASK) {
-      t.x = j < keys ? t.x : -INFINITY;
-      t.y = j + 1 < keys ? t.y : -INFINITY;
-    }
-    x[j] = t.x;
-    x[j + 1] = t.y;
-    mx2 = make_float2(fmaxf(mx2.x, t.x), fmaxf(mx2.y, t.y));
+  for (int q = 0; q < 2; ++q) {
+    dd[q] = make_float2(rc - (float)(2 * q), rc - (float)(2 * q + 1));
+    mx[q] = make_float2(-INFINITY, -INFINITY);
   }
-  return fmaxf(mx2.x, mx2.y);
+#pragma unroll
+  for (int j0 = 0; j0 < 128; j0 += 4) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int j = j0 + 2 * q;
+      float2 t = __ffma2_rn(make_float2(fabsf(dd[q].x), fabsf(dd[q].y)), make_float2(-slr, -slr),
+                            make_float2(x[j], x[j + 1]));
+      dd[q] = __fadd2_rn(dd[q], make_float2(-4.f, -4.f));
+      if (MASK) {
+        t.x = j < keys ? t.x : -INFINITY;
+        t.y = j + 1 < keys ? t.y : -INFINITY;
+      }
+      x[j] = t.x;
+      x[j + 1] = t.y;
+      mx[q] = make_float2(fmaxf(mx[q].x, t.x), fmaxf(mx[q].y, t.y));
+    }
+  }
+  return fmaxf(fmaxf(mx[0].x, mx[0].y), fmaxf(mx[1].x, mx[1].y));
 }
 
 #ifdef MB_TRACE_L2
@@ -1278,7 +1295,7 @@ __global__ void __launch_bounds__(L2_THREADS, 1) attn_fwd_long2_kernel(const __g
         }
         const float nm = -m * sc2;
         if (trw) L2TR(t, c, 4);
-        float2 ls = make_float2(0.f, 0.f);
+        float2 ls[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};  // two row-sum chains
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
           float pk[32];
@@ -1287,13 +1304,13 @@ __global__ void __launch_bounds__(L2_THREADS, 1) attn_fwd_long2_kernel(const __g
             const int cc = 64 * hh + 2 * q;
             const float2 tt = __ffma2_rn(make_float2(x[cc], x[cc + 1]), make_float2(sc2, sc2), make_float2(nm, nm));
             const float2 ee = make_float2(ex2_approx(tt.x), ex2_approx(tt.y));
-            ls = __fadd2_rn(ls, ee);
+            ls[q & 1] = __fadd2_rn(ls[q & 1], ee);
             pk[q] = __uint_as_float(pack_bf16x2(ee.x, ee.y));
           }
           sm100::tmem_st32(tP + 32 * hh, pk);
         }
         if (trw) L2TR(t, c, 5);
-        l += ls.x + ls.y;
+        l += (ls[0].x + ls[1].x) + (ls[0].y + ls[1].y);
         sm100::tmem_st_wait();
         sm100::tc_fence_before();
         __syncwarp();
