@@ -1008,7 +1008,7 @@ __device__ __forceinline__ float row_scores128(float (&x)[128], int r, int keys,
 // diagnostic builds only: clock64 stamps of CTA 0's phases over key tiles [TR0, TR0 + 16)
 constexpr int TR0 = 40;
 __device__ long long l2_trace[2][16][8];  // per warpgroup: wait S, S in, S loaded, scores, pv waited, exps, p_ready
-__device__ long long l2_mtrace[2][6][16];  // per t: S_t issued, PV_t issued, S: enter, kv ok; PV: enter
+__device__ long long l2_mtrace[2][8][16];  // per t: S_t issued, PV_t issued, S: enter, kv ok; PV: enter
 #define L2TR(t_, c_, ev_)                                                                  \
   do {                                                                                     \
     if (blockIdx.x == 0 && (c_) >= TR0 && (c_) < TR0 + 16) l2_trace[t_][(c_) - TR0][ev_] = clock64(); \
@@ -1128,7 +1128,7 @@ __global__ void __launch_bounds__(L2_THREADS, 1) attn_fwd_long2_kernel(const __g
           sm100::tma_load_2d(kv + TILE_BYTES, &tm_qkv, &kv_full[sg], 2 * H + h * d, st + j * TILE);
         }
       }
-    } else if (warp == 8 && lane == 0) {
+    } else if (warp == 8) {  // the whole warp runs the issue loop; one elected lane issues
       // ------------------------------------------------------------------ MMA issuer
       constexpr uint32_t id_s = sm100::idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t id_o = sm100::idesc_bf16(128, 64, 0, 1);
@@ -1141,9 +1141,10 @@ __global__ void __launch_bounds__(L2_THREADS, 1) attn_fwd_long2_kernel(const __g
         sm100::tc_fence_after();
         const uint32_t k = sKVa + sg * 2 * TILE_BYTES;
         for (int kk = 0; kk < d / 16; ++kk)
-          sm100::mma_bf16_ss(tbase + 128 * t, sm100::desc_kmajor_sw128(q + kk * 32), sm100::desc_kmajor_sw128(k + kk * 32),
+          sm100::mma_bf16_ss_w(tbase + 128 * t, sm100::desc_kmajor_sw128(q + kk * 32), sm100::desc_kmajor_sw128(k + kk * 32),
                              id_s, kk > 0);
-        sm100::mma_commit(&s_full[t]);
+        L2MTR(t, 5, sc[t] - 1);
+        sm100::mma_commit_w(&s_full[t]);
       };
       auto issue_pv = [&](int t, int sg, bool acc) {  // O_t += P_t V_sg (P_t from TMEM), after P_t is written
         L2MTR(t, 4, c[t]);
@@ -1153,9 +1154,10 @@ __global__ void __launch_bounds__(L2_THREADS, 1) attn_fwd_long2_kernel(const __g
         const uint32_t v = sKVa + sg * 2 * TILE_BYTES + TILE_BYTES;
 #pragma unroll
         for (int kk = 0; kk < TILE / 16; ++kk)
-          sm100::mma_bf16_ts(tbase + 384 + 64 * t, tbase + 256 + 64 * t + 8 * kk,
+          sm100::mma_bf16_ts_w(tbase + 384 + 64 * t, tbase + 256 + 64 * t + 8 * kk,
                              sm100::desc_mnmajor_sw128(v + kk * 2048, 8192), id_o, (acc || kk > 0) ? 1u : 0u);
-        sm100::mma_commit(&pv_done[t]);
+        L2MTR(t, 6, c[t]);
+        sm100::mma_commit_w(&pv_done[t]);
         ++c[t];
       };
       // flattened key-tile sequence over this CTA's units: S_t of tile g + 1 is issued as soon as
@@ -1196,9 +1198,9 @@ __global__ void __launch_bounds__(L2_THREADS, 1) attn_fwd_long2_kernel(const __g
           issue_pv(0, g % L2_NS, jj > 0);
           if (next_two) issue_s_tile(1, nu, g + 1);
           if (two) issue_pv(1, g % L2_NS, jj > 0);
-          sm100::mma_commit(&kv_empty[g % L2_NS]);
+          sm100::mma_commit_w(&kv_empty[g % L2_NS]);
         }
-        sm100::mma_commit(&q_empty[uc & 1]);  // every S of this unit has been issued
+        sm100::mma_commit_w(&q_empty[uc & 1]);  // every S of this unit has been issued
       }
     }
     __syncwarp();
