@@ -1455,29 +1455,32 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
 
   if (warp == 8) {
     // ------------------------------------------------------------------ producer / MMA issuer
-    if (lane == 0) {
+    {  // the whole warp runs the loop: lane 0 issues the TMA loads, one elected lane the MMAs
       auto buf_addr = [&](int b) { return bufs + b * BWD_BUF_BYTES; };
       auto issue_loads = [&](int i, int b) {
         const int4 e = ulist[i];
         const int h = e.z & 0xffff, st = e.x;
         uint8_t* base = buf_addr(b);
-        sm100::mbar_arrive_expect_tx(&load_full[b], BWD_BUF_BYTES);
-        sm100::tma_load_2d(base, &tm_qkv, &load_full[b], h * d, st);
-        sm100::tma_load_2d(base + TILE_BYTES, &tm_qkv, &load_full[b], H + h * d, st);
-        sm100::tma_load_2d(base + 2 * TILE_BYTES, &tm_qkv, &load_full[b], 2 * H + h * d, st);
-        sm100::tma_load_2d(base + 3 * TILE_BYTES, &tm_do, &load_full[b], h * d, st);
+        if (lane == 0) {
+          sm100::mbar_arrive_expect_tx(&load_full[b], BWD_BUF_BYTES);
+          sm100::tma_load_2d(base, &tm_qkv, &load_full[b], h * d, st);
+          sm100::tma_load_2d(base + TILE_BYTES, &tm_qkv, &load_full[b], H + h * d, st);
+          sm100::tma_load_2d(base + 2 * TILE_BYTES, &tm_qkv, &load_full[b], 2 * H + h * d, st);
+          sm100::tma_load_2d(base + 3 * TILE_BYTES, &tm_do, &load_full[b], h * d, st);
+        }
+        __syncwarp();
       };
       auto mma1 = [&](int b) {  // S = Q K^T, dP = dO V^T
         const uint32_t q = sm100::smem_u32(buf_addr(b));
         const uint32_t k = q + TILE_BYTES, v = q + 2 * TILE_BYTES, o = q + 3 * TILE_BYTES;
         constexpr uint32_t id_s = sm100::idesc_bf16(128, 128, 0, 0);
         for (int kk = 0; kk < d / 16; ++kk) {
-          sm100::mma_bf16_ss(tS, sm100::desc_kmajor_sw128(q + kk * 32), sm100::desc_kmajor_sw128(k + kk * 32), id_s,
+          sm100::mma_bf16_ss_w(tS, sm100::desc_kmajor_sw128(q + kk * 32), sm100::desc_kmajor_sw128(k + kk * 32), id_s,
                              kk > 0);
-          sm100::mma_bf16_ss(tdP, sm100::desc_kmajor_sw128(o + kk * 32), sm100::desc_kmajor_sw128(v + kk * 32), id_s,
+          sm100::mma_bf16_ss_w(tdP, sm100::desc_kmajor_sw128(o + kk * 32), sm100::desc_kmajor_sw128(v + kk * 32), id_s,
                              kk > 0);
         }
-        sm100::mma_commit(sp_full);
+        sm100::mma_commit_w(sp_full);
       };
       constexpr uint32_t id_t = sm100::idesc_bf16(128, 64, 1, 1);
       constexpr uint32_t id_q = sm100::idesc_bf16(128, 64, 0, 1);
@@ -1485,21 +1488,21 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
         const uint32_t o = sm100::smem_u32(buf_addr(b)) + 3 * TILE_BYTES;
 #pragma unroll
         for (int kk = 0; kk < TILE / 16; ++kk)
-          sm100::mma_bf16_ss(tdV, sm100::desc_mnmajor_sw128(sPa + kk * 2048, TILE * 128),
+          sm100::mma_bf16_ss_w(tdV, sm100::desc_mnmajor_sw128(sPa + kk * 2048, TILE * 128),
                              sm100::desc_mnmajor_sw128(o + kk * 2048, 8192), id_t, kk > 0);
-        sm100::mma_commit(dv_full);
+        sm100::mma_commit_w(dv_full);
       };
       auto mma_dkq = [&](int b) {  // dK = dS^T Q, dQ = dS K
         const uint32_t q = sm100::smem_u32(buf_addr(b));
         const uint32_t k = q + TILE_BYTES;
 #pragma unroll
         for (int kk = 0; kk < TILE / 16; ++kk) {
-          sm100::mma_bf16_ss(tdK, sm100::desc_mnmajor_sw128(sdSa + kk * 2048, TILE * 128),
+          sm100::mma_bf16_ss_w(tdK, sm100::desc_mnmajor_sw128(sdSa + kk * 2048, TILE * 128),
                              sm100::desc_mnmajor_sw128(q + kk * 2048, 8192), id_t, kk > 0);
-          sm100::mma_bf16_ss(tdQ, sm100::desc_kmajor_sw128(sdSa + (kk >> 2) * (TILE * 128) + (kk & 3) * 32),
+          sm100::mma_bf16_ss_w(tdQ, sm100::desc_kmajor_sw128(sdSa + (kk >> 2) * (TILE * 128) + (kk & 3) * 32),
                              sm100::desc_mnmajor_sw128(k + kk * 2048, 8192), id_q, kk > 0);
         }
-        sm100::mma_commit(acc_full);
+        sm100::mma_commit_w(acc_full);
       };
       if (nunits > 0) issue_loads(0, 0);
       if (nunits > 1) issue_loads(1, 1);
@@ -1962,7 +1965,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
     __syncwarp();
   } else if (warp == 8) {
     // ------------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    {  // the whole warp runs the issue loop; one elected lane issues
       constexpr uint32_t id_s = sm100::idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t id_t = sm100::idesc_bf16(128, 64, 1, 1);  // P^T dO, dS^T Q
       constexpr uint32_t id_q = sm100::idesc_bf16(128, 64, 0, 1);  // dS K
@@ -1974,12 +1977,12 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
         const uint32_t q = sQDa + sg * 2 * TILE_BYTES, o = q + TILE_BYTES;
         const uint32_t k = sKVa + (ucc & 1) * 2 * TILE_BYTES, v = k + TILE_BYTES;
         for (int kk = 0; kk < d / 16; ++kk) {
-          sm100::mma_bf16_ss(tS, sm100::desc_kmajor_sw128(q + kk * 32), sm100::desc_kmajor_sw128(k + kk * 32), id_s,
+          sm100::mma_bf16_ss_w(tS, sm100::desc_kmajor_sw128(q + kk * 32), sm100::desc_kmajor_sw128(k + kk * 32), id_s,
                              kk > 0);
-          sm100::mma_bf16_ss(tdP, sm100::desc_kmajor_sw128(o + kk * 32), sm100::desc_kmajor_sw128(v + kk * 32), id_s,
+          sm100::mma_bf16_ss_w(tdP, sm100::desc_kmajor_sw128(o + kk * 32), sm100::desc_kmajor_sw128(v + kk * 32), id_s,
                              kk > 0);
         }
-        sm100::mma_commit(sp_full);
+        sm100::mma_commit_w(sp_full);
       };
       if (u < U.total) {
         sm100::mbar_wait(&kv_full[0], 0);
@@ -2009,16 +2012,16 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
 #pragma unroll
         for (int kk = 0; kk < TILE / 16; ++kk) {
           const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
-          sm100::mma_bf16_ss(tdV, sm100::desc_mnmajor_sw128(sPa + kk * 2048, TILE * 128),
+          sm100::mma_bf16_ss_w(tdV, sm100::desc_mnmajor_sw128(sPa + kk * 2048, TILE * 128),
                              sm100::desc_mnmajor_sw128(o + kk * 2048, 8192), id_t, acc);
-          sm100::mma_bf16_ss(tdK, sm100::desc_mnmajor_sw128(sdSa + kk * 2048, TILE * 128),
+          sm100::mma_bf16_ss_w(tdK, sm100::desc_mnmajor_sw128(sdSa + kk * 2048, TILE * 128),
                              sm100::desc_mnmajor_sw128(q + kk * 2048, 8192), id_t, acc);
-          sm100::mma_bf16_ss(tdQ, sm100::desc_kmajor_sw128(sdSa + (kk >> 2) * (TILE * 128) + (kk & 3) * 32),
+          sm100::mma_bf16_ss_w(tdQ, sm100::desc_kmajor_sw128(sdSa + (kk >> 2) * (TILE * 128) + (kk & 3) * 32),
                              sm100::desc_mnmajor_sw128(k + kk * 2048, 8192), id_q, kk > 0);
         }
-        sm100::mma_commit(acc_full);
-        sm100::mma_commit(&qd_empty[sg]);
-        if (i2 == 0) sm100::mma_commit(&kv_empty[uc & 1]);  // the unit's last read of K_j, V_j
+        sm100::mma_commit_w(acc_full);
+        sm100::mma_commit_w(&qd_empty[sg]);
+        if (i2 == 0) sm100::mma_commit_w(&kv_empty[uc & 1]);  // the unit's last read of K_j, V_j
         u = u2, uc = uc2, i = i2, nq = nq2;
       }
     }

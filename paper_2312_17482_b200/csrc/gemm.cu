@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
+    if (rank == 0) {  // the whole warp runs the issue loop; one elected lane issues
       constexpr uint32_t idesc = sm100::idesc_bf16(BM * CG, BN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
@@ -302,19 +302,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t ad = A_MN ? sm100::desc_mnmajor_sw128(sa + k * 2048, 8192) : sm100::desc_kmajor_sw128(sa + k * 32);
             const uint64_t bd = B_MN ? sm100::desc_mnmajor_sw128(sb + k * 2048, 8192) : sm100::desc_kmajor_sw128(sb + k * 32);
-            if (CG == 2) sm100::mma_bf16_ss_pair(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-            else sm100::mma_bf16_ss(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            if (CG == 2) sm100::mma_bf16_ss_pair_w(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            else sm100::mma_bf16_ss_w(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
           uint64_t* rel = ACC == 1 ? &mdone[stage] : &empty[stage];
-          if (CG == 2) sm100::mma_commit_pair(rel);
-          else sm100::mma_commit(rel);
+          if (CG == 2) sm100::mma_commit_pair_w(rel);
+          else sm100::mma_commit_w(rel);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        if (CG == 2) sm100::mma_commit_pair(&tfull[acc]);
-        else sm100::mma_commit(&tfull[acc]);
+        if (CG == 2) sm100::mma_commit_pair_w(&tfull[acc]);
+        else sm100::mma_commit_w(&tfull[acc]);
         if (++acc == ACC) {
           acc = 0;
           acc_phase ^= 1;
@@ -903,7 +903,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
+    if (rank == 0) {  // the whole warp runs the issue loop; one elected lane issues
       constexpr uint32_t idesc = sm100::idesc_bf16(2 * BM, GB_BN, 0, 1);
       int stage = 0;
       uint32_t phase = 0;
@@ -922,16 +922,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const uint32_t sb = sa + BM * BK * 2;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            sm100::mma_bf16_ss_pair(d_tmem, sm100::desc_kmajor_sw128(sa + k * 32),
+            sm100::mma_bf16_ss_pair_w(d_tmem, sm100::desc_kmajor_sw128(sa + k * 32),
                                     sm100::desc_mnmajor_sw128(sb + k * 2048, 8192), idesc,
                                     (kb > kb0 || k > 0) ? 1u : 0u);
-          sm100::mma_commit_pair(&empty[stage]);
+          sm100::mma_commit_pair_w(&empty[stage]);
           if (++stage == GB_STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        sm100::mma_commit_pair(&tfull[acc]);
+        sm100::mma_commit_pair_w(&tfull[acc]);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
