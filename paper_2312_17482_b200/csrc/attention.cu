@@ -1673,7 +1673,7 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
 // ------------------------------------------------------------------------------------------
 constexpr int LB_NS = 2;
 constexpr int LB_THREADS = SH_THREADS + 128;  // compute warps 0-7; warpgroup 2: MMA warp 8, TMA warp 9
-constexpr int LB_SMEM = 2 * 2 * TILE_BYTES + LB_NS * 2 * TILE_BYTES + 2 * P_BYTES + 1024 + 256;
+constexpr int LB_SMEM = 2 * 2 * TILE_BYTES + LB_NS * 2 * TILE_BYTES + 3 * P_BYTES + 1024 + 256;  // P + 2 x dS
 
 // D[h, t] = sum_c dO[t, h d + c] O[t, h d + c]  (the rowsum(dO o O) of FlashAttention's backward).
 // One warp per token row: lane l reads the row's 16-byte chunks l, l + 32, ... (coalesced 512 B per
@@ -1884,8 +1884,8 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
   uint8_t* sKV = smem;                           // 2 x (K, V)
   uint8_t* sQD = sKV + 2 * 2 * TILE_BYTES;       // LB_NS x (Q, dO)
   uint8_t* sP = sQD + LB_NS * 2 * TILE_BYTES;
-  uint8_t* sdS = sP + P_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sdS + P_BYTES);
+  uint8_t* sdS = sP + P_BYTES;                   // 2 x dS: block g uses buffer g & 1
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sdS + 2 * P_BYTES);
   uint64_t* kv_full = bars;                      // [2]
   uint64_t* kv_empty = bars + 2;                 // [2]
   uint64_t* qd_full = bars + 4;                  // [LB_NS]
@@ -1895,6 +1895,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
   uint64_t* acc_full = bars + 6 + 2 * LB_NS;
   uint64_t* out_free = bars + 7 + 2 * LB_NS;     // 8 warps: dK/dV of the unit read out
   uint64_t* sp_free = bars + 8 + 2 * LB_NS;      // 8 warps: S / dP of the block are in registers
+  uint64_t* p_free = bars + 9 + 2 * LB_NS;       // dV MMAs of the block done: P may be overwritten
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1916,6 +1917,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
     sm100::mbar_init(acc_full, 1);
     sm100::mbar_init(out_free, 8);
     sm100::mbar_init(sp_free, 8);
+    sm100::mbar_init(p_free, 1);
     sm100::fence_barrier_init();
   }
   if (warp == 0) sm100::tmem_alloc(tslot, 512);
@@ -2009,15 +2011,18 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
         const int sg = g % LB_NS;
         const uint32_t q = sQDa + sg * 2 * TILE_BYTES, o = q + TILE_BYTES;
         const uint32_t k = sKVa + (uc & 1) * 2 * TILE_BYTES;
+        const uint32_t ds = sdSa + (g & 1) * P_BYTES, dq = tdQ + (g & 1) * 64;
+#pragma unroll
+        for (int kk = 0; kk < TILE / 16; ++kk)
+          sm100::mma_bf16_ss_w(tdV, sm100::desc_mnmajor_sw128(sPa + kk * 2048, TILE * 128),
+                               sm100::desc_mnmajor_sw128(o + kk * 2048, 8192), id_t, (i > 0 || kk > 0) ? 1u : 0u);
+        sm100::mma_commit_w(p_free);  // P of block g + 1 may be written while dK / dQ of block g run
 #pragma unroll
         for (int kk = 0; kk < TILE / 16; ++kk) {
-          const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
-          sm100::mma_bf16_ss_w(tdV, sm100::desc_mnmajor_sw128(sPa + kk * 2048, TILE * 128),
-                             sm100::desc_mnmajor_sw128(o + kk * 2048, 8192), id_t, acc);
-          sm100::mma_bf16_ss_w(tdK, sm100::desc_mnmajor_sw128(sdSa + kk * 2048, TILE * 128),
-                             sm100::desc_mnmajor_sw128(q + kk * 2048, 8192), id_t, acc);
-          sm100::mma_bf16_ss_w(tdQ, sm100::desc_kmajor_sw128(sdSa + (kk >> 2) * (TILE * 128) + (kk & 3) * 32),
-                             sm100::desc_mnmajor_sw128(k + kk * 2048, 8192), id_q, kk > 0);
+          sm100::mma_bf16_ss_w(tdK, sm100::desc_mnmajor_sw128(ds + kk * 2048, TILE * 128),
+                               sm100::desc_mnmajor_sw128(q + kk * 2048, 8192), id_t, (i > 0 || kk > 0) ? 1u : 0u);
+          sm100::mma_bf16_ss_w(dq, sm100::desc_kmajor_sw128(ds + (kk >> 2) * (TILE * 128) + (kk & 3) * 32),
+                               sm100::desc_mnmajor_sw128(k + kk * 2048, 8192), id_q, kk > 0);
         }
         sm100::mma_commit_w(acc_full);
         sm100::mma_commit_w(&qd_empty[sg]);
@@ -2041,21 +2046,22 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
     // fold the finished dQ block into dq_acc: a warp whose 32 query rows are all inside the sequence
     // stages its [32 x 32] fp32 block in its dS slab (128B swizzle) and one lane hands it to the TMA
     // engine as a bulk reduce-add; a ragged quarter adds its valid rows with vector reductions
-    auto dq_out = [&](int start, int q0, int len, int h, int kt) {
+    auto dq_out = [&](int start, int q0, int len, int h, int kt, int gg) {
+      const uint32_t slab = slabS + (gg & 1) * P_BYTES;
       float v[32];
-      sm100::tmem_ld32(tdQ + lane_off + 32 * ch, v);
+      sm100::tmem_ld32(tdQ + (gg & 1) * 64 + lane_off + 32 * ch, v);
       sm100::tmem_ld_wait();
       if (!col_ok) return;
       if (q0 + q4 * 32 + 32 <= len) {
 #pragma unroll
         for (int c = 0; c < 8; ++c)
-          st_shared_v4(slabS + lane * 128 + ((c ^ (lane & 7)) << 4), __float_as_uint(v[4 * c]),
+          st_shared_v4(slab + lane * 128 + ((c ^ (lane & 7)) << 4), __float_as_uint(v[4 * c]),
                        __float_as_uint(v[4 * c + 1]), __float_as_uint(v[4 * c + 2]), __float_as_uint(v[4 * c + 3]));
         sm100::fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          if (det) sm100::tma_store_2d(&tm_dq, slabS, h * d + 32 * ch, kt * nnz + start + q0 + q4 * 32);
-          else sm100::tma_reduce_add_2d(&tm_dq, slabS, h * d + 32 * ch, start + q0 + q4 * 32);
+          if (det) sm100::tma_store_2d(&tm_dq, slab, h * d + 32 * ch, kt * nnz + start + q0 + q4 * 32);
+          else sm100::tma_reduce_add_2d(&tm_dq, slab, h * d + 32 * ch, start + q0 + q4 * 32);
           sm100::bulk_commit();
         }
       } else if (q0 + r < len) {
@@ -2110,26 +2116,30 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
         sm100::tc_fence_before();
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive(sp_free);  // S / dP of the next block may overwrite TMEM
-        if (i > 0) {  // block g-1's MMAs finished (P/dS free); its dQ is ready
-          sm100::mbar_wait(acc_full, (g - 1) & 1);
-          sm100::tc_fence_after();
-          dq_out(start, q0 - TILE, len, h, jt);
-        }
+        // P is single-buffered: block g-1's dV MMAs must have read it; dS buffer g & 1 was last read by
+        // block g-2's MMAs, whose completion dq_out(g-2) waited for
+        if (g > 0) sm100::mbar_wait(p_free, (g - 1) & 1);
+        const uint32_t sdSg = sdSa + (g & 1) * P_BYTES;
         if (len - q0 >= TILE && len - kv0 >= TILE)
-          bwd_block_regs<false>(sv, dpv, sPa, sdSa, r, ch, lane, q0 - kv0, len - q0, len - kv0, sc2, sl2, lse2, rsd,
+          bwd_block_regs<false>(sv, dpv, sPa, sdSg, r, ch, lane, q0 - kv0, len - q0, len - kv0, sc2, sl2, lse2, rsd,
                                 Drs);
         else
-          bwd_block_regs<true>(sv, dpv, sPa, sdSa, r, ch, lane, q0 - kv0, len - q0, len - kv0, sc2, sl2, lse2, rsd,
+          bwd_block_regs<true>(sv, dpv, sPa, sdSg, r, ch, lane, q0 - kv0, len - q0, len - kv0, sc2, sl2, lse2, rsd,
                                Drs);
         sm100::fence_proxy_async_smem();
         sm100::tc_fence_before();
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive(elem_done);
+        if (i > 0) {  // block g-1's MMAs finished (issued a whole block ago); its dQ is ready
+          sm100::mbar_wait(acc_full, (g - 1) & 1);
+          sm100::tc_fence_after();
+          dq_out(start, q0 - TILE, len, h, jt, g - 1);
+        }
       }
       // unit end: last dQ block, then dV / dK of the key tile (rows = keys kv0 + r)
       sm100::mbar_wait(acc_full, (g - 1) & 1);
       sm100::tc_fence_after();
-      dq_out(start, (nq - 1) * TILE, len, h, jt);
+      dq_out(start, (nq - 1) * TILE, len, h, jt, g - 1);
       const bool ok = kv0 + r < len;
       const bool full = kv0 + q4 * 32 + 32 <= len;  // warp-uniform
 #pragma unroll 1
@@ -2143,7 +2153,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
         }
         if (col_ok) {
           if (full) {
-            const uint32_t stg = which == 2 ? slabP : slabS;
+            const uint32_t stg = which == 2 ? slabP : slabS + ((g - 1) & 1) * P_BYTES;
             if (which == 1) {  // the last dQ reduction may still be reading the dS slab
               if (lane == 0) sm100::bulk_wait_read0();
               __syncwarp();
