@@ -1672,7 +1672,7 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
 // dK [320,384), dQ [384,448).
 // ------------------------------------------------------------------------------------------
 constexpr int LB_NS = 2;
-constexpr int LB_THREADS = SH_THREADS + 128;  // compute warps 0-7; warpgroup 2: MMA warp 8, TMA warp 9
+constexpr int LB_THREADS = SH_THREADS + 256;  // compute warps 0-7; epilogue warps 8-11; MMA warp 12, TMA warp 13
 constexpr int LB_SMEM = 2 * 2 * TILE_BYTES + LB_NS * 2 * TILE_BYTES + 3 * P_BYTES + 1024 + 256;  // P + 2 x dS
 
 // D[h, t] = sum_c dO[t, h d + c] O[t, h d + c]  (the rowsum(dO o O) of FlashAttention's backward).
@@ -1884,19 +1884,22 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
   uint8_t* sKV = smem;                           // 2 x (K, V)
   uint8_t* sQD = sKV + 2 * 2 * TILE_BYTES;       // LB_NS x (Q, dO)
   uint8_t* sP = sQD + LB_NS * 2 * TILE_BYTES;
-  uint8_t* sdS = sP + P_BYTES;                   // 2 x dS: block g uses buffer g & 1
+  uint8_t* sdS = sP + P_BYTES;                   // 2 x dS: block g uses buffer g & 1, then stages its outputs
   uint64_t* bars = reinterpret_cast<uint64_t*>(sdS + 2 * P_BYTES);
   uint64_t* kv_full = bars;                      // [2]
   uint64_t* kv_empty = bars + 2;                 // [2]
   uint64_t* qd_full = bars + 4;                  // [LB_NS]
   uint64_t* qd_empty = bars + 4 + LB_NS;         // [LB_NS]
   uint64_t* sp_full = bars + 4 + 2 * LB_NS;
-  uint64_t* elem_done = bars + 5 + 2 * LB_NS;    // 8 warps
-  uint64_t* acc_full = bars + 6 + 2 * LB_NS;
-  uint64_t* out_free = bars + 7 + 2 * LB_NS;     // 8 warps: dK/dV of the unit read out
-  uint64_t* sp_free = bars + 8 + 2 * LB_NS;      // 8 warps: S / dP of the block are in registers
-  uint64_t* p_free = bars + 9 + 2 * LB_NS;       // dV MMAs of the block done: P may be overwritten
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint64_t* elem_done = sp_full + 1;             // 8 compute warps: P_g, dS_g in smem
+  uint64_t* out_free = sp_full + 2;              // 4 epilogue warps: the unit's dV / dK are out of TMEM
+  uint64_t* sp_free = sp_full + 3;               // 8 compute warps: S / dP of the block are in registers
+  uint64_t* p_free = sp_full + 4;                // dV MMAs of the block done: P may be overwritten
+  // per buffer b = g & 1 (a single acc_full could run two phases ahead of the decoupled epilogue):
+  uint64_t* acc_full = sp_full + 5;              // [2] block g's MMAs complete (dQ_g; dV / dK at a unit end)
+  uint64_t* ds_free = sp_full + 7;               // [2] 4 epilogue warps: dS buffer b free (its staging read)
+  uint64_t* dq_free = sp_full + 9;               // [2] 4 epilogue warps: dQ TMEM buffer b read out
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sp_full + 11);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int H = U.heads * d;
@@ -1907,6 +1910,9 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&kv_full[i], 1);
       sm100::mbar_init(&kv_empty[i], 1);
+      sm100::mbar_init(&ds_free[i], 4);
+      sm100::mbar_init(&dq_free[i], 4);
+      sm100::mbar_init(&acc_full[i], 1);
     }
     for (int i = 0; i < LB_NS; ++i) {
       sm100::mbar_init(&qd_full[i], 1);
@@ -1914,8 +1920,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
     }
     sm100::mbar_init(sp_full, 1);
     sm100::mbar_init(elem_done, 8);
-    sm100::mbar_init(acc_full, 1);
-    sm100::mbar_init(out_free, 8);
+    sm100::mbar_init(out_free, 4);
     sm100::mbar_init(sp_free, 8);
     sm100::mbar_init(p_free, 1);
     sm100::fence_barrier_init();
@@ -1927,6 +1932,8 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
   const uint32_t tbase = *tslot;
   pdl_wait();  // (PDL) the setup above touched only shared memory, TMEM and kernel parameters
   pdl_trigger();
+  // dQ is double-buffered in TMEM (block g accumulates into tdQ + 64 (g & 1)) so the epilogue
+  // warpgroup reads it out while the next block's MMAs run
   const uint32_t tS = tbase, tdP = tbase + 128, tdV = tbase + 256, tdK = tbase + 320, tdQ = tbase + 384;
   const uint32_t sKVa = sm100::smem_u32(sKV), sQDa = sm100::smem_u32(sQD), sPa = sm100::smem_u32(sP),
                  sdSa = sm100::smem_u32(sdS);
@@ -1936,38 +1943,37 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
     return (U.cu[b + 1] - U.cu[b] + TILE - 1) / TILE;
   };
 
-  // registers: 12 warps leave 168 per thread; warpgroup 2 (producer, MMA issuer, two idle warps) hands
-  // most of its share to the compute warps, which hold a block's S and dP rows in registers
-  if (warp >= 8) {
-    sm100::setmaxnreg_dec<64>();
-    if (warp == 9) {
-    // ------------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      int uc = 0, g = 0;
-      for (int u = U.first(); u < U.total; u = U.next(u), ++uc) {
-        int b, h, jt;
-        U.decode(u, b, h, jt);
-        const int st = U.cu[b], nq = (U.cu[b + 1] - st + TILE - 1) / TILE;
-        const int kb = uc & 1;
-        sm100::mbar_wait(&kv_empty[kb], ((uc >> 1) & 1) ^ 1);
-        uint8_t* kv = sKV + kb * 2 * TILE_BYTES;
-        sm100::mbar_arrive_expect_tx(&kv_full[kb], 2 * TILE_BYTES);
-        sm100::tma_load_2d(kv, &tm_qkv, &kv_full[kb], H + h * d, st + jt * TILE);
-        sm100::tma_load_2d(kv + TILE_BYTES, &tm_qkv, &kv_full[kb], 2 * H + h * d, st + jt * TILE);
-        for (int i = 0; i < nq; ++i, ++g) {
-          const int sg = g % LB_NS;
-          sm100::mbar_wait(&qd_empty[sg], ((g / LB_NS) & 1) ^ 1);
-          uint8_t* qd = sQD + sg * 2 * TILE_BYTES;
-          sm100::mbar_arrive_expect_tx(&qd_full[sg], 2 * TILE_BYTES);
-          sm100::tma_load_2d(qd, &tm_qkv, &qd_full[sg], h * d, st + i * TILE);
-          sm100::tma_load_2d(qd + TILE_BYTES, &tm_do, &qd_full[sg], h * d, st + i * TILE);
+  // registers: 16 warps leave 128 per thread; the compute warpgroups (S and dP rows in registers)
+  // take 192, the epilogue warpgroup 88 and the producer / issuer warpgroup 40
+  if (warp >= 12) {
+    sm100::setmaxnreg_dec<40>();
+    if (warp == 13) {
+      // ---------------------------------------------------------------- TMA producer
+      if (lane == 0) {
+        int uc = 0, g = 0;
+        for (int u = U.first(); u < U.total; u = U.next(u), ++uc) {
+          int b, h, jt;
+          U.decode(u, b, h, jt);
+          const int st = U.cu[b], nq = (U.cu[b + 1] - st + TILE - 1) / TILE;
+          const int kb = uc & 1;
+          sm100::mbar_wait(&kv_empty[kb], ((uc >> 1) & 1) ^ 1);
+          uint8_t* kv = sKV + kb * 2 * TILE_BYTES;
+          sm100::mbar_arrive_expect_tx(&kv_full[kb], 2 * TILE_BYTES);
+          sm100::tma_load_2d(kv, &tm_qkv, &kv_full[kb], H + h * d, st + jt * TILE);
+          sm100::tma_load_2d(kv + TILE_BYTES, &tm_qkv, &kv_full[kb], 2 * H + h * d, st + jt * TILE);
+          for (int i = 0; i < nq; ++i, ++g) {
+            const int sg = g % LB_NS;
+            sm100::mbar_wait(&qd_empty[sg], ((g / LB_NS) & 1) ^ 1);
+            uint8_t* qd = sQD + sg * 2 * TILE_BYTES;
+            sm100::mbar_arrive_expect_tx(&qd_full[sg], 2 * TILE_BYTES);
+            sm100::tma_load_2d(qd, &tm_qkv, &qd_full[sg], h * d, st + i * TILE);
+            sm100::tma_load_2d(qd + TILE_BYTES, &tm_do, &qd_full[sg], h * d, st + i * TILE);
+          }
         }
       }
-    }
-    __syncwarp();
-  } else if (warp == 8) {
-    // ------------------------------------------------------------------ MMA issuer
-    {  // the whole warp runs the issue loop; one elected lane issues
+      __syncwarp();
+    } else if (warp == 12) {
+      // ---------------------------------------------------------------- MMA issuer (whole warp, elected lane)
       constexpr uint32_t id_s = sm100::idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t id_t = sm100::idesc_bf16(128, 64, 1, 1);  // P^T dO, dS^T Q
       constexpr uint32_t id_q = sm100::idesc_bf16(128, 64, 0, 1);  // dS K
@@ -1980,9 +1986,9 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
         const uint32_t k = sKVa + (ucc & 1) * 2 * TILE_BYTES, v = k + TILE_BYTES;
         for (int kk = 0; kk < d / 16; ++kk) {
           sm100::mma_bf16_ss_w(tS, sm100::desc_kmajor_sw128(q + kk * 32), sm100::desc_kmajor_sw128(k + kk * 32), id_s,
-                             kk > 0);
+                               kk > 0);
           sm100::mma_bf16_ss_w(tdP, sm100::desc_kmajor_sw128(o + kk * 32), sm100::desc_kmajor_sw128(v + kk * 32), id_s,
-                             kk > 0);
+                               kk > 0);
         }
         sm100::mma_commit_w(sp_full);
       };
@@ -1991,8 +1997,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
         mma1(0, 0);
       }
       for (int g = 0; u < U.total; ++g) {
-        // cursor of block g + 1; its S / dP go into TMEM as soon as block g's are in registers, so
-        // they overlap block g's elementwise work and its dV / dK / dQ MMAs
+        // cursor of block g + 1; its S / dP go into TMEM as soon as block g's are in registers
         int u2 = u, uc2 = uc, i2 = i + 1, nq2 = nq;
         if (i2 == nq) {
           u2 = U.next(u);
@@ -2005,8 +2010,8 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
           if (i2 == 0) sm100::mbar_wait(&kv_full[uc2 & 1], (uc2 >> 1) & 1);
           mma1(g + 1, uc2);
         }
-        sm100::mbar_wait(elem_done, g & 1);  // P_g, dS_g in smem
-        if (i == 0 && uc > 0) sm100::mbar_wait(out_free, (uc - 1) & 1);  // previous unit's dK/dV read out
+        sm100::mbar_wait(elem_done, g & 1);                               // P_g, dS_g in smem
+        if (i == 0 && uc > 0) sm100::mbar_wait(out_free, (uc - 1) & 1);  // previous unit's dV / dK read out
         sm100::tc_fence_after();
         const int sg = g % LB_NS;
         const uint32_t q = sQDa + sg * 2 * TILE_BYTES, o = q + TILE_BYTES;
@@ -2017,6 +2022,10 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
           sm100::mma_bf16_ss_w(tdV, sm100::desc_mnmajor_sw128(sPa + kk * 2048, TILE * 128),
                                sm100::desc_mnmajor_sw128(o + kk * 2048, 8192), id_t, (i > 0 || kk > 0) ? 1u : 0u);
         sm100::mma_commit_w(p_free);  // P of block g + 1 may be written while dK / dQ of block g run
+        if (g >= 2) {                 // the epilogue has read dQ of block g - 2 out of this TMEM buffer
+          sm100::mbar_wait(&dq_free[g & 1], ((g >> 1) - 1) & 1);
+          sm100::tc_fence_after();
+        }
 #pragma unroll
         for (int kk = 0; kk < TILE / 16; ++kk) {
           sm100::mma_bf16_ss_w(tdK, sm100::desc_mnmajor_sw128(ds + kk * 2048, TILE * 128),
@@ -2024,57 +2033,133 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
           sm100::mma_bf16_ss_w(dq, sm100::desc_kmajor_sw128(ds + (kk >> 2) * (TILE * 128) + (kk & 3) * 32),
                                sm100::desc_mnmajor_sw128(k + kk * 2048, 8192), id_q, kk > 0);
         }
-        sm100::mma_commit_w(acc_full);
+        sm100::mma_commit_w(&acc_full[g & 1]);
         sm100::mma_commit_w(&qd_empty[sg]);
         if (i2 == 0) sm100::mma_commit_w(&kv_empty[uc & 1]);  // the unit's last read of K_j, V_j
         u = u2, uc = uc2, i = i2, nq = nq2;
       }
     }
     __syncwarp();
+  } else if (warp >= 8) {
+    // ------------------------------------------------------------------ epilogue warps 8-11
+    // Per block: dQ_g out of TMEM, staged as fp32 in this warp's quarter of dS buffer g & 1 (free once
+    // block g's MMAs are), handed to the TMA engine as a bulk reduce-add (det: a store into slab kt).
+    // Per unit end: dV, dK out of TMEM (then out_free), staged as bf16 in the same quarter, TMA stores.
+    // The quarter is released (ds_free) once the bulk copies have read it.
+    sm100::setmaxnreg_dec<88>();
+    const int q4 = warp & 3, r = q4 * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    int g = 0;
+    for (int u = U.first(); u < U.total; u = U.next(u)) {
+      int b, h, jt;
+      U.decode(u, b, h, jt);
+      const int start = U.cu[b], len = U.cu[b + 1] - start, kv0 = jt * TILE;
+      const int nq = (len + TILE - 1) / TILE;
+      for (int i = 0; i < nq; ++i, ++g) {
+        const int q0 = i * TILE;
+        const uint32_t stg = sdSa + (g & 1) * P_BYTES + q4 * 8192;  // 8 KB: two [32 x 32] fp32 blocks
+        sm100::mbar_wait(&acc_full[g & 1], (g >> 1) & 1);
+        sm100::tc_fence_after();
+        const bool full_rows = q0 + q4 * 32 + 32 <= len;  // warp-uniform
+#pragma unroll 1
+        for (int hh = 0; hh < 2; ++hh) {
+          float v[32];
+          sm100::tmem_ld32(tdQ + (g & 1) * 64 + lane_off + 32 * hh, v);
+          sm100::tmem_ld_wait();
+          if (hh == 1) {
+            sm100::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive(&dq_free[g & 1]);
+          }
+          if (32 * hh >= d) continue;
+          if (full_rows) {
+            const uint32_t blk = stg + hh * 4096;
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              st_shared_v4(blk + lane * 128 + ((c ^ (lane & 7)) << 4), __float_as_uint(v[4 * c]),
+                           __float_as_uint(v[4 * c + 1]), __float_as_uint(v[4 * c + 2]), __float_as_uint(v[4 * c + 3]));
+            sm100::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              if (det) sm100::tma_store_2d(&tm_dq, blk, h * d + 32 * hh, jt * nnz + start + q0 + q4 * 32);
+              else sm100::tma_reduce_add_2d(&tm_dq, blk, h * d + 32 * hh, start + q0 + q4 * 32);
+              sm100::bulk_commit();
+            }
+          } else if (q0 + r < len) {
+            float* dst = dq_acc + ((size_t)(det ? jt * nnz : 0) + start + q0 + r) * H + h * d + 32 * hh;
+            if (det) {
+#pragma unroll
+              for (int e = 0; e < 32; e += 4) *reinterpret_cast<float4*>(dst + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+            } else {
+#pragma unroll
+              for (int e = 0; e < 32; e += 4) red_add_v4(dst + e, v[e], v[e + 1], v[e + 2], v[e + 3]);
+            }
+          }
+        }
+        if (i + 1 == nq) {
+          // unit end: dV / dK of the key tile (rows = keys kv0 + r), final with block g's MMAs
+          const bool ok = kv0 + r < len;
+          const bool full = kv0 + q4 * 32 + 32 <= len;  // warp-uniform
+          if (lane == 0) sm100::bulk_wait_read0();      // the dQ blocks have left the staging quarter
+          __syncwarp();
+#pragma unroll 1
+          for (int w4 = 0; w4 < 4; ++w4) {  // (V, K) x (columns 0-31, 32-63)
+            const int which = w4 < 2 ? 2 : 1, hh = w4 & 1;
+            float v[32];
+            sm100::tmem_ld32((which == 2 ? tdV : tdK) + lane_off + 32 * hh, v);
+            sm100::tmem_ld_wait();
+            if (w4 == 3) {
+              sm100::tc_fence_before();
+              __syncwarp();
+              if (lane == 0) sm100::mbar_arrive(out_free);
+            }
+            if (!full) {
+#pragma unroll
+              for (int e = 0; e < 32; ++e) v[e] = ok ? v[e] : 0.f;
+            }
+            const bool col_ok = 32 * hh < d;
+            if (col_ok) {
+              if (full) {
+                const uint32_t blk = stg + w4 * 2048;  // [32 x 32] bf16, 64B swizzle
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                  const uint4 pk = f32_to_bf16x8(v + 8 * c);
+                  st_shared_v4(blk + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4), pk.x, pk.y, pk.z, pk.w);
+                }
+                sm100::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                  sm100::tma_store_2d(&tm_dqkv, blk, which * H + h * d + 32 * hh, start + kv0 + q4 * 32);
+                  sm100::bulk_commit();
+                }
+              } else if (ok) {
+                bf16* dst = dqkv + (size_t)(start + kv0 + r) * 3 * H + which * H + h * d + 32 * hh;
+#pragma unroll
+                for (int c = 0; c < 32; c += 8) *reinterpret_cast<uint4*>(dst + c) = f32_to_bf16x8(v + c);
+              }
+            }
+            if (dbias && which == 2) {  // db_v = column sums of dV (db_k = 0, R31; db_q in dq_finish_kernel)
+              const float cs = warp_colsum32(v, lane);
+              if (col_ok && 32 * hh + lane < d) atomicAdd(dbias + 2 * H + h * d + 32 * hh + lane, cs);
+            }
+          }
+        }
+        // the staging quarter of dS buffer g & 1 is free once the bulk copies have read it
+        if (lane == 0) sm100::bulk_wait_read0();
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(&ds_free[g & 1]);
+      }
     }
+    if (lane == 0) sm100::bulk_wait0();
   } else {
     // ------------------------------------------------------------------ compute warps 0-7
-    sm100::setmaxnreg_inc<216>();  // 2 x 128 x 216 + 128 x 64 <= 384 x 168
+    sm100::setmaxnreg_inc<192>();  // 8 x 32 x 192 + 4 x 32 x 88 + 4 x 32 x 40 <= 16 x 32 x 128
     const int ch = warp >> 2, q4 = warp & 3;
     const int r = q4 * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     const float rsd = rsqrtf((float)d);
     const float sc2 = rsd * LOG2E;
-    const bool col_ok = 32 * ch < d;
-    const uint32_t slabP = sPa + ch * (TILE * 128) + q4 * 4096, slabS = sdSa + ch * (TILE * 128) + q4 * 4096;
     int g = 0;
-    // fold the finished dQ block into dq_acc: a warp whose 32 query rows are all inside the sequence
-    // stages its [32 x 32] fp32 block in its dS slab (128B swizzle) and one lane hands it to the TMA
-    // engine as a bulk reduce-add; a ragged quarter adds its valid rows with vector reductions
-    auto dq_out = [&](int start, int q0, int len, int h, int kt, int gg) {
-      const uint32_t slab = slabS + (gg & 1) * P_BYTES;
-      float v[32];
-      sm100::tmem_ld32(tdQ + (gg & 1) * 64 + lane_off + 32 * ch, v);
-      sm100::tmem_ld_wait();
-      if (!col_ok) return;
-      if (q0 + q4 * 32 + 32 <= len) {
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          st_shared_v4(slab + lane * 128 + ((c ^ (lane & 7)) << 4), __float_as_uint(v[4 * c]),
-                       __float_as_uint(v[4 * c + 1]), __float_as_uint(v[4 * c + 2]), __float_as_uint(v[4 * c + 3]));
-        sm100::fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          if (det) sm100::tma_store_2d(&tm_dq, slab, h * d + 32 * ch, kt * nnz + start + q0 + q4 * 32);
-          else sm100::tma_reduce_add_2d(&tm_dq, slab, h * d + 32 * ch, start + q0 + q4 * 32);
-          sm100::bulk_commit();
-        }
-      } else if (q0 + r < len) {
-        float* dst = dq_acc + ((size_t)(det ? kt * nnz : 0) + start + q0 + r) * H + h * d + 32 * ch;
-        if (det) {
-#pragma unroll
-          for (int e = 0; e < 32; e += 4) *reinterpret_cast<float4*>(dst + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
-        } else {
-#pragma unroll
-          for (int e = 0; e < 32; e += 4) red_add_v4(dst + e, v[e], v[e + 1], v[e + 2], v[e + 3]);
-        }
-      }
-    };
     // LSE and D of row r of query tile ii of unit uu, loaded one block ahead of their use
     auto row_stats = [&](int uu, int ii, float& l_, float& d_) {
       l_ = 0.f, d_ = 0.f;
@@ -2096,9 +2181,6 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
       const int nq = (len + TILE - 1) / TILE;
       const float sl2 = slopes[h] * LOG2E;
       const int un = U.next(u);
-      // this warp's P / dS slabs double as dK/dV staging: the previous unit's stores must have read them
-      if (lane == 0) sm100::bulk_wait_read0();
-      __syncwarp();
       for (int i = 0; i < nq; ++i, ++g) {
         const int q0 = i * TILE;
         const float lse2 = lse_c * LOG2E;
@@ -2116,9 +2198,10 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
         sm100::tc_fence_before();
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive(sp_free);  // S / dP of the next block may overwrite TMEM
-        // P is single-buffered: block g-1's dV MMAs must have read it; dS buffer g & 1 was last read by
-        // block g-2's MMAs, whose completion dq_out(g-2) waited for
+        // P is single-buffered: block g-1's dV MMAs must have read it; dS buffer g & 1 was last used by
+        // block g-2, whose MMAs and output staging the epilogue has finished with
         if (g > 0) sm100::mbar_wait(p_free, (g - 1) & 1);
+        if (g >= 2) sm100::mbar_wait(&ds_free[g & 1], ((g >> 1) - 1) & 1);
         const uint32_t sdSg = sdSa + (g & 1) * P_BYTES;
         if (len - q0 >= TILE && len - kv0 >= TILE)
           bwd_block_regs<false>(sv, dpv, sPa, sdSg, r, ch, lane, q0 - kv0, len - q0, len - kv0, sc2, sl2, lse2, rsd,
@@ -2130,61 +2213,8 @@ __global__ void __launch_bounds__(LB_THREADS, 1) attn_bwd_long_kernel(
         sm100::tc_fence_before();
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive(elem_done);
-        if (i > 0) {  // block g-1's MMAs finished (issued a whole block ago); its dQ is ready
-          sm100::mbar_wait(acc_full, (g - 1) & 1);
-          sm100::tc_fence_after();
-          dq_out(start, q0 - TILE, len, h, jt, g - 1);
-        }
       }
-      // unit end: last dQ block, then dV / dK of the key tile (rows = keys kv0 + r)
-      sm100::mbar_wait(acc_full, (g - 1) & 1);
-      sm100::tc_fence_after();
-      dq_out(start, (nq - 1) * TILE, len, h, jt, g - 1);
-      const bool ok = kv0 + r < len;
-      const bool full = kv0 + q4 * 32 + 32 <= len;  // warp-uniform
-#pragma unroll 1
-      for (int which = 2; which >= 1; --which) {  // V then K
-        float v[32];
-        sm100::tmem_ld32((which == 2 ? tdV : tdK) + lane_off + 32 * ch, v);
-        sm100::tmem_ld_wait();
-        if (!full) {
-#pragma unroll
-          for (int e = 0; e < 32; ++e) v[e] = ok ? v[e] : 0.f;
-        }
-        if (col_ok) {
-          if (full) {
-            const uint32_t stg = which == 2 ? slabP : slabS + ((g - 1) & 1) * P_BYTES;
-            if (which == 1) {  // the last dQ reduction may still be reading the dS slab
-              if (lane == 0) sm100::bulk_wait_read0();
-              __syncwarp();
-            }
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              const uint4 pk = f32_to_bf16x8(v + 8 * c);
-              st_shared_v4(stg + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4), pk.x, pk.y, pk.z, pk.w);
-            }
-            sm100::fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              sm100::tma_store_2d(&tm_dqkv, stg, which * H + h * d + 32 * ch, start + kv0 + q4 * 32);
-              sm100::bulk_commit();
-            }
-          } else if (ok) {
-            bf16* dst = dqkv + (size_t)(start + kv0 + r) * 3 * H + which * H + h * d + 32 * ch;
-#pragma unroll
-            for (int c = 0; c < 32; c += 8) *reinterpret_cast<uint4*>(dst + c) = f32_to_bf16x8(v + c);
-          }
-        }
-        if (dbias && which == 2) {  // db_v = column sums of dV (db_k = 0, R31; db_q in dq_finish_kernel)
-          const float cs = warp_colsum32(v, lane);
-          if (col_ok && 32 * ch + lane < d) atomicAdd(dbias + 2 * H + h * d + 32 * ch + lane, cs);
-        }
-      }
-      sm100::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) sm100::mbar_arrive(out_free);
     }
-    if (lane == 0) sm100::bulk_wait0();
   }
   sm100::tc_fence_before();
   __syncthreads();
