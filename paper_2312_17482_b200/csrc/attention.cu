@@ -1665,11 +1665,12 @@ __global__ void __launch_bounds__(SH_BWD_THREADS, 1) attn_bwd_short_kernel(
 //   P = 2^(S log2e/sqrt(d) - m log2e |q - k| - LSE log2e),  dS/sqrt(d) = P (dP - D)/sqrt(d)
 //   dV_j += P^T dO_i, dK_j += dS^T Q_i  (TMEM accumulators across the unit's query tiles)
 //   dQ_i += dS K_j                        (per block, folded into an fp32 [nnz, H] buffer by
-//                                          vector reductions; dq_finish_kernel converts it)
-// Warp 9 streams K/V (double-buffered per unit) and Q/dO tiles (LB_NS-stage ring) by TMA; warp 8
-// issues S, dP of block i+1 as soon as the softmax warps have consumed block i, and dV/dK/dQ of
-// block i once P_i, dS_i are in smem.  TMEM: S [0,128), dP [128,256), dV [256,320),
-// dK [320,384), dQ [384,448).
+//                                          TMA bulk reduce-adds; dq_finish_kernel converts it)
+// Warp 13 streams K/V (double-buffered per unit) and Q/dO tiles (LB_NS-stage ring) by TMA; warp 12
+// issues S, dP of block i+1 as soon as the compute warps 0-7 hold block i's in registers, and
+// dV/dK/dQ of block i once P_i, dS_i are in smem; the epilogue warps 8-11 read dQ_i (and, at a
+// unit end, dV / dK) out of TMEM and hand them to TMA.  TMEM: S [0,128), dP [128,256),
+// dV [256,320), dK [320,384), dQ [384,512) (two buffers).
 // ------------------------------------------------------------------------------------------
 constexpr int LB_NS = 2;
 constexpr int LB_THREADS = SH_THREADS + 256;  // compute warps 0-7; epilogue warps 8-11; MMA warp 12, TMA warp 13
