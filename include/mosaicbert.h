@@ -295,7 +295,9 @@ MB_API mb_status mb_embed_backward(const mb_dims* d, const int32_t* ids, const i
  *   loss_sum += inv_norm * sum_k (logsumexp(z_k) - z_k[label_k])
  * Forward and backward in one call: dy_top (bf16 [nnz, H]) is fully written (zero on unmasked rows);
  * grads accumulate (+=).  loss_sum: device fp32 scalar (+=).  lse: device fp32[n_masked] out.
- * ws: mb_mlm_workspace_bytes(d, n_masked). */
+ * ws: mb_mlm_workspace_bytes(d, n_masked).  dy_top == NULL and g == NULL: forward only (evaluation,
+ * e.g. SURVEY F4's "train short, test long" at l up to 2048): loss_sum and lse, no gradients; only
+ * one of the two NULL -> MB_ERR_INVALID_ARG. */
 typedef struct {
   const mb_bf16 *w_t, *b_t, *ln_g, *ln_b, *emb /*[V,H], tied*/, *b_dec;
 } mb_head_params;

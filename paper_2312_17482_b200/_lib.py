@@ -400,10 +400,11 @@ def mlm_workspace_bytes(d: Dims, n_masked: int) -> int:
 
 
 def mlm_loss(d: Dims, head, y, nnz, masked_rows, labels, n_masked, inv_norm, loss_sum, lse, dy_top, grads, ws):
+    """dy_top = grads = None: forward only (loss_sum += and lse, no gradients)."""
     hp = head if isinstance(head, HeadPtrs) else head_ptrs(head)
-    hg = grads if isinstance(grads, HeadPtrs) else head_ptrs(grads)
+    hg = None if grads is None else C.byref(grads if isinstance(grads, HeadPtrs) else head_ptrs(grads))
     _ck("mb_mlm_loss", lib().mb_mlm_loss(C.byref(d), C.byref(hp), _p(y), nnz, _p(masked_rows), _p(labels), n_masked,
-                                         inv_norm, _p(loss_sum), _p(lse), _p(dy_top), C.byref(hg), _p(ws), ws.numel(),
+                                         inv_norm, _p(loss_sum), _p(lse), _p(dy_top), hg, _p(ws), ws.numel(),
                                          _stream()))
 
 

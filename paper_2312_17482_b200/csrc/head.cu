@@ -179,7 +179,9 @@ mb_status mb_mlm_loss(const mb_dims* d, const mb_head_params* p, const mb_bf16* 
                       float* loss_sum, float* lse, mb_bf16* dy_top, const mb_head_grads* g, void* ws, size_t ws_bytes,
                       mb_stream_t s_) {
   using namespace mb;
-  if (!d || !p || !y || !masked_rows || !labels || !loss_sum || !lse || !dy_top || !g || !ws) return MB_ERR_INVALID_ARG;
+  if (!d || !p || !y || !masked_rows || !labels || !loss_sum || !lse || !ws) return MB_ERR_INVALID_ARG;
+  const bool eval_only = !dy_top && !g;  // forward only: loss_sum and lse, no gradients (F4 evaluation)
+  if (!eval_only && (!dy_top || !g)) return MB_ERR_INVALID_ARG;
   if (n_masked < 0 || nnz < 0) return MB_ERR_INVALID_ARG;
   if (n_masked > nnz) return MB_ERR_SHAPE;
   MB_REQUIRE_ARCH();
@@ -192,7 +194,7 @@ mb_status mb_mlm_loss(const mb_dims* d, const mb_head_params* p, const mb_bf16* 
   const Det* det = w.det ? &w.det : nullptr;
   bf16* dyt = reinterpret_cast<bf16*>(dy_top);
   if (n_masked == 0) {
-    if (cudaMemsetAsync(dyt, 0, (size_t)nnz * H * 2, s) != cudaSuccess) return MB_ERR_CUDA;
+    if (!eval_only && cudaMemsetAsync(dyt, 0, (size_t)nnz * H * 2, s) != cudaSuccess) return MB_ERR_CUDA;
     return MB_OK;
   }
   const int n = n_masked;
@@ -226,6 +228,7 @@ mb_status mb_mlm_loss(const mb_dims* d, const mb_head_params* p, const mb_bf16* 
   MB_CHECK_LAUNCH();
   sum_kernel<<<1, 1024, 0, s>>>(w.row_loss, n, inv_norm, loss_sum);
   MB_CHECK_LAUNCH();
+  if (eval_only) return MB_OK;
   // backward: recompute z tile by tile and emit dz = (softmax(z) - onehot(y)) * inv_norm (E_DZ)
   {
     GemmArgs a;

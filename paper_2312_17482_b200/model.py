@@ -314,6 +314,43 @@ class MosaicBert:
         self._handles = [h for h in handles if h is not None]
         return nnz, n_m
 
+    def evaluate(self, ids: torch.Tensor, mask: torch.Tensor, labels: torch.Tensor) -> tuple[float, int]:
+        """Forward only, no dropout, no gradients (the inference path of SURVEY F4's "train short,
+        test long": ALiBi needs no position table, so the same weights run at any l up to 2048,
+        P:131).  Returns (sum over the labelled tokens of their cross-entropy, their count); the
+        training state (gradients, the R18 count, the loss accumulator) is left untouched."""
+        B, Lq = mask.shape
+        self.check_meta()
+        self._ensure(B, Lq)
+        cd = self.cd
+        if getattr(self, "_eval_scalars", None) is None:
+            self._eval_scalars = torch.zeros(2, dtype=torch.float32, device=self.device)  # loss, count
+        L.zero_f32(self._eval_scalars)
+        loss, count = self._eval_scalars[0:1], self._eval_scalars[1:2]
+        L._ck("mb_unpad_index", L.lib().mb_unpad_index(L._p(mask), L._p(ids), self.d.vocab, B, Lq, L._p(self.cu),
+                                                        L._p(self.indices), L._p(self.meta), L._p(self.idx_ws),
+                                                        self.idx_ws.numel(), L._stream()))
+        L._ck("mb_mlm_select", L.lib().mb_mlm_select(L._p(labels), L._p(self.indices), B * Lq, self.d.vocab,
+                                                      L._p(self.rows), L._p(self.labs), L._p(self.meta),
+                                                      L._p(count), L._p(self.sel_ws), self.sel_ws.numel(),
+                                                      L._stream()))
+        nnz, max_seqlen, status, n_m = (int(x) for x in self.meta.tolist())  # one small D2H read
+        if status != 0:
+            raise RuntimeError(f"batch rejected: {L.STATUS.get(status, status)}")
+        if nnz == 0 or n_m == 0:
+            return 0.0, n_m
+        packed = L.Packed(L._p(self.cu), B, nnz, max_seqlen)
+        e = self.emb_bucket.p
+        L.embed_forward(cd, ids, self.indices, nnz, e["emb"], e["type_emb"], e["lne_g"], e["lne_b"], self.xs[0],
+                        self.estats)
+        for l in range(self.d.layers):
+            L.encoder_forward(cd, L.layer_ptrs(self.layer_buckets[l].p), packed, self.slopes, self.xs[l],
+                              self.xs[l + 1], self.saved[l], None)
+        self._ensure_head(n_m)
+        L.mlm_loss(cd, self.head_params(), self.xs[self.d.layers], nnz, self.rows, self.labs, n_m, 1.0, loss,
+                   self.lse, None, None, self.head_ws)
+        return float(loss.item()), n_m
+
     def _meta_host(self):
         if getattr(self, "_meta_pinned", None) is None:
             self._meta_pinned = torch.zeros(4, dtype=torch.int32).pin_memory()

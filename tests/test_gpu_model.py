@@ -354,3 +354,41 @@ def test_loss_normalize_device_count():
     assert float(inv) == np.float32(1 / 5.0) and abs(float(out) - 2.5) < 1e-6
     mb.loss_normalize(ls, count_host=0.0, inv_out=inv, loss_out=out)
     assert float(inv) == 1.0 and float(out) == 12.5
+
+
+def test_evaluate_matches_training_forward():
+    """MosaicBert.evaluate (forward only, mb_mlm_loss with dy_top = grads = NULL) runs exactly the
+    training step's forward kernels: the summed loss is bitwise the micro-step's, and the training
+    state (gradients, R18 count, loss accumulator) is untouched by it."""
+    params = synth.make_model_params(synth.TINY, 4, "bert")
+    batch = synth.make_batch("C1", 77)
+    d = synth.TINY
+    model = mb.MosaicBert(mb.ModelDims(d.hidden, d.heads, d.intermediate, d.vocab, 1, d.ln_eps), params)
+    ids, mask, labels = (to_dev(batch[k], I32) for k in ("input_ids", "attention_mask", "labels"))
+    n_lab = int(((batch["labels"] != -100) & (batch["attention_mask"] != 0)).sum())
+    model.zero_grad()
+    model.micro_step(ids, mask, labels, inv_norm=1.0)
+    torch.cuda.synchronize()
+    ref_loss = float(model.loss_sum.item())
+    ref_g = [b.g.clone() for b in model.buckets]
+    ref_count = float(model.count_dev.item())
+    s_eval, n_eval = model.evaluate(ids, mask, labels)
+    assert n_eval == n_lab
+    assert s_eval == ref_loss, (s_eval, ref_loss)
+    assert float(model.loss_sum.item()) == ref_loss and float(model.count_dev.item()) == ref_count
+    assert all(torch.equal(a, b.g) for a, b in zip(ref_g, model.buckets))
+
+
+@pytest.mark.parametrize("Lq,lens", [(512, [512, 300, 129, 1]), (1024, [1024, 515, 64]), (2048, [2048, 700])])
+def test_evaluate_long_sequences_vs_oracle(Lq, lens):
+    """SURVEY F4 "train short, test long" (ALiBi lets a model trained at 128 run at longer l):
+    the same weights evaluated forward-only at l up to 2048 (the long attention kernels) give the
+    oracle's mean MLM loss within the north_star loss bar."""
+    d = synth.TINY
+    params = synth.make_model_params(d, 6, "bert")
+    batch = synth.make_batch("C1", 900 + Lq, B=len(lens), L=Lq, lengths=np.array(lens))
+    model = mb.MosaicBert(mb.ModelDims(d.hidden, d.heads, d.intermediate, d.vocab, 1, d.ln_eps), params)
+    ids, mask, labels = (to_dev(batch[k], I32) for k in ("input_ids", "attention_mask", "labels"))
+    s_eval, n = model.evaluate(ids, mask, labels)
+    oloss, _ = O.model_forward_backward(batch, params, O.alibi_slopes(d.heads), d.ln_eps)
+    assert n > 0 and abs(s_eval / n - oloss) <= 1e-2, (s_eval / n, oloss)
