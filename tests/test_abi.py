@@ -82,6 +82,13 @@ def test_host_argument_errors(lib):
     assert lib.mb_dropout_mask(ctypes.byref(bad), 0, 4, 8, 1, None) == 1
     ok = _lib.Dropout(0.1, 0, 0)
     assert lib.mb_dropout_mask(ctypes.byref(ok), 0, 4, 12, 1, None) == 2  # cols % 8 != 0
+    # mb_mlm_loss: dy_top and g must be both given (training) or both NULL (forward-only evaluation)
+    hd = _lib.dims(64, 2, 256, 128)
+    hp, hg = _lib.HeadPtrs(), _lib.HeadPtrs()
+    assert lib.mb_mlm_loss(ctypes.byref(hd), ctypes.byref(hp), 8, 4, 8, 8, 2, ctypes.c_float(1.0), 8, 8, None,
+                           ctypes.byref(hg), 8, 1 << 20, None) == 1
+    assert lib.mb_mlm_loss(ctypes.byref(hd), ctypes.byref(hp), 8, 4, 8, 8, 2, ctypes.c_float(1.0), 8, 8, 8, None, 8,
+                           1 << 20, None) == 1
     assert lib.mb_status_string(4) == b"MB_ERR_MASK_LAYOUT"
     assert lib.mb_status_string(9) == b"MB_ERR_TOKEN_RANGE"
 
