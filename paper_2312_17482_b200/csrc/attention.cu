@@ -1264,13 +1264,13 @@ __global__ void __launch_bounds__(L2_THREADS, 1) attn_fwd_long2_kernel(const __g
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive(&s_free[t]);
         if (trw) L2TR(t, c, 2);
-        if (jj == 0 && pend) {  // the previous unit's O (its PVs are done once this tile's S is in)
-          readout(pd_st, pd_len, pd_h, pd_row, pd_m, pd_l);
-          pend = false;
-        }
         const int keys = len - kv0;
         const float mx = keys >= TILE ? row_scores128<false>(x, r, keys, slr, q0 - kv0)
                                       : row_scores128<true>(x, r, keys, slr, q0 - kv0);
+        if (jj == 0 && pend) {  // the previous unit's O: after this tile's score pass its last PV is done
+          readout(pd_st, pd_len, pd_h, pd_row, pd_m, pd_l);
+          pend = false;
+        }
         if (trw) L2TR(t, c, 3);
         if (jj > 0) {
           // P_t of the previous key tile must have been consumed before P_t is rewritten, and a
