@@ -964,7 +964,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) attn_fwd_long_kernel(const __gr
 constexpr int L2_NS = 3;
 constexpr int L2_THREADS = SH_THREADS + 128;  // softmax warpgroups 0, 1; warpgroup 2: MMA warp 8, TMA warp 9
 constexpr int L2_UMAX = 2048;                 // work units per CTA (host falls back to v1 beyond)
-constexpr int L2_SMEM = 4 * TILE_BYTES + L2_NS * 2 * TILE_BYTES + 1024 + 256 + 16 * L2_UMAX;
+constexpr int L2_SMEM = 4 * TILE_BYTES + L2_NS * 2 * TILE_BYTES + 2 * TILE_BYTES + 1024 + 256 + 16 * L2_UMAX;  // + O staging
 
 struct PairUnits {  // unit u = (b * heads + h) * QP + p, valid iff 256 p < len_b
   const int* cu;
@@ -1027,6 +1027,7 @@ __device__ long long l2_mtrace[2][8][16];  // per t: S_t issued, PV_t issued, S:
 #endif
 
 __global__ void __launch_bounds__(L2_THREADS, 1) attn_fwd_long2_kernel(const __grid_constant__ CUtensorMap tm_qkv,
+                                                                      const __grid_constant__ CUtensorMap tm_o,
                                                                       PairUnits U, int d,
                                                                       const float* __restrict__ slopes,
                                                                       bf16* __restrict__ O, float* __restrict__ lse,
@@ -1035,7 +1036,8 @@ __global__ void __launch_bounds__(L2_THREADS, 1) attn_fwd_long2_kernel(const __g
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                  // [unit parity][tile] Q
   uint8_t* sKV = sQ + 4 * TILE_BYTES;  // L2_NS x (K, V)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + L2_NS * 2 * TILE_BYTES);
+  uint8_t* sO = sKV + L2_NS * 2 * TILE_BYTES;  // per warpgroup t: the finished unit's O, [32 x 32] blocks
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sO + 2 * TILE_BYTES);
   uint64_t* q_full = bars;                  // [2] per unit parity
   uint64_t* q_empty = bars + 2;             // [2]
   uint64_t* kv_full = bars + 4;             // [L2_NS]
@@ -1216,24 +1218,45 @@ __global__ void __launch_bounds__(L2_THREADS, 1) attn_fwd_long2_kernel(const __g
                    tO = tbase + 384 + 64 * t + lane_off;
     int c = 0;  // key tiles processed by this warpgroup (all units)
     // a finished unit's O: normalise, store, LSE (its last PV is pv_done phase c - 1)
+    // a warp whose 32 rows are all inside the sequence stages its [32 x 64] block as two 64B-swizzled
+    // [32 x 32] blocks in its slice of sO and one lane TMA-stores them (coalesced); a ragged quarter
+    // stores its valid rows directly
+    const uint32_t sOw = sm100::smem_u32(sO) + t * TILE_BYTES + q4 * 4096;
     auto readout = [&](int st, int len, int h, int qrow, float m_used, float l_used) {
       sm100::mbar_wait(&pv_done[t], (c - 1) & 1);
       sm100::tc_fence_after();
       const float inv = 1.f / l_used;
+      const int qbase = qrow - lane;                  // first row of this warp's quarter
+      const bool full = qbase + 32 <= len;           // warp-uniform
       bf16* dst = O + (size_t)(st + qrow) * H + h * d;
+      if (full) {
+        if (lane == 0) sm100::bulk_wait_read0();     // the previous unit's stores have left sO
+        __syncwarp();
+      }
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         float o[32];
         sm100::tmem_ld32(tO + 32 * hh, o);
         sm100::tmem_ld_wait();
-        if (32 * hh < d && qrow < len) {
+        if (32 * hh >= d) continue;
 #pragma unroll
-          for (int cc = 0; cc < 32; cc += 8) {
-            float w8[8];
+        for (int e = 0; e < 32; ++e) o[e] *= inv;
+        if (full) {
+          const uint32_t blk = sOw + hh * 2048;
 #pragma unroll
-            for (int e = 0; e < 8; ++e) w8[e] = o[cc + e] * inv;
-            *reinterpret_cast<uint4*>(dst + 32 * hh + cc) = f32_to_bf16x8(w8);
+          for (int cc = 0; cc < 4; ++cc) {
+            const uint4 pk = f32_to_bf16x8(o + 8 * cc);
+            st_shared_v4(blk + lane * 64 + ((cc ^ ((lane >> 1) & 3)) << 4), pk.x, pk.y, pk.z, pk.w);
           }
+          sm100::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            sm100::tma_store_2d(&tm_o, blk, h * d + 32 * hh, st + qbase);
+            sm100::bulk_commit();
+          }
+        } else if (qrow < len) {
+#pragma unroll
+          for (int cc = 0; cc < 32; cc += 8) *reinterpret_cast<uint4*>(dst + 32 * hh + cc) = f32_to_bf16x8(o + cc);
         }
       }
       if (qrow < len) lse[(size_t)h * nnz + st + qrow] = (m_used * sc2 + __log2f(l_used)) * LN2;  // l >= 1
@@ -1324,6 +1347,7 @@ __global__ void __launch_bounds__(L2_THREADS, 1) attn_fwd_long2_kernel(const __g
       pd_st = st, pd_len = len, pd_h = h, pd_row = q0 + r, pd_m = m, pd_l = l;
     }
     if (pend) readout(pd_st, pd_len, pd_h, pd_row, pd_m, pd_l);
+    if (lane == 0) sm100::bulk_wait0();
   }
   sm100::tc_fence_before();
   __syncthreads();
@@ -2286,7 +2310,9 @@ mb_status attention_fwd(const bf16* qkv, const int* cu, int batch, int nnz, int 
     PairUnits P{cu, heads, (max_seqlen + 2 * TILE - 1) / (2 * TILE), 0};
     P.total = batch * heads * P.QP;
     const int grid = std::max(1, std::min(P.total, num_sms()));
-    if (launch_pdl(attn_fwd_long2_kernel, dim3(grid), dim3(L2_THREADS), L2_SMEM, s, 1, tm, P, d, slopes, O, lse,
+    CUtensorMap tmo2;  // [32 rows x 32 columns] output blocks, 64-byte swizzle
+    MB_REQUIRE(make_tmap_bf16_2d(&tmo2, O, H, nnz, H, 32, 32, 64), MB_ERR_CUDA);
+    if (launch_pdl(attn_fwd_long2_kernel, dim3(grid), dim3(L2_THREADS), L2_SMEM, s, 1, tm, tmo2, P, d, slopes, O, lse,
                    nnz) != cudaSuccess)
       return MB_ERR_CUDA;
     MB_CHECK_LAUNCH();
