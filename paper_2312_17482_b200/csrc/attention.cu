@@ -327,8 +327,8 @@ __global__ void __launch_bounds__(SH_FWD_THREADS, 1) attn_fwd_short_kernel(const
 // of a row-key pair are in the same sequence).
 constexpr int S2_NSLOT = 4;
 constexpr int S2_THREADS = SH_THREADS + 128;
-constexpr int S2_UMAX = 1024;  // work units per CTA (host falls back to the v1 kernel beyond)
-constexpr int S2_SMEM = S2_NSLOT * 3 * TILE_BYTES + 1024 + 256 + 16 * S2_UMAX;
+constexpr int S2_UMAX = 96;  // work units per CTA (the host launches larger batches in chunks)
+constexpr int S2_SMEM = S2_NSLOT * 3 * TILE_BYTES + 2 * TILE_BYTES + 1024 + 256 + 16 * S2_UMAX;  // + O staging
 
 // Short-path work units: one head of a GROUP of consecutive sequences fitting one 128-row tile —
 // sequences 4g..4g+3 when their lengths sum to <= 128, else the pair 2g, 2g+1 when it fits, else
@@ -418,6 +418,7 @@ __device__ __forceinline__ float row_scores_win(float (&x)[128], int r, int lo, 
 }
 
 __global__ void __launch_bounds__(S2_THREADS, 1) attn_fwd_short2_kernel(const __grid_constant__ CUtensorMap tm_qkv,
+                                                                       const __grid_constant__ CUtensorMap tm_o,
                                                                        const int* __restrict__ cu, int batch, int heads,
                                                                        int d, const float* __restrict__ slopes,
                                                                        bf16* __restrict__ O, float* __restrict__ lse,
@@ -428,7 +429,8 @@ __global__ void __launch_bounds__(S2_THREADS, 1) attn_fwd_short2_kernel(const __
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* slots = smem;  // S2_NSLOT x (Q, K, V)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(slots + S2_NSLOT * 3 * TILE_BYTES);
+  uint8_t* sO = slots + S2_NSLOT * 3 * TILE_BYTES;  // per warpgroup t: a finished unit's O, [32 x 32] blocks
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sO + 2 * TILE_BYTES);
   uint64_t* ld_full = bars;                  // [S2_NSLOT]
   uint64_t* ld_empty = bars + S2_NSLOT;      // [S2_NSLOT]
   uint64_t* s_full = bars + 2 * S2_NSLOT;    // [2] per warpgroup
@@ -530,11 +532,20 @@ __global__ void __launch_bounds__(S2_THREADS, 1) attn_fwd_short2_kernel(const __
     const uint32_t tS = tbase + 128 * t + lane_off, tP = tbase + 256 + 64 * t + lane_off,
                    tO = tbase + 384 + 64 * t + lane_off;
     // the previous unit's O: normalise, store, LSE; then O_t may be overwritten
+    // a warp whose 32 rows are all inside the group stages its [32 x 64] block as two 64B-swizzled
+    // [32 x 32] blocks in its slice of sO and one lane TMA-stores them (coalesced); a ragged quarter
+    // stores its valid rows directly
+    const uint32_t sOw = sm100::smem_u32(sO) + t * TILE_BYTES + q4 * 4096;
     auto readout = [&](int kk, int st, int h, int glen, float m_used, float l_used) {
       sm100::mbar_wait(&o_full[t], kk & 1);
       sm100::tc_fence_after();
       const float inv = 1.f / l_used;
+      const bool full = q4 * 32 + 32 <= glen;  // warp-uniform
       bf16* dst = O + (size_t)(st + r) * H + h * d;
+      if (full) {
+        if (lane == 0) sm100::bulk_wait_read0();  // the previous unit's stores have left sO
+        __syncwarp();
+      }
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         float o[32];
@@ -545,14 +556,25 @@ __global__ void __launch_bounds__(S2_THREADS, 1) attn_fwd_short2_kernel(const __
           __syncwarp();
           if (lane == 0) sm100::mbar_arrive(&o_empty[t]);
         }
-        if (32 * hh < d && r < glen) {
+        if (32 * hh >= d) continue;
 #pragma unroll
-          for (int c = 0; c < 32; c += 8) {
-            float w8[8];
+        for (int e = 0; e < 32; ++e) o[e] *= inv;
+        if (full) {
+          const uint32_t blk = sOw + hh * 2048;
 #pragma unroll
-            for (int e = 0; e < 8; ++e) w8[e] = o[c + e] * inv;
-            *reinterpret_cast<uint4*>(dst + 32 * hh + c) = f32_to_bf16x8(w8);
+          for (int c = 0; c < 4; ++c) {
+            const uint4 pk = f32_to_bf16x8(o + 8 * c);
+            st_shared_v4(blk + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4), pk.x, pk.y, pk.z, pk.w);
           }
+          sm100::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            sm100::tma_store_2d(&tm_o, blk, h * d + 32 * hh, st + q4 * 32);
+            sm100::bulk_commit();
+          }
+        } else if (r < glen) {
+#pragma unroll
+          for (int c = 0; c < 32; c += 8) *reinterpret_cast<uint4*>(dst + 32 * hh + c) = f32_to_bf16x8(o + c);
         }
       }
       if (r < glen) lse[(size_t)h * nnz + st + r] = (m_used * sc2 + __log2f(l_used)) * LN2;  // l >= 1
@@ -602,6 +624,7 @@ __global__ void __launch_bounds__(S2_THREADS, 1) attn_fwd_short2_kernel(const __
       ++k;
     }
     if (pk_k >= 0) readout(pk_k, pk_st, pk_h, pk_glen, pk_m, pk_l);
+    if (lane == 0) sm100::bulk_wait0();
   }
   sm100::tc_fence_before();
   __syncthreads();
@@ -2261,8 +2284,7 @@ mb_status attention_fwd(const bf16* qkv, const int* cu, int batch, int nnz, int 
     const char* e = std::getenv("MB_ATTN_SHORT_FWD");
     return e && e[0] == 'v' && e[1] == '1';
   }();
-  const bool short2_fits = batch * heads <= num_sms() * S2_UMAX;
-  if (max_seqlen <= TILE && !short_v1 && short2_fits) {
+  if (max_seqlen <= TILE && !short_v1) {
     static bool attr_s2 = false;
     if (!attr_s2) {
       if (cudaFuncSetAttribute(attn_fwd_short2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, S2_SMEM) !=
@@ -2270,11 +2292,19 @@ mb_status attention_fwd(const bf16* qkv, const int* cu, int batch, int nnz, int 
         return MB_ERR_CUDA;
       attr_s2 = true;
     }
-    const int grid = std::max(1, std::min(batch * heads, num_sms()));
-    if (launch_pdl(attn_fwd_short2_kernel, dim3(grid), dim3(S2_THREADS), S2_SMEM, s, 1, tm, cu, batch, heads, d, slopes,
-                   O, lse, nnz) != cudaSuccess)
-      return MB_ERR_CUDA;
-    MB_CHECK_LAUNCH();
+    CUtensorMap tmo2;  // [32 rows x 32 columns] output blocks, 64-byte swizzle
+    MB_REQUIRE(make_tmap_bf16_2d(&tmo2, O, H, nnz, H, 32, 32, 64), MB_ERR_CUDA);
+    // a CTA's unit list holds S2_UMAX units: larger batches go in chunks of sequences (cu_seqlens
+    // holds absolute token offsets, so a chunk is just an offset into it)
+    const int chunk = std::max(1, num_sms() * S2_UMAX / heads);
+    for (int b0 = 0; b0 < batch; b0 += chunk) {
+      const int nb = std::min(chunk, batch - b0);
+      const int grid = std::max(1, std::min(nb * heads, num_sms()));
+      if (launch_pdl(attn_fwd_short2_kernel, dim3(grid), dim3(S2_THREADS), S2_SMEM, s, 1, tm, tmo2, cu + b0, nb, heads,
+                     d, slopes, O, lse, nnz) != cudaSuccess)
+        return MB_ERR_CUDA;
+      MB_CHECK_LAUNCH();
+    }
     return MB_OK;
   }
   if (max_seqlen <= TILE) {
