@@ -809,10 +809,12 @@ constexpr int GB_STAGE_BYTES = BM * BK * 2 + (GB_BN / 2) * BK * 2;  // own 128 A
 constexpr int GB_SLOT_BYTES = 2 * BM * 64 * 2;                      // a and g boxes [128 x 64] bf16 (32 KB)
 constexpr int GB_SMEM = GB_STAGES * GB_STAGE_BYTES + GB_NSLOT * GB_SLOT_BYTES + 1024 + 256;
 
-// DIRECT_STORE (default): dU leaves the registers by 32-byte stores (row per thread) and each Gd
-// slot is released as soon as the 8 warps have read it, instead of being rewritten in place and
-// TMA-stored: two of the four shared-memory passes of the epilogue disappear (kernel 400 -> 382 us
-// in isolation)
+// Default (DIRECT_STORE = false): dU is written in place over the Gd slot, and the two warps of each
+// TMEM lane quarter meet on a 64-thread named barrier after which one lane TMA-stores their [32 x 64]
+// rows of both boxes (coalesced, 128B swizzle = the in-place layout); a slot goes back to the loader
+// once its four quarter leaders' stores have read it.  DIRECT_STORE (MB_GEGLU_BWD_STORE=direct):
+// dU leaves the registers by row-per-thread 32-byte stores and each Gd slot is released as soon as the
+// 8 warps have read it (fewer shared-memory passes, faster in isolation, 0.5 % slower in the step)
 template <bool DIRECT_STORE>
 __global__ void __launch_bounds__(NTHREADS, 1)
     geglu_bwd_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -848,7 +850,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     for (int i = 0; i < GB_NSLOT; ++i) {
       sm100::mbar_init(&gfull[i], 1);
-      sm100::mbar_init(&gempty[i], DIRECT_STORE ? NUM_EPI_WARPS : 1);
+      sm100::mbar_init(&gempty[i], DIRECT_STORE ? NUM_EPI_WARPS : 4);  // TMA: the 4 quarter leaders
     }
     sm100::fence_barrier_init();
   }
@@ -1022,11 +1024,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           sts128(box_a + off, f32_to_bf16x8(ga));
           sts128(box_g + off, f32_to_bf16x8(gg));
         }
+        // the two warps of this lane quarter (32 rows x 64 columns of the box) meet, and one lane
+        // TMA-stores their rows of both boxes ([32 x 64], 128B swizzle = the in-place layout)
         sm100::fence_proxy_async_smem();
-        sm100::named_bar(1, 32 * NUM_EPI_WARPS);
-        if (gtid == 0) {
-          sm100::tma_store_2d(&tmDU, slots + sl * GB_SLOT_BYTES, nb * GB_BN + qq * 64, row0);
-          sm100::tma_store_2d(&tmDU, slots + sl * GB_SLOT_BYTES + BM * 128, I + nb * GB_BN + qq * 64, row0);
+        sm100::named_bar(2 + q, 64);
+        if (grp == 0 && lane == 0) {
+          sm100::tma_store_2d(&tmDU, box_a + q * 4096, nb * GB_BN + qq * 64, row0 + q * 32);
+          sm100::tma_store_2d(&tmDU, box_g + q * 4096, I + nb * GB_BN + qq * 64, row0 + q * 32);
           sm100::bulk_commit();
           if (qi > 0) {  // the previous quarter's stores have read their slot: hand it back
             asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
@@ -1039,7 +1043,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         acc_phase ^= 1;
       }
     }
-    if (!DIRECT_STORE && gtid == 0) {
+    if (!DIRECT_STORE && grp == 0 && lane == 0) {
       sm100::bulk_wait_read0();
       if (qi > 0) sm100::mbar_arrive(&gempty[(qi - 1) % GB_NSLOT]);
       sm100::bulk_wait0();
@@ -1161,10 +1165,12 @@ mb_status gemm(const GemmArgs& g, cudaStream_t s) {
     if (g.a_t || !g.b_t || g.ep.I % GB_BN || g.ep.ldu != 2 * g.ep.I || g.ep.ldc != 2 * g.ep.I) return MB_ERR_CONFIG;
     CUtensorMap tg, tdu;
     MB_REQUIRE(make_tmap_bf16_2d(&tg, g.ep.U, 2 * g.ep.I, g.M, g.ep.ldu, 64, BM), MB_ERR_CUDA);
-    MB_REQUIRE(make_tmap_bf16_2d(&tdu, g.ep.C, 2 * g.ep.I, g.M, g.ep.ldc, 64, BM), MB_ERR_CUDA);
-    static const bool direct = [] {  // MB_GEGLU_BWD_STORE=tma: the in-place + TMA-store epilogue (A/B)
+    MB_REQUIRE(make_tmap_bf16_2d(&tdu, g.ep.C, 2 * g.ep.I, g.M, g.ep.ldc, 64, 32), MB_ERR_CUDA);  // per lane quarter
+    // default: dU written in place into the Gd slot and TMA-stored per lane quarter (C2 step +0.5 %
+    // against row-per-thread 32-byte stores in a same-box A/B); MB_GEGLU_BWD_STORE=direct: the stores
+    static const bool direct = [] {
       const char* e = std::getenv("MB_GEGLU_BWD_STORE");
-      return !(e && e[0] == 't');
+      return e && e[0] == 'd';
     }();
     auto kern = direct ? geglu_bwd_kernel<true> : geglu_bwd_kernel<false>;
     static bool attr_gb = false;
