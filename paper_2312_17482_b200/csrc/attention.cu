@@ -2451,7 +2451,9 @@ mb_status attention_bwd(const bf16* qkv, const bf16* O, const bf16* dO, const fl
     return MB_OK;
   }
   {
-    const int rows_per = 128;
+    // one wave: two CTAs of (H/8) x 8 threads per SM, each covering an equal share of the rows
+    const int slots = 2 * num_sms();
+    const int rows_per = std::max(DQF_GROUPS, ((nnz + slots - 1) / slots + DQF_GROUPS - 1) / DQF_GROUPS * DQF_GROUPS);
     dq_finish_kernel<<<(nnz + rows_per - 1) / rows_per, dim3(H / 8, DQF_GROUPS), DQF_GROUPS * H * sizeof(float),
                        s>>>(dq_acc, nnz, H, rows_per, dqkv, dbias);
     MB_CHECK_LAUNCH();
