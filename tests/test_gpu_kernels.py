@@ -505,8 +505,9 @@ def test_embedding_fwd_bwd_repeated_ids(H):
 
 
 def test_attention_short_huge_batch_fallbacks():
-    """More (sequence, head) units than the short kernels' per-CTA unit lists hold (forward: v1
-    kernel; backward: the long kernel, which takes any length): 80,000 sequences of length 1..3."""
+    """More (sequence, head) units than the short kernels' per-CTA unit lists hold (forward: launched
+    in chunks of sequences; backward: the long kernel, which takes any length): 80,000 sequences of
+    length 1..3."""
     heads, d = 2, 32
     H = heads * d
     rng = np.random.default_rng(80000)
@@ -533,3 +534,28 @@ def test_attention_short_huge_batch_fallbacks():
     got = np64(dqkv)
     for nm, s_ in (("dq", slice(0, H)), ("dk", slice(H, 2 * H)), ("dv", slice(2 * H, 3 * H))):
         check(f"huge.{nm}", got[:, s_], ref[:, s_])
+
+
+def test_attention_short_forward_chunked_launches():
+    """The short forward launches batches beyond num_sms x 96 units in chunks of sequences (offsets
+    into cu_seqlens): 1,200 sequences x 12 heads, lengths 90..128, so the second launch holds a ragged
+    remainder and full-quarter tiles take the TMA-staged output path in both launches."""
+    heads, d = 12, 32
+    H = heads * d
+    rng = np.random.default_rng(1200)
+    B, Lmax = 1200, 128
+    lens = rng.integers(90, Lmax + 1, size=B)
+    lens[-1] = Lmax
+    mask = synth.mask_from_lengths(lens, Lmax)
+    qkv_p = synth.bf16_round(rng.standard_normal((B, Lmax, 3 * H)))
+    cu, oidx, maxlen, _ = O.unpad_index(mask)
+    nnz = len(oidx)
+    sl_np = mb.alibi_slopes(heads)
+    qkv, cud, sl = _bf(O.unpad(qkv_p, oidx)), to_dev(cu, I32), to_dev(sl_np, torch.float32)
+    Od = torch.empty(nnz, H, dtype=BF, device="cuda")
+    lse = torch.empty(heads, nnz, dtype=torch.float32, device="cuda")
+    mb.attention_forward(qkv, cud, B, nnz, maxlen, heads, d, sl, Od, lse)
+    sp = lambda t: t.reshape(B, Lmax, heads, d)  # noqa: E731
+    C, _ = O.attention_forward(sp(qkv_p[..., :H]), sp(qkv_p[..., H:2 * H]), sp(qkv_p[..., 2 * H:]), mask,
+                               sl_np.astype(np.float64))
+    check("chunked.O", np64(Od), O.unpad(C.reshape(B, Lmax, H), oidx), max_rel=2e-2)
